@@ -1,0 +1,137 @@
+"""The VaPr rollout cost + gradient dataflow, stage by stage (oracle).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.
+
+PAPER.md:162 (one iteration: "(2) Compute kinematics. (3) Compute cost
+functions ... (4) Aggregating the costs. (5) Compute backward")
+(the five large tensors) and PAPER.md:227 (quantize -> dequantize "at each
+kernel invocation").  Quantisation points (reading c19): out_spheres at the FK
+store, closest_pt[_swept] and out_vec at their producers' stores,
+grad_out_spheres after aggregation and before BK.  Costs stay FP32/double.
+
+Every stage consumes and produces *packed words* in the layout of
+oracle.codec.pack, so that each CUDA stage can be fed exactly the same packed
+inputs (parity contract 2-3).  Each stage also returns its
+double-precision pre-quantisation values and per-element tolerance scales.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import codec
+from .kinematics import sphere_centers, backward, backward_terms_abs
+from .collision import world_cost, self_cost
+
+SLOT_OS, SLOT_GOS, SLOT_OV, SLOT_CP, SLOT_CPS = range(5)
+
+
+def _cols(robot):
+    return 3 * len(robot["sphere_link"])
+
+
+def quantize_rows(v, fmt):
+    """double [P, cols] -> packed words with ONE rounding from the double."""
+    E, M = fmt
+    return codec.pack(codec.quantize_f64(v, E, M), E, M)
+
+
+def decode_rows(words, fmt, cols):
+    E, M = fmt
+    return codec.dequantize_packed(words, E, M, cols).astype(np.float64)
+
+
+def fk_stage(q, robot, fmt_os):
+    """q [P, 7] float32 -> (out_spheres words, pre-quant c [P, 3S])."""
+    c = sphere_centers(np.asarray(q, np.float32).astype(np.float64).reshape(-1, 7), robot)
+    v = c.reshape(c.shape[0], -1)
+    return quantize_rows(v, fmt_os), v
+
+
+def world_stage(os_words, fmt_os, world_idx, cuboids, offsets, robot, B, H,
+                eta, w, swept, n, fmt_out):
+    """World collision on packed out_spheres.  Returns dict with cost [B, H],
+    cost_scale [B, H], words (closest_pt[_swept]), v [P, 3S], gscale [P, S],
+    tie [P, S]."""
+    S = len(robot["sphere_link"])
+    c = decode_rows(os_words, fmt_os, 3 * S).reshape(B, H, S, 3)
+    radius = robot["sphere_xyzr"][:, 3].astype(np.float64)
+    cost = np.zeros((B, H))
+    cscale = np.zeros((B, H))
+    grad = np.zeros((B, H, S, 3))
+    gscale = np.zeros((B, H, S))
+    tie = np.zeros((B, H, S), bool)
+    world_idx = np.asarray(world_idx)
+    for wi in np.unique(world_idx):
+        sel = np.nonzero(world_idx == wi)[0]
+        cub = cuboids[offsets[wi]:offsets[wi + 1]]
+        r = world_cost(c[sel], radius, cub, eta, w, swept=bool(swept), n=n)
+        cost[sel], grad[sel], cscale[sel], gscale[sel], tie[sel] = r
+    v = grad.reshape(B * H, 3 * S)
+    return dict(cost=cost, cost_scale=cscale, words=quantize_rows(v, fmt_out),
+                v=v, gscale=gscale.reshape(B * H, S), tie=tie.reshape(B * H, S))
+
+
+def self_stage(os_words, fmt_os, robot, eta, w, fmt_ov):
+    S = len(robot["sphere_link"])
+    c = decode_rows(os_words, fmt_os, 3 * S).reshape(-1, S, 3)
+    radius = robot["sphere_xyzr"][:, 3].astype(np.float64)
+    cost, out, cscale, gscale = self_cost(c, radius, robot["pairs"], eta, w)
+    v = out.reshape(out.shape[0], -1)
+    return dict(cost=cost, cost_scale=cscale, words=quantize_rows(v, fmt_ov),
+                v=v, gscale=gscale)
+
+
+def aggregate_stage(cp_words, fmt_cp, ov_words, fmt_ov, fmt_gos, cols):
+    """grad_out_spheres = dequant(closest_pt[_swept]) + dequant(out_vec),
+    quantised to t_gos.  The sum is exact in double."""
+    v = decode_rows(cp_words, fmt_cp, cols) + decode_rows(ov_words, fmt_ov, cols)
+    return dict(words=quantize_rows(v, fmt_gos), v=v)
+
+
+def bk_stage(q, gos_words, fmt_gos, robot):
+    S = len(robot["sphere_link"])
+    q64 = np.asarray(q, np.float32).astype(np.float64).reshape(-1, 7)
+    g = decode_rows(gos_words, fmt_gos, 3 * S).reshape(-1, S, 3)
+    return dict(grad_q=backward(q64, g, robot),
+                scale=backward_terms_abs(q64, g, robot))
+
+
+@dataclass
+class RolloutResult:
+    os_words: np.ndarray
+    cp_words: np.ndarray            # closest_pt or closest_pt_swept
+    ov_words: np.ndarray
+    gos_words: np.ndarray
+    cost_pose: np.ndarray           # [B, H] world + self
+    cost_traj: np.ndarray           # [B]
+    grad_q: np.ndarray              # [B, H, 7]
+    stages: dict
+
+
+def rollout(q, world_idx, cuboids, offsets, robot, params, formats):
+    """Full vapr_cost_grad dataflow: FK -> world (discrete or swept) -> self ->
+    aggregate -> BK.  formats in slot order (os, gos,
+    ov, cp, cps)."""
+    q = np.asarray(q, np.float32)
+    B, H = q.shape[0], q.shape[1]
+    cols = _cols(robot)
+    swept = bool(params["swept"])
+    f_os, f_gos, f_ov = formats[SLOT_OS], formats[SLOT_GOS], formats[SLOT_OV]
+    f_cp = formats[SLOT_CPS] if swept else formats[SLOT_CP]
+    os_words, v_os = fk_stage(q.reshape(-1, 7), robot, f_os)
+    ws = world_stage(os_words, f_os, world_idx, cuboids, offsets, robot, B, H,
+                     params["eta_world"], params["w_world"], swept,
+                     params["sweep_steps"], f_cp)
+    ss = self_stage(os_words, f_os, robot, params["eta_self"], params["w_self"], f_ov)
+    ag = aggregate_stage(ws["words"], f_cp, ss["words"], f_ov, f_gos, cols)
+    bk = bk_stage(q.reshape(-1, 7), ag["words"], f_gos, robot)
+    cost_pose = ws["cost"] + ss["cost"].reshape(B, H)
+    return RolloutResult(os_words, ws["words"], ss["words"], ag["words"],
+                         cost_pose, cost_pose.sum(axis=1),
+                         bk["grad_q"].reshape(B, H, 7),
+                         dict(fk=v_os, world=ws, self=ss, aggregate=ag, bk=bk))
+
+
+def rollout_workload(wl, formats=None):
+    return rollout(wl.q, wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
+                   wl.params, formats if formats is not None else wl.formats)
