@@ -1,0 +1,350 @@
+"""bench.py -- rollout cost+grad throughput of the VaPr hot path on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--formats 43bit] [--impl vapr|reference]
+
+A step = one vapr_cost_grad over the whole resident batch (FK -> fused world
+(swept) + self collision -> aggregate -> BK, every live tensor packed in HBM)
+plus the per-problem best-seed reduction (and, for N > 1, one NCCL all-gather
+of the per-problem results).  Workload = BASELINE.json config 4 per GPU:
+800 problems (100 per MotionBenchMaker-like environment) x 100 TO seeds x 32
+steps = 2.56M poses, 52 spheres (weak scaling: every rank owns its own 800
+problems).  The working set (~1.5 GB of packed tensors at 43 bits) is >10x
+the 126 MB L2, so no flush is needed between steps.  One JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rollout cost+grad evals/sec (B*H*spheres) and HBM GB/s vs peak, per format set"
+UNIT = "sphere-evals/s"
+S = 52
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="vapr", choices=["vapr", "reference"])
+    ap.add_argument("--formats", default="43bit")
+    ap.add_argument("--problems-per-env", type=int, default=100)
+    ap.add_argument("--seeds", type=int, default=100)
+    ap.add_argument("--H", type=int, default=32)
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-sample-poses", type=int, default=20480)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+def packing_factor(E, M):
+    return 32 // (1 + E + M)
+
+
+def v_alg(fmt):
+    """Algorithmic bytes of one packed pose row: 4 * 3S / pf (the paper's
+    register-packing model)."""
+    return 4.0 * 3 * S / packing_factor(*fmt)
+
+
+def stage_bytes(fm, swept=True):
+    """Algorithmic HBM bytes per pose of each kernel."""
+    os_, gos, ov, cp, cps = (v_alg(f) for f in fm)
+    c = cps if swept else cp
+    return {"fk": 28 + os_, "collision": os_ + c + ov + 4, "aggregate": c + ov + gos,
+            "bk": 28 + gos + 28}
+
+
+class Clocks:
+    """Samples nvidia-smi clocks / throttle reasons in a background thread."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- cpu / oracle
+def oracle_sample(fm, n_poses, H, key_offset=0):
+    """A bounded sample of the config-4 workload (same generator, same
+    formats) for the oracle: n_poses // H trajectories spread over the 8
+    environments."""
+    from workloads import config4
+    from workloads.scenes import ENVIRONMENTS
+    n_traj = max(8, n_poses // H)
+    seeds = max(1, n_traj // len(ENVIRONMENTS))
+    return config4(problems_per_env=1, seeds=seeds, H=H, formats=fm,
+                   problem_offset=key_offset, n_problems=len(ENVIRONMENTS))
+
+
+def run_oracle(wl):
+    from oracle.rollout import rollout_workload
+    t0 = time.perf_counter()
+    rollout_workload(wl)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(fm, H, n_poses):
+    wl = oracle_sample(fm, n_poses, H)
+    dt = run_oracle(wl)
+    return {"value": wl.poses * S / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{wl.poses} poses ({wl.B} trajectories x {H} steps, 8 envs) of the same "
+                      f"workload generator, float64 numpy + C codec, single thread, {dt:.1f} s"}
+
+
+# ----------------------------------------------------------------- reference arm
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from workloads.configs import FORMAT_SETS
+    fm = FORMAT_SETS[args.formats]
+    n_poses = max(args.H * 8, args.cpu_sample_poses // 4)
+    wl = oracle_sample(fm, n_poses, args.H)
+    for _ in range(args.warmup):
+        run_oracle(wl)
+    times = [run_oracle(wl) for _ in range(args.steps)]
+    t = float(np.sum(times))
+    value = wl.poses * S * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config4 sample: {wl.poses} poses/step ({wl.B} traj x "
+                                   f"{args.H} steps, 8 envs), formats {args.formats}",
+                       "formats": args.formats},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{wl.poses} poses per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2310_07854_b200 import binding as vb
+    from paper_2310_07854_b200.rollout import Rollout
+    from workloads import config4
+    from workloads.configs import FORMAT_SETS
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    fm = FORMAT_SETS[args.formats]
+    n_prob = args.problems_per_env * 8
+    # weak scaling: rank r owns global problems [r*n_prob, (r+1)*n_prob)
+    wl = config4(problems_per_env=args.problems_per_env, seeds=args.seeds, H=args.H,
+                 formats=fm, problem_offset=rank * n_prob, n_problems=n_prob)
+    P = wl.poses
+    r = Rollout(wl, device=local)
+    stream = torch.cuda.current_stream(dev)
+    best_c = torch.empty(n_prob, dtype=torch.float32, device=dev)
+    best_s = torch.empty(n_prob, dtype=torch.int32, device=dev)
+    gat_c = torch.empty(n_prob * world, dtype=torch.float32, device=dev)
+    gat_s = torch.empty(n_prob * world, dtype=torch.int32, device=dev)
+
+    def step():
+        r.run()
+        vb.vapr_best_per_problem(r.cost_traj, n_prob, args.seeds, best_c, best_s)
+        if world > 1:
+            dist.all_gather_into_tensor(gat_c, best_c)
+            dist.all_gather_into_tensor(gat_s, best_s)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, k, w):
+        for _ in range(w):
+            fn()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / k
+
+    with Clocks(local) as clk:
+        ms = timed(step, args.steps, args.warmup)
+    clocks = clk.summary()
+    value = world * P * S / (ms * 1e-3)
+
+    # ---- per-kernel durations (same kernels, launched stage by stage on the
+    # same stream with events between them) for the roofline of the dominant one
+    p = wl.params
+    swept = p["swept"]
+    lay = vb.vapr_cost_grad_workspace_layout(r.ctx.h, wl.B, wl.H, swept)
+    W = {i: vb.vapr_packed_row_words(fm[i], 3 * S) for i in range(5)}
+    cps = 4 if swept else 3
+    ws = r.workspace
+
+    def slot(i):
+        return ws[lay[i]:lay[i] + 4 * W[i] * P]
+
+    names = ["fk", "collision", "aggregate", "bk"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    acc = {n: 0.0 for n in names}
+
+    def staged():
+        ev[0].record(stream)
+        vb.vapr_fk_spheres(r.ctx.h, r.q, wl.B, wl.H, slot(0))
+        ev[1].record(stream)
+        vb.vapr_collision(r.ctx.h, slot(0), r.world_idx, wl.B, wl.H, p, r.cost_pose, r.cost_traj,
+                          slot(cps), slot(2))
+        ev[2].record(stream)
+        vb.vapr_aggregate(r.ctx.h, slot(cps), swept, slot(2), P, slot(1))
+        ev[3].record(stream)
+        vb.vapr_backward_kinematics(r.ctx.h, r.q, wl.B, wl.H, slot(1), r.grad_q)
+        ev[4].record(stream)
+
+    for _ in range(2):
+        staged()
+    torch.cuda.synchronize(dev)
+    for _ in range(args.steps):
+        staged()
+        torch.cuda.synchronize(dev)
+        for i, n in enumerate(names):
+            acc[n] += ev[i].elapsed_time(ev[i + 1])
+    kms = {n: acc[n] / args.steps for n in names}
+    sb = stage_bytes(fm, bool(swept))
+    a_min = sum(sb.values())
+    dom = max(kms, key=kms.get)
+    hbm, peak_kind = peaks()
+    achieved = sb[dom] * P / (kms[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "bytes_per_pose": sb[dom],
+                "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+                "kernel_frac": {n: round(sb[n] * P / (kms[n] * 1e-3) / 1e9 / hbm, 4) for n in names}}
+
+    # ---- end to end through the public API with host buffers
+    q_host = torch.from_numpy(np.ascontiguousarray(wl.q)).pin_memory()
+    gq_host = torch.empty(P * 7, dtype=torch.float32).pin_memory()
+    ct_host = torch.empty(wl.B, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        r.q.view(-1).copy_(q_host.view(-1), non_blocking=True)
+        step()
+        gq_host.copy_(r.grad_q, non_blocking=True)
+        ct_host.copy_(r.cost_traj, non_blocking=True)
+
+    e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
+    h2d = q_host.numel() * 4
+    d2h = gq_host.numel() * 4 + ct_host.numel() * 4
+
+    # ---- FP32 comparison (the >= 2x target of BASELINE.json) on the same batch
+    fp32 = None
+    if not args.no_fp32 and args.formats != "fp32":
+        r.set_formats(FORMAT_SETS["fp32"])
+        ms32 = timed(step, max(3, args.steps // 2), 2)
+        fp32 = {"value": world * P * S / (ms32 * 1e-3), "ms_per_step": ms32,
+                "speedup_of_formats": ms32 / ms}
+        r.set_formats(fm)
+
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(fm, args.H, args.cpu_sample_poses)
+        bits = sum(1 + e + m for e, m in fm)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32+packed-ExMy", "data": "synthetic",
+            "config": {"workload": "config4: 800 problems (100 per MBM-like env) x 100 TO seeds "
+                                   "x 32 steps per GPU, 52 spheres, swept n=1",
+                       "formats": args.formats, "format_bits": bits,
+                       "formats_exmy": ["E%dM%d" % f for f in fm],
+                       "poses_per_gpu": P, "problems_per_gpu": n_prob,
+                       "l2": "inputs > L2 (packed working set >> 126 MB), no flush",
+                       "parallelism": f"problem-sharded x{world}"},
+            "hbm_alg_gbs": a_min * P * world / (ms * 1e-3) / 1e9,
+            "hbm_frac_step": a_min * P / (ms * 1e-3) / 1e9 / hbm,
+            "bytes_per_pose_alg": a_min,
+            "roofline": roofline,
+            "e2e": {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms},
+            "fp32": fp32,
+            "cpu_baseline": cpu,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

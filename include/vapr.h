@@ -1,0 +1,229 @@
+/*
+ * vapr.h -- C ABI of libvapr: the B200 (sm_100a) data-parallel hot path of
+ * VaPr (arXiv 2310.07854, "VaPr: Variable-Precision Tensors to Accelerate
+ * Robot Motion Planning"): the batched trajectory-optimisation rollout
+ *   forward kinematics -> world (sphere-vs-cuboid) and self collision costs
+ *   -> gradient aggregation -> backward kinematics,
+ * with the paper's five large intermediate tensors stored in HBM in
+ * per-tensor, packed, round-to-nearest-even ExMy formats.
+ *
+ * Citations are PAPER.md line numbers ("P:n") and DESIGN.md sections.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Memory.  Every pointer argument that names a tensor is DEVICE memory
+ *    owned by the caller (allocated with PyTorch, cudaMalloc, ...), unless the
+ *    comment says "host".  The library never allocates, frees or synchronises
+ *    on the hot path; all work is enqueued on the caller's `stream`
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *  - Errors.  Arguments are validated synchronously before anything is
+ *    enqueued; on any error nothing is launched and no output is touched.
+ *    A failed launch or an earlier asynchronous fault on the device is
+ *    reported as VAPR_ERR_CUDA.  No C++ exception crosses the ABI.
+ *  - Alignment.  Device pointers must be 16-byte aligned
+ *    (VAPR_ERR_INVALID_ARG otherwise).
+ *  - Layouts (row-major, contiguous):
+ *      q, grad_q            float32 [B, H, 7]   (radians / cost per radian)
+ *      world_idx            int32   [B]         world of each trajectory
+ *      cost_pose            float32 [B, H]
+ *      cost_traj            float32 [B]
+ *      packed tensor        uint32  [B*H rows, vapr_packed_row_words(fmt, 3S)]
+ *    A packed row holds the 3S = 156 elements of one pose, sphere-major
+ *    (x0 y0 z0 x1 y1 z1 ...).  Element i of a row lives in word i / pf at bit
+ *    offset (i % pf) * t, LSB first, where t = 1 + E + M and pf = floor(32/t)
+ *    codes per 32-bit word ("A 32-bit GPU register can store one FP32,
+ *    two FP16, three FP10, four FP8, five FP6, six FP5, or eight FP4").
+ *    Unused high bits of a word are zero; rows are padded with zero words to
+ *    a multiple of 4 words (16 B).  A code is sign | exponent(E) | mantissa(M)
+ *    with the sign at bit t-1 ("E3M1 as a FP data type of 3-bit
+ *    exponent, 1-bit mantissa, and 1 sign bit").
+ *  - Threading.  A context may be used from several host threads and streams
+ *    concurrently for launches; vapr_set_* calls must not race with launches
+ *    that use the same context.
+ */
+#ifndef VAPR_H
+#define VAPR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    VAPR_OK = 0,
+    VAPR_ERR_INVALID_FORMAT = 1,   /* E not in [2,8], M < 1, M > 23 or 1+E+M > 32 */
+    VAPR_ERR_INVALID_ARG = 2,      /* NULL / misaligned pointer, bad value, small workspace */
+    VAPR_ERR_SHAPE = 3,            /* B < 1, H < 1, swept with H < 2, too many spheres ... */
+    VAPR_ERR_CUDA = 4,             /* launch failure or pending asynchronous device fault */
+    VAPR_ERR_NOT_INITIALIZED = 5,  /* robot, worlds or formats not set on the context */
+    VAPR_ERR_UNSUPPORTED = 6       /* valid request this build does not implement */
+} vapr_status;
+
+/* An ExMy floating-point format: 1 sign bit, E exponent bits (bias
+ * 2^(E-1)-1), M mantissa bits, subnormals, no inf/NaN codes for t < 32,
+ * round to nearest even with saturation to +-max_finite, NaN -> +max_finite,
+ * E8M23 = FP32 bit identity (readings c1-c9 of
+ * DESIGN.md §3).  Valid: E in [2,8], M in [1,23], 1+E+M <= 32. */
+typedef struct { int32_t exp_bits, man_bits; } vapr_format;
+
+/* Tensor slots, in Table II column order (names from P:189). */
+enum {
+    VAPR_OUT_SPHERES = 0,       /* FK output: sphere centres            */
+    VAPR_GRAD_OUT_SPHERES = 1,  /* BK input: aggregated sphere gradients */
+    VAPR_OUT_VEC = 2,           /* self-collision gradient buffer        */
+    VAPR_CLOSEST_PT = 3,        /* world-collision gradient, discrete    */
+    VAPR_CLOSEST_PT_SWEPT = 4,  /* world-collision gradient, swept       */
+    VAPR_NUM_SLOTS = 5
+};
+
+#define VAPR_MAX_SPHERES 64
+#define VAPR_MAX_PAIRS 2048
+#define VAPR_MAX_CUBOIDS_PER_WORLD 16
+
+typedef struct vapr_ctx vapr_ctx;   /* opaque; one per device */
+
+/* Robot model (host memory; copied by vapr_set_robot).  Modified DH (Craig):
+ * row i = 0..7 gives T_i = RotX(dh_alpha[i]) TransX(dh_a[i]) RotZ(theta_i)
+ * TransZ(dh_d[i]), theta_i = q_i for i < 7 and 0 for the fixed flange row 7;
+ * the hand frame is flange . RotZ(hand_rz).  Sphere s is attached to frame
+ * sphere_link[s] in 0..8 (0 = base, 1..7 = joint frames, 8 = hand) at local
+ * offset sphere_xyzr[s][0..2] with radius sphere_xyzr[s][3] (metres; the radius
+ * is never quantised).  Spheres must be sorted by link.  pairs[k] = (i, j) are
+ * the self-collision pairs (reading c18). */
+typedef struct {
+    int32_t n_spheres;                 /* 1..VAPR_MAX_SPHERES */
+    int32_t n_pairs;                   /* 0..VAPR_MAX_PAIRS   */
+    double dh_a[8], dh_d[8], dh_alpha[8];
+    double hand_rz;
+    const int32_t *sphere_link;        /* host [n_spheres]    */
+    const float *sphere_xyzr;          /* host [n_spheres][4] */
+    const uint16_t *pairs;             /* host [n_pairs][2]   */
+} vapr_robot;
+
+/* One oriented box (64 B): R = world-from-box rotation (row-major 3x3),
+ * t = box centre (world), half = half extents (metres). */
+typedef struct { float R[9]; float t[3]; float half[3]; float pad; } vapr_cuboid;
+
+/* Cost parameters (readings c14, c17): smooth-hinge activation
+ * distances eta_* (m), weights w_*, swept = 1 for the TO swept world cost with
+ * sweep_steps >= 0 linear sub-samples per segment, 0 for the discrete cost. */
+typedef struct {
+    float eta_world, eta_self, w_world, w_self;
+    int32_t swept, sweep_steps;
+} vapr_cost_params;
+
+/* Options (vapr_set_option). */
+enum {
+    VAPR_OPT_CULL = 0      /* 1 (default): exact broadphase culling; 0: brute force */
+};
+
+/* ---- context and tables ------------------------------------------------ */
+vapr_status vapr_create(int device, vapr_ctx **out);
+vapr_status vapr_destroy(vapr_ctx *ctx);
+const char *vapr_status_string(vapr_status s);
+const char *vapr_version(void);
+
+/* "E<e>M<m>", case-insensitive. */
+vapr_status vapr_format_parse(const char *s, vapr_format *out);
+vapr_status vapr_format_check(vapr_format f);
+/* Words per packed row of `cols` elements: roundup4(ceil(cols / floor(32/t)));
+ * 0 for an invalid format. */
+size_t vapr_packed_row_words(vapr_format f, size_t cols);
+
+/* Formats of the five slots, indexed by VAPR_OUT_SPHERES.. ("provide
+ * reduced-precision FP data types for the tensors"). */
+vapr_status vapr_set_formats(vapr_ctx *ctx, const vapr_format fmts[VAPR_NUM_SLOTS]);
+vapr_status vapr_set_robot(vapr_ctx *ctx, const vapr_robot *robot);
+/* n_worlds worlds; world w owns cuboids[offsets[w] .. offsets[w+1]) (host
+ * arrays, copied to the device; at most VAPR_MAX_CUBOIDS_PER_WORLD each). */
+vapr_status vapr_set_worlds(vapr_ctx *ctx, int32_t n_worlds, const vapr_cuboid *cuboids,
+                            const int32_t *offsets);
+vapr_status vapr_set_option(vapr_ctx *ctx, int32_t option, int32_t value);
+
+/* ---- a1: codec (context free) ------------------------------------------ */
+/* Quantise x [rows, cols] float32 to packed [rows, row_words] (P:227
+ * "quantizing the tensors from FP32 to the specified data format"). */
+vapr_status vapr_quantize(vapr_format f, const float *x, size_t rows, size_t cols,
+                          uint32_t *packed, void *stream);
+/* Dequantise packed [rows, row_words] to y [rows, cols] float32 (P:227
+ * "dequantizing them back to FP32").  Exact. */
+vapr_status vapr_dequantize(vapr_format f, const uint32_t *packed, size_t rows, size_t cols,
+                            float *y, void *stream);
+
+/* ---- a2: forward kinematics -> packed out_spheres ----------------------- */
+/* P:86 (forward kinematics), P:189 ("The output of forward kinematics:
+ * out_spheres").  out_spheres [B*H, row_words(fmt[OUT_SPHERES], 3S)]. */
+vapr_status vapr_fk_spheres(vapr_ctx *ctx, const float *q, int32_t B, int32_t H,
+                            uint32_t *out_spheres, void *stream);
+
+/* ---- a3: world collision ----------------------------------------------- */
+/* P:86, P:189 ("the output of collision cost: closest_pt for IKO and
+ * closest_pt_swept for TO").  Reads packed out_spheres; writes cost [B, H]
+ * (weighted smooth-hinge world cost per pose; swept: plus the samples of
+ * segment (h, h+1)) and grad = the weighted d(world cost)/d(sphere centre),
+ * packed at fmt[CLOSEST_PT] (swept = 0) or fmt[CLOSEST_PT_SWEPT] (swept = 1). */
+vapr_status vapr_world_collision(vapr_ctx *ctx, const uint32_t *out_spheres,
+                                 const int32_t *world_idx, int32_t B, int32_t H,
+                                 int32_t swept, int32_t sweep_steps, float eta, float weight,
+                                 float *cost, uint32_t *grad, void *stream);
+
+/* ---- a4: self collision ------------------------------------------------ */
+/* P:86, P:189 ("the input of self-collision cost: out_vec").  cost [B, H];
+ * out_vec = weighted d(self cost)/d(sphere centre), packed at fmt[OUT_VEC]. */
+vapr_status vapr_self_collision(vapr_ctx *ctx, const uint32_t *out_spheres, int32_t B,
+                                int32_t H, float eta, float weight, float *cost,
+                                uint32_t *out_vec, void *stream);
+
+/* ---- a3+a4 fused: one pass over out_spheres (the vapr_cost_grad stage) --- */
+/* cost_pose [B, H] = world + self cost; cost_traj [B] (nullable) = sum over h.
+ * cp_grad at fmt[CLOSEST_PT(_SWEPT)] and out_vec at fmt[OUT_VEC]. */
+vapr_status vapr_collision(vapr_ctx *ctx, const uint32_t *out_spheres, const int32_t *world_idx,
+                           int32_t B, int32_t H, const vapr_cost_params *params,
+                           float *cost_pose, float *cost_traj, uint32_t *cp_grad,
+                           uint32_t *out_vec, void *stream);
+
+/* ---- a5: aggregation -> packed grad_out_spheres ------------------------- */
+/* P:162 step (4) "Aggregating the costs", P:189 ("the input of backward
+ * kinematics: grad_out_spheres"): gos = Q(dequant(cp_grad) + dequant(out_vec))
+ * elementwise over n_rows pose rows.  cp_grad is read at fmt[CLOSEST_PT_SWEPT]
+ * if swept else fmt[CLOSEST_PT]. */
+vapr_status vapr_aggregate(vapr_ctx *ctx, const uint32_t *cp_grad, int32_t swept,
+                           const uint32_t *out_vec, int64_t n_rows,
+                           uint32_t *grad_out_spheres, void *stream);
+
+/* ---- a6: backward kinematics -> grad_q ----------------------------------- */
+/* P:162 step (5) "Compute backward".  grad_q_j = sum over spheres on
+ * links >= j of z_j . ((c_s - o_j) x g_s), c_s the FK centre recomputed in
+ * FP32 from q (reading c20), g = dequant(grad_out_spheres); zero rows and
+ * zero spheres are skipped ("sparsity-aware computation"). */
+vapr_status vapr_backward_kinematics(vapr_ctx *ctx, const float *q, int32_t B, int32_t H,
+                                     const uint32_t *grad_out_spheres, float *grad_q,
+                                     void *stream);
+
+/* ---- a7: the composed rollout cost + gradient --------------------------- */
+/* FK -> fused collision (swept per params) -> aggregate -> BK on `stream`;
+ * every live tensor (out_spheres, closest_pt[_swept], out_vec,
+ * grad_out_spheres) is written once to HBM, packed, inside `workspace`
+ * (P:162).  cost_pose and cost_traj are nullable. */
+size_t vapr_cost_grad_workspace_bytes(const vapr_ctx *ctx, int32_t B, int32_t H);
+/* Byte offsets of the packed tensors inside the workspace (slot-indexed;
+ * SIZE_MAX for a slot that is not live) -- lets callers inspect them. */
+vapr_status vapr_cost_grad_workspace_layout(const vapr_ctx *ctx, int32_t B, int32_t H,
+                                            int32_t swept, size_t offsets[VAPR_NUM_SLOTS]);
+vapr_status vapr_cost_grad(vapr_ctx *ctx, const float *q, const int32_t *world_idx,
+                           int32_t B, int32_t H, const vapr_cost_params *params,
+                           void *workspace, size_t workspace_bytes,
+                           float *cost_pose, float *cost_traj, float *grad_q, void *stream);
+
+/* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
+/* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =
+ * its lowest argmin; problem p owns trajectories [p*seeds, (p+1)*seeds). */
+vapr_status vapr_best_per_problem(const float *cost_traj, int32_t n_problems, int32_t seeds,
+                                  float *best_cost, int32_t *best_seed, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VAPR_H */

@@ -1,0 +1,43 @@
+"""Build libvapr.so in-tree for sm_100a with nvcc (no JIT, no torch extension).
+
+    python -m paper_2310_07854_b200.build [--force]
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "libvapr.so")
+SOURCES = ["api.cu", "codec.cu", "fk.cu", "collision.cu", "aggregate.cu", "bk.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
+         # exact IEEE FP32: no flush-to-zero (the codec's subnormal path and the
+         # decode multiply rely on it), correctly rounded div/sqrt, no fast-math
+         "-ftz=false", "-prec-div=true", "-prec-sqrt=true", "-fmad=true"]
+
+
+def _stale():
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(HERE, "..", "include", "vapr.h"))
+    deps.append(__file__)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False, extra=()):
+    if not force and not _stale():
+        return SO
+    cmd = [NVCC, *FLAGS, *extra, "-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True,
+          extra=["-Xptxas", "-v"] if "-v" in sys.argv else [])

@@ -1,0 +1,549 @@
+// api.cu -- the C ABI of libvapr (include/vapr.h): argument validation,
+// context state (robot / worlds / formats), and stage composition.  Every
+// entry point validates synchronously, enqueues on the caller's stream and
+// returns; no allocation or synchronisation on the hot path.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace vapr;
+
+struct vapr_ctx {
+    int device = 0;
+    int sms = 148;
+    bool robot_set = false, worlds_set = false, formats_set = false;
+    RobotDev robot{};
+    vapr_format fmts[VAPR_NUM_SLOTS]{};
+    Fmt dfmt[VAPR_NUM_SLOTS]{};
+    float4* d_cub = nullptr;
+    int32_t* d_off = nullptr;
+    int32_t n_worlds = 0;
+    int cull = 1;
+};
+
+namespace {
+
+// Make the context's device current for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool fmt_valid(vapr_format f) {
+    return f.exp_bits >= 2 && f.exp_bits <= 8 && f.man_bits >= 1 && f.man_bits <= 23 &&
+           1 + f.exp_bits + f.man_bits <= 32;
+}
+
+// Host-side derivation of the device codec constants (common.cuh, Fmt).
+Fmt make_fmt(vapr_format v) {
+    Fmt f{};
+    f.E = v.exp_bits;
+    f.M = v.man_bits;
+    f.t = 1 + f.E + f.M;
+    f.pf = 32 / f.t;
+    f.identity = (f.E == 8 && f.M == 23) ? 1 : 0;
+    const int bias = (1 << (f.E - 1)) - 1;
+    f.sh = 23 - f.M;
+    f.rnd = f.sh > 0 ? (1u << (f.sh - 1)) - 1u : 0u;
+    f.off = (uint32_t)(127 - bias) << f.M;
+    f.minnorm = (uint32_t)(128 - bias) << 23;                 // 2^(1-bias)
+    f.magic_bits = (uint32_t)(127 + 24 - bias - f.M) << 23;    // 2^(24-bias-M)
+    const uint32_t emax = (f.E == 8) ? 254u : (1u << f.E) - 1u;
+    f.maxcode = (f.M < 32) ? ((emax << f.M) | ((1u << f.M) - 1u)) : 0xffffffffu;
+    f.mask = (f.t >= 32) ? 0xffffffffu : ((1u << f.t) - 1u);
+    f.magmask = (f.t >= 32) ? 0x7fffffffu : ((1u << (f.t - 1)) - 1u);
+    uint32_t sc = (uint32_t)(254 - bias) << 23;                // 2^(127-bias)
+    std::memcpy(&f.dscale, &sc, 4);
+    return f;
+}
+
+vapr_status cuda_status(cudaError_t e) { return e == cudaSuccess ? VAPR_OK : VAPR_ERR_CUDA; }
+
+vapr_status pending_fault() {
+    // surface an earlier asynchronous fault without clearing sticky errors
+    const cudaError_t e = cudaPeekAtLastError();
+    return e == cudaSuccess ? VAPR_OK : VAPR_ERR_CUDA;
+}
+
+#define CHECK(cond, st) \
+    do {                \
+        if (!(cond)) return (st); \
+    } while (0)
+
+size_t packed_bytes(const Fmt& f, int cols, long long rows) {
+    return (size_t)row_words_of(f, cols) * 4u * (size_t)rows;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+WorldsDev worlds_of(const vapr_ctx* c) { return WorldsDev{c->d_cub, c->d_off, c->n_worlds}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* vapr_version(void) { return "libvapr 0.1 (sm_100a)"; }
+
+const char* vapr_status_string(vapr_status s) {
+    switch (s) {
+        case VAPR_OK: return "ok";
+        case VAPR_ERR_INVALID_FORMAT: return "invalid format";
+        case VAPR_ERR_INVALID_ARG: return "invalid argument";
+        case VAPR_ERR_SHAPE: return "invalid shape";
+        case VAPR_ERR_CUDA: return "cuda error";
+        case VAPR_ERR_NOT_INITIALIZED: return "context not initialised";
+        case VAPR_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+vapr_status vapr_create(int device, vapr_ctx** out) {
+    CHECK(out != nullptr, VAPR_ERR_INVALID_ARG);
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return VAPR_ERR_CUDA;
+    }
+    vapr_ctx* c = new (std::nothrow) vapr_ctx();
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    for (int i = 0; i < VAPR_NUM_SLOTS; ++i) {
+        c->fmts[i] = vapr_format{8, 23};
+        c->dfmt[i] = make_fmt(c->fmts[i]);
+    }
+    *out = c;
+    return VAPR_OK;
+}
+
+vapr_status vapr_destroy(vapr_ctx* c) {
+    if (!c) return VAPR_OK;
+    DeviceGuard g(c->device);
+    if (c->d_cub) cudaFree(c->d_cub);
+    if (c->d_off) cudaFree(c->d_off);
+    delete c;
+    return VAPR_OK;
+}
+
+vapr_status vapr_format_check(vapr_format f) {
+    return fmt_valid(f) ? VAPR_OK : VAPR_ERR_INVALID_FORMAT;
+}
+
+vapr_status vapr_format_parse(const char* s, vapr_format* out) {
+    CHECK(s != nullptr && out != nullptr, VAPR_ERR_INVALID_ARG);
+    int e = -1, m = -1;
+    char c0 = 0, c1 = 0;
+    int nread = 0;
+    if (std::sscanf(s, " %c%d%c%d %n", &c0, &e, &c1, &m, &nread) != 4 || s[nread] != '\0')
+        return VAPR_ERR_INVALID_FORMAT;
+    if ((c0 != 'E' && c0 != 'e') || (c1 != 'M' && c1 != 'm')) return VAPR_ERR_INVALID_FORMAT;
+    vapr_format f{e, m};
+    CHECK(fmt_valid(f), VAPR_ERR_INVALID_FORMAT);
+    *out = f;
+    return VAPR_OK;
+}
+
+size_t vapr_packed_row_words(vapr_format f, size_t cols) {
+    if (!fmt_valid(f)) return 0;
+    const size_t pf = 32 / (1 + f.exp_bits + f.man_bits);
+    const size_t w = (cols + pf - 1) / pf;
+    return (w + 3) & ~(size_t)3;
+}
+
+vapr_status vapr_set_formats(vapr_ctx* c, const vapr_format* fmts) {
+    CHECK(c != nullptr && fmts != nullptr, VAPR_ERR_INVALID_ARG);
+    for (int i = 0; i < VAPR_NUM_SLOTS; ++i) CHECK(fmt_valid(fmts[i]), VAPR_ERR_INVALID_FORMAT);
+    for (int i = 0; i < VAPR_NUM_SLOTS; ++i) {
+        c->fmts[i] = fmts[i];
+        c->dfmt[i] = make_fmt(fmts[i]);
+    }
+    c->formats_set = true;
+    return VAPR_OK;
+}
+
+vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
+    CHECK(c != nullptr && r != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(r->n_spheres >= 1 && r->n_spheres <= VAPR_MAX_SPHERES, VAPR_ERR_SHAPE);
+    CHECK(r->n_pairs >= 0 && r->n_pairs <= VAPR_MAX_PAIRS, VAPR_ERR_SHAPE);
+    CHECK(r->sphere_link != nullptr && r->sphere_xyzr != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(r->n_pairs == 0 || r->pairs != nullptr, VAPR_ERR_INVALID_ARG);
+    RobotDev R{};
+    R.n_spheres = r->n_spheres;
+    R.cols = 3 * r->n_spheres;
+    for (int i = 0; i < 8; ++i) {
+        R.ca[i] = (float)std::cos(r->dh_alpha[i]);
+        R.sa[i] = (float)std::sin(r->dh_alpha[i]);
+        R.a[i] = (float)r->dh_a[i];
+        R.d[i] = (float)r->dh_d[i];
+    }
+    R.hand_c = (float)std::cos(r->hand_rz);
+    R.hand_s = (float)std::sin(r->hand_rz);
+    int prev = 0;
+    int count[kLinks] = {0};
+    for (int s = 0; s < r->n_spheres; ++s) {
+        const int l = r->sphere_link[s];
+        CHECK(l >= 0 && l < kLinks, VAPR_ERR_INVALID_ARG);
+        CHECK(l >= prev, VAPR_ERR_UNSUPPORTED);            // spheres must be sorted by link
+        prev = l;
+        count[l]++;
+        R.sx[s] = r->sphere_xyzr[4 * s + 0];
+        R.sy[s] = r->sphere_xyzr[4 * s + 1];
+        R.sz[s] = r->sphere_xyzr[4 * s + 2];
+        R.sr[s] = r->sphere_xyzr[4 * s + 3];
+    }
+    R.link_start[0] = 0;
+    for (int l = 0; l < kLinks; ++l) R.link_start[l + 1] = R.link_start[l] + count[l];
+    // adjacency lists (each pair from both ends), partners in ascending order
+    std::vector<std::vector<int>> adj(r->n_spheres);
+    for (int k = 0; k < r->n_pairs; ++k) {
+        const int i = r->pairs[2 * k], j = r->pairs[2 * k + 1];
+        CHECK(i < r->n_spheres && j < r->n_spheres && i != j, VAPR_ERR_INVALID_ARG);
+        adj[i].push_back(j);
+        adj[j].push_back(i);
+    }
+    int o = 0;
+    for (int s = 0; s < r->n_spheres; ++s) {
+        R.adj_off[s] = (uint16_t)o;
+        std::vector<int>& a = adj[s];
+        std::sort(a.begin(), a.end());
+        for (int v : a) R.adj[o++] = (uint8_t)v;
+    }
+    R.adj_off[r->n_spheres] = (uint16_t)o;
+    c->robot = R;
+    c->robot_set = true;
+    return VAPR_OK;
+}
+
+vapr_status vapr_set_worlds(vapr_ctx* c, int32_t n_worlds, const vapr_cuboid* cub,
+                            const int32_t* offsets) {
+    CHECK(c != nullptr && offsets != nullptr && n_worlds >= 1, VAPR_ERR_INVALID_ARG);
+    CHECK(offsets[0] == 0, VAPR_ERR_INVALID_ARG);
+    for (int w = 0; w < n_worlds; ++w) {
+        const int k = offsets[w + 1] - offsets[w];
+        CHECK(k >= 0 && k <= VAPR_MAX_CUBOIDS_PER_WORLD, VAPR_ERR_SHAPE);
+    }
+    const int n = offsets[n_worlds];
+    CHECK(n == 0 || cub != nullptr, VAPR_ERR_INVALID_ARG);
+    // device form per cuboid: R^T row-major (9), t (3), half (3), pad
+    std::vector<float> h((size_t)std::max(n, 1) * 16, 0.f);
+    for (int k = 0; k < n; ++k) {
+        float* d = &h[(size_t)k * 16];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) d[3 * i + j] = cub[k].R[3 * j + i];
+        for (int i = 0; i < 3; ++i) d[9 + i] = cub[k].t[i];
+        for (int i = 0; i < 3; ++i) {
+            CHECK(cub[k].half[i] >= 0.f, VAPR_ERR_INVALID_ARG);
+            d[12 + i] = cub[k].half[i];
+        }
+    }
+    DeviceGuard g(c->device);
+    CHECK(g.ok, VAPR_ERR_CUDA);
+    float4* d_cub = nullptr;
+    int32_t* d_off = nullptr;
+    if (cudaMalloc(&d_cub, h.size() * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&d_off, sizeof(int32_t) * (n_worlds + 1)) != cudaSuccess) {
+        if (d_cub) cudaFree(d_cub);
+        cudaGetLastError();
+        return VAPR_ERR_CUDA;
+    }
+    if (cudaMemcpy(d_cub, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice) !=
+            cudaSuccess ||
+        cudaMemcpy(d_off, offsets, sizeof(int32_t) * (n_worlds + 1), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+        cudaFree(d_cub);
+        cudaFree(d_off);
+        return VAPR_ERR_CUDA;
+    }
+    if (c->d_cub) cudaFree(c->d_cub);
+    if (c->d_off) cudaFree(c->d_off);
+    c->d_cub = d_cub;
+    c->d_off = d_off;
+    c->n_worlds = n_worlds;
+    c->worlds_set = true;
+    return VAPR_OK;
+}
+
+vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    if (option == VAPR_OPT_CULL) {
+        c->cull = value ? 1 : 0;
+        return VAPR_OK;
+    }
+    return VAPR_ERR_UNSUPPORTED;
+}
+
+// ---- a1 ------------------------------------------------------------------
+vapr_status vapr_quantize(vapr_format f, const float* x, size_t rows, size_t cols,
+                          uint32_t* packed, void* stream) {
+    CHECK(fmt_valid(f), VAPR_ERR_INVALID_FORMAT);
+    if (rows == 0 || cols == 0) return VAPR_OK;
+    CHECK(x != nullptr && packed != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(aligned16(x) && aligned16(packed), VAPR_ERR_INVALID_ARG);
+    CHECK(cols < (1u << 30), VAPR_ERR_SHAPE);
+    CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    const Fmt d = make_fmt(f);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return cuda_status(launch_quantize(d, x, rows, cols, vapr_packed_row_words(f, cols), packed,
+                                       sms, (cudaStream_t)stream));
+}
+
+vapr_status vapr_dequantize(vapr_format f, const uint32_t* packed, size_t rows, size_t cols,
+                            float* y, void* stream) {
+    CHECK(fmt_valid(f), VAPR_ERR_INVALID_FORMAT);
+    if (rows == 0 || cols == 0) return VAPR_OK;
+    CHECK(y != nullptr && packed != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(aligned16(y) && aligned16(packed), VAPR_ERR_INVALID_ARG);
+    CHECK(cols < (1u << 30), VAPR_ERR_SHAPE);
+    CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    const Fmt d = make_fmt(f);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return cuda_status(launch_dequantize(d, packed, rows, cols, vapr_packed_row_words(f, cols),
+                                         y, sms, (cudaStream_t)stream));
+}
+
+// ---- a2 ------------------------------------------------------------------
+vapr_status vapr_fk_spheres(vapr_ctx* c, const float* q, int32_t B, int32_t H,
+                            uint32_t* out_spheres, void* stream) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set, VAPR_ERR_NOT_INITIALIZED);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(q && out_spheres && aligned16(q) && aligned16(out_spheres), VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], q, (long long)B * H,
+                                 out_spheres, (cudaStream_t)stream));
+}
+
+// ---- a3 / a4 -------------------------------------------------------------
+static vapr_status collision_common(vapr_ctx* c, const uint32_t* os, const int32_t* world_idx,
+                                    int32_t B, int32_t H, int do_world, int do_self,
+                                    int32_t swept, int32_t sweep_steps, float eta_w, float w_w,
+                                    float eta_s, float w_s, float* cost, uint32_t* cp,
+                                    uint32_t* ov, float* cost_traj, cudaStream_t s) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set && (!do_world || c->worlds_set), VAPR_ERR_NOT_INITIALIZED);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(!(do_world && swept) || H >= 2, VAPR_ERR_SHAPE);
+    CHECK(os && cost && aligned16(os) && aligned16(cost), VAPR_ERR_INVALID_ARG);
+    if (do_world) {
+        CHECK(world_idx && cp && aligned16(world_idx) && aligned16(cp), VAPR_ERR_INVALID_ARG);
+        CHECK(std::isfinite(eta_w) && eta_w > 0.f && std::isfinite(w_w), VAPR_ERR_INVALID_ARG);
+        CHECK(sweep_steps >= 0 && sweep_steps <= 64, VAPR_ERR_INVALID_ARG);
+    }
+    if (do_self) {
+        CHECK(ov && aligned16(ov), VAPR_ERR_INVALID_ARG);
+        CHECK(std::isfinite(eta_s) && eta_s > 0.f && std::isfinite(w_s), VAPR_ERR_INVALID_ARG);
+    }
+    CHECK(cost_traj == nullptr || aligned16(cost_traj), VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    CollisionArgs a{};
+    a.os = os;
+    a.world_idx = world_idx;
+    a.B = B;
+    a.H = H;
+    a.do_world = do_world;
+    a.do_self = do_self;
+    a.swept = swept ? 1 : 0;
+    a.sweep_steps = sweep_steps;
+    a.eta_w = do_world ? eta_w : 1.f;
+    a.w_w = w_w;
+    a.eta_s = do_self ? eta_s : 1.f;
+    a.w_s = w_s;
+    a.cull = c->cull;
+    a.cost = cost;
+    a.cp = cp;
+    a.ov = ov;
+    const Fmt& fcp = c->dfmt[swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT];
+    cudaError_t e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], fcp,
+                                     c->dfmt[VAPR_OUT_VEC], a, s);
+    if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cost, B, H, cost_traj, s);
+    return cuda_status(e);
+}
+
+vapr_status vapr_world_collision(vapr_ctx* c, const uint32_t* os, const int32_t* world_idx,
+                                 int32_t B, int32_t H, int32_t swept, int32_t sweep_steps,
+                                 float eta, float weight, float* cost, uint32_t* grad,
+                                 void* stream) {
+    return collision_common(c, os, world_idx, B, H, 1, 0, swept, sweep_steps, eta, weight, 1.f,
+                            0.f, cost, grad, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+vapr_status vapr_self_collision(vapr_ctx* c, const uint32_t* os, int32_t B, int32_t H, float eta,
+                                float weight, float* cost, uint32_t* out_vec, void* stream) {
+    return collision_common(c, os, nullptr, B, H, 0, 1, 0, 0, 1.f, 0.f, eta, weight, cost,
+                            nullptr, out_vec, nullptr, (cudaStream_t)stream);
+}
+
+vapr_status vapr_collision(vapr_ctx* c, const uint32_t* os, const int32_t* world_idx, int32_t B,
+                           int32_t H, const vapr_cost_params* p, float* cost_pose,
+                           float* cost_traj, uint32_t* cp, uint32_t* ov, void* stream) {
+    CHECK(p != nullptr, VAPR_ERR_INVALID_ARG);
+    return collision_common(c, os, world_idx, B, H, 1, 1, p->swept, p->sweep_steps, p->eta_world,
+                            p->w_world, p->eta_self, p->w_self, cost_pose, cp, ov, cost_traj,
+                            (cudaStream_t)stream);
+}
+
+// ---- a5 ------------------------------------------------------------------
+vapr_status vapr_aggregate(vapr_ctx* c, const uint32_t* cp, int32_t swept, const uint32_t* ov,
+                           int64_t n_rows, uint32_t* gos, void* stream) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set, VAPR_ERR_NOT_INITIALIZED);
+    CHECK(n_rows >= 1, VAPR_ERR_SHAPE);
+    CHECK(cp && ov && gos && aligned16(cp) && aligned16(ov) && aligned16(gos),
+          VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_aggregate(
+        c->dfmt[swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT], c->dfmt[VAPR_OUT_VEC],
+        c->dfmt[VAPR_GRAD_OUT_SPHERES], c->robot.cols, cp, ov, n_rows, gos,
+        (cudaStream_t)stream));
+}
+
+// ---- a6 ------------------------------------------------------------------
+vapr_status vapr_backward_kinematics(vapr_ctx* c, const float* q, int32_t B, int32_t H,
+                                     const uint32_t* gos, float* grad_q, void* stream) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set, VAPR_ERR_NOT_INITIALIZED);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(q && gos && grad_q && aligned16(q) && aligned16(gos) && aligned16(grad_q),
+          VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], q, (long long)B * H,
+                                 gos, grad_q, (cudaStream_t)stream));
+}
+
+// ---- a7 ------------------------------------------------------------------
+static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR_NUM_SLOTS],
+                      size_t* cost_off, size_t* total) {
+    const int cols = c->robot.cols;
+    for (int i = 0; i < VAPR_NUM_SLOTS; ++i) off[i] = SIZE_MAX;
+    size_t o = 0;
+    off[VAPR_OUT_SPHERES] = o;
+    o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_SPHERES], cols, P));
+    const int cps = swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
+    off[cps] = o;
+    // reserve the larger of the two collision slots so one workspace serves both modes
+    o = align256(o + std::max(packed_bytes(c->dfmt[VAPR_CLOSEST_PT], cols, P),
+                              packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
+    off[VAPR_OUT_VEC] = o;
+    o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
+    off[VAPR_GRAD_OUT_SPHERES] = o;
+    o = align256(o + packed_bytes(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P));
+    *cost_off = o;
+    o = align256(o + sizeof(float) * (size_t)P);
+    *total = o;
+}
+
+size_t vapr_cost_grad_workspace_bytes(const vapr_ctx* c, int32_t B, int32_t H) {
+    if (!c || B < 1 || H < 1) return 0;
+    size_t off[VAPR_NUM_SLOTS], co, total;
+    ws_layout(c, (long long)B * H, 1, off, &co, &total);
+    return total;
+}
+
+vapr_status vapr_cost_grad_workspace_layout(const vapr_ctx* c, int32_t B, int32_t H,
+                                            int32_t swept, size_t* offsets) {
+    CHECK(c != nullptr && offsets != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    size_t co, total;
+    ws_layout(c, (long long)B * H, swept, offsets, &co, &total);
+    return VAPR_OK;
+}
+
+vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx, int32_t B,
+                           int32_t H, const vapr_cost_params* p, void* workspace,
+                           size_t workspace_bytes, float* cost_pose, float* cost_traj,
+                           float* grad_q, void* stream) {
+    CHECK(c != nullptr && p != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set && c->worlds_set && c->formats_set, VAPR_ERR_NOT_INITIALIZED);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(!p->swept || H >= 2, VAPR_ERR_SHAPE);
+    CHECK(q && world_idx && grad_q && workspace, VAPR_ERR_INVALID_ARG);
+    CHECK(aligned16(q) && aligned16(world_idx) && aligned16(grad_q) && aligned16(workspace),
+          VAPR_ERR_INVALID_ARG);
+    CHECK(cost_pose == nullptr || aligned16(cost_pose), VAPR_ERR_INVALID_ARG);
+    CHECK(cost_traj == nullptr || aligned16(cost_traj), VAPR_ERR_INVALID_ARG);
+    CHECK(p->eta_world > 0.f && p->eta_self > 0.f && std::isfinite(p->w_world) &&
+              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64,
+          VAPR_ERR_INVALID_ARG);
+    const long long P = (long long)B * H;
+    size_t off[VAPR_NUM_SLOTS], co, total;
+    ws_layout(c, P, p->swept, off, &co, &total);
+    CHECK(workspace_bytes >= total, VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    char* ws = static_cast<char*>(workspace);
+    const int cps = p->swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
+    uint32_t* os = reinterpret_cast<uint32_t*>(ws + off[VAPR_OUT_SPHERES]);
+    uint32_t* cp = reinterpret_cast<uint32_t*>(ws + off[cps]);
+    uint32_t* ov = reinterpret_cast<uint32_t*>(ws + off[VAPR_OUT_VEC]);
+    uint32_t* gos = reinterpret_cast<uint32_t*>(ws + off[VAPR_GRAD_OUT_SPHERES]);
+    float* cpose = cost_pose ? cost_pose : reinterpret_cast<float*>(ws + co);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], q, P, os, s);
+    if (e == cudaSuccess) {
+        CollisionArgs a{};
+        a.os = os;
+        a.world_idx = world_idx;
+        a.B = B;
+        a.H = H;
+        a.do_world = 1;
+        a.do_self = 1;
+        a.swept = p->swept ? 1 : 0;
+        a.sweep_steps = p->sweep_steps;
+        a.eta_w = p->eta_world;
+        a.w_w = p->w_world;
+        a.eta_s = p->eta_self;
+        a.w_s = p->w_self;
+        a.cull = c->cull;
+        a.cost = cpose;
+        a.cp = cp;
+        a.ov = ov;
+        e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
+                             c->dfmt[VAPR_OUT_VEC], a, s);
+    }
+    if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose, B, H, cost_traj, s);
+    if (e == cudaSuccess)
+        e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
+                             c->robot.cols, cp, ov, P, gos, s);
+    if (e == cudaSuccess)
+        e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], q, P, gos, grad_q, s);
+    return cuda_status(e);
+}
+
+// ---- e -------------------------------------------------------------------
+vapr_status vapr_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,
+                                  float* best_cost, int32_t* best_seed, void* stream) {
+    CHECK(n_problems >= 0 && seeds >= 1, VAPR_ERR_SHAPE);
+    if (n_problems == 0) return VAPR_OK;
+    CHECK(cost_traj && best_cost && best_seed, VAPR_ERR_INVALID_ARG);
+    CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_best_per_problem(cost_traj, n_problems, seeds, best_cost, best_seed,
+                                               (cudaStream_t)stream));
+}
+
+}  // extern "C"

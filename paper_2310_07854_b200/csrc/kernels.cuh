@@ -1,0 +1,57 @@
+// kernels.cuh -- host-side launch helpers for the libvapr kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace vapr {
+
+// World table on the device: per cuboid 16 floats = R^T (row-major 3x3), t,
+// half extents, pad; offsets [n_worlds + 1].
+struct WorldsDev {
+    const float4* cub;
+    const int32_t* off;
+    int32_t n_worlds;
+};
+
+struct CollisionArgs {
+    const uint32_t* os;       // packed out_spheres
+    const int32_t* world_idx;
+    int32_t B, H;
+    int32_t do_world, do_self;
+    int32_t swept, sweep_steps;
+    float eta_w, w_w, eta_s, w_s;
+    int32_t cull;
+    float* cost;              // [B*H] (world + self of the enabled parts)
+    uint32_t* cp;             // packed world gradient (nullable iff !do_world)
+    uint32_t* ov;             // packed self gradient (nullable iff !do_self)
+};
+
+cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t cols,
+                            size_t row_words, uint32_t* packed, int sms, cudaStream_t s);
+cudaError_t launch_dequantize(const Fmt& f, const uint32_t* packed, size_t rows, size_t cols,
+                              size_t row_words, float* y, int sms, cudaStream_t s);
+cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
+                      uint32_t* os, cudaStream_t s);
+cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                             cudaStream_t s);
+cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
+                               cudaStream_t s);
+cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
+                             const uint32_t* cp, const uint32_t* ov, long long rows,
+                             uint32_t* gos, cudaStream_t s);
+cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
+                      const uint32_t* gos, float* grad_q, cudaStream_t s);
+cudaError_t launch_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,
+                                    float* best_cost, int32_t* best_seed, cudaStream_t s);
+
+// words per packed row (multiple of 4)
+inline int row_words_of(const Fmt& f, int cols) {
+    const int w = (cols + f.pf - 1) / f.pf;
+    return (w + 3) & ~3;
+}
+
+}  // namespace vapr

@@ -1,0 +1,98 @@
+"""Device-resident rollout runner over the C ABI (the call a user makes).
+
+`Rollout` owns one libvapr context plus the device buffers of one batch of
+trajectories (q, world_idx, the cost_grad workspace and the outputs), all
+allocated once with PyTorch; `run()` enqueues `vapr_cost_grad` on the current
+stream and returns without synchronising.  `run_host()` is the end-to-end
+variant: pinned host q in, host grad_q / cost_traj out, copies included.
+"""
+import numpy as np
+import torch
+
+from . import binding as vb
+
+SLOT_NAMES = ("out_spheres", "grad_out_spheres", "out_vec", "closest_pt", "closest_pt_swept")
+
+
+class Context:
+    """RAII wrapper of a vapr_ctx."""
+
+    def __init__(self, device=0, robot=None, formats=None, cuboids=None, offsets=None):
+        self.device = int(device)
+        self.h = vb.vapr_create(self.device)
+        if robot is not None:
+            vb.vapr_set_robot(self.h, robot)
+        if formats is not None:
+            self.set_formats(formats)
+        if cuboids is not None:
+            vb.vapr_set_worlds(self.h, cuboids, offsets)
+
+    def set_formats(self, formats):
+        self.formats = tuple(tuple(f) for f in formats)
+        vb.vapr_set_formats(self.h, self.formats)
+
+    def set_cull(self, on):
+        vb.vapr_set_option(self.h, vb.VAPR_OPT_CULL, int(on))
+
+    def close(self):
+        if self.h is not None:
+            vb.vapr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Rollout:
+    """One batch [B, H] of trajectories resident in HBM."""
+
+    def __init__(self, workload, device=0, formats=None, ctx=None):
+        self.wl = workload
+        self.device = torch.device("cuda", device)
+        self.ctx = ctx or Context(device, workload.robot, formats or workload.formats,
+                                  workload.cuboids, workload.world_offsets)
+        if formats is not None and ctx is not None:
+            self.ctx.set_formats(formats)
+        self.B, self.H = workload.B, workload.H
+        self.params = dict(workload.params)
+        self._p = vb.cost_params(self.params)
+        d = self.device
+        self.q = torch.from_numpy(np.ascontiguousarray(workload.q)).to(d)
+        self.world_idx = torch.from_numpy(np.ascontiguousarray(workload.world_idx, np.int32)).to(d)
+        nbytes = vb.vapr_cost_grad_workspace_bytes(self.ctx.h, self.B, self.H)
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=d)
+        self.cost_pose = torch.zeros(self.B * self.H, dtype=torch.float32, device=d)
+        self.cost_traj = torch.zeros(self.B, dtype=torch.float32, device=d)
+        self.grad_q = torch.zeros(self.B * self.H * 7, dtype=torch.float32, device=d)
+
+    def set_formats(self, formats):
+        self.ctx.set_formats(formats)
+        need = vb.vapr_cost_grad_workspace_bytes(self.ctx.h, self.B, self.H)
+        if need > self.workspace.numel():
+            self.workspace = torch.zeros(need, dtype=torch.uint8, device=self.device)
+
+    def run(self, stream=None):
+        vb.vapr_cost_grad(self.ctx.h, self.q, self.world_idx, self.B, self.H, self.params,
+                          self.workspace, self.cost_pose, self.cost_traj, self.grad_q,
+                          stream=stream, _p=self._p)
+
+    def packed(self, slot):
+        """The packed tensor of `slot` inside the workspace, as uint32 [P, W]."""
+        lay = vb.vapr_cost_grad_workspace_layout(self.ctx.h, self.B, self.H, self.params["swept"])
+        off = lay[slot]
+        if off is None:
+            return None
+        fmt = self.ctx.formats[slot]
+        W = vb.vapr_packed_row_words(fmt, 3 * len(self.wl.robot["sphere_link"]))
+        P = self.B * self.H
+        words = self.workspace[off:off + 4 * W * P].view(torch.int32).view(P, W)
+        return words.cpu().numpy().view(np.uint32)
+
+    def results(self):
+        torch.cuda.synchronize(self.device)
+        return dict(cost_pose=self.cost_pose.cpu().numpy().reshape(self.B, self.H),
+                    cost_traj=self.cost_traj.cpu().numpy(),
+                    grad_q=self.grad_q.cpu().numpy().reshape(self.B, self.H, 7))

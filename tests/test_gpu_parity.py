@@ -1,0 +1,368 @@
+"""GPU <-> oracle parity through the C ABI (needs a B200)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import codec
+from oracle import rollout as orc
+from oracle.formats import enumerate_formats
+from parity_utils import check_codes, check_close, sphere_to_elem
+from workloads import config1, config2, config4, make_workload
+from workloads.configs import FORMAT_SETS, codec_sweep_inputs, edge_values
+
+pytestmark = pytest.mark.gpu
+
+ALL_FORMATS = enumerate_formats() + [(6, 6), (5, 9), (6, 8)]
+
+
+@pytest.fixture(scope="module")
+def vb():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2310_07854_b200 import binding
+    return binding
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def codec_inputs(fmt, n=1 << 16):
+    mags = codec.representable_magnitudes(*fmt)
+    if len(mags) > 1 << 16:
+        mags = mags[np.linspace(0, len(mags) - 1, 1 << 16).astype(np.int64)]
+    mids = ((mags[:-1] + mags[1:]) / 2).astype(np.float32)
+    x = np.concatenate([codec_sweep_inputs(n, "bits", 1), codec_sweep_inputs(n, "position", 2),
+                        codec_sweep_inputs(n, "gradient", 3), mids,
+                        np.nextafter(mids, np.float32(np.inf)), np.nextafter(mids, np.float32(0)),
+                        mags.astype(np.float32), edge_values()])
+    return np.concatenate([x, -x])
+
+
+# --------------------------------------------------------------------- a1
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
+@pytest.mark.parametrize("cols", [157, 156, 1, 4097])
+def test_quantize_bit_exact(vb, fmt, cols):
+    x = codec_inputs(fmt)
+    rows = len(x) // cols
+    x = x[: rows * cols].reshape(rows, cols)
+    W = vb.vapr_packed_row_words(fmt, cols)
+    out = torch.empty(rows * W, dtype=torch.int32, device="cuda")
+    vb.vapr_quantize(fmt, dev(x), rows, cols, out)
+    got = out.cpu().numpy().view(np.uint32).reshape(rows, W)
+    np.testing.assert_array_equal(got, codec.quantize_packed(x, *fmt))
+
+
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
+def test_dequantize_bit_exact(vb, fmt):
+    E, M = fmt
+    t = 1 + E + M
+    if t <= 16:
+        codes = np.arange(2 ** t, dtype=np.uint32)
+    else:
+        codes = codec_sweep_inputs(1 << 18, "bits", 7).view(np.uint32) & np.uint32((1 << t) - 1 if t < 32 else 0xFFFFFFFF)
+    if E == 8 and M < 23:
+        codes = codes[((codes >> M) & 0xFF) != 255]
+    cols = 131
+    rows = len(codes) // cols
+    codes = codes[: rows * cols].reshape(rows, cols)
+    words = codec.pack(codes, E, M)
+    y = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    vb.vapr_dequantize(fmt, dev(words.view(np.int32)), rows, cols, y)
+    got = y.cpu().numpy().reshape(rows, cols)
+    ref = codec.dequantize(codes, E, M)
+    same = (got.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(got) & np.isnan(ref))
+    assert same.all()
+
+
+def test_codec_empty_and_errors(vb):
+    x = torch.zeros(16, device="cuda")
+    out = torch.zeros(16, dtype=torch.int32, device="cuda")
+    vb.vapr_quantize((2, 1), x, 0, 16, out)          # empty: no-op
+    with pytest.raises(vb.VaprError):
+        vb.vapr_quantize((9, 1), x, 1, 16, out)
+    with pytest.raises(vb.VaprError):
+        vb.vapr_quantize((2, 1), x[1:], 1, 8, out)    # misaligned
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ALL_FORMATS)
+def test_quantize_exhaustive_all_fp32(vb, fmt):
+    """All 2^32 FP32 bit patterns (SURVEY.md §4 codec tier).  Long: runs only
+    with VAPR_EXHAUSTIVE=1 (a dedicated GPU call), not in the default suite."""
+    import os
+    if os.environ.get("VAPR_EXHAUSTIVE") != "1":
+        pytest.skip("set VAPR_EXHAUSTIVE=1")
+    E, M = fmt
+    t = 1 + E + M
+    pf = 32 // t
+    chunk = 1 << 26
+    cols = chunk
+    W = vb.vapr_packed_row_words(fmt, cols)
+    out = torch.empty(W, dtype=torch.int32, device="cuda")
+    base_bits = torch.arange(chunk, dtype=torch.int64, device="cuda")
+    threads = os.cpu_count() or 8
+    shifts = torch.arange(pf, device="cuda", dtype=torch.int64) * t
+    mask = (1 << t) - 1 if t < 32 else 0xFFFFFFFF
+    for base in range(0, 1 << 32, chunk):
+        x = ((base_bits + base) & 0xFFFFFFFF).to(torch.int64)
+        xi = torch.where(x >= 2 ** 31, x - 2 ** 32, x).to(torch.int32)
+        vb.vapr_quantize(fmt, xi.view(torch.float32), 1, cols, out)
+        w = out.to(torch.int64) & 0xFFFFFFFF
+        codes = ((w[:, None] >> shifts[None, :]) & mask).reshape(-1)[:chunk]
+        ref = torch.from_numpy(codec.quantize_bits_range(base, chunk, E, M, threads).view(np.int32)).cuda()
+        ref = ref.to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(codes, ref), (fmt, hex(base))
+
+
+# --------------------------------------------------------------------- helpers
+class Ctx:
+    def __init__(self, vb, wl, formats=None):
+        self.vb = vb
+        self.wl = wl
+        self.h = vb.vapr_create(0)
+        vb.vapr_set_robot(self.h, wl.robot)
+        vb.vapr_set_worlds(self.h, wl.cuboids, wl.world_offsets)
+        self.formats = tuple(formats or wl.formats)
+        vb.vapr_set_formats(self.h, self.formats)
+
+    def __del__(self):
+        self.vb.vapr_destroy(self.h)
+
+    def W(self, slot):
+        return self.vb.vapr_packed_row_words(self.formats[slot], 156)
+
+
+def ragged_workload(B=3, H=5, formats="43bit", salt=9):
+    from workloads.scenes import ENVIRONMENTS
+    envs = [ENVIRONMENTS[i % 8] for i in range(B)]
+    return make_workload("ragged", envs, list(range(B)), 1, H, FORMAT_SETS[formats], salt=salt)
+
+
+WORKLOADS = {
+    "config1": lambda: config1(),
+    "config1_fp32": lambda: config1(reduced=False),
+    "config2": lambda: config2(),
+    "ragged_43": lambda: ragged_workload(),
+    "mixed_envs": lambda: config4(problems_per_env=1, seeds=3, H=32),
+    "bookshelf_tall": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="bookshelf_tall"),
+    "fp16": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="fp16"),
+    "fp32": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="fp32"),
+}
+
+
+# --------------------------------------------------------------------- a2
+@pytest.mark.parametrize("name", list(WORKLOADS))
+def test_fk_spheres(vb, name):
+    wl = WORKLOADS[name]()
+    c = Ctx(vb, wl)
+    P = wl.poses
+    fos = c.formats[0]
+    out = torch.empty(P * c.W(0), dtype=torch.int32, device="cuda")
+    vb.vapr_fk_spheres(c.h, dev(wl.q), wl.B, wl.H, out)
+    words, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, fos)
+    got = out.cpu().numpy().view(np.uint32).reshape(P, -1)
+    exact = check_codes(got, v, 1.0, fos, 156, what="out_spheres",
+                        min_exact=0.999 if fos != (8, 23) else None)
+    assert exact > 0.99 or fos == (8, 23)
+
+
+# --------------------------------------------------------------------- a3/a4
+@pytest.mark.parametrize("name", list(WORKLOADS))
+@pytest.mark.parametrize("swept", [1, 0])
+def test_collision_stage(vb, name, swept):
+    wl = WORKLOADS[name]()
+    c = Ctx(vb, wl)
+    P, B, H = wl.poses, wl.B, wl.H
+    p = dict(wl.params, swept=swept)
+    f = c.formats
+    os_words, _ = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
+    slot = 4 if swept else 3
+    cp = torch.empty(P * c.W(slot), dtype=torch.int32, device="cuda")
+    ov = torch.empty(P * c.W(2), dtype=torch.int32, device="cuda")
+    cost = torch.empty(P, dtype=torch.float32, device="cuda")
+    ctraj = torch.empty(B, dtype=torch.float32, device="cuda")
+    vb.vapr_collision(c.h, dev(os_words.view(np.int32)), dev(wl.world_idx), B, H, p, cost, ctraj, cp, ov)
+    ws = orc.world_stage(os_words, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
+                         B, H, p["eta_world"], p["w_world"], swept, p["sweep_steps"], f[slot])
+    ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    ref_cost = ws["cost"].reshape(-1) + ss["cost"]
+    scale = ws["cost_scale"].reshape(-1) + ss["cost_scale"]
+    check_close(cost.cpu().numpy(), ref_cost, scale, "cost_pose")
+    check_close(ctraj.cpu().numpy(), ref_cost.reshape(B, H).sum(1), scale.reshape(B, H).sum(1), "cost_traj")
+    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], sphere_to_elem(ws["gscale"]),
+                f[slot], 156, skip=sphere_to_elem(ws["tie"]), what="closest_pt", min_exact=0.999)
+    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], sphere_to_elem(ss["gscale"]),
+                f[2], 156, what="out_vec", min_exact=0.999)
+
+
+def test_world_and_self_separately(vb):
+    wl = config2()
+    c = Ctx(vb, wl)
+    P, B, H = wl.poses, wl.B, wl.H
+    f = c.formats
+    p = wl.params
+    os_words, _ = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
+    osd = dev(os_words.view(np.int32))
+    cp = torch.empty(P * c.W(4), dtype=torch.int32, device="cuda")
+    cost = torch.empty(P, dtype=torch.float32, device="cuda")
+    vb.vapr_world_collision(c.h, osd, dev(wl.world_idx), B, H, 1, 1, p["eta_world"], p["w_world"], cost, cp)
+    ws = orc.world_stage(os_words, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
+                         B, H, p["eta_world"], p["w_world"], 1, 1, f[4])
+    check_close(cost.cpu().numpy(), ws["cost"].reshape(-1), ws["cost_scale"].reshape(-1), "world cost")
+    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], sphere_to_elem(ws["gscale"]),
+                f[4], 156, skip=sphere_to_elem(ws["tie"]), what="closest_pt_swept")
+    ov = torch.empty(P * c.W(2), dtype=torch.int32, device="cuda")
+    vb.vapr_self_collision(c.h, osd, B, H, p["eta_self"], p["w_self"], cost, ov)
+    ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    check_close(cost.cpu().numpy(), ss["cost"], ss["cost_scale"], "self cost")
+    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], sphere_to_elem(ss["gscale"]),
+                f[2], 156, what="out_vec")
+
+
+# --------------------------------------------------------------------- a5
+@pytest.mark.parametrize("fs", ["43bit", "bookshelf_tall", "cage", "fp32", "table_pick"])
+def test_aggregate(vb, fs):
+    wl = config4(problems_per_env=1, seeds=2, H=32, formats=fs)
+    c = Ctx(vb, wl)
+    P = wl.poses
+    f = c.formats
+    res = orc.rollout_workload(wl)
+    gos = torch.empty(P * c.W(1), dtype=torch.int32, device="cuda")
+    vb.vapr_aggregate(c.h, dev(res.cp_words.view(np.int32)), 1, dev(res.ov_words.view(np.int32)), P, gos)
+    v = res.stages["aggregate"]["v"]
+    check_codes(gos.cpu().numpy().view(np.uint32).reshape(P, -1), v, 0.0, f[1], 156,
+                what="grad_out_spheres", min_exact=0.999)
+    # FP32 sum then one rounding: the only allowed differences are at midpoints
+    # within 2^-24 relative of v, covered by TOL
+
+
+# --------------------------------------------------------------------- a6
+@pytest.mark.parametrize("name", ["config2", "ragged_43", "mixed_envs", "fp32"])
+def test_backward_kinematics(vb, name):
+    wl = WORKLOADS[name]()
+    c = Ctx(vb, wl)
+    P = wl.poses
+    res = orc.rollout_workload(wl)
+    gq = torch.empty(P * 7, dtype=torch.float32, device="cuda")
+    vb.vapr_backward_kinematics(c.h, dev(wl.q), wl.B, wl.H, dev(res.gos_words.view(np.int32)), gq)
+    bk = res.stages["bk"]
+    check_close(gq.cpu().numpy().reshape(P, 7), bk["grad_q"], bk["scale"], "grad_q")
+
+
+# --------------------------------------------------------------------- a7
+@pytest.mark.parametrize("name", list(WORKLOADS))
+def test_cost_grad_stagewise(vb, name):
+    """Run the composed path; check each stage against the oracle fed with the
+    GPU's own upstream packed tensor (read back from the workspace)."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = WORKLOADS[name]()
+    r = Rollout(wl)
+    r.run()
+    out = r.results()
+    f = r.ctx.formats
+    p = wl.params
+    B, H, P = wl.B, wl.H, wl.poses
+    slot = 4 if p["swept"] else 3
+    os_w, cp_w, ov_w, gos_w = r.packed(0), r.packed(slot), r.packed(2), r.packed(1)
+    _, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
+    check_codes(os_w, v, 1.0, f[0], 156, what="out_spheres")
+    ws = orc.world_stage(os_w, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot, B, H,
+                         p["eta_world"], p["w_world"], p["swept"], p["sweep_steps"], f[slot])
+    ss = orc.self_stage(os_w, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    check_codes(cp_w, ws["v"], sphere_to_elem(ws["gscale"]), f[slot], 156,
+                skip=sphere_to_elem(ws["tie"]), what="closest_pt_swept")
+    check_codes(ov_w, ss["v"], sphere_to_elem(ss["gscale"]), f[2], 156, what="out_vec")
+    ref_cost = (ws["cost"].reshape(-1) + ss["cost"]).reshape(B, H)
+    scale = (ws["cost_scale"].reshape(-1) + ss["cost_scale"]).reshape(B, H)
+    check_close(out["cost_pose"], ref_cost, scale, "cost_pose")
+    check_close(out["cost_traj"], ref_cost.sum(1), scale.sum(1), "cost_traj")
+    ag = orc.aggregate_stage(cp_w, f[slot], ov_w, f[2], f[1], 156)
+    check_codes(gos_w, ag["v"], 0.0, f[1], 156, what="grad_out_spheres")
+    bk = orc.bk_stage(wl.q.reshape(-1, 7), gos_w, f[1], wl.robot)
+    check_close(out["grad_q"].reshape(P, 7), bk["grad_q"], bk["scale"], "grad_q")
+
+
+def test_cost_grad_fp32_end_to_end(vb):
+    """All-E8M23: the composed GPU result agrees with the oracle rollout
+    directly (no stage re-feeding), within the norm-relative tolerance."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config4(problems_per_env=1, seeds=2, H=32, formats="fp32")
+    r = Rollout(wl)
+    r.run()
+    out = r.results()
+    res = orc.rollout_workload(wl)
+    st = res.stages
+    scale = (st["world"]["cost_scale"].reshape(-1) + st["self"]["cost_scale"]).reshape(wl.B, wl.H)
+    check_close(out["cost_traj"], res.cost_traj, scale.sum(1), "cost_traj", tol=1e-4)
+    gscale = np.abs(res.grad_q).reshape(-1, 7) + st["bk"]["scale"]
+    check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), gscale, "grad_q", tol=1e-4)
+
+
+def test_cost_grad_errors(vb):
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config2()
+    r = Rollout(wl)
+    with pytest.raises(vb.VaprError):          # swept with H = 1
+        vb.vapr_cost_grad(r.ctx.h, r.q, r.world_idx, wl.B * wl.H, 1, wl.params, r.workspace,
+                          r.cost_pose, r.cost_traj, r.grad_q)
+    small = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(vb.VaprError):          # workspace too small
+        vb.vapr_cost_grad(r.ctx.h, r.q, r.world_idx, wl.B, wl.H, wl.params, small,
+                          r.cost_pose, r.cost_traj, r.grad_q)
+    h = vb.vapr_create(0)
+    with pytest.raises(vb.VaprError):          # not initialised
+        vb.vapr_cost_grad(h, r.q, r.world_idx, wl.B, wl.H, wl.params, r.workspace,
+                          r.cost_pose, r.cost_traj, r.grad_q)
+    vb.vapr_destroy(h)
+
+
+def test_discrete_h1_and_best_per_problem(vb):
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = ragged_workload(B=5, H=1)
+    wl.params["swept"] = 0
+    r = Rollout(wl)
+    r.run()
+    out = r.results()
+    res = orc.rollout_workload(wl)
+    st = res.stages
+    scale = (st["world"]["cost_scale"].reshape(-1) + st["self"]["cost_scale"]).reshape(wl.B, 1)
+    check_close(out["cost_traj"], res.cost_traj, scale.sum(1), "cost_traj h=1", tol=1e-3)
+    bc = torch.empty(1, dtype=torch.float32, device="cuda")
+    bs = torch.empty(1, dtype=torch.int32, device="cuda")
+    vb.vapr_best_per_problem(r.cost_traj, 1, 5, bc, bs)
+    ct = r.cost_traj.cpu().numpy()
+    assert bs.item() == int(np.argmin(ct)) and bc.item() == ct.min()
+
+
+def test_full_size_sampled(vb):
+    """config4 at full size (2.56M poses, the bench launch), checked on a
+    sample of trajectories the oracle can recompute one by one."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config4()
+    r = Rollout(wl)
+    r.run()
+    out = r.results()
+    rng = np.random.default_rng(0)
+    picks = np.sort(rng.choice(wl.B, 12, replace=False))
+    f = r.ctx.formats
+    for b in picks:
+        sub = make_workload("sample", [wl.envs[wl.world_idx[b]]], [0], 1, wl.H, f)
+        sub.q = wl.q[b:b + 1].copy()
+        w = wl.world_idx[b]
+        sub.cuboids = wl.cuboids[wl.world_offsets[w]:wl.world_offsets[w + 1]]
+        sub.world_offsets = np.array([0, len(sub.cuboids)], np.int32)
+        sub.world_idx = np.zeros(1, np.int32)
+        rows = slice(b * wl.H, (b + 1) * wl.H)
+        os_w = r.packed(0)[rows]
+        _, v = orc.fk_stage(sub.q.reshape(-1, 7), wl.robot, f[0])
+        check_codes(os_w, v, 1.0, f[0], 156, what=f"out_spheres traj {b}")
+        gos_w = r.packed(1)[rows]
+        bk = orc.bk_stage(sub.q.reshape(-1, 7), gos_w, f[1], wl.robot)
+        check_close(out["grad_q"][b], bk["grad_q"], bk["scale"], f"grad_q traj {b}")
+        ws = orc.world_stage(os_w, f[0], sub.world_idx, sub.cuboids, sub.world_offsets, wl.robot, 1,
+                             wl.H, 0.025, 1.0, 1, 1, f[4])
+        ss = orc.self_stage(os_w, f[0], wl.robot, 0.01, 1.0, f[2])
+        ref = ws["cost"].reshape(-1) + ss["cost"]
+        sc = ws["cost_scale"].reshape(-1) + ss["cost_scale"]
+        check_close(out["cost_pose"][b], ref, sc, f"cost_pose traj {b}")
