@@ -49,7 +49,9 @@ def check_codes(gpu_words, v, scale, fmt, cols, skip=None, min_exact=None, what=
                       f"{[b[:5] for b in bad]}: gpu={got[bad][:5]} ref={ref[bad][:5]} "
                       f"v={v[bad][:5]}")
     exact = float(np.mean(got == ref))
-    if min_exact is not None:
+    # an exact-match rate is meaningful only when the format's step is far
+    # coarser than FP32 evaluation error (M <= 10); E8M23 codes are FP32 bits
+    if min_exact is not None and M <= 10:
         assert exact >= min_exact, f"{what}: only {exact:.5f} of codes exact"
     return exact
 
