@@ -58,19 +58,32 @@ Fmt make_fmt(vapr_format v) {
     f.M = v.man_bits;
     f.t = 1 + f.E + f.M;
     f.pf = 32 / f.t;
-    f.identity = (f.E == 8 && f.M == 23) ? 1 : 0;
     const int bias = (1 << (f.E - 1)) - 1;
     f.sh = 23 - f.M;
-    f.rnd = f.sh > 0 ? (1u << (f.sh - 1)) - 1u : 0u;
-    f.off = (uint32_t)(127 - bias) << f.M;
+    const uint32_t rnd = f.sh > 0 ? (1u << (f.sh - 1)) - 1u : 0u;
+    const uint32_t off = (uint32_t)(127 - bias) << f.M;
+    f.K = rnd - (off << f.sh);                                  // mod 2^32
     f.minnorm = (uint32_t)(128 - bias) << 23;                 // 2^(1-bias)
     f.magic_bits = (uint32_t)(127 + 24 - bias - f.M) << 23;    // 2^(24-bias-M)
     const uint32_t emax = (f.E == 8) ? 254u : (1u << f.E) - 1u;
-    f.maxcode = (f.M < 32) ? ((emax << f.M) | ((1u << f.M) - 1u)) : 0xffffffffu;
+    f.maxcode = (emax << f.M) | ((1u << f.M) - 1u);
     f.mask = (f.t >= 32) ? 0xffffffffu : ((1u << f.t) - 1u);
-    f.magmask = (f.t >= 32) ? 0x7fffffffu : ((1u << (f.t - 1)) - 1u);
+    f.signbit = (f.t >= 32) ? 0x80000000u : (1u << (f.t - 1));
+    f.keep = 0x80000000u | ((((1u << (f.E + f.M)) - 1u)) << (23 - f.M));
     uint32_t sc = (uint32_t)(254 - bias) << 23;                // 2^(127-bias)
     std::memcpy(&f.dscale, &sc, 4);
+    // hardware conversion fast paths and the |x| range where they match the
+    // reading bit for bit (verified exhaustively by tests/test_gpu_parity.py)
+    f.kind = KIND_GENERIC;
+    f.hw_limit = 0u;
+    if (f.E == 8 && f.M == 23) f.kind = KIND_IDENTITY;
+    else if (f.E == 5 && f.M == 10) { f.kind = KIND_F16; f.hw_limit = 0x477FF000u; }   // 65520
+    else if (f.E == 8 && f.M == 7) { f.kind = KIND_BF16; f.hw_limit = 0x7F7F8000u; }   // bf16max+ulp/2
+    else if (f.E == 4 && f.M == 3) { f.kind = KIND_E4M3; f.hw_limit = 0x43E80001u; }   // <= 464
+    else if (f.E == 5 && f.M == 2) { f.kind = KIND_E5M2; f.hw_limit = 0x47700000u; }   // 61440
+    else if (f.E == 2 && f.M == 1) { f.kind = KIND_E2M1; f.hw_limit = 0x7F800001u; }   // all but NaN
+    else if (f.E == 2 && f.M == 3) { f.kind = KIND_E2M3; f.hw_limit = 0x7F800001u; }
+    else if (f.E == 3 && f.M == 2) { f.kind = KIND_E3M2; f.hw_limit = 0x7F800001u; }
     return f;
 }
 
@@ -219,14 +232,30 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
         adj[i].push_back(j);
         adj[j].push_back(i);
     }
+    for (int a = 0; a < kLinks; ++a)
+        for (int b = 0; b < kLinks; ++b) R.lp_index[a][b] = -1;
+    int nlp = 0;
     int o = 0;
     for (int s = 0; s < r->n_spheres; ++s) {
         R.adj_off[s] = (uint16_t)o;
         std::vector<int>& a = adj[s];
         std::sort(a.begin(), a.end());
-        for (int v : a) R.adj[o++] = (uint8_t)v;
+        a.erase(std::unique(a.begin(), a.end()), a.end());
+        const int ls = r->sphere_link[s];
+        int L = 0;
+        for (int v : a) {
+            const int lv = r->sphere_link[v];
+            while (L <= lv) R.adj_link_off[s][L++] = (uint16_t)o;
+            if (R.lp_index[ls][lv] < 0) {
+                CHECK(nlp < 32, VAPR_ERR_UNSUPPORTED);
+                R.lp_index[ls][lv] = R.lp_index[lv][ls] = (int8_t)nlp++;
+            }
+            R.adj[o++] = (uint8_t)v;
+        }
+        while (L <= kLinks) R.adj_link_off[s][L++] = (uint16_t)o;
     }
     R.adj_off[r->n_spheres] = (uint16_t)o;
+    R.n_link_pairs = nlp;
     c->robot = R;
     c->robot_set = true;
     return VAPR_OK;

@@ -64,15 +64,19 @@ quantize_kernel(const float* __restrict__ x, uint4* __restrict__ out, GroupGeom 
             group_span(G, g, flat, n);
             const int base = int(flat - flat0);
             uint32_t w[4];
+            with_pf(f.pf, [&](auto P) {
+                constexpr int PF = decltype(P)::value;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t acc = 0;
-                for (int j = 0; j < f.pf; ++j) {
-                    const int e = k * f.pf + j;
-                    if (e < n) acc |= encode(sm[padi(base + e)], f) << (j * f.t);
+                for (int k = 0; k < 4; ++k) {
+                    float x[PF];
+#pragma unroll
+                    for (int j = 0; j < PF; ++j) {
+                        const int e = k * PF + j;
+                        x[j] = (e < n) ? sm[padi(base + e)] : 0.f;
+                    }
+                    w[k] = encode_word_t<PF>(x, f);
                 }
-                w[k] = acc;
-            }
+            });
             __stcs(out + g, make_uint4(w[0], w[1], w[2], w[3]));
         }
         __syncwarp();
@@ -101,13 +105,19 @@ dequantize_kernel(const uint4* __restrict__ in, float* __restrict__ y, GroupGeom
             const int base = int(flat - flat0);
             const uint4 v = __ldcs(in + g);
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            with_pf(f.pf, [&](auto P) {
+                constexpr int PF = decltype(P)::value;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                for (int j = 0; j < f.pf; ++j) {
-                    const int e = k * f.pf + j;
-                    if (e < n) sm[padi(base + e)] = decode(code_at(w[k], j, f), f);
+                for (int k = 0; k < 4; ++k) {
+                    float x[PF];
+                    decode_word_t<PF>(w[k], x, f);
+#pragma unroll
+                    for (int j = 0; j < PF; ++j) {
+                        const int e = k * PF + j;
+                        if (e < n) sm[padi(base + e)] = x[j];
+                    }
                 }
-            }
+            });
         }
         __syncwarp();
         for (int i = lane; i < span; i += 32) __stcs(y + flat0 + i, sm[padi(i)]);

@@ -22,52 +22,182 @@ constexpr int kJoints = 7;
 // computed once on the host (make_fmt in api.cu) so the device codec is a
 // handful of integer/FP32 ops with no table lookups.
 // ---------------------------------------------------------------------------
+enum FmtKind : int32_t {
+    KIND_GENERIC = 0,   // integer RNE path
+    KIND_IDENTITY = 1,  // E8M23: FP32 bits
+    KIND_F16 = 2,       // E5M10: cvt.rn.f16x2.f32, |x| >= 65520 / NaN -> generic
+    KIND_BF16 = 3,      // E8M7:  cvt.rn.bf16x2.f32, |x| >= bf16max + ulp/2 / NaN -> generic
+    KIND_E4M3 = 4,      // cvt.rn.satfinite.e4m3x2.f32, |x| > 464 / NaN -> generic
+    KIND_E5M2 = 5,      // cvt.rn.satfinite.e5m2x2.f32, |x| >= 61440 / NaN -> generic
+    KIND_E2M1 = 6,      // cvt.rn.satfinite.e2m1x2.f32, NaN -> generic
+    KIND_E2M3 = 7,      // cvt.rn.satfinite.e2m3x2.f32, NaN -> generic
+    KIND_E3M2 = 8       // cvt.rn.satfinite.e3m2x2.f32, NaN -> generic
+};
+
 struct Fmt {
     int32_t E, M, t, pf;
+    int32_t kind;
     int32_t sh;            // 23 - M: FP32 mantissa bits dropped
-    uint32_t rnd;          // (1 << (sh-1)) - 1: round-half-1 for RNE
-    uint32_t off;          // (127 - bias) << M: exponent re-bias in code units
+    uint32_t K;            // rnd - (off << sh) (mod 2^32): fused RNE + re-bias constant
     uint32_t minnorm;      // FP32 bits of 2^(1-bias): smallest normal of the format
     uint32_t magic_bits;   // FP32 bits of 2^(24-bias-M): its ulp is the subnormal quantum
     uint32_t maxcode;      // largest finite magnitude code (exp field 254 for E=8, c7)
     uint32_t mask;         // (1 << t) - 1
-    uint32_t magmask;      // (1 << (t-1)) - 1
+    uint32_t signbit;      // 1 << (t-1)
+    uint32_t keep;         // decode: sign | exponent+mantissa field mask in FP32 position
+    uint32_t hw_limit;     // hardware fast path valid while |x| bits < hw_limit
     float dscale;          // 2^(127 - bias): decode re-bias
-    int32_t identity;      // E8M23: raw FP32 bits
 };
 
 // FP32 -> code, round to nearest even (single rounding), saturating, NaN ->
 // +max, -0 kept (readings c2-c8).  Normal range: integer RNE on the FP32 bit
-// pattern (carry into the exponent is the correct binade change).  Format
-// subnormal range: x + 2^(24-bias-M) rounds x to the subnormal quantum in the
-// FP32 adder (RN-even), exact because no FTZ is used anywhere.
-__device__ __forceinline__ uint32_t encode(float x, const Fmt& f) {
+// pattern (a carry into the exponent is the correct binade change).  Format
+// subnormal range: |x| + 2^(24-bias-M) rounds |x| to the subnormal quantum in
+// the FP32 adder (RN-even), exact because no FTZ is used anywhere.
+__device__ __forceinline__ uint32_t encode_generic(float x, const Fmt& f) {
     const uint32_t u = __float_as_uint(x);
-    if (f.identity) return u;
-    const uint32_t s = u & 0x80000000u;
-    const uint32_t a = u ^ s;
-    const uint32_t r = a + f.rnd + ((a >> f.sh) & 1u);
-    const uint32_t cn = (r >> f.sh) - f.off;
-    const uint32_t cs = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits)))
-                        - f.magic_bits;
+    const uint32_t a = u & 0x7fffffffu;
+    const uint32_t cn = (a + f.K + ((a >> f.sh) & 1u)) >> f.sh;
+    const uint32_t cs =
+        __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits))) - f.magic_bits;
     uint32_t c = (a < f.minnorm) ? cs : cn;
-    c = min(c, f.maxcode);
-    c |= s >> (32 - f.t);
+    c = min(c, f.maxcode) | ((u >> (32 - f.t)) & f.signbit);
     return (a > 0x7f800000u) ? f.maxcode : c;
 }
 
-// code -> FP32 (exact).  The magnitude bits placed into an FP32 pattern read as
-// (1.m) 2^(e-127) (or the FP32 subnormal m 2^-149 ...); one multiply by the
-// power of two 2^(127-bias) re-biases both normals and subnormals exactly.
-__device__ __forceinline__ float decode(uint32_t c, const Fmt& f) {
-    if (f.identity) return __uint_as_float(c);
-    const uint32_t s = (c << (32 - f.t)) & 0x80000000u;
-    const float v = __fmul_rn(__uint_as_float((c & f.magmask) << f.sh), f.dscale);
-    return __uint_as_float(__float_as_uint(v) | s);
+__device__ __forceinline__ uint32_t encode(float x, const Fmt& f) {
+    return (f.kind == KIND_IDENTITY) ? __float_as_uint(x) : encode_generic(x, f);
 }
+
+// code at slot j of a word -> FP32 (exact).  The code is shifted to the top of
+// the word, an arithmetic shift moves its exponent into the FP32 exponent
+// field (the sign copies land in bits the mask clears), and one multiply by
+// the power of two 2^(127-bias) re-biases normals and subnormals alike.
+__device__ __forceinline__ float decode_slot(uint32_t w, int j, const Fmt& f) {
+    if (f.kind == KIND_IDENTITY) return __uint_as_float(w);
+    const uint32_t u = w << (32 - f.t - j * f.t);
+    const uint32_t x = uint32_t(int32_t(u) >> (8 - f.E)) & f.keep;
+    return (f.E == 8) ? __uint_as_float(x) : __fmul_rn(__uint_as_float(x), f.dscale);
+}
+
+__device__ __forceinline__ float decode(uint32_t c, const Fmt& f) { return decode_slot(c, 0, f); }
 
 __device__ __forceinline__ uint32_t code_at(uint32_t word, int slot, const Fmt& f) {
     return (f.t == 32) ? word : ((word >> (slot * f.t)) & f.mask);
+}
+
+// ---- hardware conversions (sm_100a) -------------------------------------
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_e4m3x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_e5m2x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_e2m1x2(float lo, float hi) {
+    uint16_t r;
+    asm("{ .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n mov.b16 %0, {t, 0};}"
+        : "=h"(r) : "f"(hi), "f"(lo));
+    return r & 0xffu;
+}
+__device__ __forceinline__ uint32_t cvt_e2m3x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e2m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_e3m2x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// Encode PF values x[0..PF) into one packed word (the caller sets values
+// beyond the row end to +0).  Formats with a hardware conversion use it unless
+// some value of the word needs the reading's special handling (top binade,
+// NaN), which the generic path provides; the choice is per word and bit-exact
+// either way.  PF is a compile-time constant (see with_pf).
+template <int PF>
+__device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) {
+    if (PF == 1 && f.kind == KIND_IDENTITY) return __float_as_uint(x[0]);
+    uint32_t amax = 0;
+#pragma unroll
+    for (int j = 0; j < PF; ++j) amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
+    if (amax == 0u) {               // all +-0: only the signs can be set
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < PF; ++j) w |= ((__float_as_uint(x[j]) >> (32 - f.t)) & f.signbit) << (j * f.t);
+        return w;
+    }
+    if (amax < f.hw_limit) {
+        if constexpr (PF == 2) {
+            if (f.kind == KIND_F16) return cvt_f16x2(x[0], x[1]);
+            if (f.kind == KIND_BF16) return cvt_bf16x2(x[0], x[1]);
+        } else if constexpr (PF == 4) {
+            if (f.kind == KIND_E4M3) return cvt_e4m3x2(x[0], x[1]) | (cvt_e4m3x2(x[2], x[3]) << 16);
+            if (f.kind == KIND_E5M2) return cvt_e5m2x2(x[0], x[1]) | (cvt_e5m2x2(x[2], x[3]) << 16);
+        } else if constexpr (PF == 8) {
+            if (f.kind == KIND_E2M1)
+                return cvt_e2m1x2(x[0], x[1]) | (cvt_e2m1x2(x[2], x[3]) << 8) |
+                       (cvt_e2m1x2(x[4], x[5]) << 16) | (cvt_e2m1x2(x[6], x[7]) << 24);
+        } else if constexpr (PF == 5) {
+            if (f.kind == KIND_E2M3 || f.kind == KIND_E3M2) {
+                uint32_t p0, p1, p2;
+                if (f.kind == KIND_E2M3) {
+                    p0 = cvt_e2m3x2(x[0], x[1]);
+                    p1 = cvt_e2m3x2(x[2], x[3]);
+                    p2 = cvt_e2m3x2(x[4], 0.f);
+                } else {
+                    p0 = cvt_e3m2x2(x[0], x[1]);
+                    p1 = cvt_e3m2x2(x[2], x[3]);
+                    p2 = cvt_e3m2x2(x[4], 0.f);
+                }
+                return (p0 & 0x3fu) | ((p0 >> 8) << 6) | ((p1 & 0x3fu) << 12) |
+                       ((p1 >> 8) << 18) | ((p2 & 0x3fu) << 24);
+            }
+        }
+    }
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < PF; ++j) w |= encode_generic(x[j], f) << (j * f.t);
+    return w;
+}
+
+template <int PF>
+__device__ __forceinline__ void decode_word_t(uint32_t w, float* out, const Fmt& f) {
+#pragma unroll
+    for (int j = 0; j < PF; ++j) out[j] = decode_slot(w, j, f);
+}
+
+// Run fn(std::integral_constant<int, pf>) for the runtime packing factor
+// (one uniform branch), so the per-word loops above unroll at compile time.
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
+template <class Fn>
+__device__ __forceinline__ void with_pf(int pf, Fn&& fn) {
+    switch (pf) {
+        case 1: fn(IC<1>{}); break;
+        case 2: fn(IC<2>{}); break;
+        case 3: fn(IC<3>{}); break;
+        case 4: fn(IC<4>{}); break;
+        case 5: fn(IC<5>{}); break;
+        case 6: fn(IC<6>{}); break;
+        default: fn(IC<8>{}); break;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -83,8 +213,15 @@ struct RobotDev {
     int32_t link_start[kLinks + 1];      // spheres sorted by link
     float sx[kMaxSpheres], sy[kMaxSpheres], sz[kMaxSpheres], sr[kMaxSpheres];
     // self-collision adjacency (CSR): partners of sphere s are
-    // adj[adj_off[s] .. adj_off[s+1]), each pair listed from both ends.
+    // adj[adj_off[s] .. adj_off[s+1]), each pair listed from both ends, in
+    // ascending partner order; the partners on link L are the sub-range
+    // adj[adj_link_off[s][L] .. adj_link_off[s][L+1]).
     uint16_t adj_off[kMaxSpheres + 1];
+    uint16_t adj_link_off[kMaxSpheres][kLinks + 1];
+    // link-pair broadphase: index (0..31) of the link pair (a, b) in the
+    // per-pose self mask, -1 when no listed sphere pair joins the two links
+    int8_t lp_index[kLinks][kLinks];
+    int32_t n_link_pairs;
     uint8_t adj[2 * kMaxPairs];
 };
 

@@ -366,3 +366,24 @@ def test_full_size_sampled(vb):
         ref = ws["cost"].reshape(-1) + ss["cost"]
         sc = ws["cost_scale"].reshape(-1) + ss["cost_scale"]
         check_close(out["cost_pose"][b], ref, sc, f"cost_pose traj {b}")
+
+
+@pytest.mark.parametrize("name", ["config2", "mixed_envs", "bookshelf_tall", "fp32", "ragged_43"])
+def test_cull_is_exact(vb, name):
+    """Broadphase culling skips only exactly-zero terms: outputs and every
+    packed intermediate are bit-identical with VAPR_OPT_CULL on and off."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = WORKLOADS[name]()
+    outs = []
+    for cull in (1, 0):
+        r = Rollout(wl)
+        r.ctx.set_cull(cull)
+        r.run()
+        res = r.results()
+        outs.append((res, [r.packed(i) for i in range(5)]))
+    (a, pa), (b, pb) = outs
+    for k in a:
+        np.testing.assert_array_equal(a[k].view(np.uint32), b[k].view(np.uint32), err_msg=k)
+    for x, y in zip(pa, pb):
+        if x is not None:
+            np.testing.assert_array_equal(x, y)
