@@ -248,6 +248,8 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
             while (L <= lv) R.adj_link_off[s][L++] = (uint16_t)o;
             if (R.lp_index[ls][lv] < 0) {
                 CHECK(nlp < 32, VAPR_ERR_UNSUPPORTED);
+                R.lp_a[nlp] = (int8_t)std::min(ls, lv);
+                R.lp_b[nlp] = (int8_t)std::max(ls, lv);
                 R.lp_index[ls][lv] = R.lp_index[lv][ls] = (int8_t)nlp++;
             }
             R.adj[o++] = (uint8_t)v;
@@ -256,6 +258,26 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     }
     R.adj_off[r->n_spheres] = (uint16_t)o;
     R.n_link_pairs = nlp;
+    // per-link reference sphere: the sphere minimising max_s(|o_s - o_ref| + r_s)
+    for (int l = 0; l < kLinks; ++l) {
+        R.link_ref[l] = R.link_start[l];
+        R.link_rl[l] = -1.f;
+        double best = 1e300;
+        for (int a = R.link_start[l]; a < R.link_start[l + 1]; ++a) {
+            double m = 0.0;
+            for (int b = R.link_start[l]; b < R.link_start[l + 1]; ++b) {
+                const double dx = (double)R.sx[b] - R.sx[a], dy = (double)R.sy[b] - R.sy[a],
+                             dz = (double)R.sz[b] - R.sz[a];
+                m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz) + (double)R.sr[b]);
+            }
+            if (m < best) {
+                best = m;
+                R.link_ref[l] = a;
+            }
+        }
+        // round up so the FP32 radius never under-states the double bound
+        if (best < 1e300) R.link_rl[l] = std::nextafter((float)best, 3e38f);
+    }
     c->robot = R;
     c->robot_set = true;
     return VAPR_OK;

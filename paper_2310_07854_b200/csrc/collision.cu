@@ -6,27 +6,33 @@
 // c13-c17 (box SDF, smooth hinge, summed over cuboids / listed pairs; swept =
 // linear sub-samples with the exact gradient to both endpoints).
 //
-// Tile = kTile consecutive poses (+1 halo pose on each side for the swept
-// samples).
-//  1. decode the packed rows into an FP32 shared tile (row stride 3S|1, odd);
-//  2. broadphase, per (pose, link): a bounding sphere of the link's spheres;
-//     per (pose, link, cuboid) and (segment, link, cuboid) a cull bit from the
-//     1-Lipschitz box SDF at the bounding-sphere centre; per pose a mask of
-//     the link pairs whose bounding spheres come within eta_self;
-//  3. narrowphase, one lane per (sphere, pose) item, warps sphere-major (the
-//     sphere's radius, link and partner list are warp-uniform, read from the
-//     __grid_constant__ robot as broadcasts); each item gathers its complete
-//     gradient (no scatter), encodes its 3 codes and ORs the non-zero ones into
-//     shared packed rows (OR is order-independent: deterministic);
-//  4. per-pose costs reduced in a fixed order; packed tiles streamed out.
+// One CTA per tile of kTile consecutive poses (+1 halo pose on each side for
+// the swept samples):
+//  1. decode the packed rows into an FP32 shared tile (row stride 3S|1, odd),
+//     tracking the largest decoded coordinate (quantisation-error bound);
+//  2. broadphase.  Each link's spheres lie in a ball around its reference
+//     sphere whose radius is rigid (computed once on the host) plus the
+//     quantisation-error margin.  Per (segment, link, cuboid) -- or per
+//     (pose, link, cuboid) for the discrete cost -- a cull bit from a lower
+//     bound of the 1-Lipschitz box SDF at the ball centre; per (pose, link
+//     pair) a cull bit from the ball-ball distance;
+//  3. the live (pose, link) world tasks and live (pose, link pair) self tasks
+//     are compacted into shared task lists and processed by all threads;
+//     world tasks gather the complete gradient of each sphere of the link (no
+//     scatter) and OR its codes into shared packed rows (OR is
+//     order-independent); self tasks only collect the active sphere pairs of
+//     their pose;
+//  4. one thread per pose accumulates its self gradients and costs in pair
+//     order (deterministic); per-pose costs are reduced in a fixed order and
+//     the packed tiles streamed out with coalesced stores.
 //
-// Culling is exact: a (link, cuboid) or (link, link) combination is skipped
-// only when its bound clears the activation distance by kSlack = 1e-4 m,
-// orders of magnitude above the FP32 evaluation error of the distances for
-// workspace-scale coordinates (|x| < 100 m), so every skipped term would have
-// evaluated to phi <= 0, i.e. exactly 0.  The surviving terms are accumulated
-// in the same order as without culling, so VAPR_OPT_CULL on and off give
-// bit-identical results (checked by tests/test_gpu_parity.py).
+// Culling is exact: a term is skipped only when its bound clears the
+// activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
+// evaluation error of the distances for workspace-scale coordinates
+// (|x| < 100 m), so every skipped term would evaluate to phi <= 0, i.e. to
+// exactly 0; surviving terms are accumulated in the same order with and
+// without culling, so VAPR_OPT_CULL on and off give bit-identical results
+// (tests/test_gpu_parity.py::test_cull_is_exact).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -38,6 +44,7 @@ constexpr int kTile = 64;           // poses per CTA
 constexpr int kRows = kTile + 2;    // with the two halo poses
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
+constexpr int kPairCap = 16;        // active self pairs listed per pose (else brute force)
 constexpr float kSlack = 1e-4f;
 
 struct Acc {
@@ -53,15 +60,18 @@ __device__ __forceinline__ Cub load_cub(const float4* __restrict__ cub, int k) {
                __ldg(cub + 4 * k + 3)};
 }
 
-// Box signed distance at c (for the broadphase bound).
-__device__ __forceinline__ float box_sdf(const Cub& b, float cx, float cy, float cz) {
+// Lower bound of the box signed distance at c (the exact value outside, the
+// face distance max_k(|p_k| - h_k) inside).
+__device__ __forceinline__ float box_sdf_lb(const Cub& b, float cx, float cy, float cz) {
     const float dx = cx - b.q2.y, dy = cy - b.q2.z, dz = cz - b.q2.w;
     const float px = fmaf(b.q0.x, dx, fmaf(b.q0.y, dy, b.q0.z * dz));
     const float py = fmaf(b.q0.w, dx, fmaf(b.q1.x, dy, b.q1.y * dz));
     const float pz = fmaf(b.q1.z, dx, fmaf(b.q1.w, dy, b.q2.x * dz));
     const float ux = fabsf(px) - b.q3.x, uy = fabsf(py) - b.q3.y, uz = fabsf(pz) - b.q3.z;
+    const float umax = fmaxf(ux, fmaxf(uy, uz));
+    if (umax <= 0.f) return umax;
     const float ox = fmaxf(ux, 0.f), oy = fmaxf(uy, 0.f), oz = fmaxf(uz, 0.f);
-    return sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz))) + fminf(fmaxf(ux, fmaxf(uy, uz)), 0.f);
+    return sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
 }
 
 // One sphere-vs-cuboid term: adds cw * w * h(phi) to the cost and
@@ -115,56 +125,125 @@ __device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, flo
     acc.gz = fmaf(sc, gzw, acc.gz);
 }
 
-__device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt& f) {
+__device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt& f,
+                                        uint32_t rc) {
     if (__float_as_uint(v) == 0u) return;          // +0 -> code 0 (the sparse common case)
     const uint32_t c = encode(v, f);
-    const int w = e / f.pf;
+    const int w = int((e * rc) >> 16);             // e / pf (e < 4096)
     atomicOr(row + w, c << ((e - w * f.pf) * f.t));
 }
+
+// Self pair (i, j), i < j: false when inactive; else the gradient
+// contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
+__device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const RobotDev& R,
+                                          float eta, float inv_eta, float hoe, float w, float& vx,
+                                          float& vy, float& vz, float& cost) {
+    const float dx = crow[3 * i] - crow[3 * j], dy = crow[3 * i + 1] - crow[3 * j + 1],
+                dz = crow[3 * i + 2] - crow[3 * j + 2];
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float Rs = R.sr[i] + R.sr[j] + eta;
+    // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so d2 >= fl(Rs^2)
+    // implies fl(sqrt(d2)) >= Rs, i.e. phi <= 0: exact early out.
+    if (d2 >= Rs * Rs) return false;
+    const float d = sqrtf(d2);
+    const float phi = Rs - d;
+    if (phi <= 0.f) return false;
+    float hh, dh;
+    if (phi <= eta) {
+        hh = phi * phi * hoe;
+        dh = phi * inv_eta;
+    } else {
+        hh = phi - 0.5f * eta;
+        dh = 1.f;
+    }
+    const float k = w * dh;
+    if (d > 0.f) {
+        const float inv = 1.f / d;
+        vx = k * (dx * inv);
+        vy = k * (dy * inv);
+        vz = k * (dz * inv);
+    } else {                                       // coincident centres: direction (1, 0, 0)
+        vx = k;
+        vy = vz = 0.f;
+    }
+    cost = w * hh;
+    return true;
+}
+
+struct Smem {
+    float* ctile;      // [kRows * cs], row 0 = pose p0-1
+    float4* ball;      // [kRows * kLinks] link ball (centre, radius)
+    uint32_t* wmask;   // [kRows * kLinks] bits 0-15 pose (discrete), 16-31 segment row->row+1
+    uint32_t* smask;   // [kRows] live link pairs
+    int2* krange;      // [kRows] cuboid range of the row's world
+    int* hrow;         // [kRows] step index h, -1 when the row is absent
+    float* wcost;      // [kTile * kLinks]
+    int* pcount;       // [kTile] active self pairs per pose
+    int* counters;     // [4]: world tasks, self tasks, max-coordinate bits, spare
+    uint16_t* wtask;   // [kTile * kLinks]
+    uint16_t* stask;   // [kTile * 32]
+    uint16_t* pkey;    // [kTile * kPairCap] active pair keys i * 64 + j
+    uint32_t* wcp;     // [kTile * (Wcp+1)]
+    uint32_t* wov;     // [kTile * (Wov+1)]
+};
 
 __global__ void __launch_bounds__(kThreads, 2)
 collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const Fmt fos,
                  const Fmt fcp, const Fmt fov, const CollisionArgs a, int Wos, int Wcp,
                  int Wov) {
     extern __shared__ float4 smem4[];
-    const int S = R.n_spheres;
     const int cols = R.cols;
     const int cs = cols | 1;                       // odd fp32 row stride
     const long long P = (long long)a.B * a.H;
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
-
-    // ---- shared layout (float4 first for alignment)
-    float4* lb = smem4;                                          // [kRows * 9]
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(lb + kRows * kLinks);   // [kRows * 9]
-    uint32_t* smask = wmask + kRows * kLinks;                   // [kRows]
-    int2* krange = reinterpret_cast<int2*>(smask + kRows);       // [kRows]
-    float* ctile = reinterpret_cast<float*>(krange + kRows);     // [kRows * cs], row 0 = p0-1
-    float* cpart = ctile + kRows * cs;                           // [S * kTile]
-    uint32_t* wcp = reinterpret_cast<uint32_t*>(cpart + S * kTile);   // [kTile * (Wcp+1)]
-    uint32_t* wov = wcp + (a.do_world ? kTile * (Wcp + 1) : 0);       // [kTile * (Wov+1)]
     const int WcpS = Wcp + 1, WovS = Wov + 1;
+
+    Smem sm;
+    sm.ball = smem4;
+    sm.wmask = reinterpret_cast<uint32_t*>(sm.ball + kRows * kLinks);
+    sm.smask = sm.wmask + kRows * kLinks;
+    sm.krange = reinterpret_cast<int2*>(sm.smask + kRows + (kRows & 1));
+    sm.hrow = reinterpret_cast<int*>(sm.krange + kRows);
+    sm.wcost = reinterpret_cast<float*>(sm.hrow + kRows);
+    sm.pcount = reinterpret_cast<int*>(sm.wcost + kTile * kLinks);
+    sm.counters = sm.pcount + kTile;
+    sm.wtask = reinterpret_cast<uint16_t*>(sm.counters + 4);
+    sm.stask = sm.wtask + kTile * kLinks;
+    sm.pkey = sm.stask + kTile * 32;
+    {
+        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.pkey + kTile * kPairCap);
+        sm.wcp = reinterpret_cast<uint32_t*>((e + 15) & ~uintptr_t(15));
+    }
+    sm.wov = sm.wcp + (a.do_world ? kTile * WcpS : 0);
+    sm.ctile = reinterpret_cast<float*>(sm.wov + (a.do_self ? kTile * WovS : 0));
 
     // ---- 1. decode rows p0-1 .. p0+np into the FP32 tile; zero the outputs
     const long long r_lo = max(p0 - 1, 0LL);
     const long long r_hi = min(p0 + np + 1, P);           // exclusive
     const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
+    if (tid < 4) sm.counters[tid] = 0;
+    __syncthreads();
     {
         const int nrows = int(r_hi - r_lo);
         const int nw = nrows * Wos;
         const uint32_t* src = a.os + r_lo * Wos;
         const int dr = kThreads / Wos, dw = kThreads % Wos;
         int r = tid / Wos, w = tid - (tid / Wos) * Wos;
+        uint32_t amax = 0;
         with_pf(fos.pf, [&](auto Pc) {
             constexpr int PF = decltype(Pc)::value;
             for (int i = tid; i < nw; i += kThreads) {
                 float x[PF];
                 decode_word_t<PF>(__ldg(src + i), x, fos);
-                float* dst = ctile + (row_off + r) * cs + w * PF;
+                float* dst = sm.ctile + (row_off + r) * cs + w * PF;
 #pragma unroll
                 for (int j = 0; j < PF; ++j)
-                    if (w * PF + j < cols) dst[j] = x[j];
+                    if (w * PF + j < cols) {
+                        dst[j] = x[j];
+                        amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
+                    }
                 r += dr;
                 w += dw;
                 if (w >= Wos) {
@@ -173,247 +252,311 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                 }
             }
         });
+        amax = __reduce_max_sync(0xffffffffu, amax);
+        if ((tid & 31) == 0) atomicMax(reinterpret_cast<unsigned*>(sm.counters + 2), amax);
     }
     if (a.do_world)
-        for (int i = tid; i < kTile * WcpS; i += kThreads) wcp[i] = 0u;
+        for (int i = tid; i < kTile * WcpS; i += kThreads) sm.wcp[i] = 0u;
     if (a.do_self)
-        for (int i = tid; i < kTile * WovS; i += kThreads) wov[i] = 0u;
-    // world cuboid range of every tile row
+        for (int i = tid; i < kTile * WovS; i += kThreads) sm.wov[i] = 0u;
+    for (int i = tid; i < kTile * kLinks; i += kThreads) sm.wcost[i] = 0.f;
+    if (tid < kTile) sm.pcount[tid] = 0;
+    // world cuboid range and step index h of every tile row (the only 64-bit
+    // divisions of the kernel: once per row)
     for (int row = tid; row < kRows; row += kThreads) {
         const long long pg = p0 - 1 + row;
         int2 kr = make_int2(0, 0);
-        if (a.do_world && pg >= 0 && pg < P) {
-            const int wi = __ldg(a.world_idx + pg / a.H);
-            if (wi >= 0 && wi < Wd.n_worlds) kr = make_int2(__ldg(Wd.off + wi), __ldg(Wd.off + wi + 1));
+        int hh = -1;
+        if (pg >= 0 && pg < P) {
+            const long long b = pg / a.H;
+            hh = int(pg - b * a.H);
+            if (a.do_world) {
+                const int wi = __ldg(a.world_idx + b);
+                if (wi >= 0 && wi < Wd.n_worlds)
+                    kr = make_int2(__ldg(Wd.off + wi), __ldg(Wd.off + wi + 1));
+            }
         }
-        krange[row] = kr;
+        sm.krange[row] = kr;
+        sm.hrow[row] = hh;
     }
     __syncthreads();
 
-    // ---- 2a. link bounding spheres (rows present in the tile)
+    // Quantisation margin: a decoded coordinate y of an FK value x satisfies
+    // |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) (half an ulp; the subnormal
+    // quantum covers the bottom of the range) unless the code saturated; two
+    // centres per distance and sqrt(3) per vector give the ball margin.  With
+    // a saturated coordinate in the tile (|y| == max_finite) there is no bound
+    // and culling is switched off for the tile.
+    const float amaxf = __uint_as_float((uint32_t)sm.counters[2]);
+    bool can_cull = a.cull != 0;
+    float margin = 0.f;
+    if (fos.kind != KIND_IDENTITY) {
+        if (amaxf >= decode(fos.maxcode, fos)) can_cull = false;
+        const float rel = ldexpf(1.f, -(fos.M + 1));
+        const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
+        margin = 2.f * 1.7320509f * (rel * amaxf * 1.01f + sub);
+    }
+
+    // ---- 2a. link balls (rows present in the tile)
     for (int task = tid; task < kRows * kLinks; task += kThreads) {
         const int row = task / kLinks, l = task - row * kLinks;
-        const long long pg = p0 - 1 + row;
-        if (pg < 0 || pg >= P) continue;
-        const float* c = ctile + row * cs;
-        const int s0 = R.link_start[l], s1 = R.link_start[l + 1];
-        float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
-        for (int s = s0; s < s1; ++s)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                lo[k] = fminf(lo[k], c[3 * s + k]);
-                hi[k] = fmaxf(hi[k], c[3 * s + k]);
-            }
-        const float mx = 0.5f * (lo[0] + hi[0]), my = 0.5f * (lo[1] + hi[1]),
-                    mz = 0.5f * (lo[2] + hi[2]);
-        float rad = -1.f;                  // empty link: never active
-        for (int s = s0; s < s1; ++s) {
-            const float dx = c[3 * s] - mx, dy = c[3 * s + 1] - my, dz = c[3 * s + 2] - mz;
-            rad = fmaxf(rad, sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) + R.sr[s]);
-        }
-        lb[row * kLinks + l] = make_float4(mx, my, mz, rad);
+        if (sm.hrow[row] < 0) continue;
+        const float* c = sm.ctile + row * cs + 3 * R.link_ref[l];
+        sm.ball[task] = make_float4(c[0], c[1], c[2], R.link_rl[l] + margin);
     }
     __syncthreads();
 
-    // ---- 2b. world cull masks (bits 0-15: pose, 16-31: segment row->row+1)
-    //          and self link-pair masks
+    // ---- 2b. world cull masks per (row, link); self link-pair masks per row
     const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
     for (int task = tid; task < kRows * kLinks + kRows; task += kThreads) {
         if (task < kRows * kLinks) {
             const int row = task / kLinks, l = task - row * kLinks;
-            const long long pg = p0 - 1 + row;
             uint32_t m = 0;
-            const int2 kr = krange[row];
-            if (a.do_world && pg >= 0 && pg < P && kr.y > kr.x) {
-                const float4 b0 = lb[row * kLinks + l];
-                const bool seg = nsub > 0 && row + 1 < kRows && pg + 1 < P &&
-                                 (pg + 1) % a.H != 0;
-                float4 bs = b0;
-                if (seg) {
-                    const float4 b1 = lb[(row + 1) * kLinks + l];
-                    const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
-                    const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    bs = make_float4(b0.x + 0.5f * dx, b0.y + 0.5f * dy, b0.z + 0.5f * dz,
-                                     fmaxf(b0.w, b1.w) + half);
-                }
-                if (b0.w >= 0.f) {
-                    for (int k = kr.x; k < kr.y; ++k) {
-                        const Cub cb = load_cub(Wd.cub, k);
-                        const int bit = k - kr.x;
-                        if (!a.cull || box_sdf(cb, b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack)
-                            m |= 1u << bit;
-                        if (seg && (!a.cull ||
-                                    box_sdf(cb, bs.x, bs.y, bs.z) - bs.w - a.eta_w <= kSlack))
-                            m |= 1u << (16 + bit);
+            const int2 kr = sm.krange[row];
+            const int h = sm.hrow[row];
+            if (a.do_world && h >= 0 && kr.y > kr.x && R.link_rl[l] >= 0.f) {
+                const float4 b0 = sm.ball[task];
+                if (nsub > 0) {
+                    // segment row -> row+1 of the same trajectory: one ball
+                    // around both endpoint balls bounds every sample
+                    if (h + 1 < a.H && row + 1 < kRows && sm.hrow[row + 1] >= 0) {
+                        const float4 b1 = sm.ball[task + kLinks];
+                        const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
+                        const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                        const float mx = b0.x + 0.5f * dx, my = b0.y + 0.5f * dy,
+                                    mz = b0.z + 0.5f * dz, rs = fmaxf(b0.w, b1.w) + half;
+                        for (int k = kr.x; k < kr.y; ++k)
+                            if (!can_cull ||
+                                box_sdf_lb(load_cub(Wd.cub, k), mx, my, mz) - rs - a.eta_w <= kSlack)
+                                m |= 1u << (16 + k - kr.x);
                     }
+                } else {
+                    for (int k = kr.x; k < kr.y; ++k)
+                        if (!can_cull ||
+                            box_sdf_lb(load_cub(Wd.cub, k), b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack)
+                            m |= 1u << (k - kr.x);
                 }
             }
-            wmask[task] = m;
+            sm.wmask[task] = m;
         } else {
             const int row = task - kRows * kLinks;
-            const long long pg = p0 - 1 + row;
             uint32_t m = 0;
-            if (a.do_self && pg >= 0 && pg < P) {
-                for (int la = 0; la < kLinks; ++la)
-                    for (int lbk = la; lbk < kLinks; ++lbk) {
-                        const int idx = R.lp_index[la][lbk];
-                        if (idx < 0) continue;
-                        const float4 A4 = lb[row * kLinks + la], B4 = lb[row * kLinks + lbk];
-                        const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
-                        const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                        if (!a.cull || d - A4.w - B4.w - a.eta_s <= kSlack) m |= 1u << idx;
-                    }
+            if (a.do_self && sm.hrow[row] >= 0 && row >= 1 && row <= np) {
+                for (int lp = 0; lp < R.n_link_pairs; ++lp) {
+                    const float4 A4 = sm.ball[row * kLinks + R.lp_a[lp]];
+                    const float4 B4 = sm.ball[row * kLinks + R.lp_b[lp]];
+                    const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
+                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    if (!can_cull || d - A4.w - B4.w - a.eta_s <= kSlack) m |= 1u << lp;
+                }
             }
-            smask[row] = m;
+            sm.smask[row] = m;
         }
     }
     __syncthreads();
 
-    // ---- 3. narrowphase items (sphere s, pose p), sphere-major per warp
-    const int lane = tid & 31, warp = tid >> 5;
+    // ---- 2c. task lists: live (pose, link) world tasks, live (pose, link pair) self tasks
+    if (a.do_world)
+        for (int task = tid; task < kTile * kLinks; task += kThreads) {
+            const int p = task / kLinks, l = task - p * kLinks;
+            if (p >= np) continue;
+            const int row = p + 1, h = sm.hrow[row];
+            uint32_t m;
+            if (nsub > 0)
+                m = (sm.wmask[row * kLinks + l] >> 16) |
+                    (h > 0 ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u);
+            else
+                m = sm.wmask[row * kLinks + l] & 0xffffu;
+            if (m) sm.wtask[atomicAdd(sm.counters + 0, 1)] = (uint16_t)task;
+        }
+    if (a.do_self)
+        for (int task = tid; task < kTile * 32; task += kThreads) {
+            const int p = task >> 5, lp = task & 31;
+            if (p >= np || lp >= R.n_link_pairs) continue;
+            if ((sm.smask[p + 1] >> lp) & 1u) sm.stask[atomicAdd(sm.counters + 1, 1)] = (uint16_t)task;
+        }
+    __syncthreads();
+
+    // ---- 3. world tasks (all spheres of one link of one pose) and self tasks
+    //         (active sphere pairs of one link pair of one pose)
+    const uint32_t rc_cp = 65536u / fcp.pf + 1u, rc_ov = 65536u / fov.pf + 1u;
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
-    constexpr int halves = kTile / 32;
-    const int n_tasks = S * halves;
     const float inv_n1 = 1.f / float(nsub + 1);
-    for (int task = warp; task < n_tasks; task += kWarps) {
-        const int s = task / halves;
-        const int p = (task - s * halves) * 32 + lane;
-        if (p >= np) continue;
-        const int row = p + 1;
-        const long long pg = p0 + p;
-        const int h = int(pg % a.H);
-        const float* crow = ctile + row * cs;
-        const float cx = crow[3 * s], cy = crow[3 * s + 1], cz = crow[3 * s + 2];
-        const float r = R.sr[s];
-        int ls = 0;
-#pragma unroll
-        for (int l = 1; l < kLinks; ++l) ls += (s >= R.link_start[l]) ? 1 : 0;
-        float cost = 0.f;
-        if (a.do_world) {
-            Acc acc{0.f, 0.f, 0.f, 0.f};
-            const int k0 = krange[row].x;
-            const float A = r + a.eta_w;
-            uint32_t own = wmask[row * kLinks + ls] & 0xffffu;
-            while (own) {
-                const int bit = __ffs(own) - 1;
-                own &= own - 1;
-                world_term(load_cub(Wd.cub, k0 + bit), cx, cy, cz, A, a.eta_w, inv_eta_w, hoe_w,
-                           a.w_w, 1.f, 1.f, acc);
-            }
+    const int n_wtask = sm.counters[0], n_stask = sm.counters[1];
+    for (int t = tid; t < n_wtask + n_stask; t += kThreads) {
+        if (t < n_wtask) {
+            const int task = sm.wtask[t];
+            const int p = task / kLinks, l = task - p * kLinks;
+            const int row = p + 1, h = sm.hrow[row];
+            const int k0 = sm.krange[row].x;
+            uint32_t m_own, m_fwd = 0, m_bwd = 0;
             if (nsub > 0) {
-                if (h < a.H - 1) {          // samples of segment (h, h+1): cost + (1-tau) grad
-                    const uint32_t segm = wmask[row * kLinks + ls] >> 16;
-                    if (segm) {
-                        const float* nrow = crow + cs;
-                        const float nx = nrow[3 * s], ny = nrow[3 * s + 1], nz = nrow[3 * s + 2];
-                        for (int j = 1; j <= nsub; ++j) {
-                            const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                            const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
-                                        sz = fmaf(tau, nz, omt * cz);
-                            uint32_t m = segm;
-                            while (m) {
-                                const int bit = __ffs(m) - 1;
-                                m &= m - 1;
-                                world_term(load_cub(Wd.cub, k0 + bit), sx, sy, sz, A, a.eta_w,
-                                           inv_eta_w, hoe_w, a.w_w, 1.f, omt, acc);
-                            }
-                        }
+                m_fwd = (h < a.H - 1) ? (sm.wmask[row * kLinks + l] >> 16) : 0u;
+                m_bwd = (h > 0) ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u;
+                m_own = m_fwd | m_bwd;     // a segment ball contains both endpoint balls
+            } else {
+                m_own = sm.wmask[row * kLinks + l] & 0xffffu;
+            }
+            const float* crow = sm.ctile + row * cs;
+            uint32_t* orow = sm.wcp + p * WcpS;
+            float lcost = 0.f;
+            for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
+                const float cx = crow[3 * s], cy = crow[3 * s + 1], cz = crow[3 * s + 2];
+                const float A = R.sr[s] + a.eta_w;
+                Acc acc{0.f, 0.f, 0.f, 0.f};
+                for (uint32_t m = m_own; m; m &= m - 1)
+                    world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), cx, cy, cz, A, a.eta_w,
+                               inv_eta_w, hoe_w, a.w_w, 1.f, 1.f, acc);
+                if (m_fwd) {                // samples of segment (h, h+1): cost + (1-tau) grad
+                    const float* nrow = crow + cs;
+                    const float nx = nrow[3 * s], ny = nrow[3 * s + 1], nz = nrow[3 * s + 2];
+                    for (int j = 1; j <= nsub; ++j) {
+                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                        const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
+                                    sz = fmaf(tau, nz, omt * cz);
+                        for (uint32_t m = m_fwd; m; m &= m - 1)
+                            world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A,
+                                       a.eta_w, inv_eta_w, hoe_w, a.w_w, 1.f, omt, acc);
                     }
                 }
-                if (h > 0) {                // samples of segment (h-1, h): tau grad only
-                    const uint32_t segm = wmask[(row - 1) * kLinks + ls] >> 16;
-                    if (segm) {
-                        const float* prow = crow - cs;
-                        const float qx = prow[3 * s], qy = prow[3 * s + 1], qz = prow[3 * s + 2];
-                        for (int j = 1; j <= nsub; ++j) {
-                            const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                            const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
-                                        sz = fmaf(tau, cz, omt * qz);
-                            uint32_t m = segm;
-                            while (m) {
-                                const int bit = __ffs(m) - 1;
-                                m &= m - 1;
-                                world_term(load_cub(Wd.cub, k0 + bit), sx, sy, sz, A, a.eta_w,
-                                           inv_eta_w, hoe_w, a.w_w, 0.f, tau, acc);
-                            }
-                        }
+                if (m_bwd) {                // samples of segment (h-1, h): tau grad only
+                    const float* prow = crow - cs;
+                    const float qx = prow[3 * s], qy = prow[3 * s + 1], qz = prow[3 * s + 2];
+                    for (int j = 1; j <= nsub; ++j) {
+                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                        const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
+                                    sz = fmaf(tau, cz, omt * qz);
+                        for (uint32_t m = m_bwd; m; m &= m - 1)
+                            world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A,
+                                       a.eta_w, inv_eta_w, hoe_w, a.w_w, 0.f, tau, acc);
+                    }
+                }
+                lcost += acc.cost;
+                or_code(orow, 3 * s + 0, acc.gx + 0.f, fcp, rc_cp);
+                or_code(orow, 3 * s + 1, acc.gy + 0.f, fcp, rc_cp);
+                or_code(orow, 3 * s + 2, acc.gz + 0.f, fcp, rc_cp);
+            }
+            sm.wcost[task] = lcost;
+        } else {
+            const int task = sm.stask[t - n_wtask];
+            const int p = task >> 5, lp = task & 31;
+            const int row = p + 1;
+            const float* crow = sm.ctile + row * cs;
+            const int la = R.lp_a[lp], lb = R.lp_b[lp];
+            const float4 Bb = sm.ball[row * kLinks + lb];
+            for (int i = R.link_start[la]; i < R.link_start[la + 1]; ++i) {
+                // sphere i against the ball of link lb
+                const float dx = crow[3 * i] - Bb.x, dy = crow[3 * i + 1] - Bb.y,
+                            dz = crow[3 * i + 2] - Bb.z;
+                if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - R.sr[i] - Bb.w -
+                                        a.eta_s > kSlack)
+                    continue;
+                for (int jj = R.adj_link_off[i][lb]; jj < R.adj_link_off[i][lb + 1]; ++jj) {
+                    const int j = R.adj[jj];
+                    if (la == lb && j <= i) continue;          // same link: each pair once
+                    const int lo = min(i, j), hi = max(i, j);
+                    float vx, vy, vz, c;
+                    if (self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
+                        const int slot = atomicAdd(sm.pcount + p, 1);
+                        if (slot < kPairCap) sm.pkey[p * kPairCap + slot] = (uint16_t)(lo * 64 + hi);
                     }
                 }
             }
-            cost += acc.cost;
-            uint32_t* orow = wcp + p * WcpS;
-            or_code(orow, 3 * s + 0, acc.gx + 0.f, fcp);
-            or_code(orow, 3 * s + 1, acc.gy + 0.f, fcp);
-            or_code(orow, 3 * s + 2, acc.gz + 0.f, fcp);
         }
-        if (a.do_self) {
-            float gx = 0.f, gy = 0.f, gz = 0.f, sc = 0.f;
-            const uint32_t lm = smask[row];
-            for (int l2 = 0; l2 < kLinks; ++l2) {
-                const int idx = R.lp_index[ls][l2];
-                if (idx < 0 || !((lm >> idx) & 1u)) continue;
-                const int j0 = R.adj_link_off[s][l2], j1 = R.adj_link_off[s][l2 + 1];
-                for (int jj = j0; jj < j1; ++jj) {
-                    const int o = R.adj[jj];
-                    const float dx = cx - crow[3 * o], dy = cy - crow[3 * o + 1],
-                                dz = cz - crow[3 * o + 2];
-                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const float Rs = r + R.sr[o] + a.eta_s;
-                    // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so
-                    // d2 >= fl(Rs^2) implies fl(sqrt(d2)) >= Rs, i.e. phi <= 0: exact.
-                    if (d2 >= Rs * Rs) continue;
-                    const float d = sqrtf(d2);
-                    const float phi = Rs - d;
-                    if (phi <= 0.f) continue;
-                    float hh, dh;
-                    if (phi <= a.eta_s) {
-                        hh = phi * phi * hoe_s;
-                        dh = phi * inv_eta_s;
-                    } else {
-                        hh = phi - 0.5f * a.eta_s;
-                        dh = 1.f;
-                    }
-                    float ux, uy, uz;
-                    if (d > 0.f) {
-                        const float inv = 1.f / d;
-                        ux = dx * inv;
-                        uy = dy * inv;
-                        uz = dz * inv;
-                    } else {                 // coincident centres: (1,0,0) from the lower index
-                        ux = (s < o) ? 1.f : -1.f;
-                        uy = uz = 0.f;
-                    }
-                    const float k = -a.w_s * dh;
-                    gx = fmaf(k, ux, gx);
-                    gy = fmaf(k, uy, gy);
-                    gz = fmaf(k, uz, gz);
-                    if (s < o) sc = fmaf(a.w_s, hh, sc);     // each pair's cost counted once
-                }
-            }
-            cost += sc;
-            uint32_t* orow = wov + p * WovS;
-            or_code(orow, 3 * s + 0, gx + 0.f, fov);
-            or_code(orow, 3 * s + 1, gy + 0.f, fov);
-            or_code(orow, 3 * s + 2, gz + 0.f, fov);
-        }
-        cpart[s * kTile + p] = cost;
     }
     __syncthreads();
 
-    // ---- 4. per-pose cost (fixed order) and coalesced packed stores
+    // ---- 4. per pose: self accumulation in pair order, costs.
+    // The active pairs involving a sphere s, in (i, j) key order, are exactly
+    // its partners in ascending order; both the sorted-list path and the
+    // brute-force fallback (more than kPairCap active pairs) accumulate in that
+    // order with the same arithmetic, so they give identical results.
     if (tid < np) {
-        float c = 0.f;
-        for (int s = 0; s < S; ++s) c += cpart[s * kTile + tid];
-        a.cost[p0 + tid] = c;
+        const int p = tid, row = p + 1;
+        const float* crow = sm.ctile + row * cs;
+        float cost = 0.f;
+        for (int l = 0; l < kLinks; ++l) cost += sm.wcost[p * kLinks + l];
+        if (a.do_self) {
+            const int n = sm.pcount[p];
+            uint32_t* orow = sm.wov + p * WovS;
+            float scost = 0.f;
+            if (n <= kPairCap) {
+                uint16_t key[kPairCap];
+                for (int k = 0; k < n; ++k) key[k] = sm.pkey[p * kPairCap + k];
+                for (int k = 1; k < n; ++k) {          // insertion sort by (i, j)
+                    const uint16_t v = key[k];
+                    int m = k - 1;
+                    while (m >= 0 && key[m] > v) {
+                        key[m + 1] = key[m];
+                        --m;
+                    }
+                    key[m + 1] = v;
+                }
+                unsigned long long touched = 0ull;
+                for (int k = 0; k < n; ++k) {
+                    const int i = key[k] >> 6, j = key[k] & 63;
+                    float vx, vy, vz, c;
+                    self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                    scost += c;
+                    touched |= (1ull << i) | (1ull << j);
+                }
+                while (touched) {
+                    const int s = __ffsll((long long)touched) - 1;
+                    touched &= touched - 1;
+                    float gx = 0.f, gy = 0.f, gz = 0.f;
+                    for (int k = 0; k < n; ++k) {
+                        const int i = key[k] >> 6, j = key[k] & 63;
+                        if (i != s && j != s) continue;
+                        float vx, vy, vz, c;
+                        self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                        const float sg = (i == s) ? -1.f : 1.f;
+                        gx = fmaf(sg, vx, gx);
+                        gy = fmaf(sg, vy, gy);
+                        gz = fmaf(sg, vz, gz);
+                    }
+                    or_code(orow, 3 * s + 0, gx + 0.f, fov, rc_ov);
+                    or_code(orow, 3 * s + 1, gy + 0.f, fov, rc_ov);
+                    or_code(orow, 3 * s + 2, gz + 0.f, fov, rc_ov);
+                }
+            } else {
+                for (int i = 0; i < R.n_spheres; ++i) {
+                    float gx = 0.f, gy = 0.f, gz = 0.f;
+                    bool any = false;
+                    for (int jj = R.adj_off[i]; jj < R.adj_off[i + 1]; ++jj) {
+                        const int o = R.adj[jj];
+                        const int lo = min(i, o), hi = max(i, o);
+                        float vx, vy, vz, c;
+                        if (!self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
+                            continue;
+                        any = true;
+                        if (o > i) scost += c;             // each pair once, in (i, j) order
+                        const float sg = (lo == i) ? -1.f : 1.f;
+                        gx = fmaf(sg, vx, gx);
+                        gy = fmaf(sg, vy, gy);
+                        gz = fmaf(sg, vz, gz);
+                    }
+                    if (any) {
+                        or_code(orow, 3 * i + 0, gx + 0.f, fov, rc_ov);
+                        or_code(orow, 3 * i + 1, gy + 0.f, fov, rc_ov);
+                        or_code(orow, 3 * i + 2, gz + 0.f, fov, rc_ov);
+                    }
+                }
+            }
+            cost += scost;
+        }
+        a.cost[p0 + p] = cost;
     }
+    __syncthreads();
+
+    // ---- 5. coalesced packed stores
     if (a.do_world) {
         const int n = np * Wcp;
         uint32_t* dst = a.cp + p0 * Wcp;
         const int dr = kThreads / Wcp, dw = kThreads % Wcp;
         int r = tid / Wcp, w = tid - (tid / Wcp) * Wcp;
         for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, wcp[r * WcpS + w]);
+            __stcs(dst + i, sm.wcp[r * WcpS + w]);
             r += dr;
             w += dw;
             if (w >= Wcp) {
@@ -428,7 +571,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const int dr = kThreads / Wov, dw = kThreads % Wov;
         int r = tid / Wov, w = tid - (tid / Wov) * Wov;
         for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, wov[r * WovS + w]);
+            __stcs(dst + i, sm.wov[r * WovS + w]);
             r += dr;
             w += dw;
             if (w >= Wov) {
@@ -465,6 +608,20 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
     best_seed[p] = arg;
 }
 
+size_t collision_smem(const RobotDev& R, bool do_world, bool do_self, int Wcp, int Wov) {
+    size_t b = sizeof(float4) * kRows * kLinks;                       // ball
+    b += sizeof(uint32_t) * (kRows * kLinks + kRows + (kRows & 1));   // wmask, smask
+    b += sizeof(int2) * kRows + sizeof(int) * kRows;                  // krange, hrow
+    b += sizeof(float) * kTile * kLinks;                              // wcost
+    b += sizeof(int) * (kTile + 4);                                   // pcount, counters
+    b += sizeof(uint16_t) * (kTile * kLinks + kTile * 32 + kTile * kPairCap);
+    b = (b + 15) & ~(size_t)15;
+    if (do_world) b += sizeof(uint32_t) * kTile * (Wcp + 1);
+    if (do_self) b += sizeof(uint32_t) * kTile * (Wov + 1);
+    b += sizeof(float) * (size_t)kRows * (R.cols | 1);                // ctile
+    return b + 16;
+}
+
 }  // namespace
 
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
@@ -475,12 +632,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     const int Wos = row_words_of(fos, R.cols);
     const int Wcp = a.do_world ? row_words_of(fcp, R.cols) : 0;
     const int Wov = a.do_self ? row_words_of(fov, R.cols) : 0;
-    const int cs = R.cols | 1;
-    size_t smem = sizeof(float4) * kRows * kLinks + sizeof(uint32_t) * (kRows * kLinks + kRows) +
-                  sizeof(int2) * kRows +
-                  sizeof(float) * ((size_t)kRows * cs + (size_t)R.n_spheres * kTile);
-    if (a.do_world) smem += sizeof(uint32_t) * kTile * (Wcp + 1);
-    if (a.do_self) smem += sizeof(uint32_t) * kTile * (Wov + 1);
+    const size_t smem = collision_smem(R, a.do_world, a.do_self, Wcp, Wov);
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

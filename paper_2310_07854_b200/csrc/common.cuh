@@ -177,6 +177,18 @@ __device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) 
 
 template <int PF>
 __device__ __forceinline__ void decode_word_t(uint32_t w, float* out, const Fmt& f) {
+    if constexpr (PF == 2) {
+        // E5M10: the hardware f16 -> f32 conversion is exact except for the
+        // exponent-31 codes, which are finite in this reading (c3)
+        if (f.kind == KIND_F16 && (w & 0x7C00u) != 0x7C00u && (w & 0x7C000000u) != 0x7C000000u) {
+            float lo, hi;
+            asm("{ .reg .f16 a, b;\n mov.b32 {a, b}, %2;\n cvt.f32.f16 %0, a;\n cvt.f32.f16 %1, b;}"
+                : "=f"(lo), "=f"(hi) : "r"(w));
+            out[0] = lo;
+            out[1] = hi;
+            return;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < PF; ++j) out[j] = decode_slot(w, j, f);
 }
@@ -221,7 +233,12 @@ struct RobotDev {
     // link-pair broadphase: index (0..31) of the link pair (a, b) in the
     // per-pose self mask, -1 when no listed sphere pair joins the two links
     int8_t lp_index[kLinks][kLinks];
+    int8_t lp_a[32], lp_b[32];           // links of link pair i (lp_a <= lp_b)
     int32_t n_link_pairs;
+    // link bounding spheres: reference sphere of each link and the radius
+    // max_s(|o_s - o_ref| + r_s) over its spheres (rigid: the same in any pose)
+    int32_t link_ref[kLinks];
+    float link_rl[kLinks];
     uint8_t adj[2 * kMaxPairs];
 };
 
