@@ -224,13 +224,22 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     }
     R.link_start[0] = 0;
     for (int l = 0; l < kLinks; ++l) R.link_start[l + 1] = R.link_start[l] + count[l];
-    // adjacency lists (each pair from both ends), partners in ascending order
-    std::vector<std::vector<int>> adj(r->n_spheres);
+    // canonical pair list sorted by (i, j), i < j, duplicates removed
+    std::vector<std::pair<int, int>> plist;
     for (int k = 0; k < r->n_pairs; ++k) {
         const int i = r->pairs[2 * k], j = r->pairs[2 * k + 1];
         CHECK(i < r->n_spheres && j < r->n_spheres && i != j, VAPR_ERR_INVALID_ARG);
-        adj[i].push_back(j);
-        adj[j].push_back(i);
+        plist.emplace_back(std::min(i, j), std::max(i, j));
+    }
+    std::sort(plist.begin(), plist.end());
+    plist.erase(std::unique(plist.begin(), plist.end()), plist.end());
+    R.n_pairs = (int32_t)plist.size();
+    std::vector<std::vector<std::pair<int, int>>> adj(r->n_spheres);   // (partner, pid)
+    for (int k = 0; k < (int)plist.size(); ++k) {
+        R.pair_i[k] = (uint8_t)plist[k].first;
+        R.pair_j[k] = (uint8_t)plist[k].second;
+        adj[plist[k].first].emplace_back(plist[k].second, k);
+        adj[plist[k].second].emplace_back(plist[k].first, k);
     }
     for (int a = 0; a < kLinks; ++a)
         for (int b = 0; b < kLinks; ++b) R.lp_index[a][b] = -1;
@@ -238,12 +247,12 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     int o = 0;
     for (int s = 0; s < r->n_spheres; ++s) {
         R.adj_off[s] = (uint16_t)o;
-        std::vector<int>& a = adj[s];
+        std::vector<std::pair<int, int>>& a = adj[s];
         std::sort(a.begin(), a.end());
-        a.erase(std::unique(a.begin(), a.end()), a.end());
         const int ls = r->sphere_link[s];
         int L = 0;
-        for (int v : a) {
+        for (const auto& pv : a) {
+            const int v = pv.first;
             const int lv = r->sphere_link[v];
             while (L <= lv) R.adj_link_off[s][L++] = (uint16_t)o;
             if (R.lp_index[ls][lv] < 0) {
@@ -252,6 +261,7 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
                 R.lp_b[nlp] = (int8_t)std::max(ls, lv);
                 R.lp_index[ls][lv] = R.lp_index[lv][ls] = (int8_t)nlp++;
             }
+            R.adj_pid[o] = (uint16_t)pv.second;
             R.adj[o++] = (uint8_t)v;
         }
         while (L <= kLinks) R.adj_link_off[s][L++] = (uint16_t)o;

@@ -44,7 +44,6 @@ constexpr int kTile = 64;           // poses per CTA
 constexpr int kRows = kTile + 2;    // with the two halo poses
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kPairCap = 16;        // active self pairs listed per pose (else brute force)
 constexpr float kSlack = 1e-4f;
 
 struct Acc {
@@ -178,11 +177,11 @@ struct Smem {
     int2* krange;      // [kRows] cuboid range of the row's world
     int* hrow;         // [kRows] step index h, -1 when the row is absent
     float* wcost;      // [kTile * kLinks]
-    int* pcount;       // [kTile] active self pairs per pose
+    unsigned long long* touched;   // [kTile] spheres with an active self pair
     int* counters;     // [4]: world tasks, self tasks, max-coordinate bits, spare
     uint16_t* wtask;   // [kTile * kLinks]
     uint16_t* stask;   // [kTile * 32]
-    uint16_t* pkey;    // [kTile * kPairCap] active pair keys i * 64 + j
+    uint32_t* pmask;   // [kTile * PMW] active self pairs, bit = canonical pair id
     uint32_t* wcp;     // [kTile * (Wcp+1)]
     uint32_t* wov;     // [kTile * (Wov+1)]
 };
@@ -206,14 +205,15 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     sm.smask = sm.wmask + kRows * kLinks;
     sm.krange = reinterpret_cast<int2*>(sm.smask + kRows + (kRows & 1));
     sm.hrow = reinterpret_cast<int*>(sm.krange + kRows);
-    sm.wcost = reinterpret_cast<float*>(sm.hrow + kRows);
-    sm.pcount = reinterpret_cast<int*>(sm.wcost + kTile * kLinks);
-    sm.counters = sm.pcount + kTile;
-    sm.wtask = reinterpret_cast<uint16_t*>(sm.counters + 4);
+    const int PMW = (R.n_pairs + 31) >> 5;
+    sm.touched = reinterpret_cast<unsigned long long*>(sm.hrow + kRows + (kRows & 1));
+    sm.wcost = reinterpret_cast<float*>(sm.touched + kTile);
+    sm.counters = reinterpret_cast<int*>(sm.wcost + kTile * kLinks);
+    sm.pmask = reinterpret_cast<uint32_t*>(sm.counters + 4);
+    sm.wtask = reinterpret_cast<uint16_t*>(sm.pmask + kTile * PMW);
     sm.stask = sm.wtask + kTile * kLinks;
-    sm.pkey = sm.stask + kTile * 32;
     {
-        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.pkey + kTile * kPairCap);
+        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.stask + kTile * 32);
         sm.wcp = reinterpret_cast<uint32_t*>((e + 15) & ~uintptr_t(15));
     }
     sm.wov = sm.wcp + (a.do_world ? kTile * WcpS : 0);
@@ -260,7 +260,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     if (a.do_self)
         for (int i = tid; i < kTile * WovS; i += kThreads) sm.wov[i] = 0u;
     for (int i = tid; i < kTile * kLinks; i += kThreads) sm.wcost[i] = 0.f;
-    if (tid < kTile) sm.pcount[tid] = 0;
+    if (a.do_self) {
+        for (int i = tid; i < kTile * PMW; i += kThreads) sm.pmask[i] = 0u;
+        if (tid < kTile) sm.touched[tid] = 0ull;
+    }
     // world cuboid range and step index h of every tile row (the only 64-bit
     // divisions of the kernel: once per row)
     for (int row = tid; row < kRows; row += kThreads) {
@@ -458,8 +461,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                     const int lo = min(i, j), hi = max(i, j);
                     float vx, vy, vz, c;
                     if (self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
-                        const int slot = atomicAdd(sm.pcount + p, 1);
-                        if (slot < kPairCap) sm.pkey[p * kPairCap + slot] = (uint16_t)(lo * 64 + hi);
+                        const int pid = R.adj_pid[jj];
+                        atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                        atomicOr(sm.touched + p, (1ull << lo) | (1ull << hi));
                     }
                 }
             }
@@ -467,82 +471,51 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     }
     __syncthreads();
 
-    // ---- 4. per pose: self accumulation in pair order, costs.
-    // The active pairs involving a sphere s, in (i, j) key order, are exactly
-    // its partners in ascending order; both the sorted-list path and the
-    // brute-force fallback (more than kPairCap active pairs) accumulate in that
-    // order with the same arithmetic, so they give identical results.
+    // ---- 4a. self gradients: one item per (pose, touched sphere); the active
+    //          pairs of sphere s are gathered over its partners in ascending
+    //          order (independent of culling and of the task order).
+    if (a.do_self) {
+        for (int it = tid; it < np * 64; it += kThreads) {
+            const int p = it >> 6, s = it & 63;
+            if (!((sm.touched[p] >> s) & 1ull)) continue;
+            const float* crow = sm.ctile + (p + 1) * cs;
+            const uint32_t* pm = sm.pmask + p * PMW;
+            float gx = 0.f, gy = 0.f, gz = 0.f;
+            for (int jj = R.adj_off[s]; jj < R.adj_off[s + 1]; ++jj) {
+                const int pid = R.adj_pid[jj];
+                if (!((pm[pid >> 5] >> (pid & 31)) & 1u)) continue;
+                const int o = R.adj[jj];
+                const int lo = min(s, o), hi = max(s, o);
+                float vx, vy, vz, c;
+                self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                const float sg = (lo == s) ? -1.f : 1.f;
+                gx = fmaf(sg, vx, gx);
+                gy = fmaf(sg, vy, gy);
+                gz = fmaf(sg, vz, gz);
+            }
+            uint32_t* orow = sm.wov + p * WovS;
+            or_code(orow, 3 * s + 0, gx + 0.f, fov, rc_ov);
+            or_code(orow, 3 * s + 1, gy + 0.f, fov, rc_ov);
+            or_code(orow, 3 * s + 2, gz + 0.f, fov, rc_ov);
+        }
+    }
+    // ---- 4b. per-pose cost: world per link, then the active self pairs in id order
     if (tid < np) {
-        const int p = tid, row = p + 1;
-        const float* crow = sm.ctile + row * cs;
+        const int p = tid;
         float cost = 0.f;
         for (int l = 0; l < kLinks; ++l) cost += sm.wcost[p * kLinks + l];
         if (a.do_self) {
-            const int n = sm.pcount[p];
-            uint32_t* orow = sm.wov + p * WovS;
+            const float* crow = sm.ctile + (p + 1) * cs;
+            const uint32_t* pm = sm.pmask + p * PMW;
             float scost = 0.f;
-            if (n <= kPairCap) {
-                uint16_t key[kPairCap];
-                for (int k = 0; k < n; ++k) key[k] = sm.pkey[p * kPairCap + k];
-                for (int k = 1; k < n; ++k) {          // insertion sort by (i, j)
-                    const uint16_t v = key[k];
-                    int m = k - 1;
-                    while (m >= 0 && key[m] > v) {
-                        key[m + 1] = key[m];
-                        --m;
-                    }
-                    key[m + 1] = v;
-                }
-                unsigned long long touched = 0ull;
-                for (int k = 0; k < n; ++k) {
-                    const int i = key[k] >> 6, j = key[k] & 63;
+            for (int wd = 0; wd < PMW; ++wd)
+                for (uint32_t m = pm[wd]; m; m &= m - 1) {
+                    const int pid = (wd << 5) + __ffs(m) - 1;
                     float vx, vy, vz, c;
-                    self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                    self_pair(crow, R.pair_i[pid], R.pair_j[pid], R, a.eta_s, inv_eta_s, hoe_s,
+                              a.w_s, vx, vy, vz, c);
                     scost += c;
-                    touched |= (1ull << i) | (1ull << j);
                 }
-                while (touched) {
-                    const int s = __ffsll((long long)touched) - 1;
-                    touched &= touched - 1;
-                    float gx = 0.f, gy = 0.f, gz = 0.f;
-                    for (int k = 0; k < n; ++k) {
-                        const int i = key[k] >> 6, j = key[k] & 63;
-                        if (i != s && j != s) continue;
-                        float vx, vy, vz, c;
-                        self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
-                        const float sg = (i == s) ? -1.f : 1.f;
-                        gx = fmaf(sg, vx, gx);
-                        gy = fmaf(sg, vy, gy);
-                        gz = fmaf(sg, vz, gz);
-                    }
-                    or_code(orow, 3 * s + 0, gx + 0.f, fov, rc_ov);
-                    or_code(orow, 3 * s + 1, gy + 0.f, fov, rc_ov);
-                    or_code(orow, 3 * s + 2, gz + 0.f, fov, rc_ov);
-                }
-            } else {
-                for (int i = 0; i < R.n_spheres; ++i) {
-                    float gx = 0.f, gy = 0.f, gz = 0.f;
-                    bool any = false;
-                    for (int jj = R.adj_off[i]; jj < R.adj_off[i + 1]; ++jj) {
-                        const int o = R.adj[jj];
-                        const int lo = min(i, o), hi = max(i, o);
-                        float vx, vy, vz, c;
-                        if (!self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
-                            continue;
-                        any = true;
-                        if (o > i) scost += c;             // each pair once, in (i, j) order
-                        const float sg = (lo == i) ? -1.f : 1.f;
-                        gx = fmaf(sg, vx, gx);
-                        gy = fmaf(sg, vy, gy);
-                        gz = fmaf(sg, vz, gz);
-                    }
-                    if (any) {
-                        or_code(orow, 3 * i + 0, gx + 0.f, fov, rc_ov);
-                        or_code(orow, 3 * i + 1, gy + 0.f, fov, rc_ov);
-                        or_code(orow, 3 * i + 2, gz + 0.f, fov, rc_ov);
-                    }
-                }
-            }
             cost += scost;
         }
         a.cost[p0 + p] = cost;
@@ -612,9 +585,11 @@ size_t collision_smem(const RobotDev& R, bool do_world, bool do_self, int Wcp, i
     size_t b = sizeof(float4) * kRows * kLinks;                       // ball
     b += sizeof(uint32_t) * (kRows * kLinks + kRows + (kRows & 1));   // wmask, smask
     b += sizeof(int2) * kRows + sizeof(int) * kRows;                  // krange, hrow
+    b += sizeof(int) * (kRows & 1) + sizeof(unsigned long long) * kTile;   // touched
     b += sizeof(float) * kTile * kLinks;                              // wcost
-    b += sizeof(int) * (kTile + 4);                                   // pcount, counters
-    b += sizeof(uint16_t) * (kTile * kLinks + kTile * 32 + kTile * kPairCap);
+    b += sizeof(int) * 4;                                             // counters
+    b += sizeof(uint32_t) * kTile * ((R.n_pairs + 31) >> 5);          // pmask
+    b += sizeof(uint16_t) * (kTile * kLinks + kTile * 32);
     b = (b + 15) & ~(size_t)15;
     if (do_world) b += sizeof(uint32_t) * kTile * (Wcp + 1);
     if (do_self) b += sizeof(uint32_t) * kTile * (Wov + 1);

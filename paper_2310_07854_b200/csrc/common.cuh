@@ -239,6 +239,11 @@ struct RobotDev {
     // max_s(|o_s - o_ref| + r_s) over its spheres (rigid: the same in any pose)
     int32_t link_ref[kLinks];
     float link_rl[kLinks];
+    // canonical pair ids: pairs sorted by (i, j), i < j; adj_pid[jj] is the id
+    // of the pair (s, adj[jj]); pair_i / pair_j map an id back to its spheres
+    int32_t n_pairs;
+    uint16_t adj_pid[2 * kMaxPairs];
+    uint8_t pair_i[kMaxPairs], pair_j[kMaxPairs];
     uint8_t adj[2 * kMaxPairs];
 };
 
