@@ -268,6 +268,69 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     }
     R.adj_off[r->n_spheres] = (uint16_t)o;
     R.n_link_pairs = nlp;
+    // sub-link groups: the spheres of each link split into two contiguous halves
+    auto one_center = [&](int b0, int b1, int& ref, float& rl) {
+        ref = b0;
+        rl = -1.f;
+        double best = 1e300;
+        for (int a = b0; a < b1; ++a) {
+            double m = 0.0;
+            for (int b = b0; b < b1; ++b) {
+                const double dx = (double)R.sx[b] - R.sx[a], dy = (double)R.sy[b] - R.sy[a],
+                             dz = (double)R.sz[b] - R.sz[a];
+                m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz) + (double)R.sr[b]);
+            }
+            if (m < best) {
+                best = m;
+                ref = a;
+            }
+        }
+        if (best < 1e300) rl = std::nextafter((float)best, 3e38f);
+    };
+    std::vector<int> grp_of(r->n_spheres, 0);
+    int ng = 0;
+    std::vector<int> grp_link;
+    for (int l = 0; l < kLinks; ++l) {
+        const int b0 = R.link_start[l], b1 = R.link_start[l + 1];
+        if (b1 == b0) continue;
+        const int mid = b0 + (b1 - b0 + 1) / 2;
+        const int cuts[3] = {b0, mid, b1};
+        for (int h = 0; h < 2; ++h) {
+            if (cuts[h + 1] == cuts[h]) continue;
+            one_center(cuts[h], cuts[h + 1], R.grp_ref[ng], R.grp_rl[ng]);
+            for (int s2 = cuts[h]; s2 < cuts[h + 1]; ++s2) grp_of[s2] = ng;
+            grp_link.push_back(l);
+            ++ng;
+        }
+    }
+    R.n_groups = ng;
+    {
+        // group pairs, ordered by link pair then (ga, gb); pair ids of each
+        int ngp = 0, npid = 0;
+        for (int lp = 0; lp < nlp; ++lp) {
+            R.lp_gp_off[lp] = (uint8_t)ngp;
+            for (int ga = 0; ga < ng; ++ga)
+                for (int gb = ga; gb < ng; ++gb) {
+                    const int la = grp_link[ga], lb = grp_link[gb];
+                    if (!((la == R.lp_a[lp] && lb == R.lp_b[lp]) ||
+                          (la == R.lp_b[lp] && lb == R.lp_a[lp])))
+                        continue;
+                    const int start = npid;
+                    for (int k = 0; k < (int)plist.size(); ++k) {
+                        const int gi = grp_of[plist[k].first], gj = grp_of[plist[k].second];
+                        if ((gi == ga && gj == gb) || (gi == gb && gj == ga)) R.gp_pid[npid++] = (uint16_t)k;
+                    }
+                    if (npid == start) continue;
+                    CHECK(ngp < kMaxGroupPairs, VAPR_ERR_UNSUPPORTED);
+                    R.gp_a[ngp] = (uint8_t)ga;
+                    R.gp_b[ngp] = (uint8_t)gb;
+                    R.gp_off[ngp] = (uint16_t)start;
+                    ++ngp;
+                }
+        }
+        R.lp_gp_off[nlp] = (uint8_t)ngp;
+        R.gp_off[ngp] = (uint16_t)npid;
+    }
     // per-link reference sphere: the sphere minimising max_s(|o_s - o_ref| + r_s)
     for (int l = 0; l < kLinks; ++l) {
         R.link_ref[l] = R.link_start[l];

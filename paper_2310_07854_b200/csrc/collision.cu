@@ -10,21 +10,22 @@
 // the swept samples):
 //  1. decode the packed rows into an FP32 shared tile (row stride 3S|1, odd),
 //     tracking the largest decoded coordinate (quantisation-error bound);
-//  2. broadphase.  Each link's spheres lie in a ball around its reference
-//     sphere whose radius is rigid (computed once on the host) plus the
-//     quantisation-error margin.  Per (segment, link, cuboid) -- or per
-//     (pose, link, cuboid) for the discrete cost -- a cull bit from a lower
-//     bound of the 1-Lipschitz box SDF at the ball centre; per (pose, link
-//     pair) a cull bit from the ball-ball distance;
-//  3. the live (pose, link) world tasks and live (pose, link pair) self tasks
+//  2. broadphase.  The spheres of a link (or of a half-link group) lie in a
+//     ball around a reference sphere whose radius is rigid (computed once on
+//     the host) plus the quantisation-error margin.  World: per (segment,
+//     link, cuboid) -- or per (pose, link, cuboid) for the discrete cost -- a
+//     cull bit from a lower bound of the 1-Lipschitz box SDF at the ball
+//     centre.  Self: per (pose, link pair) a ball-ball test, then per live
+//     link pair its (<= 4) half-link group pairs;
+//  3. the live (pose, link) world tasks and live (pose, group pair) self tasks
 //     are compacted into shared task lists and processed by all threads;
 //     world tasks gather the complete gradient of each sphere of the link (no
 //     scatter) and OR its codes into shared packed rows (OR is
-//     order-independent); self tasks only collect the active sphere pairs of
-//     their pose;
-//  4. one thread per pose accumulates its self gradients and costs in pair
-//     order (deterministic); per-pose costs are reduced in a fixed order and
-//     the packed tiles streamed out with coalesced stores.
+//     order-independent); self tasks mark the active sphere pairs of their
+//     pose in a per-pose bitmask over canonical pair ids;
+//  4. one item per (pose, touched sphere) gathers its self gradient over its
+//     partners in ascending order; one thread per pose sums its costs in a
+//     fixed order; the packed tiles are streamed out with coalesced stores.
 //
 // Culling is exact: a term is skipped only when its bound clears the
 // activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
@@ -171,7 +172,6 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 
 struct Smem {
     float* ctile;      // [kRows * cs], row 0 = pose p0-1
-    float4* ball;      // [kRows * kLinks] link ball (centre, radius)
     uint32_t* wmask;   // [kRows * kLinks] bits 0-15 pose (discrete), 16-31 segment row->row+1
     uint32_t* smask;   // [kRows] live link pairs
     int2* krange;      // [kRows] cuboid range of the row's world
@@ -180,7 +180,7 @@ struct Smem {
     unsigned long long* touched;   // [kTile] spheres with an active self pair
     int* counters;     // [4]: world tasks, self tasks, max-coordinate bits, spare
     uint16_t* wtask;   // [kTile * kLinks]
-    uint16_t* stask;   // [kTile * 32]
+    uint16_t* stask;   // [kTile * n_group_pairs]
     uint32_t* pmask;   // [kTile * PMW] active self pairs, bit = canonical pair id
     uint32_t* wcp;     // [kTile * (Wcp+1)]
     uint32_t* wov;     // [kTile * (Wov+1)]
@@ -200,8 +200,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     const int WcpS = Wcp + 1, WovS = Wov + 1;
 
     Smem sm;
-    sm.ball = smem4;
-    sm.wmask = reinterpret_cast<uint32_t*>(sm.ball + kRows * kLinks);
+    sm.wmask = reinterpret_cast<uint32_t*>(smem4);
     sm.smask = sm.wmask + kRows * kLinks;
     sm.krange = reinterpret_cast<int2*>(sm.smask + kRows + (kRows & 1));
     sm.hrow = reinterpret_cast<int*>(sm.krange + kRows);
@@ -213,7 +212,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     sm.wtask = reinterpret_cast<uint16_t*>(sm.pmask + kTile * PMW);
     sm.stask = sm.wtask + kTile * kLinks;
     {
-        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.stask + kTile * 32);
+        const uintptr_t e =
+            reinterpret_cast<uintptr_t>(sm.stask + kTile * R.lp_gp_off[R.n_link_pairs]);
         sm.wcp = reinterpret_cast<uint32_t*>((e + 15) & ~uintptr_t(15));
     }
     sm.wov = sm.wcp + (a.do_world ? kTile * WcpS : 0);
@@ -300,30 +300,27 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         margin = 2.f * 1.7320509f * (rel * amaxf * 1.01f + sub);
     }
 
-    // ---- 2a. link balls (rows present in the tile)
-    for (int task = tid; task < kRows * kLinks; task += kThreads) {
-        const int row = task / kLinks, l = task - row * kLinks;
-        if (sm.hrow[row] < 0) continue;
-        const float* c = sm.ctile + row * cs + 3 * R.link_ref[l];
-        sm.ball[task] = make_float4(c[0], c[1], c[2], R.link_rl[l] + margin);
-    }
-    __syncthreads();
+    // ball of link / group `ref` in tile row `row`: (centre, radius)
+    auto ball = [&](int row, int ref, float rl) {
+        const float* c = sm.ctile + row * cs + 3 * ref;
+        return make_float4(c[0], c[1], c[2], rl + margin);
+    };
 
     // ---- 2b. world cull masks per (row, link); self link-pair masks per row
     const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
-    for (int task = tid; task < kRows * kLinks + kRows; task += kThreads) {
-        if (task < kRows * kLinks) {
+    for (int task = tid; task < kRows * kLinks; task += kThreads) {
+        {
             const int row = task / kLinks, l = task - row * kLinks;
             uint32_t m = 0;
             const int2 kr = sm.krange[row];
             const int h = sm.hrow[row];
             if (a.do_world && h >= 0 && kr.y > kr.x && R.link_rl[l] >= 0.f) {
-                const float4 b0 = sm.ball[task];
+                const float4 b0 = ball(row, R.link_ref[l], R.link_rl[l]);
                 if (nsub > 0) {
                     // segment row -> row+1 of the same trajectory: one ball
                     // around both endpoint balls bounds every sample
                     if (h + 1 < a.H && row + 1 < kRows && sm.hrow[row + 1] >= 0) {
-                        const float4 b1 = sm.ball[task + kLinks];
+                        const float4 b1 = ball(row + 1, R.link_ref[l], R.link_rl[l]);
                         const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
                         const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                         const float mx = b0.x + 0.5f * dx, my = b0.y + 0.5f * dy,
@@ -341,19 +338,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                 }
             }
             sm.wmask[task] = m;
-        } else {
-            const int row = task - kRows * kLinks;
-            uint32_t m = 0;
-            if (a.do_self && sm.hrow[row] >= 0 && row >= 1 && row <= np) {
-                for (int lp = 0; lp < R.n_link_pairs; ++lp) {
-                    const float4 A4 = sm.ball[row * kLinks + R.lp_a[lp]];
-                    const float4 B4 = sm.ball[row * kLinks + R.lp_b[lp]];
-                    const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
-                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    if (!can_cull || d - A4.w - B4.w - a.eta_s <= kSlack) m |= 1u << lp;
-                }
-            }
-            sm.smask[row] = m;
         }
     }
     __syncthreads();
@@ -376,7 +360,24 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         for (int task = tid; task < kTile * 32; task += kThreads) {
             const int p = task >> 5, lp = task & 31;
             if (p >= np || lp >= R.n_link_pairs) continue;
-            if ((sm.smask[p + 1] >> lp) & 1u) sm.stask[atomicAdd(sm.counters + 1, 1)] = (uint16_t)task;
+            const int row = p + 1;
+            const int la = R.lp_a[lp], lb = R.lp_b[lp];
+            float4 A4 = ball(row, R.link_ref[la], R.link_rl[la]);
+            float4 B4 = ball(row, R.link_ref[lb], R.link_rl[lb]);
+            float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
+            if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s > kSlack)
+                continue;
+            for (int g = R.lp_gp_off[lp]; g < R.lp_gp_off[lp + 1]; ++g) {
+                const int ga = R.gp_a[g], gb = R.gp_b[g];
+                A4 = ball(row, R.grp_ref[ga], R.grp_rl[ga]);
+                B4 = ball(row, R.grp_ref[gb], R.grp_rl[gb]);
+                dx = A4.x - B4.x;
+                dy = A4.y - B4.y;
+                dz = A4.z - B4.z;
+                if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s > kSlack)
+                    continue;
+                sm.stask[atomicAdd(sm.counters + 1, 1)] = (uint16_t)(p * kMaxGroupPairs + g);
+            }
         }
     __syncthreads();
 
@@ -443,28 +444,15 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             sm.wcost[task] = lcost;
         } else {
             const int task = sm.stask[t - n_wtask];
-            const int p = task >> 5, lp = task & 31;
-            const int row = p + 1;
-            const float* crow = sm.ctile + row * cs;
-            const int la = R.lp_a[lp], lb = R.lp_b[lp];
-            const float4 Bb = sm.ball[row * kLinks + lb];
-            for (int i = R.link_start[la]; i < R.link_start[la + 1]; ++i) {
-                // sphere i against the ball of link lb
-                const float dx = crow[3 * i] - Bb.x, dy = crow[3 * i + 1] - Bb.y,
-                            dz = crow[3 * i + 2] - Bb.z;
-                if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - R.sr[i] - Bb.w -
-                                        a.eta_s > kSlack)
-                    continue;
-                for (int jj = R.adj_link_off[i][lb]; jj < R.adj_link_off[i][lb + 1]; ++jj) {
-                    const int j = R.adj[jj];
-                    if (la == lb && j <= i) continue;          // same link: each pair once
-                    const int lo = min(i, j), hi = max(i, j);
-                    float vx, vy, vz, c;
-                    if (self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
-                        const int pid = R.adj_pid[jj];
-                        atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
-                        atomicOr(sm.touched + p, (1ull << lo) | (1ull << hi));
-                    }
+            const int p = task / kMaxGroupPairs, g = task - p * kMaxGroupPairs;
+            const float* crow = sm.ctile + (p + 1) * cs;
+            for (int k = R.gp_off[g]; k < R.gp_off[g + 1]; ++k) {
+                const int pid = R.gp_pid[k];
+                const int i = R.pair_i[pid], j = R.pair_j[pid];
+                float vx, vy, vz, c;
+                if (self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
+                    atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                    atomicOr(sm.touched + p, (1ull << i) | (1ull << j));
                 }
             }
         }
@@ -582,14 +570,13 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
 }
 
 size_t collision_smem(const RobotDev& R, bool do_world, bool do_self, int Wcp, int Wov) {
-    size_t b = sizeof(float4) * kRows * kLinks;                       // ball
-    b += sizeof(uint32_t) * (kRows * kLinks + kRows + (kRows & 1));   // wmask, smask
+    size_t b = sizeof(uint32_t) * (kRows * kLinks + kRows + (kRows & 1));   // wmask, smask
     b += sizeof(int2) * kRows + sizeof(int) * kRows;                  // krange, hrow
     b += sizeof(int) * (kRows & 1) + sizeof(unsigned long long) * kTile;   // touched
     b += sizeof(float) * kTile * kLinks;                              // wcost
     b += sizeof(int) * 4;                                             // counters
     b += sizeof(uint32_t) * kTile * ((R.n_pairs + 31) >> 5);          // pmask
-    b += sizeof(uint16_t) * (kTile * kLinks + kTile * 32);
+    b += sizeof(uint16_t) * (kTile * kLinks + kTile * R.lp_gp_off[R.n_link_pairs]);
     b = (b + 15) & ~(size_t)15;
     if (do_world) b += sizeof(uint32_t) * kTile * (Wcp + 1);
     if (do_self) b += sizeof(uint32_t) * kTile * (Wov + 1);

@@ -16,6 +16,7 @@ constexpr int kMaxPairs = VAPR_MAX_PAIRS;
 constexpr int kMaxCuboids = VAPR_MAX_CUBOIDS_PER_WORLD;
 constexpr int kLinks = 9;          // link0..link7, hand
 constexpr int kJoints = 7;
+constexpr int kMaxGroupPairs = 128;
 
 // ---------------------------------------------------------------------------
 // ExMy format descriptor (readings c1-c9).  All derived constants are
@@ -244,6 +245,16 @@ struct RobotDev {
     int32_t n_pairs;
     uint16_t adj_pid[2 * kMaxPairs];
     uint8_t pair_i[kMaxPairs], pair_j[kMaxPairs];
+    // sub-link groups (each link's spheres split in two contiguous halves),
+    // each with a reference sphere and a rigid bounding radius, for the
+    // two-level self-collision broadphase: link pair -> group pairs -> pairs.
+    int32_t n_groups;
+    int32_t grp_ref[2 * kLinks];
+    float grp_rl[2 * kLinks];
+    uint8_t lp_gp_off[33];               // group pairs of link pair lp: [off[lp], off[lp+1])
+    uint8_t gp_a[kMaxGroupPairs], gp_b[kMaxGroupPairs];
+    uint16_t gp_off[kMaxGroupPairs + 1]; // pair ids of group pair g: gp_pid[gp_off[g] ..]
+    uint16_t gp_pid[kMaxPairs];
     uint8_t adj[2 * kMaxPairs];
 };
 
