@@ -133,6 +133,16 @@ __device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt
     atomicOr(row + w, c << ((e - w * f.pf) * f.t));
 }
 
+// Append to a shared list with one atomic per warp; every lane of the warp
+// must call it.  Returns the lane's slot (meaningful only when pred).
+__device__ __forceinline__ int warp_append(int* counter, bool pred, int lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
 // Self pair (i, j), i < j: false when inactive; else the gradient
 // contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
 __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const RobotDev& R,
@@ -178,9 +188,11 @@ struct Smem {
     int* hrow;         // [kRows] step index h, -1 when the row is absent
     float* wcost;      // [kTile * kLinks]
     unsigned long long* touched;   // [kTile] spheres with an active self pair
-    int* counters;     // [4]: world tasks, self tasks, max-coordinate bits, spare
+    int* counters;     // [8]: world tasks, self tasks, max-coordinate bits, live link
+                       //      pairs, touched spheres
     uint16_t* wtask;   // [kTile * kLinks]
     uint16_t* stask;   // [kTile * n_group_pairs]
+    uint16_t* l1;      // [kTile * 64] live (pose, link pair), later touched (pose, sphere)
     uint32_t* pmask;   // [kTile * PMW] active self pairs, bit = canonical pair id
     uint32_t* wcp;     // [kTile * (Wcp+1)]
     uint32_t* wov;     // [kTile * (Wov+1)]
@@ -208,12 +220,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     sm.touched = reinterpret_cast<unsigned long long*>(sm.hrow + kRows + (kRows & 1));
     sm.wcost = reinterpret_cast<float*>(sm.touched + kTile);
     sm.counters = reinterpret_cast<int*>(sm.wcost + kTile * kLinks);
-    sm.pmask = reinterpret_cast<uint32_t*>(sm.counters + 4);
+    sm.pmask = reinterpret_cast<uint32_t*>(sm.counters + 8);
     sm.wtask = reinterpret_cast<uint16_t*>(sm.pmask + kTile * PMW);
     sm.stask = sm.wtask + kTile * kLinks;
+    sm.l1 = sm.stask + kTile * R.lp_gp_off[R.n_link_pairs];
     {
-        const uintptr_t e =
-            reinterpret_cast<uintptr_t>(sm.stask + kTile * R.lp_gp_off[R.n_link_pairs]);
+        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.l1 + kTile * 64);
         sm.wcp = reinterpret_cast<uint32_t*>((e + 15) & ~uintptr_t(15));
     }
     sm.wov = sm.wcp + (a.do_world ? kTile * WcpS : 0);
@@ -223,7 +235,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     const long long r_lo = max(p0 - 1, 0LL);
     const long long r_hi = min(p0 + np + 1, P);           // exclusive
     const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
-    if (tid < 4) sm.counters[tid] = 0;
+    if (tid < 8) sm.counters[tid] = 0;
     __syncthreads();
     {
         const int nrows = int(r_hi - r_lo);
@@ -342,145 +354,183 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     }
     __syncthreads();
 
-    // ---- 2c. task lists: live (pose, link) world tasks, live (pose, link pair) self tasks
+    // ---- 2c. task lists (dense, appended with one atomic per warp):
+    //          live (pose, link) world tasks and live (pose, link pair) self
+    //          candidates.  Loops run over whole warps so every lane votes.
+    const int lane = tid & 31;
     if (a.do_world)
-        for (int task = tid; task < kTile * kLinks; task += kThreads) {
+        for (int base = tid - lane; base < kTile * kLinks; base += kThreads) {
+            const int task = base + lane;
             const int p = task / kLinks, l = task - p * kLinks;
-            if (p >= np) continue;
-            const int row = p + 1, h = sm.hrow[row];
-            uint32_t m;
-            if (nsub > 0)
-                m = (sm.wmask[row * kLinks + l] >> 16) |
-                    (h > 0 ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u);
-            else
-                m = sm.wmask[row * kLinks + l] & 0xffffu;
-            if (m) sm.wtask[atomicAdd(sm.counters + 0, 1)] = (uint16_t)task;
+            bool live = false;
+            if (p < np) {
+                const int row = p + 1, h = sm.hrow[row];
+                uint32_t m;
+                if (nsub > 0)
+                    m = (sm.wmask[row * kLinks + l] >> 16) |
+                        (h > 0 ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u);
+                else
+                    m = sm.wmask[row * kLinks + l] & 0xffffu;
+                live = m != 0u;
+            }
+            const int slot = warp_append(sm.counters + 0, live, lane);
+            if (live) sm.wtask[slot] = (uint16_t)task;
         }
     if (a.do_self)
-        for (int task = tid; task < kTile * 32; task += kThreads) {
-            const int p = task >> 5, lp = task & 31;
-            if (p >= np || lp >= R.n_link_pairs) continue;
-            const int row = p + 1;
-            const int la = R.lp_a[lp], lb = R.lp_b[lp];
-            float4 A4 = ball(row, R.link_ref[la], R.link_rl[la]);
-            float4 B4 = ball(row, R.link_ref[lb], R.link_rl[lb]);
-            float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
-            if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s > kSlack)
-                continue;
-            for (int g = R.lp_gp_off[lp]; g < R.lp_gp_off[lp + 1]; ++g) {
-                const int ga = R.gp_a[g], gb = R.gp_b[g];
-                A4 = ball(row, R.grp_ref[ga], R.grp_rl[ga]);
-                B4 = ball(row, R.grp_ref[gb], R.grp_rl[gb]);
-                dx = A4.x - B4.x;
-                dy = A4.y - B4.y;
-                dz = A4.z - B4.z;
-                if (can_cull && sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s > kSlack)
-                    continue;
-                sm.stask[atomicAdd(sm.counters + 1, 1)] = (uint16_t)(p * kMaxGroupPairs + g);
+        for (int base = tid - lane; base < kTile * R.n_link_pairs; base += kThreads) {
+            const int task = base + lane;
+            const int p = task / R.n_link_pairs, lp = task - p * R.n_link_pairs;
+            bool live = false;
+            if (p < np) {
+                const int row = p + 1;
+                const int la = R.lp_a[lp], lb = R.lp_b[lp];
+                const float4 A4 = ball(row, R.link_ref[la], R.link_rl[la]);
+                const float4 B4 = ball(row, R.link_ref[lb], R.link_rl[lb]);
+                const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
+                live = !can_cull ||
+                       sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s <= kSlack;
             }
+            const int slot = warp_append(sm.counters + 3, live, lane);
+            if (live) sm.l1[slot] = (uint16_t)(p * 32 + lp);
         }
     __syncthreads();
+    // self level 2: the (<= 4) half-link group pairs of every live link pair
+    if (a.do_self) {
+        const int n1 = sm.counters[3];
+        for (int base = tid - lane; base < n1 * 4; base += kThreads) {
+            const int it = base + lane;
+            bool live = false;
+            int p = 0, g = 0;
+            if (it < n1 * 4) {
+                const int e = sm.l1[it >> 2];
+                p = e >> 5;
+                const int lp = e & 31;
+                g = R.lp_gp_off[lp] + (it & 3);
+                if (g < R.lp_gp_off[lp + 1]) {
+                    const int row = p + 1;
+                    const int ga = R.gp_a[g], gb = R.gp_b[g];
+                    const float4 A4 = ball(row, R.grp_ref[ga], R.grp_rl[ga]);
+                    const float4 B4 = ball(row, R.grp_ref[gb], R.grp_rl[gb]);
+                    const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
+                    live = !can_cull ||
+                           sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s <= kSlack;
+                }
+            }
+            const int slot = warp_append(sm.counters + 1, live, lane);
+            if (live) sm.stask[slot] = (uint16_t)(p * kMaxGroupPairs + g);
+        }
+    }
+    __syncthreads();
 
-    // ---- 3. world tasks (all spheres of one link of one pose) and self tasks
-    //         (active sphere pairs of one link pair of one pose)
+    // ---- 3a. world tasks: all spheres of one link of one pose
     const uint32_t rc_cp = 65536u / fcp.pf + 1u, rc_ov = 65536u / fov.pf + 1u;
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
     const float inv_n1 = 1.f / float(nsub + 1);
     const int n_wtask = sm.counters[0], n_stask = sm.counters[1];
-    for (int t = tid; t < n_wtask + n_stask; t += kThreads) {
-        if (t < n_wtask) {
-            const int task = sm.wtask[t];
-            const int p = task / kLinks, l = task - p * kLinks;
-            const int row = p + 1, h = sm.hrow[row];
-            const int k0 = sm.krange[row].x;
-            uint32_t m_own, m_fwd = 0, m_bwd = 0;
-            if (nsub > 0) {
-                m_fwd = (h < a.H - 1) ? (sm.wmask[row * kLinks + l] >> 16) : 0u;
-                m_bwd = (h > 0) ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u;
-                m_own = m_fwd | m_bwd;     // a segment ball contains both endpoint balls
-            } else {
-                m_own = sm.wmask[row * kLinks + l] & 0xffffu;
-            }
-            const float* crow = sm.ctile + row * cs;
-            uint32_t* orow = sm.wcp + p * WcpS;
-            float lcost = 0.f;
-            for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
-                const float cx = crow[3 * s], cy = crow[3 * s + 1], cz = crow[3 * s + 2];
-                const float A = R.sr[s] + a.eta_w;
-                Acc acc{0.f, 0.f, 0.f, 0.f};
-                for (uint32_t m = m_own; m; m &= m - 1)
-                    world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), cx, cy, cz, A, a.eta_w,
-                               inv_eta_w, hoe_w, a.w_w, 1.f, 1.f, acc);
-                if (m_fwd) {                // samples of segment (h, h+1): cost + (1-tau) grad
-                    const float* nrow = crow + cs;
-                    const float nx = nrow[3 * s], ny = nrow[3 * s + 1], nz = nrow[3 * s + 2];
-                    for (int j = 1; j <= nsub; ++j) {
-                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                        const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
-                                    sz = fmaf(tau, nz, omt * cz);
-                        for (uint32_t m = m_fwd; m; m &= m - 1)
-                            world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A,
-                                       a.eta_w, inv_eta_w, hoe_w, a.w_w, 1.f, omt, acc);
-                    }
-                }
-                if (m_bwd) {                // samples of segment (h-1, h): tau grad only
-                    const float* prow = crow - cs;
-                    const float qx = prow[3 * s], qy = prow[3 * s + 1], qz = prow[3 * s + 2];
-                    for (int j = 1; j <= nsub; ++j) {
-                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                        const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
-                                    sz = fmaf(tau, cz, omt * qz);
-                        for (uint32_t m = m_bwd; m; m &= m - 1)
-                            world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A,
-                                       a.eta_w, inv_eta_w, hoe_w, a.w_w, 0.f, tau, acc);
-                    }
-                }
-                lcost += acc.cost;
-                or_code(orow, 3 * s + 0, acc.gx + 0.f, fcp, rc_cp);
-                or_code(orow, 3 * s + 1, acc.gy + 0.f, fcp, rc_cp);
-                or_code(orow, 3 * s + 2, acc.gz + 0.f, fcp, rc_cp);
-            }
-            sm.wcost[task] = lcost;
+    for (int t = tid; t < n_wtask; t += kThreads) {
+        const int task = sm.wtask[t];
+        const int p = task / kLinks, l = task - p * kLinks;
+        const int row = p + 1, h = sm.hrow[row];
+        const int k0 = sm.krange[row].x;
+        uint32_t m_own, m_fwd = 0, m_bwd = 0;
+        if (nsub > 0) {
+            m_fwd = (h < a.H - 1) ? (sm.wmask[row * kLinks + l] >> 16) : 0u;
+            m_bwd = (h > 0) ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u;
+            m_own = m_fwd | m_bwd;     // a segment ball contains both endpoint balls
         } else {
-            const int task = sm.stask[t - n_wtask];
-            const int p = task / kMaxGroupPairs, g = task - p * kMaxGroupPairs;
-            const float* crow = sm.ctile + (p + 1) * cs;
-            for (int k = R.gp_off[g]; k < R.gp_off[g + 1]; ++k) {
-                const int pid = R.gp_pid[k];
-                const int i = R.pair_i[pid], j = R.pair_j[pid];
-                float vx, vy, vz, c;
-                if (self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
-                    atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
-                    atomicOr(sm.touched + p, (1ull << i) | (1ull << j));
+            m_own = sm.wmask[row * kLinks + l] & 0xffffu;
+        }
+        const float* crow = sm.ctile + row * cs;
+        uint32_t* orow = sm.wcp + p * WcpS;
+        float lcost = 0.f;
+        for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
+            const float cx = crow[3 * s], cy = crow[3 * s + 1], cz = crow[3 * s + 2];
+            const float A = R.sr[s] + a.eta_w;
+            Acc acc{0.f, 0.f, 0.f, 0.f};
+            for (uint32_t m = m_own; m; m &= m - 1)
+                world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), cx, cy, cz, A, a.eta_w, inv_eta_w,
+                           hoe_w, a.w_w, 1.f, 1.f, acc);
+            if (m_fwd) {                // samples of segment (h, h+1): cost + (1-tau) grad
+                const float* nrow = crow + cs;
+                const float nx = nrow[3 * s], ny = nrow[3 * s + 1], nz = nrow[3 * s + 2];
+                for (int j = 1; j <= nsub; ++j) {
+                    const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                    const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
+                                sz = fmaf(tau, nz, omt * cz);
+                    for (uint32_t m = m_fwd; m; m &= m - 1)
+                        world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w,
+                                   inv_eta_w, hoe_w, a.w_w, 1.f, omt, acc);
                 }
+            }
+            if (m_bwd) {                // samples of segment (h-1, h): tau grad only
+                const float* prow = crow - cs;
+                const float qx = prow[3 * s], qy = prow[3 * s + 1], qz = prow[3 * s + 2];
+                for (int j = 1; j <= nsub; ++j) {
+                    const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                    const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
+                                sz = fmaf(tau, cz, omt * qz);
+                    for (uint32_t m = m_bwd; m; m &= m - 1)
+                        world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w,
+                                   inv_eta_w, hoe_w, a.w_w, 0.f, tau, acc);
+                }
+            }
+            lcost += acc.cost;
+            or_code(orow, 3 * s + 0, acc.gx + 0.f, fcp, rc_cp);
+            or_code(orow, 3 * s + 1, acc.gy + 0.f, fcp, rc_cp);
+            or_code(orow, 3 * s + 2, acc.gz + 0.f, fcp, rc_cp);
+        }
+        sm.wcost[task] = lcost;
+    }
+    // ---- 3b. self tasks: the active sphere pairs of one group pair of one pose
+    for (int t = tid; t < n_stask; t += kThreads) {
+        const int task = sm.stask[t];
+        const int p = task / kMaxGroupPairs, g = task - p * kMaxGroupPairs;
+        const float* crow = sm.ctile + (p + 1) * cs;
+        for (int k = R.gp_off[g]; k < R.gp_off[g + 1]; ++k) {
+            const int pid = R.gp_pid[k];
+            const int i = R.pair_i[pid], j = R.pair_j[pid];
+            float vx, vy, vz, c;
+            if (self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
+                atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                atomicOr(sm.touched + p, (1ull << i) | (1ull << j));
             }
         }
     }
     __syncthreads();
 
-    // ---- 4a. self gradients: one item per (pose, touched sphere); the active
-    //          pairs of sphere s are gathered over its partners in ascending
-    //          order (independent of culling and of the task order).
+    // ---- 4a. self gradients: one item per (pose, touched sphere), gathered
+    //          over the pose's active pairs in canonical id order, which for a
+    //          fixed sphere s is its partners in ascending order (independent
+    //          of culling and of the task order).
     if (a.do_self) {
-        for (int it = tid; it < np * 64; it += kThreads) {
+        for (int base = tid - lane; base < np * 64; base += kThreads) {
+            const int it = base + lane;
             const int p = it >> 6, s = it & 63;
-            if (!((sm.touched[p] >> s) & 1ull)) continue;
+            const bool live = it < np * 64 && ((sm.touched[p] >> s) & 1ull);
+            const int slot = warp_append(sm.counters + 4, live, lane);
+            if (live) sm.l1[slot] = (uint16_t)it;        // l1 is free again
+        }
+        __syncthreads();
+        const int nt = sm.counters[4];
+        for (int t = tid; t < nt; t += kThreads) {
+            const int it = sm.l1[t];
+            const int p = it >> 6, s = it & 63;
             const float* crow = sm.ctile + (p + 1) * cs;
             const uint32_t* pm = sm.pmask + p * PMW;
             float gx = 0.f, gy = 0.f, gz = 0.f;
-            for (int jj = R.adj_off[s]; jj < R.adj_off[s + 1]; ++jj) {
-                const int pid = R.adj_pid[jj];
-                if (!((pm[pid >> 5] >> (pid & 31)) & 1u)) continue;
-                const int o = R.adj[jj];
-                const int lo = min(s, o), hi = max(s, o);
-                float vx, vy, vz, c;
-                self_pair(crow, lo, hi, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
-                const float sg = (lo == s) ? -1.f : 1.f;
-                gx = fmaf(sg, vx, gx);
-                gy = fmaf(sg, vy, gy);
-                gz = fmaf(sg, vz, gz);
-            }
+            for (int wd = 0; wd < PMW; ++wd)
+                for (uint32_t m = pm[wd]; m; m &= m - 1) {
+                    const int pid = (wd << 5) + __ffs(m) - 1;
+                    const int i = R.pair_i[pid], j = R.pair_j[pid];
+                    if (i != s && j != s) continue;
+                    float vx, vy, vz, c;
+                    self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                    const float sg = (i == s) ? -1.f : 1.f;
+                    gx = fmaf(sg, vx, gx);
+                    gy = fmaf(sg, vy, gy);
+                    gz = fmaf(sg, vz, gz);
+                }
             uint32_t* orow = sm.wov + p * WovS;
             or_code(orow, 3 * s + 0, gx + 0.f, fov, rc_ov);
             or_code(orow, 3 * s + 1, gy + 0.f, fov, rc_ov);
@@ -492,7 +542,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const int p = tid;
         float cost = 0.f;
         for (int l = 0; l < kLinks; ++l) cost += sm.wcost[p * kLinks + l];
-        if (a.do_self) {
+        if (a.do_self && sm.touched[p]) {
             const float* crow = sm.ctile + (p + 1) * cs;
             const uint32_t* pm = sm.pmask + p * PMW;
             float scost = 0.f;
@@ -574,9 +624,9 @@ size_t collision_smem(const RobotDev& R, bool do_world, bool do_self, int Wcp, i
     b += sizeof(int2) * kRows + sizeof(int) * kRows;                  // krange, hrow
     b += sizeof(int) * (kRows & 1) + sizeof(unsigned long long) * kTile;   // touched
     b += sizeof(float) * kTile * kLinks;                              // wcost
-    b += sizeof(int) * 4;                                             // counters
+    b += sizeof(int) * 8;                                             // counters
     b += sizeof(uint32_t) * kTile * ((R.n_pairs + 31) >> 5);          // pmask
-    b += sizeof(uint16_t) * (kTile * kLinks + kTile * R.lp_gp_off[R.n_link_pairs]);
+    b += sizeof(uint16_t) * (kTile * kLinks + kTile * R.lp_gp_off[R.n_link_pairs] + kTile * 64);
     b = (b + 15) & ~(size_t)15;
     if (do_world) b += sizeof(uint32_t) * kTile * (Wcp + 1);
     if (do_self) b += sizeof(uint32_t) * kTile * (Wov + 1);
