@@ -30,13 +30,17 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     extern __shared__ unsigned long long smem8[];
     const int WS = W + 1;
     unsigned long long* smask = smem8;                                // [kTile]
-    float* sq = reinterpret_cast<float*>(smask + kTile);              // [kTile * 7]
+    float4* so = reinterpret_cast<float4*>(smask + kTile);            // [kMaxSpheres] sphere offsets
+    float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
     uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
 
     smask[tid] = 0ull;
+    // sphere offsets are indexed per lane (by each pose's non-zero spheres):
+    // stage them in shared memory instead of the serialising constant bank
+    for (int i = tid; i < R.n_spheres; i += kTile) so[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
     for (int i = tid; i < np * kJoints; i += kTile) sq[i] = __ldcs(q + p0 * kJoints + i);
     __syncthreads();
     {
@@ -104,7 +108,8 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                     g[k] = decode(code_at(row[wi], e - wi * f.pf, f), f);
                 }
                 float cx, cy, cz;
-                xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
+                const float4 o4 = so[s];
+                xf_apply(X, o4.x, o4.y, o4.z, cx, cy, cz);
                 Fx += g[0];
                 Fy += g[1];
                 Fz += g[2];
@@ -140,7 +145,8 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
                       const uint32_t* gos, float* grad_q, cudaStream_t s) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
-    const size_t smem = sizeof(unsigned long long) * kTile + sizeof(float) * kTile * kJoints +
+    const size_t smem = sizeof(unsigned long long) * kTile + sizeof(float4) * kMaxSpheres +
+                        sizeof(float) * kTile * kJoints +
                         sizeof(uint32_t) * kTile * (W + 1);
     cudaError_t e = cudaFuncSetAttribute(bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

@@ -8,8 +8,11 @@
 //
 // One CTA per tile of kTile consecutive poses (+1 halo pose on each side for
 // the swept samples):
-//  1. decode the packed rows into an FP32 shared tile (row stride 3S|1, odd),
-//     tracking the largest decoded coordinate (quantisation-error bound);
+//  0. stage in shared memory everything that lanes index divergently: the
+//     robot's pair / group tables, sphere radii, and the cuboids of the
+//     tile's worlds (constant-bank reads serialise on divergent addresses);
+//  1. load the packed rows with all loads in flight, decode them into an FP32
+//     tile (row stride 3S|1, odd), track the largest decoded coordinate;
 //  2. broadphase.  The spheres of a link (or of a half-link group) lie in a
 //     ball around a reference sphere whose radius is rigid (computed once on
 //     the host) plus the quantisation-error margin.  World: per (segment,
@@ -18,14 +21,14 @@
 //     centre.  Self: per (pose, link pair) a ball-ball test, then per live
 //     link pair its (<= 4) half-link group pairs;
 //  3. the live (pose, link) world tasks and live (pose, group pair) self tasks
-//     are compacted into shared task lists and processed by all threads;
-//     world tasks gather the complete gradient of each sphere of the link (no
-//     scatter) and OR its codes into shared packed rows (OR is
-//     order-independent); self tasks mark the active sphere pairs of their
-//     pose in a per-pose bitmask over canonical pair ids;
-//  4. one item per (pose, touched sphere) gathers its self gradient over its
-//     partners in ascending order; one thread per pose sums its costs in a
-//     fixed order; the packed tiles are streamed out with coalesced stores.
+//     are compacted into dense shared lists (one atomic per warp) and
+//     processed by all threads; world tasks gather the complete gradient of
+//     each sphere of the link (no scatter) and OR its codes into shared packed
+//     rows (OR is order-independent); self tasks mark the active sphere pairs
+//     of their pose in a per-pose bitmask over canonical pair ids;
+//  4. one item per (pose, touched sphere) gathers its self gradient over the
+//     active pairs in id order; one thread per pose sums its costs in a fixed
+//     order; the packed tiles are streamed out with coalesced stores.
 //
 // Culling is exact: a term is skipped only when its bound clears the
 // activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
@@ -45,6 +48,9 @@ constexpr int kTile = 64;           // poses per CTA
 constexpr int kRows = kTile + 2;    // with the two halo poses
 constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
+constexpr int kWorldCache = 4;      // distinct worlds whose cuboids a tile caches
+constexpr int kMaxLoads = 4;        // 16-byte loads in flight per thread when decoding
+constexpr int kUncached = 1 << 20;  // cuboid index offset marking a global (uncached) cuboid
 constexpr float kSlack = 1e-4f;
 
 struct Acc {
@@ -54,11 +60,6 @@ struct Acc {
 struct Cub {
     float4 q0, q1, q2, q3;   // R^T (9), t (3), h (3), pad
 };
-
-__device__ __forceinline__ Cub load_cub(const float4* __restrict__ cub, int k) {
-    return Cub{__ldg(cub + 4 * k), __ldg(cub + 4 * k + 1), __ldg(cub + 4 * k + 2),
-               __ldg(cub + 4 * k + 3)};
-}
 
 // Lower bound of the box signed distance at c (the exact value outside, the
 // face distance max_k(|p_k| - h_k) inside).
@@ -145,13 +146,13 @@ __device__ __forceinline__ int warp_append(int* counter, bool pred, int lane) {
 
 // Self pair (i, j), i < j: false when inactive; else the gradient
 // contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
-__device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const RobotDev& R,
+__device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const float* sr,
                                           float eta, float inv_eta, float hoe, float w, float& vx,
                                           float& vy, float& vz, float& cost) {
     const float dx = crow[3 * i] - crow[3 * j], dy = crow[3 * i + 1] - crow[3 * j + 1],
                 dz = crow[3 * i + 2] - crow[3 * j + 2];
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float Rs = R.sr[i] + R.sr[j] + eta;
+    const float Rs = sr[i] + sr[j] + eta;
     // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so d2 >= fl(Rs^2)
     // implies fl(sqrt(d2)) >= Rs, i.e. phi <= 0: exact early out.
     if (d2 >= Rs * Rs) return false;
@@ -180,120 +181,233 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
     return true;
 }
 
-struct Smem {
-    float* ctile;      // [kRows * cs], row 0 = pose p0-1
-    uint32_t* wmask;   // [kRows * kLinks] bits 0-15 pose (discrete), 16-31 segment row->row+1
-    uint32_t* smask;   // [kRows] live link pairs
-    int2* krange;      // [kRows] cuboid range of the row's world
-    int* hrow;         // [kRows] step index h, -1 when the row is absent
-    float* wcost;      // [kTile * kLinks]
-    unsigned long long* touched;   // [kTile] spheres with an active self pair
-    int* counters;     // [8]: world tasks, self tasks, max-coordinate bits, live link
-                       //      pairs, touched spheres
-    uint16_t* wtask;   // [kTile * kLinks]
-    uint16_t* stask;   // [kTile * n_group_pairs]
-    uint16_t* l1;      // [kTile * 64] live (pose, link pair), later touched (pose, sphere)
-    uint32_t* pmask;   // [kTile * PMW] active self pairs, bit = canonical pair id
-    uint32_t* wcp;     // [kTile * (Wcp+1)]
-    uint32_t* wov;     // [kTile * (Wov+1)]
+// Shared-memory carve-up (sizes depend on the robot and the formats).
+struct Layout {
+    int pmw, ngp, npairs;
+    unsigned cub, touched, krange, wmask, hrow, wslot, wcost, counters, pmask, sr, rl, ref, pij,
+        gpid, gpoff, gpab, lpab, lpgp, wtask, stask, l1, wcp, wov, ctile, total;
 };
+
+__host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, int do_self,
+                                              int Wcp, int Wov) {
+    Layout L{};
+    L.pmw = (R.n_pairs + 31) >> 5;
+    L.ngp = R.lp_gp_off[R.n_link_pairs];
+    L.npairs = R.n_pairs;
+    unsigned o = 0;
+    auto take = [&](unsigned bytes, unsigned align) {
+        o = (o + align - 1) / align * align;
+        const unsigned at = o;
+        o += bytes;
+        return at;
+    };
+    L.cub = take(sizeof(float4) * 4 * kMaxCuboids * kWorldCache, 16);
+    L.touched = take(sizeof(unsigned long long) * kTile, 8);
+    L.krange = take(sizeof(int2) * kRows, 8);
+    L.wmask = take(sizeof(uint32_t) * kRows * kLinks, 4);
+    L.hrow = take(sizeof(int) * kRows, 4);
+    L.wslot = take(sizeof(int) * kRows, 4);
+    L.wcost = take(sizeof(float) * kTile * kLinks, 4);
+    L.counters = take(sizeof(int) * 8, 4);
+    L.pmask = take(sizeof(uint32_t) * kTile * L.pmw, 4);
+    L.sr = take(sizeof(float) * kMaxSpheres, 4);
+    L.rl = take(sizeof(float) * 3 * kLinks, 4);          // link radii [9], group radii [18]
+    L.ref = take(sizeof(int) * 3 * kLinks, 4);           // link refs [9], group refs [18]
+    L.pij = take(sizeof(uint16_t) * L.npairs, 2);
+    L.gpid = take(sizeof(uint16_t) * L.npairs, 2);
+    L.gpoff = take(sizeof(uint16_t) * (kMaxGroupPairs + 1), 2);
+    L.gpab = take(sizeof(uint16_t) * kMaxGroupPairs, 2);
+    L.lpab = take(sizeof(uint16_t) * 33, 2);
+    L.lpgp = take(sizeof(uint16_t) * 33, 2);
+    L.wtask = take(sizeof(uint16_t) * kTile * kLinks, 2);
+    L.stask = take(sizeof(uint16_t) * kTile * (L.ngp > 0 ? L.ngp : 1), 2);
+    L.l1 = take(sizeof(uint16_t) * kTile * 64, 2);
+    L.wcp = take(do_world ? sizeof(uint32_t) * kTile * (Wcp + 1) : 0u, 16);
+    L.wov = take(do_self ? sizeof(uint32_t) * kTile * (Wov + 1) : 0u, 16);
+    L.ctile = take(sizeof(float) * kRows * (R.cols | 1), 16);
+    L.total = o + 16;
+    return L;
+}
 
 __global__ void __launch_bounds__(kThreads, 2)
 collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const Fmt fos,
                  const Fmt fcp, const Fmt fov, const CollisionArgs a, int Wos, int Wcp,
                  int Wov) {
     extern __shared__ float4 smem4[];
+    char* base = reinterpret_cast<char*>(smem4);
+    const Layout L = make_layout(R, a.do_world, a.do_self, Wcp, Wov);
+    Cub* scub = reinterpret_cast<Cub*>(base + L.cub);            // [kWorldCache * 16]
+    unsigned long long* touched = reinterpret_cast<unsigned long long*>(base + L.touched);
+    int2* krange = reinterpret_cast<int2*>(base + L.krange);     // cuboid range of each row
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(base + L.wmask);
+    int* hrow = reinterpret_cast<int*>(base + L.hrow);           // step index h, -1 if absent
+    int* wslot = reinterpret_cast<int*>(base + L.wslot);         // world of each row
+    float* wcost = reinterpret_cast<float*>(base + L.wcost);
+    int* counters = reinterpret_cast<int*>(base + L.counters);
+    uint32_t* pmask = reinterpret_cast<uint32_t*>(base + L.pmask);
+    float* ssr = reinterpret_cast<float*>(base + L.sr);
+    float* link_rl = reinterpret_cast<float*>(base + L.rl);
+    float* grp_rl = link_rl + kLinks;
+    int* link_ref = reinterpret_cast<int*>(base + L.ref);
+    int* grp_ref = link_ref + kLinks;
+    uint16_t* spij = reinterpret_cast<uint16_t*>(base + L.pij);  // i | j << 8
+    uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + L.gpid);
+    uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + L.gpoff);
+    uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + L.gpab);  // a | b << 8
+    uint16_t* slpab = reinterpret_cast<uint16_t*>(base + L.lpab);
+    uint16_t* slpgp = reinterpret_cast<uint16_t*>(base + L.lpgp);
+    uint16_t* wtask = reinterpret_cast<uint16_t*>(base + L.wtask);
+    uint16_t* stask = reinterpret_cast<uint16_t*>(base + L.stask);
+    uint16_t* l1 = reinterpret_cast<uint16_t*>(base + L.l1);
+    uint32_t* wcp = reinterpret_cast<uint32_t*>(base + L.wcp);
+    uint32_t* wov = reinterpret_cast<uint32_t*>(base + L.wov);
+    float* ctile = reinterpret_cast<float*>(base + L.ctile);
+
     const int cols = R.cols;
     const int cs = cols | 1;                       // odd fp32 row stride
     const long long P = (long long)a.B * a.H;
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int WcpS = Wcp + 1, WovS = Wov + 1;
+    const int PMW = L.pmw;
 
-    Smem sm;
-    sm.wmask = reinterpret_cast<uint32_t*>(smem4);
-    sm.smask = sm.wmask + kRows * kLinks;
-    sm.krange = reinterpret_cast<int2*>(sm.smask + kRows + (kRows & 1));
-    sm.hrow = reinterpret_cast<int*>(sm.krange + kRows);
-    const int PMW = (R.n_pairs + 31) >> 5;
-    sm.touched = reinterpret_cast<unsigned long long*>(sm.hrow + kRows + (kRows & 1));
-    sm.wcost = reinterpret_cast<float*>(sm.touched + kTile);
-    sm.counters = reinterpret_cast<int*>(sm.wcost + kTile * kLinks);
-    sm.pmask = reinterpret_cast<uint32_t*>(sm.counters + 8);
-    sm.wtask = reinterpret_cast<uint16_t*>(sm.pmask + kTile * PMW);
-    sm.stask = sm.wtask + kTile * kLinks;
-    sm.l1 = sm.stask + kTile * R.lp_gp_off[R.n_link_pairs];
-    {
-        const uintptr_t e = reinterpret_cast<uintptr_t>(sm.l1 + kTile * 64);
-        sm.wcp = reinterpret_cast<uint32_t*>((e + 15) & ~uintptr_t(15));
+    // ---- 0. stage the divergently-indexed tables; rows' step index and world
+    if (tid < 8) counters[tid] = 0;
+    for (int i = tid; i < R.n_spheres; i += kThreads) ssr[i] = R.sr[i];
+    if (tid < kLinks) {
+        link_rl[tid] = R.link_rl[tid];
+        link_ref[tid] = R.link_ref[tid];
     }
-    sm.wov = sm.wcp + (a.do_world ? kTile * WcpS : 0);
-    sm.ctile = reinterpret_cast<float*>(sm.wov + (a.do_self ? kTile * WovS : 0));
+    if (tid < 2 * kLinks) {
+        grp_rl[tid] = R.grp_rl[tid];
+        grp_ref[tid] = R.grp_ref[tid];
+    }
+    if (a.do_self) {
+        for (int i = tid; i < L.npairs; i += kThreads) {
+            spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
+            sgpid[i] = R.gp_pid[i];
+        }
+        for (int i = tid; i <= L.ngp; i += kThreads) sgpoff[i] = R.gp_off[i];
+        for (int i = tid; i < L.ngp; i += kThreads)
+            sgpab[i] = (uint16_t)(R.gp_a[i] | (R.gp_b[i] << 8));
+        for (int i = tid; i < R.n_link_pairs; i += kThreads)
+            slpab[i] = (uint16_t)(R.lp_a[i] | (R.lp_b[i] << 8));
+        for (int i = tid; i <= R.n_link_pairs; i += kThreads) slpgp[i] = R.lp_gp_off[i];
+    }
+    for (int row = tid; row < kRows; row += kThreads) {
+        const long long pg = p0 - 1 + row;
+        int hh = -1, wi = -1;
+        if (pg >= 0 && pg < P) {
+            const long long b = pg / a.H;      // the only 64-bit divisions: once per row
+            hh = int(pg - b * a.H);
+            if (a.do_world) {
+                wi = __ldg(a.world_idx + b);
+                if (wi < 0 || wi >= Wd.n_worlds) wi = -1;
+            }
+        }
+        hrow[row] = hh;
+        wslot[row] = wi;
+    }
+    __syncthreads();
+    // cuboid cache: the distinct worlds of the tile's rows (trajectories are
+    // contiguous, so a tile rarely sees more than two); a row whose world does
+    // not fit reads its cuboids from global memory (index + kUncached).
+    if (a.do_world && tid == 0) {
+        int nw = 0;
+        for (int row = 0; row < kRows; ++row) {
+            const int wi = wslot[row];
+            int slot = -1;
+            if (wi >= 0) {
+                for (int k = 0; k < nw; ++k)
+                    if (l1[k] == wi) slot = k;
+                if (slot < 0 && nw < kWorldCache) {
+                    l1[nw] = (uint16_t)wi;      // l1 doubles as scratch here
+                    slot = nw++;
+                }
+            }
+            wslot[row] = (wi >= 0 && slot < 0) ? -2 - wi : slot;
+        }
+        counters[5] = nw;
+    }
+    __syncthreads();
+    if (a.do_world) {
+        const int nw = counters[5];
+        for (int i = tid; i < nw * kMaxCuboids * 4; i += kThreads) {
+            const int k = i / (kMaxCuboids * 4), rest = i - k * kMaxCuboids * 4;
+            const int wi = l1[k];
+            const int c0 = __ldg(Wd.off + wi), c1 = __ldg(Wd.off + wi + 1);
+            if (c0 + (rest >> 2) < c1)
+                reinterpret_cast<float4*>(scub)[i] = __ldg(Wd.cub + 4 * (c0 + (rest >> 2)) + (rest & 3));
+        }
+        for (int row = tid; row < kRows; row += kThreads) {
+            const int sl = wslot[row];
+            int2 kr = make_int2(0, 0);
+            if (sl >= 0) {
+                const int wi = l1[sl];
+                kr = make_int2(sl * kMaxCuboids,
+                               sl * kMaxCuboids + __ldg(Wd.off + wi + 1) - __ldg(Wd.off + wi));
+            } else if (sl <= -2) {
+                const int wi = -2 - sl;
+                kr = make_int2(kUncached + __ldg(Wd.off + wi), kUncached + __ldg(Wd.off + wi + 1));
+            }
+            krange[row] = kr;
+        }
+    }
 
-    // ---- 1. decode rows p0-1 .. p0+np into the FP32 tile; zero the outputs
+    // ---- 1. load the packed rows p0-1 .. p0+np (all loads in flight), decode
     const long long r_lo = max(p0 - 1, 0LL);
     const long long r_hi = min(p0 + np + 1, P);           // exclusive
     const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
-    if (tid < 8) sm.counters[tid] = 0;
-    __syncthreads();
+    uint32_t amax = 0;
     {
-        const int nrows = int(r_hi - r_lo);
-        const int nw = nrows * Wos;
-        const uint32_t* src = a.os + r_lo * Wos;
-        const int dr = kThreads / Wos, dw = kThreads % Wos;
-        int r = tid / Wos, w = tid - (tid / Wos) * Wos;
-        uint32_t amax = 0;
-        with_pf(fos.pf, [&](auto Pc) {
-            constexpr int PF = decltype(Pc)::value;
-            for (int i = tid; i < nw; i += kThreads) {
-                float x[PF];
-                decode_word_t<PF>(__ldg(src + i), x, fos);
-                float* dst = sm.ctile + (row_off + r) * cs + w * PF;
+        const int Q = Wos / 4;                            // 16-byte groups per row
+        const int nq = int(r_hi - r_lo) * Q;
+        const uint4* src = reinterpret_cast<const uint4*>(a.os + r_lo * Wos);
+        for (int q0 = 0; q0 < nq; q0 += kThreads * kMaxLoads) {
+            uint4 v[kMaxLoads];
 #pragma unroll
-                for (int j = 0; j < PF; ++j)
-                    if (w * PF + j < cols) {
-                        dst[j] = x[j];
-                        amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
+            for (int k = 0; k < kMaxLoads; ++k) {
+                const int q = q0 + k * kThreads + tid;
+                if (q < nq) v[k] = __ldcs(src + q);
+            }
+            with_pf(fos.pf, [&](auto Pc) {
+                constexpr int PF = decltype(Pc)::value;
+#pragma unroll
+                for (int k = 0; k < kMaxLoads; ++k) {
+                    const int q = q0 + k * kThreads + tid;
+                    if (q < nq) {
+                        const int r = q / Q, g = q - r * Q;
+                        float* drow = ctile + (row_off + r) * cs;
+                        const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4) {
+                            float x[PF];
+                            decode_word_t<PF>(w4[j4], x, fos);
+                            const int e0 = (4 * g + j4) * PF;
+#pragma unroll
+                            for (int j = 0; j < PF; ++j)
+                                if (e0 + j < cols) {
+                                    drow[e0 + j] = x[j];
+                                    amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
+                                }
+                        }
                     }
-                r += dr;
-                w += dw;
-                if (w >= Wos) {
-                    w -= Wos;
-                    ++r;
                 }
-            }
-        });
-        amax = __reduce_max_sync(0xffffffffu, amax);
-        if ((tid & 31) == 0) atomicMax(reinterpret_cast<unsigned*>(sm.counters + 2), amax);
-    }
-    if (a.do_world)
-        for (int i = tid; i < kTile * WcpS; i += kThreads) sm.wcp[i] = 0u;
-    if (a.do_self)
-        for (int i = tid; i < kTile * WovS; i += kThreads) sm.wov[i] = 0u;
-    for (int i = tid; i < kTile * kLinks; i += kThreads) sm.wcost[i] = 0.f;
-    if (a.do_self) {
-        for (int i = tid; i < kTile * PMW; i += kThreads) sm.pmask[i] = 0u;
-        if (tid < kTile) sm.touched[tid] = 0ull;
-    }
-    // world cuboid range and step index h of every tile row (the only 64-bit
-    // divisions of the kernel: once per row)
-    for (int row = tid; row < kRows; row += kThreads) {
-        const long long pg = p0 - 1 + row;
-        int2 kr = make_int2(0, 0);
-        int hh = -1;
-        if (pg >= 0 && pg < P) {
-            const long long b = pg / a.H;
-            hh = int(pg - b * a.H);
-            if (a.do_world) {
-                const int wi = __ldg(a.world_idx + b);
-                if (wi >= 0 && wi < Wd.n_worlds)
-                    kr = make_int2(__ldg(Wd.off + wi), __ldg(Wd.off + wi + 1));
-            }
+            });
         }
-        sm.krange[row] = kr;
-        sm.hrow[row] = hh;
     }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(counters + 2), amax);
+    if (a.do_world)
+        for (int i = tid; i < kTile * WcpS; i += kThreads) wcp[i] = 0u;
+    if (a.do_self) {
+        for (int i = tid; i < kTile * WovS; i += kThreads) wov[i] = 0u;
+        for (int i = tid; i < kTile * PMW; i += kThreads) pmask[i] = 0u;
+        if (tid < kTile) touched[tid] = 0ull;
+    }
+    for (int i = tid; i < kTile * kLinks; i += kThreads) wcost[i] = 0.f;
     __syncthreads();
 
     // Quantisation margin: a decoded coordinate y of an FK value x satisfies
@@ -302,7 +416,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     // centres per distance and sqrt(3) per vector give the ball margin.  With
     // a saturated coordinate in the tile (|y| == max_finite) there is no bound
     // and culling is switched off for the tile.
-    const float amaxf = __uint_as_float((uint32_t)sm.counters[2]);
+    const float amaxf = __uint_as_float((uint32_t)counters[2]);
     bool can_cull = a.cull != 0;
     float margin = 0.f;
     if (fos.kind != KIND_IDENTITY) {
@@ -311,113 +425,113 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
         margin = 2.f * 1.7320509f * (rel * amaxf * 1.01f + sub);
     }
-
-    // ball of link / group `ref` in tile row `row`: (centre, radius)
+    // ball of link / group with reference sphere `ref` in tile row `row`
     auto ball = [&](int row, int ref, float rl) {
-        const float* c = sm.ctile + row * cs + 3 * ref;
+        const float* c = ctile + row * cs + 3 * ref;
         return make_float4(c[0], c[1], c[2], rl + margin);
     };
+    auto cuboid = [&](int k) -> Cub {
+        if (k < kUncached) return scub[k];
+        const int g = k - kUncached;
+        return Cub{__ldg(Wd.cub + 4 * g), __ldg(Wd.cub + 4 * g + 1), __ldg(Wd.cub + 4 * g + 2),
+                   __ldg(Wd.cub + 4 * g + 3)};
+    };
 
-    // ---- 2b. world cull masks per (row, link); self link-pair masks per row
+    // ---- 2. world cull masks per (row, link): bits 0-15 pose (discrete),
+    //         bits 16-31 segment row -> row+1 (swept)
     const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
-    for (int task = tid; task < kRows * kLinks; task += kThreads) {
-        {
+    if (a.do_world)
+        for (int task = tid; task < kRows * kLinks; task += kThreads) {
             const int row = task / kLinks, l = task - row * kLinks;
             uint32_t m = 0;
-            const int2 kr = sm.krange[row];
-            const int h = sm.hrow[row];
-            if (a.do_world && h >= 0 && kr.y > kr.x && R.link_rl[l] >= 0.f) {
-                const float4 b0 = ball(row, R.link_ref[l], R.link_rl[l]);
+            const int2 kr = krange[row];
+            const int h = hrow[row];
+            if (h >= 0 && kr.y > kr.x && link_rl[l] >= 0.f) {
+                const float4 b0 = ball(row, link_ref[l], link_rl[l]);
                 if (nsub > 0) {
                     // segment row -> row+1 of the same trajectory: one ball
                     // around both endpoint balls bounds every sample
-                    if (h + 1 < a.H && row + 1 < kRows && sm.hrow[row + 1] >= 0) {
-                        const float4 b1 = ball(row + 1, R.link_ref[l], R.link_rl[l]);
+                    if (h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0) {
+                        const float4 b1 = ball(row + 1, link_ref[l], link_rl[l]);
                         const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
                         const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                         const float mx = b0.x + 0.5f * dx, my = b0.y + 0.5f * dy,
                                     mz = b0.z + 0.5f * dz, rs = fmaxf(b0.w, b1.w) + half;
                         for (int k = kr.x; k < kr.y; ++k)
                             if (!can_cull ||
-                                box_sdf_lb(load_cub(Wd.cub, k), mx, my, mz) - rs - a.eta_w <= kSlack)
+                                box_sdf_lb(cuboid(k), mx, my, mz) - rs - a.eta_w <= kSlack)
                                 m |= 1u << (16 + k - kr.x);
                     }
                 } else {
                     for (int k = kr.x; k < kr.y; ++k)
                         if (!can_cull ||
-                            box_sdf_lb(load_cub(Wd.cub, k), b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack)
+                            box_sdf_lb(cuboid(k), b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack)
                             m |= 1u << (k - kr.x);
                 }
             }
-            sm.wmask[task] = m;
+            wmask[task] = m;
         }
-    }
     __syncthreads();
-
-    // ---- 2c. task lists (dense, appended with one atomic per warp):
-    //          live (pose, link) world tasks and live (pose, link pair) self
-    //          candidates.  Loops run over whole warps so every lane votes.
-    const int lane = tid & 31;
-    if (a.do_world)
-        for (int base = tid - lane; base < kTile * kLinks; base += kThreads) {
-            const int task = base + lane;
-            const int p = task / kLinks, l = task - p * kLinks;
-            bool live = false;
-            if (p < np) {
-                const int row = p + 1, h = sm.hrow[row];
-                uint32_t m;
-                if (nsub > 0)
-                    m = (sm.wmask[row * kLinks + l] >> 16) |
-                        (h > 0 ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u);
-                else
-                    m = sm.wmask[row * kLinks + l] & 0xffffu;
-                live = m != 0u;
-            }
-            const int slot = warp_append(sm.counters + 0, live, lane);
-            if (live) sm.wtask[slot] = (uint16_t)task;
-        }
+    // self level 1: live (pose, link pair) by the link balls (l1 list)
     if (a.do_self)
-        for (int base = tid - lane; base < kTile * R.n_link_pairs; base += kThreads) {
-            const int task = base + lane;
+        for (int b0 = tid - lane; b0 < kTile * R.n_link_pairs; b0 += kThreads) {
+            const int task = b0 + lane;
             const int p = task / R.n_link_pairs, lp = task - p * R.n_link_pairs;
             bool live = false;
             if (p < np) {
-                const int row = p + 1;
-                const int la = R.lp_a[lp], lb = R.lp_b[lp];
-                const float4 A4 = ball(row, R.link_ref[la], R.link_rl[la]);
-                const float4 B4 = ball(row, R.link_ref[lb], R.link_rl[lb]);
+                const int la = slpab[lp] & 0xff, lb = slpab[lp] >> 8;
+                const float4 A4 = ball(p + 1, link_ref[la], link_rl[la]);
+                const float4 B4 = ball(p + 1, link_ref[lb], link_rl[lb]);
                 const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
                 live = !can_cull ||
                        sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s <= kSlack;
             }
-            const int slot = warp_append(sm.counters + 3, live, lane);
-            if (live) sm.l1[slot] = (uint16_t)(p * 32 + lp);
+            const int slot = warp_append(counters + 3, live, lane);
+            if (live) l1[slot] = (uint16_t)(p * 32 + lp);
+        }
+    // live (pose, link) world tasks
+    if (a.do_world)
+        for (int b0 = tid - lane; b0 < kTile * kLinks; b0 += kThreads) {
+            const int task = b0 + lane;
+            const int p = task / kLinks, l = task - p * kLinks;
+            bool live = false;
+            if (p < np) {
+                const int row = p + 1, h = hrow[row];
+                uint32_t m;
+                if (nsub > 0)
+                    m = (wmask[row * kLinks + l] >> 16) |
+                        (h > 0 ? (wmask[(row - 1) * kLinks + l] >> 16) : 0u);
+                else
+                    m = wmask[row * kLinks + l] & 0xffffu;
+                live = m != 0u;
+            }
+            const int slot = warp_append(counters + 0, live, lane);
+            if (live) wtask[slot] = (uint16_t)task;
         }
     __syncthreads();
-    // self level 2: the (<= 4) half-link group pairs of every live link pair
+    // self level 2: live (pose, group pair) among the (<= 4) of each live link pair
     if (a.do_self) {
-        const int n1 = sm.counters[3];
-        for (int base = tid - lane; base < n1 * 4; base += kThreads) {
-            const int it = base + lane;
+        const int n1 = counters[3];
+        for (int b0 = tid - lane; b0 < n1 * 4; b0 += kThreads) {
+            const int it = b0 + lane;
             bool live = false;
             int p = 0, g = 0;
             if (it < n1 * 4) {
-                const int e = sm.l1[it >> 2];
+                const int e = l1[it >> 2];
                 p = e >> 5;
                 const int lp = e & 31;
-                g = R.lp_gp_off[lp] + (it & 3);
-                if (g < R.lp_gp_off[lp + 1]) {
-                    const int row = p + 1;
-                    const int ga = R.gp_a[g], gb = R.gp_b[g];
-                    const float4 A4 = ball(row, R.grp_ref[ga], R.grp_rl[ga]);
-                    const float4 B4 = ball(row, R.grp_ref[gb], R.grp_rl[gb]);
+                g = slpgp[lp] + (it & 3);
+                if (g < slpgp[lp + 1]) {
+                    const int ga = sgpab[g] & 0xff, gb = sgpab[g] >> 8;
+                    const float4 A4 = ball(p + 1, grp_ref[ga], grp_rl[ga]);
+                    const float4 B4 = ball(p + 1, grp_ref[gb], grp_rl[gb]);
                     const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
                     live = !can_cull ||
                            sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - A4.w - B4.w - a.eta_s <= kSlack;
                 }
             }
-            const int slot = warp_append(sm.counters + 1, live, lane);
-            if (live) sm.stask[slot] = (uint16_t)(p * kMaxGroupPairs + g);
+            const int slot = warp_append(counters + 1, live, lane);
+            if (live) stask[slot] = (uint16_t)(p * kMaxGroupPairs + g);
         }
     }
     __syncthreads();
@@ -427,30 +541,30 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
     const float inv_n1 = 1.f / float(nsub + 1);
-    const int n_wtask = sm.counters[0], n_stask = sm.counters[1];
+    const int n_wtask = counters[0], n_stask = counters[1];
     for (int t = tid; t < n_wtask; t += kThreads) {
-        const int task = sm.wtask[t];
+        const int task = wtask[t];
         const int p = task / kLinks, l = task - p * kLinks;
-        const int row = p + 1, h = sm.hrow[row];
-        const int k0 = sm.krange[row].x;
+        const int row = p + 1, h = hrow[row];
+        const int k0 = krange[row].x;
         uint32_t m_own, m_fwd = 0, m_bwd = 0;
         if (nsub > 0) {
-            m_fwd = (h < a.H - 1) ? (sm.wmask[row * kLinks + l] >> 16) : 0u;
-            m_bwd = (h > 0) ? (sm.wmask[(row - 1) * kLinks + l] >> 16) : 0u;
+            m_fwd = (h < a.H - 1) ? (wmask[row * kLinks + l] >> 16) : 0u;
+            m_bwd = (h > 0) ? (wmask[(row - 1) * kLinks + l] >> 16) : 0u;
             m_own = m_fwd | m_bwd;     // a segment ball contains both endpoint balls
         } else {
-            m_own = sm.wmask[row * kLinks + l] & 0xffffu;
+            m_own = wmask[row * kLinks + l] & 0xffffu;
         }
-        const float* crow = sm.ctile + row * cs;
-        uint32_t* orow = sm.wcp + p * WcpS;
+        const float* crow = ctile + row * cs;
+        uint32_t* orow = wcp + p * WcpS;
         float lcost = 0.f;
         for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
             const float cx = crow[3 * s], cy = crow[3 * s + 1], cz = crow[3 * s + 2];
-            const float A = R.sr[s] + a.eta_w;
+            const float A = ssr[s] + a.eta_w;
             Acc acc{0.f, 0.f, 0.f, 0.f};
             for (uint32_t m = m_own; m; m &= m - 1)
-                world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), cx, cy, cz, A, a.eta_w, inv_eta_w,
-                           hoe_w, a.w_w, 1.f, 1.f, acc);
+                world_term(cuboid(k0 + __ffs(m) - 1), cx, cy, cz, A, a.eta_w, inv_eta_w, hoe_w,
+                           a.w_w, 1.f, 1.f, acc);
             if (m_fwd) {                // samples of segment (h, h+1): cost + (1-tau) grad
                 const float* nrow = crow + cs;
                 const float nx = nrow[3 * s], ny = nrow[3 * s + 1], nz = nrow[3 * s + 2];
@@ -459,8 +573,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                     const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
                                 sz = fmaf(tau, nz, omt * cz);
                     for (uint32_t m = m_fwd; m; m &= m - 1)
-                        world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w,
-                                   inv_eta_w, hoe_w, a.w_w, 1.f, omt, acc);
+                        world_term(cuboid(k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w,
+                                   hoe_w, a.w_w, 1.f, omt, acc);
                 }
             }
             if (m_bwd) {                // samples of segment (h-1, h): tau grad only
@@ -471,8 +585,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                     const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
                                 sz = fmaf(tau, cz, omt * qz);
                     for (uint32_t m = m_bwd; m; m &= m - 1)
-                        world_term(load_cub(Wd.cub, k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w,
-                                   inv_eta_w, hoe_w, a.w_w, 0.f, tau, acc);
+                        world_term(cuboid(k0 + __ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w,
+                                   hoe_w, a.w_w, 0.f, tau, acc);
                 }
             }
             lcost += acc.cost;
@@ -480,20 +594,20 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             or_code(orow, 3 * s + 1, acc.gy + 0.f, fcp, rc_cp);
             or_code(orow, 3 * s + 2, acc.gz + 0.f, fcp, rc_cp);
         }
-        sm.wcost[task] = lcost;
+        wcost[task] = lcost;
     }
     // ---- 3b. self tasks: the active sphere pairs of one group pair of one pose
     for (int t = tid; t < n_stask; t += kThreads) {
-        const int task = sm.stask[t];
+        const int task = stask[t];
         const int p = task / kMaxGroupPairs, g = task - p * kMaxGroupPairs;
-        const float* crow = sm.ctile + (p + 1) * cs;
-        for (int k = R.gp_off[g]; k < R.gp_off[g + 1]; ++k) {
-            const int pid = R.gp_pid[k];
-            const int i = R.pair_i[pid], j = R.pair_j[pid];
+        const float* crow = ctile + (p + 1) * cs;
+        for (int k = sgpoff[g]; k < sgpoff[g + 1]; ++k) {
+            const int pid = sgpid[k];
+            const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
             float vx, vy, vz, c;
-            if (self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
-                atomicOr(sm.pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
-                atomicOr(sm.touched + p, (1ull << i) | (1ull << j));
+            if (self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c)) {
+                atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                atomicOr(touched + p, (1ull << i) | (1ull << j));
             }
         }
     }
@@ -504,34 +618,34 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     //          fixed sphere s is its partners in ascending order (independent
     //          of culling and of the task order).
     if (a.do_self) {
-        for (int base = tid - lane; base < np * 64; base += kThreads) {
-            const int it = base + lane;
+        for (int b0 = tid - lane; b0 < np * 64; b0 += kThreads) {
+            const int it = b0 + lane;
             const int p = it >> 6, s = it & 63;
-            const bool live = it < np * 64 && ((sm.touched[p] >> s) & 1ull);
-            const int slot = warp_append(sm.counters + 4, live, lane);
-            if (live) sm.l1[slot] = (uint16_t)it;        // l1 is free again
+            const bool live = it < np * 64 && ((touched[p] >> s) & 1ull);
+            const int slot = warp_append(counters + 4, live, lane);
+            if (live) l1[slot] = (uint16_t)it;        // l1 is free again
         }
         __syncthreads();
-        const int nt = sm.counters[4];
+        const int nt = counters[4];
         for (int t = tid; t < nt; t += kThreads) {
-            const int it = sm.l1[t];
+            const int it = l1[t];
             const int p = it >> 6, s = it & 63;
-            const float* crow = sm.ctile + (p + 1) * cs;
-            const uint32_t* pm = sm.pmask + p * PMW;
+            const float* crow = ctile + (p + 1) * cs;
+            const uint32_t* pm = pmask + p * PMW;
             float gx = 0.f, gy = 0.f, gz = 0.f;
             for (int wd = 0; wd < PMW; ++wd)
                 for (uint32_t m = pm[wd]; m; m &= m - 1) {
                     const int pid = (wd << 5) + __ffs(m) - 1;
-                    const int i = R.pair_i[pid], j = R.pair_j[pid];
+                    const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
                     if (i != s && j != s) continue;
                     float vx, vy, vz, c;
-                    self_pair(crow, i, j, R, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                    self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
                     const float sg = (i == s) ? -1.f : 1.f;
                     gx = fmaf(sg, vx, gx);
                     gy = fmaf(sg, vy, gy);
                     gz = fmaf(sg, vz, gz);
                 }
-            uint32_t* orow = sm.wov + p * WovS;
+            uint32_t* orow = wov + p * WovS;
             or_code(orow, 3 * s + 0, gx + 0.f, fov, rc_ov);
             or_code(orow, 3 * s + 1, gy + 0.f, fov, rc_ov);
             or_code(orow, 3 * s + 2, gz + 0.f, fov, rc_ov);
@@ -541,17 +655,17 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     if (tid < np) {
         const int p = tid;
         float cost = 0.f;
-        for (int l = 0; l < kLinks; ++l) cost += sm.wcost[p * kLinks + l];
-        if (a.do_self && sm.touched[p]) {
-            const float* crow = sm.ctile + (p + 1) * cs;
-            const uint32_t* pm = sm.pmask + p * PMW;
+        for (int l = 0; l < kLinks; ++l) cost += wcost[p * kLinks + l];
+        if (a.do_self && touched[p]) {
+            const float* crow = ctile + (p + 1) * cs;
+            const uint32_t* pm = pmask + p * PMW;
             float scost = 0.f;
             for (int wd = 0; wd < PMW; ++wd)
                 for (uint32_t m = pm[wd]; m; m &= m - 1) {
                     const int pid = (wd << 5) + __ffs(m) - 1;
                     float vx, vy, vz, c;
-                    self_pair(crow, R.pair_i[pid], R.pair_j[pid], R, a.eta_s, inv_eta_s, hoe_s,
-                              a.w_s, vx, vy, vz, c);
+                    self_pair(crow, spij[pid] & 0xff, spij[pid] >> 8, ssr, a.eta_s, inv_eta_s,
+                              hoe_s, a.w_s, vx, vy, vz, c);
                     scost += c;
                 }
             cost += scost;
@@ -567,7 +681,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const int dr = kThreads / Wcp, dw = kThreads % Wcp;
         int r = tid / Wcp, w = tid - (tid / Wcp) * Wcp;
         for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, sm.wcp[r * WcpS + w]);
+            __stcs(dst + i, wcp[r * WcpS + w]);
             r += dr;
             w += dw;
             if (w >= Wcp) {
@@ -582,7 +696,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const int dr = kThreads / Wov, dw = kThreads % Wov;
         int r = tid / Wov, w = tid - (tid / Wov) * Wov;
         for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, sm.wov[r * WovS + w]);
+            __stcs(dst + i, wov[r * WovS + w]);
             r += dr;
             w += dw;
             if (w >= Wov) {
@@ -619,21 +733,6 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
     best_seed[p] = arg;
 }
 
-size_t collision_smem(const RobotDev& R, bool do_world, bool do_self, int Wcp, int Wov) {
-    size_t b = sizeof(uint32_t) * (kRows * kLinks + kRows + (kRows & 1));   // wmask, smask
-    b += sizeof(int2) * kRows + sizeof(int) * kRows;                  // krange, hrow
-    b += sizeof(int) * (kRows & 1) + sizeof(unsigned long long) * kTile;   // touched
-    b += sizeof(float) * kTile * kLinks;                              // wcost
-    b += sizeof(int) * 8;                                             // counters
-    b += sizeof(uint32_t) * kTile * ((R.n_pairs + 31) >> 5);          // pmask
-    b += sizeof(uint16_t) * (kTile * kLinks + kTile * R.lp_gp_off[R.n_link_pairs] + kTile * 64);
-    b = (b + 15) & ~(size_t)15;
-    if (do_world) b += sizeof(uint32_t) * kTile * (Wcp + 1);
-    if (do_self) b += sizeof(uint32_t) * kTile * (Wov + 1);
-    b += sizeof(float) * (size_t)kRows * (R.cols | 1);                // ctile
-    return b + 16;
-}
-
 }  // namespace
 
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
@@ -644,7 +743,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     const int Wos = row_words_of(fos, R.cols);
     const int Wcp = a.do_world ? row_words_of(fcp, R.cols) : 0;
     const int Wov = a.do_self ? row_words_of(fov, R.cols) : 0;
-    const size_t smem = collision_smem(R, a.do_world, a.do_self, Wcp, Wov);
+    const size_t smem = make_layout(R, a.do_world, a.do_self, Wcp, Wov).total;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
