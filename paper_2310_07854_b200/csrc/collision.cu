@@ -37,6 +37,8 @@
 // exactly 0; surviving terms are accumulated in the same order with and
 // without culling, so VAPR_OPT_CULL on and off give bit-identical results
 // (tests/test_gpu_parity.py::test_cull_is_exact).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -44,9 +46,9 @@ namespace vapr {
 
 namespace {
 
-constexpr int kTile = 64;           // poses per CTA
+constexpr int kTile = 32;           // poses per tile
 constexpr int kRows = kTile + 2;    // with the two halo poses
-constexpr int kWarps = 8;
+constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kWorldCache = 4;      // distinct worlds whose cuboids a tile caches
 constexpr int kMaxLoads = 4;        // 16-byte loads in flight per thread when decoding
@@ -229,7 +231,7 @@ __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, i
     return L;
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
 collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const Fmt fos,
                  const Fmt fcp, const Fmt fov, const CollisionArgs a, int Wos, int Wcp,
                  int Wov) {
@@ -266,15 +268,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     const int cols = R.cols;
     const int cs = cols | 1;                       // odd fp32 row stride
     const long long P = (long long)a.B * a.H;
-    const long long p0 = (long long)blockIdx.x * kTile;
-    const int np = (int)min((long long)kTile, P - p0);
+    const long long n_tiles = (P + kTile - 1) / kTile;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int WcpS = Wcp + 1, WovS = Wov + 1;
     const int PMW = L.pmw;
 
-    // ---- 0. stage the divergently-indexed tables; rows' step index and world
-    if (tid < 8) counters[tid] = 0;
+    // ---- 0. stage the divergently-indexed tables (once per persistent CTA)
     for (int i = tid; i < R.n_spheres; i += kThreads) ssr[i] = R.sr[i];
     if (tid < kLinks) {
         link_rl[tid] = R.link_rl[tid];
@@ -296,6 +296,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             slpab[i] = (uint16_t)(R.lp_a[i] | (R.lp_b[i] << 8));
         for (int i = tid; i <= R.n_link_pairs; i += kThreads) slpgp[i] = R.lp_gp_off[i];
     }
+    __syncthreads();
+
+    for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const long long p0 = tile * kTile;
+    const int np = (int)min((long long)kTile, P - p0);
+    if (tid < 8) counters[tid] = 0;
+    // rows' step index h and world
     for (int row = tid; row < kRows; row += kThreads) {
         const long long pg = p0 - 1 + row;
         int hh = -1, wi = -1;
@@ -311,28 +318,39 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         wslot[row] = wi;
     }
     __syncthreads();
-    // cuboid cache: the distinct worlds of the tile's rows (trajectories are
-    // contiguous, so a tile rarely sees more than two); a row whose world does
-    // not fit reads its cuboids from global memory (index + kUncached).
-    if (a.do_world && tid == 0) {
-        int nw = 0;
-        for (int row = 0; row < kRows; ++row) {
-            const int wi = wslot[row];
-            int slot = -1;
-            if (wi >= 0) {
-                for (int k = 0; k < nw; ++k)
-                    if (l1[k] == wi) slot = k;
-                if (slot < 0 && nw < kWorldCache) {
-                    l1[nw] = (uint16_t)wi;      // l1 doubles as scratch here
-                    slot = nw++;
-                }
-            }
-            wslot[row] = (wi >= 0 && slot < 0) ? -2 - wi : slot;
-        }
-        counters[5] = nw;
-    }
-    __syncthreads();
+    // cuboid cache: every run of consecutive rows with the same world gets
+    // the next cache slot (trajectories are contiguous, so a tile sees one to
+    // three runs); rows beyond kWorldCache runs read their cuboids from
+    // global memory (index + kUncached).
     if (a.do_world) {
+        int myslot = -1, mywi = -1;
+        bool starts = false;
+        if (tid < kRows) {
+            mywi = wslot[tid];
+            int runs = 0, prev = -1;
+            for (int r = 0; r <= tid; ++r) {
+                const int w = wslot[r];
+                if (w >= 0 && w != prev) ++runs;
+                if (w >= 0) prev = w;
+            }
+            if (mywi >= 0) {
+                myslot = runs - 1;
+                int pw = -1;
+                for (int r = tid - 1; r >= 0 && pw < 0; --r) pw = wslot[r];
+                starts = (pw != mywi);
+            }
+            if (tid == kRows - 1) counters[5] = min(runs, kWorldCache);
+        }
+        __syncthreads();
+        if (tid < kRows) {
+            if (mywi >= 0 && myslot < kWorldCache) {
+                wslot[tid] = myslot;
+                if (starts) l1[myslot] = (uint16_t)mywi;     // l1 doubles as scratch here
+            } else {
+                wslot[tid] = (mywi >= 0) ? -2 - mywi : -1;
+            }
+        }
+        __syncthreads();
         const int nw = counters[5];
         for (int i = tid; i < nw * kMaxCuboids * 4; i += kThreads) {
             const int k = i / (kMaxCuboids * 4), rest = i - k * kMaxCuboids * 4;
@@ -705,6 +723,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             }
         }
     }
+    __syncthreads();
+    }  // tile loop
 }
 
 __global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
@@ -747,7 +767,14 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long long grid = (P + kTile - 1) / kTile;
+    // persistent CTAs: as many as fit on the device (the robot tables are
+    // staged once per CTA), each looping over tiles
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, collision_kernel, kThreads, smem);
+    const long long tiles = (P + kTile - 1) / kTile;
+    const long long grid = std::min<long long>(tiles, (long long)sms * std::max(per_sm, 1));
     collision_kernel<<<(unsigned)grid, kThreads, smem, s>>>(R, W, fos, fcp, fov, a, Wos, Wcp,
                                                             Wov);
     return cudaGetLastError();
