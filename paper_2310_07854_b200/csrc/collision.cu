@@ -50,9 +50,6 @@ constexpr int kTile = 32;           // poses per tile
 constexpr int kRows = kTile + 2;    // with the two halo poses
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kWorldCache = 4;      // distinct worlds whose cuboids a tile caches
-constexpr int kMaxLoads = 4;        // 16-byte loads in flight per thread when decoding
-constexpr int kUncached = 1 << 20;  // cuboid index offset marking a global (uncached) cuboid
 constexpr float kSlack = 1e-4f;
 
 struct Acc {
@@ -136,6 +133,18 @@ __device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt
     atomicOr(row + w, c << ((e - w * f.pf) * f.t));
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Append to a shared list with one atomic per warp; every lane of the warp
 // must call it.  Returns the lane's slot (meaningful only when pred).
 __device__ __forceinline__ int warp_append(int* counter, bool pred, int lane) {
@@ -186,12 +195,12 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 // Shared-memory carve-up (sizes depend on the robot and the formats).
 struct Layout {
     int pmw, ngp, npairs;
-    unsigned cub, touched, krange, wmask, hrow, wslot, wcost, counters, pmask, sr, rl, ref, pij,
+    unsigned stage, swid, touched, krange, wmask, hrow, wslot, wcost, counters, pmask, sr, rl, ref, pij,
         gpid, gpoff, gpab, lpab, lpgp, wtask, stask, l1, wcp, wov, ctile, total;
 };
 
 __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, int do_self,
-                                              int Wcp, int Wov) {
+                                              int Wos, int Wcp, int Wov) {
     Layout L{};
     L.pmw = (R.n_pairs + 31) >> 5;
     L.ngp = R.lp_gp_off[R.n_link_pairs];
@@ -203,7 +212,8 @@ __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, i
         o += bytes;
         return at;
     };
-    L.cub = take(sizeof(float4) * 4 * kMaxCuboids * kWorldCache, 16);
+    L.stage = take(sizeof(uint32_t) * 2 * kRows * Wos, 16);
+    L.swid = take(sizeof(int) * 2 * kRows, 4);
     L.touched = take(sizeof(unsigned long long) * kTile, 8);
     L.krange = take(sizeof(int2) * kRows, 8);
     L.wmask = take(sizeof(uint32_t) * kRows * kLinks, 4);
@@ -237,8 +247,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                  int Wov) {
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
-    const Layout L = make_layout(R, a.do_world, a.do_self, Wcp, Wov);
-    Cub* scub = reinterpret_cast<Cub*>(base + L.cub);            // [kWorldCache * 16]
+    const Layout L = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov);
+    uint32_t* stage = reinterpret_cast<uint32_t*>(base + L.stage);   // [2][kRows * Wos] packed rows
+    int* swid = reinterpret_cast<int*>(base + L.swid);              // [2][kRows] world index
     unsigned long long* touched = reinterpret_cast<unsigned long long*>(base + L.touched);
     int2* krange = reinterpret_cast<int2*>(base + L.krange);     // cuboid range of each row
     uint32_t* wmask = reinterpret_cast<uint32_t*>(base + L.wmask);
@@ -298,123 +309,84 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     }
     __syncthreads();
 
+    // ---- cp.async prefetch of a tile's packed rows (p0-1 .. p0+np, clamped)
+    //      and of its rows' world indices into stage buffer `buf`, so the
+    //      global-memory latency of tile t+1 overlaps the compute of tile t.
+    const int stage_words = kRows * Wos;
+    auto prefetch = [&](long long tl, int buf) {
+        if (tl >= n_tiles) return;
+        const long long q0 = tl * kTile;
+        const int nq_ = (int)min((long long)kTile, P - q0);
+        const long long rlo = max(q0 - 1, 0LL), rhi = min(q0 + nq_ + 1, P);
+        const int nq = int(rhi - rlo) * (Wos / 4);
+        const uint4* src = reinterpret_cast<const uint4*>(a.os + rlo * Wos);
+        uint4* dst = reinterpret_cast<uint4*>(stage + buf * stage_words);
+        for (int q = tid; q < nq; q += kThreads) cp_async16(dst + q, src + q);
+        if (a.do_world)
+            for (int row = tid; row < kRows; row += kThreads) {
+                const long long pg = q0 - 1 + row;
+                if (pg >= 0 && pg < P) cp_async4(swid + buf * kRows + row, a.world_idx + pg / a.H);
+            }
+    };
+    prefetch(blockIdx.x, 0);
+    cp_async_commit();
+    int buf = 0;
+
     for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const long long p0 = tile * kTile;
     const int np = (int)min((long long)kTile, P - p0);
+    prefetch(tile + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait_1();                 // this thread's copies of the current tile
     if (tid < 8) counters[tid] = 0;
-    // rows' step index h and world
+    __syncthreads();                   // ... and everyone else's
+    // rows' step index h and cuboid range
     for (int row = tid; row < kRows; row += kThreads) {
         const long long pg = p0 - 1 + row;
-        int hh = -1, wi = -1;
+        int hh = -1;
+        int2 kr = make_int2(0, 0);
         if (pg >= 0 && pg < P) {
-            const long long b = pg / a.H;      // the only 64-bit divisions: once per row
-            hh = int(pg - b * a.H);
+            hh = int(pg % a.H);                // 64-bit division: once per row
             if (a.do_world) {
-                wi = __ldg(a.world_idx + b);
-                if (wi < 0 || wi >= Wd.n_worlds) wi = -1;
+                const int wi = swid[buf * kRows + row];
+                if (wi >= 0 && wi < Wd.n_worlds) kr = make_int2(__ldg(Wd.off + wi), __ldg(Wd.off + wi + 1));
             }
         }
         hrow[row] = hh;
-        wslot[row] = wi;
-    }
-    __syncthreads();
-    // cuboid cache: every run of consecutive rows with the same world gets
-    // the next cache slot (trajectories are contiguous, so a tile sees one to
-    // three runs); rows beyond kWorldCache runs read their cuboids from
-    // global memory (index + kUncached).
-    if (a.do_world) {
-        int myslot = -1, mywi = -1;
-        bool starts = false;
-        if (tid < kRows) {
-            mywi = wslot[tid];
-            int runs = 0, prev = -1;
-            for (int r = 0; r <= tid; ++r) {
-                const int w = wslot[r];
-                if (w >= 0 && w != prev) ++runs;
-                if (w >= 0) prev = w;
-            }
-            if (mywi >= 0) {
-                myslot = runs - 1;
-                int pw = -1;
-                for (int r = tid - 1; r >= 0 && pw < 0; --r) pw = wslot[r];
-                starts = (pw != mywi);
-            }
-            if (tid == kRows - 1) counters[5] = min(runs, kWorldCache);
-        }
-        __syncthreads();
-        if (tid < kRows) {
-            if (mywi >= 0 && myslot < kWorldCache) {
-                wslot[tid] = myslot;
-                if (starts) l1[myslot] = (uint16_t)mywi;     // l1 doubles as scratch here
-            } else {
-                wslot[tid] = (mywi >= 0) ? -2 - mywi : -1;
-            }
-        }
-        __syncthreads();
-        const int nw = counters[5];
-        for (int i = tid; i < nw * kMaxCuboids * 4; i += kThreads) {
-            const int k = i / (kMaxCuboids * 4), rest = i - k * kMaxCuboids * 4;
-            const int wi = l1[k];
-            const int c0 = __ldg(Wd.off + wi), c1 = __ldg(Wd.off + wi + 1);
-            if (c0 + (rest >> 2) < c1)
-                reinterpret_cast<float4*>(scub)[i] = __ldg(Wd.cub + 4 * (c0 + (rest >> 2)) + (rest & 3));
-        }
-        for (int row = tid; row < kRows; row += kThreads) {
-            const int sl = wslot[row];
-            int2 kr = make_int2(0, 0);
-            if (sl >= 0) {
-                const int wi = l1[sl];
-                kr = make_int2(sl * kMaxCuboids,
-                               sl * kMaxCuboids + __ldg(Wd.off + wi + 1) - __ldg(Wd.off + wi));
-            } else if (sl <= -2) {
-                const int wi = -2 - sl;
-                kr = make_int2(kUncached + __ldg(Wd.off + wi), kUncached + __ldg(Wd.off + wi + 1));
-            }
-            krange[row] = kr;
-        }
+        krange[row] = kr;
     }
 
-    // ---- 1. load the packed rows p0-1 .. p0+np (all loads in flight), decode
+    // ---- 1. decode the staged packed rows into the FP32 tile
     const long long r_lo = max(p0 - 1, 0LL);
     const long long r_hi = min(p0 + np + 1, P);           // exclusive
     const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
     uint32_t amax = 0;
     {
-        const int Q = Wos / 4;                            // 16-byte groups per row
-        const int nq = int(r_hi - r_lo) * Q;
-        const uint4* src = reinterpret_cast<const uint4*>(a.os + r_lo * Wos);
-        for (int q0 = 0; q0 < nq; q0 += kThreads * kMaxLoads) {
-            uint4 v[kMaxLoads];
+        const int nw = int(r_hi - r_lo) * Wos;
+        const uint32_t* sw = stage + buf * stage_words;
+        const int dr = kThreads / Wos, dw = kThreads % Wos;
+        int r = tid / Wos, w = tid - (tid / Wos) * Wos;
+        with_pf(fos.pf, [&](auto Pc) {
+            constexpr int PF = decltype(Pc)::value;
+            for (int i = tid; i < nw; i += kThreads) {
+                float x[PF];
+                decode_word_t<PF>(sw[i], x, fos);
+                float* drow = ctile + (row_off + r) * cs;
+                const int e0 = w * PF;
 #pragma unroll
-            for (int k = 0; k < kMaxLoads; ++k) {
-                const int q = q0 + k * kThreads + tid;
-                if (q < nq) v[k] = __ldcs(src + q);
-            }
-            with_pf(fos.pf, [&](auto Pc) {
-                constexpr int PF = decltype(Pc)::value;
-#pragma unroll
-                for (int k = 0; k < kMaxLoads; ++k) {
-                    const int q = q0 + k * kThreads + tid;
-                    if (q < nq) {
-                        const int r = q / Q, g = q - r * Q;
-                        float* drow = ctile + (row_off + r) * cs;
-                        const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-                        for (int j4 = 0; j4 < 4; ++j4) {
-                            float x[PF];
-                            decode_word_t<PF>(w4[j4], x, fos);
-                            const int e0 = (4 * g + j4) * PF;
-#pragma unroll
-                            for (int j = 0; j < PF; ++j)
-                                if (e0 + j < cols) {
-                                    drow[e0 + j] = x[j];
-                                    amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
-                                }
-                        }
+                for (int j = 0; j < PF; ++j)
+                    if (e0 + j < cols) {
+                        drow[e0 + j] = x[j];
+                        amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
                     }
+                r += dr;
+                w += dw;
+                if (w >= Wos) {
+                    w -= Wos;
+                    ++r;
                 }
-            });
-        }
+            }
+        });
     }
     amax = __reduce_max_sync(0xffffffffu, amax);
     if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(counters + 2), amax);
@@ -448,11 +420,11 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         const float* c = ctile + row * cs + 3 * ref;
         return make_float4(c[0], c[1], c[2], rl + margin);
     };
+    // cuboids are read through L1 (a problem's world is shared by all its
+    // seeds' tiles, so the lines stay resident)
     auto cuboid = [&](int k) -> Cub {
-        if (k < kUncached) return scub[k];
-        const int g = k - kUncached;
-        return Cub{__ldg(Wd.cub + 4 * g), __ldg(Wd.cub + 4 * g + 1), __ldg(Wd.cub + 4 * g + 2),
-                   __ldg(Wd.cub + 4 * g + 3)};
+        return Cub{__ldg(Wd.cub + 4 * k), __ldg(Wd.cub + 4 * k + 1), __ldg(Wd.cub + 4 * k + 2),
+                   __ldg(Wd.cub + 4 * k + 3)};
     };
 
     // ---- 2. world cull masks per (row, link): bits 0-15 pose (discrete),
@@ -724,7 +696,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         }
     }
     __syncthreads();
+    buf ^= 1;
     }  // tile loop
+    cp_async_wait_all();
 }
 
 __global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
@@ -763,7 +737,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     const int Wos = row_words_of(fos, R.cols);
     const int Wcp = a.do_world ? row_words_of(fcp, R.cols) : 0;
     const int Wov = a.do_self ? row_words_of(fov, R.cols) : 0;
-    const size_t smem = make_layout(R, a.do_world, a.do_self, Wcp, Wov).total;
+    const size_t smem = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov).total;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
