@@ -199,8 +199,18 @@ struct Layout {
         gpid, gpoff, gpab, lpab, lpgp, wtask, stask, l1, wcp, wov, ctile, total;
 };
 
+// FP32 tile row stride: a multiple of 4 floats (16-byte vector stores), at
+// least one packed row's worth of decoded elements, and not a multiple of 32
+// (rows of one column spread over several banks).
+__host__ __device__ inline int tile_stride(int cols, int Wos, int pf) {
+    int cs = ((cols + 3) & ~3);
+    if (cs < Wos * pf) cs = Wos * pf;
+    if (cs % 32 == 0) cs += 4;
+    return cs;
+}
+
 __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, int do_self,
-                                              int Wos, int Wcp, int Wov) {
+                                              int Wos, int Wcp, int Wov, int pfos) {
     Layout L{};
     L.pmw = (R.n_pairs + 31) >> 5;
     L.ngp = R.lp_gp_off[R.n_link_pairs];
@@ -234,9 +244,9 @@ __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, i
     L.wtask = take(sizeof(uint16_t) * kTile * kLinks, 2);
     L.stask = take(sizeof(uint16_t) * kTile * (L.ngp > 0 ? L.ngp : 1), 2);
     L.l1 = take(sizeof(uint16_t) * kTile * 64, 2);
-    L.wcp = take(do_world ? sizeof(uint32_t) * kTile * (Wcp + 1) : 0u, 16);
-    L.wov = take(do_self ? sizeof(uint32_t) * kTile * (Wov + 1) : 0u, 16);
-    L.ctile = take(sizeof(float) * kRows * (R.cols | 1), 16);
+    L.wcp = take(do_world ? sizeof(uint32_t) * kTile * Wcp : 0u, 16);
+    L.wov = take(do_self ? sizeof(uint32_t) * kTile * Wov : 0u, 16);
+    L.ctile = take(sizeof(float) * kRows * tile_stride(R.cols, Wos, pfos), 16);
     L.total = o + 16;
     return L;
 }
@@ -247,7 +257,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
                  int Wov) {
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
-    const Layout L = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov);
+    const Layout L = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov, fos.pf);
     uint32_t* stage = reinterpret_cast<uint32_t*>(base + L.stage);   // [2][kRows * Wos] packed rows
     int* swid = reinterpret_cast<int*>(base + L.swid);              // [2][kRows] world index
     unsigned long long* touched = reinterpret_cast<unsigned long long*>(base + L.touched);
@@ -277,12 +287,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     float* ctile = reinterpret_cast<float*>(base + L.ctile);
 
     const int cols = R.cols;
-    const int cs = cols | 1;                       // odd fp32 row stride
+    const int cs = tile_stride(cols, Wos, fos.pf);  // fp32 tile row stride
     const long long P = (long long)a.B * a.H;
     const long long n_tiles = (P + kTile - 1) / kTile;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int WcpS = Wcp + 1, WovS = Wov + 1;
+    const int WcpS = Wcp, WovS = Wov;              // packed output row strides (16 B multiples)
     const int PMW = L.pmw;
 
     // ---- 0. stage the divergently-indexed tables (once per persistent CTA)
@@ -360,44 +370,49 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     const long long r_lo = max(p0 - 1, 0LL);
     const long long r_hi = min(p0 + np + 1, P);           // exclusive
     const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
-    uint32_t amax = 0;
+    float amax = 0.f;
     {
-        const int nw = int(r_hi - r_lo) * Wos;
-        const uint32_t* sw = stage + buf * stage_words;
-        const int dr = kThreads / Wos, dw = kThreads % Wos;
-        int r = tid / Wos, w = tid - (tid / Wos) * Wos;
+        // one thread per 16-byte group of 4 packed words (4 PF elements,
+        // starting at a multiple of 4): one 16-byte shared load, 4 PF decodes,
+        // PF 16-byte shared stores
+        const int Q = Wos / 4;
+        const int nq = int(r_hi - r_lo) * Q;
+        const uint4* sw = reinterpret_cast<const uint4*>(stage + buf * stage_words);
         with_pf(fos.pf, [&](auto Pc) {
             constexpr int PF = decltype(Pc)::value;
-            for (int i = tid; i < nw; i += kThreads) {
-                float x[PF];
-                decode_word_t<PF>(sw[i], x, fos);
-                float* drow = ctile + (row_off + r) * cs;
-                const int e0 = w * PF;
+            for (int q = tid; q < nq; q += kThreads) {
+                const int r = q / Q, g = q - r * Q;
+                const uint4 v = sw[q];
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                float x[4 * PF];
 #pragma unroll
-                for (int j = 0; j < PF; ++j)
-                    if (e0 + j < cols) {
-                        drow[e0 + j] = x[j];
-                        amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
-                    }
-                r += dr;
-                w += dw;
-                if (w >= Wos) {
-                    w -= Wos;
-                    ++r;
+                for (int j4 = 0; j4 < 4; ++j4) decode_word_t<PF>(w4[j4], x + j4 * PF, fos);
+                float4* d4 = reinterpret_cast<float4*>(ctile + (row_off + r) * cs + 4 * PF * g);
+#pragma unroll
+                for (int j = 0; j < PF; ++j) {
+                    d4[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(x[4 * j]), fabsf(x[4 * j + 1])),
+                                             fmaxf(fabsf(x[4 * j + 2]), fabsf(x[4 * j + 3]))));
                 }
             }
         });
     }
-    amax = __reduce_max_sync(0xffffffffu, amax);
-    if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(counters + 2), amax);
+    {
+        uint32_t ab = __float_as_uint(amax);            // non-negative: bits are monotone
+        ab = __reduce_max_sync(0xffffffffu, ab);
+        if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(counters + 2), ab);
+    }
     if (a.do_world)
-        for (int i = tid; i < kTile * WcpS; i += kThreads) wcp[i] = 0u;
+        for (int i = tid; i < kTile * WcpS / 4; i += kThreads)
+            reinterpret_cast<uint4*>(wcp)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (a.do_self) {
-        for (int i = tid; i < kTile * WovS; i += kThreads) wov[i] = 0u;
+        for (int i = tid; i < kTile * WovS / 4; i += kThreads)
+            reinterpret_cast<uint4*>(wov)[i] = make_uint4(0u, 0u, 0u, 0u);
         for (int i = tid; i < kTile * PMW; i += kThreads) pmask[i] = 0u;
         if (tid < kTile) touched[tid] = 0ull;
     }
     for (int i = tid; i < kTile * kLinks; i += kThreads) wcost[i] = 0.f;
+    for (int i = tid; i < kRows * kLinks; i += kThreads) wmask[i] = 0u;
     __syncthreads();
 
     // Quantisation margin: a decoded coordinate y of an FK value x satisfies
@@ -430,36 +445,36 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     // ---- 2. world cull masks per (row, link): bits 0-15 pose (discrete),
     //         bits 16-31 segment row -> row+1 (swept)
     const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
+    // One task per (row, cuboid): the cuboid is loaded once and tested
+    // against the 9 link balls; the (rare) live bits are ORed into wmask.
     if (a.do_world)
-        for (int task = tid; task < kRows * kLinks; task += kThreads) {
-            const int row = task / kLinks, l = task - row * kLinks;
-            uint32_t m = 0;
+        for (int task = tid; task < kRows * kMaxCuboids; task += kThreads) {
+            const int row = task / kMaxCuboids, kk = task - row * kMaxCuboids;
             const int2 kr = krange[row];
             const int h = hrow[row];
-            if (h >= 0 && kr.y > kr.x && link_rl[l] >= 0.f) {
+            if (h < 0 || kk >= kr.y - kr.x) continue;
+            const Cub cb = cuboid(kr.x + kk);
+            const bool seg = nsub > 0 && h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0;
+            for (int l = 0; l < kLinks; ++l) {
+                if (link_rl[l] < 0.f) continue;
                 const float4 b0 = ball(row, link_ref[l], link_rl[l]);
+                bool live;
                 if (nsub > 0) {
+                    if (!seg) continue;
                     // segment row -> row+1 of the same trajectory: one ball
                     // around both endpoint balls bounds every sample
-                    if (h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0) {
-                        const float4 b1 = ball(row + 1, link_ref[l], link_rl[l]);
-                        const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
-                        const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                        const float mx = b0.x + 0.5f * dx, my = b0.y + 0.5f * dy,
-                                    mz = b0.z + 0.5f * dz, rs = fmaxf(b0.w, b1.w) + half;
-                        for (int k = kr.x; k < kr.y; ++k)
-                            if (!can_cull ||
-                                box_sdf_lb(cuboid(k), mx, my, mz) - rs - a.eta_w <= kSlack)
-                                m |= 1u << (16 + k - kr.x);
-                    }
+                    const float4 b1 = ball(row + 1, link_ref[l], link_rl[l]);
+                    const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
+                    const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    live = !can_cull || box_sdf_lb(cb, b0.x + 0.5f * dx, b0.y + 0.5f * dy,
+                                                   b0.z + 0.5f * dz) -
+                                                fmaxf(b0.w, b1.w) - half - a.eta_w <= kSlack;
+                    if (live) atomicOr(wmask + row * kLinks + l, 1u << (16 + kk));
                 } else {
-                    for (int k = kr.x; k < kr.y; ++k)
-                        if (!can_cull ||
-                            box_sdf_lb(cuboid(k), b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack)
-                            m |= 1u << (k - kr.x);
+                    live = !can_cull || box_sdf_lb(cb, b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack;
+                    if (live) atomicOr(wmask + row * kLinks + l, 1u << kk);
                 }
             }
-            wmask[task] = m;
         }
     __syncthreads();
     // self level 1: live (pose, link pair) by the link balls (l1 list)
@@ -664,36 +679,14 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     }
     __syncthreads();
 
-    // ---- 5. coalesced packed stores
+    // ---- 5. coalesced 16-byte packed stores (tile rows are contiguous in HBM)
     if (a.do_world) {
-        const int n = np * Wcp;
-        uint32_t* dst = a.cp + p0 * Wcp;
-        const int dr = kThreads / Wcp, dw = kThreads % Wcp;
-        int r = tid / Wcp, w = tid - (tid / Wcp) * Wcp;
-        for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, wcp[r * WcpS + w]);
-            r += dr;
-            w += dw;
-            if (w >= Wcp) {
-                w -= Wcp;
-                ++r;
-            }
-        }
+        uint4* dst = reinterpret_cast<uint4*>(a.cp + p0 * Wcp);
+        for (int i = tid; i < np * Wcp / 4; i += kThreads) __stcs(dst + i, reinterpret_cast<const uint4*>(wcp)[i]);
     }
     if (a.do_self) {
-        const int n = np * Wov;
-        uint32_t* dst = a.ov + p0 * Wov;
-        const int dr = kThreads / Wov, dw = kThreads % Wov;
-        int r = tid / Wov, w = tid - (tid / Wov) * Wov;
-        for (int i = tid; i < n; i += kThreads) {
-            __stcs(dst + i, wov[r * WovS + w]);
-            r += dr;
-            w += dw;
-            if (w >= Wov) {
-                w -= Wov;
-                ++r;
-            }
-        }
+        uint4* dst = reinterpret_cast<uint4*>(a.ov + p0 * Wov);
+        for (int i = tid; i < np * Wov / 4; i += kThreads) __stcs(dst + i, reinterpret_cast<const uint4*>(wov)[i]);
     }
     __syncthreads();
     buf ^= 1;
@@ -737,7 +730,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     const int Wos = row_words_of(fos, R.cols);
     const int Wcp = a.do_world ? row_words_of(fcp, R.cols) : 0;
     const int Wov = a.do_self ? row_words_of(fov, R.cols) : 0;
-    const size_t smem = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov).total;
+    const size_t smem = make_layout(R, a.do_world, a.do_self, Wos, Wcp, Wov, fos.pf).total;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
