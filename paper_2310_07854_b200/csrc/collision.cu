@@ -56,6 +56,10 @@ struct Acc {
     float cost, gx, gy, gz;
 };
 
+#ifdef VAPR_PHASES
+__device__ unsigned long long g_phase_cycles[16];
+#endif
+
 struct Cub {
     float4 q0, q1, q2, q3;   // R^T (9), t (3), h (3), pad
 };
@@ -69,9 +73,9 @@ __device__ __forceinline__ float box_sdf_lb(const Cub& b, float cx, float cy, fl
     const float pz = fmaf(b.q1.z, dx, fmaf(b.q1.w, dy, b.q2.x * dz));
     const float ux = fabsf(px) - b.q3.x, uy = fabsf(py) - b.q3.y, uz = fabsf(pz) - b.q3.z;
     const float umax = fmaxf(ux, fmaxf(uy, uz));
-    if (umax <= 0.f) return umax;
     const float ox = fmaxf(ux, 0.f), oy = fmaxf(uy, 0.f), oz = fmaxf(uz, 0.f);
-    return sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
+    const float out = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
+    return (umax <= 0.f) ? umax : out;          // branch-free: independent tests interleave
 }
 
 // One sphere-vs-cuboid term: adds cw * w * h(phi) to the cost and
@@ -251,7 +255,7 @@ __host__ __device__ inline Layout make_layout(const RobotDev& R, int do_world, i
     return L;
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 6)
 collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const Fmt fos,
                  const Fmt fcp, const Fmt fov, const CollisionArgs a, int Wos, int Wcp,
                  int Wov) {
@@ -342,6 +346,19 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     cp_async_commit();
     int buf = 0;
 
+#ifdef VAPR_PHASES
+    __shared__ unsigned long long ph_acc[16];
+    if (tid < 16) ph_acc[tid] = 0ull;
+    long long ph_t = clock64();
+#define VAPR_PHASE(i)                                   \
+    if (tid == 0) {                                     \
+        const long long t_ = clock64();                 \
+        ph_acc[i] += (unsigned long long)(t_ - ph_t);   \
+        ph_t = t_;                                      \
+    }
+#else
+#define VAPR_PHASE(i)
+#endif
     for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const long long p0 = tile * kTile;
     const int np = (int)min((long long)kTile, P - p0);
@@ -350,6 +367,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     cp_async_wait_1();                 // this thread's copies of the current tile
     if (tid < 8) counters[tid] = 0;
     __syncthreads();                   // ... and everyone else's
+    VAPR_PHASE(1);
     // rows' step index h and cuboid range
     for (int row = tid; row < kRows; row += kThreads) {
         const long long pg = p0 - 1 + row;
@@ -364,6 +382,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         }
         hrow[row] = hh;
         krange[row] = kr;
+        if (kr.y > kr.x) atomicMax(counters + 6, kr.y - kr.x);
     }
 
     // ---- 1. decode the staged packed rows into the FP32 tile
@@ -414,6 +433,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     for (int i = tid; i < kTile * kLinks; i += kThreads) wcost[i] = 0.f;
     for (int i = tid; i < kRows * kLinks; i += kThreads) wmask[i] = 0u;
     __syncthreads();
+    VAPR_PHASE(2);
 
     // Quantisation margin: a decoded coordinate y of an FK value x satisfies
     // |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) (half an ulp; the subnormal
@@ -445,38 +465,41 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
     // ---- 2. world cull masks per (row, link): bits 0-15 pose (discrete),
     //         bits 16-31 segment row -> row+1 (swept)
     const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
-    // One task per (row, cuboid): the cuboid is loaded once and tested
-    // against the 9 link balls; the (rare) live bits are ORed into wmask.
-    if (a.do_world)
-        for (int task = tid; task < kRows * kMaxCuboids; task += kThreads) {
-            const int row = task / kMaxCuboids, kk = task - row * kMaxCuboids;
+    // One task per (row, cuboid, link) triple, cuboid-major so the lanes of
+    // a warp mostly share the cuboid (an L1 broadcast); the (rare) live bits
+    // are ORed into wmask.
+    if (a.do_world) {
+        const int kmax = counters[6];
+        const int ntask = kRows * kLinks * kmax;
+        for (int task = tid; task < ntask; task += kThreads) {
+            const int kk = task / (kRows * kLinks);
+            const int rl = task - kk * (kRows * kLinks);
+            const int row = rl / kLinks, l = rl - row * kLinks;
             const int2 kr = krange[row];
             const int h = hrow[row];
-            if (h < 0 || kk >= kr.y - kr.x) continue;
+            if (h < 0 || kk >= kr.y - kr.x || link_rl[l] < 0.f) continue;
             const Cub cb = cuboid(kr.x + kk);
-            const bool seg = nsub > 0 && h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0;
-            for (int l = 0; l < kLinks; ++l) {
-                if (link_rl[l] < 0.f) continue;
-                const float4 b0 = ball(row, link_ref[l], link_rl[l]);
-                bool live;
-                if (nsub > 0) {
-                    if (!seg) continue;
-                    // segment row -> row+1 of the same trajectory: one ball
-                    // around both endpoint balls bounds every sample
-                    const float4 b1 = ball(row + 1, link_ref[l], link_rl[l]);
-                    const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
-                    const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    live = !can_cull || box_sdf_lb(cb, b0.x + 0.5f * dx, b0.y + 0.5f * dy,
-                                                   b0.z + 0.5f * dz) -
-                                                fmaxf(b0.w, b1.w) - half - a.eta_w <= kSlack;
-                    if (live) atomicOr(wmask + row * kLinks + l, 1u << (16 + kk));
-                } else {
-                    live = !can_cull || box_sdf_lb(cb, b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack;
-                    if (live) atomicOr(wmask + row * kLinks + l, 1u << kk);
-                }
+            const float4 b0 = ball(row, link_ref[l], link_rl[l]);
+            if (nsub > 0) {
+                if (!(h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0)) continue;
+                // segment row -> row+1 of the same trajectory: one ball
+                // around both endpoint balls bounds every sample
+                const float4 b1 = ball(row + 1, link_ref[l], link_rl[l]);
+                const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
+                const float half = 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                const bool live =
+                    !can_cull || box_sdf_lb(cb, b0.x + 0.5f * dx, b0.y + 0.5f * dy, b0.z + 0.5f * dz) -
+                                         fmaxf(b0.w, b1.w) - half - a.eta_w <= kSlack;
+                if (live) atomicOr(wmask + row * kLinks + l, 1u << (16 + kk));
+            } else {
+                const bool live =
+                    !can_cull || box_sdf_lb(cb, b0.x, b0.y, b0.z) - b0.w - a.eta_w <= kSlack;
+                if (live) atomicOr(wmask + row * kLinks + l, 1u << kk);
             }
         }
+    }
     __syncthreads();
+    VAPR_PHASE(3);
     // self level 1: live (pose, link pair) by the link balls (l1 list)
     if (a.do_self)
         for (int b0 = tid - lane; b0 < kTile * R.n_link_pairs; b0 += kThreads) {
@@ -514,6 +537,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             if (live) wtask[slot] = (uint16_t)task;
         }
     __syncthreads();
+    VAPR_PHASE(4);
     // self level 2: live (pose, group pair) among the (<= 4) of each live link pair
     if (a.do_self) {
         const int n1 = counters[3];
@@ -540,6 +564,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         }
     }
     __syncthreads();
+    VAPR_PHASE(5);
 
     // ---- 3a. world tasks: all spheres of one link of one pose
     const uint32_t rc_cp = 65536u / fcp.pf + 1u, rc_ov = 65536u / fov.pf + 1u;
@@ -617,6 +642,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         }
     }
     __syncthreads();
+    VAPR_PHASE(6);
 
     // ---- 4a. self gradients: one item per (pose, touched sphere), gathered
     //          over the pose's active pairs in canonical id order, which for a
@@ -631,6 +657,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
             if (live) l1[slot] = (uint16_t)it;        // l1 is free again
         }
         __syncthreads();
+    VAPR_PHASE(7);
         const int nt = counters[4];
         for (int t = tid; t < nt; t += kThreads) {
             const int it = l1[t];
@@ -678,6 +705,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         a.cost[p0 + p] = cost;
     }
     __syncthreads();
+    VAPR_PHASE(8);
 
     // ---- 5. coalesced 16-byte packed stores (tile rows are contiguous in HBM)
     if (a.do_world) {
@@ -689,9 +717,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const WorldsDev Wd, const F
         for (int i = tid; i < np * Wov / 4; i += kThreads) __stcs(dst + i, reinterpret_cast<const uint4*>(wov)[i]);
     }
     __syncthreads();
+    VAPR_PHASE(9);
     buf ^= 1;
     }  // tile loop
     cp_async_wait_all();
+#ifdef VAPR_PHASES
+    if (tid < 16) atomicAdd(&g_phase_cycles[tid], ph_acc[tid]);
+#endif
 }
 
 __global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
@@ -721,6 +753,17 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
 }
 
 }  // namespace
+
+#ifdef VAPR_PHASES
+extern "C" int vapr_debug_phase_cycles(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
