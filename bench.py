@@ -184,6 +184,7 @@ def main():
     import torch.distributed as dist
     from paper_2310_07854_b200 import binding as vb
     from paper_2310_07854_b200.rollout import Rollout
+    from paper_2310_07854_b200.dist import shard_problems, gather_best, max_over_ranks
     from workloads import config4
     from workloads.configs import FORMAT_SETS
 
@@ -197,22 +198,19 @@ def main():
     fm = FORMAT_SETS[args.formats]
     n_prob = args.problems_per_env * 8
     # weak scaling: rank r owns global problems [r*n_prob, (r+1)*n_prob)
+    ids = shard_problems(rank, world, per_rank=n_prob)
     wl = config4(problems_per_env=args.problems_per_env, seeds=args.seeds, H=args.H,
-                 formats=fm, problem_offset=rank * n_prob, n_problems=n_prob)
+                 formats=fm, problem_offset=ids[0], n_problems=len(ids))
     P = wl.poses
     r = Rollout(wl, device=local)
     stream = torch.cuda.current_stream(dev)
     best_c = torch.empty(n_prob, dtype=torch.float32, device=dev)
     best_s = torch.empty(n_prob, dtype=torch.int32, device=dev)
-    gat_c = torch.empty(n_prob * world, dtype=torch.float32, device=dev)
-    gat_s = torch.empty(n_prob * world, dtype=torch.int32, device=dev)
 
     def step():
         r.run()
         vb.vapr_best_per_problem(r.cost_traj, n_prob, args.seeds, best_c, best_s)
-        if world > 1:
-            dist.all_gather_into_tensor(gat_c, best_c)
-            dist.all_gather_into_tensor(gat_s, best_s)
+        gather_best(best_c, best_s, world)       # the path's only collective
 
     def barrier():
         if world > 1:
@@ -230,12 +228,7 @@ def main():
             fn()
         e1.record(stream)
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / k
+        return max_over_ranks(e0.elapsed_time(e1), dev) / k
 
     with Clocks(local) as clk:
         ms = timed(step, args.steps, args.warmup)

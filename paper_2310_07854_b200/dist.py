@@ -1,0 +1,46 @@
+"""Multi-GPU plumbing: problem sharding across ranks with
+no collective on the hot path, and the single final all-gather of per-problem
+results.  One process per GPU (torch.distributed: NCCL on GPUs, gloo in the
+CPU tests).
+
+Planning problems are independent ("optimizing multiple
+trajectories simultaneously with different initialization"; PAPER.md:35 / 238
+parallel evaluation), so a rank owns whole problems: weak scaling gives every
+rank its own block of `per_rank` problems, strong scaling splits a fixed
+global set round-robin so every rank sees the same environment mix.
+"""
+import torch
+import torch.distributed as dist
+
+
+def shard_problems(rank, world, per_rank=None, n_global=None, mode="weak"):
+    """Global problem ids owned by `rank`.
+
+    weak:   [rank * per_rank, (rank + 1) * per_rank)
+    strong: rank, rank + world, rank + 2 world, ... < n_global"""
+    if mode == "weak":
+        return list(range(rank * per_rank, (rank + 1) * per_rank))
+    if mode == "strong":
+        return list(range(rank, n_global, world))
+    raise ValueError(mode)
+
+
+def gather_best(best_cost, best_seed, world):
+    """All-gather the per-problem (best cost, best seed) of every rank; the
+    only collective of the path (rank-major result, [world * n])."""
+    if world == 1:
+        return best_cost, best_seed
+    gc = torch.empty(world * best_cost.numel(), dtype=best_cost.dtype, device=best_cost.device)
+    gs = torch.empty(world * best_seed.numel(), dtype=best_seed.dtype, device=best_seed.device)
+    dist.all_gather_into_tensor(gc, best_cost.contiguous())
+    dist.all_gather_into_tensor(gs, best_seed.contiguous())
+    return gc, gs
+
+
+def max_over_ranks(value, device):
+    """Max of a scalar over ranks (the bench's timing rule)."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

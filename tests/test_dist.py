@@ -1,0 +1,78 @@
+"""Multi-process (gloo, world_size 2, CPU) checks of the sharding and of the
+final per-problem gather; GPU kernels are not needed: the
+per-problem reduction here uses the same definition as vapr_best_per_problem
+(min cost, lowest argmin seed)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2310_07854_b200.dist import shard_problems, gather_best, max_over_ranks
+from workloads import config4
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        per_rank, seeds = 4, 3
+        ids = shard_problems(rank, world, per_rank=per_rank)
+        # each rank generates only its own problems (weak scaling)
+        wl = config4(problems_per_env=1, seeds=seeds, H=4, problem_offset=ids[0], n_problems=len(ids))
+        # stand-in trajectory costs: a deterministic function of the rank's own inputs
+        cost = torch.from_numpy(wl.q.reshape(len(ids) * seeds, -1).astype(np.float64).sum(1))
+        c = cost.view(len(ids), seeds)
+        best_c, best_s = c.min(1).values, c.argmin(1).to(torch.int32)
+        gc, gs = gather_best(best_c, best_s, world)
+        t = max_over_ranks(float(rank + 1), torch.device("cpu"))
+        q.put((rank, gc.numpy(), gs.numpy(), t))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gather_matches_single_process():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-process reference over all 8 problems
+    wl = config4(problems_per_env=1, seeds=3, H=4, problem_offset=0, n_problems=8)
+    cost = wl.q.reshape(8 * 3, -1).astype(np.float64).sum(1).reshape(8, 3)
+    for rank, gc, gs, t in res:
+        np.testing.assert_allclose(gc, cost.min(1))
+        np.testing.assert_array_equal(gs, cost.argmin(1))
+        assert t == 2.0                       # max over ranks
+
+
+def test_shard_partitions():
+    strong = [shard_problems(r, 4, n_global=800, mode="strong") for r in range(4)]
+    assert sorted(sum(strong, [])) == list(range(800))
+    assert all(len(s) == 200 for s in strong)
+    weak = [shard_problems(r, 8, per_rank=800) for r in range(8)]
+    assert sorted(sum(weak, [])) == list(range(6400))
+    # a shard of the global generator equals generating the shard directly
+    full = config4(problems_per_env=2, seeds=2, H=3)
+    part = config4(problems_per_env=2, seeds=2, H=3, problem_offset=8, n_problems=8)
+    np.testing.assert_array_equal(full.q[16:], part.q)
+    np.testing.assert_array_equal(full.cuboids[full.world_offsets[8]:], part.cuboids)
