@@ -277,9 +277,16 @@ def main():
     dom = max(kms, key=kms.get)
     hbm, peak_kind = peaks()
     achieved = sb[dom] * P / (kms[dom] * 1e-3) / 1e9
+    traffic = None
+    try:        # DRAM bytes per launch from the committed ncu capture of this workload
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1", "traffic.json")))
+        if tj["formats"] == args.formats and tj["poses"] == P:
+            traffic = tj["bytes_per_launch"].get(dom)
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "bytes_per_pose": sb[dom],
+                "traffic": traffic, "bytes_per_launch_alg": sb[dom] * P, "bytes_per_pose": sb[dom],
                 "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
                 "kernel_frac": {n: round(sb[n] * P / (kms[n] * 1e-3) / 1e9 / hbm, 4) for n in names}}
 
