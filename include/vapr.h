@@ -79,7 +79,7 @@ enum {
 };
 
 #define VAPR_MAX_SPHERES 64
-#define VAPR_MAX_PAIRS 2048
+#define VAPR_MAX_PAIRS 1024
 #define VAPR_MAX_CUBOIDS_PER_WORLD 16
 
 typedef struct vapr_ctx vapr_ctx;   /* opaque; one per device */

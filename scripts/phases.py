@@ -47,8 +47,11 @@ else:
     vb.vapr_collision(r.ctx.h, slot(0), r.world_idx, B, H, wl.params, r.cost_pose, r.cost_traj, slot(4), slot(2))
 torch.cuda.synchronize()
 fn(buf, 1)
-tot = sum(buf)
-names = ["", "prefetch+wait", "rows+decode+zero", "masks", "self L1 + wtask", "self L2", "tasks 3a/3b",
-         "4a list", "4a gather + 4b cost", "stores"]
+tot = sum(buf[1:10])
+names = ["", "wait", "rows+decode+zero", "balls", "world masks + self L1", "wtask list + self L2",
+         "tasks (world, self)", "per-pose cost + touched list", "self gather", "stores"]
 for i in range(1, 10):
     print(f"phase {i} {names[i]:24s} {100 * buf[i] / max(tot, 1):5.1f}%  {buf[i] / 1e6:10.1f} Mcyc")
+tiles = (P + 31) // 32
+print(f"per tile: world tasks {buf[10]/tiles:.1f}  self group-pair tasks {buf[11]/tiles:.1f}  live link pairs {buf[12]/tiles:.1f}  touched spheres {buf[13]/tiles:.1f}  kmax {buf[14]/tiles:.2f}")
+print(f"cycles per tile (thread 0 view, summed phases): {sum(buf[1:10])/tiles:.0f}")
