@@ -6,29 +6,28 @@
 // c13-c17 (box SDF, smooth hinge, summed over cuboids / listed pairs; swept =
 // linear sub-samples with the exact gradient to both endpoints).
 //
-// One CTA per tile of kTile consecutive poses (+1 halo pose on each side for
-// the swept samples):
-//  0. stage in shared memory everything that lanes index divergently: the
-//     robot's pair / group tables, sphere radii, and the cuboids of the
-//     tile's worlds (constant-bank reads serialise on divergent addresses);
-//  1. load the packed rows with all loads in flight, decode them into an FP32
-//     tile (row stride 3S|1, odd), track the largest decoded coordinate;
-//  2. broadphase.  The spheres of a link (or of a half-link group) lie in a
-//     ball around a reference sphere whose radius is rigid (computed once on
-//     the host) plus the quantisation-error margin.  World: per (segment,
-//     link, cuboid) -- or per (pose, link, cuboid) for the discrete cost -- a
-//     cull bit from a lower bound of the 1-Lipschitz box SDF at the ball
-//     centre.  Self: per (pose, link pair) a ball-ball test, then per live
-//     link pair its (<= 4) half-link group pairs;
-//  3. the live (pose, link) world tasks and live (pose, group pair) self tasks
-//     are compacted into dense shared lists (one atomic per warp) and
-//     processed by all threads; world tasks gather the complete gradient of
-//     each sphere of the link (no scatter) and OR its codes into shared packed
-//     rows (OR is order-independent); self tasks mark the active sphere pairs
-//     of their pose in a per-pose bitmask over canonical pair ids;
-//  4. one item per (pose, touched sphere) gathers its self gradient over the
-//     active pairs in id order; one thread per pose sums its costs in a fixed
-//     order; the packed tiles are streamed out with coalesced stores.
+// One warp per tile of kTP = 31 consecutive poses, one pose per lane, plus
+// the halo poses p0-1 and p0+31 for the swept samples (warps are independent:
+// no CTA barrier in the tile loop; the robot tables are staged once per CTA):
+//  1. load the packed rows (16-byte loads, all in flight) and decode them into
+//     an FP32 tile (odd row stride: lane-per-pose accesses are conflict-free);
+//     track the largest decoded coordinate;
+//  2. broadphase, 32 poses per instruction.  The spheres of a link (or of a
+//     half-link group) lie in a ball around a reference sphere whose radius is
+//     rigid (computed once on the host) plus the quantisation-error margin.
+//     World: per (segment, link, cuboid) -- or per (pose, link, cuboid) for
+//     the discrete cost -- a cull bit from the squared distance of the ball
+//     centre to the box.  Self: per (pose, link pair) a ball-ball test that
+//     selects half-link group pairs;
+//  3. the sparse work goes through warp work queues (every lane gets an item):
+//     live (pose, sphere) world items gather the complete gradient of the
+//     sphere (no scatter) and OR its codes into shared packed rows (OR is
+//     order-independent); live (pose, group pair) self items test the group
+//     balls and then the candidate sphere pairs, marking active pairs in a
+//     per-pose bitmask over canonical pair ids; (pose, touched sphere) items
+//     gather the self gradient over the active pairs in id order.  Costs come
+//     back to the pose's lane and are summed in a fixed order;
+//  4. the packed rows are streamed out with coalesced 16-byte stores.
 //
 // Culling is exact: a term is skipped only when its bound clears the
 // activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
@@ -46,37 +45,15 @@ namespace vapr {
 
 namespace {
 
-constexpr int kTile = 32;           // poses per tile
-constexpr int kRows = kTile + 2;    // with the two halo poses
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
 constexpr float kSlack = 1e-4f;
 
 struct Acc {
     float cost, gx, gy, gz;
 };
 
-#ifdef VAPR_PHASES
-__device__ unsigned long long g_phase_cycles[16];
-#endif
-
 struct Cub {
     float4 q0, q1, q2, q3;   // R^T (9), t (3), h (3), pad
 };
-
-// Lower bound of the box signed distance at c (the exact value outside, the
-// face distance max_k(|p_k| - h_k) inside).
-__device__ __forceinline__ float box_sdf_lb(const Cub& b, float cx, float cy, float cz) {
-    const float dx = cx - b.q2.y, dy = cy - b.q2.z, dz = cz - b.q2.w;
-    const float px = fmaf(b.q0.x, dx, fmaf(b.q0.y, dy, b.q0.z * dz));
-    const float py = fmaf(b.q0.w, dx, fmaf(b.q1.x, dy, b.q1.y * dz));
-    const float pz = fmaf(b.q1.z, dx, fmaf(b.q1.w, dy, b.q2.x * dz));
-    const float ux = fabsf(px) - b.q3.x, uy = fabsf(py) - b.q3.y, uz = fabsf(pz) - b.q3.z;
-    const float umax = fmaxf(ux, fmaxf(uy, uz));
-    const float ox = fmaxf(ux, 0.f), oy = fmaxf(uy, 0.f), oz = fmaxf(uz, 0.f);
-    const float out = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
-    return (umax <= 0.f) ? umax : out;          // branch-free: independent tests interleave
-}
 
 // One sphere-vs-cuboid term: adds cw * w * h(phi) to the cost and
 // -gw * w * h'(phi) * grad sdf to the gradient.
@@ -137,28 +114,6 @@ __device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt
     atomicOr(row + w, c << ((e - w * f.pf) * f.t));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Append to a shared list with one atomic per warp; every lane of the warp
-// must call it.  Returns the lane's slot (meaningful only when pred).
-__device__ __forceinline__ int warp_append(int* counter, bool pred, int lane) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    int base = 0;
-    if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    return base + __popc(m & ((1u << lane) - 1u));
-}
-
 // Self pair (i, j), i < j: false when inactive; else the gradient
 // contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
 __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const float* sr,
@@ -196,28 +151,28 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
     return true;
 }
 
-// Shared-memory carve-up and derived sizes, computed once on the host and
-// passed by value (kernel-parameter space): nothing of it is recomputed in
-// the tile loop.
-struct Geo {
-    int Wos, Wcp, Wov;         // packed row words
-    int Qos;                   // 16-byte groups per out_spheres row
-    int cs;                    // FP32 tile row stride (floats)
-    int pmw;                   // words of the per-pose active-pair mask
-    int ngp;                   // half-link group pairs
-    int npairs, nlp, S;
-    uint32_t rc_cp, rc_ov;     // e / pf reciprocals (16-bit fixed point)
-    // byte offsets into dynamic shared memory
-    unsigned stage, ctile, lball, scub, kcache, wmask, hrow, krange, wcost, counters, pmask, touched, spm, sr,
-        rl, ref, pij, gpid, gpoff, gpab, lpab, lpgp, l1, stask, wtask, wcp, wov, total;
-};
+// ---------------------------------------------------------------------------
+// Shared-memory carve-up, computed once on the host and passed by value:
+// the robot tables every warp of the CTA reads (staged once per CTA), then one
+// private workspace per warp.
+constexpr int kTP = 31;            // poses per warp tile: lanes 0..30 own one pose each
+constexpr int kTR = kTP + 2;       // tile rows: poses p0 - 1 .. p0 + 31
+constexpr int kQ = 128;            // work-queue window (items)
 
-inline int tile_stride(int cols, int Wos, int pf) {
-    int cs = ((cols + 3) & ~3);
-    if (cs < Wos * pf) cs = Wos * pf;
-    if (cs % 32 == 0) cs += 4;           // rows of one column spread over banks
-    return cs;
-}
+struct Geo {
+    int Wos, Wcp, Wov;             // packed row words
+    int Qos;                       // 16-byte groups per out_spheres row
+    int cs;                        // FP32 tile row stride (odd: lane-per-pose access is conflict-free)
+    int pmw;                       // words of the per-pose active-pair mask
+    int ngp, npairs, nlp, S;
+    uint32_t rc_cp, rc_ov;         // e / pf reciprocals (16-bit fixed point)
+    uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
+    unsigned long long lmask[kLinks];   // spheres of each link
+    // CTA tables (byte offsets from the start of dynamic shared memory)
+    unsigned sr, rl, ref, pij, gpid, gpoff, gpab, lpab, lpgp, spm, slink, tables;
+    // per-warp workspace (byte offsets from the warp's base), its size
+    unsigned rows, cpo, ovo, pmask, touched, pwm, wm, pk0, qi, qc, warp;
+};
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
              int do_self) {
@@ -226,7 +181,8 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.Wcp = do_world ? row_words_of(fcp, R.cols) : 0;
     g.Wov = do_self ? row_words_of(fov, R.cols) : 0;
     g.Qos = g.Wos / 4;
-    g.cs = tile_stride(R.cols, g.Wos, fos.pf);
+    int cs = std::max(R.cols, g.Wos * fos.pf);
+    g.cs = cs | 1;
     g.pmw = (R.n_pairs + 31) >> 5;
     g.ngp = R.lp_gp_off[R.n_link_pairs];
     g.npairs = R.n_pairs;
@@ -234,6 +190,14 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.S = R.n_spheres;
     g.rc_cp = 65536u / fcp.pf + 1u;
     g.rc_ov = 65536u / fov.pf + 1u;
+    g.rc_q = (1u << 20) / (uint32_t)g.Qos + 1u;     // exact for q < kTR * Qos (checked below)
+    for (int q = 0; q < kTR * g.Qos; ++q)
+        if (int((uint32_t(q) * g.rc_q) >> 20) != q / g.Qos) g.rc_q = 0;
+    for (int l = 0; l < kLinks; ++l) {
+        unsigned long long m = 0;
+        for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) m |= 1ull << s;
+        g.lmask[l] = m;
+    }
     unsigned o = 0;
     auto take = [&](unsigned bytes, unsigned align) {
         o = (o + align - 1) / align * align;
@@ -241,19 +205,6 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
         o += bytes;
         return at;
     };
-    g.stage = take(4u * kRows * g.Wos + 16u * kRows, 16);      // + world ids (kRows ints)
-    g.ctile = take(4u * kRows * g.cs, 16);
-    g.lball = take(16u * kRows * kLinks, 16);
-    g.scub = take(64u * kMaxCuboids * 2, 16);                  // 2-world cuboid cache
-    g.kcache = take(4u * kRows, 4);
-    g.touched = take(8u * kTile + 4u * kTile, 8);
-    g.krange = take(8u * kRows, 8);
-    g.wmask = take(4u * kRows * kLinks, 4);
-    g.hrow = take(4u * kRows, 4);
-    g.wcost = take(4u * kTile * kMaxSpheres, 4);
-    g.counters = take(4u * 8, 4);
-    g.pmask = take(4u * kTile * g.pmw, 4);
-    g.spm = take(do_self ? 4u * g.S * g.pmw : 0u, 4);
     g.sr = take(4u * kMaxSpheres, 4);
     g.rl = take(4u * 3 * kLinks, 4);
     g.ref = take(4u * 3 * kLinks, 4);
@@ -263,580 +214,494 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.gpab = take(2u * kMaxGroupPairs, 2);
     g.lpab = take(2u * 33, 2);
     g.lpgp = take(2u * 33, 2);
-    g.l1 = take(2u * kTile * 64, 2);
-    g.stask = take(2u * kTile * (g.ngp > 0 ? g.ngp : 1), 2);
-    g.wtask = take(2u * kTile * kMaxSpheres + kMaxSpheres, 2);   // + sphere -> link table
-    g.wcp = take(4u * kTile * g.Wcp, 16);
-    g.wov = take(4u * kTile * g.Wov, 16);
-    g.total = o + 16;
+    g.slink = take(kMaxSpheres, 1);
+    g.spm = take(do_self ? 4u * g.S * g.pmw : 0u, 4);
+    g.tables = take(0, 16);
+    o = 0;
+    g.rows = take(4u * kTR * g.cs, 16);
+    g.cpo = take(4u * kTP * g.Wcp, 16);
+    g.ovo = take(4u * kTP * g.Wov, 16);
+    g.touched = take(do_self ? 8u * kTP : 0u, 8);
+    g.pmask = take(do_self ? 4u * kTP * g.pmw : 0u, 4);
+    g.pwm = take(do_self ? 4u * kTP : 0u, 4);
+    g.wm = take(do_world ? 4u * kTP * kLinks : 0u, 4);
+    g.pk0 = take(do_world ? 4u * kTP : 0u, 4);
+    g.qi = take(2u * kQ, 2);
+    g.qc = take(4u * kQ, 4);
+    g.warp = take(0, 16);
     return g;
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+// Warp work queue.  Every lane owns the items given by the set bits of its
+// 128-bit mask (item = p << shift | bit); the warp processes all of them, kQ
+// at a time, LPI lanes per item (fn(item, sub) with sub = 0 .. LPI-1), and,
+// with LPI == 1, each lane gets back the sum of the costs `fn` returned for
+// its own items in ascending bit order (the items of a lane are contiguous in
+// the queue, so the order is fixed by the mask alone and never by which lane
+// processed what).  All lanes must call it.
+template <int LPI, typename Fn>
+__device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long long hi, int p,
+                                            int shift, uint16_t* qi, float* qc, int lane,
+                                            Fn&& fn) {
+    const int n = __popcll(lo) + __popcll(hi);
+    int inc = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    const int T = __shfl_sync(0xffffffffu, inc, 31);
+    const int base = inc - n;
+    float sum = 0.f;
+    int cur = base;
+    for (int win = 0; win < T; win += kQ) {
+        const int wend = win + kQ;
+        while (cur < base + n && cur < wend) {
+            int bit;
+            if (lo) {
+                bit = __ffsll((long long)lo) - 1;
+                lo &= lo - 1;
+            } else {
+                bit = 63 + __ffsll((long long)hi);
+                hi &= hi - 1;
+            }
+            qi[cur - win] = (uint16_t)((p << shift) | bit);
+            ++cur;
+        }
+        __syncwarp();
+        const int cnt = min(kQ, T - win);
+        if constexpr (LPI == 1) {
+            for (int i = lane; i < cnt; i += 32) qc[i] = fn((int)qi[i], 0);
+            __syncwarp();
+            const int e = min(base + n, win + cnt);
+            for (int idx = max(base, win); idx < e; ++idx) sum += qc[idx - win];
+        } else {
+            const int sub = lane % LPI;
+            for (int i = lane / LPI; i < cnt; i += 32 / LPI) fn((int)qi[i], sub);
+        }
+        __syncwarp();
+    }
+    return sum;
+}
+
+// One warp processes a tile of kTP consecutive poses, one pose per lane (the
+// arithmetic of every broadphase test runs for 32 poses per instruction, with
+// uniform loops and no index math); the sparse narrowphase work (live world
+// spheres, live group pairs, touched spheres) goes through warp work queues
+// so that every lane has an item.  Warps are independent: no CTA barrier in
+// the tile loop.
+__global__ void __launch_bounds__(256, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
-    uint32_t* stage = reinterpret_cast<uint32_t*>(base + G.stage);    // packed rows of one tile
-    int* swid = reinterpret_cast<int*>(stage + kRows * G.Wos);        // world index per row
-    float* ctile = reinterpret_cast<float*>(base + G.ctile);
-    float4* lball = reinterpret_cast<float4*>(base + G.lball);        // link ball per (row, link)
-    Cub* scub = reinterpret_cast<Cub*>(base + G.scub);                // cuboids of <= 2 worlds
-    int* kcache = reinterpret_cast<int*>(base + G.kcache);            // row's cache base, -1: global
-    unsigned long long* touched = reinterpret_cast<unsigned long long*>(base + G.touched);
-    uint32_t* pwm = reinterpret_cast<uint32_t*>(touched + kTile);   // [kTile] non-zero pmask words
-    int2* krange = reinterpret_cast<int2*>(base + G.krange);
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(base + G.wmask);
-    int* hrow = reinterpret_cast<int*>(base + G.hrow);
-    float* wcost = reinterpret_cast<float*>(base + G.wcost);
-    int* counters = reinterpret_cast<int*>(base + G.counters);
-    uint32_t* pmask = reinterpret_cast<uint32_t*>(base + G.pmask);
-    uint32_t* spm = reinterpret_cast<uint32_t*>(base + G.spm);       // pair-id mask of each sphere
     float* ssr = reinterpret_cast<float*>(base + G.sr);
-    float* link_rl = reinterpret_cast<float*>(base + G.rl);
-    float* grp_rl = link_rl + kLinks;
-    int* link_ref = reinterpret_cast<int*>(base + G.ref);
-    int* grp_ref = link_ref + kLinks;
+    float* srl = reinterpret_cast<float*>(base + G.rl);        // link_rl[9], grp_rl[18]
+    int* sref = reinterpret_cast<int*>(base + G.ref);          // link_ref[9], grp_ref[18]
     uint16_t* spij = reinterpret_cast<uint16_t*>(base + G.pij);     // i | j << 8
     uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + G.gpid);
     uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
     uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + G.gpab);   // a | b << 8
-    uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);
+    uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);   // a | b << 8
     uint16_t* slpgp = reinterpret_cast<uint16_t*>(base + G.lpgp);
-    uint16_t* l1 = reinterpret_cast<uint16_t*>(base + G.l1);
-    uint16_t* stask = reinterpret_cast<uint16_t*>(base + G.stask);
-    uint16_t* wtask = reinterpret_cast<uint16_t*>(base + G.wtask);
-    uint8_t* slink = reinterpret_cast<uint8_t*>(wtask + kTile * kMaxSpheres);   // link of sphere
-    uint32_t* wcp = reinterpret_cast<uint32_t*>(base + G.wcp);
-    uint32_t* wov = reinterpret_cast<uint32_t*>(base + G.wov);
+    uint8_t* slink = reinterpret_cast<uint8_t*>(base + G.slink);
+    uint32_t* spm = reinterpret_cast<uint32_t*>(base + G.spm);     // pair-id mask of each sphere
 
-    const int cs = G.cs, PMW = G.pmw;
-    const long long P = (long long)a.B * a.H;
-    const long long n_tiles = (P + kTile - 1) / kTile;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int PMW = G.pmw;
 
-    // ---- 0. stage the divergently-indexed tables (once per persistent CTA)
-    for (int i = tid; i < G.S; i += kThreads) ssr[i] = R.sr[i];
-    if (tid < kLinks)
-        for (int s2 = R.link_start[tid]; s2 < R.link_start[tid + 1]; ++s2) slink[s2] = (uint8_t)tid;
+    // ---- stage the robot tables (once per CTA)
+    for (int i = tid; i < G.S; i += blockDim.x) {
+        ssr[i] = R.sr[i];
+        int l = 0;
+        while (l < kLinks - 1 && i >= R.link_start[l + 1]) ++l;
+        slink[i] = (uint8_t)l;
+    }
     if (tid < kLinks) {
-        link_rl[tid] = R.link_rl[tid];
-        link_ref[tid] = R.link_ref[tid];
+        srl[tid] = R.link_rl[tid];
+        sref[tid] = R.link_ref[tid];
     }
     if (tid < 2 * kLinks) {
-        grp_rl[tid] = R.grp_rl[tid];
-        grp_ref[tid] = R.grp_ref[tid];
+        srl[kLinks + tid] = R.grp_rl[tid];
+        sref[kLinks + tid] = R.grp_ref[tid];
     }
     if (a.do_self) {
-        for (int i = tid; i < G.npairs; i += kThreads) {
+        for (int i = tid; i < G.npairs; i += blockDim.x) {
             spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
             sgpid[i] = R.gp_pid[i];
         }
-        for (int i = tid; i <= G.ngp; i += kThreads) sgpoff[i] = R.gp_off[i];
-        for (int i = tid; i < G.ngp; i += kThreads)
+        for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
+        for (int i = tid; i < G.ngp; i += blockDim.x)
             sgpab[i] = (uint16_t)(R.gp_a[i] | (R.gp_b[i] << 8));
-        for (int i = tid; i < G.nlp; i += kThreads)
+        for (int i = tid; i <= R.n_link_pairs; i += blockDim.x) slpgp[i] = R.lp_gp_off[i];
+        for (int i = tid; i < R.n_link_pairs; i += blockDim.x)
             slpab[i] = (uint16_t)(R.lp_a[i] | (R.lp_b[i] << 8));
-        for (int i = tid; i <= G.nlp; i += kThreads) slpgp[i] = R.lp_gp_off[i];
-        // spm[s]: bit pid set iff sphere s belongs to pair pid
-        for (int i = tid; i < G.S * PMW; i += kThreads) spm[i] = 0u;
+        for (int i = tid; i < G.S * PMW; i += blockDim.x) spm[i] = 0u;
     }
     __syncthreads();
     if (a.do_self)
-        for (int pid = tid; pid < G.npairs; pid += kThreads) {
+        for (int pid = tid; pid < G.npairs; pid += blockDim.x) {
             atomicOr(spm + R.pair_i[pid] * PMW + (pid >> 5), 1u << (pid & 31));
             atomicOr(spm + R.pair_j[pid] * PMW + (pid >> 5), 1u << (pid & 31));
         }
+    __syncthreads();
 
-    // cp.async prefetch of a tile's packed rows (p0-1 .. p0+np, clamped) and
-    // of its rows' world indices into the stage buffer
-    auto prefetch = [&](long long tl) {
-        if (tl >= n_tiles) return;
-        const long long q0 = tl * kTile;
-        const long long rlo = max(q0 - 1, 0LL), rhi = min(q0 + kTile + 1, P);
-        const int nq = int(rhi - rlo) * G.Qos;
-        const uint4* src = reinterpret_cast<const uint4*>(a.os + rlo * G.Wos);
-        uint4* dst = reinterpret_cast<uint4*>(stage);
-        for (int q = tid; q < nq; q += kThreads) cp_async16(dst + q, src + q);
-        if (a.do_world && tid < kRows) {
-            const long long pg = q0 - 1 + tid;
-            if (pg >= 0 && pg < P) cp_async4(swid + tid, a.world_idx + pg / a.H);
-        }
-    };
-    // contiguous chunk of tiles per CTA: consecutive tiles belong to the same
-    // trajectories / problems, so the problem's cuboids stay in L1
-    const long long per_cta = (n_tiles + gridDim.x - 1) / gridDim.x;
-    const long long t_begin = blockIdx.x * per_cta;
-    const long long t_end = min(n_tiles, t_begin + per_cta);
-    if (t_begin < t_end) prefetch(t_begin);
-    cp_async_commit();
+    // ---- the warp's workspace
+    char* wb = base + G.tables + (unsigned)warp * G.warp;
+    float* rows = reinterpret_cast<float*>(wb + G.rows);
+    uint32_t* cpo = reinterpret_cast<uint32_t*>(wb + G.cpo);
+    uint32_t* ovo = reinterpret_cast<uint32_t*>(wb + G.ovo);
+    unsigned long long* touched = reinterpret_cast<unsigned long long*>(wb + G.touched);
+    uint32_t* pmask = reinterpret_cast<uint32_t*>(wb + G.pmask);
+    uint32_t* pwm = reinterpret_cast<uint32_t*>(wb + G.pwm);
+    uint32_t* wm = reinterpret_cast<uint32_t*>(wb + G.wm);
+    int* pk0 = reinterpret_cast<int*>(wb + G.pk0);
+    uint16_t* qi = reinterpret_cast<uint16_t*>(wb + G.qi);
+    float* qc = reinterpret_cast<float*>(wb + G.qc);
+
+    const int cs = G.cs;
+    const long long P = (long long)a.B * a.H;
+    const long long n_tiles = (P + kTP - 1) / kTP;
+    // a contiguous chunk of tiles per warp: consecutive tiles share the
+    // problem, so its cuboids stay in L1
+    const long long NW = (long long)gridDim.x * nwarps;
+    const long long per = (n_tiles + NW - 1) / NW;
+    const long long t_begin = ((long long)blockIdx.x * nwarps + warp) * per;
+    const long long t_end = min(n_tiles, t_begin + per);
 
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
-    const int nsub = (a.do_world && a.swept) ? a.sweep_steps : 0;
+    const bool swept = a.do_world && a.swept;
+    const int nsub = swept ? a.sweep_steps : 0;
     const float inv_n1 = 1.f / float(nsub + 1);
-
-#ifdef VAPR_PHASES
-    __shared__ unsigned long long ph_acc[16];
-    if (tid < 16) ph_acc[tid] = 0ull;
-    long long ph_t = clock64();
-#define VAPR_PHASE(i)                                   \
-    if (tid == 0) {                                     \
-        const long long t_ = clock64();                 \
-        ph_acc[i] += (unsigned long long)(t_ - ph_t);   \
-        ph_t = t_;                                      \
-    }
-#else
-#define VAPR_PHASE(i)
-#endif
+    const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
+    const float fmax_os = decode(fos.maxcode, fos);
 
     for (long long tile = t_begin; tile < t_end; ++tile) {
-    const long long p0 = tile * kTile;
-    const int np = (int)min((long long)kTile, P - p0);
-    const long long r_lo = max(p0 - 1, 0LL);
-    const long long r_hi = min(p0 + np + 1, P);           // exclusive
-    const int row_off = int(r_lo - (p0 - 1));             // tile row of global row r_lo
-    cp_async_wait_all();
-    if (tid < 8) counters[tid] = 0;
-    __syncthreads();
-    VAPR_PHASE(1);
-
-    // ---- 1. rows' step index and cuboid range; decode; zero the outputs
-    if (tid < kRows) {
-        const int row = tid;
-        const long long pg = p0 - 1 + row;
-        int hh = -1;
-        int2 kr = make_int2(0, 0);
-        if (pg >= 0 && pg < P) {
-            hh = int(pg % a.H);                // 64-bit division: once per row
+        const long long p0 = tile * kTP;
+        const int np = (int)min((long long)kTP, P - p0);
+        const long long r_lo = max(p0 - 1, 0LL);
+        const long long r_hi = min(p0 + kTP + 1, P);      // exclusive
+        const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
+        // the lane's pose p0 + lane = tile row lane + 1 (lane 31: the halo
+        // pose, used only for the segment that ends there)
+        const long long pg = p0 + lane;
+        int h = -1, k0 = 0, K = 0;
+        if (pg < P) {
+            const long long b = pg / a.H;
+            h = int(pg - b * a.H);
             if (a.do_world) {
-                const int wi = swid[row];
-                if (wi >= 0 && wi < Wd.n_worlds)
-                    kr = make_int2(__ldg(Wd.off + wi), __ldg(Wd.off + wi + 1));
-            }
-        }
-        hrow[row] = hh;
-        krange[row] = kr;
-        if (kr.y > kr.x) atomicMax(counters + 6, kr.y - kr.x);
-    }
-    float amax = 0.f;
-    {
-        // one thread per 16-byte group of 4 packed words (4 PF elements
-        // starting at a multiple of 4): one 16-byte shared load, 4 PF
-        // decodes, PF 16-byte shared stores
-        const int nq = int(r_hi - r_lo) * G.Qos;
-        const uint4* sw = reinterpret_cast<const uint4*>(stage);
-        int r = tid / G.Qos, g = tid - (tid / G.Qos) * G.Qos;
-        const int dr = kThreads / G.Qos, dg = kThreads - dr * G.Qos;
-        with_pf(fos.pf, [&](auto Pc) {
-            constexpr int PF = decltype(Pc)::value;
-            for (int q = tid; q < nq; q += kThreads) {
-                const uint4 v = sw[q];
-                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                float x[4 * PF];
-#pragma unroll
-                for (int j4 = 0; j4 < 4; ++j4) decode_word_t<PF>(w4[j4], x + j4 * PF, fos);
-                float4* d4 = reinterpret_cast<float4*>(ctile + (row_off + r) * cs + 4 * PF * g);
-#pragma unroll
-                for (int j = 0; j < PF; ++j) {
-                    d4[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(x[4 * j]), fabsf(x[4 * j + 1])),
-                                             fmaxf(fabsf(x[4 * j + 2]), fabsf(x[4 * j + 3]))));
-                }
-                r += dr;
-                g += dg;
-                if (g >= G.Qos) {
-                    g -= G.Qos;
-                    ++r;
+                const int wi = __ldg(a.world_idx + b);
+                if (wi >= 0 && wi < Wd.n_worlds) {
+                    k0 = __ldg(Wd.off + wi);
+                    K = __ldg(Wd.off + wi + 1) - k0;
                 }
             }
-        });
-    }
-    {
-        uint32_t ab = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));   // non-negative
-        if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(counters + 2), ab);
-    }
-    if (a.do_world)
-        for (int i = tid; i < kTile * G.Wcp / 4; i += kThreads)
-            reinterpret_cast<uint4*>(wcp)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (a.do_self) {
-        for (int i = tid; i < kTile * G.Wov / 4; i += kThreads)
-            reinterpret_cast<uint4*>(wov)[i] = make_uint4(0u, 0u, 0u, 0u);
-        for (int i = tid; i < kTile * PMW; i += kThreads) pmask[i] = 0u;
-        if (tid < kTile) {
-            touched[tid] = 0ull;
-            pwm[tid] = 0u;
         }
-    }
-    if (a.do_world)
-        for (int i = tid; i < kTile * G.S; i += kThreads) wcost[i] = 0.f;
-    for (int i = tid; i < kRows * kLinks; i += kThreads) wmask[i] = 0u;
-    __syncthreads();
-    VAPR_PHASE(2);
 
-    // the stage buffer is free: prefetch the next tile behind this one's compute
-    if (tile + 1 < t_end) prefetch(tile + 1);
-    cp_async_commit();
-
-    // Quantisation margin: a decoded coordinate y of an FK value x satisfies
-    // |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) (half an ulp; the subnormal
-    // quantum covers the bottom of the range) unless the code saturated; two
-    // centres per distance and sqrt(3) per vector give the ball margin.  With
-    // a saturated coordinate in the tile (|y| == max_finite) there is no bound
-    // and culling is switched off for the tile.
-    const float amaxf = __uint_as_float((uint32_t)counters[2]);
-    bool can_cull = a.cull != 0;
-    float margin = 0.f;
-    if (fos.kind != KIND_IDENTITY) {
-        if (amaxf >= decode(fos.maxcode, fos)) can_cull = false;
-        const float rel = ldexpf(1.f, -(fos.M + 1));
-        const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
-        margin = 2.f * 1.7320509f * (rel * amaxf * 1.01f + sub);
-    }
-    // cuboid kk of the world of tile row `row` (global range start k0)
-    auto cuboid = [&](int row, int k0, int kk) -> Cub {
-        const int c = kcache[row];
-        if (c >= 0) return scub[c + kk];
-        const int k = k0 + kk;
-        return Cub{__ldg(Wd.cub + 4 * k), __ldg(Wd.cub + 4 * k + 1), __ldg(Wd.cub + 4 * k + 2),
-                   __ldg(Wd.cub + 4 * k + 3)};
-    };
-    // cuboid cache: the worlds of the first and last pose of the tile (a tile
-    // spans one or two trajectories in practice); other rows read global memory
-    if (a.do_world) {
-        const int wa = (hrow[1] >= 0) ? swid[1] : -1, wb = (hrow[np] >= 0) ? swid[np] : -1;
-        for (int i = tid; i < 2 * kMaxCuboids * 4; i += kThreads) {
-            const int slot = i / (kMaxCuboids * 4), rest = i - slot * kMaxCuboids * 4;
-            const int w = slot ? wb : wa;
-            if (w < 0 || w >= Wd.n_worlds) continue;
-            const int c0 = __ldg(Wd.off + w), c1 = __ldg(Wd.off + w + 1);
-            if (c0 + (rest >> 2) < c1)
-                reinterpret_cast<float4*>(scub)[i] = __ldg(Wd.cub + 4 * (c0 + (rest >> 2)) + (rest & 3));
-        }
-        if (tid < kRows) {
-            const int w = swid[tid];
-            kcache[tid] = (hrow[tid] < 0) ? -1 : (w == wa ? 0 : (w == wb ? kMaxCuboids : -1));
-        }
-    }
-    // link balls of every present row
-    for (int i = tid; i < kRows * kLinks; i += kThreads) {
-        const int row = i / kLinks, l = i - row * kLinks;
-        const float* c = ctile + row * cs + 3 * link_ref[l];
-        lball[i] = make_float4(c[0], c[1], c[2], link_rl[l] + margin);
-    }
-    __syncthreads();
-    VAPR_PHASE(3);
-
-    // ---- 2. broadphase
-    // world: one task per (cuboid, row, link) triple, cuboid-major so the
-    // lanes of a warp mostly share the cuboid (an L1 broadcast); the (rare)
-    // live bits are ORed into wmask: bits 0-15 pose (discrete), 16-31 segment
-    // row -> row+1 (swept; a ball around both endpoint balls bounds every
-    // sample on the segment)
-    if (a.do_world) {
-        const int kmax = counters[6];
-        const int ntask = kRows * kLinks * kmax;
-        // four independent triples per step so their loads and arithmetic interleave
-        for (int t0 = tid; t0 < ntask; t0 += 4 * kThreads) {
-            float sdf[4], lim[4];
-            int wi[4], bit[4];
+        // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
+        float amax = 0.f;
+        {
+            const int nq = int(r_hi - r_lo) * G.Qos;
+            const uint4* src = os4 + r_lo * G.Qos;
+            float* dst0 = rows + row_off * cs;
+            with_pf(fos.pf, [&](auto Pc) {
+                constexpr int PF = decltype(Pc)::value;
+#pragma unroll 2
+                for (int q = lane; q < nq; q += 32) {
+                    const int r = int((uint32_t(q) * G.rc_q) >> 20);
+                    const int g = q - r * G.Qos;
+                    const uint4 v = __ldg(src + q);
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                    float x[4 * PF];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int task = t0 + u * kThreads;
-                wi[u] = -1;
-                sdf[u] = 0.f;
-                lim[u] = 0.f;
-                bit[u] = 0;
-                if (task >= ntask) continue;
-                const int kk = task / (kRows * kLinks);
-                const int rl = task - kk * (kRows * kLinks);
-                const int row = rl / kLinks, l = rl - row * kLinks;
-                const int2 kr = krange[row];
-                const int h = hrow[row];
-                if (h < 0 || kk >= kr.y - kr.x || link_rl[l] < 0.f) continue;
-                const float4 b0 = lball[rl];
-                float mx = b0.x, my = b0.y, mz = b0.z, rs = b0.w;
-                bit[u] = kk;
-                if (nsub > 0) {
-                    if (!(h + 1 < a.H && row + 1 < kRows && hrow[row + 1] >= 0)) continue;
-                    const float4 b1 = lball[rl + kLinks];
-                    const float dx = b1.x - b0.x, dy = b1.y - b0.y, dz = b1.z - b0.z;
-                    mx += 0.5f * dx;
-                    my += 0.5f * dy;
-                    mz += 0.5f * dz;
-                    rs = fmaxf(b0.w, b1.w) + 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-                    bit[u] += 16;
-                }
-                const Cub cb = cuboid(row, kr.x, kk);
-                sdf[u] = box_sdf_lb(cb, mx, my, mz);
-                lim[u] = rs + a.eta_w + kSlack;
-                wi[u] = rl;
-            }
+                    for (int j4 = 0; j4 < 4; ++j4) decode_word_t<PF>(w4[j4], x + j4 * PF, fos);
+                    float* d = dst0 + r * cs + 4 * PF * g;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (wi[u] >= 0 && (!can_cull || sdf[u] <= lim[u])) atomicOr(wmask + wi[u], 1u << bit[u]);
-        }
-    }
-    // self level 1: live (pose, link pair) by the link balls (l1 list)
-    if (a.do_self)
-        for (int b0 = tid - lane; b0 < kTile * 32; b0 += kThreads) {
-            const int task = b0 + lane;
-            const int p = task >> 5, lp = task & 31;
-            bool live = false;
-            if (p < np && lp < G.nlp) {
-                const int la = slpab[lp] & 0xff, lb = slpab[lp] >> 8;
-                const float4 A4 = lball[(p + 1) * kLinks + la], B4 = lball[(p + 1) * kLinks + lb];
-                const float dx = A4.x - B4.x, dy = A4.y - B4.y, dz = A4.z - B4.z;
-                const float lim = A4.w + B4.w + a.eta_s + kSlack;
-                live = !can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim;
-            }
-            const int slot = warp_append(counters + 3, live, lane);
-            if (live) l1[slot] = (uint16_t)task;
-        }
-    __syncthreads();
-    VAPR_PHASE(4);
-
-    // live (pose, sphere) world items (the sphere's link has a live cuboid);
-    // self level 2: live (pose, group pair)
-    if (a.do_world)
-        for (int b0 = tid - lane; b0 < kTile * G.S; b0 += kThreads) {
-            const int item = b0 + lane;
-            const int p = item / G.S, sp = item - p * G.S;
-            bool live = false;
-            if (p < np) {
-                const int row = p + 1, h = hrow[row], l = slink[sp];
-                uint32_t m;
-                if (nsub > 0)
-                    m = (wmask[row * kLinks + l] >> 16) |
-                        (h > 0 ? (wmask[(row - 1) * kLinks + l] >> 16) : 0u);
-                else
-                    m = wmask[row * kLinks + l] & 0xffffu;
-                live = m != 0u;
-            }
-            const int slot = warp_append(counters + 0, live, lane);
-            if (live) wtask[slot] = (uint16_t)item;
-        }
-    if (a.do_self) {
-        const int n1 = counters[3];
-        for (int b0 = tid - lane; b0 < n1 * 4; b0 += kThreads) {
-            const int it = b0 + lane;
-            bool live = false;
-            int p = 0, g = 0;
-            if (it < n1 * 4) {
-                const int e = l1[it >> 2];
-                p = e >> 5;
-                const int lp = e & 31;
-                g = slpgp[lp] + (it & 3);
-                if (g < slpgp[lp + 1]) {
-                    const int ga = sgpab[g] & 0xff, gb = sgpab[g] >> 8;
-                    const float* ca = ctile + (p + 1) * cs + 3 * grp_ref[ga];
-                    const float* cb = ctile + (p + 1) * cs + 3 * grp_ref[gb];
-                    const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
-                    const float lim = grp_rl[ga] + grp_rl[gb] + 2.f * margin + a.eta_s + kSlack;
-                    live = !can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim;
-                }
-            }
-            const int slot = warp_append(counters + 1, live, lane);
-            if (live) stask[slot] = (uint16_t)(p * kMaxGroupPairs + g);
-        }
-    }
-    __syncthreads();
-    VAPR_PHASE(5);
-
-    // ---- 3a. world tasks: all spheres of one link of one pose
-    const int n_wtask = counters[0], n_stask = counters[1];
-#ifdef VAPR_PHASES
-    if (tid == 0) {
-        ph_acc[10] += n_wtask;
-        ph_acc[11] += n_stask;
-        ph_acc[12] += counters[3];
-        ph_acc[14] += counters[6];
-    }
-#endif
-    for (int t = tid; t < n_wtask; t += kThreads) {
-        const int item = wtask[t];
-        const int p = item / G.S, sp = item - p * G.S;
-        const int l = slink[sp];
-        const int row = p + 1, h = hrow[row];
-        const int k0 = krange[row].x;
-        uint32_t m_own, m_fwd = 0, m_bwd = 0;
-        if (nsub > 0) {
-            m_fwd = (h < a.H - 1) ? (wmask[row * kLinks + l] >> 16) : 0u;
-            m_bwd = (h > 0) ? (wmask[(row - 1) * kLinks + l] >> 16) : 0u;
-            m_own = m_fwd | m_bwd;     // a segment ball contains both endpoint balls
-        } else {
-            m_own = wmask[row * kLinks + l] & 0xffffu;
-        }
-        const float* crow = ctile + row * cs;
-        const float cx = crow[3 * sp], cy = crow[3 * sp + 1], cz = crow[3 * sp + 2];
-        const float A = ssr[sp] + a.eta_w;
-        Acc acc{0.f, 0.f, 0.f, 0.f};
-        for (uint32_t m = m_own; m; m &= m - 1)
-            world_term(cuboid(row, k0, __ffs(m) - 1), cx, cy, cz, A, a.eta_w, inv_eta_w, hoe_w,
-                       a.w_w, 1.f, 1.f, acc);
-        if (m_fwd) {                // samples of segment (h, h+1): cost + (1-tau) grad
-            const float* nrow = crow + cs;
-            const float nx = nrow[3 * sp], ny = nrow[3 * sp + 1], nz = nrow[3 * sp + 2];
-            for (int j = 1; j <= nsub; ++j) {
-                const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                const float sx = fmaf(tau, nx, omt * cx), sy = fmaf(tau, ny, omt * cy),
-                            sz = fmaf(tau, nz, omt * cz);
-                for (uint32_t m = m_fwd; m; m &= m - 1)
-                    world_term(cuboid(row, k0, __ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w,
-                               hoe_w, a.w_w, 1.f, omt, acc);
-            }
-        }
-        if (m_bwd) {                // samples of segment (h-1, h): tau grad only
-            const float* prow = crow - cs;
-            const float qx = prow[3 * sp], qy = prow[3 * sp + 1], qz = prow[3 * sp + 2];
-            for (int j = 1; j <= nsub; ++j) {
-                const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                const float sx = fmaf(tau, cx, omt * qx), sy = fmaf(tau, cy, omt * qy),
-                            sz = fmaf(tau, cz, omt * qz);
-                for (uint32_t m = m_bwd; m; m &= m - 1)
-                    world_term(cuboid(row, k0, __ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w,
-                               hoe_w, a.w_w, 0.f, tau, acc);
-            }
-        }
-        uint32_t* orow = wcp + p * G.Wcp;
-        or_code(orow, 3 * sp + 0, acc.gx + 0.f, fcp, G.rc_cp);
-        or_code(orow, 3 * sp + 1, acc.gy + 0.f, fcp, G.rc_cp);
-        or_code(orow, 3 * sp + 2, acc.gz + 0.f, fcp, G.rc_cp);
-        wcost[item] = acc.cost;
-    }
-    // ---- 3b. self tasks: the active sphere pairs of one group pair of one
-    //          pose, four candidate pairs in flight per step (independent loads
-    //          and arithmetic interleave)
-    for (int t = tid; t < n_stask; t += kThreads) {
-        const int task = stask[t];
-        const int p = task / kMaxGroupPairs, g = task - p * kMaxGroupPairs;
-        const float* crow = ctile + (p + 1) * cs;
-        unsigned long long tb = 0ull;
-        uint32_t wm = 0u;
-        const int k0 = sgpoff[g], k1 = sgpoff[g + 1];
-        for (int k = k0; k < k1; k += 4) {
-            int pid[4], ii[4], jj[4];
-            float d2[4], Rs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                pid[u] = (k + u < k1) ? sgpid[k + u] : sgpid[k];
-                ii[u] = spij[pid[u]] & 0xff;
-                jj[u] = spij[pid[u]] >> 8;
-                const float dx = crow[3 * ii[u]] - crow[3 * jj[u]];
-                const float dy = crow[3 * ii[u] + 1] - crow[3 * jj[u] + 1];
-                const float dz = crow[3 * ii[u] + 2] - crow[3 * jj[u] + 2];
-                d2[u] = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                Rs[u] = ssr[ii[u]] + ssr[jj[u]] + a.eta_s;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
-                if (k + u >= k1 || d2[u] >= Rs[u] * Rs[u]) continue;
-                if (Rs[u] - sqrtf(d2[u]) <= 0.f) continue;
-                atomicOr(pmask + p * PMW + (pid[u] >> 5), 1u << (pid[u] & 31));
-                wm |= 1u << (pid[u] >> 5);
-                tb |= (1ull << ii[u]) | (1ull << jj[u]);
-            }
-        }
-        if (tb) {
-            atomicOr(touched + p, tb);
-            atomicOr(pwm + p, wm);
-        }
-    }
-    __syncthreads();
-    VAPR_PHASE(6);
-
-    // ---- 4a. per pose: list its touched spheres; sum its cost in a fixed
-    //          order (world per link, then the active self pairs by pair id)
-    if (tid < np) {
-        const int p = tid;
-        float cost = 0.f;
-        if (a.do_world)
-            for (int sp = 0; sp < G.S; ++sp) cost += wcost[p * G.S + sp];
-        if (a.do_self) {
-            unsigned long long tb = touched[p];
-            if (tb) {
-                int slot = atomicAdd(counters + 4, __popcll(tb));
-                for (; tb; tb &= tb - 1) l1[slot++] = (uint16_t)(p * 64 + __ffsll((long long)tb) - 1);
-                const float* crow = ctile + (p + 1) * cs;
-                const uint32_t* pm = pmask + p * PMW;
-                float scost = 0.f;
-                for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
-                    const int wd = __ffs(wmk) - 1;
-                    for (uint32_t m = pm[wd]; m; m &= m - 1) {
-                        const int pid = (wd << 5) + __ffs(m) - 1;
-                        float vx, vy, vz, c;
-                        self_pair(crow, spij[pid] & 0xff, spij[pid] >> 8, ssr, a.eta_s,
-                                  inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
-                        scost += c;
+                    for (int j = 0; j < 4 * PF; ++j) {
+                        d[j] = x[j];
+                        amax = fmaxf(amax, fabsf(x[j]));
                     }
                 }
-                cost += scost;
+            });
+        }
+        amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(amax)));
+        if (a.do_world)
+            for (int i = lane; i < np * G.Wcp / 4; i += 32)
+                reinterpret_cast<uint4*>(cpo)[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (a.do_self) {
+            for (int i = lane; i < np * G.Wov / 4; i += 32)
+                reinterpret_cast<uint4*>(ovo)[i] = make_uint4(0u, 0u, 0u, 0u);
+            for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
+            if (lane < kTP) {
+                touched[lane] = 0ull;
+                pwm[lane] = 0u;
             }
         }
-        a.cost[p0 + p] = cost;
-    }
-    __syncthreads();
-    VAPR_PHASE(7);
+        if (a.do_world && lane < kTP) pk0[lane] = k0;
+        __syncwarp();
 
-    // ---- 4b. self gradients: one item per (pose, touched sphere), gathered
-    //          over its active pairs in canonical id order -- for a fixed
-    //          sphere that is its partners in ascending order, independent of
-    //          culling and of the task order
-    if (a.do_self) {
-        const int nt = counters[4];
-#ifdef VAPR_PHASES
-        if (tid == 0) ph_acc[13] += nt;
-#endif
-        for (int t = tid; t < nt; t += kThreads) {
-            const int it = l1[t];
-            const int p = it >> 6, s = it & 63;
-            const float* crow = ctile + (p + 1) * cs;
-            const uint32_t* pm = pmask + p * PMW;
-            const uint32_t* sm_ = spm + s * PMW;
-            float gx = 0.f, gy = 0.f, gz = 0.f;
-            for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
-                const int wd = __ffs(wmk) - 1;
-                for (uint32_t m = pm[wd] & sm_[wd]; m; m &= m - 1) {
-                    const int pid = (wd << 5) + __ffs(m) - 1;
-                    const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
-                    float vx, vy, vz, c;
-                    self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
-                    const float sg = (i == s) ? -1.f : 1.f;
-                    gx = fmaf(sg, vx, gx);
-                    gy = fmaf(sg, vy, gy);
-                    gz = fmaf(sg, vz, gz);
+        // Quantisation margin: a decoded coordinate y of an FK value x
+        // satisfies |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) unless the code
+        // saturated; two centres per distance and sqrt(3) per vector give the
+        // ball margin.  A saturated coordinate in the tile switches culling off.
+        bool can_cull = a.cull != 0;
+        float margin = 0.f;
+        if (fos.kind != KIND_IDENTITY) {
+            if (amax >= fmax_os) can_cull = false;
+            const float rel = ldexpf(1.f, -(fos.M + 1));
+            const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
+            margin = 2.f * 1.7320509f * (rel * amax * 1.01f + sub);
+        }
+        const float* myrow = rows + (lane + 1) * cs;
+
+        // ---- 2. world
+        float wcost = 0.f;
+        if (a.do_world) {
+            // test ball per link: swept -> the segment (pose pg-1, pose pg),
+            // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
+            // (it bounds every sample on the segment); discrete -> pose pg
+            const bool tv = swept ? (h >= 1) : (lane < np);
+            float bx[kLinks], by[kLinks], bz[kLinks], lim2[kLinks];
+            const float* prow = rows + lane * cs;
+#pragma unroll
+            for (int l = 0; l < kLinks; ++l) {
+                const int r3 = 3 * sref[l];
+                float cx = myrow[r3], cy = myrow[r3 + 1], cz = myrow[r3 + 2];
+                float rr = srl[l] + margin;
+                if (swept) {
+                    const float dx = prow[r3] - cx, dy = prow[r3 + 1] - cy, dz = prow[r3 + 2] - cz;
+                    cx = fmaf(0.5f, dx, cx);
+                    cy = fmaf(0.5f, dy, cy);
+                    cz = fmaf(0.5f, dz, cz);
+                    rr += 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                }
+                bx[l] = cx;
+                by[l] = cy;
+                bz[l] = cz;
+                const float lim = rr + a.eta_w + kSlack;
+                lim2[l] = (srl[l] < 0.f) ? -1.f : lim * lim;     // a link without spheres: never live
+            }
+            uint32_t fm[kLinks];
+#pragma unroll
+            for (int l = 0; l < kLinks; ++l) fm[l] = 0u;
+            const int Kw = __reduce_max_sync(0xffffffffu, tv ? K : 0);
+            for (int k = 0; k < Kw; ++k) {
+                const int ci = (k < K) ? k0 + k : 0;
+                const float4 q0 = __ldg(Wd.cub + 4 * ci), q1 = __ldg(Wd.cub + 4 * ci + 1);
+                const float4 q2 = __ldg(Wd.cub + 4 * ci + 2), q3 = __ldg(Wd.cub + 4 * ci + 3);
+                const bool kv = tv && k < K;
+#pragma unroll
+                for (int l = 0; l < kLinks; ++l) {
+                    // squared distance from the ball centre to the box (0 inside)
+                    const float dx = bx[l] - q2.y, dy = by[l] - q2.z, dz = bz[l] - q2.w;
+                    const float px = fmaf(q0.x, dx, fmaf(q0.y, dy, q0.z * dz));
+                    const float py = fmaf(q0.w, dx, fmaf(q1.x, dy, q1.y * dz));
+                    const float pz = fmaf(q1.z, dx, fmaf(q1.w, dy, q2.x * dz));
+                    const float ox = fmaxf(fabsf(px) - q3.x, 0.f);
+                    const float oy = fmaxf(fabsf(py) - q3.y, 0.f);
+                    const float oz = fmaxf(fabsf(pz) - q3.z, 0.f);
+                    const float o2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
+                    const bool live = (o2 <= lim2[l]) || (!can_cull && lim2[l] >= 0.f);
+                    if (kv && live) fm[l] |= 1u << k;
                 }
             }
-            uint32_t* orow = wov + p * G.Wov;
-            or_code(orow, 3 * s + 0, gx + 0.f, fov, G.rc_ov);
-            or_code(orow, 3 * s + 1, gy + 0.f, fov, G.rc_ov);
-            or_code(orow, 3 * s + 2, gz + 0.f, fov, G.rc_ov);
+            // per pose: own / forward / backward cuboid masks of each link
+            unsigned long long smask = 0ull;
+#pragma unroll
+            for (int l = 0; l < kLinks; ++l) {
+                uint32_t v, own;
+                if (swept) {
+                    const uint32_t fwd = __shfl_down_sync(0xffffffffu, fm[l], 1);
+                    v = (fwd & 0xffffu) | (fm[l] << 16);
+                    own = fwd | fm[l];
+                } else {
+                    v = own = fm[l];
+                }
+                if (lane < np) {
+                    wm[lane * kLinks + l] = v;
+                    if (own) smask |= G.lmask[l];
+                }
+            }
+            __syncwarp();
+            // live (pose, sphere) items: the complete gradient of the sphere
+            // (no scatter), its codes ORed into the packed tile row
+            wcost = warp_queue<1>(smask, 0ull, lane, 6, qi, qc, lane, [&](int it, int) -> float {
+                const int p = it >> 6, sp = it & 63;
+                const int l = slink[sp];
+                const uint32_t v = wm[p * kLinks + l];
+                uint32_t m_own, m_fwd = 0u, m_bwd = 0u;
+                if (swept) {
+                    m_fwd = v & 0xffffu;
+                    m_bwd = v >> 16;
+                    m_own = m_fwd | m_bwd;
+                } else {
+                    m_own = v;
+                }
+                const float4* cub = Wd.cub + 4 * pk0[p];
+                auto cuboid = [&](int kk) -> Cub {
+                    return Cub{__ldg(cub + 4 * kk), __ldg(cub + 4 * kk + 1), __ldg(cub + 4 * kk + 2),
+                               __ldg(cub + 4 * kk + 3)};
+                };
+                const float* crow = rows + (p + 1) * cs;
+                const float cx = crow[3 * sp], cy = crow[3 * sp + 1], cz = crow[3 * sp + 2];
+                const float A = ssr[sp] + a.eta_w;
+                Acc acc{0.f, 0.f, 0.f, 0.f};
+                // terms in a fixed order: the pose itself, the samples of
+                // segment (h, h+1) (cost + (1-tau) grad), the samples of
+                // segment (h-1, h) (tau grad only) -- one call site
+                const float* nrow = crow + cs;
+                const float* qrow = crow - cs;
+                const int nt = 1 + (m_fwd ? nsub : 0) + (m_bwd ? nsub : 0);
+                for (int t = 0; t < nt; ++t) {
+                    float sx = cx, sy = cy, sz = cz, cw = 1.f, gw = 1.f;
+                    uint32_t m = m_own;
+                    if (t > 0) {
+                        const bool fw = m_fwd && t <= nsub;
+                        const int j = fw ? t : t - (m_fwd ? nsub : 0);
+                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                        const float* o = fw ? nrow : qrow;
+                        const float ox = o[3 * sp], oy = o[3 * sp + 1], oz = o[3 * sp + 2];
+                        if (fw) {
+                            sx = fmaf(tau, ox, omt * cx);
+                            sy = fmaf(tau, oy, omt * cy);
+                            sz = fmaf(tau, oz, omt * cz);
+                            gw = omt;
+                            m = m_fwd;
+                        } else {
+                            sx = fmaf(tau, cx, omt * ox);
+                            sy = fmaf(tau, cy, omt * oy);
+                            sz = fmaf(tau, cz, omt * oz);
+                            cw = 0.f;
+                            gw = tau;
+                            m = m_bwd;
+                        }
+                    }
+                    for (; m; m &= m - 1)
+                        world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
+                                   a.w_w, cw, gw, acc);
+                }
+                uint32_t* orow = cpo + p * G.Wcp;
+                or_code(orow, 3 * sp + 0, acc.gx + 0.f, fcp, G.rc_cp);
+                or_code(orow, 3 * sp + 1, acc.gy + 0.f, fcp, G.rc_cp);
+                or_code(orow, 3 * sp + 2, acc.gz + 0.f, fcp, G.rc_cp);
+                return acc.cost;
+            });
         }
-    }
-    __syncthreads();
-    VAPR_PHASE(8);
 
-    // ---- 5. coalesced 16-byte packed stores (tile rows are contiguous in HBM)
-    if (a.do_world) {
-        uint4* dst = reinterpret_cast<uint4*>(a.cp + p0 * G.Wcp);
-        for (int i = tid; i < np * G.Wcp / 4; i += kThreads)
-            __stcs(dst + i, reinterpret_cast<const uint4*>(wcp)[i]);
-    }
-    if (a.do_self) {
-        uint4* dst = reinterpret_cast<uint4*>(a.ov + p0 * G.Wov);
-        for (int i = tid; i < np * G.Wov / 4; i += kThreads)
-            __stcs(dst + i, reinterpret_cast<const uint4*>(wov)[i]);
-    }
-    __syncthreads();
-    VAPR_PHASE(9);
+        // ---- 3. self
+        float scost = 0.f;
+        if (a.do_self) {
+            // broadphase, per pose (uniform loops, 32 poses per instruction):
+            // link-ball pairs, then the half-link group pairs of the link
+            // pairs that are live in any lane of the warp
+            unsigned long long glo = 0ull, ghi = 0ull;
+            {
+                const bool pv = lane < np;
+                for (int lp = 0; lp < G.nlp; ++lp) {
+                    const int la = slpab[lp] & 0xff, lb = slpab[lp] >> 8;
+                    const float* ca = myrow + 3 * sref[la];
+                    const float* cb = myrow + 3 * sref[lb];
+                    const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
+                    const float lim = srl[la] + srl[lb] + 2.f * margin + a.eta_s + kSlack;
+                    const bool live =
+                        pv && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim);
+                    if (!__any_sync(0xffffffffu, live)) continue;
+                    const int g1 = slpgp[lp + 1];
+                    for (int g = slpgp[lp]; g < g1; ++g) {
+                        const int ga = sgpab[g] & 0xff, gb = sgpab[g] >> 8;
+                        const float* ga3 = myrow + 3 * sref[kLinks + ga];
+                        const float* gb3 = myrow + 3 * sref[kLinks + gb];
+                        const float ex = ga3[0] - gb3[0], ey = ga3[1] - gb3[1], ez = ga3[2] - gb3[2];
+                        const float glim = srl[kLinks + ga] + srl[kLinks + gb] + 2.f * margin +
+                                           a.eta_s + kSlack;
+                        if (live && (!can_cull || fmaf(ex, ex, fmaf(ey, ey, ez * ez)) <= glim * glim)) {
+                            if (g < 64) glo |= 1ull << g;
+                            else ghi |= 1ull << (g - 64);
+                        }
+                    }
+                }
+            }
+            // narrowphase, 4 lanes per live (pose, group pair): its candidate
+            // pairs; active pairs are marked in the pose's pair-id mask
+            warp_queue<4>(glo, ghi, lane, 7, qi, qc, lane, [&](int it, int sub) -> float {
+                const int p = it >> 7, g = it & 127;
+                const float* crow = rows + (p + 1) * cs;
+                unsigned long long tb = 0ull;
+                uint32_t wmk = 0u;
+                const int k1s = sgpoff[g + 1];
+                for (int k = sgpoff[g] + sub; k < k1s; k += 4) {
+                    const int pid = sgpid[k];
+                    const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
+                    const float dx = crow[3 * i] - crow[3 * j];
+                    const float dy = crow[3 * i + 1] - crow[3 * j + 1];
+                    const float dz = crow[3 * i + 2] - crow[3 * j + 2];
+                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    const float Rs = ssr[i] + ssr[j] + a.eta_s;
+                    // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
+                    if (d2 >= Rs * Rs || Rs - sqrtf(d2) <= 0.f) continue;
+                    atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                    wmk |= 1u << (pid >> 5);
+                    tb |= (1ull << i) | (1ull << j);
+                }
+                if (tb) {
+                    atomicOr(touched + p, tb);
+                    atomicOr(pwm + p, wmk);
+                }
+                return 0.f;
+            });
+            __syncwarp();
+            // gradients: one item per (pose, touched sphere), gathered over its
+            // active pairs in canonical id order (for a fixed sphere: its
+            // partners ascending, independent of culling and of the task
+            // order); the item also returns the cost of the pairs it leads
+            // (i == s), so a pose's self cost is summed in pair-id order
+            const unsigned long long tb = (lane < np) ? touched[lane] : 0ull;
+            scost = warp_queue<1>(tb, 0ull, lane, 6, qi, qc, lane, [&](int it, int) -> float {
+                const int p = it >> 6, s = it & 63;
+                const float* crow = rows + (p + 1) * cs;
+                const uint32_t* pm = pmask + p * PMW;
+                const uint32_t* sm_ = spm + s * PMW;
+                float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
+                for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
+                    const int wd = __ffs(wmk) - 1;
+                    for (uint32_t m = pm[wd] & sm_[wd]; m; m &= m - 1) {
+                        const int pid = (wd << 5) + __ffs(m) - 1;
+                        const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
+                        float vx, vy, vz, c;
+                        self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                        const float sg = (i == s) ? -1.f : 1.f;
+                        gx = fmaf(sg, vx, gx);
+                        gy = fmaf(sg, vy, gy);
+                        gz = fmaf(sg, vz, gz);
+                        if (i == s) c_lead += c;
+                    }
+                }
+                uint32_t* orow = ovo + p * G.Wov;
+                or_code(orow, 3 * s + 0, gx + 0.f, fov, G.rc_ov);
+                or_code(orow, 3 * s + 1, gy + 0.f, fov, G.rc_ov);
+                or_code(orow, 3 * s + 2, gz + 0.f, fov, G.rc_ov);
+                return c_lead;
+            });
+        }
+        if (lane < np) a.cost[p0 + lane] = wcost + scost;
+        __syncwarp();
+
+        // ---- 4. coalesced 16-byte packed stores (the tile's rows are
+        //         contiguous in HBM)
+        if (a.do_world) {
+            uint4* dst = reinterpret_cast<uint4*>(a.cp + p0 * G.Wcp);
+            for (int i = lane; i < np * G.Wcp / 4; i += 32)
+                __stcs(dst + i, reinterpret_cast<const uint4*>(cpo)[i]);
+        }
+        if (a.do_self) {
+            uint4* dst = reinterpret_cast<uint4*>(a.ov + p0 * G.Wov);
+            for (int i = lane; i < np * G.Wov / 4; i += 32)
+                __stcs(dst + i, reinterpret_cast<const uint4*>(ovo)[i]);
+        }
+        __syncwarp();
     }  // tile loop
-    cp_async_wait_all();
-#ifdef VAPR_PHASES
-    if (tid < 16) atomicAdd(&g_phase_cycles[tid], ph_acc[tid]);
-#endif
 }
 
 __global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
@@ -865,18 +730,8 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
     best_seed[p] = arg;
 }
 
-}  // namespace
 
-#ifdef VAPR_PHASES
-extern "C" int vapr_debug_phase_cycles(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
-    if (reset) {
-        unsigned long long z[16] = {0};
-        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-    }
-    return 0;
-}
-#endif
+}  // namespace
 
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
@@ -884,19 +739,26 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     const long long P = (long long)a.B * a.H;
     if (P <= 0) return cudaSuccess;
     const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self);
-    const size_t smem = G.total;
+    if (G.rc_q == 0) return cudaErrorInvalidValue;
+    int dev = 0, sms = 148, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // as many warps per CTA as shared memory holds (the tables are staged
+    // once per CTA), at most 8; one persistent CTA per SM
+    int nw = (optin - (int)G.tables) / (int)G.warp;
+    nw = std::min(nw, 8);
+    if (nw < 1) return cudaErrorInvalidValue;
+    const size_t smem = G.tables + (size_t)nw * G.warp;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    // persistent CTAs: as many as fit on the device (the robot tables are
-    // staged once per CTA), each looping over tiles
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, collision_kernel, kThreads, smem);
-    const long long tiles = (P + kTile - 1) / kTile;
-    const long long grid = std::min<long long>(tiles, (long long)sms * std::max(per_sm, 1));
-    collision_kernel<<<(unsigned)grid, kThreads, smem, s>>>(R, G, W, fos, fcp, fov, a);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, collision_kernel, 32 * nw, smem);
+    const long long tiles = (P + kTP - 1) / kTP;
+    const long long grid = std::min<long long>((tiles + nw - 1) / nw,
+                                               (long long)sms * std::max(per_sm, 1));
+    collision_kernel<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
     return cudaGetLastError();
 }
 
