@@ -13,6 +13,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libvapr.so")
+# development hook: A/B timing of kernel variants built with
+# `python -m paper_2310_07854_b200.build --variant NAME -DMACRO=...`
+if os.environ.get("VAPR_SO"):
+    SO_PATH = os.path.abspath(os.environ["VAPR_SO"])
 
 VAPR_OUT_SPHERES, VAPR_GRAD_OUT_SPHERES, VAPR_OUT_VEC, VAPR_CLOSEST_PT, VAPR_CLOSEST_PT_SWEPT = range(5)
 VAPR_NUM_SLOTS = 5

@@ -38,6 +38,19 @@ def build(force=False, verbose=False, extra=()):
     return SO
 
 
+def build_variant(name, defines):
+    """Build a variant library (extra -D flags) to variants/libvapr_NAME.so."""
+    out = os.path.join(HERE, "variants", f"libvapr_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *FLAGS, *defines, "-o", out] + [os.path.join(CSRC, s) for s in SOURCES]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True,
-          extra=["-Xptxas", "-v"] if "-v" in sys.argv else [])
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]))
+    else:
+        build(force="--force" in sys.argv, verbose=True,
+              extra=["-Xptxas", "-v"] if "-v" in sys.argv else [])

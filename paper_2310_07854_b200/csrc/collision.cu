@@ -106,12 +106,26 @@ __device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, flo
     acc.gz = fmaf(sc, gzw, acc.gz);
 }
 
-__device__ __forceinline__ void or_code(uint32_t* row, int e, float v, const Fmt& f,
-                                        uint32_t rc) {
-    if (__float_as_uint(v) == 0u) return;          // +0 -> code 0 (the sparse common case)
-    const uint32_t c = encode(v, f);
-    const int w = int((e * rc) >> 16);             // e / pf (e < 4096)
-    atomicOr(row + w, c << ((e - w * f.pf) * f.t));
+// OR the codes of the vector (vx, vy, vz) at elements e .. e+2 into a packed
+// row: codes sharing a word go in one atomic, +0 components (code 0, the
+// sparse common case) in none.
+__device__ __forceinline__ void or_code3(uint32_t* row, int e, float vx, float vy, float vz,
+                                         const Fmt& f, uint32_t rc) {
+    const float v[3] = {vx, vy, vz};
+    int cw = -1;
+    uint32_t acc = 0u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int ec = e + c;
+        const int w = int((ec * rc) >> 16);            // ec / pf (ec < 4096)
+        if (w != cw) {
+            if (acc) atomicOr(row + cw, acc);
+            cw = w;
+            acc = 0u;
+        }
+        if (__float_as_uint(v[c]) != 0u) acc |= encode(v[c], f) << ((ec - w * f.pf) * f.t);
+    }
+    if (acc) atomicOr(row + cw, acc);
 }
 
 // Self pair (i, j), i < j: false when inactive; else the gradient
@@ -155,8 +169,21 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 // Shared-memory carve-up, computed once on the host and passed by value:
 // the robot tables every warp of the CTA reads (staged once per CTA), then one
 // private workspace per warp.
-constexpr int kTP = 31;            // poses per warp tile: lanes 0..30 own one pose each
-constexpr int kTR = kTP + 2;       // tile rows: poses p0 - 1 .. p0 + 31
+#ifndef VAPR_DEC_UNROLL
+#define VAPR_DEC_UNROLL 2
+#endif
+#ifndef VAPR_FUSED_SPLIT         // 1: world and self as two passes
+#define VAPR_FUSED_SPLIT 1
+#endif
+#ifndef VAPR_PHASE_SYNC          // 1: CTA barriers between the phases of a tile
+#define VAPR_PHASE_SYNC 0
+#endif
+constexpr int kDecUnroll = VAPR_DEC_UNROLL;
+constexpr int kLPP = 2;            // lanes per pose: lane = half * 16 + p
+constexpr int kPL = 32 / kLPP;     // pose lanes per half
+constexpr int kTP = kPL - 1;       // poses per warp tile (pose lane kPL-1: the halo pose)
+constexpr int kTR = kTP + 2;       // tile rows: poses p0 - 1 .. p0 + kTP
+constexpr int kLH = (kLinks + kLPP - 1) / kLPP;   // links per half in the world broadphase
 constexpr int kQ = 128;            // work-queue window (items)
 
 struct Geo {
@@ -169,9 +196,9 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, gpid, gpoff, gpab, lpab, lpgp, spm, slink, tables;
+    unsigned sr, rl, ref, pij, prec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
-    unsigned rows, cpo, ovo, pmask, touched, pwm, wm, pk0, qi, qc, warp;
+    unsigned rows, pmask, touched, pwm, wm, pk0, qi, qc, warp;
 };
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
@@ -209,7 +236,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.rl = take(4u * 3 * kLinks, 4);
     g.ref = take(4u * 3 * kLinks, 4);
     g.pij = take(2u * g.npairs, 2);
-    g.gpid = take(2u * g.npairs, 2);
+    g.prec = take(8u * g.npairs, 8);
     g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
     g.gpab = take(2u * kMaxGroupPairs, 2);
     g.lpab = take(2u * 33, 2);
@@ -219,8 +246,6 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.tables = take(0, 16);
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
-    g.cpo = take(4u * kTP * g.Wcp, 16);
-    g.ovo = take(4u * kTP * g.Wov, 16);
     g.touched = take(do_self ? 8u * kTP : 0u, 8);
     g.pmask = take(do_self ? 4u * kTP * g.pmw : 0u, 4);
     g.pwm = take(do_self ? 4u * kTP : 0u, 4);
@@ -290,7 +315,7 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
 // spheres, live group pairs, touched spheres) goes through warp work queues
 // so that every lane has an item.  Warps are independent: no CTA barrier in
 // the tile loop.
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(512, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
@@ -300,7 +325,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     float* srl = reinterpret_cast<float*>(base + G.rl);        // link_rl[9], grp_rl[18]
     int* sref = reinterpret_cast<int*>(base + G.ref);          // link_ref[9], grp_ref[18]
     uint16_t* spij = reinterpret_cast<uint16_t*>(base + G.pij);     // i | j << 8
-    uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + G.gpid);
+    uint2* sprec = reinterpret_cast<uint2*>(base + G.prec);        // candidate pairs in group-pair order
     uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
     uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + G.gpab);   // a | b << 8
     uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);   // a | b << 8
@@ -309,6 +334,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint32_t* spm = reinterpret_cast<uint32_t*>(base + G.spm);     // pair-id mask of each sphere
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
     const int PMW = G.pmw;
 
     // ---- stage the robot tables (once per CTA)
@@ -329,7 +355,11 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     if (a.do_self) {
         for (int i = tid; i < G.npairs; i += blockDim.x) {
             spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
-            sgpid[i] = R.gp_pid[i];
+            // record k of the group-pair order: 3i | 3j << 8 | pid << 16, and
+            // the activation distance r_i + r_j + eta
+            const int pid = R.gp_pid[i], pi = R.pair_i[pid], pj = R.pair_j[pid];
+            sprec[i] = make_uint2((uint32_t)(3 * pi) | ((uint32_t)(3 * pj) << 8) | ((uint32_t)pid << 16),
+                                  __float_as_uint(R.sr[pi] + R.sr[pj] + a.eta_s));
         }
         for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
         for (int i = tid; i < G.ngp; i += blockDim.x)
@@ -350,8 +380,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     // ---- the warp's workspace
     char* wb = base + G.tables + (unsigned)warp * G.warp;
     float* rows = reinterpret_cast<float*>(wb + G.rows);
-    uint32_t* cpo = reinterpret_cast<uint32_t*>(wb + G.cpo);
-    uint32_t* ovo = reinterpret_cast<uint32_t*>(wb + G.ovo);
     unsigned long long* touched = reinterpret_cast<unsigned long long*>(wb + G.touched);
     uint32_t* pmask = reinterpret_cast<uint32_t*>(wb + G.pmask);
     uint32_t* pwm = reinterpret_cast<uint32_t*>(wb + G.pwm);
@@ -378,15 +406,18 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
     const float fmax_os = decode(fos.maxcode, fos);
 
-    for (long long tile = t_begin; tile < t_end; ++tile) {
+    for (long long it_ = 0; it_ < per; ++it_) {
+        const long long tile = t_begin + it_;
+        if (!VAPR_PHASE_SYNC && tile >= t_end) break;
         const long long p0 = tile * kTP;
-        const int np = (int)min((long long)kTP, P - p0);
+        // np = 0: a warp past its last tile keeps hitting the phase barriers
+        const int np = (tile < t_end) ? (int)min((long long)kTP, P - p0) : 0;
         const long long r_lo = max(p0 - 1, 0LL);
         const long long r_hi = min(p0 + kTP + 1, P);      // exclusive
         const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
         // the lane's pose p0 + lane = tile row lane + 1 (lane 31: the halo
         // pose, used only for the segment that ends there)
-        const long long pg = p0 + lane;
+        const long long pg = p0 + pl;
         int h = -1, k0 = 0, K = 0;
         if (pg < P) {
             const long long b = pg / a.H;
@@ -403,12 +434,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
         float amax = 0.f;
         {
-            const int nq = int(r_hi - r_lo) * G.Qos;
+            const int nq = (np > 0) ? int(r_hi - r_lo) * G.Qos : 0;
             const uint4* src = os4 + r_lo * G.Qos;
             float* dst0 = rows + row_off * cs;
             with_pf(fos.pf, [&](auto Pc) {
                 constexpr int PF = decltype(Pc)::value;
-#pragma unroll 2
+#pragma unroll kDecUnroll
                 for (int q = lane; q < nq; q += 32) {
                     const int r = int((uint32_t(q) * G.rc_q) >> 20);
                     const int g = q - r * G.Qos;
@@ -427,20 +458,25 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             });
         }
         amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(amax)));
+        // the output rows are zero-filled here and their non-zero codes ORed in
+        // with atomics (__syncwarp orders the fill before every lane's atomics)
+        uint32_t* const cpg = a.do_world ? a.cp + p0 * G.Wcp : nullptr;
+        uint32_t* const ovg = a.do_self ? a.ov + p0 * G.Wov : nullptr;
         if (a.do_world)
             for (int i = lane; i < np * G.Wcp / 4; i += 32)
-                reinterpret_cast<uint4*>(cpo)[i] = make_uint4(0u, 0u, 0u, 0u);
+                reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
         if (a.do_self) {
             for (int i = lane; i < np * G.Wov / 4; i += 32)
-                reinterpret_cast<uint4*>(ovo)[i] = make_uint4(0u, 0u, 0u, 0u);
+                reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
             if (lane < kTP) {
                 touched[lane] = 0ull;
                 pwm[lane] = 0u;
             }
         }
-        if (a.do_world && lane < kTP) pk0[lane] = k0;
+        if (a.do_world && half == 0 && pl < kTP) pk0[pl] = k0;
         __syncwarp();
+        if (VAPR_PHASE_SYNC) __syncthreads();
 
         // Quantisation margin: a decoded coordinate y of an FK value x
         // satisfies |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) unless the code
@@ -454,7 +490,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
             margin = 2.f * 1.7320509f * (rel * amax * 1.01f + sub);
         }
-        const float* myrow = rows + (lane + 1) * cs;
+        const float* myrow = rows + (pl + 1) * cs;
+        const bool owner = half == 0 && pl < np;     // the lane that owns pose pl's results
 
         // ---- 2. world
         float wcost = 0.f;
@@ -462,14 +499,16 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // test ball per link: swept -> the segment (pose pg-1, pose pg),
             // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
             // (it bounds every sample on the segment); discrete -> pose pg
-            const bool tv = swept ? (h >= 1) : (lane < np);
-            float bx[kLinks], by[kLinks], bz[kLinks], lim2[kLinks];
-            const float* prow = rows + lane * cs;
+            const bool tv = swept ? (h >= 1) : (pl < np);
+            float bx[kLH], by[kLH], bz[kLH], lim2[kLH];
+            const float* prow = rows + pl * cs;
 #pragma unroll
-            for (int l = 0; l < kLinks; ++l) {
-                const int r3 = 3 * sref[l];
+            for (int u = 0; u < kLH; ++u) {
+                const int l = half * kLH + u;
+                const int lc = min(l, kLinks - 1);
+                const int r3 = 3 * sref[lc];
                 float cx = myrow[r3], cy = myrow[r3 + 1], cz = myrow[r3 + 2];
-                float rr = srl[l] + margin;
+                float rr = srl[lc] + margin;
                 if (swept) {
                     const float dx = prow[r3] - cx, dy = prow[r3 + 1] - cy, dz = prow[r3 + 2] - cz;
                     cx = fmaf(0.5f, dx, cx);
@@ -477,15 +516,16 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     cz = fmaf(0.5f, dz, cz);
                     rr += 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                 }
-                bx[l] = cx;
-                by[l] = cy;
-                bz[l] = cz;
+                bx[u] = cx;
+                by[u] = cy;
+                bz[u] = cz;
                 const float lim = rr + a.eta_w + kSlack;
-                lim2[l] = (srl[l] < 0.f) ? -1.f : lim * lim;     // a link without spheres: never live
+                // a link without spheres (or past the last link): never live
+                lim2[u] = (l >= kLinks || srl[lc] < 0.f) ? -1.f : lim * lim;
             }
-            uint32_t fm[kLinks];
+            uint32_t fm[kLH];
 #pragma unroll
-            for (int l = 0; l < kLinks; ++l) fm[l] = 0u;
+            for (int u = 0; u < kLH; ++u) fm[u] = 0u;
             const int Kw = __reduce_max_sync(0xffffffffu, tv ? K : 0);
             for (int k = 0; k < Kw; ++k) {
                 const int ci = (k < K) ? k0 + k : 0;
@@ -493,9 +533,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const float4 q2 = __ldg(Wd.cub + 4 * ci + 2), q3 = __ldg(Wd.cub + 4 * ci + 3);
                 const bool kv = tv && k < K;
 #pragma unroll
-                for (int l = 0; l < kLinks; ++l) {
+                for (int u = 0; u < kLH; ++u) {
                     // squared distance from the ball centre to the box (0 inside)
-                    const float dx = bx[l] - q2.y, dy = by[l] - q2.z, dz = bz[l] - q2.w;
+                    const float dx = bx[u] - q2.y, dy = by[u] - q2.z, dz = bz[u] - q2.w;
                     const float px = fmaf(q0.x, dx, fmaf(q0.y, dy, q0.z * dz));
                     const float py = fmaf(q0.w, dx, fmaf(q1.x, dy, q1.y * dz));
                     const float pz = fmaf(q1.z, dx, fmaf(q1.w, dy, q2.x * dz));
@@ -503,31 +543,35 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     const float oy = fmaxf(fabsf(py) - q3.y, 0.f);
                     const float oz = fmaxf(fabsf(pz) - q3.z, 0.f);
                     const float o2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-                    const bool live = (o2 <= lim2[l]) || (!can_cull && lim2[l] >= 0.f);
-                    if (kv && live) fm[l] |= 1u << k;
+                    const bool live = (o2 <= lim2[u]) || (!can_cull && lim2[u] >= 0.f);
+                    if (kv && live) fm[u] |= 1u << k;
                 }
             }
             // per pose: own / forward / backward cuboid masks of each link
+            // (forward = the segment of pose lane pl + 1, same half)
             unsigned long long smask = 0ull;
 #pragma unroll
-            for (int l = 0; l < kLinks; ++l) {
+            for (int u = 0; u < kLH; ++u) {
+                const int l = half * kLH + u;
                 uint32_t v, own;
                 if (swept) {
-                    const uint32_t fwd = __shfl_down_sync(0xffffffffu, fm[l], 1);
-                    v = (fwd & 0xffffu) | (fm[l] << 16);
-                    own = fwd | fm[l];
+                    const uint32_t fwd = __shfl_down_sync(0xffffffffu, fm[u], 1);
+                    v = (fwd & 0xffffu) | (fm[u] << 16);
+                    own = fwd | fm[u];
                 } else {
-                    v = own = fm[l];
+                    v = own = fm[u];
                 }
-                if (lane < np) {
-                    wm[lane * kLinks + l] = v;
+                if (pl < np && l < kLinks) {
+                    wm[pl * kLinks + l] = v;
                     if (own) smask |= G.lmask[l];
                 }
             }
+            smask |= __shfl_xor_sync(0xffffffffu, smask, kPL);
+            if (!owner) smask = 0ull;
             __syncwarp();
             // live (pose, sphere) items: the complete gradient of the sphere
             // (no scatter), its codes ORed into the packed tile row
-            wcost = warp_queue<1>(smask, 0ull, lane, 6, qi, qc, lane, [&](int it, int) -> float {
+            wcost = warp_queue<1>(smask, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
                 const int p = it >> 6, sp = it & 63;
                 const int l = slink[sp];
                 const uint32_t v = wm[p * kLinks + l];
@@ -582,14 +626,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
                                    a.w_w, cw, gw, acc);
                 }
-                uint32_t* orow = cpo + p * G.Wcp;
-                or_code(orow, 3 * sp + 0, acc.gx + 0.f, fcp, G.rc_cp);
-                or_code(orow, 3 * sp + 1, acc.gy + 0.f, fcp, G.rc_cp);
-                or_code(orow, 3 * sp + 2, acc.gz + 0.f, fcp, G.rc_cp);
+                uint32_t* orow = cpg + p * G.Wcp;
+                or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
                 return acc.cost;
             });
         }
 
+        if (VAPR_PHASE_SYNC) __syncthreads();
         // ---- 3. self
         float scost = 0.f;
         if (a.do_self) {
@@ -598,15 +641,17 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // pairs that are live in any lane of the warp
             unsigned long long glo = 0ull, ghi = 0ull;
             {
-                const bool pv = lane < np;
-                for (int lp = 0; lp < G.nlp; ++lp) {
+                const bool pv = pl < np;
+                for (int lp0 = 0; lp0 < G.nlp; lp0 += kLPP) {
+                    const int lp = min(lp0 + half, G.nlp - 1);
+                    const bool lpv = pv && lp0 + half < G.nlp;
                     const int la = slpab[lp] & 0xff, lb = slpab[lp] >> 8;
                     const float* ca = myrow + 3 * sref[la];
                     const float* cb = myrow + 3 * sref[lb];
                     const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
                     const float lim = srl[la] + srl[lb] + 2.f * margin + a.eta_s + kSlack;
                     const bool live =
-                        pv && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim);
+                        lpv && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim);
                     if (!__any_sync(0xffffffffu, live)) continue;
                     const int g1 = slpgp[lp + 1];
                     for (int g = slpgp[lp]; g < g1; ++g) {
@@ -623,27 +668,30 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     }
                 }
             }
+            glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
+            ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
+            if (!owner) glo = ghi = 0ull;
             // narrowphase, 4 lanes per live (pose, group pair): its candidate
             // pairs; active pairs are marked in the pose's pair-id mask
-            warp_queue<4>(glo, ghi, lane, 7, qi, qc, lane, [&](int it, int sub) -> float {
+            warp_queue<4>(glo, ghi, pl, 7, qi, qc, lane, [&](int it, int sub) -> float {
                 const int p = it >> 7, g = it & 127;
                 const float* crow = rows + (p + 1) * cs;
                 unsigned long long tb = 0ull;
                 uint32_t wmk = 0u;
                 const int k1s = sgpoff[g + 1];
                 for (int k = sgpoff[g] + sub; k < k1s; k += 4) {
-                    const int pid = sgpid[k];
-                    const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
-                    const float dx = crow[3 * i] - crow[3 * j];
-                    const float dy = crow[3 * i + 1] - crow[3 * j + 1];
-                    const float dz = crow[3 * i + 2] - crow[3 * j + 2];
+                    const uint2 rec = sprec[k];
+                    const float* ci = crow + (rec.x & 0xffu);
+                    const float* cj = crow + ((rec.x >> 8) & 0xffu);
+                    const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
                     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const float Rs = ssr[i] + ssr[j] + a.eta_s;
+                    const float Rs = __uint_as_float(rec.y);
                     // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
                     if (d2 >= Rs * Rs || Rs - sqrtf(d2) <= 0.f) continue;
+                    const int pid = rec.x >> 16;
                     atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
                     wmk |= 1u << (pid >> 5);
-                    tb |= (1ull << i) | (1ull << j);
+                    tb |= (1ull << ((rec.x & 0xffu) / 3)) | (1ull << (((rec.x >> 8) & 0xffu) / 3));
                 }
                 if (tb) {
                     atomicOr(touched + p, tb);
@@ -657,8 +705,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // partners ascending, independent of culling and of the task
             // order); the item also returns the cost of the pairs it leads
             // (i == s), so a pose's self cost is summed in pair-id order
-            const unsigned long long tb = (lane < np) ? touched[lane] : 0ull;
-            scost = warp_queue<1>(tb, 0ull, lane, 6, qi, qc, lane, [&](int it, int) -> float {
+            const unsigned long long tb = owner ? touched[pl] : 0ull;
+            scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
                 const int p = it >> 6, s = it & 63;
                 const float* crow = rows + (p + 1) * cs;
                 const uint32_t* pm = pmask + p * PMW;
@@ -678,29 +726,17 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         if (i == s) c_lead += c;
                     }
                 }
-                uint32_t* orow = ovo + p * G.Wov;
-                or_code(orow, 3 * s + 0, gx + 0.f, fov, G.rc_ov);
-                or_code(orow, 3 * s + 1, gy + 0.f, fov, G.rc_ov);
-                or_code(orow, 3 * s + 2, gz + 0.f, fov, G.rc_ov);
+                uint32_t* orow = ovg + p * G.Wov;
+                or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
                 return c_lead;
             });
         }
-        if (lane < np) a.cost[p0 + lane] = wcost + scost;
+        if (owner) {
+            const float c = wcost + scost;
+            a.cost[p0 + pl] = a.cost_accumulate ? a.cost[p0 + pl] + c : c;
+        }
         __syncwarp();
 
-        // ---- 4. coalesced 16-byte packed stores (the tile's rows are
-        //         contiguous in HBM)
-        if (a.do_world) {
-            uint4* dst = reinterpret_cast<uint4*>(a.cp + p0 * G.Wcp);
-            for (int i = lane; i < np * G.Wcp / 4; i += 32)
-                __stcs(dst + i, reinterpret_cast<const uint4*>(cpo)[i]);
-        }
-        if (a.do_self) {
-            uint4* dst = reinterpret_cast<uint4*>(a.ov + p0 * G.Wov);
-            for (int i = lane; i < np * G.Wov / 4; i += 32)
-                __stcs(dst + i, reinterpret_cast<const uint4*>(ovo)[i]);
-        }
-        __syncwarp();
     }  // tile loop
 }
 
@@ -733,11 +769,10 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
 
 }  // namespace
 
-cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
-                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
-                             cudaStream_t s) {
+cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                                  const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                                  cudaStream_t s) {
     const long long P = (long long)a.B * a.H;
-    if (P <= 0) return cudaSuccess;
     const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self);
     if (G.rc_q == 0) return cudaErrorInvalidValue;
     int dev = 0, sms = 148, optin = 0;
@@ -747,7 +782,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     // as many warps per CTA as shared memory holds (the tables are staged
     // once per CTA), at most 8; one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
-    nw = std::min(nw, 8);
+    nw = std::min(nw, 16);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
@@ -760,6 +795,25 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
                                                (long long)sms * std::max(per_sm, 1));
     collision_kernel<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
     return cudaGetLastError();
+}
+
+// World and self run as two passes over the tile rows (the second adds its
+// cost to the first's, i.e. the same wcost + scost): each pass keeps a
+// smaller instruction working set, which beats re-reading out_spheres.
+cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                             cudaStream_t s) {
+    const long long P = (long long)a.B * a.H;
+    if (P <= 0) return cudaSuccess;
+    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self))
+        return launch_collision_pass(R, W, fos, fcp, fov, a, s);
+    CollisionArgs aw = a, as = a;
+    aw.do_self = 0;
+    as.do_world = 0;
+    as.cost_accumulate = 1;
+    cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, aw, s);
+    if (e != cudaSuccess) return e;
+    return launch_collision_pass(R, W, fos, fcp, fov, as, s);
 }
 
 cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,

@@ -27,6 +27,7 @@ struct CollisionArgs {
     float* cost;              // [B*H] (world + self of the enabled parts)
     uint32_t* cp;             // packed world gradient (nullable iff !do_world)
     uint32_t* ov;             // packed self gradient (nullable iff !do_self)
+    int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
 };
 
 cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t cols,
