@@ -26,6 +26,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "rollout cost+grad evals/sec (B*H*spheres) and HBM GB/s vs peak, per format set"
 UNIT = "sphere-evals/s"
+# libvapr launches per step: fk, collision world pass, collision self pass,
+# traj_reduce, aggregate, bk (vapr_cost_grad) + best_per_problem
+LAUNCHES_PER_STEP = 7
 S = 52
 
 
@@ -338,7 +341,7 @@ def main():
                     "ms_per_step": e2e_ms},
             "fp32": fp32,
             "cpu_baseline": cpu,
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -196,7 +196,7 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, prec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
+    unsigned sr, rl, ref, pij, prec, grec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
     unsigned rows, pmask, touched, pwm, wm, pk0, qi, qc, warp;
 };
@@ -237,6 +237,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.ref = take(4u * 3 * kLinks, 4);
     g.pij = take(2u * g.npairs, 2);
     g.prec = take(8u * g.npairs, 8);
+    g.grec = take(8u * kMaxGroupPairs, 8);
     g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
     g.gpab = take(2u * kMaxGroupPairs, 2);
     g.lpab = take(2u * 33, 2);
@@ -326,6 +327,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     int* sref = reinterpret_cast<int*>(base + G.ref);          // link_ref[9], grp_ref[18]
     uint16_t* spij = reinterpret_cast<uint16_t*>(base + G.pij);     // i | j << 8
     uint2* sprec = reinterpret_cast<uint2*>(base + G.prec);        // candidate pairs in group-pair order
+    uint2* sgrec = reinterpret_cast<uint2*>(base + G.grec);        // group-pair ball tests
     uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
     uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + G.gpab);   // a | b << 8
     uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);   // a | b << 8
@@ -362,8 +364,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                   __float_as_uint(R.sr[pi] + R.sr[pj] + a.eta_s));
         }
         for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
-        for (int i = tid; i < G.ngp; i += blockDim.x)
+        for (int i = tid; i < G.ngp; i += blockDim.x) {
             sgpab[i] = (uint16_t)(R.gp_a[i] | (R.gp_b[i] << 8));
+            // 3 ref_a | 3 ref_b << 8, and the static part of the cull distance
+            const int ga = R.gp_a[i], gb = R.gp_b[i];
+            sgrec[i] = make_uint2((uint32_t)(3 * R.grp_ref[ga]) | ((uint32_t)(3 * R.grp_ref[gb]) << 8),
+                                  __float_as_uint(R.grp_rl[ga] + R.grp_rl[gb] + a.eta_s + kSlack));
+        }
         for (int i = tid; i <= R.n_link_pairs; i += blockDim.x) slpgp[i] = R.lp_gp_off[i];
         for (int i = tid; i < R.n_link_pairs; i += blockDim.x)
             slpab[i] = (uint16_t)(R.lp_a[i] | (R.lp_b[i] << 8));
@@ -636,69 +643,114 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ---- 3. self
         float scost = 0.f;
         if (a.do_self) {
-            // broadphase, per pose (uniform loops, 32 poses per instruction):
-            // link-ball pairs, then the half-link group pairs of the link
-            // pairs that are live in any lane of the warp
+            // broadphase, per pose (uniform loop, the two lanes of a pose split
+            // the list): every half-link group pair, a ball-ball test
             unsigned long long glo = 0ull, ghi = 0ull;
-            {
-                const bool pv = pl < np;
-                for (int lp0 = 0; lp0 < G.nlp; lp0 += kLPP) {
-                    const int lp = min(lp0 + half, G.nlp - 1);
-                    const bool lpv = pv && lp0 + half < G.nlp;
-                    const int la = slpab[lp] & 0xff, lb = slpab[lp] >> 8;
-                    const float* ca = myrow + 3 * sref[la];
-                    const float* cb = myrow + 3 * sref[lb];
+            if (pl < np) {
+                const float m2 = 2.f * margin;
+                for (int g = half; g < G.ngp; g += kLPP) {
+                    const uint2 r = sgrec[g];
+                    const float* ca = myrow + (r.x & 0xffu);
+                    const float* cb = myrow + ((r.x >> 8) & 0xffu);
                     const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
-                    const float lim = srl[la] + srl[lb] + 2.f * margin + a.eta_s + kSlack;
-                    const bool live =
-                        lpv && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim);
-                    if (!__any_sync(0xffffffffu, live)) continue;
-                    const int g1 = slpgp[lp + 1];
-                    for (int g = slpgp[lp]; g < g1; ++g) {
-                        const int ga = sgpab[g] & 0xff, gb = sgpab[g] >> 8;
-                        const float* ga3 = myrow + 3 * sref[kLinks + ga];
-                        const float* gb3 = myrow + 3 * sref[kLinks + gb];
-                        const float ex = ga3[0] - gb3[0], ey = ga3[1] - gb3[1], ez = ga3[2] - gb3[2];
-                        const float glim = srl[kLinks + ga] + srl[kLinks + gb] + 2.f * margin +
-                                           a.eta_s + kSlack;
-                        if (live && (!can_cull || fmaf(ex, ex, fmaf(ey, ey, ez * ez)) <= glim * glim)) {
-                            if (g < 64) glo |= 1ull << g;
-                            else ghi |= 1ull << (g - 64);
-                        }
+                    const float lim = __uint_as_float(r.y) + m2;
+                    if (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) {
+                        if (g < 64) glo |= 1ull << g;
+                        else ghi |= 1ull << (g - 64);
                     }
                 }
             }
             glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
             ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
             if (!owner) glo = ghi = 0ull;
-            // narrowphase, 4 lanes per live (pose, group pair): its candidate
-            // pairs; active pairs are marked in the pose's pair-id mask
-            warp_queue<4>(glo, ghi, pl, 7, qi, qc, lane, [&](int it, int sub) -> float {
-                const int p = it >> 7, g = it & 127;
-                const float* crow = rows + (p + 1) * cs;
-                unsigned long long tb = 0ull;
-                uint32_t wmk = 0u;
-                const int k1s = sgpoff[g + 1];
-                for (int k = sgpoff[g] + sub; k < k1s; k += 4) {
-                    const uint2 rec = sprec[k];
-                    const float* ci = crow + (rec.x & 0xffu);
-                    const float* cj = crow + ((rec.x >> 8) & 0xffu);
-                    const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
-                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const float Rs = __uint_as_float(rec.y);
-                    // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
-                    if (d2 >= Rs * Rs || Rs - sqrtf(d2) <= 0.f) continue;
-                    const int pid = rec.x >> 16;
-                    atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
-                    wmk |= 1u << (pid >> 5);
-                    tb |= (1ull << ((rec.x & 0xffu) / 3)) | (1ull << (((rec.x >> 8) & 0xffu) / 3));
+            // narrowphase: the live (pose, group pair) entries are listed, each
+            // expanded into chunks of <= 4 candidate pairs, one chunk per lane
+            // (balanced whatever the group-pair sizes); active pairs are marked
+            // in the pose's pair-id mask
+            {
+                uint16_t* qx = reinterpret_cast<uint16_t*>(qc);     // kQ floats = 2 kQ chunk items
+                constexpr int kX = 2 * kQ;
+                const int n = __popcll(glo) + __popcll(ghi);
+                int inc = n;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += t;
                 }
-                if (tb) {
-                    atomicOr(touched + p, tb);
-                    atomicOr(pwm + p, wmk);
+                const int T = __shfl_sync(0xffffffffu, inc, 31);
+                const int base = inc - n;
+                int cur = base;
+                for (int win = 0; win < T; win += kQ) {
+                    while (cur < base + n && cur < win + kQ) {
+                        int bit;
+                        if (glo) {
+                            bit = __ffsll((long long)glo) - 1;
+                            glo &= glo - 1;
+                        } else {
+                            bit = 63 + __ffsll((long long)ghi);
+                            ghi &= ghi - 1;
+                        }
+                        qi[cur - win] = (uint16_t)((pl << 7) | bit);
+                        ++cur;
+                    }
+                    __syncwarp();
+                    const int cnt = min(kQ, T - win);
+                    for (int e0 = 0; e0 < cnt; e0 += 32) {
+                        const int e = e0 + lane;
+                        int nch = 0;
+                        if (e < cnt) {
+                            const int g = qi[e] & 127;
+                            nch = (sgpoff[g + 1] - sgpoff[g] + 3) >> 2;
+                        }
+                        int cinc = nch;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const int t = __shfl_up_sync(0xffffffffu, cinc, d);
+                            if (lane >= d) cinc += t;
+                        }
+                        const int C = __shfl_sync(0xffffffffu, cinc, 31);
+                        const int off = cinc - nch;
+                        for (int cw = 0; cw < C; cw += kX) {
+                            const int c0 = max(0, cw - off), c1 = min(nch, cw + kX - off);
+                            for (int c = c0; c < c1; ++c) qx[off + c - cw] = (uint16_t)(e | (c << 7));
+                            __syncwarp();
+                            const int ccnt = min(kX, C - cw);
+                            for (int i = lane; i < ccnt; i += 32) {
+                                const int xi = qx[i];
+                                const int ent = qi[xi & 127];
+                                const int p = ent >> 7, g = ent & 127;
+                                const float* crow = rows + (p + 1) * cs;
+                                const int k0c = sgpoff[g] + 4 * (xi >> 7);
+                                const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
+                                unsigned long long tb = 0ull;
+                                uint32_t wmk = 0u;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int k = k0c + u;
+                                    const uint2 rec = sprec[min(k, k1c - 1)];
+                                    const float* ci = crow + (rec.x & 0xffu);
+                                    const float* cj = crow + ((rec.x >> 8) & 0xffu);
+                                    const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
+                                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                                    const float Rs = __uint_as_float(rec.y);
+                                    // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
+                                    if (k >= k1c || d2 >= Rs * Rs || Rs - sqrtf(d2) <= 0.f) continue;
+                                    const int pid = rec.x >> 16;
+                                    atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                                    wmk |= 1u << (pid >> 5);
+                                    tb |= (1ull << ((rec.x & 0xffu) / 3)) |
+                                          (1ull << (((rec.x >> 8) & 0xffu) / 3));
+                                }
+                                if (tb) {
+                                    atomicOr(touched + p, tb);
+                                    atomicOr(pwm + p, wmk);
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
                 }
-                return 0.f;
-            });
+            }
             __syncwarp();
             // gradients: one item per (pose, touched sphere), gathered over its
             // active pairs in canonical id order (for a fixed sphere: its

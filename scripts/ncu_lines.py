@@ -3,13 +3,16 @@
     python scripts/ncu_lines.py report.ncu-rep kernel_regex [top]
 """
 import csv
+import os
 import io
 import subprocess
 import sys
 
 rep, k = sys.argv[1], sys.argv[2]
+# NCU_LAUNCH=i picks the i-th matching launch of the report
+EXTRA = ["--launch-skip", os.environ["NCU_LAUNCH"], "--launch-count", "1"] if os.environ.get("NCU_LAUNCH") else []
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}", *EXTRA,
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Line No"'))

@@ -3,17 +3,20 @@
     python scripts/ncu_ranges.py report.ncu-rep kernel_regex name:lo-hi [name:lo-hi ...]
 """
 import csv
+import os
 import io
 import subprocess
 import sys
 
 rep, k = sys.argv[1], sys.argv[2]
+# NCU_LAUNCH=i picks the i-th matching launch of the report
+EXTRA = ["--launch-skip", os.environ["NCU_LAUNCH"], "--launch-count", "1"] if os.environ.get("NCU_LAUNCH") else []
 ranges = []
 for a in sys.argv[3:]:
     name, r = a.split(":")
     lo, hi = r.split("-")
     ranges.append((name, int(lo), int(hi)))
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}", *EXTRA,
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Line No"'))

@@ -1,6 +1,6 @@
 """Run a few vapr_cost_grad steps of the bench workload (config 4 per GPU) for
 ncu: `python scripts/prof_step.py [--formats 43bit] [--steps 3]`.
-Launch order per step: fk, collision, traj_reduce, aggregate, bk."""
+Launch order per step: fk, collision (world pass, self pass), traj_reduce, aggregate, bk."""
 import argparse
 import os
 import sys
