@@ -5,13 +5,15 @@
 // different format and hence a different packing factor.
 //
 // One CTA per tile of kRows pose rows.  Both input tiles are streamed into
-// shared memory with 16-byte coalesced loads; rows whose input words are all
-// zero are flagged on the way.  The inputs are >99 % zero in the paper's
-// workloads ("sparsity-aware computation by skipping zero
-// computations"): a flagged-zero row produces zero output words without any
-// decoding (+0 + +0 = +0 -> code 0), and inside a non-zero row an output word
-// whose overlapping input words are zero is zero as well.  Each thread emits
-// one 16-byte group of 4 output words (coalesced 16-byte stores).
+// shared memory with 16-byte coalesced loads, then three word-parallel passes
+// (each templated on its own packing factor): decode closest_pt into an FP32
+// tile, decode out_vec and add (all-zero words skipped: "sparsity-aware
+// computation by skipping zero computations"), encode the sums into packed
+// grad_out_spheres words (hardware cvt where exact) with coalesced stores.
+// The sum is the same single FP32 addition per element as before, so the
+// result is bit-identical to decode(cp) + decode(ov) -> encode.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -22,73 +24,84 @@ namespace {
 constexpr int kRows = 64;
 constexpr int kThreads = 256;
 
-// e / pf for e < 4096 and pf in 1..8 via a 16-bit reciprocal (exact there).
-__device__ __forceinline__ int div_pf(int e, uint32_t recip) { return int((e * recip) >> 16); }
+// Decode the packed tile `src` (rows of W words, pf values per word) into the
+// FP32 tile x (stride xs): x = value (ADD = false) or x += value (ADD = true).
+// One thread per word.  Pass 1 (ADD = false) raises *negz when it decodes a
+// -0.  Pass 2 skips an all-zero word (x + +0 = x) unless the tile holds a -0
+// (x = -0 needs the add: -0 + +0 = +0).
+template <int PF, bool ADD>
+__device__ __forceinline__ void decode_tile(const uint32_t* src, int W, int nr, int cols,
+                                            uint32_t rw, float* x, int xs, const Fmt& f,
+                                            int* negz) {
+    const bool skip_zero = ADD ? (*negz == 0) : true;
+    for (int i = threadIdx.x; i < nr * W; i += kThreads) {
+        const int r = int((uint32_t(i) * rw) >> 24), w = i - r * W;
+        const uint32_t v = src[i];
+        const int e0 = w * PF;
+        float* xr = x + r * xs + e0;
+        if (v == 0u && skip_zero) {
+            if (!ADD) {
+#pragma unroll
+                for (int j = 0; j < PF; ++j)
+                    if (e0 + j < cols) xr[j] = 0.f;
+            }
+            continue;
+        }
+        float d[PF];
+        decode_word_t<PF>(v, d, f);
+        bool nz = false;
+#pragma unroll
+        for (int j = 0; j < PF; ++j)
+            if (e0 + j < cols) {
+                if (!ADD) nz |= __float_as_uint(d[j]) == 0x80000000u;
+                xr[j] = ADD ? xr[j] + d[j] : d[j];
+            }
+        if (!ADD && nz) *negz = 1;
+    }
+}
 
 __global__ void __launch_bounds__(kThreads)
 aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, int Wo, int Wg,
                  const uint32_t* __restrict__ cp, const uint32_t* __restrict__ ov,
-                 long long rows, uint32_t* __restrict__ gos, uint32_t rc_cp, uint32_t rc_ov) {
+                 long long rows, uint32_t* __restrict__ gos, uint32_t rw_c, uint32_t rw_o,
+                 uint32_t rw_g, int xs) {
     extern __shared__ uint4 smem_a[];
     uint32_t* sc = reinterpret_cast<uint32_t*>(smem_a);     // [kRows * Wc]
     uint32_t* so = sc + kRows * Wc;                         // [kRows * Wo]
-    int* nz = reinterpret_cast<int*>(so + kRows * Wo);      // [kRows]
+    float* x = reinterpret_cast<float*>(so + kRows * Wo);   // [kRows * xs] FP32 sums
+    __shared__ int negz;
     const long long r0 = (long long)blockIdx.x * kRows;
     const int nr = (int)min((long long)kRows, rows - r0);
     const int tid = threadIdx.x;
-    if (tid < kRows) nz[tid] = 0;
-    __syncthreads();
+    if (tid == 0) negz = 0;
     {
         const uint4* gc = reinterpret_cast<const uint4*>(cp + r0 * Wc);
         const uint4* go = reinterpret_cast<const uint4*>(ov + r0 * Wo);
         const int qc = Wc / 4, qo = Wo / 4;
-        for (int i = tid; i < nr * qc; i += kThreads) {
-            const uint4 v = __ldcs(gc + i);
-            reinterpret_cast<uint4*>(sc)[i] = v;
-            if (v.x | v.y | v.z | v.w) nz[i / qc] = 1;
-        }
-        for (int i = tid; i < nr * qo; i += kThreads) {
-            const uint4 v = __ldcs(go + i);
-            reinterpret_cast<uint4*>(so)[i] = v;
-            if (v.x | v.y | v.z | v.w) nz[i / qo] = 1;
-        }
+#pragma unroll 4
+        for (int i = tid; i < nr * qc; i += kThreads) reinterpret_cast<uint4*>(sc)[i] = __ldcs(gc + i);
+#pragma unroll 4
+        for (int i = tid; i < nr * qo; i += kThreads) reinterpret_cast<uint4*>(so)[i] = __ldcs(go + i);
     }
     __syncthreads();
-    const int qg = Wg / 4;
-    uint4* dst = reinterpret_cast<uint4*>(gos + r0 * Wg);
+    with_pf(fcp.pf, [&](auto Pc) {
+        decode_tile<decltype(Pc)::value, false>(sc, Wc, nr, cols, rw_c, x, xs, fcp, &negz);
+    });
+    __syncthreads();
+    with_pf(fov.pf, [&](auto Pc) {
+        decode_tile<decltype(Pc)::value, true>(so, Wo, nr, cols, rw_o, x, xs, fov, &negz);
+    });
+    __syncthreads();
+    uint32_t* dst = gos + r0 * Wg;
     with_pf(fg.pf, [&](auto Pc) {
         constexpr int PF = decltype(Pc)::value;
-        for (int i = tid; i < nr * qg; i += kThreads) {
-            const int r = i / qg, g = i - r * qg;
-            uint32_t out[4] = {0u, 0u, 0u, 0u};
-            if (nz[r]) {
-                const uint32_t* crow = sc + r * Wc;
-                const uint32_t* orow = so + r * Wo;
+        for (int i = tid; i < nr * Wg; i += kThreads) {
+            const int r = int((uint32_t(i) * rw_g) >> 24), w = i - r * Wg;
+            const int e0 = w * PF;
+            float v[PF];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int e0 = (4 * g + k) * PF;
-                    if (e0 >= cols) continue;
-                    const int e1 = min(e0 + PF, cols) - 1;
-                    uint32_t any = 0;
-                    for (int m = div_pf(e0, rc_cp); m <= div_pf(e1, rc_cp); ++m) any |= crow[m];
-                    for (int m = div_pf(e0, rc_ov); m <= div_pf(e1, rc_ov); ++m) any |= orow[m];
-                    if (!any) continue;
-                    float x[PF];
-#pragma unroll
-                    for (int j = 0; j < PF; ++j) {
-                        const int e = e0 + j;
-                        x[j] = 0.f;
-                        if (e < cols) {
-                            const int ic = div_pf(e, rc_cp), io = div_pf(e, rc_ov);
-                            const uint32_t cc = code_at(crow[ic], e - ic * fcp.pf, fcp);
-                            const uint32_t co = code_at(orow[io], e - io * fov.pf, fov);
-                            if (cc | co) x[j] = decode(cc, fcp) + decode(co, fov);
-                        }
-                    }
-                    out[k] = encode_word_t<PF>(x, fg);
-                }
-            }
-            __stcs(dst + i, make_uint4(out[0], out[1], out[2], out[3]));
+            for (int j = 0; j < PF; ++j) v[j] = (e0 + j < cols) ? x[r * xs + e0 + j] : 0.f;
+            __stcs(dst + i, encode_word_t<PF>(v, fg));
         }
     });
 }
@@ -101,14 +114,22 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
     if (rows <= 0) return cudaSuccess;
     const int Wc = row_words_of(fcp, cols), Wo = row_words_of(fov, cols),
               Wg = row_words_of(fgos, cols);
-    const uint32_t rc_cp = 65536u / fcp.pf + 1u, rc_ov = 65536u / fov.pf + 1u;
-    const size_t smem = sizeof(uint32_t) * kRows * (Wc + Wo) + sizeof(int) * kRows;
+    // i / W for i < kRows * W via 24-bit reciprocals: exact while
+    // kRows W^2 < 2^24, and i * rw fits 32 bits
+    const uint32_t rw_c = (1u << 24) / Wc + 1u, rw_o = (1u << 24) / Wo + 1u,
+                   rw_g = (1u << 24) / Wg + 1u;
+    for (int Wx : {Wc, Wo, Wg})
+        if ((long long)kRows * Wx * Wx >= (1 << 24) ||
+            (long long)kRows * Wx * ((1u << 24) / Wx + 1u) >= (1ll << 32))
+            return cudaErrorInvalidValue;
+    const int xs = cols | 1;                     // odd stride: word-parallel passes spread over banks
+    const size_t smem = sizeof(uint32_t) * kRows * (Wc + Wo) + sizeof(float) * kRows * xs;
     cudaError_t e = cudaFuncSetAttribute(aggregate_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long grid = (rows + kRows - 1) / kRows;
     aggregate_kernel<<<(unsigned)grid, kThreads, smem, s>>>(fcp, fov, fgos, cols, Wc, Wo, Wg, cp,
-                                                            ov, rows, gos, rc_cp, rc_ov);
+                                                            ov, rows, gos, rw_c, rw_o, rw_g, xs);
     return cudaGetLastError();
 }
 

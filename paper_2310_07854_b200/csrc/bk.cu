@@ -9,9 +9,9 @@
 // (reading c20: the Jacobian of the true FK, not of the quantised spheres).
 //
 // The CTA streams its tile of packed gradient rows into shared memory with
-// coalesced loads and, for the rare non-zero words, marks the spheres they
-// touch in a per-pose 64-bit mask.  One thread per pose then runs the chain
-// only if its mask is non-zero; each link's (F_l, M_l) is folded into the
+// coalesced 16-byte loads; each thread then finds its pose's non-zero spheres
+// (a 64-bit mask, SWAR test per word) and runs the chain only if the mask is
+// non-zero; each link's (F_l, M_l) is folded into the
 // joint accumulators j <= l as soon as the link's frame is known, so no frame
 // is stored and no prefix/total difference (cancellation) is formed.
 #include "common.cuh"
@@ -26,55 +26,64 @@ constexpr int kTile = 128;                 // poses (= threads) per CTA
 __global__ void __launch_bounds__(kTile)
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
-          uint32_t rc) {
+          uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt) {
     extern __shared__ unsigned long long smem8[];
-    const int WS = W + 1;
-    unsigned long long* smask = smem8;                                // [kTile]
-    float4* so = reinterpret_cast<float4*>(smask + kTile);            // [kMaxSpheres] sphere offsets
+    const int WS = W + 4;                 // 16-byte aligned rows
+    float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
     float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
     uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
 
-    smask[tid] = 0ull;
     // sphere offsets are indexed per lane (by each pose's non-zero spheres):
     // stage them in shared memory instead of the serialising constant bank
     for (int i = tid; i < R.n_spheres; i += kTile) so[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
     for (int i = tid; i < np * kJoints; i += kTile) sq[i] = __ldcs(q + p0 * kJoints + i);
     __syncthreads();
     {
-        const int nw = np * W;
-        const uint32_t* src = gos + p0 * W;
-        const int dr = kTile / W, dw = kTile % W;
-        int r = tid / W, w = tid - (tid / W) * W;
-        for (int i = tid; i < nw; i += kTile) {
-            const uint32_t v = __ldcs(src + i);
-            sw[r * WS + w] = v;
-            if (v) {
-                unsigned long long m = 0;
-                for (int j = 0; j < f.pf; ++j)
-                    if (code_at(v, j, f)) {
-                        const int e = w * f.pf + j;
-                        if (e < R.cols) m |= 1ull << (e / 3);
-                    }
-                atomicOr(smask + r, m);
-            }
-            r += dr;
-            w += dw;
-            if (w >= W) {
-                w -= W;
-                ++r;
-            }
+        // plain 16-byte copy of the tile (rows are 16-byte multiples), several
+        // loads in flight
+        const int Q = W / 4, nq = np * Q;
+        const uint4* src = reinterpret_cast<const uint4*>(gos + p0 * W);
+#pragma unroll 4
+        for (int i = tid; i < nq; i += kTile) {
+            const uint4 v = __ldcs(src + i);
+            const int r = int((uint32_t(i) * rq) >> 20), g = i - r * Q;
+            *reinterpret_cast<uint4*>(sw + r * WS + 4 * g) = v;
         }
     }
     __syncthreads();
+
+    // the pose's non-zero spheres, from its own row (16-byte reads, stride
+    // W + 4 words: conflict-free per quarter warp); a word's non-zero fields
+    // come from one SWAR test, the rare non-zero words are then walked
+    unsigned long long mask = 0ull;
+    if (tid < np) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(sw + tid * WS);
+        for (int g = 0; g < W / 4; ++g) {
+            const uint4 v = r4[g];
+            if (!(v.x | v.y | v.z | v.w)) continue;
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // top bit of each t-bit field set iff the field is non-zero
+                uint32_t nzf = (((w4[k] & f_lo) + f_lo) | w4[k]) & f_hi;
+                const int ebase = (4 * g + k) * f.pf;
+                while (nzf) {
+                    const int b = __ffs(nzf) - 1;
+                    nzf &= nzf - 1;
+                    const int e = ebase + int(((uint32_t)(b + 1) * rt) >> 16) - 1;
+                    if (e < R.cols) mask |= 1ull << (e / 3);
+                }
+            }
+        }
+    }
 
     float gq[kJoints];
 #pragma unroll
     for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
 
-    const unsigned long long mask = (tid < np) ? smask[tid] : 0ull;
     if (mask) {
         const uint32_t* row = sw + tid * WS;
         float zx[kJoints], zy[kJoints], zz[kJoints], ox[kJoints], oy[kJoints], oz[kJoints];
@@ -145,15 +154,25 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
                       const uint32_t* gos, float* grad_q, cudaStream_t s) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
-    const size_t smem = sizeof(unsigned long long) * kTile + sizeof(float4) * kMaxSpheres +
+    const size_t smem = sizeof(float4) * kMaxSpheres +
                         sizeof(float) * kTile * kJoints +
-                        sizeof(uint32_t) * kTile * (W + 1);
+                        sizeof(uint32_t) * kTile * (W + 4);
     cudaError_t e = cudaFuncSetAttribute(bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     const uint32_t rc = 65536u / fgos.pf + 1u;
+    const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
+    // SWAR masks of the format's fields: top bits, low t-1 bits; slot = (b+1)/t - 1
+    uint32_t f_lo = 0u, f_hi = 0u;
+    for (int j = 0; j < fgos.pf; ++j) {
+        const int at = j * fgos.t;
+        f_hi |= 1u << (at + fgos.t - 1);
+        f_lo |= (uint32_t)(((1ull << (fgos.t - 1)) - 1ull) << at);
+    }
+    const uint32_t rt = 65536u / fgos.t + 1u;
     const long long grid = (P + kTile - 1) / kTile;
-    bk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc);
+    bk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc, rq, f_lo,
+                                                  f_hi, rt);
     return cudaGetLastError();
 }
 

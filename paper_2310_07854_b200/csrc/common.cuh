@@ -125,6 +125,35 @@ __device__ __forceinline__ uint32_t cvt_e3m2x2(float lo, float hi) {
     return r;
 }
 
+// One value -> its code: the hardware conversion where it is bit-identical to
+// the reading (|x| below the format's hw_limit, non-NaN), the generic integer
+// path elsewhere.  Exact either way, so the choice may be made per value.
+__device__ __forceinline__ uint32_t encode1(float x, const Fmt& f) {
+    if (f.kind == KIND_IDENTITY) return __float_as_uint(x);
+    const uint32_t a = __float_as_uint(x) & 0x7fffffffu;
+    if (a < f.hw_limit) {
+        switch (f.kind) {
+            case KIND_F16: {
+                uint16_t h;
+                asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(x));
+                return h;
+            }
+            case KIND_BF16: {
+                uint16_t h;
+                asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
+                return h;
+            }
+            case KIND_E4M3: return cvt_e4m3x2(x, 0.f) & 0xffu;
+            case KIND_E5M2: return cvt_e5m2x2(x, 0.f) & 0xffu;
+            case KIND_E2M1: return cvt_e2m1x2(x, 0.f) & 0xfu;
+            case KIND_E2M3: return cvt_e2m3x2(x, 0.f) & 0x3fu;
+            case KIND_E3M2: return cvt_e3m2x2(x, 0.f) & 0x3fu;
+            default: break;
+        }
+    }
+    return encode_generic(x, f);
+}
+
 // Encode PF values x[0..PF) into one packed word (the caller sets values
 // beyond the row end to +0).  Formats with a hardware conversion use it unless
 // some value of the word needs the reading's special handling (top binade,
