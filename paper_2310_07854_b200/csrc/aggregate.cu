@@ -21,8 +21,8 @@ namespace vapr {
 
 namespace {
 
-constexpr int kRows = 64;
-constexpr int kThreads = 256;
+constexpr int kRows = 32;
+constexpr int kThreads = 128;
 
 // Decode the packed tile `src` (rows of W words, pf values per word) into the
 // FP32 tile x (stride xs): x = value (ADD = false) or x += value (ADD = true).
@@ -42,8 +42,7 @@ __device__ __forceinline__ void decode_tile(const uint32_t* src, int W, int nr, 
         if (v == 0u && skip_zero) {
             if (!ADD) {
 #pragma unroll
-                for (int j = 0; j < PF; ++j)
-                    if (e0 + j < cols) xr[j] = 0.f;
+                for (int j = 0; j < PF; ++j) xr[j] = 0.f;
             }
             continue;
         }
@@ -51,11 +50,10 @@ __device__ __forceinline__ void decode_tile(const uint32_t* src, int W, int nr, 
         decode_word_t<PF>(v, d, f);
         bool nz = false;
 #pragma unroll
-        for (int j = 0; j < PF; ++j)
-            if (e0 + j < cols) {
-                if (!ADD) nz |= __float_as_uint(d[j]) == 0x80000000u;
-                xr[j] = ADD ? xr[j] + d[j] : d[j];
-            }
+        for (int j = 0; j < PF; ++j) {
+            if (!ADD) nz |= __float_as_uint(d[j]) == 0x80000000u;
+            xr[j] = ADD ? xr[j] + d[j] : d[j];
+        }
         if (!ADD && nz) *negz = 1;
     }
 }
@@ -92,6 +90,12 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
         decode_tile<decltype(Pc)::value, true>(so, Wo, nr, cols, rw_o, x, xs, fov, &negz);
     });
     __syncthreads();
+    // slots past the last element encode as code 0 whatever the inputs' padding
+    for (int i = tid; i < nr * (xs - cols); i += kThreads) {
+        const int r = i / (xs - cols);
+        x[r * xs + cols + (i - r * (xs - cols))] = 0.f;
+    }
+    __syncthreads();
     uint32_t* dst = gos + r0 * Wg;
     with_pf(fg.pf, [&](auto Pc) {
         constexpr int PF = decltype(Pc)::value;
@@ -100,7 +104,7 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
             const int e0 = w * PF;
             float v[PF];
 #pragma unroll
-            for (int j = 0; j < PF; ++j) v[j] = (e0 + j < cols) ? x[r * xs + e0 + j] : 0.f;
+            for (int j = 0; j < PF; ++j) v[j] = x[r * xs + e0 + j];
             __stcs(dst + i, encode_word_t<PF>(v, fg));
         }
     });
@@ -122,7 +126,9 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
         if ((long long)kRows * Wx * Wx >= (1 << 24) ||
             (long long)kRows * Wx * ((1u << 24) / Wx + 1u) >= (1ll << 32))
             return cudaErrorInvalidValue;
-    const int xs = cols | 1;                     // odd stride: word-parallel passes spread over banks
+    // FP32 tile wide enough for every word of all three rows (the padding
+    // slots hold +0), odd stride: the word-parallel passes spread over banks
+    const int xs = std::max(Wc * fcp.pf, std::max(Wo * fov.pf, Wg * fgos.pf)) | 1;
     const size_t smem = sizeof(uint32_t) * kRows * (Wc + Wo) + sizeof(float) * kRows * xs;
     cudaError_t e = cudaFuncSetAttribute(aggregate_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
