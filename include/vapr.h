@@ -124,6 +124,10 @@ vapr_status vapr_create(int device, vapr_ctx **out);
 vapr_status vapr_destroy(vapr_ctx *ctx);
 const char *vapr_status_string(vapr_status s);
 const char *vapr_version(void);
+/* The CUDA runtime's error string behind the most recent VAPR_ERR_CUDA
+ * returned on the calling host thread ("no error" if none); a static string
+ * owned by the CUDA runtime, never freed by the caller.  Diagnostics only. */
+const char *vapr_last_cuda_error(void);
 
 /* "E<e>M<m>", case-insensitive. */
 vapr_status vapr_format_parse(const char *s, vapr_format *out);

@@ -27,6 +27,7 @@ STATUS = {0: "VAPR_OK", 1: "VAPR_ERR_INVALID_FORMAT", 2: "VAPR_ERR_INVALID_ARG",
 
 # every symbol include/vapr.h declares (checked by tests/test_abi.py)
 EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
+           "vapr_last_cuda_error",
            "vapr_format_parse", "vapr_format_check", "vapr_packed_row_words",
            "vapr_set_formats", "vapr_set_robot", "vapr_set_worlds", "vapr_set_option",
            "vapr_quantize", "vapr_dequantize", "vapr_fk_spheres", "vapr_world_collision",
@@ -71,6 +72,7 @@ def _load():
         "vapr_destroy": ([P], I32),
         "vapr_status_string": ([I32], ctypes.c_char_p),
         "vapr_version": ([], ctypes.c_char_p),
+        "vapr_last_cuda_error": ([], ctypes.c_char_p),
         "vapr_format_parse": ([ctypes.c_char_p, ctypes.POINTER(vapr_format)], I32),
         "vapr_format_check": ([vapr_format], I32),
         "vapr_packed_row_words": ([vapr_format, SZ], SZ),
@@ -103,6 +105,8 @@ lib = _load()
 
 def _check(st, where):
     if st != 0:
+        if STATUS.get(st) == "VAPR_ERR_CUDA":
+            where = f"{where} [{lib.vapr_last_cuda_error().decode()}]"
         raise VaprError(st, where)
 
 

@@ -87,12 +87,18 @@ Fmt make_fmt(vapr_format v) {
     return f;
 }
 
-vapr_status cuda_status(cudaError_t e) { return e == cudaSuccess ? VAPR_OK : VAPR_ERR_CUDA; }
+thread_local cudaError_t t_last_cuda_error = cudaSuccess;
+
+vapr_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return VAPR_OK;
+    t_last_cuda_error = e;
+    return VAPR_ERR_CUDA;
+}
 
 vapr_status pending_fault() {
     // surface an earlier asynchronous fault without clearing sticky errors
     const cudaError_t e = cudaPeekAtLastError();
-    return e == cudaSuccess ? VAPR_OK : VAPR_ERR_CUDA;
+    return cuda_status(e);
 }
 
 #define CHECK(cond, st) \
@@ -113,6 +119,8 @@ WorldsDev worlds_of(const vapr_ctx* c) { return WorldsDev{c->d_cub, c->d_off, c-
 extern "C" {
 
 const char* vapr_version(void) { return "libvapr 0.1 (sm_100a)"; }
+
+const char* vapr_last_cuda_error(void) { return cudaGetErrorString(t_last_cuda_error); }
 
 const char* vapr_status_string(vapr_status s) {
     switch (s) {

@@ -179,6 +179,13 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #define VAPR_PHASE_SYNC 0
 #endif
 constexpr int kDecUnroll = VAPR_DEC_UNROLL;
+#ifdef VAPR_STATS
+// work counters of the variant build -DVAPR_STATS (scripts/collision_stats.py)
+__device__ unsigned long long g_stats[8];
+#define VAPR_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define VAPR_STAT(i, v)
+#endif
 constexpr int kLPP = 2;            // lanes per pose: lane = half * 16 + p
 constexpr int kPL = 32 / kLPP;     // pose lanes per half
 constexpr int kTP = kPL - 1;       // poses per warp tile (pose lane kPL-1: the halo pose)
@@ -578,6 +585,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             __syncwarp();
             // live (pose, sphere) items: the complete gradient of the sphere
             // (no scatter), its codes ORed into the packed tile row
+            VAPR_STAT(0, __popcll(smask));
             wcost = warp_queue<1>(smask, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
                 const int p = it >> 6, sp = it & 63;
                 const int l = slink[sp];
@@ -629,6 +637,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                             m = m_bwd;
                         }
                     }
+                    VAPR_STAT(1, __popc(m));
                     for (; m; m &= m - 1)
                         world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
                                    a.w_w, cw, gw, acc);
@@ -663,6 +672,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
             ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
             if (!owner) glo = ghi = 0ull;
+            VAPR_STAT(2, __popcll(glo) + __popcll(ghi));
             // narrowphase: the live (pose, group pair) entries are listed, each
             // expanded into chunks of <= 4 candidate pairs, one chunk per lane
             // (balanced whatever the group-pair sizes); active pairs are marked
@@ -722,6 +732,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 const float* crow = rows + (p + 1) * cs;
                                 const int k0c = sgpoff[g] + 4 * (xi >> 7);
                                 const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
+                                VAPR_STAT(3, 1);
+                                VAPR_STAT(4, k1c - k0c);
                                 unsigned long long tb = 0ull;
                                 uint32_t wmk = 0u;
 #pragma unroll
@@ -758,6 +770,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // order); the item also returns the cost of the pairs it leads
             // (i == s), so a pose's self cost is summed in pair-id order
             const unsigned long long tb = owner ? touched[pl] : 0ull;
+            VAPR_STAT(5, __popcll(tb));
+            if (owner) VAPR_STAT(6, __popc(pwm[pl]));
             scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
                 const int p = it >> 6, s = it & 63;
                 const float* crow = rows + (p + 1) * cs;
@@ -783,6 +797,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 return c_lead;
             });
         }
+        if (owner) VAPR_STAT(7, 1);
         if (owner) {
             const float c = wcost + scost;
             a.cost[p0 + pl] = a.cost_accumulate ? a.cost[p0 + pl] + c : c;
@@ -820,6 +835,17 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
 
 
 }  // namespace
+
+#ifdef VAPR_STATS
+extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                                   const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,

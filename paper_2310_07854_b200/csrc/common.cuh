@@ -171,7 +171,11 @@ __device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) 
         for (int j = 0; j < PF; ++j) w |= ((__float_as_uint(x[j]) >> (32 - f.t)) & f.signbit) << (j * f.t);
         return w;
     }
+#ifdef VAPR_NO_HW_ENCODE
+    if (false) {
+#else
     if (amax < f.hw_limit) {
+#endif
         if constexpr (PF == 2) {
             if (f.kind == KIND_F16) return cvt_f16x2(x[0], x[1]);
             if (f.kind == KIND_BF16) return cvt_bf16x2(x[0], x[1]);

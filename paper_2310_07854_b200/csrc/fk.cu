@@ -39,8 +39,9 @@ struct Emitter {
         }
     }
     __device__ __forceinline__ void flush(uint32_t* row, int W, const Fmt& f) {
-        if (count) {
-            while (count < PF) push(0.f, row, f);   // the tail of the last word is +0
+        if (count) {                                // the tail of the last word is +0
+            const int pad = PF - count;
+            for (int k = 0; k < pad; ++k) push(0.f, row, f);
         }
         for (; word < W; ++word) row[word] = 0u;    // 16-byte row padding
     }

@@ -148,6 +148,9 @@ WORKLOADS = {
     "bookshelf_tall": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="bookshelf_tall"),
     "fp16": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="fp16"),
     "fp32": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="fp32"),
+    "pf5_pf8": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="pf5_pf8"),
+    "pf3": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="pf3"),
+    "bf16": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="bf16"),
 }
 
 

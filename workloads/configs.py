@@ -33,6 +33,11 @@ FORMAT_SETS = {
     "config1_e4m3": ((4, 3),) + ((8, 23),) * 4,
     # per-slot maxima of Table II quoted in the appendix
     "maxima46": ((5, 10), (4, 3), (3, 2), (4, 3), (4, 3)),
+    # packing-factor coverage for the parity tests: pf 5 and 8 leave a
+    # partial last word in a 156-element row; pf 3 (t = 10); E8M7 (bf16 cvt)
+    "pf5_pf8": ((2, 3), (2, 1), (3, 2), (2, 1), (4, 1)),
+    "pf3": ((5, 4), (3, 6), (6, 3), (2, 7), (4, 5)),
+    "bf16": ((8, 7),) * 5,
 }
 FORMAT_SETS["43bit"] = FORMAT_SETS["table_under_pick"]
 
