@@ -169,8 +169,8 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 // Shared-memory carve-up, computed once on the host and passed by value:
 // the robot tables every warp of the CTA reads (staged once per CTA), then one
 // private workspace per warp.
-#ifndef VAPR_DEC_UNROLL
-#define VAPR_DEC_UNROLL 2
+#ifndef VAPR_DEC_LOADS          // 16-byte loads in flight per lane in the tile decode
+#define VAPR_DEC_LOADS 2
 #endif
 #ifndef VAPR_FUSED_SPLIT         // 1: world and self as two passes
 #define VAPR_FUSED_SPLIT 1
@@ -178,7 +178,7 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_PHASE_SYNC          // 1: CTA barriers between the phases of a tile
 #define VAPR_PHASE_SYNC 0
 #endif
-constexpr int kDecUnroll = VAPR_DEC_UNROLL;
+constexpr int kDecLoads = VAPR_DEC_LOADS;
 #ifdef VAPR_STATS
 // work counters of the variant build -DVAPR_STATS (scripts/collision_stats.py)
 __device__ unsigned long long g_stats[8];
@@ -453,20 +453,33 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             float* dst0 = rows + row_off * cs;
             with_pf(fos.pf, [&](auto Pc) {
                 constexpr int PF = decltype(Pc)::value;
-#pragma unroll kDecUnroll
-                for (int q = lane; q < nq; q += 32) {
-                    const int r = int((uint32_t(q) * G.rc_q) >> 20);
-                    const int g = q - r * G.Qos;
-                    const uint4 v = __ldg(src + q);
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                    float x[4 * PF];
+                // kDecLoads 16-byte loads in flight per lane, then one word
+                // at a time through the decoder (few live temporaries)
+                for (int q0 = lane; q0 < nq; q0 += 32 * kDecLoads) {
+                    uint4 v[kDecLoads];
 #pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4) decode_word_t<PF>(w4[j4], x + j4 * PF, fos);
-                    float* d = dst0 + r * cs + 4 * PF * g;
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
+                        v[u] = (q < nq) ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
+                    }
 #pragma unroll
-                    for (int j = 0; j < 4 * PF; ++j) {
-                        d[j] = x[j];
-                        amax = fmaxf(amax, fabsf(x[j]));
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
+                        if (q >= nq) break;
+                        const int r = int((uint32_t(q) * G.rc_q) >> 20);
+                        const int g = q - r * G.Qos;
+                        float* d = dst0 + r * cs + 4 * PF * g;
+                        const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4) {
+                            float x[PF];
+                            decode_word_t<PF>(w4[j4], x, fos);
+#pragma unroll
+                            for (int j = 0; j < PF; ++j) {
+                                d[j4 * PF + j] = x[j];
+                                amax = fmaxf(amax, fabsf(x[j]));
+                            }
+                        }
                     }
                 }
             });
