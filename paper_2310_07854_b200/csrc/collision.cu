@@ -205,7 +205,7 @@ struct Geo {
     // CTA tables (byte offsets from the start of dynamic shared memory)
     unsigned sr, rl, ref, pij, prec, grec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
-    unsigned rows, pmask, touched, pwm, wm, pk0, qi, qc, warp;
+    unsigned rows, pmask, pwm, wm, pk0, qi, qc, warp;
 };
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
@@ -254,7 +254,6 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.tables = take(0, 16);
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
-    g.touched = take(do_self ? 8u * kTP : 0u, 8);
     g.pmask = take(do_self ? 4u * kTP * g.pmw : 0u, 4);
     g.pwm = take(do_self ? 4u * kTP : 0u, 4);
     g.wm = take(do_world ? 4u * kTP * kLinks : 0u, 4);
@@ -263,6 +262,17 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.qc = take(4u * kQ, 4);
     g.warp = take(0, 16);
     return g;
+}
+
+// bit i of x -> bit 2i of the result
+__device__ __forceinline__ unsigned long long spread_bits(uint32_t x) {
+    unsigned long long v = x;
+    v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
 }
 
 // Warp work queue.  Every lane owns the items given by the set bits of its
@@ -394,7 +404,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     // ---- the warp's workspace
     char* wb = base + G.tables + (unsigned)warp * G.warp;
     float* rows = reinterpret_cast<float*>(wb + G.rows);
-    unsigned long long* touched = reinterpret_cast<unsigned long long*>(wb + G.touched);
     uint32_t* pmask = reinterpret_cast<uint32_t*>(wb + G.pmask);
     uint32_t* pwm = reinterpret_cast<uint32_t*>(wb + G.pwm);
     uint32_t* wm = reinterpret_cast<uint32_t*>(wb + G.wm);
@@ -496,10 +505,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             for (int i = lane; i < np * G.Wov / 4; i += 32)
                 reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
-            if (lane < kTP) {
-                touched[lane] = 0ull;
-                pwm[lane] = 0u;
-            }
+            if (lane < kTP) pwm[lane] = 0u;
         }
         if (a.do_world && half == 0 && pl < kTP) pk0[pl] = k0;
         __syncwarp();
@@ -667,23 +673,29 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         if (a.do_self) {
             // broadphase, per pose (uniform loop, the two lanes of a pose split
             // the list): every half-link group pair, a ball-ball test
-            unsigned long long glo = 0ull, ghi = 0ull;
+            // bit it of a0/a1 (it < 32 / >= 32) <- group pair g = kLPP it + half
+            uint32_t a0 = 0u, a1 = 0u;
             if (pl < np) {
                 const float m2 = 2.f * margin;
-                for (int g = half; g < G.ngp; g += kLPP) {
-                    const uint2 r = sgrec[g];
+#pragma unroll 2
+                for (int it = 0; kLPP * it + half < G.ngp; ++it) {
+                    const uint2 r = sgrec[kLPP * it + half];
                     const float* ca = myrow + (r.x & 0xffu);
                     const float* cb = myrow + ((r.x >> 8) & 0xffu);
                     const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
                     const float lim = __uint_as_float(r.y) + m2;
-                    if (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) {
-                        if (g < 64) glo |= 1ull << g;
-                        else ghi |= 1ull << (g - 64);
-                    }
+                    const uint32_t live =
+                        (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) ? 1u : 0u;
+                    if (it < 32) a0 |= live << it;
+                    else a1 |= live << (it - 32);
                 }
             }
-            glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
-            ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
+            // interleave the two halves' bits into the group-pair mask
+            static_assert(kLPP == 2, "the interleave below assumes two lanes per pose");
+            const uint32_t b0 = __shfl_xor_sync(0xffffffffu, a0, kPL);
+            const uint32_t b1 = __shfl_xor_sync(0xffffffffu, a1, kPL);
+            unsigned long long glo = spread_bits(half ? b0 : a0) | (spread_bits(half ? a0 : b0) << 1);
+            unsigned long long ghi = spread_bits(half ? b1 : a1) | (spread_bits(half ? a1 : b1) << 1);
             if (!owner) glo = ghi = 0ull;
             VAPR_STAT(2, __popcll(glo) + __popcll(ghi));
             // narrowphase: the live (pose, group pair) entries are listed, each
@@ -747,7 +759,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
                                 VAPR_STAT(3, 1);
                                 VAPR_STAT(4, k1c - k0c);
-                                unsigned long long tb = 0ull;
                                 uint32_t wmk = 0u;
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
@@ -763,13 +774,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                     const int pid = rec.x >> 16;
                                     atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
                                     wmk |= 1u << (pid >> 5);
-                                    tb |= (1ull << ((rec.x & 0xffu) / 3)) |
-                                          (1ull << (((rec.x >> 8) & 0xffu) / 3));
                                 }
-                                if (tb) {
-                                    atomicOr(touched + p, tb);
-                                    atomicOr(pwm + p, wmk);
-                                }
+                                if (wmk) atomicOr(pwm + p, wmk);
                             }
                             __syncwarp();
                         }
@@ -782,7 +788,16 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // partners ascending, independent of culling and of the task
             // order); the item also returns the cost of the pairs it leads
             // (i == s), so a pose's self cost is summed in pair-id order
-            const unsigned long long tb = owner ? touched[pl] : 0ull;
+            // the pose's touched spheres, from its active pairs
+            unsigned long long tb = 0ull;
+            if (owner)
+                for (uint32_t wmk = pwm[pl]; wmk; wmk &= wmk - 1) {
+                    const int wd = __ffs(wmk) - 1;
+                    for (uint32_t m = pmask[pl * PMW + wd]; m; m &= m - 1) {
+                        const int ij = spij[(wd << 5) + __ffs(m) - 1];
+                        tb |= (1ull << (ij & 0xff)) | (1ull << (ij >> 8));
+                    }
+                }
             VAPR_STAT(5, __popcll(tb));
             if (owner) VAPR_STAT(6, __popc(pwm[pl]));
             scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
