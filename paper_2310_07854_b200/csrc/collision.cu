@@ -812,7 +812,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         const int pid = (wd << 5) + __ffs(m) - 1;
                         const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
                         float vx, vy, vz, c;
-                        self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c);
+                        // always active here (same test as the narrowphase that marked it)
+                        if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy,
+                                       vz, c))
+                            continue;
                         const float sg = (i == s) ? -1.f : 1.f;
                         gx = fmaf(sg, vx, gx);
                         gy = fmaf(sg, vy, gy);
