@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--problems-per-env", type=int, default=100)
     ap.add_argument("--seeds", type=int, default=100)
     ap.add_argument("--H", type=int, default=32)
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="e2e: trajectory chunks of the pipelined host call (0 = automatic)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-sample-poses", type=int, default=20480)
@@ -299,10 +301,11 @@ def main():
     ct_host = torch.empty(wl.B, dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        r.q.view(-1).copy_(q_host.view(-1), non_blocking=True)
-        step()
-        gq_host.copy_(r.grad_q, non_blocking=True)
-        ct_host.copy_(r.cost_traj, non_blocking=True)
+        # vapr_cost_grad_host: H2D of q, compute and D2H of grad_q / cost_traj
+        # pipelined over trajectory chunks (the public host-buffer call)
+        r.run_host(q_host, gq_host, ct_host, n_chunks=args.chunks)
+        vb.vapr_best_per_problem(r.cost_traj, n_prob, args.seeds, best_c, best_s)
+        gather_best(best_c, best_s, world)
 
     e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
     h2d = q_host.numel() * 4
@@ -336,7 +339,7 @@ def main():
             "hbm_frac_step": a_min * P / (ms * 1e-3) / 1e9 / hbm,
             "bytes_per_pose_alg": a_min,
             "roofline": roofline,
-            "e2e": {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT,
+            "e2e": {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT, "chunks": args.chunks,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "fp32": fp32,

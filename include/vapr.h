@@ -221,6 +221,28 @@ vapr_status vapr_cost_grad(vapr_ctx *ctx, const float *q, const int32_t *world_i
                            void *workspace, size_t workspace_bytes,
                            float *cost_pose, float *cost_traj, float *grad_q, void *stream);
 
+/* The same computation from HOST buffers: q_host [B, H, 7] in, grad_q_host
+ * [B, H, 7] and cost_traj_host [B] (nullable) out, with the host<->device
+ * copies pipelined against the compute.  The batch is split into n_chunks
+ * contiguous trajectory ranges (0 = automatic: about 320k poses per chunk);
+ * chunk i's H2D copy, chunk i-1's compute and chunk i-2's D2H copies run
+ * concurrently on two context-owned copy streams and `stream`.  Every output
+ * is bit-identical to vapr_cost_grad's (the kernels see the same rows).
+ * Device buffers (caller-owned): q_dev [B*H*7], workspace (as for
+ * vapr_cost_grad), cost_pose_dev [B*H] (nullable: workspace scratch),
+ * cost_traj_dev [B], grad_q_dev [B*H*7].  Host buffers should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to overlap; pageable
+ * memory works but serialises.  The call is stream-ordered: it returns after
+ * enqueueing, and everything (including the D2H copies) is complete when
+ * `stream` is.  Errors: as vapr_cost_grad; VAPR_ERR_INVALID_ARG for null or
+ * misaligned device buffers or n_chunks < 0. */
+vapr_status vapr_cost_grad_host(vapr_ctx *ctx, const float *q_host, const int32_t *world_idx,
+                                int32_t B, int32_t H, const vapr_cost_params *params,
+                                void *workspace, size_t workspace_bytes, float *q_dev,
+                                float *cost_pose_dev, float *cost_traj_dev, float *grad_q_dev,
+                                float *cost_traj_host, float *grad_q_host, int32_t n_chunks,
+                                void *stream);
+
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =
  * its lowest argmin; problem p owns trajectories [p*seeds, (p+1)*seeds). */

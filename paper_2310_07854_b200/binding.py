@@ -33,7 +33,8 @@ EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
            "vapr_quantize", "vapr_dequantize", "vapr_fk_spheres", "vapr_world_collision",
            "vapr_self_collision", "vapr_collision", "vapr_aggregate",
            "vapr_backward_kinematics", "vapr_cost_grad_workspace_bytes",
-           "vapr_cost_grad_workspace_layout", "vapr_cost_grad", "vapr_best_per_problem")
+           "vapr_cost_grad_workspace_layout", "vapr_cost_grad", "vapr_cost_grad_host",
+           "vapr_best_per_problem")
 
 
 class VaprError(RuntimeError):
@@ -91,6 +92,8 @@ def _load():
         "vapr_cost_grad_workspace_bytes": ([P, I32, I32], SZ),
         "vapr_cost_grad_workspace_layout": ([P, I32, I32, I32, ctypes.POINTER(SZ * 5)], I32),
         "vapr_cost_grad": ([P, P, P, I32, I32, ctypes.POINTER(vapr_cost_params), P, SZ, P, P, P, P], I32),
+        "vapr_cost_grad_host": ([P, P, P, I32, I32, ctypes.POINTER(vapr_cost_params), P, SZ, P, P, P,
+                                 P, P, P, I32, P], I32),
         "vapr_best_per_problem": ([P, I32, I32, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
@@ -116,6 +119,17 @@ def _ptr(t):
         return None
     if not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(t):
+    """Host pointer of a contiguous CPU tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if t.is_cuda:
+        raise ValueError("expected a host (CPU) tensor")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
     return ctypes.c_void_p(t.data_ptr())
@@ -273,3 +287,16 @@ def vapr_cost_grad(ctx, q, world_idx, B, H, params, workspace, cost_pose, cost_t
     _check(lib.vapr_cost_grad(ctx, _ptr(q), _ptr(world_idx), B, H, ctypes.byref(p),
                               _ptr(workspace), nbytes, _ptr(cost_pose), _ptr(cost_traj),
                               _ptr(grad_q), _stream(stream)), "vapr_cost_grad")
+
+
+def vapr_cost_grad_host(ctx, q_host, world_idx, B, H, params, workspace, q_dev, cost_pose_dev,
+                        cost_traj_dev, grad_q_dev, cost_traj_host, grad_q_host, n_chunks=0,
+                        stream=None, _p=None):
+    """Host-buffer variant with pipelined copies (include/vapr.h)."""
+    p = _p if _p is not None else cost_params(params)
+    nbytes = workspace.numel() * workspace.element_size()
+    _check(lib.vapr_cost_grad_host(ctx, _hptr(q_host), _ptr(world_idx), B, H, ctypes.byref(p),
+                                   _ptr(workspace), nbytes, _ptr(q_dev), _ptr(cost_pose_dev),
+                                   _ptr(cost_traj_dev), _ptr(grad_q_dev), _hptr(cost_traj_host),
+                                   _hptr(grad_q_host), int(n_chunks), _stream(stream)),
+           "vapr_cost_grad_host")

@@ -26,6 +26,13 @@ struct vapr_ctx {
     int32_t* d_off = nullptr;
     int32_t n_worlds = 0;
     int cull = 1;
+    // vapr_cost_grad_host: copy streams and an event pool (created lazily)
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> events;
+    // collision tile-scheduler slots (device, kSchedSlots x {next, done}) and
+    // the host-side slot cursor
+    unsigned int* d_sched = nullptr;
+    unsigned int sched_next = 0;
 };
 
 namespace {
@@ -147,6 +154,16 @@ vapr_status vapr_create(int device, vapr_ctx** out) {
     CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
     c->device = device;
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    {
+        DeviceGuard g(device);
+        if (!g.ok || cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess ||
+            cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess) {
+            if (c->d_sched) cudaFree(c->d_sched);
+            delete c;
+            cudaGetLastError();
+            return VAPR_ERR_CUDA;
+        }
+    }
     for (int i = 0; i < VAPR_NUM_SLOTS; ++i) {
         c->fmts[i] = vapr_format{8, 23};
         c->dfmt[i] = make_fmt(c->fmts[i]);
@@ -160,6 +177,10 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     DeviceGuard g(c->device);
     if (c->d_cub) cudaFree(c->d_cub);
     if (c->d_off) cudaFree(c->d_off);
+    if (c->d_sched) cudaFree(c->d_sched);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     delete c;
     return VAPR_OK;
 }
@@ -510,7 +531,7 @@ static vapr_status collision_common(vapr_ctx* c, const uint32_t* os, const int32
     a.ov = ov;
     const Fmt& fcp = c->dfmt[swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT];
     cudaError_t e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], fcp,
-                                     c->dfmt[VAPR_OUT_VEC], a, s);
+                                     c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cost, B, H, cost_traj, s);
     return cuda_status(e);
 }
@@ -606,6 +627,66 @@ vapr_status vapr_cost_grad_workspace_layout(const vapr_ctx* c, int32_t B, int32_
     return VAPR_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The vapr_cost_grad launch sequence for trajectories [b0, b0 + nb) of a
+// batch of B (all device pointers are the whole-batch buffers; rows are
+// contiguous per pose, so a trajectory range is a contiguous row range of
+// every tensor).
+cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx, int b0,
+                              int nb, int B, int H, const vapr_cost_params* p, void* workspace,
+                              const size_t* off, float* cpose, float* cost_traj, float* grad_q,
+                              cudaStream_t s) {
+    (void)B;
+    char* ws = static_cast<char*>(workspace);
+    const int cps = p->swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
+    const long long p0 = (long long)b0 * H, P = (long long)nb * H;
+    const int cols = c->robot.cols;
+    auto rows_of = [&](int slot) {
+        return reinterpret_cast<uint32_t*>(ws + off[slot]) + p0 * row_words_of(c->dfmt[slot], cols);
+    };
+    uint32_t* os = rows_of(VAPR_OUT_SPHERES);
+    uint32_t* cp = rows_of(cps);
+    uint32_t* ov = rows_of(VAPR_OUT_VEC);
+    uint32_t* gos = rows_of(VAPR_GRAD_OUT_SPHERES);
+    const float* qc = q + p0 * kJoints;
+    cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], qc, P, os, s);
+    if (e == cudaSuccess) {
+        CollisionArgs a{};
+        a.os = os;
+        a.world_idx = world_idx + b0;
+        a.B = nb;
+        a.H = H;
+        a.do_world = 1;
+        a.do_self = 1;
+        a.swept = p->swept ? 1 : 0;
+        a.sweep_steps = p->sweep_steps;
+        a.eta_w = p->eta_world;
+        a.w_w = p->w_world;
+        a.eta_s = p->eta_self;
+        a.w_s = p->w_self;
+        a.cull = c->cull;
+        a.cost = cpose + p0;
+        a.cp = cp;
+        a.ov = ov;
+        e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
+                             c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
+    }
+    if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose + p0, nb, H, cost_traj + b0, s);
+    if (e == cudaSuccess)
+        e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
+                             cols, cp, ov, P, gos, s);
+    if (e == cudaSuccess)
+        e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s);
+    return e;
+}
+
+}  // namespace
+
+extern "C" {
+
 vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx, int32_t B,
                            int32_t H, const vapr_cost_params* p, void* workspace,
                            size_t workspace_bytes, float* cost_pose, float* cost_traj,
@@ -628,42 +709,81 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
     CHECK(workspace_bytes >= total, VAPR_ERR_INVALID_ARG);
     DeviceGuard g(c->device);
     CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
-    char* ws = static_cast<char*>(workspace);
-    const int cps = p->swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
-    uint32_t* os = reinterpret_cast<uint32_t*>(ws + off[VAPR_OUT_SPHERES]);
-    uint32_t* cp = reinterpret_cast<uint32_t*>(ws + off[cps]);
-    uint32_t* ov = reinterpret_cast<uint32_t*>(ws + off[VAPR_OUT_VEC]);
-    uint32_t* gos = reinterpret_cast<uint32_t*>(ws + off[VAPR_GRAD_OUT_SPHERES]);
-    float* cpose = cost_pose ? cost_pose : reinterpret_cast<float*>(ws + co);
-    cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], q, P, os, s);
-    if (e == cudaSuccess) {
-        CollisionArgs a{};
-        a.os = os;
-        a.world_idx = world_idx;
-        a.B = B;
-        a.H = H;
-        a.do_world = 1;
-        a.do_self = 1;
-        a.swept = p->swept ? 1 : 0;
-        a.sweep_steps = p->sweep_steps;
-        a.eta_w = p->eta_world;
-        a.w_w = p->w_world;
-        a.eta_s = p->eta_self;
-        a.w_s = p->w_self;
-        a.cull = c->cull;
-        a.cost = cpose;
-        a.cp = cp;
-        a.ov = ov;
-        e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
-                             c->dfmt[VAPR_OUT_VEC], a, s);
+    float* cpose = cost_pose ? cost_pose
+                             : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
+    return cuda_status(enqueue_cost_grad(c, q, world_idx, 0, B, B, H, p, workspace, off, cpose,
+                                         cost_traj, grad_q, (cudaStream_t)stream));
+}
+
+vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t* world_idx,
+                                int32_t B, int32_t H, const vapr_cost_params* p, void* workspace,
+                                size_t workspace_bytes, float* q_dev, float* cost_pose_dev,
+                                float* cost_traj_dev, float* grad_q_dev, float* cost_traj_host,
+                                float* grad_q_host, int32_t n_chunks, void* stream) {
+    CHECK(c != nullptr && p != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(c->robot_set && c->worlds_set && c->formats_set, VAPR_ERR_NOT_INITIALIZED);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(!p->swept || H >= 2, VAPR_ERR_SHAPE);
+    CHECK(q_host && grad_q_host && world_idx && workspace && q_dev && cost_traj_dev && grad_q_dev,
+          VAPR_ERR_INVALID_ARG);
+    CHECK(aligned16(q_dev) && aligned16(world_idx) && aligned16(grad_q_dev) &&
+              aligned16(workspace) && aligned16(cost_traj_dev),
+          VAPR_ERR_INVALID_ARG);
+    CHECK(cost_pose_dev == nullptr || aligned16(cost_pose_dev), VAPR_ERR_INVALID_ARG);
+    CHECK(n_chunks >= 0, VAPR_ERR_INVALID_ARG);
+    CHECK(p->eta_world > 0.f && p->eta_self > 0.f && std::isfinite(p->w_world) &&
+              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64,
+          VAPR_ERR_INVALID_ARG);
+    const long long P = (long long)B * H;
+    size_t off[VAPR_NUM_SLOTS], co, total;
+    ws_layout(c, P, p->swept, off, &co, &total);
+    CHECK(workspace_bytes >= total, VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    float* cpose = cost_pose_dev ? cost_pose_dev
+                                 : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
+    // chunking: whole trajectories, about 320k poses per chunk by default
+    int nc = n_chunks;
+    if (nc == 0) nc = (int)std::max(1LL, std::min<long long>(16, (P + 327679) / 327680));
+    nc = std::min(nc, B);
+    const int Bc = (B + nc - 1) / nc;
+    nc = (B + Bc - 1) / Bc;
+    cudaError_t e = cudaSuccess;
+    if (!c->s_in) e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess && !c->s_out) e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking);
+    while (e == cudaSuccess && c->events.size() < (size_t)(2 * nc + 2)) {
+        cudaEvent_t ev;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) c->events.push_back(ev);
     }
-    if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose, B, H, cost_traj, s);
-    if (e == cudaSuccess)
-        e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
-                             c->robot.cols, cp, ov, P, gos, s);
-    if (e == cudaSuccess)
-        e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], q, P, gos, grad_q, s);
+    if (e != cudaSuccess) return cuda_status(e);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t* ev = c->events.data();
+    // the copy streams start after the work already enqueued on `stream`
+    e = cudaEventRecord(ev[0], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_in, ev[0], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_out, ev[0], 0);
+    for (int i = 0; i < nc && e == cudaSuccess; ++i) {
+        const int b0 = i * Bc, nb = std::min(Bc, B - b0);
+        const size_t qo = (size_t)b0 * H * kJoints, qn = (size_t)nb * H * kJoints * sizeof(float);
+        e = cudaMemcpyAsync(q_dev + qo, q_host + qo, qn, cudaMemcpyHostToDevice, c->s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2 + 2 * i], c->s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 + 2 * i], 0);
+        if (e == cudaSuccess)
+            e = enqueue_cost_grad(c, q_dev, world_idx, b0, nb, B, H, p, workspace, off, cpose,
+                                  cost_traj_dev, grad_q_dev, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[3 + 2 * i], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_out, ev[3 + 2 * i], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(grad_q_host + qo, grad_q_dev + qo, qn, cudaMemcpyDeviceToHost,
+                                c->s_out);
+        if (e == cudaSuccess && cost_traj_host)
+            e = cudaMemcpyAsync(cost_traj_host + b0, cost_traj_dev + b0, sizeof(float) * nb,
+                                cudaMemcpyDeviceToHost, c->s_out);
+    }
+    // `stream` completes only after the last D2H copy
+    if (e == cudaSuccess) e = cudaEventRecord(ev[1], c->s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[1], 0);
     return cuda_status(e);
 }
 

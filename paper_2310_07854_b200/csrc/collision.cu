@@ -175,10 +175,11 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_FUSED_SPLIT         // 1: world and self as two passes
 #define VAPR_FUSED_SPLIT 1
 #endif
-#ifndef VAPR_PHASE_SYNC          // 1: CTA barriers between the phases of a tile
-#define VAPR_PHASE_SYNC 0
+#ifndef VAPR_GRAB                // consecutive tiles a warp takes per scheduler grab
+#define VAPR_GRAB 1
 #endif
 constexpr int kDecLoads = VAPR_DEC_LOADS;
+constexpr int kGrab = VAPR_GRAB;
 #ifdef VAPR_STATS
 // work counters of the variant build -DVAPR_STATS (scripts/collision_stats.py)
 __device__ unsigned long long g_stats[8];
@@ -352,7 +353,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint8_t* slink = reinterpret_cast<uint8_t*>(base + G.slink);
     uint32_t* spm = reinterpret_cast<uint32_t*>(base + G.spm);     // pair-id mask of each sphere
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
     const int PMW = G.pmw;
 
@@ -414,12 +415,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
     const long long n_tiles = (P + kTP - 1) / kTP;
-    // a contiguous chunk of tiles per warp: consecutive tiles share the
-    // problem, so its cuboids stay in L1
-    const long long NW = (long long)gridDim.x * nwarps;
-    const long long per = (n_tiles + NW - 1) / NW;
-    const long long t_begin = ((long long)blockIdx.x * nwarps + warp) * per;
-    const long long t_end = min(n_tiles, t_begin + per);
+    // dynamic scheduling: a warp takes kGrab consecutive tiles at a time
+    // from a global counter (collision-dense tiles cost several times the
+    // average, so static ranges leave a long tail; consecutive tiles share
+    // the problem and its cuboids)
+    unsigned int* sched = a.sched;              // [0] next grab, [1] finished CTAs
+    const long long n_grabs = (n_tiles + kGrab - 1) / kGrab;
+    long long grab = -1, tile = 0, t_end = 0;
 
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
@@ -429,12 +431,17 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
     const float fmax_os = decode(fos.maxcode, fos);
 
-    for (long long it_ = 0; it_ < per; ++it_) {
-        const long long tile = t_begin + it_;
-        if (!VAPR_PHASE_SYNC && tile >= t_end) break;
+    for (;;) {
+        if (tile >= t_end) {
+            unsigned int gi = 0;
+            if (lane == 0) gi = atomicAdd(sched, 1u);
+            grab = __shfl_sync(0xffffffffu, gi, 0);
+            if (grab >= n_grabs) break;
+            tile = grab * kGrab;
+            t_end = min(n_tiles, tile + kGrab);
+        }
         const long long p0 = tile * kTP;
-        // np = 0: a warp past its last tile keeps hitting the phase barriers
-        const int np = (tile < t_end) ? (int)min((long long)kTP, P - p0) : 0;
+        const int np = (int)min((long long)kTP, P - p0);
         const long long r_lo = max(p0 - 1, 0LL);
         const long long r_hi = min(p0 + kTP + 1, P);      // exclusive
         const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
@@ -457,7 +464,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
         float amax = 0.f;
         {
-            const int nq = (np > 0) ? int(r_hi - r_lo) * G.Qos : 0;
+            const int nq = int(r_hi - r_lo) * G.Qos;
             const uint4* src = os4 + r_lo * G.Qos;
             float* dst0 = rows + row_off * cs;
             with_pf(fos.pf, [&](auto Pc) {
@@ -509,7 +516,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         }
         if (a.do_world && half == 0 && pl < kTP) pk0[pl] = k0;
         __syncwarp();
-        if (VAPR_PHASE_SYNC) __syncthreads();
 
         // Quantisation margin: a decoded coordinate y of an FK value x
         // satisfies |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) unless the code
@@ -667,7 +673,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             });
         }
 
-        if (VAPR_PHASE_SYNC) __syncthreads();
         // ---- 3. self
         float scost = 0.f;
         if (a.do_self) {
@@ -835,7 +840,18 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         }
         __syncwarp();
 
+        ++tile;
     }  // tile loop
+    // the last CTA to finish resets the scheduler slot for its next use
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+            sched[0] = 0u;
+            sched[1] = 0u;
+            __threadfence();
+        }
+    }
 }
 
 __global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
@@ -900,7 +916,7 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, collision_kernel, 32 * nw, smem);
     const long long tiles = (P + kTP - 1) / kTP;
-    const long long grid = std::min<long long>((tiles + nw - 1) / nw,
+    const long long grid = std::min<long long>((tiles + kGrab * nw - 1) / (kGrab * nw),
                                                (long long)sms * std::max(per_sm, 1));
     collision_kernel<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
     return cudaGetLastError();
@@ -910,13 +926,24 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
 // cost to the first's, i.e. the same wcost + scost): each pass keeps a
 // smaller instruction working set, which beats re-reading out_spheres.
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
-                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
-                             cudaStream_t s) {
-    const long long P = (long long)a.B * a.H;
+                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a0,
+                             unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s) {
+    const long long P = (long long)a0.B * a0.H;
     if (P <= 0) return cudaSuccess;
-    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self))
+    // each pass takes the next scheduler slot of the context's ring (the
+    // kernel's last CTA leaves it zeroed); kSchedSlots passes may be in flight
+    auto slot = [&]() {
+        const unsigned k = __atomic_fetch_add(sched_next, 1u, __ATOMIC_RELAXED) % kSchedSlots;
+        return sched_ring + 2 * k;
+    };
+    CollisionArgs a = a0;
+    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self)) {
+        a.sched = slot();
         return launch_collision_pass(R, W, fos, fcp, fov, a, s);
+    }
     CollisionArgs aw = a, as = a;
+    aw.sched = slot();
+    as.sched = slot();
     aw.do_self = 0;
     as.do_world = 0;
     as.cost_accumulate = 1;

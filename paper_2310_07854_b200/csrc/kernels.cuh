@@ -28,6 +28,7 @@ struct CollisionArgs {
     uint32_t* cp;             // packed world gradient (nullable iff !do_world)
     uint32_t* ov;             // packed self gradient (nullable iff !do_self)
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
+    unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero
 };
 
 cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t cols,
@@ -38,7 +39,8 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
                       uint32_t* os, cudaStream_t s);
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
-                             cudaStream_t s);
+                             unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);
+constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight collision passes)
 cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
                                cudaStream_t s);
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,

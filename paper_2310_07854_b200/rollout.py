@@ -79,6 +79,16 @@ class Rollout:
                           self.workspace, self.cost_pose, self.cost_traj, self.grad_q,
                           stream=stream, _p=self._p)
 
+    def run_host(self, q_host, grad_q_host, cost_traj_host=None, n_chunks=0, stream=None):
+        """End to end from host buffers: q_host [B, H, 7] float32 in, grad_q_host
+        [B, H, 7] (and cost_traj_host [B]) out, copies pipelined against the
+        compute inside vapr_cost_grad_host; stream-ordered (synchronise the
+        stream before reading the host outputs).  Pinned host tensors overlap."""
+        vb.vapr_cost_grad_host(self.ctx.h, q_host, self.world_idx, self.B, self.H, self.params,
+                               self.workspace, self.q, self.cost_pose, self.cost_traj,
+                               self.grad_q, cost_traj_host, grad_q_host, n_chunks,
+                               stream=stream, _p=self._p)
+
     def packed(self, slot):
         """The packed tensor of `slot` inside the workspace, as uint32 [P, W]."""
         lay = vb.vapr_cost_grad_workspace_layout(self.ctx.h, self.B, self.H, self.params["swept"])

@@ -302,6 +302,48 @@ def test_cost_grad_fp32_end_to_end(vb):
     check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), gscale, "grad_q", tol=1e-4)
 
 
+@pytest.mark.parametrize("n_chunks,pinned", [(1, True), (5, True), (0, True), (7, False)])
+def test_cost_grad_host_matches_device_path(vb, n_chunks, pinned):
+    """vapr_cost_grad_host (pipelined host copies, trajectory chunks) gives
+    bit-identical grad_q / cost_traj / cost_pose to vapr_cost_grad, for
+    ragged chunkings and pageable host memory; the workspace tensors too."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config4(problems_per_env=1, seeds=3, H=32)          # B = 24: ragged chunks
+    r = Rollout(wl)
+    r.run()
+    ref = r.results()
+    ref_ws = r.workspace.clone()
+    r.grad_q.zero_()
+    r.cost_traj.zero_()
+    r.cost_pose.zero_()
+    r.q.zero_()                                  # the host path must upload q itself
+    q_host = torch.from_numpy(np.ascontiguousarray(wl.q, np.float32))
+    gq_host = torch.full((wl.B * wl.H * 7,), float("nan"), dtype=torch.float32)
+    ct_host = torch.full((wl.B,), float("nan"), dtype=torch.float32)
+    if pinned:
+        q_host, gq_host, ct_host = q_host.pin_memory(), gq_host.pin_memory(), ct_host.pin_memory()
+    r.run_host(q_host, gq_host, ct_host, n_chunks=n_chunks)
+    torch.cuda.current_stream().synchronize()
+    assert np.array_equal(gq_host.numpy().view(np.uint32),
+                          ref["grad_q"].reshape(-1).view(np.uint32))
+    assert np.array_equal(ct_host.numpy().view(np.uint32), ref["cost_traj"].view(np.uint32))
+    assert np.array_equal(r.cost_pose.cpu().numpy().view(np.uint32),
+                          ref["cost_pose"].reshape(-1).view(np.uint32))
+    assert torch.equal(r.workspace, ref_ws)
+
+
+def test_cost_grad_host_errors(vb):
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config2()
+    r = Rollout(wl)
+    q_host = torch.from_numpy(np.ascontiguousarray(wl.q, np.float32))
+    gq = torch.zeros(wl.B * wl.H * 7)
+    with pytest.raises(vb.VaprError):          # negative chunk count
+        r.run_host(q_host, gq, None, n_chunks=-1)
+    with pytest.raises(ValueError):            # device tensor where a host buffer is expected
+        r.run_host(r.q, gq, None)
+
+
 def test_cost_grad_errors(vb):
     from paper_2310_07854_b200.rollout import Rollout
     wl = config2()
