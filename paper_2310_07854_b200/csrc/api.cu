@@ -742,9 +742,11 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
     float* cpose = cost_pose_dev ? cost_pose_dev
                                  : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
-    // chunking: whole trajectories, about 320k poses per chunk by default
+    // chunking: whole trajectories, about 640k poses per chunk by default
+    // (measured on the bench workload: fewer chunks overlap less, more pay
+    // the per-launch fixed costs)
     int nc = n_chunks;
-    if (nc == 0) nc = (int)std::max(1LL, std::min<long long>(16, (P + 327679) / 327680));
+    if (nc == 0) nc = (int)std::max(1LL, std::min<long long>(16, (P + 655359) / 655360));
     nc = std::min(nc, B);
     const int Bc = (B + nc - 1) / nc;
     nc = (B + Bc - 1) / Bc;
