@@ -165,12 +165,6 @@ __device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) 
     uint32_t amax = 0;
 #pragma unroll
     for (int j = 0; j < PF; ++j) amax = max(amax, __float_as_uint(x[j]) & 0x7fffffffu);
-    if (amax == 0u) {               // all +-0: only the signs can be set
-        uint32_t w = 0;
-#pragma unroll
-        for (int j = 0; j < PF; ++j) w |= ((__float_as_uint(x[j]) >> (32 - f.t)) & f.signbit) << (j * f.t);
-        return w;
-    }
 #ifdef VAPR_NO_HW_ENCODE
     if (false) {
 #else
@@ -202,6 +196,13 @@ __device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) 
                        ((p1 >> 8) << 18) | ((p2 & 0x3fu) << 24);
             }
         }
+    }
+    // generic path (the hardware conversions above already map +-0 exactly)
+    if (amax == 0u) {               // all +-0: only the signs can be set
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < PF; ++j) w |= ((__float_as_uint(x[j]) >> (32 - f.t)) & f.signbit) << (j * f.t);
+        return w;
     }
     uint32_t w = 0;
 #pragma unroll
