@@ -774,8 +774,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                     const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
                                     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                                     const float Rs = __uint_as_float(rec.y);
-                                    // same exact early-out as self_pair: d2 >= fl(Rs^2) => phi <= 0
-                                    if (k >= k1c || d2 >= Rs * Rs || Rs - sqrtf(d2) <= 0.f) continue;
+                                    // d2 >= fl(Rs^2) => phi <= 0 (self_pair's exact early-out);
+                                    // the rare d2 within an ulp of Rs^2 is settled by self_pair
+                                    // in the gather (an inactive marked pair contributes nothing)
+                                    if (k >= k1c || d2 >= Rs * Rs) continue;
                                     const int pid = rec.x >> 16;
                                     atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
                                     wmk |= 1u << (pid >> 5);
