@@ -384,9 +384,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
         for (int i = tid; i < G.ngp; i += blockDim.x) {
             sgpab[i] = (uint16_t)(R.gp_a[i] | (R.gp_b[i] << 8));
-            // 3 ref_a | 3 ref_b << 8, and the static part of the cull distance
+            // byte offsets 12 ref_a | 12 ref_b << 16 in a row, and the static
+            // part of the cull distance
             const int ga = R.gp_a[i], gb = R.gp_b[i];
-            sgrec[i] = make_uint2((uint32_t)(3 * R.grp_ref[ga]) | ((uint32_t)(3 * R.grp_ref[gb]) << 8),
+            sgrec[i] = make_uint2((uint32_t)(12 * R.grp_ref[ga]) | ((uint32_t)(12 * R.grp_ref[gb]) << 16),
                                   __float_as_uint(R.grp_rl[ga] + R.grp_rl[gb] + a.eta_s + kSlack));
         }
         for (int i = tid; i <= R.n_link_pairs; i += blockDim.x) slpgp[i] = R.lp_gp_off[i];
@@ -682,18 +683,24 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             uint32_t a0 = 0u, a1 = 0u;
             if (pl < np) {
                 const float m2 = 2.f * margin;
-#pragma unroll 2
-                for (int it = 0; kLPP * it + half < G.ngp; ++it) {
+                const char* rb = reinterpret_cast<const char*>(myrow);
+                auto test = [&](int it) -> uint32_t {
                     const uint2 r = sgrec[kLPP * it + half];
-                    const float* ca = myrow + (r.x & 0xffu);
-                    const float* cb = myrow + ((r.x >> 8) & 0xffu);
+                    const float* ca = reinterpret_cast<const float*>(rb + (r.x & 0xffffu));
+                    const float* cb = reinterpret_cast<const float*>(rb + (r.x >> 16));
                     const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
                     const float lim = __uint_as_float(r.y) + m2;
-                    const uint32_t live =
-                        (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) ? 1u : 0u;
-                    if (it < 32) a0 |= live << it;
-                    else a1 |= live << (it - 32);
-                }
+                    return (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) ? 1u : 0u;
+                };
+                // funnel-shift accumulators: after n tests bit j sits at 32 - n + j
+                const int n_it = (G.ngp - half + kLPP - 1) / kLPP;
+                const int n0 = min(n_it, 32), n1 = n_it - n0;
+#pragma unroll 2
+                for (int it = 0; it < n0; ++it) a0 = __funnelshift_r(a0, test(it), 1);
+#pragma unroll 2
+                for (int it = 32; it < n_it; ++it) a1 = __funnelshift_r(a1, test(it), 1);
+                a0 = (n0 > 0) ? (a0 >> (32 - n0)) : 0u;
+                a1 = (n1 > 0) ? (a1 >> (32 - n1)) : 0u;
             }
             // interleave the two halves' bits into the group-pair mask
             static_assert(kLPP == 2, "the interleave below assumes two lanes per pose");
