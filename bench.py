@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--chunks", type=int, default=0,
                     help="e2e: trajectory chunks of the pipelined host call (0 = automatic)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the end-to-end leg (profiling runs: keeps the launch list to the device step)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-sample-poses", type=int, default=20480)
     return ap.parse_args()
@@ -307,9 +309,13 @@ def main():
         vb.vapr_best_per_problem(r.cost_traj, n_prob, args.seeds, best_c, best_s)
         gather_best(best_c, best_s, world)
 
-    e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
-    h2d = q_host.numel() * 4
-    d2h = gq_host.numel() * 4 + ct_host.numel() * 4
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
+        e2e = {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT, "chunks": args.chunks,
+               "h2d_bytes_per_step": q_host.numel() * 4,
+               "d2h_bytes_per_step": gq_host.numel() * 4 + ct_host.numel() * 4,
+               "ms_per_step": e2e_ms}
 
     # ---- FP32 comparison (the >= 2x target of BASELINE.json) on the same batch
     fp32 = None
@@ -339,9 +345,7 @@ def main():
             "hbm_frac_step": a_min * P / (ms * 1e-3) / 1e9 / hbm,
             "bytes_per_pose_alg": a_min,
             "roofline": roofline,
-            "e2e": {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT, "chunks": args.chunks,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms},
+            "e2e": e2e,
             "fp32": fp32,
             "cpu_baseline": cpu,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,

@@ -20,14 +20,19 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"reg
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Line No"'))
-rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
-h = rows[0]
+rows = list(csv.reader(io.StringIO("\n".join(lines))))
+h = rows[start]
 iw = h.index("Warp Stall Sampling (All Samples)")
 ii = h.index("Instructions Executed")
 acc = {n: [0, 0] for n, _, _ in ranges}
 acc["other"] = [0, 0]
 tw = ti = 0
-for r in rows[1:]:
+MAIN = os.environ.get("NCU_MAIN_FILE", "collision.cu")
+cur = ""
+for r in rows:
+    if r and r[0] in ("File Name", "File Path"):
+        cur = r[1]
+        continue
     if len(r) <= ii or not r[0].isdigit():
         continue
     try:
@@ -36,6 +41,11 @@ for r in rows[1:]:
         continue
     ln = int(r[0])
     tw += w; ti += n
+    if not cur.endswith(MAIN):
+        key = "file:" + os.path.basename(cur)
+        acc.setdefault(key, [0, 0])
+        acc[key][0] += w; acc[key][1] += n
+        continue
     for name, lo, hi in ranges:
         if lo <= ln <= hi:
             acc[name][0] += w; acc[name][1] += n
