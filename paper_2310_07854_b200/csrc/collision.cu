@@ -175,6 +175,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_FUSED_SPLIT         // 1: world and self as two passes
 #define VAPR_FUSED_SPLIT 1
 #endif
+#ifndef VAPR_MAX_WARPS          // cap on warps per (persistent, one per SM) CTA
+#define VAPR_MAX_WARPS 16
+#endif
 #ifndef VAPR_GRAB                // consecutive tiles a warp takes per scheduler grab
 #define VAPR_GRAB 1
 #endif
@@ -334,7 +337,7 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
 // spheres, live group pairs, touched spheres) goes through warp work queues
 // so that every lane has an item.  Warps are independent: no CTA barrier in
 // the tile loop.
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
@@ -916,7 +919,7 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // as many warps per CTA as shared memory holds (the tables are staged
     // once per CTA), at most 8; one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
-    nw = std::min(nw, 16);
+    nw = std::min(nw, VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
     cudaError_t e = cudaFuncSetAttribute(collision_kernel,
