@@ -32,9 +32,14 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
     float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
     uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
+    float* sg = reinterpret_cast<float*>(sw + kTile * WS);            // [kTile * 7] grad_q
+    __shared__ unsigned long long s_mask[kTile];
+    __shared__ int s_act[kTile];
+    __shared__ int s_nact;
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
+    if (tid == 0) s_nact = 0;
 
     // sphere offsets are indexed per lane (by each pose's non-zero spheres):
     // stage them in shared memory instead of the serialising constant bank
@@ -80,19 +85,30 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
         }
     }
 
-    float gq[kJoints];
-#pragma unroll
-    for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
-
+    // compact the poses with a non-zero gradient so the chains below run in
+    // full warps (each pose's result is independent of the order)
     if (mask) {
-        const uint32_t* row = sw + tid * WS;
+        const int k = atomicAdd(&s_nact, 1);
+        s_act[k] = tid;
+        s_mask[k] = mask;
+    }
+    for (int i = tid; i < np * kJoints; i += kTile) sg[i] = 0.f;
+    __syncthreads();
+    const int nact = s_nact;
+    for (int k = tid; k < nact; k += kTile) {
+        const int pp = s_act[k];
+        const unsigned long long pmask = s_mask[k];
+        float gq[kJoints];
+#pragma unroll
+        for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
+        const uint32_t* row = sw + pp * WS;
         float zx[kJoints], zy[kJoints], zz[kJoints], ox[kJoints], oy[kJoints], oz[kJoints];
         Xf X;
         xf_identity(X);
 #pragma unroll
         for (int l = 1; l < kLinks; ++l) {
             if (l <= kJoints) {
-                fk_step(X, R, l - 1, sq[tid * kJoints + l - 1]);
+                fk_step(X, R, l - 1, sq[pp * kJoints + l - 1]);
                 zx[l - 1] = X.r[2];
                 zy[l - 1] = X.r[5];
                 zz[l - 1] = X.r[8];
@@ -103,7 +119,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 fk_hand(X, R);
             }
             const int s0 = R.link_start[l], s1 = R.link_start[l + 1];
-            unsigned long long lm = (mask >> s0) & ((s1 - s0 >= 64) ? ~0ull : ((1ull << (s1 - s0)) - 1ull));
+            unsigned long long lm = (pmask >> s0) & ((s1 - s0 >= 64) ? ~0ull : ((1ull << (s1 - s0)) - 1ull));
             if (!lm) continue;
             float Fx = 0.f, Fy = 0.f, Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f;
             while (lm) {
@@ -111,10 +127,10 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 lm &= lm - 1;
                 float g[3];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const int e = 3 * s + k;
+                for (int c = 0; c < 3; ++c) {
+                    const int e = 3 * s + c;
                     const int wi = int((e * rc) >> 16);
-                    g[k] = decode(code_at(row[wi], e - wi * f.pf, f), f);
+                    g[c] = decode(code_at(row[wi], e - wi * f.pf, f), f);
                 }
                 float cx, cy, cz;
                 const float4 o4 = so[s];
@@ -137,15 +153,12 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 }
             }
         }
-    }
-    __syncthreads();
-    // stage grad_q through smem (reuse sq) for a coalesced store
-    if (tid < np) {
 #pragma unroll
-        for (int j = 0; j < kJoints; ++j) sq[tid * kJoints + j] = gq[j];
+        for (int j = 0; j < kJoints; ++j) sg[pp * kJoints + j] = gq[j];
     }
     __syncthreads();
-    for (int i = tid; i < np * kJoints; i += kTile) __stcs(grad_q + p0 * kJoints + i, sq[i]);
+    // coalesced grad_q store (zero for poses without a gradient)
+    for (int i = tid; i < np * kJoints; i += kTile) __stcs(grad_q + p0 * kJoints + i, sg[i]);
 }
 
 }  // namespace
@@ -156,7 +169,7 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     const int W = row_words_of(fgos, R.cols);
     const size_t smem = sizeof(float4) * kMaxSpheres +
                         sizeof(float) * kTile * kJoints +
-                        sizeof(uint32_t) * kTile * (W + 4);
+                        sizeof(uint32_t) * kTile * (W + 4) + sizeof(float) * kTile * kJoints;
     cudaError_t e = cudaFuncSetAttribute(bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
