@@ -78,9 +78,18 @@ __device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, flo
         else glz = (pz >= 0.f) ? 1.f : -1.f;
     } else {
         const float ox = fmaxf(ux, 0.f), oy = fmaxf(uy, 0.f), oz = fmaxf(uz, 0.f);
-        const float on = sqrtf(fmaf(ox, ox, fmaf(oy, oy, oz * oz)));
+        // |o| and 1/|o| from one MUFU rsqrt (~2 ulp; parity tolerance 1e-5),
+        // the IEEE path for arguments near the FP32 underflow
+        const float o2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
+        float on, inv;
+        if (o2 >= 1e-30f) {
+            inv = rsqrtf(o2);
+            on = o2 * inv;
+        } else {
+            on = sqrtf(o2);
+            inv = 1.f / on;
+        }
         sdf = on;
-        const float inv = 1.f / on;
         glx = (px >= 0.f) ? ox * inv : -(ox * inv);
         gly = (py >= 0.f) ? oy * inv : -(oy * inv);
         glz = (pz >= 0.f) ? oz * inv : -(oz * inv);
@@ -140,7 +149,15 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
     // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so d2 >= fl(Rs^2)
     // implies fl(sqrt(d2)) >= Rs, i.e. phi <= 0: exact early out.
     if (d2 >= Rs * Rs) return false;
-    const float d = sqrtf(d2);
+    // d and 1/d from one MUFU rsqrt (~2 ulp), IEEE near underflow
+    float d, dinv;
+    if (d2 >= 1e-30f) {
+        dinv = rsqrtf(d2);
+        d = d2 * dinv;
+    } else {
+        d = sqrtf(d2);
+        dinv = (d > 0.f) ? 1.f / d : 0.f;
+    }
     const float phi = Rs - d;
     if (phi <= 0.f) return false;
     float hh, dh;
@@ -153,10 +170,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
     }
     const float k = w * dh;
     if (d > 0.f) {
-        const float inv = 1.f / d;
-        vx = k * (dx * inv);
-        vy = k * (dy * inv);
-        vz = k * (dz * inv);
+        vx = k * (dx * dinv);
+        vy = k * (dy * dinv);
+        vz = k * (dz * dinv);
     } else {                                       // coincident centres: direction (1, 0, 0)
         vx = k;
         vy = vz = 0.f;
