@@ -210,8 +210,53 @@ __device__ __forceinline__ uint32_t encode_word_t(const float* x, const Fmt& f) 
     return w;
 }
 
+// two 8-bit codes (low 16 bits of w) -> two FP32 values via f16x2
+__device__ __forceinline__ void cvt2_f8(uint32_t w, float* out, bool e5m2) {
+    uint32_t h;
+    const uint16_t c = (uint16_t)(w & 0xffffu);
+    if (e5m2) asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h) : "h"(c));
+    else asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(c));
+    asm("{ .reg .f16 a, b;\n mov.b32 {a, b}, %2;\n cvt.f32.f16 %0, a;\n cvt.f32.f16 %1, b;}"
+        : "=f"(out[0]), "=f"(out[1]) : "r"(h));
+}
+
 template <int PF>
 __device__ __forceinline__ void decode_word_t(uint32_t w, float* out, const Fmt& f) {
+    if constexpr (PF == 4) {
+        // E4M3 / E5M2 through the hardware f8 -> f16 conversion (exact: every
+        // value of both formats is an f16 value), except the codes that are
+        // finite in this reading but NaN / inf in the hardware encodings:
+        // E4M3 S.1111.111 (480), E5M2 exponent field 31
+        if (f.kind == KIND_E4M3) {
+            if ((((w & 0x7f7f7f7fu) + 0x01010101u) & 0x80808080u) == 0u) {
+                cvt2_f8(w, out, false);
+                cvt2_f8(w >> 16, out + 2, false);
+                return;
+            }
+        } else if (f.kind == KIND_E5M2) {
+            const uint32_t e = w & 0x7c7c7c7cu;
+            // a byte's exponent field is 31 iff (e_byte + 0x04) carries into bit 7
+            if ((((e + 0x04040404u) & 0x80808080u)) == 0u) {
+                cvt2_f8(w, out, true);
+                cvt2_f8(w >> 16, out + 2, true);
+                return;
+            }
+        }
+    }
+    if constexpr (PF == 8) {
+        // E2M1 (no special codes) through cvt.rn.f16x2.e2m1x2, one byte = two codes
+        if (f.kind == KIND_E2M1) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                uint32_t h;
+                const uint16_t c = (uint16_t)((w >> (8 * b)) & 0xffu);
+                asm("{ .reg .b8 t;\n cvt.u8.u16 t, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;}" : "=r"(h) : "h"(c));
+                asm("{ .reg .f16 a, b;\n mov.b32 {a, b}, %2;\n cvt.f32.f16 %0, a;\n cvt.f32.f16 %1, b;}"
+                    : "=f"(out[2 * b]), "=f"(out[2 * b + 1]) : "r"(h));
+            }
+            return;
+        }
+    }
     if constexpr (PF == 2) {
         // E5M10: the hardware f16 -> f32 conversion is exact except for the
         // exponent-31 codes, which are finite in this reading (c3)

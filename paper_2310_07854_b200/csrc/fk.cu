@@ -49,7 +49,7 @@ struct Emitter {
 
 __global__ void __launch_bounds__(kTile)
 fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
-          long long P, int W, uint32_t* __restrict__ os) {
+          long long P, int W, uint32_t* __restrict__ os, uint32_t rq) {
     extern __shared__ uint32_t smem[];
     const int WS = W + 1;
     float* sq = reinterpret_cast<float*>(smem);    // [kTile * 7]
@@ -84,19 +84,14 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     }
     __syncthreads();
 
-    // coalesced tile store: consecutive threads write consecutive words
-    const int nw = np * W;
-    const int dr = kTile / W, dw = kTile % W;
-    int r = tid / W, w = tid - (tid / W) * W;
-    uint32_t* dst = os + p0 * W;
-    for (int i = tid; i < nw; i += kTile) {
-        __stcs(dst + i, sw[r * WS + w]);
-        r += dr;
-        w += dw;
-        if (w >= W) {
-            w -= W;
-            ++r;
-        }
+    // coalesced 16-byte tile store (rows are 16-byte multiples): four
+    // conflict-free scalar shared reads per uint4
+    const int Q = W / 4, nq = np * Q;
+    uint4* dst = reinterpret_cast<uint4*>(os + p0 * W);
+    for (int i = tid; i < nq; i += kTile) {
+        const int r = int((uint32_t(i) * rq) >> 20), g = i - r * Q;
+        const uint32_t* src = sw + r * WS + 4 * g;
+        __stcs(dst + i, make_uint4(src[0], src[1], src[2], src[3]));
     }
 }
 
@@ -111,7 +106,8 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
                                          (int)smem);
     if (e != cudaSuccess) return e;
     const long long grid = (P + kTile - 1) / kTile;
-    fk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os);
+    const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
+    fk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq);
     return cudaGetLastError();
 }
 

@@ -139,6 +139,42 @@ def ragged_workload(B=3, H=5, formats="43bit", salt=9):
     return make_workload("ragged", envs, list(range(B)), 1, H, FORMAT_SETS[formats], salt=salt)
 
 
+def _rot(rng):
+    """Uniform random rotation (row-major 3x3) from a unit quaternion."""
+    w, x, y, z = rng.normal(size=4) / 1.0
+    n = np.sqrt(w * w + x * x + y * y + z * z)
+    w, x, y, z = w / n, x / n, y / n, z / n
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                     [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                     [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+
+def edge_worlds_workload(formats="43bit", H=16, seeds=4):
+    """Edge cases of the world tables: an empty world, a world at the
+    16-cuboid maximum (rotated boxes all around the arm), and a world whose
+    one large box engulfs the lower arm (sphere centres inside: the SDF's
+    inside branch and the linear part of the hinge)."""
+    rng = np.random.Generator(np.random.Philox(key=0xED6E))
+    rows = []
+    for k in range(16):
+        r = np.zeros(16, np.float32)
+        r[0:9] = _rot(rng).reshape(-1)
+        ang = 2 * np.pi * k / 16
+        rad = rng.uniform(0.25, 0.7)
+        r[9:12] = (rad * np.cos(ang), rad * np.sin(ang), rng.uniform(0.05, 0.9))
+        r[12:15] = rng.uniform(0.03, 0.15, 3)
+        rows.append(r)
+    big = np.zeros(16, np.float32)
+    big[0:9] = np.eye(3).reshape(-1)
+    big[9:12] = (0.0, 0.0, 0.35)
+    big[12:15] = (0.25, 0.25, 0.35)
+    rows.append(big)
+    cub = np.stack(rows).astype(np.float32)
+    off = np.array([0, 0, 16, 17], np.int32)
+    return make_workload("edge_worlds", ["empty", "max16", "engulf"], [0, 1, 2], seeds, H,
+                         FORMAT_SETS[formats], cuboids=cub, offsets=off, salt=21)
+
+
 WORKLOADS = {
     "config1": lambda: config1(),
     "config1_fp32": lambda: config1(reduced=False),
@@ -151,6 +187,9 @@ WORKLOADS = {
     "pf5_pf8": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="pf5_pf8"),
     "pf3": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="pf3"),
     "bf16": lambda: config4(problems_per_env=1, seeds=2, H=32, formats="bf16"),
+    "edge_worlds": lambda: edge_worlds_workload(),
+    "edge_worlds_fp32": lambda: edge_worlds_workload(formats="fp32"),
+    "h2_min_swept": lambda: ragged_workload(B=4, H=2, salt=23),
 }
 
 
