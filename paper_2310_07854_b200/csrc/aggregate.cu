@@ -21,8 +21,14 @@ namespace vapr {
 
 namespace {
 
-constexpr int kRows = 32;
-constexpr int kThreads = 128;
+#ifndef VAPR_AGG_ROWS
+#define VAPR_AGG_ROWS 16
+#endif
+constexpr int kRows = VAPR_AGG_ROWS;
+#ifndef VAPR_AGG_THREADS
+#define VAPR_AGG_THREADS 128
+#endif
+constexpr int kThreads = VAPR_AGG_THREADS;
 
 // Decode the packed tile `src` (rows of W words, pf values per word) into the
 // FP32 tile x (stride xs): x = value (ADD = false) or x += value (ADD = true).
@@ -90,10 +96,12 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
         decode_tile<decltype(Pc)::value, true>(so, Wo, nr, cols, rw_o, x, xs, fov, &negz);
     });
     __syncthreads();
-    // slots past the last element encode as code 0 whatever the inputs' padding
-    for (int i = tid; i < nr * (xs - cols); i += kThreads) {
-        const int r = i / (xs - cols);
-        x[r * xs + cols + (i - r * (xs - cols))] = 0.f;
+    // slots past the last element that the encode pass reads: +0, whatever
+    // the inputs' padding held
+    const int tail = Wg * fg.pf - cols;
+    for (int i = tid; i < nr * tail; i += kThreads) {
+        const int r = i / tail;
+        x[r * xs + cols + (i - r * tail)] = 0.f;
     }
     __syncthreads();
     uint32_t* dst = gos + r0 * Wg;
