@@ -224,9 +224,10 @@ vapr_status vapr_cost_grad(vapr_ctx *ctx, const float *q, const int32_t *world_i
 /* The same computation from HOST buffers: q_host [B, H, 7] in, grad_q_host
  * [B, H, 7] and cost_traj_host [B] (nullable) out, with the host<->device
  * copies pipelined against the compute.  The batch is split into n_chunks
- * contiguous trajectory ranges (0 = automatic: about 640k poses per chunk);
- * chunk i's H2D copy, chunk i-1's compute and chunk i-2's D2H copies run
- * concurrently on two context-owned copy streams and `stream`.  Every output
+ * contiguous trajectory ranges (0 = automatic: up to ~900k poses per chunk;
+ * the first and last chunks are a quarter of the others, so the exposed
+ * copies are short); chunk i's H2D copy, chunk i-1's compute and chunk i-2's
+ * D2H copies run concurrently on two context-owned copy streams and `stream`.  Every output
  * is bit-identical to vapr_cost_grad's (the kernels see the same rows).
  * Device buffers (caller-owned): q_dev [B*H*7], workspace (as for
  * vapr_cost_grad), cost_pose_dev [B*H] (nullable: workspace scratch),

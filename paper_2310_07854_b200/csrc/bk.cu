@@ -21,7 +21,10 @@ namespace vapr {
 
 namespace {
 
-constexpr int kTile = 128;                 // poses (= threads) per CTA
+#ifndef VAPR_BK_TILE
+#define VAPR_BK_TILE 128
+#endif
+constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
 
 __global__ void __launch_bounds__(kTile)
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
