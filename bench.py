@@ -327,7 +327,8 @@ def main():
         r.set_formats(fm)
 
     if rank == 0:
-        cpu = None if args.no_cpu else cpu_baseline(fm, args.H, args.cpu_sample_poses)
+        # the oracle leg runs on rank 0 of a 1-GPU run only (the contract)
+        cpu = None if (args.no_cpu or world > 1) else cpu_baseline(fm, args.H, args.cpu_sample_poses)
         bits = sum(1 + e + m for e, m in fm)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
