@@ -14,6 +14,7 @@ Modules:
   kinematics  Panda FK / BK in float64
   collision   box SDF, smooth hinge, world (discrete/swept) and self costs
   rollout     the staged FK -> world -> self -> aggregate -> BK dataflow
+  lbfgs       L-BFGS two-loop direction, N-scale line search, history (N1)
 Parity status of each function is listed in DESIGN.md §4 (all pinned; the
 "3.5x-4.4x tensor size reduction" figure of PAPER.md:316 is parity unpinned
 and is not computed here).
