@@ -244,6 +244,42 @@ vapr_status vapr_cost_grad_host(vapr_ctx *ctx, const float *q_host, const int32_
                                 float *cost_traj_host, float *grad_q_host, int32_t n_chunks,
                                 void *stream);
 
+/* ---- N1: the optimiser steps around vapr_cost_grad ----- */
+/* PAPER.md:162 "(1) Given N, step scales of step direction ... (6) Use line
+ * search to pick one from N. (7) Lastly, compute step direction (L-BFGS) and
+ * buffer updates".  Readings c29-c33.  A batch
+ * item b owns the D-vector x[b] (for trajectory optimisation D = 7 H: the
+ * trajectory's joint values, layout [B, H, 7] = [B, D]).  All pointers are
+ * device pointers, row-major, 4-byte aligned, caller-owned; scales is a HOST
+ * array of N strictly increasing positive floats, 1 <= N <= 32. */
+#define VAPR_LBFGS_MAX_M 32
+#define VAPR_LBFGS_MAX_D 512
+
+/* Step (1): the N x B line-search batch cand[n, b, :] = fl(x[b] + fl(s_n d[b]))
+ * ([N, B, D], i.e. N*B trajectories in vapr_cost_grad's layout). */
+vapr_status vapr_lbfgs_candidates(const float *x, const float *d, int32_t B, int32_t D,
+                                  const float *scales, int32_t N, float *cand, void *stream);
+
+/* Steps (6) and (7) for every batch item, given the costs cand_cost [N, B]
+ * and gradients cand_grad [N, B, D] of the candidates (vapr_cost_grad on
+ * the batch above): chosen[b] = the argmin candidate if its cost is strictly
+ * below cost[b] (ties to the smaller scale), else -1.  Accepted: x, g, cost
+ * take the candidate's values, (x' - x, g' - g) joins the history when
+ * s.y > curvature_eps (FIFO of m, slot head[b], count[b]).  Rejected: a
+ * non-empty history is cleared, else d is shrunk tenfold (c32).  Finally d
+ * (in: the direction the candidates used) becomes the two-loop direction
+ * -H g.  History buffers: hist_s, hist_y [B, m, D], hist_rho [B, m],
+ * hist_count, hist_head [B] (zero-initialised by the caller for an empty
+ * history).  chosen is nullable.  Errors: VAPR_ERR_SHAPE for B < 0, D < 1,
+ * D > VAPR_LBFGS_MAX_D, N outside [1, 32], m outside [1, VAPR_LBFGS_MAX_M];
+ * VAPR_ERR_INVALID_ARG for null buffers or non-positive / non-increasing
+ * scales. */
+vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float *scales, int32_t N,
+                            const float *cand_cost, const float *cand_grad, float *x, float *g,
+                            float *cost, float *d, float *hist_s, float *hist_y, float *hist_rho,
+                            int32_t *hist_count, int32_t *hist_head, int32_t *chosen, int32_t m,
+                            float curvature_eps, void *stream);
+
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =
  * its lowest argmin; problem p owns trajectories [p*seeds, (p+1)*seeds). */

@@ -34,7 +34,7 @@ EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
            "vapr_self_collision", "vapr_collision", "vapr_aggregate",
            "vapr_backward_kinematics", "vapr_cost_grad_workspace_bytes",
            "vapr_cost_grad_workspace_layout", "vapr_cost_grad", "vapr_cost_grad_host",
-           "vapr_best_per_problem")
+           "vapr_lbfgs_candidates", "vapr_lbfgs_step", "vapr_best_per_problem")
 
 
 class VaprError(RuntimeError):
@@ -94,6 +94,9 @@ def _load():
         "vapr_cost_grad": ([P, P, P, I32, I32, ctypes.POINTER(vapr_cost_params), P, SZ, P, P, P, P], I32),
         "vapr_cost_grad_host": ([P, P, P, I32, I32, ctypes.POINTER(vapr_cost_params), P, SZ, P, P, P,
                                  P, P, P, I32, P], I32),
+        "vapr_lbfgs_candidates": ([P, P, I32, I32, P, I32, P, P], I32),
+        "vapr_lbfgs_step": ([I32, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32,
+                             ctypes.c_float, P], I32),
         "vapr_best_per_problem": ([P, I32, I32, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
@@ -300,3 +303,25 @@ def vapr_cost_grad_host(ctx, q_host, world_idx, B, H, params, workspace, q_dev, 
                                    _ptr(cost_traj_dev), _ptr(grad_q_dev), _hptr(cost_traj_host),
                                    _hptr(grad_q_host), int(n_chunks), _stream(stream)),
            "vapr_cost_grad_host")
+
+
+def _scales(scales):
+    arr = (ctypes.c_float * len(scales))(*[float(v) for v in scales])
+    return arr, len(scales)
+
+
+def vapr_lbfgs_candidates(x, d, B, D, scales, cand, stream=None):
+    """cand [N, B, D] = fl(x + fl(s_n d)) (include/vapr.h, N1 step (1))."""
+    arr, n = _scales(scales)
+    _check(lib.vapr_lbfgs_candidates(_ptr(x), _ptr(d), B, D, arr, n, _ptr(cand), _stream(stream)),
+           "vapr_lbfgs_candidates")
+
+
+def vapr_lbfgs_step(B, D, scales, cand_cost, cand_grad, x, g, cost, d, hist_s, hist_y, hist_rho,
+                    hist_count, hist_head, chosen=None, m=10, curvature_eps=1e-10, stream=None):
+    """Line-search selection, history update and two-loop direction (N1 steps (6), (7))."""
+    arr, n = _scales(scales)
+    _check(lib.vapr_lbfgs_step(B, D, arr, n, _ptr(cand_cost), _ptr(cand_grad), _ptr(x), _ptr(g),
+                               _ptr(cost), _ptr(d), _ptr(hist_s), _ptr(hist_y), _ptr(hist_rho),
+                               _ptr(hist_count), _ptr(hist_head), _ptr(chosen), int(m),
+                               float(curvature_eps), _stream(stream)), "vapr_lbfgs_step")

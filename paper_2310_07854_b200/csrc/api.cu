@@ -802,6 +802,47 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     return cuda_status(e);
 }
 
+// ---- N1 ------------------------------------------------------------------
+static bool scales_ok(const float* scales, int32_t N, LbfgsScales* out) {
+    if (!scales || N < 1 || N > 32) return false;
+    for (int i = 0; i < N; ++i) {
+        if (!(scales[i] > 0.f) || !std::isfinite(scales[i])) return false;
+        if (i > 0 && !(scales[i] > scales[i - 1])) return false;
+        out->s[i] = scales[i];
+    }
+    return true;
+}
+
+vapr_status vapr_lbfgs_candidates(const float* x, const float* d, int32_t B, int32_t D,
+                                  const float* scales, int32_t N, float* cand, void* stream) {
+    CHECK(B >= 0 && D >= 1 && N >= 1 && N <= 32, VAPR_ERR_SHAPE);
+    if (B == 0) return VAPR_OK;
+    LbfgsScales sc{};
+    CHECK(x && d && cand && scales_ok(scales, N, &sc), VAPR_ERR_INVALID_ARG);
+    CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_lbfgs_candidates(x, d, B, D, N, sc, cand, (cudaStream_t)stream));
+}
+
+vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float* scales, int32_t N,
+                            const float* cand_cost, const float* cand_grad, float* x, float* g,
+                            float* cost, float* d, float* hist_s, float* hist_y, float* hist_rho,
+                            int32_t* hist_count, int32_t* hist_head, int32_t* chosen, int32_t m,
+                            float curvature_eps, void* stream) {
+    CHECK(B >= 0 && D >= 1 && D <= VAPR_LBFGS_MAX_D && N >= 1 && N <= 32 && m >= 1 &&
+              m <= VAPR_LBFGS_MAX_M,
+          VAPR_ERR_SHAPE);
+    if (B == 0) return VAPR_OK;
+    LbfgsScales sc{};
+    CHECK(scales_ok(scales, N, &sc) && std::isfinite(curvature_eps), VAPR_ERR_INVALID_ARG);
+    CHECK(cand_cost && cand_grad && x && g && cost && d && hist_s && hist_y && hist_rho &&
+              hist_count && hist_head,
+          VAPR_ERR_INVALID_ARG);
+    CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    return cuda_status(launch_lbfgs_step(B, D, N, sc, cand_cost, cand_grad, x, g, cost, d, hist_s,
+                                         hist_y, hist_rho, hist_count, hist_head, chosen, m,
+                                         curvature_eps, (cudaStream_t)stream));
+}
+
 // ---- e -------------------------------------------------------------------
 vapr_status vapr_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,
                                   float* best_cost, int32_t* best_seed, void* stream) {

@@ -1,5 +1,6 @@
 // kernels.cuh -- host-side launch helpers for the libvapr kernels.
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -48,6 +49,16 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
                              uint32_t* gos, cudaStream_t s);
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s);
+// N1 optimiser (lbfgs.cu)
+struct LbfgsScales {
+    float s[32];
+};
+cudaError_t launch_lbfgs_candidates(const float* x, const float* d, long long B, int D, int N,
+                                    const LbfgsScales& sc, float* cand, cudaStream_t s);
+cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const float* cand_cost,
+                              const float* cand_grad, float* x, float* g, float* cost, float* d,
+                              float* hs, float* hy, float* hrho, int32_t* hcount, int32_t* hhead,
+                              int32_t* chosen, int m, float eps, cudaStream_t s);
 cudaError_t launch_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,
                                     float* best_cost, int32_t* best_seed, cudaStream_t s);
 

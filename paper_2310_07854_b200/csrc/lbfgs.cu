@@ -1,0 +1,238 @@
+// lbfgs.cu -- N1: the optimiser steps around the rollout.
+// "(1) Given N, step scales of step direction ... (6) Use line search to pick
+// one from N. (7) Lastly, compute step direction (L-BFGS) and buffer
+// updates"; PAPER.md:86 (the L-BFGS step-direction kernel).  Readings c29-c33
+// (DESIGN.md §3): FIFO history of (s, y) pairs kept when s.y > eps, two-loop
+// recursion with gamma = s.y / y.y of the newest pair, argmin line search
+// with ties to the smaller scale and a strict-improvement guard, history
+// cleared (or the rejected direction shrunk tenfold) after a failed search.
+//
+// candidates_kernel: the N x B line-search batch, x + s_n d, one rounding per
+//   operation (fl(x + fl(s d))), float4-vectorised, HBM-bound.
+// lbfgs_step_kernel: one warp per batch item; its D-vectors live in registers
+//   (D <= 32 * kMaxPerLane), every dot product is a warp reduction, the
+//   history is streamed twice (two-loop recursion) with coalesced loads.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace vapr {
+
+namespace {
+
+constexpr int kMaxPerLane = 16;        // D <= 512
+constexpr int kStepWarps = 4;
+
+__global__ void candidates_kernel(const float* __restrict__ x, const float* __restrict__ d,
+                                  long long BD, int N, const __grid_constant__ LbfgsScales sc,
+                                  float* __restrict__ cand) {
+    const long long total = (long long)N * BD;
+    const bool vec = (BD & 3) == 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    if (vec) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* d4 = reinterpret_cast<const float4*>(d);
+        float4* c4 = reinterpret_cast<float4*>(cand);
+        const long long BD4 = BD >> 2;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total >> 2; i += stride) {
+            const int n = int(i / BD4);
+            const long long j = i - n * BD4;
+            const float s = sc.s[n];
+            const float4 xv = __ldg(x4 + j), dv = __ldg(d4 + j);
+            c4[i] = make_float4(__fadd_rn(xv.x, __fmul_rn(s, dv.x)), __fadd_rn(xv.y, __fmul_rn(s, dv.y)),
+                                __fadd_rn(xv.z, __fmul_rn(s, dv.z)), __fadd_rn(xv.w, __fmul_rn(s, dv.w)));
+        }
+    } else {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+            const int n = int(i / BD);
+            const long long j = i - n * BD;
+            cand[i] = __fadd_rn(__ldg(x + j), __fmul_rn(sc.s[n], __ldg(d + j)));
+        }
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// the lane's elements of a D-vector: i = lane + 32 k, k < kMaxPerLane
+template <typename F>
+__device__ __forceinline__ void for_lane(int D, int lane, F&& f) {
+#pragma unroll
+    for (int k = 0; k < kMaxPerLane; ++k) {
+        const int i = lane + 32 * k;
+        if (i < D) f(k, i);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kStepWarps)
+lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
+                  const float* __restrict__ cand_cost,
+                  const float* __restrict__ cand_grad, float* __restrict__ x,
+                  float* __restrict__ g, float* __restrict__ cost, float* __restrict__ d,
+                  float* __restrict__ hs, float* __restrict__ hy, float* __restrict__ hrho,
+                  int32_t* __restrict__ hcount, int32_t* __restrict__ hhead,
+                  int32_t* __restrict__ chosen, int m, float eps) {
+    __shared__ float s_alpha[kStepWarps][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int b = blockIdx.x * kStepWarps + wib;
+    if (b >= B) return;
+    const long long o = (long long)b * D;
+
+    // (6) line search: argmin over the candidates, ties to the smaller scale,
+    // strict improvement on the current cost required (NaN never improves)
+    float best = cost[b];
+    int nb = -1;
+    for (int n0 = 0; n0 < N; n0 += 32) {
+        const int n = n0 + lane;
+        const float c = (n < N) ? cand_cost[(long long)n * B + b] : 0.f;
+        // sequential scan semantics: candidate n wins iff c < every earlier
+        // candidate and c < best so far -> the smallest index of the minimum
+        const bool ok = n < N && c < best;
+        float cm = ok ? c : __int_as_float(0x7f800000);
+        int im = ok ? n : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float c2 = __shfl_xor_sync(0xffffffffu, cm, off);
+            const int i2 = __shfl_xor_sync(0xffffffffu, im, off);
+            if (c2 < cm || (c2 == cm && i2 < im)) {
+                cm = c2;
+                im = i2;
+            }
+        }
+        if (im != 0x7fffffff) {
+            best = cm;
+            nb = im;
+        }
+    }
+    if (lane == 0 && chosen) chosen[b] = nb;
+
+    int count = hcount[b], head = hhead[b];
+    float gv[kMaxPerLane], q[kMaxPerLane];
+    if (nb < 0) {
+        // c32: no improvement -> clear a non-empty history (next d = -g), or
+        // shrink an already steepest-descent direction tenfold
+        if (count > 0) {
+            for_lane(D, lane, [&](int, int i) { d[o + i] = -g[o + i]; });
+            if (lane == 0) {
+                hcount[b] = 0;
+                hhead[b] = 0;
+            }
+        } else {
+            for_lane(D, lane, [&](int, int i) { d[o + i] = 0.1f * d[o + i]; });
+        }
+        return;
+    }
+
+    // accept candidate nb: x' = fl(x + fl(s d)) (the evaluated point), g' its
+    // gradient; the pair (s, y) = (x' - x, g' - g) joins the history iff s.y > eps
+    const float s = sc.s[nb];
+    const float* gn = cand_grad + ((long long)nb * B + b) * D;
+    float sv[kMaxPerLane], yv[kMaxPerLane];
+    float sy = 0.f, yy = 0.f;
+    for_lane(D, lane, [&](int k, int i) {
+        const float xo = x[o + i];
+        const float xn = __fadd_rn(xo, __fmul_rn(s, d[o + i]));
+        const float gnew = gn[i];
+        sv[k] = xn - xo;
+        yv[k] = gnew - g[o + i];
+        sy = fmaf(sv[k], yv[k], sy);
+        yy = fmaf(yv[k], yv[k], yy);
+        x[o + i] = xn;
+        g[o + i] = gnew;
+        gv[k] = gnew;
+    });
+    sy = warp_sum(sy);
+    yy = warp_sum(yy);
+    if (lane == 0) cost[b] = best;
+    if (sy > eps) {
+        const long long so = ((long long)b * m + head) * D;
+        for_lane(D, lane, [&](int k, int i) {
+            hs[so + i] = sv[k];
+            hy[so + i] = yv[k];
+        });
+        if (lane == 0) hrho[(long long)b * m + head] = 1.f / sy;
+        head = (head + 1 == m) ? 0 : head + 1;
+        count = min(count + 1, m);
+        if (lane == 0) {
+            hhead[b] = head;
+            hcount[b] = count;
+        }
+        __syncwarp();
+    }
+
+    // (7) two-loop recursion over the history, newest to oldest and back
+#pragma unroll
+    for (int k = 0; k < kMaxPerLane; ++k) q[k] = gv[k];
+    float* alpha = s_alpha[wib];
+    for (int t = 0; t < count; ++t) {
+        int slot = head - 1 - t;
+        if (slot < 0) slot += m;
+        const float* si = hs + ((long long)b * m + slot) * D;
+        const float* yi = hy + ((long long)b * m + slot) * D;
+        float dot = 0.f;
+        for_lane(D, lane, [&](int k, int i) { dot = fmaf(si[i], q[k], dot); });
+        const float a = hrho[(long long)b * m + slot] * warp_sum(dot);
+        if (lane == 0) alpha[t] = a;
+        for_lane(D, lane, [&](int k, int i) { q[k] = fmaf(-a, yi[i], q[k]); });
+    }
+    __syncwarp();
+    // gamma from the newest pair (the one just stored when accepted, else the
+    // previous newest: recompute its s.y and y.y)
+    float gamma = 1.f;
+    if (count > 0) {
+        const int newest = (head == 0) ? m - 1 : head - 1;
+        const float* si = hs + ((long long)b * m + newest) * D;
+        const float* yi = hy + ((long long)b * m + newest) * D;
+        float a = 0.f, c = 0.f;
+        for_lane(D, lane, [&](int, int i) {
+            a = fmaf(si[i], yi[i], a);
+            c = fmaf(yi[i], yi[i], c);
+        });
+        gamma = warp_sum(a) / warp_sum(c);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxPerLane; ++k) q[k] *= gamma;
+    for (int t = count - 1; t >= 0; --t) {           // oldest to newest
+        int slot = head - 1 - t;
+        if (slot < 0) slot += m;
+        const float* si = hs + ((long long)b * m + slot) * D;
+        const float* yi = hy + ((long long)b * m + slot) * D;
+        float dot = 0.f;
+        for_lane(D, lane, [&](int k, int i) { dot = fmaf(yi[i], q[k], dot); });
+        const float beta = hrho[(long long)b * m + slot] * warp_sum(dot);
+        const float coef = alpha[t] - beta;
+        for_lane(D, lane, [&](int k, int i) { q[k] = fmaf(si[i], coef, q[k]); });
+    }
+    for_lane(D, lane, [&](int k, int i) { d[o + i] = -q[k]; });
+}
+
+}  // namespace
+
+cudaError_t launch_lbfgs_candidates(const float* x, const float* d, long long B, int D, int N,
+                                    const LbfgsScales& sc, float* cand, cudaStream_t s) {
+    const long long BD = B * (long long)D;
+    if (BD <= 0 || N <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long work = ((BD & 3) == 0 ? (BD >> 2) : BD) * N;
+    const long long grid = std::min<long long>((work + 255) / 256, (long long)sms * 8);
+    candidates_kernel<<<(unsigned)grid, 256, 0, s>>>(x, d, BD, N, sc, cand);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const float* cand_cost,
+                              const float* cand_grad, float* x, float* g, float* cost, float* d,
+                              float* hs, float* hy, float* hrho, int32_t* hcount, int32_t* hhead,
+                              int32_t* chosen, int m, float eps, cudaStream_t s) {
+    if (B <= 0) return cudaSuccess;
+    const int grid = (B + kStepWarps - 1) / kStepWarps;
+    lbfgs_step_kernel<<<grid, 32 * kStepWarps, 0, s>>>(B, D, N, sc, cand_cost, cand_grad, x, g,
+                                                       cost, d, hs, hy, hrho, hcount, hhead,
+                                                       chosen, m, eps);
+    return cudaGetLastError();
+}
+
+}  // namespace vapr
