@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--chunks", type=int, default=0,
                     help="e2e: trajectory chunks of the pipelined host call (0 = automatic)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
+    ap.add_argument("--no-to", action="store_true",
+                    help="skip the TO-iteration leg (N1: L-BFGS + N-scale line search)")
     ap.add_argument("--no-e2e", action="store_true",
                     help="skip the end-to-end leg (profiling runs: keeps the launch list to the device step)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -317,6 +319,21 @@ def main():
                "d2h_bytes_per_step": gq_host.numel() * 4 + ct_host.numel() * 4,
                "ms_per_step": e2e_ms}
 
+    # ---- a full TO iteration: candidates for N step
+    # scales, vapr_cost_grad over the N x B batch, line search + L-BFGS
+    to_iter = None
+    if not args.no_to:
+        from paper_2310_07854_b200.optimize import TrajOpt
+        opt = TrajOpt(wl, device=local)
+        opt.reset()
+        to_ms = timed(opt.step, max(3, args.steps // 4), 2)
+        to_iter = {"ms_per_iteration": to_ms, "line_search_scales": list(opt.scales),
+                   "trajectories": opt.B * world, "poses_evaluated_per_iteration": opt.N * P * world,
+                   "trajectory_iterations_per_s": opt.B * world / (to_ms * 1e-3),
+                   "history_m": opt.m}
+        del opt
+        torch.cuda.empty_cache()
+
     # ---- FP32 comparison (the >= 2x target of BASELINE.json) on the same batch
     fp32 = None
     if not args.no_fp32 and args.formats != "fp32":
@@ -348,6 +365,7 @@ def main():
             "roofline": roofline,
             "e2e": e2e,
             "fp32": fp32,
+            "to_iteration": to_iter,
             "cpu_baseline": cpu,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clocks,

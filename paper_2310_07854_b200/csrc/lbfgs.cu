@@ -22,31 +22,29 @@ namespace {
 constexpr int kMaxPerLane = 16;        // D <= 512
 constexpr int kStepWarps = 4;
 
+// grid.y = the scale index n: cand[n] = fl(x + fl(s_n d)), no index division
 __global__ void candidates_kernel(const float* __restrict__ x, const float* __restrict__ d,
-                                  long long BD, int N, const __grid_constant__ LbfgsScales sc,
+                                  long long BD, const __grid_constant__ LbfgsScales sc,
                                   float* __restrict__ cand) {
-    const long long total = (long long)N * BD;
-    const bool vec = (BD & 3) == 0;
+    const int n = blockIdx.y;
+    const float s = sc.s[n];
     const long long stride = (long long)gridDim.x * blockDim.x;
-    if (vec) {
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((BD & 3) == 0) {
         const float4* x4 = reinterpret_cast<const float4*>(x);
         const float4* d4 = reinterpret_cast<const float4*>(d);
-        float4* c4 = reinterpret_cast<float4*>(cand);
-        const long long BD4 = BD >> 2;
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total >> 2; i += stride) {
-            const int n = int(i / BD4);
-            const long long j = i - n * BD4;
-            const float s = sc.s[n];
-            const float4 xv = __ldg(x4 + j), dv = __ldg(d4 + j);
-            c4[i] = make_float4(__fadd_rn(xv.x, __fmul_rn(s, dv.x)), __fadd_rn(xv.y, __fmul_rn(s, dv.y)),
-                                __fadd_rn(xv.z, __fmul_rn(s, dv.z)), __fadd_rn(xv.w, __fmul_rn(s, dv.w)));
+        float4* c4 = reinterpret_cast<float4*>(cand + n * BD);
+        for (long long i = i0; i < (BD >> 2); i += stride) {
+            const float4 xv = __ldg(x4 + i), dv = __ldg(d4 + i);
+            __stcs(c4 + i, make_float4(__fadd_rn(xv.x, __fmul_rn(s, dv.x)),
+                                       __fadd_rn(xv.y, __fmul_rn(s, dv.y)),
+                                       __fadd_rn(xv.z, __fmul_rn(s, dv.z)),
+                                       __fadd_rn(xv.w, __fmul_rn(s, dv.w))));
         }
     } else {
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-            const int n = int(i / BD);
-            const long long j = i - n * BD;
-            cand[i] = __fadd_rn(__ldg(x + j), __fmul_rn(sc.s[n], __ldg(d + j)));
-        }
+        float* c = cand + n * BD;
+        for (long long i = i0; i < BD; i += stride)
+            c[i] = __fadd_rn(__ldg(x + i), __fmul_rn(s, __ldg(d + i)));
     }
 }
 
@@ -217,9 +215,10 @@ cudaError_t launch_lbfgs_candidates(const float* x, const float* d, long long B,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long work = ((BD & 3) == 0 ? (BD >> 2) : BD) * N;
-    const long long grid = std::min<long long>((work + 255) / 256, (long long)sms * 8);
-    candidates_kernel<<<(unsigned)grid, 256, 0, s>>>(x, d, BD, N, sc, cand);
+    const long long work = (BD & 3) == 0 ? (BD >> 2) : BD;
+    const long long gx = std::max<long long>(1, std::min<long long>((work + 255) / 256,
+                                                                   (long long)sms * 8 / N + 1));
+    candidates_kernel<<<dim3((unsigned)gx, (unsigned)N), 256, 0, s>>>(x, d, BD, sc, cand);
     return cudaGetLastError();
 }
 
