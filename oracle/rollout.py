@@ -18,6 +18,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .ikcost import bound_cost, pose_cost
+
 from . import codec
 from .kinematics import sphere_centers, backward, backward_terms_abs
 from .collision import world_cost, self_cost
@@ -108,10 +110,33 @@ class RolloutResult:
     stages: dict
 
 
-def rollout(q, world_idx, cuboids, offsets, robot, params, formats):
+def ik_terms(q, world_idx, robot, params, goals, H):
+    """N2 (PAPER.md:162 step (3)): pose + bound cost [P] and their joint
+    gradient [P, 7] (oracle/ikcost.py), or None when both weights are 0."""
+    wp, wr, wb = (float(params.get(k, 0.0)) for k in ("w_pose_pos", "w_pose_rot", "w_bound"))
+    if wp == 0.0 and wr == 0.0 and wb == 0.0:
+        return None
+    q64 = np.asarray(q, np.float32).astype(np.float64).reshape(-1, 7)
+    cost = np.zeros(q64.shape[0])
+    grad = np.zeros_like(q64)
+    if wp != 0.0 or wr != 0.0:
+        gi = np.repeat(np.asarray(world_idx), H)
+        G = np.asarray(goals, np.float32).astype(np.float64)[gi]
+        c, g = pose_cost(q64, robot, G[:, :9].reshape(-1, 3, 3), G[:, 9:], wp, wr)
+        cost += c
+        grad += g
+    if wb != 0.0:
+        c, g = bound_cost(q64, robot["q_lo"], robot["q_hi"], wb)
+        cost += c
+        grad += g
+    return cost, grad
+
+
+def rollout(q, world_idx, cuboids, offsets, robot, params, formats, goals=None):
     """Full vapr_cost_grad dataflow: FK -> world (discrete or swept) -> self ->
-    aggregate -> BK.  formats in slot order (os, gos,
-    ov, cp, cps)."""
+    aggregate -> BK, plus the IKO pose / bound terms when
+    their weights are non-zero (N2).  formats in slot order (os, gos, ov, cp,
+    cps)."""
     q = np.asarray(q, np.float32)
     B, H = q.shape[0], q.shape[1]
     cols = _cols(robot)
@@ -126,12 +151,17 @@ def rollout(q, world_idx, cuboids, offsets, robot, params, formats):
     ag = aggregate_stage(ws["words"], f_cp, ss["words"], f_ov, f_gos, cols)
     bk = bk_stage(q.reshape(-1, 7), ag["words"], f_gos, robot)
     cost_pose = ws["cost"] + ss["cost"].reshape(B, H)
+    grad_q = bk["grad_q"].reshape(B, H, 7)
+    ik = ik_terms(q, world_idx, robot, params, goals, H)
+    if ik is not None:
+        cost_pose = cost_pose + ik[0].reshape(B, H)
+        grad_q = grad_q + ik[1].reshape(B, H, 7)
     return RolloutResult(os_words, ws["words"], ss["words"], ag["words"],
-                         cost_pose, cost_pose.sum(axis=1),
-                         bk["grad_q"].reshape(B, H, 7),
-                         dict(fk=v_os, world=ws, self=ss, aggregate=ag, bk=bk))
+                         cost_pose, cost_pose.sum(axis=1), grad_q,
+                         dict(fk=v_os, world=ws, self=ss, aggregate=ag, bk=bk, ik=ik))
 
 
 def rollout_workload(wl, formats=None):
     return rollout(wl.q, wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
-                   wl.params, formats if formats is not None else wl.formats)
+                   wl.params, formats if formats is not None else wl.formats,
+                   goals=getattr(wl, "goals", None))

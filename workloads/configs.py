@@ -42,7 +42,8 @@ FORMAT_SETS = {
 FORMAT_SETS["43bit"] = FORMAT_SETS["table_under_pick"]
 
 DEFAULT_PARAMS = dict(eta_world=0.025, eta_self=0.01, w_world=1.0,
-                      w_self=1.0, swept=1, sweep_steps=1)
+                      w_self=1.0, swept=1, sweep_steps=1,
+                      w_pose_pos=0.0, w_pose_rot=0.0, w_bound=0.0)
 
 
 @dataclass
@@ -56,6 +57,7 @@ class Workload:
     params: dict = field(default_factory=lambda: dict(DEFAULT_PARAMS))
     envs: tuple = ()              # environment of each world
     formats: tuple = FP32
+    goals: np.ndarray = None      # [n_worlds, 12] float32 (R row-major, p): IKO pose goals (N2)
 
     @property
     def B(self):
@@ -129,6 +131,45 @@ def config5(problems_per_env=10, seeds=20, H=32):
     ids = list(range(problems_per_env * len(ENVIRONMENTS)))
     envs = [ENVIRONMENTS[p % len(ENVIRONMENTS)] for p in ids]
     return make_workload("config5", envs, ids, seeds, H, FP32, salt=5)
+
+
+def make_goals(keys):
+    """One end-effector goal pose per problem (N2, reading c37): position
+    uniform in a box in front of the robot, orientation a uniform random
+    rotation (unit quaternion from 4 normals).  Pure sampling -- no robot
+    arithmetic (reachability is not required of a cost-function workload)."""
+    out = np.zeros((len(keys), 12), np.float32)
+    for i, k in enumerate(keys):
+        rng = np.random.Generator(np.random.Philox(key=_key(k, 0x60A1)))
+        w, x, y, z = rng.normal(size=4)
+        n = np.sqrt(w * w + x * x + y * y + z * z)
+        w, x, y, z = w / n, x / n, y / n, z / n
+        R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                      [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                      [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+        out[i, :9] = R.reshape(-1)
+        out[i, 9:] = rng.uniform([0.3, -0.4, 0.2], [0.7, 0.4, 0.7])
+    return out
+
+
+IKO_PARAMS = dict(swept=0, sweep_steps=0, w_pose_pos=1.0, w_pose_rot=0.5, w_bound=1.0)
+
+
+def config_iko(problems_per_env=10, seeds=400, formats="43bit", problem_offset=0,
+               n_problems=None):
+    """N2 IKO workload: H = 1, `seeds` random joint configurations per problem
+    (100-2000 IKO seeds), discrete world collision (closest_pt,
+    slot 3), self collision, pose cost to the problem's goal and joint-bound
+    cost (PAPER.md:162 step (3)); problems cycle through the 8 environments."""
+    total = problems_per_env * len(ENVIRONMENTS)
+    if n_problems is None:
+        n_problems = total
+    ids = list(range(problem_offset, problem_offset + n_problems))
+    envs = [ENVIRONMENTS[p % len(ENVIRONMENTS)] for p in ids]
+    fm = FORMAT_SETS[formats] if isinstance(formats, str) else formats
+    wl = make_workload("iko", envs, ids, seeds, 1, fm, params=IKO_PARAMS, salt=7)
+    wl.goals = make_goals([(7, int(p)) for p in ids])
+    return wl
 
 
 def codec_sweep_inputs(n, kind, key=0):
