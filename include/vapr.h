@@ -100,6 +100,7 @@ typedef struct {
     const int32_t *sphere_link;        /* host [n_spheres]    */
     const float *sphere_xyzr;          /* host [n_spheres][4] */
     const uint16_t *pairs;             /* host [n_pairs][2]   */
+    double q_lo[7], q_hi[7];           /* joint limits (rad), for the bound cost (N2, c36) */
 } vapr_robot;
 
 /* One oriented box (64 B): R = world-from-box rotation (row-major 3x3),
@@ -108,10 +109,17 @@ typedef struct { float R[9]; float t[3]; float half[3]; float pad; } vapr_cuboid
 
 /* Cost parameters (readings c14, c17): smooth-hinge activation
  * distances eta_* (m), weights w_*, swept = 1 for the TO swept world cost with
- * sweep_steps >= 0 linear sub-samples per segment, 0 for the discrete cost. */
+ * sweep_steps >= 0 linear sub-samples per segment, 0 for the discrete cost.
+ * The IKO terms of vapr_cost_grad (N2, PAPER.md:162 step (3) "pose ... and
+ * bound position"; readings c34-c36): pose cost w_pose_pos |p - p_g|^2 +
+ * w_pose_rot |R - R_g|_F^2 of the hand frame against the goal of the
+ * trajectory's problem (vapr_set_goals, indexed like world_idx), bound cost
+ * w_bound sum_j max(0, q_j - q_hi)^2 + max(0, q_lo - q_j)^2.  All three 0
+ * (the TO default): no IKO terms. */
 typedef struct {
     float eta_world, eta_self, w_world, w_self;
     int32_t swept, sweep_steps;
+    float w_pose_pos, w_pose_rot, w_bound;
 } vapr_cost_params;
 
 /* Options (vapr_set_option). */
@@ -128,6 +136,13 @@ const char *vapr_version(void);
  * returned on the calling host thread ("no error" if none); a static string
  * owned by the CUDA runtime, never freed by the caller.  Diagnostics only. */
 const char *vapr_last_cuda_error(void);
+
+/* IKO pose goals (N2): goals[w] = the hand-frame goal of problem / world w,
+ * 12 floats (R row-major 3x3, then p), host memory, copied; n_goals >= 0.
+ * vapr_cost_grad reads goal world_idx[b] for trajectory b when a pose weight
+ * is non-zero (VAPR_ERR_NOT_INITIALIZED if no goals were set; an index
+ * outside [0, n_goals) contributes no pose cost). */
+vapr_status vapr_set_goals(vapr_ctx *ctx, const float *goals, int32_t n_goals);
 
 /* "E<e>M<m>", case-insensitive. */
 vapr_status vapr_format_parse(const char *s, vapr_format *out);

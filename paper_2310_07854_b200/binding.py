@@ -29,7 +29,8 @@ STATUS = {0: "VAPR_OK", 1: "VAPR_ERR_INVALID_FORMAT", 2: "VAPR_ERR_INVALID_ARG",
 EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
            "vapr_last_cuda_error",
            "vapr_format_parse", "vapr_format_check", "vapr_packed_row_words",
-           "vapr_set_formats", "vapr_set_robot", "vapr_set_worlds", "vapr_set_option",
+           "vapr_set_formats", "vapr_set_robot", "vapr_set_worlds", "vapr_set_goals",
+           "vapr_set_option",
            "vapr_quantize", "vapr_dequantize", "vapr_fk_spheres", "vapr_world_collision",
            "vapr_self_collision", "vapr_collision", "vapr_aggregate",
            "vapr_backward_kinematics", "vapr_cost_grad_workspace_bytes",
@@ -52,13 +53,16 @@ class vapr_robot(ctypes.Structure):
                 ("dh_a", ctypes.c_double * 8), ("dh_d", ctypes.c_double * 8),
                 ("dh_alpha", ctypes.c_double * 8), ("hand_rz", ctypes.c_double),
                 ("sphere_link", ctypes.c_void_p), ("sphere_xyzr", ctypes.c_void_p),
-                ("pairs", ctypes.c_void_p)]
+                ("pairs", ctypes.c_void_p),
+                ("q_lo", ctypes.c_double * 7), ("q_hi", ctypes.c_double * 7)]
 
 
 class vapr_cost_params(ctypes.Structure):
     _fields_ = [("eta_world", ctypes.c_float), ("eta_self", ctypes.c_float),
                 ("w_world", ctypes.c_float), ("w_self", ctypes.c_float),
-                ("swept", ctypes.c_int32), ("sweep_steps", ctypes.c_int32)]
+                ("swept", ctypes.c_int32), ("sweep_steps", ctypes.c_int32),
+                ("w_pose_pos", ctypes.c_float), ("w_pose_rot", ctypes.c_float),
+                ("w_bound", ctypes.c_float)]
 
 
 def _load():
@@ -80,6 +84,7 @@ def _load():
         "vapr_set_formats": ([P, P], I32),
         "vapr_set_robot": ([P, ctypes.POINTER(vapr_robot)], I32),
         "vapr_set_worlds": ([P, I32, P, P], I32),
+        "vapr_set_goals": ([P, P, I32], I32),
         "vapr_set_option": ([P, I32, I32], I32),
         "vapr_quantize": ([vapr_format, P, SZ, SZ, P, P], I32),
         "vapr_dequantize": ([vapr_format, P, SZ, SZ, P, P], I32),
@@ -213,6 +218,9 @@ def vapr_set_robot(ctx, robot):
         r.dh_d[i] = float(robot["dh_d"][i])
         r.dh_alpha[i] = float(robot["dh_alpha"][i])
     r.hand_rz = float(robot["hand_rz"])
+    for j in range(7):
+        r.q_lo[j] = float(robot["q_lo"][j])
+        r.q_hi[j] = float(robot["q_hi"][j])
     r.sphere_link = link.ctypes.data
     r.sphere_xyzr = xyzr.ctypes.data
     r.pairs = pairs.ctypes.data if pairs.size else None
@@ -226,13 +234,22 @@ def vapr_set_worlds(ctx, cuboids, offsets):
                                off.ctypes.data), "vapr_set_worlds")
 
 
+def vapr_set_goals(ctx, goals):
+    "IKO hand-frame goals, one per problem / world: [n, 12] (R row-major, p)."
+    g = np.ascontiguousarray(goals, np.float32).reshape(-1, 12)
+    _check(lib.vapr_set_goals(ctx, g.ctypes.data if g.size else None, g.shape[0]),
+           "vapr_set_goals")
+
+
 def vapr_set_option(ctx, option, value):
     _check(lib.vapr_set_option(ctx, option, int(value)), "vapr_set_option")
 
 
 def cost_params(p):
     return vapr_cost_params(float(p["eta_world"]), float(p["eta_self"]), float(p["w_world"]),
-                            float(p["w_self"]), int(p["swept"]), int(p["sweep_steps"]))
+                            float(p["w_self"]), int(p["swept"]), int(p["sweep_steps"]),
+                            float(p.get("w_pose_pos", 0.0)), float(p.get("w_pose_rot", 0.0)),
+                            float(p.get("w_bound", 0.0)))
 
 
 def vapr_fk_spheres(ctx, q, B, H, out_spheres, stream=None):

@@ -33,6 +33,10 @@ struct vapr_ctx {
     // the host-side slot cursor
     unsigned int* d_sched = nullptr;
     unsigned int sched_next = 0;
+    // IKO goals (N2)
+    float* d_goals = nullptr;
+    int32_t n_goals = 0;
+    bool goals_set = false;
 };
 
 namespace {
@@ -159,6 +163,7 @@ vapr_status vapr_create(int device, vapr_ctx** out) {
         if (!g.ok || cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess ||
             cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess) {
             if (c->d_sched) cudaFree(c->d_sched);
+    if (c->d_goals) cudaFree(c->d_goals);
             delete c;
             cudaGetLastError();
             return VAPR_ERR_CUDA;
@@ -178,10 +183,30 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     if (c->d_cub) cudaFree(c->d_cub);
     if (c->d_off) cudaFree(c->d_off);
     if (c->d_sched) cudaFree(c->d_sched);
+    if (c->d_goals) cudaFree(c->d_goals);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     delete c;
+    return VAPR_OK;
+}
+
+vapr_status vapr_set_goals(vapr_ctx* c, const float* goals, int32_t n_goals) {
+    CHECK(c != nullptr && n_goals >= 0, VAPR_ERR_INVALID_ARG);
+    CHECK(n_goals == 0 || goals != nullptr, VAPR_ERR_INVALID_ARG);
+    DeviceGuard g(c->device);
+    CHECK(g.ok, VAPR_ERR_CUDA);
+    if (c->d_goals) cudaFree(c->d_goals);
+    c->d_goals = nullptr;
+    c->n_goals = 0;
+    if (n_goals > 0) {
+        const size_t bytes = sizeof(float) * 12 * (size_t)n_goals;
+        if (cuda_status(cudaMalloc(&c->d_goals, bytes)) != VAPR_OK) return VAPR_ERR_CUDA;
+        if (cuda_status(cudaMemcpy(c->d_goals, goals, bytes, cudaMemcpyHostToDevice)) != VAPR_OK)
+            return VAPR_ERR_CUDA;
+    }
+    c->n_goals = n_goals;
+    c->goals_set = true;
     return VAPR_OK;
 }
 
@@ -238,6 +263,10 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     }
     R.hand_c = (float)std::cos(r->hand_rz);
     R.hand_s = (float)std::sin(r->hand_rz);
+    for (int j = 0; j < kJoints; ++j) {
+        R.q_lo[j] = (float)r->q_lo[j];
+        R.q_hi[j] = (float)r->q_hi[j];
+    }
     int prev = 0;
     int count[kLinks] = {0};
     for (int s = 0; s < r->n_spheres; ++s) {
@@ -652,7 +681,18 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     uint32_t* ov = rows_of(VAPR_OUT_VEC);
     uint32_t* gos = rows_of(VAPR_GRAD_OUT_SPHERES);
     const float* qc = q + p0 * kJoints;
-    cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], qc, P, os, s);
+    // IKO terms (N2): FK writes cost_pose = pose + bound, the collision passes add
+    IkArgs ik{};
+    ik.goals = c->d_goals;
+    ik.n_goals = c->n_goals;
+    ik.world_idx = world_idx + b0;
+    ik.H = H;
+    ik.w_pos = p->w_pose_pos;
+    ik.w_rot = p->w_pose_rot;
+    ik.w_bound = p->w_bound;
+    ik.cost = cpose + p0;
+    const bool iko = ik_on(ik);
+    cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], qc, P, os, s, iko ? &ik : nullptr);
     if (e == cudaSuccess) {
         CollisionArgs a{};
         a.os = os;
@@ -671,6 +711,7 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.cost = cpose + p0;
         a.cp = cp;
         a.ov = ov;
+        a.cost_accumulate = iko ? 1 : 0;
         e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
                              c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
@@ -679,7 +720,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
                              cols, cp, ov, P, gos, s);
     if (e == cudaSuccess)
-        e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s);
+        e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
+                      iko ? &ik : nullptr);
     return e;
 }
 
@@ -701,8 +743,11 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
     CHECK(cost_pose == nullptr || aligned16(cost_pose), VAPR_ERR_INVALID_ARG);
     CHECK(cost_traj == nullptr || aligned16(cost_traj), VAPR_ERR_INVALID_ARG);
     CHECK(p->eta_world > 0.f && p->eta_self > 0.f && std::isfinite(p->w_world) &&
-              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64,
+              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64 &&
+              std::isfinite(p->w_pose_pos) && std::isfinite(p->w_pose_rot) &&
+              std::isfinite(p->w_bound),
           VAPR_ERR_INVALID_ARG);
+    CHECK((p->w_pose_pos == 0.f && p->w_pose_rot == 0.f) || c->goals_set, VAPR_ERR_NOT_INITIALIZED);
     const long long P = (long long)B * H;
     size_t off[VAPR_NUM_SLOTS], co, total;
     ws_layout(c, P, p->swept, off, &co, &total);
@@ -732,8 +777,11 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     CHECK(cost_pose_dev == nullptr || aligned16(cost_pose_dev), VAPR_ERR_INVALID_ARG);
     CHECK(n_chunks >= 0, VAPR_ERR_INVALID_ARG);
     CHECK(p->eta_world > 0.f && p->eta_self > 0.f && std::isfinite(p->w_world) &&
-              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64,
+              std::isfinite(p->w_self) && p->sweep_steps >= 0 && p->sweep_steps <= 64 &&
+              std::isfinite(p->w_pose_pos) && std::isfinite(p->w_pose_rot) &&
+              std::isfinite(p->w_bound),
           VAPR_ERR_INVALID_ARG);
+    CHECK((p->w_pose_pos == 0.f && p->w_pose_rot == 0.f) || c->goals_set, VAPR_ERR_NOT_INITIALIZED);
     const long long P = (long long)B * H;
     size_t off[VAPR_NUM_SLOTS], co, total;
     ws_layout(c, P, p->swept, off, &co, &total);

@@ -26,10 +26,11 @@ namespace {
 #endif
 constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
 
+template <bool IKO>
 __global__ void __launch_bounds__(kTile)
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
-          uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt) {
+          uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik) {
     extern __shared__ unsigned long long smem8[];
     const int WS = W + 4;                 // 16-byte aligned rows
     float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
@@ -90,7 +91,10 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 
     // compact the poses with a non-zero gradient so the chains below run in
     // full warps (each pose's result is independent of the order)
-    if (mask) {
+    // with the IKO pose cost every pose is active (its hand frame carries a
+    // force and a torque whatever its sphere gradients)
+    const bool pose_on = IKO && (ik.w_pos != 0.f || ik.w_rot != 0.f);
+    if (tid < np && (mask || pose_on)) {
         const int k = atomicAdd(&s_nact, 1);
         s_act[k] = tid;
         s_mask[k] = mask;
@@ -123,8 +127,25 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
             }
             const int s0 = R.link_start[l], s1 = R.link_start[l + 1];
             unsigned long long lm = (pmask >> s0) & ((s1 - s0 >= 64) ? ~0ull : ((1ull << (s1 - s0)) - 1ull));
-            if (!lm) continue;
+            const bool hand_ik = pose_on && l == kLinks - 1;
+            if (!lm && !hand_ik) continue;
             float Fx = 0.f, Fy = 0.f, Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f;
+            if (hand_ik) {
+                // N2: the pose cost's force F at the hand origin p and torque tau
+                // act on the hand link: F_l += F, M_l += p x F + tau
+                const long long pg = p0 + pp;
+                const int wi = ik.world_idx[pg / ik.H];
+                if (wi >= 0 && wi < ik.n_goals) {
+                    float F[3], tau[3];
+                    ik_pose_cost(X, ik.goals + 12 * wi, ik.w_pos, ik.w_rot, F, tau);
+                    Fx = F[0];
+                    Fy = F[1];
+                    Fz = F[2];
+                    Mx = X.p[1] * F[2] - X.p[2] * F[1] + tau[0];
+                    My = X.p[2] * F[0] - X.p[0] * F[2] + tau[1];
+                    Mz = X.p[0] * F[1] - X.p[1] * F[0] + tau[2];
+                }
+            }
             while (lm) {
                 const int s = s0 + __ffsll((long long)lm) - 1;
                 lm &= lm - 1;
@@ -160,6 +181,14 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
         for (int j = 0; j < kJoints; ++j) sg[pp * kJoints + j] = gq[j];
     }
     __syncthreads();
+    // N2 bound cost: its gradient is per joint, for every pose
+    if (IKO && ik.w_bound != 0.f && tid < np)
+        for (int j = 0; j < kJoints; ++j) {
+            float dq;
+            ik_bound(sq[tid * kJoints + j], R.q_lo[j], R.q_hi[j], ik.w_bound, dq);
+            sg[tid * kJoints + j] += dq;
+        }
+    __syncthreads();
     // coalesced grad_q store (zero for poses without a gradient)
     for (int i = tid; i < np * kJoints; i += kTile) __stcs(grad_q + p0 * kJoints + i, sg[i]);
 }
@@ -167,15 +196,13 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 }  // namespace
 
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
-                      const uint32_t* gos, float* grad_q, cudaStream_t s) {
+                      const uint32_t* gos, float* grad_q, cudaStream_t s, const IkArgs* ik) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
     const size_t smem = sizeof(float4) * kMaxSpheres +
                         sizeof(float) * kTile * kJoints +
                         sizeof(uint32_t) * kTile * (W + 4) + sizeof(float) * kTile * kJoints;
-    cudaError_t e = cudaFuncSetAttribute(bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
     const uint32_t rc = 65536u / fgos.pf + 1u;
     const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
     // SWAR masks of the format's fields: top bits, low t-1 bits; slot = (b+1)/t - 1
@@ -187,8 +214,13 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     }
     const uint32_t rt = 65536u / fgos.t + 1u;
     const long long grid = (P + kTile - 1) / kTile;
-    bk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc, rq, f_lo,
-                                                  f_hi, rt);
+    const bool iko = ik && ik_on(*ik);
+    auto kern = iko ? bk_kernel<true> : bk_kernel<false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    IkArgs none{};
+    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc, rq, f_lo, f_hi, rt,
+                                             iko ? *ik : none);
     return cudaGetLastError();
 }
 

@@ -302,6 +302,7 @@ struct RobotDev {
     int32_t cols;                        // 3 * n_spheres
     float ca[8], sa[8], a[8], d[8];      // modified-DH rows (cos/sin alpha, a, d)
     float hand_c, hand_s;                // RotZ(hand_rz)
+    float q_lo[kJoints], q_hi[kJoints];  // joint limits (bound cost, N2)
     int32_t link_start[kLinks + 1];      // spheres sorted by link
     float sx[kMaxSpheres], sy[kMaxSpheres], sz[kMaxSpheres], sr[kMaxSpheres];
     // self-collision adjacency (CSR): partners of sphere s are
@@ -397,6 +398,44 @@ __device__ __forceinline__ void fk_step(Xf& X, const RobotDev& R, int row, float
 __device__ __forceinline__ void fk_hand(Xf& X, const RobotDev& R) {
     xf_dh(X, R.ca[7], R.sa[7], R.a[7], R.d[7], 1.f, 0.f);
     xf_rotz(X, R.hand_c, R.hand_s);
+}
+
+// N2 pose cost of the hand frame X against the goal G (12 floats: R
+// row-major, p) -- reading c35: w_pos |p - p_g|^2 + w_rot |R - R_g|_F^2, with
+// the force F = 2 w_pos (p - p_g) at p and the torque
+// tau = -2 w_rot sum_k r_k x g_k (columns) that carry its gradient to the joints.
+__device__ __forceinline__ float ik_pose_cost(const Xf& X, const float* G, float w_pos, float w_rot,
+                                              float* F, float* tau) {
+    const float dx = X.p[0] - G[9], dy = X.p[1] - G[10], dz = X.p[2] - G[11];
+    float rr = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const float e = X.r[i] - G[i];
+        rr = fmaf(e, e, rr);
+    }
+    F[0] = 2.f * w_pos * dx;
+    F[1] = 2.f * w_pos * dy;
+    F[2] = 2.f * w_pos * dz;
+    float tx = 0.f, ty = 0.f, tz = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {        // r_k = (r[k], r[3+k], r[6+k]), g_k likewise
+        const float ax = X.r[k], ay = X.r[3 + k], az = X.r[6 + k];
+        const float bx = G[k], by = G[3 + k], bz = G[6 + k];
+        tx += ay * bz - az * by;
+        ty += az * bx - ax * bz;
+        tz += ax * by - ay * bx;
+    }
+    tau[0] = -2.f * w_rot * tx;
+    tau[1] = -2.f * w_rot * ty;
+    tau[2] = -2.f * w_rot * tz;
+    return w_pos * fmaf(dx, dx, fmaf(dy, dy, dz * dz)) + w_rot * rr;
+}
+
+// N2 joint-bound cost (reading c36) of one joint and its derivative.
+__device__ __forceinline__ float ik_bound(float q, float lo, float hi, float w, float& dq) {
+    const float a = fmaxf(q - hi, 0.f), b = fmaxf(lo - q, 0.f);
+    dq = 2.f * w * (a - b);
+    return w * fmaf(a, a, b * b);
 }
 
 }  // namespace vapr

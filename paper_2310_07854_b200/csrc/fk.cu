@@ -47,9 +47,10 @@ struct Emitter {
     }
 };
 
+template <bool IKO>
 __global__ void __launch_bounds__(kTile)
 fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
-          long long P, int W, uint32_t* __restrict__ os, uint32_t rq) {
+          long long P, int W, uint32_t* __restrict__ os, uint32_t rq, const IkArgs ik) {
     extern __shared__ uint32_t smem[];
     const int WS = W + 1;
     float* sq = reinterpret_cast<float*>(smem);    // [kTile * 7]
@@ -70,7 +71,23 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
             xf_identity(X);
             for (int l = 0; l < kLinks; ++l) {
                 if (l >= 1 && l <= kJoints) fk_step(X, R, l - 1, sq[tid * kJoints + l - 1]);
-                if (l == kLinks - 1) fk_hand(X, R);
+                if (l == kLinks - 1) {
+                    fk_hand(X, R);
+                    if constexpr (IKO) {   // N2: pose + bound cost of this pose -> cost_pose
+                        float c = 0.f, F[3], tau[3];
+                        const long long pg = p0 + tid;
+                        const int wi = ik.world_idx[pg / ik.H];
+                        if ((ik.w_pos != 0.f || ik.w_rot != 0.f) && wi >= 0 && wi < ik.n_goals)
+                            c = ik_pose_cost(X, ik.goals + 12 * wi, ik.w_pos, ik.w_rot, F, tau);
+                        if (ik.w_bound != 0.f)
+                            for (int j = 0; j < kJoints; ++j) {
+                                float dq;
+                                c += ik_bound(sq[tid * kJoints + j], R.q_lo[j], R.q_hi[j],
+                                              ik.w_bound, dq);
+                            }
+                        ik.cost[pg] = c;
+                    }
+                }
                 for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
                     float cx, cy, cz;
                     xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
@@ -98,16 +115,19 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 }  // namespace
 
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
-                      uint32_t* os, cudaStream_t s) {
+                      uint32_t* os, cudaStream_t s, const IkArgs* ik) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fos, R.cols);
     const size_t smem = sizeof(float) * kTile * kJoints + sizeof(uint32_t) * kTile * (W + 1);
-    cudaError_t e = cudaFuncSetAttribute(fk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const bool iko = ik && ik_on(*ik);
+    auto kern = iko ? fk_kernel<true> : fk_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     const long long grid = (P + kTile - 1) / kTile;
     const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
-    fk_kernel<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq);
+    IkArgs none{};
+    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq, iko ? *ik : none);
     return cudaGetLastError();
 }
 

@@ -36,8 +36,21 @@ cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t co
                             size_t row_words, uint32_t* packed, int sms, cudaStream_t s);
 cudaError_t launch_dequantize(const Fmt& f, const uint32_t* packed, size_t rows, size_t cols,
                               size_t row_words, float* y, int sms, cudaStream_t s);
+// IKO terms of vapr_cost_grad (N2): pose cost of the hand frame against
+// goals[world_idx[pose / H]] and the joint-bound cost; disabled when all
+// weights are 0 (then the pointers may be null)
+struct IkArgs {
+    const float* goals;        // [n_goals][12] R row-major, p
+    int32_t n_goals;
+    const int32_t* world_idx;  // [B] (the chunk's)
+    int32_t H;
+    float w_pos, w_rot, w_bound;
+    float* cost;               // FK: cost_pose [P] = pose + bound (the collision passes add)
+};
+inline bool ik_on(const IkArgs& k) { return k.w_pos != 0.f || k.w_rot != 0.f || k.w_bound != 0.f; }
+
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
-                      uint32_t* os, cudaStream_t s);
+                      uint32_t* os, cudaStream_t s, const IkArgs* ik = nullptr);
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                              unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);
@@ -48,7 +61,8 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
                              const uint32_t* cp, const uint32_t* ov, long long rows,
                              uint32_t* gos, cudaStream_t s);
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
-                      const uint32_t* gos, float* grad_q, cudaStream_t s);
+                      const uint32_t* gos, float* grad_q, cudaStream_t s,
+                      const IkArgs* ik = nullptr);
 // N1 optimiser (lbfgs.cu)
 struct LbfgsScales {
     float s[32];

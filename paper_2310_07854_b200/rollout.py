@@ -17,7 +17,8 @@ SLOT_NAMES = ("out_spheres", "grad_out_spheres", "out_vec", "closest_pt", "close
 class Context:
     """RAII wrapper of a vapr_ctx."""
 
-    def __init__(self, device=0, robot=None, formats=None, cuboids=None, offsets=None):
+    def __init__(self, device=0, robot=None, formats=None, cuboids=None, offsets=None,
+                 goals=None):
         self.device = int(device)
         self.h = vb.vapr_create(self.device)
         if robot is not None:
@@ -26,6 +27,8 @@ class Context:
             self.set_formats(formats)
         if cuboids is not None:
             vb.vapr_set_worlds(self.h, cuboids, offsets)
+        if goals is not None:
+            vb.vapr_set_goals(self.h, goals)
 
     def set_formats(self, formats):
         self.formats = tuple(tuple(f) for f in formats)
@@ -53,7 +56,8 @@ class Rollout:
         self.wl = workload
         self.device = torch.device("cuda", device)
         self.ctx = ctx or Context(device, workload.robot, formats or workload.formats,
-                                  workload.cuboids, workload.world_offsets)
+                                  workload.cuboids, workload.world_offsets,
+                                  getattr(workload, "goals", None))
         if formats is not None and ctx is not None:
             self.ctx.set_formats(formats)
         self.B, self.H = workload.B, workload.H
