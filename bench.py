@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--chunks", type=int, default=0,
                     help="e2e: trajectory chunks of the pipelined host call (0 = automatic)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
+    ap.add_argument("--no-iko", action="store_true",
+                    help="skip the IKO leg (N2: H = 1, 1000 seeds x 800 problems, pose + bound costs)")
     ap.add_argument("--no-to", action="store_true",
                     help="skip the TO-iteration leg (N1: L-BFGS + N-scale line search)")
     ap.add_argument("--no-e2e", action="store_true",
@@ -334,6 +336,25 @@ def main():
         del opt
         torch.cuda.empty_cache()
 
+    # ---- the IKO workload: H = 1, pose + bound + discrete
+    # world + self costs; one vapr_cost_grad and one full L-BFGS iteration
+    iko = None
+    if not args.no_iko:
+        from paper_2310_07854_b200.optimize import TrajOpt
+        from workloads import config_iko
+        wli = config_iko(problems_per_env=args.problems_per_env, seeds=1000, formats=fm,
+                         problem_offset=ids[0], n_problems=len(ids))
+        opt = TrajOpt(wli, device=local)
+        opt.reset()
+        ev_ms = timed(opt.base.run, max(3, args.steps // 2), 2)
+        it_ms = timed(opt.step, max(3, args.steps // 4), 2)
+        iko = {"poses": wli.poses * world, "seeds_per_problem": 1000,
+               "cost_grad_ms": ev_ms, "cost_grad_pose_evals_per_s": wli.poses * world / (ev_ms * 1e-3),
+               "iteration_ms": it_ms, "line_search_scales": list(opt.scales),
+               "seed_iterations_per_s": wli.B * world / (it_ms * 1e-3)}
+        del opt
+        torch.cuda.empty_cache()
+
     # ---- FP32 comparison (the >= 2x target of BASELINE.json) on the same batch
     fp32 = None
     if not args.no_fp32 and args.formats != "fp32":
@@ -366,6 +387,7 @@ def main():
             "e2e": e2e,
             "fp32": fp32,
             "to_iteration": to_iter,
+            "iko": iko,
             "cpu_baseline": cpu,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clocks,

@@ -9,9 +9,10 @@
 //
 // candidates_kernel: the N x B line-search batch, x + s_n d, one rounding per
 //   operation (fl(x + fl(s d))), float4-vectorised, HBM-bound.
-// lbfgs_step_kernel: one warp per batch item; its D-vectors live in registers
-//   (D <= 32 * kMaxPerLane), every dot product is a warp reduction, the
-//   history is streamed twice (two-loop recursion) with coalesced loads.
+// lbfgs_step_kernel: LPI lanes per batch item (the smallest power of two >= D,
+//   at most 32: IKO's D = 7 packs four items per warp); the item's D-vectors
+//   live in registers, every dot product is a sub-group reduction, the history
+//   is streamed twice (two-loop recursion) with coalesced loads.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -48,22 +49,31 @@ __global__ void candidates_kernel(const float* __restrict__ x, const float* __re
     }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// sum / max over the LPI lanes of a sub-group (xor shuffles stay inside it)
+template <int LPI>
+__device__ __forceinline__ float grp_sum(float v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = LPI / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, LPI);
+    return v;
+}
+template <int LPI>
+__device__ __forceinline__ int grp_max(int v) {
+#pragma unroll
+    for (int o = LPI / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o, LPI));
+    return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
-// the lane's elements of a D-vector: i = lane + 32 k, k < kMaxPerLane
-template <typename F>
-__device__ __forceinline__ void for_lane(int D, int lane, F&& f) {
-#pragma unroll
-    for (int k = 0; k < kMaxPerLane; ++k) {
-        const int i = lane + 32 * k;
-        if (i < D) f(k, i);
-    }
-}
-
+// One sub-group of LPI lanes per batch item (32 / LPI items per warp; LPI =
+// the smallest power of two >= D, at most 32), its D-vectors in registers
+// (element i = sub-lane + LPI k).  Every shuffle is executed by the whole
+// warp: branches between the items of a warp are predicated, loop bounds are
+// warp maxima.
+template <int LPI>
 __global__ void __launch_bounds__(32 * kStepWarps)
 lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
                   const float* __restrict__ cand_cost,
@@ -72,28 +82,37 @@ lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
                   float* __restrict__ hs, float* __restrict__ hy, float* __restrict__ hrho,
                   int32_t* __restrict__ hcount, int32_t* __restrict__ hhead,
                   int32_t* __restrict__ chosen, int m, float eps) {
-    __shared__ float s_alpha[kStepWarps][32];
+    constexpr int G = 32 / LPI;                    // items per warp
+    constexpr int KPL = (LPI == 32) ? kMaxPerLane : 1;   // LPI < 32 only when D <= LPI
+    __shared__ float s_alpha[kStepWarps][G][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int b = blockIdx.x * kStepWarps + wib;
-    if (b >= B) return;
-    const long long o = (long long)b * D;
+    const int sub = lane / LPI, sl = lane % LPI;
+    const int b = (blockIdx.x * kStepWarps + wib) * G + sub;
+    const bool valid = b < B;
+    if (__all_sync(0xffffffffu, !valid)) return;
+    const long long o = (long long)(valid ? b : 0) * D;
+    auto each = [&](auto&& f) {
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const int i = sl + LPI * k;
+            if (valid && i < D) f(k, i);
+        }
+    };
 
     // (6) line search: argmin over the candidates, ties to the smaller scale,
     // strict improvement on the current cost required (NaN never improves)
-    float best = cost[b];
+    float best = valid ? cost[b] : 0.f;
     int nb = -1;
-    for (int n0 = 0; n0 < N; n0 += 32) {
-        const int n = n0 + lane;
-        const float c = (n < N) ? cand_cost[(long long)n * B + b] : 0.f;
-        // sequential scan semantics: candidate n wins iff c < every earlier
-        // candidate and c < best so far -> the smallest index of the minimum
-        const bool ok = n < N && c < best;
+    for (int n0 = 0; n0 < N; n0 += LPI) {
+        const int n = n0 + sl;
+        const float c = (valid && n < N) ? cand_cost[(long long)n * B + b] : 0.f;
+        const bool ok = valid && n < N && c < best;
         float cm = ok ? c : __int_as_float(0x7f800000);
         int im = ok ? n : 0x7fffffff;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float c2 = __shfl_xor_sync(0xffffffffu, cm, off);
-            const int i2 = __shfl_xor_sync(0xffffffffu, im, off);
+        for (int off = LPI / 2; off > 0; off >>= 1) {
+            const float c2 = __shfl_xor_sync(0xffffffffu, cm, off, LPI);
+            const int i2 = __shfl_xor_sync(0xffffffffu, im, off, LPI);
             if (c2 < cm || (c2 == cm && i2 < im)) {
                 cm = c2;
                 im = i2;
@@ -104,106 +123,121 @@ lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
             nb = im;
         }
     }
-    if (lane == 0 && chosen) chosen[b] = nb;
+    if (valid && sl == 0 && chosen) chosen[b] = nb;
 
-    int count = hcount[b], head = hhead[b];
-    float gv[kMaxPerLane], q[kMaxPerLane];
-    if (nb < 0) {
+    int count = valid ? hcount[b] : 0, head = valid ? hhead[b] : 0;
+    const bool acc = valid && nb >= 0;
+    if (valid && nb < 0) {
         // c32: no improvement -> clear a non-empty history (next d = -g), or
         // shrink an already steepest-descent direction tenfold
         if (count > 0) {
-            for_lane(D, lane, [&](int, int i) { d[o + i] = -g[o + i]; });
-            if (lane == 0) {
+            each([&](int, int i) { d[o + i] = -g[o + i]; });
+            if (sl == 0) {
                 hcount[b] = 0;
                 hhead[b] = 0;
             }
         } else {
-            for_lane(D, lane, [&](int, int i) { d[o + i] = 0.1f * d[o + i]; });
+            each([&](int, int i) { d[o + i] = 0.1f * d[o + i]; });
         }
-        return;
     }
 
     // accept candidate nb: x' = fl(x + fl(s d)) (the evaluated point), g' its
     // gradient; the pair (s, y) = (x' - x, g' - g) joins the history iff s.y > eps
-    const float s = sc.s[nb];
-    const float* gn = cand_grad + ((long long)nb * B + b) * D;
-    float sv[kMaxPerLane], yv[kMaxPerLane];
-    float sy = 0.f, yy = 0.f;
-    for_lane(D, lane, [&](int k, int i) {
-        const float xo = x[o + i];
-        const float xn = __fadd_rn(xo, __fmul_rn(s, d[o + i]));
-        const float gnew = gn[i];
-        sv[k] = xn - xo;
-        yv[k] = gnew - g[o + i];
-        sy = fmaf(sv[k], yv[k], sy);
-        yy = fmaf(yv[k], yv[k], yy);
-        x[o + i] = xn;
-        g[o + i] = gnew;
-        gv[k] = gnew;
-    });
-    sy = warp_sum(sy);
-    yy = warp_sum(yy);
-    if (lane == 0) cost[b] = best;
-    if (sy > eps) {
-        const long long so = ((long long)b * m + head) * D;
-        for_lane(D, lane, [&](int k, int i) {
-            hs[so + i] = sv[k];
-            hy[so + i] = yv[k];
+    float gv[KPL], q[KPL], sv[KPL], yv[KPL];
+    float sy = 0.f;
+    if (acc) {
+        const float s = sc.s[nb];
+        const float* gn = cand_grad + ((long long)nb * B + b) * D;
+        each([&](int k, int i) {
+            const float xo = x[o + i];
+            const float xn = __fadd_rn(xo, __fmul_rn(s, d[o + i]));
+            const float gnew = gn[i];
+            sv[k] = xn - xo;
+            yv[k] = gnew - g[o + i];
+            sy = fmaf(sv[k], yv[k], sy);
+            x[o + i] = xn;
+            g[o + i] = gnew;
+            gv[k] = gnew;
         });
-        if (lane == 0) hrho[(long long)b * m + head] = 1.f / sy;
-        head = (head + 1 == m) ? 0 : head + 1;
-        count = min(count + 1, m);
-        if (lane == 0) {
-            hhead[b] = head;
-            hcount[b] = count;
-        }
-        __syncwarp();
     }
-
-    // (7) two-loop recursion over the history, newest to oldest and back
-#pragma unroll
-    for (int k = 0; k < kMaxPerLane; ++k) q[k] = gv[k];
-    float* alpha = s_alpha[wib];
-    for (int t = 0; t < count; ++t) {
-        int slot = head - 1 - t;
-        if (slot < 0) slot += m;
-        const float* si = hs + ((long long)b * m + slot) * D;
-        const float* yi = hy + ((long long)b * m + slot) * D;
-        float dot = 0.f;
-        for_lane(D, lane, [&](int k, int i) { dot = fmaf(si[i], q[k], dot); });
-        const float a = hrho[(long long)b * m + slot] * warp_sum(dot);
-        if (lane == 0) alpha[t] = a;
-        for_lane(D, lane, [&](int k, int i) { q[k] = fmaf(-a, yi[i], q[k]); });
+    sy = grp_sum<LPI>(sy);
+    if (acc) {
+        if (sl == 0) cost[b] = best;
+        if (sy > eps) {
+            const long long so = ((long long)b * m + head) * D;
+            each([&](int k, int i) {
+                hs[so + i] = sv[k];
+                hy[so + i] = yv[k];
+            });
+            if (sl == 0) hrho[(long long)b * m + head] = 1.f / sy;
+            head = (head + 1 == m) ? 0 : head + 1;
+            count = min(count + 1, m);
+            if (sl == 0) {
+                hhead[b] = head;
+                hcount[b] = count;
+            }
+        }
     }
     __syncwarp();
-    // gamma from the newest pair (the one just stored when accepted, else the
-    // previous newest: recompute its s.y and y.y)
-    float gamma = 1.f;
-    if (count > 0) {
-        const int newest = (head == 0) ? m - 1 : head - 1;
-        const float* si = hs + ((long long)b * m + newest) * D;
-        const float* yi = hy + ((long long)b * m + newest) * D;
-        float a = 0.f, c = 0.f;
-        for_lane(D, lane, [&](int, int i) {
-            a = fmaf(si[i], yi[i], a);
-            c = fmaf(yi[i], yi[i], c);
-        });
-        gamma = warp_sum(a) / warp_sum(c);
-    }
+
+    // (7) two-loop recursion over the history, newest to oldest and back
+    // (accepted items; the loop bound is the warp's largest history)
+    const int cnt = acc ? count : 0;
+    const int tmax = warp_max(cnt);
 #pragma unroll
-    for (int k = 0; k < kMaxPerLane; ++k) q[k] *= gamma;
-    for (int t = count - 1; t >= 0; --t) {           // oldest to newest
+    for (int k = 0; k < KPL; ++k) q[k] = acc ? gv[k] : 0.f;
+    float* alpha = s_alpha[wib][sub];
+    for (int t = 0; t < tmax; ++t) {
+        const bool on = t < cnt;
         int slot = head - 1 - t;
         if (slot < 0) slot += m;
-        const float* si = hs + ((long long)b * m + slot) * D;
-        const float* yi = hy + ((long long)b * m + slot) * D;
+        const float* si = hs + ((long long)(valid ? b : 0) * m + slot) * D;
+        const float* yi = hy + ((long long)(valid ? b : 0) * m + slot) * D;
         float dot = 0.f;
-        for_lane(D, lane, [&](int k, int i) { dot = fmaf(yi[i], q[k], dot); });
-        const float beta = hrho[(long long)b * m + slot] * warp_sum(dot);
-        const float coef = alpha[t] - beta;
-        for_lane(D, lane, [&](int k, int i) { q[k] = fmaf(si[i], coef, q[k]); });
+        if (on) each([&](int k, int i) { dot = fmaf(si[i], q[k], dot); });
+        dot = grp_sum<LPI>(dot);
+        if (on) {
+            const float a = hrho[(long long)b * m + slot] * dot;
+            if (sl == 0) alpha[t] = a;
+            each([&](int k, int i) { q[k] = fmaf(-a, yi[i], q[k]); });
+        }
     }
-    for_lane(D, lane, [&](int k, int i) { d[o + i] = -q[k]; });
+    __syncwarp();
+    // gamma from the newest pair
+    float gamma = 1.f;
+    {
+        float a = 0.f, c = 0.f;
+        const int newest = (head == 0) ? m - 1 : head - 1;
+        if (cnt > 0) {
+            const float* si = hs + ((long long)b * m + newest) * D;
+            const float* yi = hy + ((long long)b * m + newest) * D;
+            each([&](int, int i) {
+                a = fmaf(si[i], yi[i], a);
+                c = fmaf(yi[i], yi[i], c);
+            });
+        }
+        a = grp_sum<LPI>(a);
+        c = grp_sum<LPI>(c);
+        if (cnt > 0) gamma = a / c;
+    }
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) q[k] *= gamma;
+    for (int t = tmax - 1; t >= 0; --t) {            // oldest to newest
+        const bool on = t < cnt;
+        int slot = head - 1 - t;
+        if (slot < 0) slot += m;
+        const float* si = hs + ((long long)(valid ? b : 0) * m + slot) * D;
+        const float* yi = hy + ((long long)(valid ? b : 0) * m + slot) * D;
+        float dot = 0.f;
+        if (on) each([&](int k, int i) { dot = fmaf(yi[i], q[k], dot); });
+        dot = grp_sum<LPI>(dot);
+        if (on) {
+            const float beta = hrho[(long long)b * m + slot] * dot;
+            const float coef = alpha[t] - beta;
+            each([&](int k, int i) { q[k] = fmaf(si[i], coef, q[k]); });
+        }
+    }
+    if (acc) each([&](int k, int i) { d[o + i] = -q[k]; });
 }
 
 }  // namespace
@@ -227,10 +261,21 @@ cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const 
                               float* hs, float* hy, float* hrho, int32_t* hcount, int32_t* hhead,
                               int32_t* chosen, int m, float eps, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
-    const int grid = (B + kStepWarps - 1) / kStepWarps;
-    lbfgs_step_kernel<<<grid, 32 * kStepWarps, 0, s>>>(B, D, N, sc, cand_cost, cand_grad, x, g,
-                                                       cost, d, hs, hy, hrho, hcount, hhead,
-                                                       chosen, m, eps);
+    // lanes per item: the smallest power of two >= D, at most 32
+    const int lpi = D <= 4 ? 4 : D <= 8 ? 8 : D <= 16 ? 16 : 32;
+    const int per_block = kStepWarps * (32 / lpi);
+    const int grid = (B + per_block - 1) / per_block;
+#define VAPR_LBFGS_LAUNCH(L)                                                                      \
+    lbfgs_step_kernel<L><<<grid, 32 * kStepWarps, 0, s>>>(B, D, N, sc, cand_cost, cand_grad, x, \
+                                                          g, cost, d, hs, hy, hrho, hcount,       \
+                                                          hhead, chosen, m, eps)
+    switch (lpi) {
+        case 4: VAPR_LBFGS_LAUNCH(4); break;
+        case 8: VAPR_LBFGS_LAUNCH(8); break;
+        case 16: VAPR_LBFGS_LAUNCH(16); break;
+        default: VAPR_LBFGS_LAUNCH(32); break;
+    }
+#undef VAPR_LBFGS_LAUNCH
     return cudaGetLastError();
 }
 

@@ -11,15 +11,17 @@ import torch  # noqa: E402
 
 from paper_2310_07854_b200 import binding as vb  # noqa: E402
 from paper_2310_07854_b200.optimize import TrajOpt  # noqa: E402
-from workloads import config4  # noqa: E402
+from workloads import config4, config_iko  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--ppe", type=int, default=100)
 ap.add_argument("--seeds", type=int, default=100)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--formats", default="43bit")
+ap.add_argument("--iko", action="store_true", help="the N2 IKO workload (H=1, --seeds per problem)")
 a = ap.parse_args()
-wl = config4(problems_per_env=a.ppe, seeds=a.seeds, H=32, formats=a.formats)
+wl = (config_iko(problems_per_env=a.ppe, seeds=a.seeds, formats=a.formats) if a.iko else
+      config4(problems_per_env=a.ppe, seeds=a.seeds, H=32, formats=a.formats))
 opt = TrajOpt(wl)
 opt.reset()
 for _ in range(2):

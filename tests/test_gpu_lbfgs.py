@@ -72,7 +72,8 @@ def _random_state(rng, B, D, m):
                 d=d, cost=cost, cc=cc, cg=cg)
 
 
-@pytest.mark.parametrize("B,D,m", [(64, 224, 10), (40, 37, 4), (8, 512, 32)])
+@pytest.mark.parametrize("B,D,m", [(64, 224, 10), (40, 37, 4), (8, 512, 32), (50, 7, 10),
+                                   (33, 3, 5), (21, 12, 10), (9, 16, 32)])
 def test_step_matches_oracle(vb, B, D, m):
     rng = np.random.default_rng(B + D + m)
     st = _random_state(rng, B, D, m)
