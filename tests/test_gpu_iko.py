@@ -123,3 +123,15 @@ def test_ik_solved_by_trajopt(vb, formats):
     assert np.array_equal(out["cost_traj"].view(np.uint32), prev.view(np.uint32))
     assert np.array_equal(out["grad_q"].reshape(-1).view(np.uint32),
                           opt.g.cpu().numpy().view(np.uint32))
+
+
+def test_set_goals_errors(vb):
+    h = vb.vapr_create(0)
+    try:
+        with pytest.raises(vb.VaprError):                   # n > 0 with a null pointer
+            vb._check(vb.lib.vapr_set_goals(h, None, 3), "null goals")
+        vb._check(vb.lib.vapr_set_goals(h, None, 0), "empty goals")   # n = 0: allowed
+        with pytest.raises(vb.VaprError):
+            vb._check(vb.lib.vapr_set_goals(h, None, -1), "negative")
+    finally:
+        vb.vapr_destroy(h)

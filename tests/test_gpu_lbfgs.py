@@ -235,3 +235,31 @@ def test_trajopt_on_robot_workload(vb, formats):
     out = fresh.results()
     assert np.array_equal(out["cost_traj"].view(np.uint32), cost.view(np.uint32))
     assert np.array_equal(out["grad_q"].reshape(-1).view(np.uint32), g.view(np.uint32))
+
+
+def test_lbfgs_errors(vb):
+    B, D = 4, 8
+    z = lambda n: torch.zeros(n, device="cuda")
+    x, d, g, c = z(B * D), z(B * D), z(B * D), z(B)
+    cand = z(2 * B * D)
+    with pytest.raises(vb.VaprError):                       # scales not increasing
+        vb.vapr_lbfgs_candidates(x, d, B, D, (0.3, 0.1), cand)
+    with pytest.raises(vb.VaprError):                       # non-positive scale
+        vb.vapr_lbfgs_candidates(x, d, B, D, (0.0, 0.1), cand)
+    with pytest.raises(vb.VaprError):                       # N > 32
+        vb.vapr_lbfgs_candidates(x, d, B, D, tuple(0.01 * (i + 1) for i in range(33)), cand)
+    hs, hy, hr = z(B * 4 * D), z(B * 4 * D), z(B * 4)
+    cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    head = torch.zeros_like(cnt)
+    with pytest.raises(vb.VaprError):                       # D above VAPR_LBFGS_MAX_D
+        vb.vapr_lbfgs_step(B, 513, (0.1, 1.0), z(2 * B), z(2 * B * 513), z(B * 513), z(B * 513),
+                           c, z(B * 513), z(B * 4 * 513), z(B * 4 * 513), hr, cnt, head, None, 4)
+    with pytest.raises(vb.VaprError):                       # m above VAPR_LBFGS_MAX_M
+        vb.vapr_lbfgs_step(B, D, (0.1, 1.0), z(2 * B), cand, x, g, c, d, hs, hy, hr, cnt, head,
+                           None, 33)
+    with pytest.raises(ValueError):                          # host tensor where device expected
+        vb.vapr_lbfgs_step(B, D, (0.1, 1.0), z(2 * B), cand, x.cpu(), g, c, d, hs, hy, hr, cnt,
+                           head, None, 4)
+    # B = 0 is a no-op
+    vb.vapr_lbfgs_candidates(x, d, 0, D, (0.1,), cand)
+    vb.vapr_lbfgs_step(0, D, (0.1,), z(1), cand, x, g, c, d, hs, hy, hr, cnt, head, None, 4)
