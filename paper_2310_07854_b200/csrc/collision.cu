@@ -223,7 +223,7 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, prec, grec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
+    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
     unsigned rows, pmask, pwm, wm, pk0, qi, qc, warp;
 };
@@ -264,6 +264,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.ref = take(4u * 3 * kLinks, 4);
     g.pij = take(2u * g.npairs, 2);
     g.prec = take(8u * g.npairs, 8);
+    g.gpid = take(2u * g.npairs, 2);
     g.grec = take(8u * kMaxGroupPairs, 8);
     g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
     g.gpab = take(2u * kMaxGroupPairs, 2);
@@ -365,6 +366,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint16_t* spij = reinterpret_cast<uint16_t*>(base + G.pij);     // i | j << 8
     uint2* sprec = reinterpret_cast<uint2*>(base + G.prec);        // candidate pairs in group-pair order
     uint2* sgrec = reinterpret_cast<uint2*>(base + G.grec);        // group-pair ball tests
+    uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + G.gpid);  // pair id of each record
     uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
     uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + G.gpab);   // a | b << 8
     uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);   // a | b << 8
@@ -394,11 +396,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     if (a.do_self) {
         for (int i = tid; i < G.npairs; i += blockDim.x) {
             spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
-            // record k of the group-pair order: 3i | 3j << 8 | pid << 16, and
-            // the activation distance r_i + r_j + eta
+            // record k of the group-pair order: byte offsets 12 i | 12 j << 16 in
+            // a row, and the activation distance r_i + r_j + eta; its pair id
+            // (needed only for an active pair) in sgpid[k]
             const int pid = R.gp_pid[i], pi = R.pair_i[pid], pj = R.pair_j[pid];
-            sprec[i] = make_uint2((uint32_t)(3 * pi) | ((uint32_t)(3 * pj) << 8) | ((uint32_t)pid << 16),
+            sprec[i] = make_uint2((uint32_t)(12 * pi) | ((uint32_t)(12 * pj) << 16),
                                   __float_as_uint(R.sr[pi] + R.sr[pj] + a.eta_s));
+            sgpid[i] = (uint16_t)pid;
         }
         for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
         for (int i = tid; i < G.ngp; i += blockDim.x) {
@@ -505,15 +509,26 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         const int r = int((uint32_t(q) * G.rc_q) >> 20);
                         const int g = q - r * G.Qos;
                         float* d = dst0 + r * cs + 4 * PF * g;
-                        const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                        if constexpr (PF == 2) {
+                            // E5M10 (the 43-bit set): one SWAR special-code test per group
+                            float x[8];
+                            decode_group_t<2>(v[u], x, fos);
 #pragma unroll
-                        for (int j4 = 0; j4 < 4; ++j4) {
-                            float x[PF];
-                            decode_word_t<PF>(w4[j4], x, fos);
-#pragma unroll
-                            for (int j = 0; j < PF; ++j) {
-                                d[j4 * PF + j] = x[j];
+                            for (int j = 0; j < 8; ++j) {
+                                d[j] = x[j];
                                 amax = fmaxf(amax, fabsf(x[j]));
+                            }
+                        } else {
+                            const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                            for (int j4 = 0; j4 < 4; ++j4) {
+                                float x[PF];
+                                decode_word_t<PF>(w4[j4], x, fos);
+#pragma unroll
+                                for (int j = 0; j < PF; ++j) {
+                                    d[j4 * PF + j] = x[j];
+                                    amax = fmaxf(amax, fabsf(x[j]));
+                                }
                             }
                         }
                     }
@@ -795,8 +810,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 for (int u = 0; u < 4; ++u) {
                                     const int k = k0c + u;
                                     const uint2 rec = sprec[min(k, k1c - 1)];
-                                    const float* ci = crow + (rec.x & 0xffu);
-                                    const float* cj = crow + ((rec.x >> 8) & 0xffu);
+                                    const char* cb8 = reinterpret_cast<const char*>(crow);
+                                    const float* ci = reinterpret_cast<const float*>(cb8 + (rec.x & 0xffffu));
+                                    const float* cj = reinterpret_cast<const float*>(cb8 + (rec.x >> 16));
                                     const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
                                     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                                     const float Rs = __uint_as_float(rec.y);
@@ -804,7 +820,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                     // the rare d2 within an ulp of Rs^2 is settled by self_pair
                                     // in the gather (an inactive marked pair contributes nothing)
                                     if (k >= k1c || d2 >= Rs * Rs) continue;
-                                    const int pid = rec.x >> 16;
+                                    const int pid = sgpid[k];
                                     atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
                                     wmk |= 1u << (pid >> 5);
                                 }

@@ -273,6 +273,33 @@ __device__ __forceinline__ void decode_word_t(uint32_t w, float* out, const Fmt&
     for (int j = 0; j < PF; ++j) out[j] = decode_slot(w, j, f);
 }
 
+// A 16-byte group of 4 words -> 4 PF values.  For E5M10 the exponent-31
+// test (the codes the hardware conversion cannot take, c3) is one SWAR test
+// for all eight halves: (e + 0x0400) carries into bit 15 of a half iff its
+// exponent field e is 0x7C00.
+template <int PF>
+__device__ __forceinline__ void decode_group_t(const uint4& v, float* out, const Fmt& f) {
+    if constexpr (PF == 2) {
+        if (f.kind == KIND_F16) {
+            const uint32_t t = (((v.x & 0x7C007C00u) + 0x04000400u) | ((v.y & 0x7C007C00u) + 0x04000400u) |
+                                ((v.z & 0x7C007C00u) + 0x04000400u) | ((v.w & 0x7C007C00u) + 0x04000400u)) &
+                               0x80008000u;
+            if (t == 0u) {
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    asm("{ .reg .f16 a, b;\n mov.b32 {a, b}, %2;\n cvt.f32.f16 %0, a;\n cvt.f32.f16 %1, b;}"
+                        : "=f"(out[2 * k]), "=f"(out[2 * k + 1]) : "r"(w4[k]));
+                return;
+            }
+        }
+    }
+    decode_word_t<PF>(v.x, out, f);
+    decode_word_t<PF>(v.y, out + PF, f);
+    decode_word_t<PF>(v.z, out + 2 * PF, f);
+    decode_word_t<PF>(v.w, out + 3 * PF, f);
+}
+
 // Run fn(std::integral_constant<int, pf>) for the runtime packing factor
 // (one uniform branch), so the per-word loops above unroll at compile time.
 template <int V>
