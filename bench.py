@@ -202,9 +202,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("VAPR_DIST_BACKEND", "nccl") != "nccl":
+        local = 0                     # functional multi-rank check on one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; VAPR_DIST_BACKEND=gloo is a functional check of the
+        # multi-rank logic on one GPU (never a measurement)
+        backend = os.environ.get("VAPR_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     fm = FORMAT_SETS[args.formats]
     n_prob = args.problems_per_env * 8
@@ -373,8 +381,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32+packed-ExMy", "data": "synthetic",
-            "config": {"workload": "config4: 800 problems (100 per MBM-like env) x 100 TO seeds "
-                                   "x 32 steps per GPU, 52 spheres, swept n=1",
+            "config": {"workload": f"config4: {n_prob} problems ({args.problems_per_env} per "
+                                   f"MBM-like env) x {args.seeds} TO seeds x {args.H} steps per GPU, "
+                                   "52 spheres, swept n=1",
                        "formats": args.formats, "format_bits": bits,
                        "formats_exmy": ["E%dM%d" % f for f in fm],
                        "poses_per_gpu": P, "problems_per_gpu": n_prob,

@@ -30,6 +30,10 @@ def gather_best(best_cost, best_seed, world):
     only collective of the path (rank-major result, [world * n])."""
     if world == 1:
         return best_cost, best_seed
+    if dist.get_backend() != "nccl" and best_cost.is_cuda:
+        # gloo (CPU tests, functional checks): gather through host tensors
+        gc, gs = gather_best(best_cost.cpu(), best_seed.cpu(), world)
+        return gc.to(best_cost.device), gs.to(best_seed.device)
     gc = torch.empty(world * best_cost.numel(), dtype=best_cost.dtype, device=best_cost.device)
     gs = torch.empty(world * best_seed.numel(), dtype=best_seed.dtype, device=best_seed.device)
     dist.all_gather_into_tensor(gc, best_cost.contiguous())
@@ -41,6 +45,7 @@ def max_over_ranks(value, device):
     """Max of a scalar over ranks (the bench's timing rule)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
