@@ -124,7 +124,10 @@ typedef struct {
 
 /* Options (vapr_set_option). */
 enum {
-    VAPR_OPT_CULL = 0      /* 1 (default): exact broadphase culling; 0: brute force */
+    VAPR_OPT_CULL = 0,     /* 1 (default): exact broadphase culling; 0: brute force */
+    VAPR_OPT_STREAMS = 1   /* vapr_cost_grad: trajectory chunks on this many context-owned
+                              streams (1..8, default 1), forked from and joined back to the
+                              caller's stream; results are bit-identical for any value */
 };
 
 /* ---- context and tables ------------------------------------------------ */

@@ -33,6 +33,9 @@ struct vapr_ctx {
     // the host-side slot cursor
     unsigned int* d_sched = nullptr;
     unsigned int sched_next = 0;
+    // VAPR_OPT_STREAMS: concurrent trajectory chunks in vapr_cost_grad
+    int n_streams = 1;
+    cudaStream_t par[8] = {};
     // IKO goals (N2)
     float* d_goals = nullptr;
     int32_t n_goals = 0;
@@ -184,6 +187,8 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     if (c->d_off) cudaFree(c->d_off);
     if (c->d_sched) cudaFree(c->d_sched);
     if (c->d_goals) cudaFree(c->d_goals);
+    for (cudaStream_t st : c->par)
+        if (st) cudaStreamDestroy(st);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -467,6 +472,11 @@ vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
     CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
     if (option == VAPR_OPT_CULL) {
         c->cull = value ? 1 : 0;
+        return VAPR_OK;
+    }
+    if (option == VAPR_OPT_STREAMS) {
+        CHECK(value >= 1 && value <= 8, VAPR_ERR_INVALID_ARG);
+        c->n_streams = value;
         return VAPR_OK;
     }
     return VAPR_ERR_UNSUPPORTED;
@@ -756,8 +766,35 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
     CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
     float* cpose = cost_pose ? cost_pose
                              : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
-    return cuda_status(enqueue_cost_grad(c, q, world_idx, 0, B, B, H, p, workspace, off, cpose,
-                                         cost_traj, grad_q, (cudaStream_t)stream));
+    cudaStream_t s0 = (cudaStream_t)stream;
+    const int ns = std::min(c->n_streams, B);
+    if (ns <= 1)
+        return cuda_status(enqueue_cost_grad(c, q, world_idx, 0, B, B, H, p, workspace, off, cpose,
+                                             cost_traj, grad_q, s0));
+    // VAPR_OPT_STREAMS: trajectory chunks on context-owned streams, forked
+    // from and joined back to the caller's stream (each chunk's kernels see
+    // exactly its rows, so the results do not depend on the split)
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < ns && e == cudaSuccess; ++i)
+        if (!c->par[i]) e = cudaStreamCreateWithFlags(&c->par[i], cudaStreamNonBlocking);
+    while (e == cudaSuccess && c->events.size() < (size_t)(ns + 1)) {
+        cudaEvent_t ev;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) c->events.push_back(ev);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(c->events[0], s0);
+    const int Bc = (B + ns - 1) / ns;
+    for (int i = 0; i < ns && e == cudaSuccess; ++i) {
+        const int b0 = i * Bc, nb = std::min(Bc, B - b0);
+        if (nb <= 0) break;
+        e = cudaStreamWaitEvent(c->par[i], c->events[0], 0);
+        if (e == cudaSuccess)
+            e = enqueue_cost_grad(c, q, world_idx, b0, nb, B, H, p, workspace, off, cpose, cost_traj,
+                                  grad_q, c->par[i]);
+        if (e == cudaSuccess) e = cudaEventRecord(c->events[1 + i], c->par[i]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, c->events[1 + i], 0);
+    }
+    return cuda_status(e);
 }
 
 vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t* world_idx,

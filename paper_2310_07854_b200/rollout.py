@@ -37,6 +37,9 @@ class Context:
     def set_cull(self, on):
         vb.vapr_set_option(self.h, vb.VAPR_OPT_CULL, int(on))
 
+    def set_streams(self, n):
+        vb.vapr_set_option(self.h, vb.VAPR_OPT_STREAMS, int(n))
+
     def close(self):
         if self.h is not None:
             vb.vapr_destroy(self.h)
