@@ -47,6 +47,36 @@ struct Emitter {
     }
 };
 
+// E5M10 (two codes per word, the 43-bit set's out_spheres format): a sphere's
+// three values per call with a phase bit (uniform across the CTA: every pose
+// has the same sphere sequence) and the hardware f16x2 conversion where it is
+// exact (|x| < 65520), the generic word encoder otherwise.
+struct EmitterF16 {
+    float buf = 0.f;
+    bool odd = false;
+    int word = 0;
+    __device__ __forceinline__ static uint32_t enc2(float a, float b, const Fmt& f) {
+        const uint32_t amax = max(__float_as_uint(a) & 0x7fffffffu, __float_as_uint(b) & 0x7fffffffu);
+        if (amax < f.hw_limit) return cvt_f16x2(a, b);
+        const float x[2] = {a, b};
+        return encode_word_t<2>(x, f);
+    }
+    __device__ __forceinline__ void sphere(float x, float y, float z, uint32_t* row, const Fmt& f) {
+        if (!odd) {
+            row[word++] = enc2(x, y, f);
+            buf = z;
+        } else {
+            row[word++] = enc2(buf, x, f);
+            row[word++] = enc2(y, z, f);
+        }
+        odd = !odd;
+    }
+    __device__ __forceinline__ void flush(uint32_t* row, int W, const Fmt& f) {
+        if (odd) row[word++] = enc2(buf, 0.f, f);
+        for (; word < W; ++word) row[word] = 0u;
+    }
+};
+
 template <bool IKO>
 __global__ void __launch_bounds__(kTile)
 fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
@@ -64,9 +94,9 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 
     if (tid < np) {
         uint32_t* row = sw + tid * WS;
-        with_pf(f.pf, [&](auto Pc) {
-            constexpr int PF = decltype(Pc)::value;
-            Emitter<PF> em;
+        // the chain, the IKO terms at the hand, and every sphere centre handed
+        // to `emit(x, y, z)` in sphere order
+        auto walk = [&](auto&& emit) {
             Xf X;
             xf_identity(X);
             for (int l = 0; l < kLinks; ++l) {
@@ -91,13 +121,26 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
                     float cx, cy, cz;
                     xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
-                    em.push(cx, row, f);
-                    em.push(cy, row, f);
-                    em.push(cz, row, f);
+                    emit(cx, cy, cz);
                 }
             }
+        };
+        if (f.kind == KIND_F16) {
+            EmitterF16 em;
+            walk([&](float x, float y, float z) { em.sphere(x, y, z, row, f); });
             em.flush(row, W, f);
-        });
+        } else {
+            with_pf(f.pf, [&](auto Pc) {
+                constexpr int PF = decltype(Pc)::value;
+                Emitter<PF> em;
+                walk([&](float x, float y, float z) {
+                    em.push(x, row, f);
+                    em.push(y, row, f);
+                    em.push(z, row, f);
+                });
+                em.flush(row, W, f);
+            });
+        }
     }
     __syncthreads();
 
