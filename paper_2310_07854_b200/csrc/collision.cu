@@ -223,7 +223,7 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, gpab, lpab, lpgp, spm, slink, tables;
+    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, slink, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
     unsigned rows, pmask, pwm, wm, pk0, qi, qc, warp;
 };
@@ -267,11 +267,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.gpid = take(2u * g.npairs, 2);
     g.grec = take(8u * kMaxGroupPairs, 8);
     g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
-    g.gpab = take(2u * kMaxGroupPairs, 2);
-    g.lpab = take(2u * 33, 2);
-    g.lpgp = take(2u * 33, 2);
     g.slink = take(kMaxSpheres, 1);
-    g.spm = take(do_self ? 4u * g.S * g.pmw : 0u, 4);
     g.tables = take(0, 16);
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
@@ -368,11 +364,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint2* sgrec = reinterpret_cast<uint2*>(base + G.grec);        // group-pair ball tests
     uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + G.gpid);  // pair id of each record
     uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
-    uint16_t* sgpab = reinterpret_cast<uint16_t*>(base + G.gpab);   // a | b << 8
-    uint16_t* slpab = reinterpret_cast<uint16_t*>(base + G.lpab);   // a | b << 8
-    uint16_t* slpgp = reinterpret_cast<uint16_t*>(base + G.lpgp);
     uint8_t* slink = reinterpret_cast<uint8_t*>(base + G.slink);
-    uint32_t* spm = reinterpret_cast<uint32_t*>(base + G.spm);     // pair-id mask of each sphere
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
@@ -406,24 +398,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         }
         for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
         for (int i = tid; i < G.ngp; i += blockDim.x) {
-            sgpab[i] = (uint16_t)(R.gp_a[i] | (R.gp_b[i] << 8));
             // byte offsets 12 ref_a | 12 ref_b << 16 in a row, and the static
             // part of the cull distance
             const int ga = R.gp_a[i], gb = R.gp_b[i];
             sgrec[i] = make_uint2((uint32_t)(12 * R.grp_ref[ga]) | ((uint32_t)(12 * R.grp_ref[gb]) << 16),
                                   __float_as_uint(R.grp_rl[ga] + R.grp_rl[gb] + a.eta_s + kSlack));
         }
-        for (int i = tid; i <= R.n_link_pairs; i += blockDim.x) slpgp[i] = R.lp_gp_off[i];
-        for (int i = tid; i < R.n_link_pairs; i += blockDim.x)
-            slpab[i] = (uint16_t)(R.lp_a[i] | (R.lp_b[i] << 8));
-        for (int i = tid; i < G.S * PMW; i += blockDim.x) spm[i] = 0u;
     }
-    __syncthreads();
-    if (a.do_self)
-        for (int pid = tid; pid < G.npairs; pid += blockDim.x) {
-            atomicOr(spm + R.pair_i[pid] * PMW + (pid >> 5), 1u << (pid & 31));
-            atomicOr(spm + R.pair_j[pid] * PMW + (pid >> 5), 1u << (pid & 31));
-        }
     __syncthreads();
 
     // ---- the warp's workspace
@@ -853,13 +834,14 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const int p = it >> 6, s = it & 63;
                 const float* crow = rows + (p + 1) * cs;
                 const uint32_t* pm = pmask + p * PMW;
-                const uint32_t* sm_ = spm + s * PMW;
                 float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
+                // the pose's active pairs in id order, those with sphere s
                 for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
                     const int wd = __ffs(wmk) - 1;
-                    for (uint32_t m = pm[wd] & sm_[wd]; m; m &= m - 1) {
+                    for (uint32_t m = pm[wd]; m; m &= m - 1) {
                         const int pid = (wd << 5) + __ffs(m) - 1;
                         const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
+                        if (i != s && j != s) continue;
                         float vx, vy, vz, c;
                         // always active here (same test as the narrowphase that marked it)
                         if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy,
