@@ -291,12 +291,15 @@ vapr_status vapr_lbfgs_candidates(const float *x, const float *d, int32_t B, int
  * history).  chosen is nullable.  Errors: VAPR_ERR_SHAPE for B < 0, D < 1,
  * D > VAPR_LBFGS_MAX_D, N outside [1, 32], m outside [1, VAPR_LBFGS_MAX_M];
  * VAPR_ERR_INVALID_ARG for null buffers or non-positive / non-increasing
- * scales. */
+ * scales.  fixed (nullable, device, [D] bytes, shared by all items): a
+ * non-zero entry freezes that coordinate -- its gradient (as stored and as
+ * used) and direction are 0, so the optimisation runs over the free
+ * coordinates only (N4: trajectory endpoints held at start and goal). */
 vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float *scales, int32_t N,
                             const float *cand_cost, const float *cand_grad, float *x, float *g,
                             float *cost, float *d, float *hist_s, float *hist_y, float *hist_rho,
                             int32_t *hist_count, int32_t *hist_head, int32_t *chosen, int32_t m,
-                            float curvature_eps, void *stream);
+                            float curvature_eps, const uint8_t *fixed, void *stream);
 
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =

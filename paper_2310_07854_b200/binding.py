@@ -102,7 +102,7 @@ def _load():
                                  P, P, P, I32, P], I32),
         "vapr_lbfgs_candidates": ([P, P, I32, I32, P, I32, P, P], I32),
         "vapr_lbfgs_step": ([I32, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32,
-                             ctypes.c_float, P], I32),
+                             ctypes.c_float, P, P], I32),
         "vapr_best_per_problem": ([P, I32, I32, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
@@ -336,10 +336,12 @@ def vapr_lbfgs_candidates(x, d, B, D, scales, cand, stream=None):
 
 
 def vapr_lbfgs_step(B, D, scales, cand_cost, cand_grad, x, g, cost, d, hist_s, hist_y, hist_rho,
-                    hist_count, hist_head, chosen=None, m=10, curvature_eps=1e-10, stream=None):
+                    hist_count, hist_head, chosen=None, m=10, curvature_eps=1e-10, fixed=None,
+                    stream=None):
     """Line-search selection, history update and two-loop direction (N1 steps (6), (7))."""
     arr, n = _scales(scales)
     _check(lib.vapr_lbfgs_step(B, D, arr, n, _ptr(cand_cost), _ptr(cand_grad), _ptr(x), _ptr(g),
                                _ptr(cost), _ptr(d), _ptr(hist_s), _ptr(hist_y), _ptr(hist_rho),
                                _ptr(hist_count), _ptr(hist_head), _ptr(chosen), int(m),
-                               float(curvature_eps), _stream(stream)), "vapr_lbfgs_step")
+                               float(curvature_eps), _ptr(fixed), _stream(stream)),
+           "vapr_lbfgs_step")

@@ -912,7 +912,7 @@ vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float* scales, int32_t N
                             const float* cand_cost, const float* cand_grad, float* x, float* g,
                             float* cost, float* d, float* hist_s, float* hist_y, float* hist_rho,
                             int32_t* hist_count, int32_t* hist_head, int32_t* chosen, int32_t m,
-                            float curvature_eps, void* stream) {
+                            float curvature_eps, const uint8_t* fixed, void* stream) {
     CHECK(B >= 0 && D >= 1 && D <= VAPR_LBFGS_MAX_D && N >= 1 && N <= 32 && m >= 1 &&
               m <= VAPR_LBFGS_MAX_M,
           VAPR_ERR_SHAPE);
@@ -925,7 +925,7 @@ vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float* scales, int32_t N
     CHECK(pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
     return cuda_status(launch_lbfgs_step(B, D, N, sc, cand_cost, cand_grad, x, g, cost, d, hist_s,
                                          hist_y, hist_rho, hist_count, hist_head, chosen, m,
-                                         curvature_eps, (cudaStream_t)stream));
+                                         curvature_eps, fixed, (cudaStream_t)stream));
 }
 
 // ---- e -------------------------------------------------------------------

@@ -72,7 +72,8 @@ cudaError_t launch_lbfgs_candidates(const float* x, const float* d, long long B,
 cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const float* cand_cost,
                               const float* cand_grad, float* x, float* g, float* cost, float* d,
                               float* hs, float* hy, float* hrho, int32_t* hcount, int32_t* hhead,
-                              int32_t* chosen, int m, float eps, cudaStream_t s);
+                              int32_t* chosen, int m, float eps, const uint8_t* fixed,
+                              cudaStream_t s);
 cudaError_t launch_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,
                                     float* best_cost, int32_t* best_seed, cudaStream_t s);
 

@@ -81,7 +81,8 @@ lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
                   float* __restrict__ g, float* __restrict__ cost, float* __restrict__ d,
                   float* __restrict__ hs, float* __restrict__ hy, float* __restrict__ hrho,
                   int32_t* __restrict__ hcount, int32_t* __restrict__ hhead,
-                  int32_t* __restrict__ chosen, int m, float eps) {
+                  int32_t* __restrict__ chosen, int m, float eps,
+                  const uint8_t* __restrict__ fixed) {
     constexpr int G = 32 / LPI;                    // items per warp
     constexpr int KPL = (LPI == 32) ? kMaxPerLane : 1;   // LPI < 32 only when D <= LPI
     __shared__ float s_alpha[kStepWarps][G][32];
@@ -131,13 +132,13 @@ lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
         // c32: no improvement -> clear a non-empty history (next d = -g), or
         // shrink an already steepest-descent direction tenfold
         if (count > 0) {
-            each([&](int, int i) { d[o + i] = -g[o + i]; });
+            each([&](int, int i) { d[o + i] = (fixed && fixed[i]) ? 0.f : -g[o + i]; });
             if (sl == 0) {
                 hcount[b] = 0;
                 hhead[b] = 0;
             }
         } else {
-            each([&](int, int i) { d[o + i] = 0.1f * d[o + i]; });
+            each([&](int, int i) { d[o + i] = (fixed && fixed[i]) ? 0.f : 0.1f * d[o + i]; });
         }
     }
 
@@ -151,9 +152,10 @@ lbfgs_step_kernel(int B, int D, int N, const __grid_constant__ LbfgsScales sc,
         each([&](int k, int i) {
             const float xo = x[o + i];
             const float xn = __fadd_rn(xo, __fmul_rn(s, d[o + i]));
-            const float gnew = gn[i];
+            const bool fz = fixed && fixed[i];
+            const float gnew = fz ? 0.f : gn[i];
             sv[k] = xn - xo;
-            yv[k] = gnew - g[o + i];
+            yv[k] = gnew - (fz ? 0.f : g[o + i]);
             sy = fmaf(sv[k], yv[k], sy);
             x[o + i] = xn;
             g[o + i] = gnew;
@@ -259,7 +261,8 @@ cudaError_t launch_lbfgs_candidates(const float* x, const float* d, long long B,
 cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const float* cand_cost,
                               const float* cand_grad, float* x, float* g, float* cost, float* d,
                               float* hs, float* hy, float* hrho, int32_t* hcount, int32_t* hhead,
-                              int32_t* chosen, int m, float eps, cudaStream_t s) {
+                              int32_t* chosen, int m, float eps, const uint8_t* fixed,
+                              cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
     // lanes per item: the smallest power of two >= D, at most 32
     const int lpi = D <= 4 ? 4 : D <= 8 ? 8 : D <= 16 ? 16 : 32;
@@ -268,7 +271,7 @@ cudaError_t launch_lbfgs_step(int B, int D, int N, const LbfgsScales& sc, const 
 #define VAPR_LBFGS_LAUNCH(L)                                                                      \
     lbfgs_step_kernel<L><<<grid, 32 * kStepWarps, 0, s>>>(B, D, N, sc, cand_cost, cand_grad, x, \
                                                           g, cost, d, hs, hy, hrho, hcount,       \
-                                                          hhead, chosen, m, eps)
+                                                          hhead, chosen, m, eps, fixed)
     switch (lpi) {
         case 4: VAPR_LBFGS_LAUNCH(4); break;
         case 8: VAPR_LBFGS_LAUNCH(8); break;

@@ -26,7 +26,7 @@ class TrajOpt:
     values), cost = the rollout cost (world swept + self collision)."""
 
     def __init__(self, workload, scales=DEFAULT_SCALES, m=10, curvature_eps=1e-10, device=0,
-                 formats=None):
+                 formats=None, fixed=None):
         self.wl = workload
         self.scales = tuple(float(s) for s in scales)
         self.N = len(self.scales)
@@ -48,6 +48,13 @@ class TrajOpt:
         self.hist_count = torch.zeros(B, dtype=torch.int32, device=dev)
         self.hist_head = torch.zeros(B, dtype=torch.int32, device=dev)
         self.chosen = torch.zeros(B, dtype=torch.int32, device=dev)
+        # frozen coordinates (D-vector of bools shared by all items), e.g.
+        # the first and last waypoint of every trajectory (N4)
+        self.fixed = None
+        if fixed is not None:
+            fx = np.asarray(fixed, np.uint8).reshape(-1)
+            assert fx.size == D
+            self.fixed = torch.from_numpy(fx).to(dev)
 
     @property
     def x(self):
@@ -73,6 +80,8 @@ class TrajOpt:
         else:
             self.base.q.copy_(torch.from_numpy(np.ascontiguousarray(self.wl.q)))
         self.base.run()
+        if self.fixed is not None:           # gradient over the free coordinates only
+            self.g.view(self.B, self.D).mul_((self.fixed == 0).to(self.g.dtype)[None, :])
         self.d.copy_(self.g).neg_()
         self.hist_count.zero_()
         self.hist_head.zero_()
@@ -86,7 +95,8 @@ class TrajOpt:
         vb.vapr_lbfgs_step(self.B, self.D, self.scales, self.lines.cost_traj,
                            self.lines.grad_q.view(-1), self.x, self.g, self.cost, self.d,
                            self.hist_s, self.hist_y, self.hist_rho, self.hist_count,
-                           self.hist_head, self.chosen, self.m, self.eps, stream=stream)
+                           self.hist_head, self.chosen, self.m, self.eps, fixed=self.fixed,
+                           stream=stream)
 
     def run(self, iters):
         """reset() then `iters` iterations; returns the per-iteration mean cost."""

@@ -415,26 +415,43 @@ def main():
     ap.add_argument("--target", type=float, default=0.99)
     ap.add_argument("--problems-per-env", type=int, default=10)
     ap.add_argument("--seeds", type=int, default=20)
+    ap.add_argument("--evaluator", default="proxy", choices=["proxy", "pipeline"],
+                    help="proxy: gradient/cost fidelity vs E8M23 (config 5); pipeline: the N4 "
+                         "IKO -> TO success rate, target = the all-E8M23 rate per environment")
     ap.add_argument("--out", default="trials.jsonl")
     a = ap.parse_args()
-    from workloads import config5
-    wl = config5(problems_per_env=a.problems_per_env, seeds=a.seeds)
     t0 = time.perf_counter()
-    ev = GpuProxyEvaluator(wl, a.seeds)
-    targets = {e: a.target for e in sorted(set(wl.envs))}
+    extra = {}
+    if a.evaluator == "pipeline":
+        from .pipeline import PipelineEvaluator
+        ev = PipelineEvaluator(problems_per_env=a.problems_per_env)
+        base = ev.evaluate((FP32,) * 5)
+        targets = dict(base)              # no lower success than FP32
+        envs = sorted(base)
+        poses = ev.ik_wl.poses + ev.to_wl.poses
+        extra = {"evaluator": "pipeline", "fp32_rates": base}
+    else:
+        from workloads import config5
+        wl = config5(problems_per_env=a.problems_per_env, seeds=a.seeds)
+        ev = GpuProxyEvaluator(wl, a.seeds)
+        envs = sorted(set(wl.envs))
+        targets = {e: a.target for e in envs}
+        poses = wl.poses
+        extra = {"evaluator": "proxy"}
     with open(a.out, "w") as log:
         memo = Memo(ev, targets, log)
         res = vapr_search(memo, budget=a.budget, pop_size=a.pop, seed=a.seed)
     dt = time.perf_counter() - t0
     best = res["best"]
-    print(json.dumps({"phase1_minima": res["minima"],
+    print(json.dumps({**extra, "phase1_minima": res["minima"],
                       "phase1_witness": [fmt_str(r.witness) for r in res["phase1"]],
                       "phase1_monotone": [r.monotone for r in res["phase1"]],
                       "reduced_space": res["space_size"], "reduction": round(res["reduction"], 3),
                       "evaluations": res["evaluations"], "seconds": round(dt, 2),
                       "evals_per_s": round(res["evaluations"] / dt, 2),
                       "best": [fmt_str(f) for f in best.config], "best_bits": best.total_bits,
-                      "best_feasible": best.feasible, "poses_per_eval": wl.poses}))
+                      "best_feasible": best.feasible, "best_rates": best.rates,
+                      "poses_per_eval": poses}))
 
 
 if __name__ == "__main__":
