@@ -42,6 +42,10 @@ struct vapr_ctx {
     bool goals_set = false;
 };
 
+#ifndef VAPR_END_CHUNK_WEIGHT      // vapr_cost_grad_host: first / last chunk size relative to the others
+#define VAPR_END_CHUNK_WEIGHT 0.25
+#endif
+
 namespace {
 
 // Make the context's device current for the duration of a call.
@@ -838,10 +842,11 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     // are short
     std::vector<int> cb(nc + 1, 0);
     {
-        const double wsum = (nc >= 3) ? (nc - 2) + 0.5 : nc;
+        const double ew = VAPR_END_CHUNK_WEIGHT;
+        const double wsum = (nc >= 3) ? (nc - 2) + 2.0 * ew : nc;
         double acc = 0.0;
         for (int i = 0; i < nc; ++i) {
-            acc += (nc >= 3 && (i == 0 || i == nc - 1)) ? 0.25 : 1.0;
+            acc += (nc >= 3 && (i == 0 || i == nc - 1)) ? ew : 1.0;
             cb[i + 1] = (int)std::llround(B * acc / wsum);
         }
         cb[nc] = B;
