@@ -68,6 +68,14 @@ typedef enum {
  * DESIGN.md §3).  Valid: E in [2,8], M in [1,23], 1+E+M <= 32. */
 typedef struct { int32_t exp_bits, man_bits; } vapr_format;
 
+/* IEEE special-value mode: OR'd into man_bits of E5M10
+ * or E8M7 only.  Encoding is the hardware round-to-nearest conversion
+ * unconditionally (overflow -> +-inf, NaN -> NaN: PAPER.md:259's
+ * __floats2half2_rn path) and the top exponent decodes to inf / NaN, instead
+ * of the all-finite reading (c3-c7).  Identical to the reading for every
+ * finite |x| below the format's overflow threshold. */
+#define VAPR_FMT_IEEE 0x100
+
 /* Tensor slots, in Table II column order (names from P:189). */
 enum {
     VAPR_OUT_SPHERES = 0,       /* FK output: sphere centres            */

@@ -194,3 +194,32 @@ def quantize_packed(x, E, M):
 def dequantize_packed(words, E, M, cols):
     """packed words -> [rows, cols] FP32 (oracle of vapr_dequantize)."""
     return dequantize(unpack(words, E, M, cols), E, M)
+
+
+# ----------------------------------------------------------------- IEEE mode
+# VAPR_FMT_IEEE (N4; PAPER.md:259 "__floats2half2_rn"): E5M10 / E8M7 with the
+# IEEE special values -- round to nearest even, overflow to +-inf, NaN kept.
+# The definitions are the library conversions themselves: numpy float16 for
+# E5M10 and torch bfloat16 (CPU) for E8M7.
+FMT_IEEE = 0x100
+
+
+def quantize_ieee(x, E, M):
+    """float32 array -> IEEE binary16 / bfloat16 codes (uint32)."""
+    x = np.asarray(x, np.float32)
+    if (E, M) == (5, 10):
+        return x.astype(np.float16).view(np.uint16).astype(np.uint32)
+    if (E, M) == (8, 7):
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)
+        return t.view(torch.int16).numpy().view(np.uint16).astype(np.uint32)
+    raise ValueError("IEEE mode is defined for E5M10 and E8M7 only")
+
+
+def dequantize_ieee(codes, E, M):
+    c = np.asarray(codes, np.uint32).astype(np.uint16)
+    if (E, M) == (5, 10):
+        return c.view(np.float16).astype(np.float32)
+    if (E, M) == (8, 7):
+        return (c.astype(np.uint32) << 16).view(np.float32)
+    raise ValueError("IEEE mode is defined for E5M10 and E8M7 only")

@@ -65,13 +65,17 @@ struct DeviceGuard {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool fmt_valid(vapr_format f) {
-    return f.exp_bits >= 2 && f.exp_bits <= 8 && f.man_bits >= 1 && f.man_bits <= 23 &&
-           1 + f.exp_bits + f.man_bits <= 32;
+    const int m = f.man_bits & ~VAPR_FMT_IEEE;
+    if (f.man_bits & VAPR_FMT_IEEE)             // IEEE mode: E5M10 and E8M7 only
+        return (f.exp_bits == 5 && m == 10) || (f.exp_bits == 8 && m == 7);
+    return f.exp_bits >= 2 && f.exp_bits <= 8 && m >= 1 && m <= 23 && 1 + f.exp_bits + m <= 32;
 }
 
 // Host-side derivation of the device codec constants (common.cuh, Fmt).
 Fmt make_fmt(vapr_format v) {
     Fmt f{};
+    const bool ieee = (v.man_bits & VAPR_FMT_IEEE) != 0;
+    v.man_bits &= ~VAPR_FMT_IEEE;
     f.E = v.exp_bits;
     f.M = v.man_bits;
     f.t = 1 + f.E + f.M;
@@ -102,6 +106,13 @@ Fmt make_fmt(vapr_format v) {
     else if (f.E == 2 && f.M == 1) { f.kind = KIND_E2M1; f.hw_limit = 0x7F800001u; }   // all but NaN
     else if (f.E == 2 && f.M == 3) { f.kind = KIND_E2M3; f.hw_limit = 0x7F800001u; }
     else if (f.E == 3 && f.M == 2) { f.kind = KIND_E3M2; f.hw_limit = 0x7F800001u; }
+    f.nancode = f.maxcode;
+    if (ieee) {                     // reading c41 (common.cuh, KIND_F16_IEEE)
+        f.kind = (f.E == 5) ? KIND_F16_IEEE : KIND_GENERIC;
+        f.hw_limit = 0u;
+        f.maxcode = (f.E == 5) ? 0x7C00u : 0x7F80u;   // the encode clamp: overflow -> inf
+        f.nancode = 0x7FFFu;                          // the hardware conversions' canonical NaN
+    }
     return f;
 }
 
@@ -239,7 +250,7 @@ vapr_status vapr_format_parse(const char* s, vapr_format* out) {
 
 size_t vapr_packed_row_words(vapr_format f, size_t cols) {
     if (!fmt_valid(f)) return 0;
-    const size_t pf = 32 / (1 + f.exp_bits + f.man_bits);
+    const size_t pf = 32 / (1 + f.exp_bits + (f.man_bits & ~VAPR_FMT_IEEE));
     const size_t w = (cols + pf - 1) / pf;
     return (w + 3) & ~(size_t)3;
 }

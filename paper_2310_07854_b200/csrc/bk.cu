@@ -26,7 +26,10 @@ namespace {
 #endif
 constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
 
-template <bool IKO>
+// IKO: the N2 pose / bound terms; SP: the gradient slot is IEEE E5M10 (its
+// exponent-31 codes decode to inf / NaN, reading c41) -- a separate
+// instantiation so the common ones carry no fixup.
+template <bool IKO, bool SP>
 __global__ void __launch_bounds__(kTile)
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
@@ -154,7 +157,8 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 for (int c = 0; c < 3; ++c) {
                     const int e = 3 * s + c;
                     const int wi = int((e * rc) >> 16);
-                    g[c] = decode(code_at(row[wi], e - wi * f.pf, f), f);
+                    const uint32_t code = code_at(row[wi], e - wi * f.pf, f);
+                    g[c] = SP ? decode_sp(code, f) : decode(code, f);
                 }
                 float cx, cy, cz;
                 const float4 o4 = so[s];
@@ -215,7 +219,9 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     const uint32_t rt = 65536u / fgos.t + 1u;
     const long long grid = (P + kTile - 1) / kTile;
     const bool iko = ik && ik_on(*ik);
-    auto kern = iko ? bk_kernel<true> : bk_kernel<false>;
+    const bool sp = fgos.kind == KIND_F16_IEEE;
+    auto kern = iko ? (sp ? bk_kernel<true, true> : bk_kernel<true, false>)
+                    : (sp ? bk_kernel<false, true> : bk_kernel<false, false>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     IkArgs none{};

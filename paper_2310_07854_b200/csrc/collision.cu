@@ -434,6 +434,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     const int nsub = swept ? a.sweep_steps : 0;
     const float inv_n1 = 1.f / float(nsub + 1);
     const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
+    // the clamp code's value: coordinates at or beyond it may be saturated
+    // (all-finite) or inf (IEEE mode: 65536 for E5M10, inf for E8M7)
     const float fmax_os = decode(fos.maxcode, fos);
 
     for (;;) {

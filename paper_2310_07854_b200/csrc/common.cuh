@@ -32,7 +32,14 @@ enum FmtKind : int32_t {
     KIND_E5M2 = 5,      // cvt.rn.satfinite.e5m2x2.f32, |x| >= 61440 / NaN -> generic
     KIND_E2M1 = 6,      // cvt.rn.satfinite.e2m1x2.f32, NaN -> generic
     KIND_E2M3 = 7,      // cvt.rn.satfinite.e2m3x2.f32, NaN -> generic
-    KIND_E3M2 = 8       // cvt.rn.satfinite.e3m2x2.f32, NaN -> generic
+    KIND_E3M2 = 8,      // cvt.rn.satfinite.e3m2x2.f32, NaN -> generic
+    // IEEE special-value mode (VAPR_FMT_IEEE; reading c41).  Encoding is the
+    // generic path for both IEEE formats -- exact IEEE RNE once maxcode is the
+    // inf code (overflow clamps to +-inf) and nancode the conversions'
+    // canonical NaN 0x7FFF.  IEEE E8M7 is KIND_GENERIC (exponent 255 decodes
+    // to inf / NaN by itself); IEEE E5M10 gets this kind, tested only on the
+    // decode slow paths, so the all-finite fast paths are unchanged.
+    KIND_F16_IEEE = 9
 };
 
 struct Fmt {
@@ -42,12 +49,14 @@ struct Fmt {
     uint32_t K;            // rnd - (off << sh) (mod 2^32): fused RNE + re-bias constant
     uint32_t minnorm;      // FP32 bits of 2^(1-bias): smallest normal of the format
     uint32_t magic_bits;   // FP32 bits of 2^(24-bias-M): its ulp is the subnormal quantum
-    uint32_t maxcode;      // largest finite magnitude code (exp field 254 for E=8, c7)
+    uint32_t maxcode;      // encode clamp: largest finite magnitude code (exp field 254
+                           // for E=8, c7); IEEE mode: the inf code
     uint32_t mask;         // (1 << t) - 1
     uint32_t signbit;      // 1 << (t-1)
     uint32_t keep;         // decode: sign | exponent+mantissa field mask in FP32 position
     uint32_t hw_limit;     // hardware fast path valid while |x| bits < hw_limit
     float dscale;          // 2^(127 - bias): decode re-bias
+    uint32_t nancode;      // encode of NaN: maxcode (c8) / 0x7FFF (IEEE)
 };
 
 // FP32 -> code, round to nearest even (single rounding), saturating, NaN ->
@@ -63,7 +72,7 @@ __device__ __forceinline__ uint32_t encode_generic(float x, const Fmt& f) {
         __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits))) - f.magic_bits;
     uint32_t c = (a < f.minnorm) ? cs : cn;
     c = min(c, f.maxcode) | ((u >> (32 - f.t)) & f.signbit);
-    return (a > 0x7f800000u) ? f.maxcode : c;
+    return (a > 0x7f800000u) ? f.nancode : c;
 }
 
 __device__ __forceinline__ uint32_t encode(float x, const Fmt& f) {
@@ -76,12 +85,24 @@ __device__ __forceinline__ uint32_t encode(float x, const Fmt& f) {
 // the power of two 2^(127-bias) re-biases normals and subnormals alike.
 __device__ __forceinline__ float decode_slot(uint32_t w, int j, const Fmt& f) {
     if (f.kind == KIND_IDENTITY) return __uint_as_float(w);
+    // (E8M7 exponent 255 lands in the FP32 exponent field as inf / NaN: codes
+    // the all-finite reading never produces, IEEE mode's specials; IEEE E5M10
+    // exponent-31 codes are fixed up by decode() / taken by the hardware path)
     const uint32_t u = w << (32 - f.t - j * f.t);
     const uint32_t x = uint32_t(int32_t(u) >> (8 - f.E)) & f.keep;
     return (f.E == 8) ? __uint_as_float(x) : __fmul_rn(__uint_as_float(x), f.dscale);
 }
 
 __device__ __forceinline__ float decode(uint32_t c, const Fmt& f) { return decode_slot(c, 0, f); }
+
+// decode() for a format that may be IEEE E5M10 (KIND_F16_IEEE): exponent 31 ->
+// FP32 inf / NaN, sign and payload kept.  Kept apart so decode() carries no
+// fixup in the kernels' common instantiations.
+__device__ __forceinline__ float decode_sp(uint32_t c, const Fmt& f) {
+    const float v = decode_slot(c, 0, f);
+    const uint32_t sp = ((c & 0x8000u) << 16) | 0x7F800000u | ((c & 0x3FFu) << 13);
+    return (f.kind == KIND_F16_IEEE && (c & 0x7C00u) == 0x7C00u) ? __uint_as_float(sp) : v;
+}
 
 __device__ __forceinline__ uint32_t code_at(uint32_t word, int slot, const Fmt& f) {
     return (f.t == 32) ? word : ((word >> (slot * f.t)) & f.mask);
@@ -259,8 +280,10 @@ __device__ __forceinline__ void decode_word_t(uint32_t w, float* out, const Fmt&
     }
     if constexpr (PF == 2) {
         // E5M10: the hardware f16 -> f32 conversion is exact except for the
-        // exponent-31 codes, which are finite in this reading (c3)
-        if (f.kind == KIND_F16 && (w & 0x7C00u) != 0x7C00u && (w & 0x7C000000u) != 0x7C000000u) {
+        // exponent-31 codes, which are finite in this reading (c3; IEEE mode:
+        // they are inf / NaN, and the hardware decode takes every code)
+        if ((f.kind == KIND_F16 && (w & 0x7C00u) != 0x7C00u && (w & 0x7C000000u) != 0x7C000000u) ||
+            f.kind == KIND_F16_IEEE) {
             float lo, hi;
             asm("{ .reg .f16 a, b;\n mov.b32 {a, b}, %2;\n cvt.f32.f16 %0, a;\n cvt.f32.f16 %1, b;}"
                 : "=f"(lo), "=f"(hi) : "r"(w));
