@@ -133,9 +133,15 @@ typedef struct {
 /* Options (vapr_set_option). */
 enum {
     VAPR_OPT_CULL = 0,     /* 1 (default): exact broadphase culling; 0: brute force */
-    VAPR_OPT_STREAMS = 1   /* vapr_cost_grad: trajectory chunks on this many context-owned
+    VAPR_OPT_STREAMS = 1,  /* vapr_cost_grad: trajectory chunks on this many context-owned
                               streams (1..8, default 1), forked from and joined back to the
                               caller's stream; results are bit-identical for any value */
+    VAPR_OPT_SPARSE = 2    /* N3: 1 = vapr_cost_grad stores grad_out_spheres in the sparse
+                              form (aggregation writes it, BK reads it; the workspace holds
+                              the sparse region instead of the dense slot, see
+                              vapr_cost_grad_sparse_layout); 0 (default) = dense.  cost and
+                              grad_q are bit-identical either way.  Changes the workspace
+                              size: query vapr_cost_grad_workspace_bytes after setting it. */
 };
 
 /* ---- context and tables ------------------------------------------------ */
@@ -308,6 +314,48 @@ vapr_status vapr_lbfgs_step(int32_t B, int32_t D, const float *scales, int32_t N
                             float *cost, float *d, float *hist_s, float *hist_y, float *hist_rho,
                             int32_t *hist_count, int32_t *hist_head, int32_t *chosen, int32_t m,
                             float curvature_eps, const uint8_t *fixed, void *stream);
+
+/* ---- N3: sparsity-aware storage of a sphere tensor ----- */
+/* "grad_out_spheres, out_vec, closest_pt, and closest_pt_swept
+ * have more than 99% of sparsity".  Reading c42 (definition in
+ * oracle/sparse.py).  A packed sphere tensor of `rows` rows of cols = 3S codes
+ * (S <= 64 spheres, codes c = x, y, z of sphere s at 3s + c) in sparse form:
+ *   mask[rows]  uint64: bit s set iff one of sphere s's three codes is
+ *               non-zero as a t-bit integer (a -0 code counts);
+ *   off[rows]   uint32: the row's first word in pool (0 for an empty row);
+ *   pool        uint32: a row's codes are those of its set spheres in
+ *               ascending order, code index i = 3k + c for the k-th set
+ *               sphere, in word off + i / pf at bits (i % pf) t (LSB-first,
+ *               pf = floor(32 / t), as in dense rows); n = ceil(3 popc(mask)
+ *               / pf) words, unused high slots 0;
+ *   used        uint32 (device): pool words in use, = the sum of n.
+ * Rows occupy disjoint word ranges inside the pool capacity; their placement
+ * is the writer's (this library: each tile of 16 consecutive rows packs its
+ * rows back to back from word 16 wmax tile, wmax = ceil(cols / pf), so the
+ * layout is deterministic); everything else is determined.  Row offsets are
+ * 32-bit: the capacity must stay below 2^32 words (VAPR_ERR_SHAPE).  Stored
+ * data: 12 bytes per row + 4 used bytes. */
+
+/* Pool capacity that always suffices: rows * ceil(cols / pf) words. */
+size_t vapr_sparse_pool_words(vapr_format f, size_t cols, size_t rows);
+/* Dense packed [rows, row_words] -> sparse form.  mask, off, pool, used:
+ * device, caller-owned, 8 / 4 / 4 / 4-byte aligned; pool_words >=
+ * vapr_sparse_pool_words (else VAPR_ERR_SHAPE); *used is reset by the call
+ * (stream-ordered).  cols % 3 == 0 and cols / 3 <= 64, else VAPR_ERR_SHAPE. */
+vapr_status vapr_sparsify(vapr_format f, const uint32_t *packed, size_t rows, size_t cols,
+                          uint64_t *mask, uint32_t *off, uint32_t *pool, size_t pool_words,
+                          uint32_t *used, void *stream);
+/* Sparse form -> dense packed [rows, row_words] (padding words 0). */
+vapr_status vapr_densify(vapr_format f, const uint64_t *mask, const uint32_t *off,
+                         const uint32_t *pool, size_t rows, size_t cols, uint32_t *packed,
+                         void *stream);
+/* With VAPR_OPT_SPARSE = 1: byte offsets inside vapr_cost_grad's workspace
+ * of grad_out_spheres' mask [B*H], off [B*H], used [1] and pool
+ * [pool_words], in that order; *pool_words = the pool capacity.  The dense
+ * slot's entry of vapr_cost_grad_workspace_layout is SIZE_MAX in this mode.
+ * VAPR_ERR_INVALID_ARG when the option is off. */
+vapr_status vapr_cost_grad_sparse_layout(const vapr_ctx *ctx, int32_t B, int32_t H,
+                                         size_t offsets[4], size_t *pool_words);
 
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =

@@ -22,6 +22,7 @@ VAPR_OUT_SPHERES, VAPR_GRAD_OUT_SPHERES, VAPR_OUT_VEC, VAPR_CLOSEST_PT, VAPR_CLO
 VAPR_NUM_SLOTS = 5
 VAPR_OPT_CULL = 0
 VAPR_OPT_STREAMS = 1
+VAPR_OPT_SPARSE = 2
 STATUS = {0: "VAPR_OK", 1: "VAPR_ERR_INVALID_FORMAT", 2: "VAPR_ERR_INVALID_ARG",
           3: "VAPR_ERR_SHAPE", 4: "VAPR_ERR_CUDA", 5: "VAPR_ERR_NOT_INITIALIZED",
           6: "VAPR_ERR_UNSUPPORTED"}
@@ -36,7 +37,9 @@ EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
            "vapr_self_collision", "vapr_collision", "vapr_aggregate",
            "vapr_backward_kinematics", "vapr_cost_grad_workspace_bytes",
            "vapr_cost_grad_workspace_layout", "vapr_cost_grad", "vapr_cost_grad_host",
-           "vapr_lbfgs_candidates", "vapr_lbfgs_step", "vapr_best_per_problem")
+           "vapr_lbfgs_candidates", "vapr_lbfgs_step", "vapr_best_per_problem",
+           "vapr_sparse_pool_words", "vapr_sparsify", "vapr_densify",
+           "vapr_cost_grad_sparse_layout")
 
 
 class VaprError(RuntimeError):
@@ -104,6 +107,11 @@ def _load():
         "vapr_lbfgs_step": ([I32, I32, P, I32, P, P, P, P, P, P, P, P, P, P, P, P, I32,
                              ctypes.c_float, P, P], I32),
         "vapr_best_per_problem": ([P, I32, I32, P, P, P], I32),
+        "vapr_sparse_pool_words": ([vapr_format, SZ, SZ], SZ),
+        "vapr_sparsify": ([vapr_format, P, SZ, SZ, P, P, P, SZ, P, P], I32),
+        "vapr_densify": ([vapr_format, P, P, P, SZ, SZ, P, P], I32),
+        "vapr_cost_grad_sparse_layout": ([P, I32, I32, ctypes.POINTER(SZ * 4), ctypes.POINTER(SZ)],
+                                         I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -184,6 +192,21 @@ def vapr_quantize(f, x, rows, cols, packed, stream=None):
 def vapr_dequantize(f, packed, rows, cols, y, stream=None):
     _check(lib.vapr_dequantize(fmt(f), _ptr(packed), rows, cols, _ptr(y), _stream(stream)),
            "vapr_dequantize")
+
+
+def vapr_sparse_pool_words(f, cols, rows):
+    return int(lib.vapr_sparse_pool_words(fmt(f), cols, rows))
+
+
+def vapr_sparsify(f, packed, rows, cols, mask, off, pool, used, stream=None):
+    """Dense packed rows -> sparse form (N3); pool capacity from pool.numel()."""
+    _check(lib.vapr_sparsify(fmt(f), _ptr(packed), rows, cols, _ptr(mask), _ptr(off), _ptr(pool),
+                             pool.numel(), _ptr(used), _stream(stream)), "vapr_sparsify")
+
+
+def vapr_densify(f, mask, off, pool, rows, cols, packed, stream=None):
+    _check(lib.vapr_densify(fmt(f), _ptr(mask), _ptr(off), _ptr(pool), rows, cols, _ptr(packed),
+                            _stream(stream)), "vapr_densify")
 
 
 def vapr_best_per_problem(cost_traj, n_problems, seeds, best_cost, best_seed, stream=None):
@@ -299,6 +322,15 @@ def vapr_cost_grad_workspace_layout(ctx, B, H, swept):
     _check(lib.vapr_cost_grad_workspace_layout(ctx, B, H, int(swept), ctypes.byref(arr)),
            "vapr_cost_grad_workspace_layout")
     return [None if v == ctypes.c_size_t(-1).value else int(v) for v in arr]
+
+
+def vapr_cost_grad_sparse_layout(ctx, B, H):
+    """(byte offsets of mask, off, used, pool; pool capacity in words) with VAPR_OPT_SPARSE."""
+    arr = (ctypes.c_size_t * 4)()
+    pw = ctypes.c_size_t()
+    _check(lib.vapr_cost_grad_sparse_layout(ctx, B, H, ctypes.byref(arr), ctypes.byref(pw)),
+           "vapr_cost_grad_sparse_layout")
+    return [int(v) for v in arr], int(pw.value)
 
 
 def vapr_cost_grad(ctx, q, world_idx, B, H, params, workspace, cost_pose, cost_traj, grad_q,

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libvapr.so")
-SOURCES = ["api.cu", "codec.cu", "fk.cu", "collision.cu", "aggregate.cu", "bk.cu", "lbfgs.cu"]
+SOURCES = ["api.cu", "codec.cu", "fk.cu", "collision.cu", "aggregate.cu", "bk.cu", "lbfgs.cu", "sparse.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",

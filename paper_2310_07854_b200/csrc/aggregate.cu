@@ -12,10 +12,15 @@
 // grad_out_spheres words (hardware cvt where exact) with coalesced stores.
 // The sum is the same single FP32 addition per element as before, so the
 // result is bit-identical to decode(cp) + decode(ov) -> encode.
+//
+// SPARSE (N3, VAPR_OPT_SPARSE): the third pass is emit_sparse_rows (a warp
+// per row, a lane per sphere: encode3 -- the same codes as encode_word_t --
+// then bitmap, rank and packing) writing the tile in the sparse form.
 #include <algorithm>
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sparse.cuh"
 
 namespace vapr {
 
@@ -64,11 +69,12 @@ __device__ __forceinline__ void decode_tile(const uint32_t* src, int W, int nr, 
     }
 }
 
+template <bool SPARSE>
 __global__ void __launch_bounds__(kThreads)
 aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, int Wo, int Wg,
                  const uint32_t* __restrict__ cp, const uint32_t* __restrict__ ov,
                  long long rows, uint32_t* __restrict__ gos, uint32_t rw_c, uint32_t rw_o,
-                 uint32_t rw_g, int xs) {
+                 uint32_t rw_g, int xs, const SparseOut sp) {
     extern __shared__ uint4 smem_a[];
     uint32_t* sc = reinterpret_cast<uint32_t*>(smem_a);     // [kRows * Wc]
     uint32_t* so = sc + kRows * Wc;                         // [kRows * Wo]
@@ -96,6 +102,18 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
         decode_tile<decltype(Pc)::value, true>(so, Wo, nr, cols, rw_o, x, xs, fov, &negz);
     });
     __syncthreads();
+    if constexpr (SPARSE) {
+        __shared__ SparseTileSmem<kRows> sm;
+        uint32_t* wbuf = reinterpret_cast<uint32_t*>(x + kRows * xs);   // [kWarps * cols]
+        emit_sparse_rows<kRows, kThreads / 32>(nr, cols / 3, fg, sp.rcp, sm, wbuf, cols, r0,
+                                               sp.seg0 + (uint32_t)blockIdx.x * kRows * sp.wmax, sp.mask,
+                                               sp.off, sp.pool, sp.used,
+                                               [&](int r, int s, uint32_t* c) {
+                                                   const float* xr = x + r * xs + 3 * s;
+                                                   encode3(xr[0], xr[1], xr[2], fg, c);
+                                               });
+        return;
+    }
     // slots past the last element that the encode pass reads: +0, whatever
     // the inputs' padding held
     const int tail = Wg * fg.pf - cols;
@@ -122,7 +140,7 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
 
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
-                             uint32_t* gos, cudaStream_t s) {
+                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse) {
     if (rows <= 0) return cudaSuccess;
     const int Wc = row_words_of(fcp, cols), Wo = row_words_of(fov, cols),
               Wg = row_words_of(fgos, cols);
@@ -137,13 +155,20 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
     // FP32 tile wide enough for every word of all three rows (the padding
     // slots hold +0), odd stride: the word-parallel passes spread over banks
     const int xs = std::max(Wc * fcp.pf, std::max(Wo * fov.pf, Wg * fgos.pf)) | 1;
-    const size_t smem = sizeof(uint32_t) * kRows * (Wc + Wo) + sizeof(float) * kRows * xs;
-    cudaError_t e = cudaFuncSetAttribute(aggregate_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t smem = sizeof(uint32_t) * kRows * (Wc + Wo) + sizeof(float) * kRows * xs;
+    if (sparse) smem += sizeof(uint32_t) * (kThreads / 32) * cols;  // per-warp code buffers
+    auto kern = sparse ? aggregate_kernel<true> : aggregate_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    SparseOut spo{};
+    if (sparse) {
+        spo = *sparse;
+        spo.wmax = (uint32_t)((cols + fgos.pf - 1) / fgos.pf);
+        spo.rcp = 65536u / fgos.pf + 1u;
+    }
     const long long grid = (rows + kRows - 1) / kRows;
-    aggregate_kernel<<<(unsigned)grid, kThreads, smem, s>>>(fcp, fov, fgos, cols, Wc, Wo, Wg, cp,
-                                                            ov, rows, gos, rw_c, rw_o, rw_g, xs);
+    kern<<<(unsigned)grid, kThreads, smem, s>>>(fcp, fov, fgos, cols, Wc, Wo, Wg, cp, ov, rows, gos,
+                                                rw_c, rw_o, rw_g, xs, spo);
     return cudaGetLastError();
 }
 

@@ -36,6 +36,8 @@ struct vapr_ctx {
     // VAPR_OPT_STREAMS: concurrent trajectory chunks in vapr_cost_grad
     int n_streams = 1;
     cudaStream_t par[8] = {};
+    // N3: grad_out_spheres in the sparse form (VAPR_OPT_SPARSE)
+    int sparse = 0;
     // IKO goals (N2)
     float* d_goals = nullptr;
     int32_t n_goals = 0;
@@ -61,6 +63,11 @@ struct DeviceGuard {
         if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
     }
 };
+
+// sparse form of a tensor (N3): pool capacity in words (every row full)
+size_t sparse_pool_words_of(const Fmt& f, int cols, long long rows) {
+    return (size_t)rows * (size_t)((cols + f.pf - 1) / f.pf);
+}
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -494,7 +501,49 @@ vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
         c->n_streams = value;
         return VAPR_OK;
     }
+    if (option == VAPR_OPT_SPARSE) {
+        CHECK(value == 0 || value == 1, VAPR_ERR_INVALID_ARG);
+        c->sparse = value;
+        return VAPR_OK;
+    }
     return VAPR_ERR_UNSUPPORTED;
+}
+
+// ---- N3: sparse form ------------------------------------------------------
+size_t vapr_sparse_pool_words(vapr_format f, size_t cols, size_t rows) {
+    if (!fmt_valid(f) || cols == 0) return 0;
+    return sparse_pool_words_of(make_fmt(f), (int)cols, (long long)rows);
+}
+
+vapr_status vapr_sparsify(vapr_format f, const uint32_t* packed, size_t rows, size_t cols,
+                          uint64_t* mask, uint32_t* off, uint32_t* pool, size_t pool_words,
+                          uint32_t* used, void* stream) {
+    CHECK(fmt_valid(f), VAPR_ERR_INVALID_FORMAT);
+    CHECK(cols > 0 && cols % 3 == 0 && cols / 3 <= 64, VAPR_ERR_SHAPE);
+    CHECK(used != nullptr, VAPR_ERR_INVALID_ARG);
+    const Fmt F = make_fmt(f);
+    CHECK(pool_words >= sparse_pool_words_of(F, (int)cols, (long long)rows), VAPR_ERR_SHAPE);
+    CHECK(sparse_pool_words_of(F, (int)cols, (long long)rows) <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);
+    CHECK(rows == 0 || (packed && mask && off && pool), VAPR_ERR_INVALID_ARG);
+    CHECK(aligned16(packed) && (reinterpret_cast<uintptr_t>(mask) & 7u) == 0, VAPR_ERR_INVALID_ARG);
+    return cuda_status(launch_sparsify(F, packed, (long long)rows, (int)cols,
+                                       SparseOut{reinterpret_cast<unsigned long long*>(mask), off,
+                                                 pool, used},
+                                       (cudaStream_t)stream));
+}
+
+vapr_status vapr_densify(vapr_format f, const uint64_t* mask, const uint32_t* off,
+                         const uint32_t* pool, size_t rows, size_t cols, uint32_t* packed,
+                         void* stream) {
+    CHECK(fmt_valid(f), VAPR_ERR_INVALID_FORMAT);
+    CHECK(cols > 0 && cols % 3 == 0 && cols / 3 <= 64, VAPR_ERR_SHAPE);
+    if (rows == 0) return VAPR_OK;
+    CHECK(mask && off && pool && packed, VAPR_ERR_INVALID_ARG);
+    CHECK((reinterpret_cast<uintptr_t>(mask) & 7u) == 0, VAPR_ERR_INVALID_ARG);
+    return cuda_status(launch_densify(make_fmt(f),
+                                      SparseIn{reinterpret_cast<const unsigned long long*>(mask),
+                                               off, pool},
+                                      (long long)rows, (int)cols, packed, (cudaStream_t)stream));
 }
 
 // ---- a1 ------------------------------------------------------------------
@@ -644,8 +693,11 @@ vapr_status vapr_backward_kinematics(vapr_ctx* c, const float* q, int32_t B, int
 }
 
 // ---- a7 ------------------------------------------------------------------
+// sp (nullable): with c->sparse, the byte offsets of grad_out_spheres' mask,
+// off, used and pool, and the pool capacity in words
 static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR_NUM_SLOTS],
-                      size_t* cost_off, size_t* total) {
+                      size_t* cost_off, size_t* total, size_t* sp = nullptr,
+                      size_t* pool_words = nullptr) {
     const int cols = c->robot.cols;
     for (int i = 0; i < VAPR_NUM_SLOTS; ++i) off[i] = SIZE_MAX;
     size_t o = 0;
@@ -658,8 +710,24 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
                               packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
     off[VAPR_OUT_VEC] = o;
     o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
-    off[VAPR_GRAD_OUT_SPHERES] = o;
-    o = align256(o + packed_bytes(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P));
+    if (c->sparse) {
+        size_t so[4];
+        so[0] = o;                                            // mask [P] uint64
+        o = align256(o + sizeof(uint64_t) * (size_t)P);
+        so[1] = o;                                            // off [P] uint32
+        o = align256(o + sizeof(uint32_t) * (size_t)P);
+        so[2] = o;                                            // used
+        o = align256(o + sizeof(uint32_t));
+        so[3] = o;                                            // pool
+        const size_t pw = sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P);
+        o = align256(o + sizeof(uint32_t) * pw);
+        if (sp)
+            for (int i = 0; i < 4; ++i) sp[i] = so[i];
+        if (pool_words) *pool_words = pw;
+    } else {
+        off[VAPR_GRAD_OUT_SPHERES] = o;
+        o = align256(o + packed_bytes(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P));
+    }
     *cost_off = o;
     o = align256(o + sizeof(float) * (size_t)P);
     *total = o;
@@ -681,6 +749,16 @@ vapr_status vapr_cost_grad_workspace_layout(const vapr_ctx* c, int32_t B, int32_
     return VAPR_OK;
 }
 
+vapr_status vapr_cost_grad_sparse_layout(const vapr_ctx* c, int32_t B, int32_t H,
+                                         size_t* offsets, size_t* pool_words) {
+    CHECK(c != nullptr && offsets != nullptr && pool_words != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
+    CHECK(c->sparse, VAPR_ERR_INVALID_ARG);
+    size_t off[VAPR_NUM_SLOTS], co, total;
+    ws_layout(c, (long long)B * H, 1, off, &co, &total, offsets, pool_words);
+    return VAPR_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -693,7 +771,6 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
                               int nb, int B, int H, const vapr_cost_params* p, void* workspace,
                               const size_t* off, float* cpose, float* cost_traj, float* grad_q,
                               cudaStream_t s) {
-    (void)B;
     char* ws = static_cast<char*>(workspace);
     const int cps = p->swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
     const long long p0 = (long long)b0 * H, P = (long long)nb * H;
@@ -704,7 +781,23 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     uint32_t* os = rows_of(VAPR_OUT_SPHERES);
     uint32_t* cp = rows_of(cps);
     uint32_t* ov = rows_of(VAPR_OUT_VEC);
-    uint32_t* gos = rows_of(VAPR_GRAD_OUT_SPHERES);
+    uint32_t* gos = c->sparse ? nullptr : rows_of(VAPR_GRAD_OUT_SPHERES);
+    // N3: grad_out_spheres in the sparse form (rows p0.. of mask / off; the
+    // pool and its cursor are shared by all chunks)
+    SparseOut spo{};
+    SparseIn spi{};
+    if (c->sparse) {
+        size_t so[4], pw, o2[VAPR_NUM_SLOTS], co2, tot2;
+        ws_layout(c, (long long)B * H, p->swept, o2, &co2, &tot2, so, &pw);
+        spo.mask = reinterpret_cast<unsigned long long*>(ws + so[0]) + p0;
+        spo.off = reinterpret_cast<uint32_t*>(ws + so[1]) + p0;
+        spo.used = reinterpret_cast<uint32_t*>(ws + so[2]);
+        spo.pool = reinterpret_cast<uint32_t*>(ws + so[3]);
+        spo.seg0 = (uint32_t)sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, p0);
+        spi.mask = spo.mask;
+        spi.off = spo.off;
+        spi.pool = spo.pool;
+    }
     const float* qc = q + p0 * kJoints;
     // IKO terms (N2): FK writes cost_pose = pose + bound, the collision passes add
     IkArgs ik{};
@@ -743,10 +836,10 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose + p0, nb, H, cost_traj + b0, s);
     if (e == cudaSuccess)
         e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
-                             cols, cp, ov, P, gos, s);
+                             cols, cp, ov, P, gos, s, c->sparse ? &spo : nullptr);
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
-                      iko ? &ik : nullptr);
+                      iko ? &ik : nullptr, c->sparse ? &spi : nullptr);
     return e;
 }
 
@@ -783,6 +876,14 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
                              : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
     cudaStream_t s0 = (cudaStream_t)stream;
     const int ns = std::min(c->n_streams, B);
+    if (c->sparse) {            // N3: the sparse pool's counter, before any chunk
+        size_t so[4], pw;
+        ws_layout(c, P, p->swept, off, &co, &total, so, &pw);
+        CHECK(pw <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);          // 32-bit row offsets
+        const cudaError_t e0 =
+            cudaMemsetAsync(static_cast<char*>(workspace) + so[2], 0, sizeof(uint32_t), s0);
+        if (e0 != cudaSuccess) return cuda_status(e0);
+    }
     if (ns <= 1)
         return cuda_status(enqueue_cost_grad(c, q, world_idx, 0, B, B, H, p, workspace, off, cpose,
                                              cost_traj, grad_q, s0));
@@ -875,6 +976,13 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     if (e != cudaSuccess) return cuda_status(e);
     cudaStream_t s = (cudaStream_t)stream;
     cudaEvent_t* ev = c->events.data();
+    if (c->sparse) {            // N3: the sparse pool's counter, before any chunk
+        size_t so[4], pw;
+        ws_layout(c, P, p->swept, off, &co, &total, so, &pw);
+        CHECK(pw <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);          // 32-bit row offsets
+        e = cudaMemsetAsync(static_cast<char*>(workspace) + so[2], 0, sizeof(uint32_t), s);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
     // the copy streams start after the work already enqueued on `stream`
     e = cudaEventRecord(ev[0], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_in, ev[0], 0);

@@ -14,6 +14,11 @@
 // non-zero; each link's (F_l, M_l) is folded into the
 // joint accumulators j <= l as soon as the link's frame is known, so no frame
 // is stored and no prefix/total difference (cancellation) is formed.
+//
+// SPR (N3, VAPR_OPT_SPARSE): grad_out_spheres in the sparse form -- the mask
+// is the row's bitmap and the k-th set sphere's codes are 3k + c of the row's
+// pool range, read straight from global memory (L2: the aggregation pass just
+// wrote them); no tile copy, no SWAR scan.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -29,17 +34,18 @@ constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
 // IKO: the N2 pose / bound terms; SP: the gradient slot is IEEE E5M10 (its
 // exponent-31 codes decode to inf / NaN, reading c41) -- a separate
 // instantiation so the common ones carry no fixup.
-template <bool IKO, bool SP>
+template <bool IKO, bool SP, bool SPR>
 __global__ void __launch_bounds__(kTile)
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
-          uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik) {
+          uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik,
+          const SparseIn spi) {
     extern __shared__ unsigned long long smem8[];
     const int WS = W + 4;                 // 16-byte aligned rows
     float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
     float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
     uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
-    float* sg = reinterpret_cast<float*>(sw + kTile * WS);            // [kTile * 7] grad_q
+    float* sg = reinterpret_cast<float*>(sw + (SPR ? 0 : kTile * WS));  // [kTile * 7] grad_q
     __shared__ unsigned long long s_mask[kTile];
     __shared__ int s_act[kTile];
     __shared__ int s_nact;
@@ -53,7 +59,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     for (int i = tid; i < R.n_spheres; i += kTile) so[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
     for (int i = tid; i < np * kJoints; i += kTile) sq[i] = __ldcs(q + p0 * kJoints + i);
     __syncthreads();
-    {
+    if (!SPR) {
         // plain 16-byte copy of the tile (rows are 16-byte multiples), several
         // loads in flight
         const int Q = W / 4, nq = np * Q;
@@ -71,7 +77,9 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     // W + 4 words: conflict-free per quarter warp); a word's non-zero fields
     // come from one SWAR test, the rare non-zero words are then walked
     unsigned long long mask = 0ull;
-    if (tid < np) {
+    if (SPR) {
+        if (tid < np) mask = __ldcs(spi.mask + p0 + tid);
+    } else if (tid < np) {
         const uint4* r4 = reinterpret_cast<const uint4*>(sw + tid * WS);
         for (int g = 0; g < W / 4; ++g) {
             const uint4 v = r4[g];
@@ -111,7 +119,9 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
         float gq[kJoints];
 #pragma unroll
         for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
-        const uint32_t* row = sw + pp * WS;
+        const uint32_t* row = SPR ? spi.pool + spi.off[p0 + pp] : sw + pp * WS;
+        // SPR: rank of the next set sphere (spheres of link 0 carry no joint)
+        int kr = SPR ? __popcll(pmask & ((1ull << R.link_start[1]) - 1ull)) : 0;
         float zx[kJoints], zy[kJoints], zz[kJoints], ox[kJoints], oy[kJoints], oz[kJoints];
         Xf X;
         xf_identity(X);
@@ -155,11 +165,12 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 float g[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const int e = 3 * s + c;
+                    const int e = SPR ? 3 * kr + c : 3 * s + c;
                     const int wi = int((e * rc) >> 16);
                     const uint32_t code = code_at(row[wi], e - wi * f.pf, f);
                     g[c] = SP ? decode_sp(code, f) : decode(code, f);
                 }
+                if (SPR) ++kr;
                 float cx, cy, cz;
                 const float4 o4 = so[s];
                 xf_apply(X, o4.x, o4.y, o4.z, cx, cy, cz);
@@ -200,12 +211,14 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 }  // namespace
 
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
-                      const uint32_t* gos, float* grad_q, cudaStream_t s, const IkArgs* ik) {
+                      const uint32_t* gos, float* grad_q, cudaStream_t s, const IkArgs* ik,
+                      const SparseIn* sparse) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
     const size_t smem = sizeof(float4) * kMaxSpheres +
                         sizeof(float) * kTile * kJoints +
-                        sizeof(uint32_t) * kTile * (W + 4) + sizeof(float) * kTile * kJoints;
+                        sizeof(uint32_t) * kTile * (sparse ? 0 : W + 4) +
+                        sizeof(float) * kTile * kJoints;
     cudaError_t e = cudaSuccess;
     const uint32_t rc = 65536u / fgos.pf + 1u;
     const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
@@ -220,13 +233,18 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     const long long grid = (P + kTile - 1) / kTile;
     const bool iko = ik && ik_on(*ik);
     const bool sp = fgos.kind == KIND_F16_IEEE;
-    auto kern = iko ? (sp ? bk_kernel<true, true> : bk_kernel<true, false>)
-                    : (sp ? bk_kernel<false, true> : bk_kernel<false, false>);
+    auto pick = [&](auto spr) {
+        constexpr bool S = decltype(spr)::value;
+        return iko ? (sp ? bk_kernel<true, true, S> : bk_kernel<true, false, S>)
+                   : (sp ? bk_kernel<false, true, S> : bk_kernel<false, false, S>);
+    };
+    auto kern = sparse ? pick(IC<1>{}) : pick(IC<0>{});
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     IkArgs none{};
+    const SparseIn dense{};
     kern<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc, rq, f_lo, f_hi, rt,
-                                             iko ? *ik : none);
+                                             iko ? *ik : none, sparse ? *sparse : dense);
     return cudaGetLastError();
 }
 

@@ -57,12 +57,33 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
 constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight collision passes)
 cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
                                cudaStream_t s);
+// N3 sparse form of a sphere tensor (include/vapr.h "N3"; sparse.cuh)
+struct SparseOut {
+    unsigned long long* mask;  // [rows] (the caller offsets it to the first row)
+    uint32_t* off;             // [rows]
+    uint32_t* pool;            // shared by all rows / chunks
+    uint32_t* used;            // pool words in use (a counter)
+    uint32_t seg0;             // pool word of the launch's row 0 segment: row0 * ceil(cols / pf)
+    uint32_t wmax;             // ceil(cols / pf) (set by the launcher)
+    uint32_t rcp;              // 65536 / pf + 1 (set by the launcher)
+};
+struct SparseIn {
+    const unsigned long long* mask;
+    const uint32_t* off;
+    const uint32_t* pool;
+};
+cudaError_t launch_sparsify(const Fmt& f, const uint32_t* packed, long long rows, int cols,
+                            const SparseOut& o, cudaStream_t s);
+cudaError_t launch_densify(const Fmt& f, const SparseIn& in, long long rows, int cols,
+                           uint32_t* packed, cudaStream_t s);
+// sparse (nullable): write grad_out_spheres in the sparse form instead of gos
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
-                             uint32_t* gos, cudaStream_t s);
+                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr);
+// sparse (nullable): read grad_out_spheres from the sparse form instead of gos
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s,
-                      const IkArgs* ik = nullptr);
+                      const IkArgs* ik = nullptr, const SparseIn* sparse = nullptr);
 // N1 optimiser (lbfgs.cu)
 struct LbfgsScales {
     float s[32];

@@ -40,6 +40,10 @@ class Context:
     def set_streams(self, n):
         vb.vapr_set_option(self.h, vb.VAPR_OPT_STREAMS, int(n))
 
+    def set_sparse(self, on):
+        """N3: grad_out_spheres in the sparse form inside vapr_cost_grad."""
+        vb.vapr_set_option(self.h, vb.VAPR_OPT_SPARSE, int(on))
+
     def close(self):
         if self.h is not None:
             vb.vapr_destroy(self.h)
@@ -55,7 +59,7 @@ class Context:
 class Rollout:
     """One batch [B, H] of trajectories resident in HBM."""
 
-    def __init__(self, workload, device=0, formats=None, ctx=None):
+    def __init__(self, workload, device=0, formats=None, ctx=None, sparse=False):
         self.wl = workload
         self.device = torch.device("cuda", device)
         self.ctx = ctx or Context(device, workload.robot, formats or workload.formats,
@@ -63,6 +67,9 @@ class Rollout:
                                   getattr(workload, "goals", None))
         if formats is not None and ctx is not None:
             self.ctx.set_formats(formats)
+        self.sparse = bool(sparse)
+        if sparse:
+            self.ctx.set_sparse(True)
         self.B, self.H = workload.B, workload.H
         self.params = dict(workload.params)
         self._p = vb.cost_params(self.params)
@@ -95,6 +102,19 @@ class Rollout:
                                self.workspace, self.q, self.cost_pose, self.cost_traj,
                                self.grad_q, cost_traj_host, grad_q_host, n_chunks,
                                stream=stream, _p=self._p)
+
+    def sparse_gos(self):
+        """N3 (sparse mode): grad_out_spheres' mask [P] uint64, off [P], the
+        pool (its whole capacity) and the count of words in use, as numpy arrays."""
+        torch.cuda.synchronize(self.device)
+        (mo, oo, uo, po), pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        P = self.B * self.H
+        ws = self.workspace
+        mask = ws[mo:mo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64)
+        off = ws[oo:oo + 4 * P].view(torch.int32).cpu().numpy().view(np.uint32)
+        used = int(ws[uo:uo + 4].view(torch.int32).cpu().numpy().view(np.uint32)[0])
+        pool = ws[po:po + 4 * pw].view(torch.int32).cpu().numpy().view(np.uint32)
+        return dict(mask=mask, off=off, pool=pool, used=used)
 
     def packed(self, slot):
         """The packed tensor of `slot` inside the workspace, as uint32 [P, W]."""
