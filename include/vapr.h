@@ -350,12 +350,16 @@ vapr_status vapr_densify(vapr_format f, const uint64_t *mask, const uint32_t *of
                          const uint32_t *pool, size_t rows, size_t cols, uint32_t *packed,
                          void *stream);
 /* With VAPR_OPT_SPARSE = 1: byte offsets inside vapr_cost_grad's workspace
- * of grad_out_spheres' mask [B*H], off [B*H], used [1] and pool
- * [pool_words], in that order; *pool_words = the pool capacity.  The dense
- * slot's entry of vapr_cost_grad_workspace_layout is SIZE_MAX in this mode.
+ * of (0) grad_out_spheres' mask [B*H], (1) its off [B*H], (2) used [1], (3)
+ * the pool [pool_words], and the per-pose sphere bitmaps [B*H] uint64 of (4)
+ * closest_pt[_swept] and (5) out_vec; *pool_words = the pool capacity.  In
+ * this mode the collision passes do not zero-fill their rows: a field of a
+ * closest_pt / out_vec row is valid only where its sphere's bit is set (the
+ * others are stale), and the aggregation reads only those.  The dense
+ * grad_out_spheres entry of vapr_cost_grad_workspace_layout is SIZE_MAX.
  * VAPR_ERR_INVALID_ARG when the option is off. */
 vapr_status vapr_cost_grad_sparse_layout(const vapr_ctx *ctx, int32_t B, int32_t H,
-                                         size_t offsets[4], size_t *pool_words);
+                                         size_t offsets[6], size_t *pool_words);
 
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =

@@ -64,6 +64,9 @@ struct DeviceGuard {
     }
 };
 
+// vapr_cost_grad_sparse_layout entries (N3)
+constexpr int kSparseOffs = 6;
+
 // sparse form of a tensor (N3): pool capacity in words (every row full)
 size_t sparse_pool_words_of(const Fmt& f, int cols, long long rows) {
     return (size_t)rows * (size_t)((cols + f.pf - 1) / f.pf);
@@ -711,7 +714,7 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
     off[VAPR_OUT_VEC] = o;
     o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
     if (c->sparse) {
-        size_t so[4];
+        size_t so[kSparseOffs];
         so[0] = o;                                            // mask [P] uint64
         o = align256(o + sizeof(uint64_t) * (size_t)P);
         so[1] = o;                                            // off [P] uint32
@@ -721,8 +724,12 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
         so[3] = o;                                            // pool
         const size_t pw = sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P);
         o = align256(o + sizeof(uint32_t) * pw);
+        so[4] = o;                                            // closest_pt bitmaps [P]
+        o = align256(o + sizeof(uint64_t) * (size_t)P);
+        so[5] = o;                                            // out_vec bitmaps [P]
+        o = align256(o + sizeof(uint64_t) * (size_t)P);
         if (sp)
-            for (int i = 0; i < 4; ++i) sp[i] = so[i];
+            for (int i = 0; i < kSparseOffs; ++i) sp[i] = so[i];
         if (pool_words) *pool_words = pw;
     } else {
         off[VAPR_GRAD_OUT_SPHERES] = o;
@@ -786,14 +793,17 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     // pool and its cursor are shared by all chunks)
     SparseOut spo{};
     SparseIn spi{};
+    unsigned long long *cp_mask = nullptr, *ov_mask = nullptr;
     if (c->sparse) {
-        size_t so[4], pw, o2[VAPR_NUM_SLOTS], co2, tot2;
+        size_t so[kSparseOffs], pw, o2[VAPR_NUM_SLOTS], co2, tot2;
         ws_layout(c, (long long)B * H, p->swept, o2, &co2, &tot2, so, &pw);
         spo.mask = reinterpret_cast<unsigned long long*>(ws + so[0]) + p0;
         spo.off = reinterpret_cast<uint32_t*>(ws + so[1]) + p0;
         spo.used = reinterpret_cast<uint32_t*>(ws + so[2]);
         spo.pool = reinterpret_cast<uint32_t*>(ws + so[3]);
         spo.seg0 = (uint32_t)sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, p0);
+        cp_mask = reinterpret_cast<unsigned long long*>(ws + so[4]) + p0;
+        ov_mask = reinterpret_cast<unsigned long long*>(ws + so[5]) + p0;
         spi.mask = spo.mask;
         spi.off = spo.off;
         spi.pool = spo.pool;
@@ -830,13 +840,18 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.cp = cp;
         a.ov = ov;
         a.cost_accumulate = iko ? 1 : 0;
+        a.cp_mask = cp_mask;
+        a.ov_mask = ov_mask;
         e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
                              c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
     if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose + p0, nb, H, cost_traj + b0, s);
     if (e == cudaSuccess)
-        e = launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], c->dfmt[VAPR_GRAD_OUT_SPHERES],
-                             cols, cp, ov, P, gos, s, c->sparse ? &spo : nullptr);
+        e = c->sparse ? launch_aggregate_masked(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
+                                                c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
+                                                ov, ov_mask, P, spo, s)
+                      : launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
+                                         c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, ov, P, gos, s);
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
                       iko ? &ik : nullptr, c->sparse ? &spi : nullptr);
@@ -877,7 +892,7 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
     cudaStream_t s0 = (cudaStream_t)stream;
     const int ns = std::min(c->n_streams, B);
     if (c->sparse) {            // N3: the sparse pool's counter, before any chunk
-        size_t so[4], pw;
+        size_t so[kSparseOffs], pw;
         ws_layout(c, P, p->swept, off, &co, &total, so, &pw);
         CHECK(pw <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);          // 32-bit row offsets
         const cudaError_t e0 =
@@ -977,7 +992,7 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     cudaStream_t s = (cudaStream_t)stream;
     cudaEvent_t* ev = c->events.data();
     if (c->sparse) {            // N3: the sparse pool's counter, before any chunk
-        size_t so[4], pw;
+        size_t so[kSparseOffs], pw;
         ws_layout(c, P, p->swept, off, &co, &total, so, &pw);
         CHECK(pw <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);          // 32-bit row offsets
         e = cudaMemsetAsync(static_cast<char*>(workspace) + so[2], 0, sizeof(uint32_t), s);

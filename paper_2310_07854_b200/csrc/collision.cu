@@ -115,6 +115,40 @@ __device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, flo
     acc.gz = fmaf(sc, gzw, acc.gz);
 }
 
+// N3 masked rows (not zero-filled): a sphere with a non-zero code sets its
+// bitmap bit and overwrites its three fields (clear, then OR: the other
+// spheres' fields of a shared word are untouched)
+__device__ __forceinline__ void or_code3_masked(uint32_t* row, int e, float vx, float vy, float vz,
+                                                const Fmt& f, uint32_t rc,
+                                                unsigned long long* pmask) {
+    const float v[3] = {vx, vy, vz};
+    uint32_t c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c[k] = (__float_as_uint(v[k]) != 0u) ? encode(v[k], f) : 0u;
+    if (!(c[0] | c[1] | c[2])) return;
+    atomicOr(pmask, 1ull << (e / 3));
+    int cw = -1;
+    uint32_t acc = 0u, fm = 0u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int ec = e + k;
+        const int w = int((ec * rc) >> 16);
+        if (w != cw) {
+            if (cw >= 0) {
+                atomicAnd(row + cw, ~fm);
+                if (acc) atomicOr(row + cw, acc);
+            }
+            cw = w;
+            acc = fm = 0u;
+        }
+        const int sh = (ec - w * f.pf) * f.t;
+        acc |= c[k] << sh;
+        fm |= f.mask << sh;
+    }
+    atomicAnd(row + cw, ~fm);
+    if (acc) atomicOr(row + cw, acc);
+}
+
 // OR the codes of the vector (vx, vy, vz) at elements e .. e+2 into a packed
 // row: codes sharing a word go in one atomic, +0 components (code 0, the
 // sparse common case) in none.
@@ -350,6 +384,10 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
 // spheres, live group pairs, touched spheres) goes through warp work queues
 // so that every lane has an item.  Warps are independent: no CTA barrier in
 // the tile loop.
+// MASKED (N3, VAPR_OPT_SPARSE): per-pose sphere bitmaps instead of zero-filled
+// rows -- its own instantiation, so the dense one carries no extra code (the
+// kernel is instruction-cache sensitive).
+template <bool MASKED>
 __global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
@@ -523,12 +561,22 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // with atomics (__syncwarp orders the fill before every lane's atomics)
         uint32_t* const cpg = a.do_world ? a.cp + p0 * G.Wcp : nullptr;
         uint32_t* const ovg = a.do_self ? a.ov + p0 * G.Wov : nullptr;
-        if (a.do_world)
+        // N3 masked rows: only the tile's bitmaps are cleared
+        unsigned long long* const cpm = (MASKED && a.do_world) ? a.cp_mask + p0 : nullptr;
+        unsigned long long* const ovm = (MASKED && a.do_self) ? a.ov_mask + p0 : nullptr;
+        if (cpm) {
+            if (lane < np) cpm[lane] = 0ull;
+        } else if (a.do_world) {
             for (int i = lane; i < np * G.Wcp / 4; i += 32)
                 reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
         if (a.do_self) {
-            for (int i = lane; i < np * G.Wov / 4; i += 32)
-                reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (ovm) {
+                if (lane < np) ovm[lane] = 0ull;
+            } else {
+                for (int i = lane; i < np * G.Wov / 4; i += 32)
+                    reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
+            }
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
             if (lane < kTP) pwm[lane] = 0u;
         }
@@ -686,7 +734,11 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                    a.w_w, cw, gw, acc);
                 }
                 uint32_t* orow = cpg + p * G.Wcp;
-                or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
+                if (MASKED)
+                    or_code3_masked(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp,
+                                    G.rc_cp, cpm + p);
+                else
+                    or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
                 return acc.cost;
             });
         }
@@ -857,7 +909,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     }
                 }
                 uint32_t* orow = ovg + p * G.Wov;
-                or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
+                if (MASKED)
+                    or_code3_masked(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov, ovm + p);
+                else
+                    or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
                 return c_lead;
             });
         }
@@ -938,15 +993,15 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     nw = std::min(nw, VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
-    cudaError_t e = cudaFuncSetAttribute(collision_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = (a.cp_mask || a.ov_mask) ? collision_kernel<true> : collision_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, collision_kernel, 32 * nw, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nw, smem);
     const long long tiles = (P + kTP - 1) / kTP;
     const long long grid = std::min<long long>((tiles + kGrab * nw - 1) / (kGrab * nw),
                                                (long long)sms * std::max(per_sm, 1));
-    collision_kernel<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
+    kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
     return cudaGetLastError();
 }
 

@@ -28,6 +28,12 @@ struct CollisionArgs {
     float* cost;              // [B*H] (world + self of the enabled parts)
     uint32_t* cp;             // packed world gradient (nullable iff !do_world)
     uint32_t* ov;             // packed self gradient (nullable iff !do_self)
+    // N3 (VAPR_OPT_SPARSE; nullable = dense): per-pose sphere bitmaps of cp / ov.
+    // With them the rows are not zero-filled: a sphere with a non-zero code
+    // sets its bit and overwrites its own fields, and readers take only the
+    // fields of set spheres.
+    unsigned long long* cp_mask;
+    unsigned long long* ov_mask;
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
     unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero
 };
@@ -80,6 +86,11 @@ cudaError_t launch_densify(const Fmt& f, const SparseIn& in, long long rows, int
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
                              uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr);
+// N3 masked inputs (cp / ov rows + sphere bitmaps, not zero-filled) -> sparse form
+cudaError_t launch_aggregate_masked(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
+                                    const uint32_t* cp, const unsigned long long* cpm,
+                                    const uint32_t* ov, const unsigned long long* ovm,
+                                    long long rows, const SparseOut& sparse, cudaStream_t s);
 // sparse (nullable): read grad_out_spheres from the sparse form instead of gos
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s,

@@ -107,7 +107,7 @@ class Rollout:
         """N3 (sparse mode): grad_out_spheres' mask [P] uint64, off [P], the
         pool (its whole capacity) and the count of words in use, as numpy arrays."""
         torch.cuda.synchronize(self.device)
-        (mo, oo, uo, po), pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        (mo, oo, uo, po, _, _), pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
         P = self.B * self.H
         ws = self.workspace
         mask = ws[mo:mo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64)
@@ -115,6 +115,40 @@ class Rollout:
         used = int(ws[uo:uo + 4].view(torch.int32).cpu().numpy().view(np.uint32)[0])
         pool = ws[po:po + 4 * pw].view(torch.int32).cpu().numpy().view(np.uint32)
         return dict(mask=mask, off=off, pool=pool, used=used)
+
+    def sphere_masks(self):
+        """N3 (sparse mode): per-pose sphere bitmaps of closest_pt[_swept] and
+        out_vec (uint64 [P] each)."""
+        torch.cuda.synchronize(self.device)
+        (_, _, _, _, cmo, omo), _ = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        P = self.B * self.H
+        ws = self.workspace
+        return (ws[cmo:cmo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64),
+                ws[omo:omo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64))
+
+    def packed_masked(self, slot):
+        """N3 (sparse mode): a collision slot's rows with the fields of unset
+        spheres zeroed -- the dense mode's rows."""
+        words = self.packed(slot)
+        cm, om = self.sphere_masks()
+        m = om if slot == vb.VAPR_OUT_VEC else cm
+        fmt = self.ctx.formats[slot]
+        t = 1 + fmt[0] + (fmt[1] & 0xFF)
+        pf = 32 // t
+        cols = 3 * len(self.wl.robot["sphere_link"])
+        out = words.copy()
+        for e in range(cols):
+            keep = ((m >> np.uint64(e // 3)) & np.uint64(1)).astype(bool)
+            w, q = e // pf, e % pf
+            fm = np.uint32(((1 << t) - 1) << (q * t)) if t < 32 else np.uint32(0xFFFFFFFF)
+            out[~keep, w] &= ~fm
+        W = words.shape[1]
+        # padding slots of the last used word and padding words are never written
+        for e in range(cols, W * pf):
+            w, q = e // pf, e % pf
+            fm = np.uint32(((1 << t) - 1) << (q * t)) if t < 32 else np.uint32(0xFFFFFFFF)
+            out[:, w] &= ~fm
+        return out
 
     def packed(self, slot):
         """The packed tensor of `slot` inside the workspace, as uint32 [P, W]."""

@@ -192,16 +192,20 @@ def check_pair(wl, a, b):
     sg = b.sparse_gos()
     check_sparse_rows(sg["mask"], sg["off"], sg["pool"], sg["used"], ref_mask, ref_rows)
     assert b.packed(1) is None         # no dense slot in sparse mode
+    # the collision rows (not zero-filled in sparse mode) restricted to their
+    # bitmaps' spheres are the dense mode's rows
+    slot = 4 if wl.params["swept"] else 3
+    for sl in (slot, 2):
+        assert np.array_equal(b.packed_masked(sl), a.packed(sl)), sl
     # oracle parity of the sparse mode itself: its rows, densified by the
     # oracle, against the oracle's aggregation of the GPU's own collision
     # outputs (the dense stagewise rule), and BK of those codes
     p = wl.params
-    slot = 4 if p["swept"] else 3
     f = b.ctx.formats
     g_codes = osp.densify(sg["mask"], [sg["pool"][int(o):int(o) + osp.row_words(m, *fg)]
                                        for m, o in zip(sg["mask"], sg["off"])], *fg, cols)
     g_words = codec.pack(g_codes, *fg)
-    ag = orc.aggregate_stage(b.packed(slot), f[slot], b.packed(2), f[2], fg, cols)
+    ag = orc.aggregate_stage(b.packed_masked(slot), f[slot], b.packed_masked(2), f[2], fg, cols)
     check_codes(g_words, ag["v"], 0.0, fg, cols, what="sparse grad_out_spheres")
     bk = orc.bk_stage(wl.q.reshape(-1, 7), g_words, fg, wl.robot)
     ik = orc.ik_terms(wl.q, wl.world_idx, wl.robot, p, getattr(wl, "goals", None), wl.H)
@@ -216,6 +220,26 @@ def test_cost_grad_sparse_equals_dense(vb, formats):
     wl = config4(problems_per_env=1, seeds=6, H=32, formats=formats)
     a, b = run_pair(wl)
     check_pair(wl, a, b)
+
+
+def test_cost_grad_sparse_stale_rows(vb):
+    """Sparse mode never zero-fills the collision rows: a second batch after a
+    first one (different trajectories, stale fields everywhere) must give
+    exactly the dense mode's results on the second batch."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl1 = config4(problems_per_env=1, seeds=8, H=32, formats="43bit")
+    rng = np.random.default_rng(77)
+    wl2 = dataclasses.replace(wl1, q=(wl1.q + rng.normal(0, 0.3, wl1.q.shape)).astype(np.float32))
+    assert not np.array_equal(wl1.q, wl2.q)
+    b = Rollout(wl1, sparse=True)
+    b.run()
+    b.run()
+    b.q.copy_(torch.from_numpy(np.ascontiguousarray(wl2.q)))
+    b.run()
+    a = Rollout(wl2)
+    a.run()
+    b.wl = wl2
+    check_pair(wl2, a, b)
 
 
 def test_cost_grad_sparse_streams_and_host(vb):
