@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--H", type=int, default=32)
     ap.add_argument("--chunks", type=int, default=0,
                     help="e2e: trajectory chunks of the pipelined host call (0 = automatic)")
+    ap.add_argument("--storage", default="sparse", choices=["sparse", "dense"],
+                    help="grad_out_spheres / collision-output storage inside vapr_cost_grad "
+                         "(VAPR_OPT_SPARSE, N3; results bit-identical)")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
     ap.add_argument("--no-iko", action="store_true",
                     help="skip the IKO leg (N2: H = 1, 1000 seeds x 800 problems, pose + bound costs)")
@@ -221,7 +224,8 @@ def main():
     wl = config4(problems_per_env=args.problems_per_env, seeds=args.seeds, H=args.H,
                  formats=fm, problem_offset=ids[0], n_problems=len(ids))
     P = wl.poses
-    r = Rollout(wl, device=local)
+    sparse = args.storage == "sparse"
+    r = Rollout(wl, device=local, sparse=sparse)
     stream = torch.cuda.current_stream(dev)
     best_c = torch.empty(n_prob, dtype=torch.float32, device=dev)
     best_s = torch.empty(n_prob, dtype=torch.int32, device=dev)
@@ -254,14 +258,16 @@ def main():
     clocks = clk.summary()
     value = world * P * S / (ms * 1e-3)
 
-    # ---- per-kernel durations (same kernels, launched stage by stage on the
-    # same stream with events between them) for the roofline of the dominant one
+    # ---- per-kernel durations (the stage entry points, launched stage by
+    # stage on the same stream with events between them; dense storage: the
+    # standalone calls take dense tensors) for the roofline of the dominant one
     p = wl.params
     swept = p["swept"]
-    lay = vb.vapr_cost_grad_workspace_layout(r.ctx.h, wl.B, wl.H, swept)
+    rd = Rollout(wl, device=local) if sparse else r
+    lay = vb.vapr_cost_grad_workspace_layout(rd.ctx.h, wl.B, wl.H, swept)
     W = {i: vb.vapr_packed_row_words(fm[i], 3 * S) for i in range(5)}
     cps = 4 if swept else 3
-    ws = r.workspace
+    ws = rd.workspace
 
     def slot(i):
         return ws[lay[i]:lay[i] + 4 * W[i] * P]
@@ -272,14 +278,14 @@ def main():
 
     def staged():
         ev[0].record(stream)
-        vb.vapr_fk_spheres(r.ctx.h, r.q, wl.B, wl.H, slot(0))
+        vb.vapr_fk_spheres(rd.ctx.h, rd.q, wl.B, wl.H, slot(0))
         ev[1].record(stream)
-        vb.vapr_collision(r.ctx.h, slot(0), r.world_idx, wl.B, wl.H, p, r.cost_pose, r.cost_traj,
-                          slot(cps), slot(2))
+        vb.vapr_collision(rd.ctx.h, slot(0), rd.world_idx, wl.B, wl.H, p, rd.cost_pose,
+                          rd.cost_traj, slot(cps), slot(2))
         ev[2].record(stream)
-        vb.vapr_aggregate(r.ctx.h, slot(cps), swept, slot(2), P, slot(1))
+        vb.vapr_aggregate(rd.ctx.h, slot(cps), swept, slot(2), P, slot(1))
         ev[3].record(stream)
-        vb.vapr_backward_kinematics(r.ctx.h, r.q, wl.B, wl.H, slot(1), r.grad_q)
+        vb.vapr_backward_kinematics(rd.ctx.h, rd.q, wl.B, wl.H, slot(1), rd.grad_q)
         ev[4].record(stream)
 
     for _ in range(2):
@@ -303,7 +309,10 @@ def main():
             traffic = tj["bytes_per_launch"].get(dom)
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+    if rd is not r:
+        del rd, ws
+        torch.cuda.empty_cache()
+    roofline = {"bound": "hbm", "kernel": dom, "stage_calls": "dense standalone entry points", "achieved": achieved, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "bytes_per_launch_alg": sb[dom] * P, "bytes_per_pose": sb[dom],
                 "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
@@ -334,7 +343,7 @@ def main():
     to_iter = None
     if not args.no_to:
         from paper_2310_07854_b200.optimize import TrajOpt
-        opt = TrajOpt(wl, device=local)
+        opt = TrajOpt(wl, device=local, sparse=sparse)
         opt.reset()
         to_ms = timed(opt.step, max(3, args.steps // 4), 2)
         to_iter = {"ms_per_iteration": to_ms, "line_search_scales": list(opt.scales),
@@ -352,7 +361,7 @@ def main():
         from workloads import config_iko
         wli = config_iko(problems_per_env=args.problems_per_env, seeds=1000, formats=fm,
                          problem_offset=ids[0], n_problems=len(ids))
-        opt = TrajOpt(wli, device=local)
+        opt = TrajOpt(wli, device=local, sparse=sparse)
         opt.reset()
         ev_ms = timed(opt.base.run, max(3, args.steps // 2), 2)
         it_ms = timed(opt.step, max(3, args.steps // 4), 2)
@@ -369,8 +378,23 @@ def main():
         r.set_formats(FORMAT_SETS["fp32"])
         ms32 = timed(step, max(3, args.steps // 2), 2)
         fp32 = {"value": world * P * S / (ms32 * 1e-3), "ms_per_step": ms32,
-                "speedup_of_formats": ms32 / ms}
+                "speedup_of_formats": ms32 / ms, "storage": args.storage}
         r.set_formats(fm)
+        if sparse:
+            # the paper's baseline layout: FP32 in dense storage (its sparsity is
+            # compute skipping only)
+            r32 = Rollout(wl, device=local, formats=FORMAT_SETS["fp32"])
+
+            def step32():
+                r32.run()
+                vb.vapr_best_per_problem(r32.cost_traj, n_prob, args.seeds, best_c, best_s)
+                gather_best(best_c, best_s, world)
+
+            ms32d = timed(step32, max(3, args.steps // 2), 2)
+            fp32["dense_ms_per_step"] = ms32d
+            fp32["speedup_vs_dense_fp32"] = ms32d / ms
+            del r32
+            torch.cuda.empty_cache()
 
     if rank == 0:
         # the oracle leg runs on rank 0 of a 1-GPU run only (the contract)
@@ -385,6 +409,9 @@ def main():
                                    f"MBM-like env) x {args.seeds} TO seeds x {args.H} steps per GPU, "
                                    "52 spheres, swept n=1",
                        "formats": args.formats, "format_bits": bits,
+                       "storage": args.storage + (" (VAPR_OPT_SPARSE: collision outputs as masked "
+                                                   "rows, grad_out_spheres as bitmap + packed codes)"
+                                                   if sparse else ""),
                        "formats_exmy": ["E%dM%d" % f for f in fm],
                        "poses_per_gpu": P, "problems_per_gpu": n_prob,
                        "l2": "inputs > L2 (packed working set >> 126 MB), no flush",

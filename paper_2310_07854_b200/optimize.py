@@ -26,7 +26,7 @@ class TrajOpt:
     values), cost = the rollout cost (world swept + self collision)."""
 
     def __init__(self, workload, scales=DEFAULT_SCALES, m=10, curvature_eps=1e-10, device=0,
-                 formats=None, fixed=None):
+                 formats=None, fixed=None, sparse=False):
         self.wl = workload
         self.scales = tuple(float(s) for s in scales)
         self.N = len(self.scales)
@@ -35,10 +35,10 @@ class TrajOpt:
         self.B, self.H = workload.B, workload.H
         self.D = 7 * self.H
         # the iterate and its cost / gradient live in the base rollout's buffers
-        self.base = Rollout(workload, device=device, formats=formats)
+        self.base = Rollout(workload, device=device, formats=formats, sparse=sparse)
         cand = dataclasses.replace(workload, q=np.tile(workload.q, (self.N, 1, 1)),
                                    world_idx=np.tile(workload.world_idx, self.N))
-        self.lines = Rollout(cand, device=device, formats=formats)
+        self.lines = Rollout(cand, device=device, formats=formats, sparse=sparse)
         dev = self.base.device
         B, D, m = self.B, self.D, self.m
         self.d = torch.zeros(B * D, dtype=torch.float32, device=dev)
