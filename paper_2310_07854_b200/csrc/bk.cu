@@ -16,9 +16,9 @@
 // is stored and no prefix/total difference (cancellation) is formed.
 //
 // SPR (N3, VAPR_OPT_SPARSE): grad_out_spheres in the sparse form -- the mask
-// is the row's bitmap and the k-th set sphere's codes are 3k + c of the row's
-// pool range, read straight from global memory (L2: the aggregation pass just
-// wrote them); no tile copy, no SWAR scan.
+// is the row's bitmap, the row's pool words (L2: the aggregation pass just
+// wrote them) are copied to the pose's shared row, and the k-th set sphere's
+// codes are 3k + c of it; no dense tile copy, no SWAR scan.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -45,7 +45,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
     float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
     uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
-    float* sg = reinterpret_cast<float*>(sw + (SPR ? 0 : kTile * WS));  // [kTile * 7] grad_q
+    float* sg = reinterpret_cast<float*>(sw + kTile * WS);            // [kTile * 7] grad_q
     __shared__ unsigned long long s_mask[kTile];
     __shared__ int s_act[kTile];
     __shared__ int s_nact;
@@ -78,7 +78,18 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     // come from one SWAR test, the rare non-zero words are then walked
     unsigned long long mask = 0ull;
     if (SPR) {
-        if (tid < np) mask = __ldcs(spi.mask + p0 + tid);
+        // the row's pool words (ceil(3 popc / pf), contiguous) into the
+        // pose's shared row: independent loads, all in flight, instead of a
+        // global load per sphere inside the chain
+        if (tid < np) {
+            mask = __ldcs(spi.mask + p0 + tid);
+            if (mask) {
+                const uint32_t n = ((uint32_t)(3 * __popcll(mask) + f.pf - 1) * rc) >> 16;
+                const uint32_t* src = spi.pool + __ldcs(spi.off + p0 + tid);
+                uint32_t* dst = sw + tid * WS;
+                for (uint32_t w = 0; w < n; ++w) dst[w] = __ldcs(src + w);
+            }
+        }
     } else if (tid < np) {
         const uint4* r4 = reinterpret_cast<const uint4*>(sw + tid * WS);
         for (int g = 0; g < W / 4; ++g) {
@@ -119,7 +130,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
         float gq[kJoints];
 #pragma unroll
         for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
-        const uint32_t* row = SPR ? spi.pool + spi.off[p0 + pp] : sw + pp * WS;
+        const uint32_t* row = sw + pp * WS;
         // SPR: rank of the next set sphere (spheres of link 0 carry no joint)
         int kr = SPR ? __popcll(pmask & ((1ull << R.link_start[1]) - 1ull)) : 0;
         float zx[kJoints], zy[kJoints], zz[kJoints], ox[kJoints], oy[kJoints], oz[kJoints];
@@ -217,7 +228,7 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     const int W = row_words_of(fgos, R.cols);
     const size_t smem = sizeof(float4) * kMaxSpheres +
                         sizeof(float) * kTile * kJoints +
-                        sizeof(uint32_t) * kTile * (sparse ? 0 : W + 4) +
+                        sizeof(uint32_t) * kTile * (W + 4) +
                         sizeof(float) * kTile * kJoints;
     cudaError_t e = cudaSuccess;
     const uint32_t rc = 65536u / fgos.pf + 1u;
