@@ -361,6 +361,18 @@ vapr_status vapr_densify(vapr_format f, const uint64_t *mask, const uint32_t *of
 vapr_status vapr_cost_grad_sparse_layout(const vapr_ctx *ctx, int32_t B, int32_t H,
                                          size_t offsets[6], size_t *pool_words);
 
+/* ---- test-only export (libvapr_tap.so, built with -DVAPR_DEBUG_TAP) ----- */
+/* SURVEY.md §8(b) "Test-only export", §8(c) parity contract (i): the next
+ * launch that produces `slot` also writes that slot's FP32 pre-quantisation
+ * values to dst (device, [rows, 3S] float32, caller-owned; zero-filled by the
+ * launch first, so elements the kernel never encodes read +0).  One-shot;
+ * dst = NULL disarms.  Not thread-safe (one process-wide table).  The
+ * aggregation taps the dense form only.  Release builds (libvapr.so) do not
+ * export the symbol and carry no tap code. */
+#ifdef VAPR_DEBUG_TAP
+vapr_status vapr_debug_tap(vapr_ctx *ctx, int32_t slot, float *dst);
+#endif
+
 /* ---- e: per-problem reduction (multi-GPU sharding) ---------------------- */
 /* best_cost[p] = min over the seeds of problem p of cost_traj, best_seed[p] =
  * its lowest argmin; problem p owns trajectories [p*seeds, (p+1)*seeds). */

@@ -117,6 +117,9 @@ def _load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    if hasattr(lib, "vapr_debug_tap"):        # the test-only tap build (VAPR_SO=libvapr_tap.so)
+        lib.vapr_debug_tap.argtypes = [P, I32, P]
+        lib.vapr_debug_tap.restype = I32
     return lib
 
 

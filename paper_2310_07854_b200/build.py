@@ -9,6 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libvapr.so")
+# test-only debug-tap build (-DVAPR_DEBUG_TAP; tap.cuh): parity contract (i)
+TAP_SO = os.path.join(HERE, "libvapr_tap.so")
 SOURCES = ["api.cu", "codec.cu", "fk.cu", "collision.cu", "aggregate.cu", "bk.cu", "lbfgs.cu", "sparse.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -18,23 +20,27 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-ftz=false", "-prec-div=true", "-prec-sqrt=true", "-fmad=true"]
 
 
-def _stale():
-    if not os.path.exists(SO):
+def _stale(so=SO):
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "vapr.h"))
     deps.append(__file__)
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, extra=()):
-    if not force and not _stale():
-        return SO
-    cmd = [NVCC, *FLAGS, *extra, "-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+def build(force=False, verbose=False, extra=(), tap=True):
+    """libvapr.so (release) and, with tap, libvapr_tap.so (the test-only
+    debug-tap build of the same sources)."""
+    outs = [(SO, [])] + ([(TAP_SO, ["-DVAPR_DEBUG_TAP"])] if tap else [])
+    for so, defs in outs:
+        if not force and not _stale(so):
+            continue
+        cmd = [NVCC, *FLAGS, *extra, *defs, "-o", so] + [os.path.join(CSRC, s) for s in SOURCES]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
     return SO
 
 

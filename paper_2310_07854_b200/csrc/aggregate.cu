@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sparse.cuh"
+#include "tap.cuh"
 
 namespace vapr {
 
@@ -102,6 +103,12 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
         decode_tile<decltype(Pc)::value, true>(so, Wo, nr, cols, rw_o, x, xs, fov, &negz);
     });
     __syncthreads();
+#ifdef VAPR_DEBUG_TAP
+    for (int i = tid; i < nr * cols; i += kThreads) {
+        const int r = i / cols, e = i - r * cols;
+        VAPR_TAP(1, (r0 + r) * cols + e, x[r * xs + e]);
+    }
+#endif
     if constexpr (SPARSE) {
         __shared__ SparseTileSmem<kRows> sm;
         uint32_t* wbuf = reinterpret_cast<uint32_t*>(x + kRows * xs);   // [kWarps * cols]
@@ -252,8 +259,14 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
         spo.rcp = 65536u / fgos.pf + 1u;
     }
     const long long grid = (rows + kRows - 1) / kRows;
+#ifdef VAPR_DEBUG_TAP
+    const bool tapped = tap_arm(1, rows, cols, s) != nullptr;
+#endif
     kern<<<(unsigned)grid, kThreads, smem, s>>>(fcp, fov, fgos, cols, Wc, Wo, Wg, cp, ov, rows, gos,
                                                 rw_c, rw_o, rw_g, xs, spo);
+#ifdef VAPR_DEBUG_TAP
+    if (tapped) tap_disarm(1, s);
+#endif
     return cudaGetLastError();
 }
 

@@ -48,6 +48,12 @@ struct vapr_ctx {
 #define VAPR_END_CHUNK_WEIGHT 0.25
 #endif
 
+#ifdef VAPR_DEBUG_TAP
+namespace vapr {
+float* g_tap_host[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+}
+#endif
+
 namespace {
 
 // Make the context's device current for the duration of a call.
@@ -511,6 +517,15 @@ vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
     }
     return VAPR_ERR_UNSUPPORTED;
 }
+
+// ---- test-only debug tap (tap.cuh) -----------------------
+#ifdef VAPR_DEBUG_TAP
+vapr_status vapr_debug_tap(vapr_ctx* c, int32_t slot, float* dst) {
+    CHECK(c != nullptr && slot >= 0 && slot < VAPR_NUM_SLOTS, VAPR_ERR_INVALID_ARG);
+    vapr::g_tap_host[slot] = dst;
+    return VAPR_OK;
+}
+#endif
 
 // ---- N3: sparse form ------------------------------------------------------
 size_t vapr_sparse_pool_words(vapr_format f, size_t cols, size_t rows) {

@@ -40,6 +40,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tap.cuh"
 
 namespace vapr {
 
@@ -734,6 +735,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                    a.w_w, cw, gw, acc);
                 }
                 uint32_t* orow = cpg + p * G.Wcp;
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp, acc.gx + 0.f);
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 1, acc.gy + 0.f);
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 2, acc.gz + 0.f);
                 if (MASKED)
                     or_code3_masked(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp,
                                     G.rc_cp, cpm + p);
@@ -909,6 +913,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     }
                 }
                 uint32_t* orow = ovg + p * G.Wov;
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 1, gy + 0.f);
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 2, gz + 0.f);
                 if (MASKED)
                     or_code3_masked(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov, ovm + p);
                 else
@@ -1001,7 +1008,16 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const long long tiles = (P + kTP - 1) / kTP;
     const long long grid = std::min<long long>((tiles + kGrab * nw - 1) / (kGrab * nw),
                                                (long long)sms * std::max(per_sm, 1));
+#ifdef VAPR_DEBUG_TAP
+    const int tw = a.swept ? 4 : 3;
+    const bool tap_w = a.do_world && tap_arm(tw, P, R.cols, s);
+    const bool tap_s = a.do_self && tap_arm(2, P, R.cols, s);
+#endif
     kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
+#ifdef VAPR_DEBUG_TAP
+    if (tap_w) tap_disarm(tw, s);
+    if (tap_s) tap_disarm(2, s);
+#endif
     return cudaGetLastError();
 }
 

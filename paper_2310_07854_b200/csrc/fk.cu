@@ -17,6 +17,7 @@
 // rows (W words per pose), which keeps 5 CTAs (20 warps) per SM at 16 bits.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tap.cuh"
 
 namespace vapr {
 
@@ -121,6 +122,9 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
                     float cx, cy, cz;
                     xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
+                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s, cx);
+                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 1, cy);
+                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 2, cz);
                     emit(cx, cy, cz);
                 }
             }
@@ -170,7 +174,13 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
     const long long grid = (P + kTile - 1) / kTile;
     const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
     IkArgs none{};
+#ifdef VAPR_DEBUG_TAP
+    const bool tapped = tap_arm(0, P, R.cols, s) != nullptr;
+#endif
     kern<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq, iko ? *ik : none);
+#ifdef VAPR_DEBUG_TAP
+    if (tapped) tap_disarm(0, s);
+#endif
     return cudaGetLastError();
 }
 

@@ -14,6 +14,8 @@ HEADER = os.path.join(ROOT, "include", "vapr.h")
 def declared_symbols():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    # the test-only export of the tap build (libvapr_tap.so) is not in libvapr.so
+    src = re.sub(r"#ifdef VAPR_DEBUG_TAP.*?#endif", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(vapr_[a-z_0-9]+)\s*\(", src)))
 
 
@@ -24,6 +26,18 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(vb.lib, s), s
     assert sorted(vb.EXPORTS) == syms
+
+
+def test_debug_tap_only_in_the_tap_build():
+    """release builds omit vapr_debug_tap; the tap build
+    (libvapr_tap.so) exports it and every release symbol."""
+    from paper_2310_07854_b200 import binding as vb
+    from paper_2310_07854_b200.build import TAP_SO
+    assert not hasattr(vb.lib, "vapr_debug_tap")
+    tap = ctypes.CDLL(TAP_SO)
+    assert hasattr(tap, "vapr_debug_tap")
+    for s in declared_symbols():
+        assert hasattr(tap, s), s
 
 
 def test_format_helpers():
