@@ -11,12 +11,12 @@ sharding of the problems across ranks ("Synthetic inputs").
 from .robot import panda_robot, READY_POSE, ROBOT_FRAMES
 from .scenes import ENVIRONMENTS, make_world, make_worlds
 from .trajectories import make_trajectories
-from .configs import (FORMAT_SETS, Workload, config1, config2, config4,
+from .configs import (FORMAT_SETS, Workload, config1, config2, config3, config4,
                       config5, config_iko, make_workload, make_goals,
                       codec_sweep_inputs, edge_values)
 
 __all__ = ["panda_robot", "READY_POSE", "ROBOT_FRAMES", "ENVIRONMENTS",
            "make_world", "make_worlds", "make_trajectories", "FORMAT_SETS",
-           "Workload", "config1", "config2", "config4", "config5",
+           "Workload", "config1", "config2", "config3", "config4", "config5",
            "config_iko", "make_workload", "make_goals", "codec_sweep_inputs",
            "edge_values"]

@@ -126,6 +126,18 @@ def config4(problems_per_env=100, seeds=100, H=32, formats="43bit",
     return make_workload("config4", envs, ids, seeds, H, fm, salt=4)
 
 
+def config3(n_problems=400, seeds=80, H=32, formats=FP32):
+    """BASELINE config 3's cost path: the three bookshelf
+    environments, 400 problems x 80 TO seeds (top of the paper's TO sweep,
+    P:191) x 32 steps = 1.024M poses; problem p uses bookshelf_{small, tall,
+    thin}[p % 3]."""
+    shelves = ("bookshelf_small", "bookshelf_tall", "bookshelf_thin")
+    ids = list(range(n_problems))
+    envs = [shelves[p % 3] for p in ids]
+    fm = FORMAT_SETS[formats] if isinstance(formats, str) else formats
+    return make_workload("config3", envs, ids, seeds, H, fm, salt=3)
+
+
 def config5(problems_per_env=10, seeds=20, H=32):
     """NSGA-II proxy batch: 8 envs x 10 problems x 20 seeds x 32 steps."""
     ids = list(range(problems_per_env * len(ENVIRONMENTS)))
