@@ -49,3 +49,36 @@ def max_over_ranks(value, device):
                      device=device if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class ShardedEvaluator:
+    """The search's candidate evaluation spread over the ranks (SURVEY.md
+    §8(e), config 5: "the 20 candidates of a generation are spread across
+    GPUs (each evaluates the full proxy batch); fitness is gathered the same
+    way").  Every rank runs the same deterministic search; for a batch of
+    candidates rank r evaluates candidates r, r + N, ... on its own GPU and
+    the fitness lists are all-gathered (a host-side object gather: a few
+    floats per candidate) and put back in candidate order, so every rank's
+    memo and search state stay identical.  world = 1: the inner evaluator."""
+
+    def __init__(self, inner, rank=None, world=None):
+        self.inner = inner
+        self.rank = dist.get_rank() if rank is None else rank
+        self.world = dist.get_world_size() if world is None else world
+        self.local_evaluations = 0
+
+    def __call__(self, configs):
+        configs = list(configs)
+        if self.world == 1:
+            self.local_evaluations += len(configs)
+            return self.inner(configs)
+        mine = configs[self.rank::self.world]
+        res = self.inner(mine) if mine else []
+        self.local_evaluations += len(mine)
+        parts = [None] * self.world
+        dist.all_gather_object(parts, list(res))
+        out = [None] * len(configs)
+        for r in range(self.world):
+            for k, v in enumerate(parts[r]):
+                out[r + k * self.world] = v
+        return out

@@ -21,6 +21,7 @@ only device work is libvapr's vapr_cost_grad.
     python -m paper_2310_07854_b200.search --budget 500 --out trials.jsonl
 """
 import argparse
+import os
 import json
 import random
 import time
@@ -422,6 +423,18 @@ def main():
     a = ap.parse_args()
     t0 = time.perf_counter()
     extra = {}
+    # multi-GPU (torchrun): candidates of every batch spread over the ranks
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     if a.evaluator == "pipeline":
         from .pipeline import PipelineEvaluator
         ev = PipelineEvaluator(problems_per_env=a.problems_per_env)
@@ -438,9 +451,15 @@ def main():
         targets = {e: a.target for e in envs}
         poses = wl.poses
         extra = {"evaluator": "proxy"}
-    with open(a.out, "w") as log:
+    if world > 1:
+        from .dist import ShardedEvaluator
+        ev = ShardedEvaluator(ev, rank, world)
+        extra["ranks"] = world
+    with open(a.out if rank == 0 else os.devnull, "w") as log:
         memo = Memo(ev, targets, log)
         res = vapr_search(memo, budget=a.budget, pop_size=a.pop, seed=a.seed)
+    if rank != 0:
+        return
     dt = time.perf_counter() - t0
     best = res["best"]
     print(json.dumps({**extra, "phase1_minima": res["minima"],

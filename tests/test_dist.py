@@ -76,3 +76,66 @@ def test_shard_partitions():
     part = config4(problems_per_env=2, seeds=2, H=3, problem_offset=8, n_problems=8)
     np.testing.assert_array_equal(full.q[16:], part.q)
     np.testing.assert_array_equal(full.cuboids[full.world_offsets[8]:], part.cuboids)
+
+
+# ------------------------------------------------ search over ranks (config 5)
+def _fake_rates(configs):
+    """A deterministic stand-in for the GPU evaluator: per-environment rates
+    falling with fewer bits in each slot (thresholds differ per slot)."""
+    out = []
+    for c in configs:
+        bits = [1 + e + m for e, m in c]
+        ok = sum(b >= t for b, t in zip(bits, (9, 5, 4, 5, 6)))
+        out.append({"env_a": ok / 5.0, "env_b": 1.0 if bits[0] >= 9 else 0.5})
+    return out
+
+
+def _search_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_07854_b200.dist import ShardedEvaluator
+        from paper_2310_07854_b200.search import Memo, vapr_search
+        calls = []
+
+        def inner(cs):
+            calls.append(len(cs))
+            return _fake_rates(cs)
+
+        ev = ShardedEvaluator(inner, rank, world)
+        memo = Memo(ev, {"env_a": 0.99, "env_b": 0.99})
+        res = vapr_search(memo, budget=120, pop_size=20, seed=3)
+        q.put((rank, [t.config for t in memo.trials], res["best"].config, res["minima"],
+               ev.local_evaluations, sum(calls)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_search_candidates_sharded_over_ranks():
+    """The same search on 2 ranks (each evaluating every other candidate, the
+    fitness all-gathered) visits the same trials in the same order and returns
+    the same result as one process; the evaluations split between the ranks."""
+    from paper_2310_07854_b200.search import Memo, vapr_search
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_search_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    memo = Memo(_fake_rates, {"env_a": 0.99, "env_b": 0.99})
+    ref = vapr_search(memo, budget=120, pop_size=20, seed=3)
+    ref_trials = [t.config for t in memo.trials]
+    for rank, trials, best, minima, local, called in res:
+        assert trials == ref_trials
+        assert best == ref["best"].config and minima == ref["minima"]
+        assert local == called
+    total = sum(r[4] for r in res)
+    assert total == len(ref_trials)
+    assert abs(res[0][4] - res[1][4]) <= len(ref_trials) // 4 + 8   # roughly half each
