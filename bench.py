@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true",
                     help="skip the end-to-end leg (profiling runs: keeps the launch list to the device step)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph legs")
     ap.add_argument("--cpu-sample-poses", type=int, default=20480)
     return ap.parse_args()
 
@@ -318,6 +319,21 @@ def main():
                 "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
                 "kernel_frac": {n: round(sb[n] * P / (kms[n] * 1e-3) / 1e9 / hbm, 4) for n in names}}
 
+    # ---- the step as a CUDA graph (SURVEY.md §8(d) timing protocol), on the
+    # bench workload and on the launch-bound config 2 (eager vs graph)
+    graph = None
+    if not args.no_graph:
+        from workloads import config2
+        g = r.capture_graph()
+        graph = {"ms_per_step": timed(g.replay, args.steps, args.warmup)}
+        del g
+        r2 = Rollout(config2(), device=local, sparse=sparse)
+        g2 = r2.capture_graph()
+        graph["config2_eager_us"] = 1e3 * timed(r2.run, 50, 10)
+        graph["config2_graph_us"] = 1e3 * timed(g2.replay, 50, 10)
+        del g2, r2
+        torch.cuda.empty_cache()
+
     # ---- end to end through the public API with host buffers
     q_host = torch.from_numpy(np.ascontiguousarray(wl.q)).pin_memory()
     gq_host = torch.empty(P * 7, dtype=torch.float32).pin_memory()
@@ -421,6 +437,7 @@ def main():
             "bytes_per_pose_alg": a_min,
             "roofline": roofline,
             "e2e": e2e,
+            "graph": graph,
             "fp32": fp32,
             "to_iteration": to_iter,
             "iko": iko,

@@ -93,6 +93,22 @@ class Rollout:
                           self.workspace, self.cost_pose, self.cost_traj, self.grad_q,
                           stream=stream, _p=self._p)
 
+    def capture_graph(self, warmup=2):
+        """vapr_cost_grad captured in a CUDA graph (SURVEY.md §8(d) timing
+        protocol; launch-bound small batches): replay() re-runs it on the
+        buffers' current contents (update q in place between replays)."""
+        import torch
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.run()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        return g
+
     def run_host(self, q_host, grad_q_host, cost_traj_host=None, n_chunks=0, stream=None):
         """End to end from host buffers: q_host [B, H, 7] float32 in, grad_q_host
         [B, H, 7] (and cost_traj_host [B]) out, copies pipelined against the
