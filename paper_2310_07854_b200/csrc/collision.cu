@@ -488,8 +488,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         }
         const long long p0 = tile * kTP;
         const int np = (int)min((long long)kTP, P - p0);
-        const long long r_lo = max(p0 - 1, 0LL);
-        const long long r_hi = min(p0 + kTP + 1, P);      // exclusive
+        // halo rows p0 - 1 and p0 + 15 only for the swept world pass (the
+        // segments that cross the tile edges); self and discrete need none
+        const long long r_lo = swept ? max(p0 - 1, 0LL) : p0;
+        const long long r_hi = swept ? min(p0 + kTP + 1, P) : p0 + np;   // exclusive
         const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
         // the lane's pose p0 + lane = tile row lane + 1 (lane 31: the halo
         // pose, used only for the segment that ends there)
