@@ -12,6 +12,8 @@ readings:
        applied at p and the torque tau = -2 w_rot sum_k r_k x g_k (r_k, g_k the
        columns of R, R_g): dR = [w]x R for a rotation w, and
        <R - R_g, [w]x R> = w . sum_k r_k x (r_k - g_k);
+  c43  ee_pose: the hand frame as position + unit quaternion (w, x, y, z), the
+       one with w >= 0 (`ee_pose`);
   c36  bound cost  C = w_b sum_j (max(0, q_j - q_hi_j)^2 + max(0, q_lo_j - q_j)^2),
        gradient 2 w_b (max(0, q_j - q_hi_j) - max(0, q_lo_j - q_j)).
 
@@ -27,6 +29,47 @@ def hand_pose(q, robot):
     """q [P, 7] -> (R [P, 3, 3], p [P, 3]) of the hand frame (c34)."""
     F = link_frames(q, robot)
     return F[:, 8, :3, :3], F[:, 8, :3, 3]
+
+
+def quat_from_matrix(R):
+    """R [P, 3, 3] -> unit quaternions [P, 4] = (w, x, y, z), w >= 0 (reading
+    c43: the canonical one of the two).  Shepperd's method: the largest of
+    1 + tr, 1 + 2 R_ii - tr gives the well-conditioned component."""
+    R = np.asarray(R, np.float64).reshape(-1, 3, 3)
+    out = np.zeros((R.shape[0], 4))
+    for n, m in enumerate(R):
+        tr = m[0, 0] + m[1, 1] + m[2, 2]
+        if tr > 0:
+            s = 2.0 * np.sqrt(1.0 + tr)
+            w, x, y, z = 0.25 * s, (m[2, 1] - m[1, 2]) / s, (m[0, 2] - m[2, 0]) / s, (m[1, 0] - m[0, 1]) / s
+        elif m[0, 0] > m[1, 1] and m[0, 0] > m[2, 2]:
+            s = 2.0 * np.sqrt(1.0 + m[0, 0] - m[1, 1] - m[2, 2])
+            w, x, y, z = (m[2, 1] - m[1, 2]) / s, 0.25 * s, (m[0, 1] + m[1, 0]) / s, (m[0, 2] + m[2, 0]) / s
+        elif m[1, 1] > m[2, 2]:
+            s = 2.0 * np.sqrt(1.0 + m[1, 1] - m[0, 0] - m[2, 2])
+            w, x, y, z = (m[0, 2] - m[2, 0]) / s, (m[0, 1] + m[1, 0]) / s, 0.25 * s, (m[1, 2] + m[2, 1]) / s
+        else:
+            s = 2.0 * np.sqrt(1.0 + m[2, 2] - m[0, 0] - m[1, 1])
+            w, x, y, z = (m[1, 0] - m[0, 1]) / s, (m[0, 2] + m[2, 0]) / s, (m[1, 2] + m[2, 1]) / s, 0.25 * s
+        v = np.array([w, x, y, z])
+        out[n] = -v if w < 0 else v
+    return out
+
+
+def matrix_from_quat(qt):
+    """(w, x, y, z) [P, 4] -> R [P, 3, 3] (the textbook unit-quaternion form)."""
+    w, x, y, z = (np.asarray(qt, np.float64).reshape(-1, 4)[:, k] for k in range(4))
+    return np.stack([
+        np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
+        np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
+        np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)], 1)
+
+
+def ee_pose(q, robot):
+    """vapr_fk_spheres' optional ee_pose: the
+    hand frame (c34) as [P, 7] = (p_x, p_y, p_z, q_w, q_x, q_y, q_z), w >= 0."""
+    R, p = hand_pose(np.asarray(q, np.float64).reshape(-1, 7), robot)
+    return np.concatenate([p, quat_from_matrix(R)], axis=1)
 
 
 def pose_cost(q, robot, goal_R, goal_p, w_pos, w_rot):

@@ -86,3 +86,38 @@ def test_bound_gradient_finite_differences():
         cp, _ = K.bound_cost(q + e, lo, hi, 0.8)
         cm, _ = K.bound_cost(q - e, lo, hi, 0.8)
         np.testing.assert_allclose(g[:, j], (cp - cm) / (2 * h), rtol=1e-5, atol=1e-8)
+
+
+def test_ee_pose_at_zero_closed_form():
+    """q = 0: the flange sits at (0.088, 0, 0.926) with z pointing down
+    (SURVEY.md §8(c) FK pins), i.e. R_flange = diag(1, -1, -1); the hand is
+    the flange turned by hand_rz about its z: R = diag(1,-1,-1) RotZ(hand_rz),
+    whose quaternion is (0, cos(hand_rz/2), -sin(hand_rz/2), 0) up to sign."""
+    e = K.ee_pose(np.zeros((1, 7)), ROBOT)[0]
+    np.testing.assert_allclose(e[:3], [0.088, 0.0, 0.926], atol=1e-3)
+    th = ROBOT["hand_rz"]
+    ref = np.array([0.0, np.cos(th / 2), -np.sin(th / 2), 0.0])
+    assert np.allclose(e[3:], ref, atol=1e-9) or np.allclose(e[3:], -ref, atol=1e-9)
+
+
+def test_quaternion_round_trip_and_branches():
+    """Every Shepperd branch (positive trace, and each diagonal entry the
+    largest): matrix -> quaternion -> matrix is the identity map, the
+    quaternion is unit with w >= 0."""
+    rng = np.random.default_rng(4)
+    Rs = [rot([0, 0, 1], 0.3), rot([1, 0, 0], 3.0), rot([0, 1, 0], 3.0), rot([0, 0, 1], 3.0),
+          rot([1, 1, 0], np.pi), np.eye(3)]
+    Rs += [rot(rng.normal(size=3), rng.uniform(0, np.pi)) for _ in range(50)]
+    R = np.stack(Rs)
+    qt = K.quat_from_matrix(R)
+    np.testing.assert_allclose(np.linalg.norm(qt, axis=1), 1.0, atol=1e-12)
+    assert np.all(qt[:, 0] >= 0)
+    np.testing.assert_allclose(K.matrix_from_quat(qt), R, atol=1e-12)
+
+
+def test_ee_pose_matches_hand_frame():
+    q = rand_q(np.random.default_rng(9), 20)
+    R, p = K.hand_pose(q, ROBOT)
+    e = K.ee_pose(q, ROBOT)
+    np.testing.assert_allclose(e[:, :3], p, atol=0)
+    np.testing.assert_allclose(K.matrix_from_quat(e[:, 3:]), R, atol=1e-12)
