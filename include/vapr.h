@@ -190,9 +190,12 @@ vapr_status vapr_dequantize(vapr_format f, const uint32_t *packed, size_t rows, 
 
 /* ---- a2: forward kinematics -> packed out_spheres ----------------------- */
 /* P:86 (forward kinematics), P:189 ("The output of forward kinematics:
- * out_spheres").  out_spheres [B*H, row_words(fmt[OUT_SPHERES], 3S)]. */
+ * out_spheres").  out_spheres [B*H, row_words(fmt[OUT_SPHERES], 3S)].
+ * ee_pose (nullable, 16-byte aligned): [B*H, 7] FP32 hand frame (reading c34)
+ * as (p_x, p_y, p_z, q_w, q_x, q_y, q_z), the unit quaternion with q_w >= 0
+ * (reading c43). */
 vapr_status vapr_fk_spheres(vapr_ctx *ctx, const float *q, int32_t B, int32_t H,
-                            uint32_t *out_spheres, void *stream);
+                            uint32_t *out_spheres, float *ee_pose, void *stream);
 
 /* ---- a3: world collision ----------------------------------------------- */
 /* P:86, P:189 ("the output of collision cost: closest_pt for IKO and

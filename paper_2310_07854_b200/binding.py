@@ -92,7 +92,7 @@ def _load():
         "vapr_set_option": ([P, I32, I32], I32),
         "vapr_quantize": ([vapr_format, P, SZ, SZ, P, P], I32),
         "vapr_dequantize": ([vapr_format, P, SZ, SZ, P, P], I32),
-        "vapr_fk_spheres": ([P, P, I32, I32, P, P], I32),
+        "vapr_fk_spheres": ([P, P, I32, I32, P, P, P], I32),
         "vapr_world_collision": ([P, P, P, I32, I32, I32, I32, F, F, P, P, P], I32),
         "vapr_self_collision": ([P, P, I32, I32, F, F, P, P, P], I32),
         "vapr_collision": ([P, P, P, I32, I32, ctypes.POINTER(vapr_cost_params), P, P, P, P, P], I32),
@@ -279,8 +279,10 @@ def cost_params(p):
                             float(p.get("w_bound", 0.0)))
 
 
-def vapr_fk_spheres(ctx, q, B, H, out_spheres, stream=None):
-    _check(lib.vapr_fk_spheres(ctx, _ptr(q), B, H, _ptr(out_spheres), _stream(stream)),
+def vapr_fk_spheres(ctx, q, B, H, out_spheres, stream=None, ee_pose=None):
+    """ee_pose (optional): [B*H, 7] float32 hand position + unit quaternion (w >= 0)."""
+    _check(lib.vapr_fk_spheres(ctx, _ptr(q), B, H, _ptr(out_spheres),
+                               _ptr(ee_pose) if ee_pose is not None else None, _stream(stream)),
            "vapr_fk_spheres")
 
 

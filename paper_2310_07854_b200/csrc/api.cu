@@ -599,15 +599,16 @@ vapr_status vapr_dequantize(vapr_format f, const uint32_t* packed, size_t rows, 
 
 // ---- a2 ------------------------------------------------------------------
 vapr_status vapr_fk_spheres(vapr_ctx* c, const float* q, int32_t B, int32_t H,
-                            uint32_t* out_spheres, void* stream) {
+                            uint32_t* out_spheres, float* ee_pose, void* stream) {
     CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
     CHECK(c->robot_set, VAPR_ERR_NOT_INITIALIZED);
     CHECK(B >= 1 && H >= 1, VAPR_ERR_SHAPE);
     CHECK(q && out_spheres && aligned16(q) && aligned16(out_spheres), VAPR_ERR_INVALID_ARG);
     DeviceGuard g(c->device);
     CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
+    CHECK(ee_pose == nullptr || aligned16(ee_pose), VAPR_ERR_INVALID_ARG);
     return cuda_status(launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], q, (long long)B * H,
-                                 out_spheres, (cudaStream_t)stream));
+                                 out_spheres, (cudaStream_t)stream, nullptr, ee_pose));
 }
 
 // ---- a3 / a4 -------------------------------------------------------------

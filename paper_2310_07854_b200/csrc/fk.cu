@@ -78,10 +78,38 @@ struct EmitterF16 {
     }
 };
 
-template <bool IKO>
+// ee_pose (reading c43): the hand frame as position +
+// unit quaternion (w, x, y, z) with w >= 0, Shepperd's method (the largest of
+// 1 + tr, 1 + 2 R_ii - tr picks the well-conditioned component).  X.r is
+// row-major.
+__device__ __forceinline__ void hand_ee_pose(const Xf& X, float* e) {
+    const float* m = X.r;
+    const float tr = m[0] + m[4] + m[8];
+    float w, x, y, z;
+    if (tr > 0.f) {
+        const float s = 2.f * sqrtf(1.f + tr);
+        w = 0.25f * s; x = (m[7] - m[5]) / s; y = (m[2] - m[6]) / s; z = (m[3] - m[1]) / s;
+    } else if (m[0] > m[4] && m[0] > m[8]) {
+        const float s = 2.f * sqrtf(1.f + m[0] - m[4] - m[8]);
+        w = (m[7] - m[5]) / s; x = 0.25f * s; y = (m[1] + m[3]) / s; z = (m[2] + m[6]) / s;
+    } else if (m[4] > m[8]) {
+        const float s = 2.f * sqrtf(1.f + m[4] - m[0] - m[8]);
+        w = (m[2] - m[6]) / s; x = (m[1] + m[3]) / s; y = 0.25f * s; z = (m[5] + m[7]) / s;
+    } else {
+        const float s = 2.f * sqrtf(1.f + m[8] - m[0] - m[4]);
+        w = (m[3] - m[1]) / s; x = (m[2] + m[6]) / s; y = (m[5] + m[7]) / s; z = 0.25f * s;
+    }
+    const float sg = (w < 0.f) ? -1.f : 1.f;
+    e[0] = X.p[0]; e[1] = X.p[1]; e[2] = X.p[2];
+    e[3] = sg * w; e[4] = sg * x; e[5] = sg * y; e[6] = sg * z;
+}
+
+// EE: also write ee_pose -- its own instantiation (the common one keeps its registers)
+template <bool IKO, bool EE>
 __global__ void __launch_bounds__(kTile)
 fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
-          long long P, int W, uint32_t* __restrict__ os, uint32_t rq, const IkArgs ik) {
+          long long P, int W, uint32_t* __restrict__ os, uint32_t rq, const IkArgs ik,
+          float* __restrict__ ee) {
     extern __shared__ uint32_t smem[];
     const int WS = W + 1;
     float* sq = reinterpret_cast<float*>(smem);    // [kTile * 7]
@@ -104,6 +132,7 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 if (l >= 1 && l <= kJoints) fk_step(X, R, l - 1, sq[tid * kJoints + l - 1]);
                 if (l == kLinks - 1) {
                     fk_hand(X, R);
+                    if constexpr (EE) hand_ee_pose(X, ee + (p0 + tid) * 7);
                     if constexpr (IKO) {   // N2: pose + bound cost of this pose -> cost_pose
                         float c = 0.f, F[3], tau[3];
                         const long long pg = p0 + tid;
@@ -162,12 +191,13 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 }  // namespace
 
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
-                      uint32_t* os, cudaStream_t s, const IkArgs* ik) {
+                      uint32_t* os, cudaStream_t s, const IkArgs* ik, float* ee) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fos, R.cols);
     const size_t smem = sizeof(float) * kTile * kJoints + sizeof(uint32_t) * kTile * (W + 1);
     const bool iko = ik && ik_on(*ik);
-    auto kern = iko ? fk_kernel<true> : fk_kernel<false>;
+    auto kern = iko ? (ee ? fk_kernel<true, true> : fk_kernel<true, false>)
+                    : (ee ? fk_kernel<false, true> : fk_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -177,7 +207,7 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
 #ifdef VAPR_DEBUG_TAP
     const bool tapped = tap_arm(0, P, R.cols, s) != nullptr;
 #endif
-    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq, iko ? *ik : none);
+    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq, iko ? *ik : none, ee);
 #ifdef VAPR_DEBUG_TAP
     if (tapped) tap_disarm(0, s);
 #endif

@@ -55,8 +55,10 @@ struct IkArgs {
 };
 inline bool ik_on(const IkArgs& k) { return k.w_pos != 0.f || k.w_rot != 0.f || k.w_bound != 0.f; }
 
+// ee (nullable): [P, 7] hand position + unit quaternion (w >= 0)
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
-                      uint32_t* os, cudaStream_t s, const IkArgs* ik = nullptr);
+                      uint32_t* os, cudaStream_t s, const IkArgs* ik = nullptr,
+                      float* ee = nullptr);
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                              unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);

@@ -135,3 +135,31 @@ def test_set_goals_errors(vb):
             vb._check(vb.lib.vapr_set_goals(h, None, -1), "negative")
     finally:
         vb.vapr_destroy(h)
+
+
+@pytest.mark.parametrize("fmt", ["43bit", "fp32"])
+def test_fk_ee_pose_matches_oracle(vb, fmt):
+    """vapr_fk_spheres' optional ee_pose (reading c43)
+    against oracle/ikcost.ee_pose: positions within FP32 evaluation error,
+    the quaternion unit with w >= 0 and its rotation equal to the oracle's
+    (compared as matrices: q and -q are the same rotation when w ~ 0); the
+    packed out_spheres are unchanged by asking for it."""
+    from paper_2310_07854_b200.rollout import Rollout
+    wl = config_iko(problems_per_env=2, seeds=64, formats=fmt)
+    r = Rollout(wl)
+    P = wl.poses
+    W = vb.vapr_packed_row_words(r.ctx.formats[0], 156)
+    os_a = torch.zeros(P * W, dtype=torch.int32, device="cuda")
+    os_b = torch.zeros(P * W, dtype=torch.int32, device="cuda")
+    ee = torch.full((P * 7,), float("nan"), dtype=torch.float32, device="cuda")
+    vb.vapr_fk_spheres(r.ctx.h, r.q, wl.B, wl.H, os_a)
+    vb.vapr_fk_spheres(r.ctx.h, r.q, wl.B, wl.H, os_b, ee_pose=ee)
+    torch.cuda.synchronize()
+    assert torch.equal(os_a, os_b)
+    got = ee.cpu().numpy().reshape(P, 7).astype(np.float64)
+    ref = K.ee_pose(wl.q.reshape(-1, 7), wl.robot)
+    np.testing.assert_allclose(got[:, :3], ref[:, :3], atol=2e-5)
+    np.testing.assert_allclose(np.linalg.norm(got[:, 3:], axis=1), 1.0, atol=2e-6)
+    assert np.all(got[:, 3] >= 0)
+    np.testing.assert_allclose(K.matrix_from_quat(got[:, 3:]), K.matrix_from_quat(ref[:, 3:]),
+                               atol=2e-5)
