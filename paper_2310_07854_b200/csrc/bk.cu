@@ -34,11 +34,15 @@ constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
 // IKO: the N2 pose / bound terms; SP: the gradient slot is IEEE E5M10 (its
 // exponent-31 codes decode to inf / NaN, reading c41) -- a separate
 // instantiation so the common ones carry no fixup.
-#ifndef VAPR_BK_MINB
-#define VAPR_BK_MINB 1
+// VAPR_BK_MINB (tuning knob): minimum resident CTAs per SM; unset = the plain
+// bound (an explicit 1 lets ptxas use ~150 registers and is slower)
+#ifdef VAPR_BK_MINB
+#define VAPR_BK_BOUNDS __launch_bounds__(kTile, VAPR_BK_MINB)
+#else
+#define VAPR_BK_BOUNDS __launch_bounds__(kTile)
 #endif
 template <bool IKO, bool SP, bool SPR>
-__global__ void __launch_bounds__(kTile, VAPR_BK_MINB)
+__global__ void VAPR_BK_BOUNDS
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
           uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik,
