@@ -259,6 +259,22 @@ def main():
     clocks = clk.summary()
     value = world * P * S / (ms * 1e-3)
 
+    # measured sparsity of the gradient tensors ("report the
+    # measured nonzero fraction per run"; PAPER.md:196 >99 % zeros), from the
+    # sparse mode's per-pose sphere bitmaps of the last step
+    sparsity = None
+    if sparse:
+        offs, _ = vb.vapr_cost_grad_sparse_layout(r.ctx.h, wl.B, wl.H)
+        names_m = {"grad_out_spheres": offs[0], "closest_pt_swept": offs[4], "out_vec": offs[5]}
+        sparsity = {}
+        for nm, o in names_m.items():
+            m = r.workspace[o:o + 8 * P].view(torch.int64)
+            bits = torch.zeros(P, dtype=torch.int64, device=dev)
+            for k in range(S):
+                bits += (m >> k) & 1
+            sparsity[nm] = {"nonzero_sphere_frac": round(float(bits.sum()) / (P * S), 5),
+                            "nonzero_pose_frac": round(float((bits > 0).sum()) / P, 4)}
+
     # ---- per-kernel durations (the stage entry points, launched stage by
     # stage on the same stream with events between them; dense storage: the
     # standalone calls take dense tensors) for the roofline of the dominant one
@@ -438,6 +454,7 @@ def main():
             "roofline": roofline,
             "e2e": e2e,
             "graph": graph,
+            "sparsity": sparsity,
             "fp32": fp32,
             "to_iteration": to_iter,
             "iko": iko,

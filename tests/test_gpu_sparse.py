@@ -278,3 +278,15 @@ def test_sparse_bytes_below_dense(vb):
     sparse = 12 * P + 4 * sg["used"]
     assert sparse == osp.sparse_bytes(sg["mask"], *b.ctx.formats[1])
     assert sparse < dense / 3
+
+
+def test_cost_grad_sparse_ieee_formats(vb):
+    """Sparse storage with IEEE E5M10 slots (c41; BK's SP + SPR
+    instantiation): bit-identical to the dense mode with the same formats."""
+    from oracle.codec import FMT_IEEE
+    wl = config4(problems_per_env=1, seeds=6, H=32, formats="fp16")
+    wl = dataclasses.replace(wl, formats=((5, 10 | FMT_IEEE),) * 5)
+    a, b = run_pair(wl)
+    ra, rb = a.results(), b.results()
+    for k in ("cost_pose", "cost_traj", "grad_q"):
+        assert np.array_equal(ra[k].view(np.uint32), rb[k].view(np.uint32)), k
