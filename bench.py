@@ -329,9 +329,18 @@ def main():
     if rd is not r:
         del rd, ws
         torch.cuda.empty_cache()
+    issue = None
+    try:        # the dominant kernel is issue-bound: its ncu issue utilisation
+        ij = json.load(open(os.path.join(ROOT, "profiles", "r1", "issue.json")))
+        issue = ij.get(dom)
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "stage_calls": "dense standalone entry points", "achieved": achieved, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "bytes_per_launch_alg": sb[dom] * P, "bytes_per_pose": sb[dom],
+                "limiter": ("instruction issue (ncu, profiles/r1/issue.json); HBM frac is low "
+                            "because the collision passes spend ~10x more issue slots than bytes"),
+                "issue": issue,
                 "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
                 "kernel_frac": {n: round(sb[n] * P / (kms[n] * 1e-3) / 1e9 / hbm, 4) for n in names}}
 
