@@ -290,3 +290,33 @@ def test_cost_grad_sparse_ieee_formats(vb):
     ra, rb = a.results(), b.results()
     for k in ("cost_pose", "cost_traj", "grad_q"):
         assert np.array_equal(ra[k].view(np.uint32), rb[k].view(np.uint32)), k
+
+
+@pytest.mark.parametrize("case", ["ragged", "edge_worlds", "discrete_h1", "no_contact"])
+def test_cost_grad_sparse_edge_cases(vb, case):
+    """Sparse storage on the parity suite's edge workloads: ragged B x H (rows
+    not a multiple of the 16-row tiles), obstacle-dense edge worlds, the
+    discrete H = 1 workload (closest_pt, slot 3), and a batch with no contact
+    at all (every bitmap empty, no pool words)."""
+    from test_gpu_parity import edge_worlds_workload, ragged_workload
+    if case == "ragged":
+        wl = ragged_workload()
+    elif case == "edge_worlds":
+        wl = edge_worlds_workload()
+    elif case == "discrete_h1":
+        wl = config_iko(problems_per_env=1, seeds=40, formats="43bit")
+        p = dict(wl.params)
+        p.update(w_pose_pos=0.0, w_pose_rot=0.0, w_bound=0.0)
+        wl = dataclasses.replace(wl, params=p)
+    else:
+        wl = config4(problems_per_env=1, seeds=4, H=8, formats="43bit")
+        cub = wl.cuboids.copy()
+        cub[:, 9:12] += 100.0                 # every obstacle far away
+        p = dict(wl.params)
+        p.update(w_self=0.0)
+        wl = dataclasses.replace(wl, cuboids=cub, params=p)
+    a, b = run_pair(wl)
+    check_pair(wl, a, b)
+    if case == "no_contact":
+        sg = b.sparse_gos()
+        assert sg["used"] == 0 and not sg["mask"].any()
