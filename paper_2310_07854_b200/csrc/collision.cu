@@ -986,6 +986,9 @@ extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
 }
 #endif
 
+#ifndef VAPR_SPREAD_SMALL
+#define VAPR_SPREAD_SMALL 1
+#endif
 cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                                   const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                                   cudaStream_t s) {
@@ -1008,7 +1011,12 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nw, smem);
     const long long tiles = (P + kTP - 1) / kTP;
-    const long long grid = std::min<long long>((tiles + kGrab * nw - 1) / (kGrab * nw),
+    // enough CTAs for every warp to have a chunk; small batches: spread up to
+    // one CTA per tile over the SMs (latency: a lone SM's issue slots shared
+    // by its 16 warps would serialise the few tiles there are)
+    const long long need = (tiles + kGrab * nw - 1) / (kGrab * nw);
+    const long long spread = VAPR_SPREAD_SMALL ? std::min<long long>(tiles, sms) : need;
+    const long long grid = std::min<long long>(std::max(need, spread),
                                                (long long)sms * std::max(per_sm, 1));
 #ifdef VAPR_DEBUG_TAP
     const int tw = a.swept ? 4 : 3;
