@@ -544,9 +544,12 @@ vapr_status vapr_sparsify(vapr_format f, const uint32_t* packed, size_t rows, si
     CHECK(sparse_pool_words_of(F, (int)cols, (long long)rows) <= 0xFFFFFFFFull, VAPR_ERR_SHAPE);
     CHECK(rows == 0 || (packed && mask && off && pool), VAPR_ERR_INVALID_ARG);
     CHECK(aligned16(packed) && (reinterpret_cast<uintptr_t>(mask) & 7u) == 0, VAPR_ERR_INVALID_ARG);
-    return cuda_status(launch_sparsify(F, packed, (long long)rows, (int)cols,
-                                       SparseOut{reinterpret_cast<unsigned long long*>(mask), off,
-                                                 pool, used},
+    SparseOut o{};
+    o.mask = reinterpret_cast<unsigned long long*>(mask);
+    o.off = off;
+    o.pool = pool;
+    o.used = used;
+    return cuda_status(launch_sparsify(F, packed, (long long)rows, (int)cols, o,
                                        (cudaStream_t)stream));
 }
 
