@@ -756,6 +756,7 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
     }
     *cost_off = o;
     o = align256(o + sizeof(float) * (size_t)P);
+    o = align256(o + sizeof(float) * (size_t)P);     // the self pass's cost (after cost_off)
     *total = o;
 }
 
@@ -813,6 +814,7 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     SparseOut spo{};
     SparseIn spi{};
     unsigned long long *cp_mask = nullptr, *ov_mask = nullptr;
+    float* self_cost = nullptr;
     if (c->sparse) {
         size_t so[kSparseOffs], pw, o2[VAPR_NUM_SLOTS], co2, tot2;
         ws_layout(c, (long long)B * H, p->swept, o2, &co2, &tot2, so, &pw);
@@ -861,10 +863,18 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.cost_accumulate = iko ? 1 : 0;
         a.cp_mask = cp_mask;
         a.ov_mask = ov_mask;
+        {   // the self pass's separate cost (workspace, after the scratch cost_pose)
+            size_t o3[VAPR_NUM_SLOTS], co3, tot3;
+            ws_layout(c, (long long)B * H, p->swept, o3, &co3, &tot3);
+            self_cost = reinterpret_cast<float*>(ws + align256(co3 + sizeof(float) * (size_t)B * H)) + p0;
+        }
+        a.self_cost = self_cost;
         e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
                              c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
-    if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cpose + p0, nb, H, cost_traj + b0, s);
+    // combines the self pass's cost into cost_pose (always) and sums cost_traj
+    if (e == cudaSuccess)
+        e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost);
     if (e == cudaSuccess)
         e = c->sparse ? launch_aggregate_masked(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,

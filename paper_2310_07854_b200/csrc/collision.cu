@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
+    // programmatic dependent launch (vapr_cost_grad): the world pass lets the
+    // self pass launch at once, so its CTAs take SMs as world CTAs retire
+    if (a.pdl == 1) asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
     float* ssr = reinterpret_cast<float*>(base + G.sr);
@@ -944,15 +947,25 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             __threadfence();
         }
     }
+    // the self pass completes only after the world pass: stream-ordered work
+    // after it (aggregation, BK) sees both passes' outputs
+    if (a.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-__global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
-                                   float* __restrict__ cost_traj) {
+__global__ void traj_reduce_kernel(float* __restrict__ cost_pose, int B, int H,
+                                   float* __restrict__ cost_traj, const float* __restrict__ add) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     float c = 0.f;
-    for (int h = 0; h < H; ++h) c += cost_pose[(long long)b * H + h];
-    cost_traj[b] = c;
+    for (int h = 0; h < H; ++h) {
+        float v = cost_pose[(long long)b * H + h];
+        if (add) {                      // world (+ IKO) then self: the fused order
+            v = v + add[(long long)b * H + h];
+            cost_pose[(long long)b * H + h] = v;
+        }
+        c += v;
+    }
+    if (cost_traj) cost_traj[b] = c;
 }
 
 __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems, int seeds,
@@ -989,6 +1002,9 @@ extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
 #ifndef VAPR_SPREAD_SMALL
 #define VAPR_SPREAD_SMALL 1
 #endif
+#ifndef VAPR_PDL
+#define VAPR_PDL 1
+#endif
 cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                                   const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                                   cudaStream_t s) {
@@ -1023,7 +1039,22 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const bool tap_w = a.do_world && tap_arm(tw, P, R.cols, s);
     const bool tap_s = a.do_self && tap_arm(2, P, R.cols, s);
 #endif
-    kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
+    if (a.pdl == 2) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(32 * nw);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, R, G, W, fos, fcp, fov, a);
+        if (e != cudaSuccess) return e;
+    } else {
+        kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
+    }
 #ifdef VAPR_DEBUG_TAP
     if (tap_w) tap_disarm(tw, s);
     if (tap_s) tap_disarm(2, s);
@@ -1056,15 +1087,23 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     aw.do_self = 0;
     as.do_world = 0;
     as.cost_accumulate = 1;
+    if (VAPR_PDL && a.self_cost) {
+        // the self pass writes its own cost and may start while the world
+        // pass's last tiles run (it reads only out_spheres)
+        as.cost = a.self_cost;
+        as.cost_accumulate = 0;
+        aw.pdl = 1;
+        as.pdl = 2;
+    }
     cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, aw, s);
     if (e != cudaSuccess) return e;
     return launch_collision_pass(R, W, fos, fcp, fov, as, s);
 }
 
-cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s) {
+cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
+                               cudaStream_t s, const float* add) {
     if (B <= 0) return cudaSuccess;
-    traj_reduce_kernel<<<(B + 255) / 256, 256, 0, s>>>(cost_pose, B, H, cost_traj);
+    traj_reduce_kernel<<<(B + 255) / 256, 256, 0, s>>>(cost_pose, B, H, cost_traj, add);
     return cudaGetLastError();
 }
 

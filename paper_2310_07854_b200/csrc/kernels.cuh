@@ -34,6 +34,11 @@ struct CollisionArgs {
     // fields of set spheres.
     unsigned long long* cp_mask;
     unsigned long long* ov_mask;
+    // vapr_cost_grad (nullable): the self pass writes its cost here and
+    // traj_reduce adds it, so the self pass may overlap the world pass's tail
+    // (programmatic dependent launch); the order of the sums is unchanged
+    float* self_cost;
+    int32_t pdl;              // internal: 1 = trigger dependents at start, 2 = wait at exit
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
     unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero
 };
@@ -63,8 +68,10 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                              unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);
 constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight collision passes)
-cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s);
+// add (nullable): cost_pose += add first (the self pass's separate cost);
+// cost_traj (nullable): the per-trajectory sums
+cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
+                               cudaStream_t s, const float* add = nullptr);
 // N3 sparse form of a sphere tensor (include/vapr.h "N3"; sparse.cuh)
 struct SparseOut {
     unsigned long long* mask;  // [rows] (the caller offsets it to the first row)
