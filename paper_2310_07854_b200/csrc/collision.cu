@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
-    // programmatic dependent launch (vapr_cost_grad): the world pass lets the
-    // self pass launch at once, so its CTAs take SMs as world CTAs retire
+    // programmatic dependent launch (vapr_cost_grad): the first pass lets the
+    // second launch at once, so its CTAs take SMs as the first's retire
     if (a.pdl == 1) asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
@@ -947,7 +947,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             __threadfence();
         }
     }
-    // the self pass completes only after the world pass: stream-ordered work
+    // the second pass completes only after the first: stream-ordered work
     // after it (aggregation, BK) sees both passes' outputs
     if (a.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -1088,12 +1088,16 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     as.do_world = 0;
     as.cost_accumulate = 1;
     if (VAPR_PDL && a.self_cost) {
-        // the self pass writes its own cost and may start while the world
-        // pass's last tiles run (it reads only out_spheres)
+        // the self pass writes its own cost, so neither pass depends on the
+        // other (both read only out_spheres): the self pass (the longer tail)
+        // runs first and the world pass starts on the SMs its CTAs leave
         as.cost = a.self_cost;
         as.cost_accumulate = 0;
-        aw.pdl = 1;
-        as.pdl = 2;
+        as.pdl = 1;
+        aw.pdl = 2;
+        cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, as, s);
+        if (e != cudaSuccess) return e;
+        return launch_collision_pass(R, W, fos, fcp, fov, aw, s);
     }
     cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, aw, s);
     if (e != cudaSuccess) return e;
