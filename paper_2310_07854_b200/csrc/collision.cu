@@ -1062,9 +1062,12 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     return cudaGetLastError();
 }
 
-// World and self run as two passes over the tile rows (the second adds its
-// cost to the first's, i.e. the same wcost + scost): each pass keeps a
-// smaller instruction working set, which beats re-reading out_spheres.
+// World and self run as two passes over the tile rows: each pass keeps a
+// smaller instruction working set, which beats re-reading out_spheres.  With
+// a0.self_cost (vapr_cost_grad) the self pass runs first into its own cost
+// array and the world pass is its programmatic dependent launch (traj_reduce
+// adds the two in the fused order); otherwise world first, the self pass
+// adding its cost to the world pass's (the same wcost + scost).
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a0,
                              unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s) {
