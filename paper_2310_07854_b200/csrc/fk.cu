@@ -8,13 +8,15 @@
 // buffer (PF = codes per word, a compile-time constant via with_pf; the
 // element count is warp-uniform, so there is no divergence) and every full
 // buffer is encoded into one packed word (hardware cvt fast path for
-// E5M10 / E8M7 / FP8 / FP6 / FP4) and stored into the pose's shared row
-// (stride W+1 words, odd, so the 32 lanes -- 32 poses writing the same word
-// index -- hit 32 distinct banks).  The CTA then streams its tile of packed
-// rows to HBM with coalesced stores.  Link frames are NOT written to memory:
-// backward kinematics recomputes them, so HBM sees q
-// (28 B/pose) in and out_spheres out, and shared memory holds only the packed
-// rows (W words per pose), which keeps 5 CTAs (20 warps) per SM at 16 bits.
+// E5M10 / E8M7 / FP8 / FP6 / FP4).  Each warp stages its 32 rows 16 words
+// at a time in a small shared chunk (stride 17 words, odd, so the 32 lanes --
+// 32 poses writing the same word index -- hit 32 distinct banks); every full
+// chunk is streamed to HBM at once, four lanes per pose writing its 64
+// contiguous bytes (two whole sectors) with 16-byte stores.  Shared memory per
+// warp is a fixed 2.2 KB whatever the row width, so occupancy is set by
+// registers, not by a staged row tile.  Link frames are NOT written to
+// memory: backward kinematics recomputes them, so HBM sees q
+// (28 B/pose) in and out_spheres out.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tap.cuh"
@@ -24,27 +26,65 @@ namespace vapr {
 namespace {
 
 constexpr int kTile = 128;   // poses (= threads) per CTA
+#ifndef VAPR_FK_MINB             // resident CTAs per SM the register budget targets
+#define VAPR_FK_MINB 10
+#endif
+
+constexpr int kChunk = 16;          // words per pose per warp flush
+constexpr int kCS = kChunk + 1;      // chunk row stride (odd: conflict-free lane writes)
+
+// A warp's rows, kChunk words at a time: put() is warp-uniform (every pose
+// has the same word sequence), a full chunk goes to HBM as 64-byte segments
+// per pose (lane = 4 pose + part), poses >= np are computed but not stored.
+struct RowStore {
+    uint32_t* buf;                   // this warp's [32][kCS] chunk
+    uint32_t* os;                    // the warp's first row in HBM
+    int W, np, lane;
+    int n = 0, chunk = 0;
+    __device__ __forceinline__ void put(uint32_t v) {
+        buf[lane * kCS + n] = v;
+        if (++n == kChunk) drain();
+    }
+    __device__ __forceinline__ void drain() {
+        __syncwarp();
+        const int parts = n >> 2;    // n is a multiple of 4 (rows are 16-byte multiples)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = k * 32 + lane, p = i >> 2, part = i & 3;
+            if (p < np && part < parts) {
+                const uint32_t* src = buf + p * kCS + 4 * part;
+                __stcs(reinterpret_cast<uint4*>(os + (long long)p * W + chunk * kChunk + 4 * part),
+                       make_uint4(src[0], src[1], src[2], src[3]));
+            }
+        }
+        __syncwarp();
+        n = 0;
+        ++chunk;
+    }
+};
 
 template <int PF>
 struct Emitter {
     float buf[PF];
     int count = 0;
     int word = 0;
-    __device__ __forceinline__ void push(float v, uint32_t* row, const Fmt& f) {
+    __device__ __forceinline__ void push(float v, RowStore& row, const Fmt& f) {
 #pragma unroll
         for (int j = 0; j < PF - 1; ++j) buf[j] = buf[j + 1];
         buf[PF - 1] = v;
         if (++count == PF) {
-            row[word++] = encode_word_t<PF>(buf, f);
+            row.put(encode_word_t<PF>(buf, f));
+            ++word;
             count = 0;
         }
     }
-    __device__ __forceinline__ void flush(uint32_t* row, int W, const Fmt& f) {
+    __device__ __forceinline__ void flush(RowStore& row, int W, const Fmt& f) {
         if (count) {                                // the tail of the last word is +0
             const int pad = PF - count;
             for (int k = 0; k < pad; ++k) push(0.f, row, f);
         }
-        for (; word < W; ++word) row[word] = 0u;    // 16-byte row padding
+        for (; word < W; ++word) row.put(0u);      // 16-byte row padding
+        if (row.n) row.drain();
     }
 };
 
@@ -62,19 +102,25 @@ struct EmitterF16 {
         const float x[2] = {a, b};
         return encode_word_t<2>(x, f);
     }
-    __device__ __forceinline__ void sphere(float x, float y, float z, uint32_t* row, const Fmt& f) {
+    __device__ __forceinline__ void sphere(float x, float y, float z, RowStore& row, const Fmt& f) {
         if (!odd) {
-            row[word++] = enc2(x, y, f);
+            row.put(enc2(x, y, f));
+            ++word;
             buf = z;
         } else {
-            row[word++] = enc2(buf, x, f);
-            row[word++] = enc2(y, z, f);
+            row.put(enc2(buf, x, f));
+            row.put(enc2(y, z, f));
+            word += 2;
         }
         odd = !odd;
     }
-    __device__ __forceinline__ void flush(uint32_t* row, int W, const Fmt& f) {
-        if (odd) row[word++] = enc2(buf, 0.f, f);
-        for (; word < W; ++word) row[word] = 0u;
+    __device__ __forceinline__ void flush(RowStore& row, int W, const Fmt& f) {
+        if (odd) {
+            row.put(enc2(buf, 0.f, f));
+            ++word;
+        }
+        for (; word < W; ++word) row.put(0u);
+        if (row.n) row.drain();
     }
 };
 
@@ -106,23 +152,24 @@ __device__ __forceinline__ void hand_ee_pose(const Xf& X, float* e) {
 
 // EE: also write ee_pose -- its own instantiation (the common one keeps its registers)
 template <bool IKO, bool EE>
-__global__ void __launch_bounds__(kTile)
+__global__ void __launch_bounds__(kTile, VAPR_FK_MINB)
 fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
-          long long P, int W, uint32_t* __restrict__ os, uint32_t rq, const IkArgs ik,
+          long long P, int W, uint32_t* __restrict__ os, const IkArgs ik,
           float* __restrict__ ee) {
-    extern __shared__ uint32_t smem[];
-    const int WS = W + 1;
-    float* sq = reinterpret_cast<float*>(smem);    // [kTile * 7]
-    uint32_t* sw = smem + kTile * kJoints;         // [kTile * WS]
+    __shared__ float sq[kTile * kJoints];
+    __shared__ uint32_t sw[kTile * kCS];
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w0 = tid & ~31;
+    const bool valid = tid < np;
 
-    for (int i = tid; i < np * kJoints; i += kTile) sq[i] = __ldcs(q + p0 * kJoints + i);
+    // poses past the end walk q = 0 (every lane takes part in the chunk drains)
+    for (int i = tid; i < kTile * kJoints; i += kTile)
+        sq[i] = (i < np * kJoints) ? __ldcs(q + p0 * kJoints + i) : 0.f;
     __syncthreads();
 
-    if (tid < np) {
-        uint32_t* row = sw + tid * WS;
+    if (w0 < np) {
+        RowStore row{sw + w0 * kCS, os + (p0 + w0) * W, W, np - w0, lane};
         // the chain, the IKO terms at the hand, and every sphere centre handed
         // to `emit(x, y, z)` in sphere order
         auto walk = [&](auto&& emit) {
@@ -132,11 +179,13 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                 if (l >= 1 && l <= kJoints) fk_step(X, R, l - 1, sq[tid * kJoints + l - 1]);
                 if (l == kLinks - 1) {
                     fk_hand(X, R);
-                    if constexpr (EE) hand_ee_pose(X, ee + (p0 + tid) * 7);
+                    if constexpr (EE) {
+                        if (valid) hand_ee_pose(X, ee + (p0 + tid) * 7);
+                    }
                     if constexpr (IKO) {   // N2: pose + bound cost of this pose -> cost_pose
                         float c = 0.f, F[3], tau[3];
                         const long long pg = p0 + tid;
-                        const int wi = ik.world_idx[pg / ik.H];
+                        const int wi = valid ? ik.world_idx[pg / ik.H] : -1;
                         if ((ik.w_pos != 0.f || ik.w_rot != 0.f) && wi >= 0 && wi < ik.n_goals)
                             c = ik_pose_cost(X, ik.goals + 12 * wi, ik.w_pos, ik.w_rot, F, tau);
                         if (ik.w_bound != 0.f)
@@ -145,15 +194,17 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
                                 c += ik_bound(sq[tid * kJoints + j], R.q_lo[j], R.q_hi[j],
                                               ik.w_bound, dq);
                             }
-                        ik.cost[pg] = c;
+                        if (valid) ik.cost[pg] = c;
                     }
                 }
                 for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
                     float cx, cy, cz;
                     xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
-                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s, cx);
-                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 1, cy);
-                    VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 2, cz);
+                    if (valid) {
+                        VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s, cx);
+                        VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 1, cy);
+                        VAPR_TAP(0, (p0 + tid) * R.cols + 3 * s + 2, cz);
+                    }
                     emit(cx, cy, cz);
                 }
             }
@@ -175,17 +226,6 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
             });
         }
     }
-    __syncthreads();
-
-    // coalesced 16-byte tile store (rows are 16-byte multiples): four
-    // conflict-free scalar shared reads per uint4
-    const int Q = W / 4, nq = np * Q;
-    uint4* dst = reinterpret_cast<uint4*>(os + p0 * W);
-    for (int i = tid; i < nq; i += kTile) {
-        const int r = int((uint32_t(i) * rq) >> 20), g = i - r * Q;
-        const uint32_t* src = sw + r * WS + 4 * g;
-        __stcs(dst + i, make_uint4(src[0], src[1], src[2], src[3]));
-    }
 }
 
 }  // namespace
@@ -194,20 +234,15 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
                       uint32_t* os, cudaStream_t s, const IkArgs* ik, float* ee) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fos, R.cols);
-    const size_t smem = sizeof(float) * kTile * kJoints + sizeof(uint32_t) * kTile * (W + 1);
     const bool iko = ik && ik_on(*ik);
     auto kern = iko ? (ee ? fk_kernel<true, true> : fk_kernel<true, false>)
                     : (ee ? fk_kernel<false, true> : fk_kernel<false, false>);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
     const long long grid = (P + kTile - 1) / kTile;
-    const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
     IkArgs none{};
 #ifdef VAPR_DEBUG_TAP
     const bool tapped = tap_arm(0, P, R.cols, s) != nullptr;
 #endif
-    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fos, q, P, W, os, rq, iko ? *ik : none, ee);
+    kern<<<(unsigned)grid, kTile, 0, s>>>(R, fos, q, P, W, os, iko ? *ik : none, ee);
 #ifdef VAPR_DEBUG_TAP
     if (tapped) tap_disarm(0, s);
 #endif
