@@ -8,13 +8,13 @@
 // buffer (PF = codes per word, a compile-time constant via with_pf; the
 // element count is warp-uniform, so there is no divergence) and every full
 // buffer is encoded into one packed word (hardware cvt fast path for
-// E5M10 / E8M7 / FP8 / FP6 / FP4).  Each warp stages its 32 rows 16 words
-// at a time in a small shared chunk (stride 17 words, odd, so the 32 lanes --
+// E5M10 / E8M7 / FP8 / FP6 / FP4).  Each warp stages its 32 rows 32 words
+// at a time in a small shared chunk (stride 33 words, odd, so the 32 lanes --
 // 32 poses writing the same word index -- hit 32 distinct banks); every full
-// chunk is streamed to HBM at once, four lanes per pose writing its 64
-// contiguous bytes (two whole sectors) with 16-byte stores.  Shared memory per
-// warp is a fixed 2.2 KB whatever the row width, so occupancy is set by
-// registers, not by a staged row tile.  Link frames are NOT written to
+// chunk is streamed to HBM at once, eight lanes per pose writing its 128
+// contiguous bytes (one whole line) with 16-byte stores.  Shared memory per
+// warp is a fixed 4.2 KB whatever the row width, so occupancy is set by
+// registers (10 CTAs, 40 warps per SM), not by a staged row tile.  Link frames are NOT written to
 // memory: backward kinematics recomputes them, so HBM sees q
 // (28 B/pose) in and out_spheres out.
 #include "common.cuh"
@@ -30,12 +30,16 @@ constexpr int kTile = 128;   // poses (= threads) per CTA
 #define VAPR_FK_MINB 10
 #endif
 
-constexpr int kChunk = 16;          // words per pose per warp flush
+#ifndef VAPR_FK_CHUNK            // words per pose per warp flush (a multiple of 4)
+#define VAPR_FK_CHUNK 32
+#endif
+constexpr int kChunk = VAPR_FK_CHUNK;
+constexpr int kLPR = kChunk / 4;     // lanes per pose row segment in a drain
 constexpr int kCS = kChunk + 1;      // chunk row stride (odd: conflict-free lane writes)
 
 // A warp's rows, kChunk words at a time: put() is warp-uniform (every pose
-// has the same word sequence), a full chunk goes to HBM as 64-byte segments
-// per pose (lane = 4 pose + part), poses >= np are computed but not stored.
+// has the same word sequence), a full chunk goes to HBM as 128-byte segments
+// per pose (lane = kLPR pose + part), poses >= np are computed but not stored.
 struct RowStore {
     uint32_t* buf;                   // this warp's [32][kCS] chunk
     uint32_t* os;                    // the warp's first row in HBM
@@ -49,8 +53,8 @@ struct RowStore {
         __syncwarp();
         const int parts = n >> 2;    // n is a multiple of 4 (rows are 16-byte multiples)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = k * 32 + lane, p = i >> 2, part = i & 3;
+        for (int k = 0; k < kLPR; ++k) {
+            const int i = k * 32 + lane, p = i / kLPR, part = i % kLPR;
             if (p < np && part < parts) {
                 const uint32_t* src = buf + p * kCS + 4 * part;
                 __stcs(reinterpret_cast<uint4*>(os + (long long)p * W + chunk * kChunk + 4 * part),
