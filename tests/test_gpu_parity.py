@@ -209,6 +209,35 @@ def test_fk_spheres(vb, name):
     assert exact > 0.99 or fos == (8, 23)
 
 
+@pytest.mark.parametrize("formats", ["43bit", "fp32", "pf3", "pf5_pf8"])
+def test_fk_chunk_tails(vb, formats):
+    """FK's per-warp chunk drains (fk.cu): 287 poses = two full 128-pose CTAs
+    and a tail CTA whose one warp has 31 live lanes, with row widths that
+    leave a partial last chunk (FP32: 156 words = 4 x 32 + 28).  Every row
+    word, padding included, against the oracle; the buffer past the last
+    pose stays untouched."""
+    wl = ragged_workload(B=7, H=41, formats=formats, salt=31)
+    c = Ctx(vb, wl)
+    P, W = wl.poses, c.W(0)
+    assert P == 287
+    fos = c.formats[0]
+    out = torch.full((P * W + 64,), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    vb.vapr_fk_spheres(c.h, dev(wl.q), wl.B, wl.H, out)
+    words, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, fos)
+    got = out[:P * W].cpu().numpy().view(np.uint32).reshape(P, -1)
+    check_codes(got, v, 1.0, fos, 156, what="out_spheres",
+                min_exact=0.999 if fos != (8, 23) else None)
+    # padding: the unused code slots of the last used word and every word after it are +0
+    t = 1 + fos[0] + fos[1]
+    pf = 32 // t
+    used = -(-156 // pf)
+    tail_bits = (156 - (used - 1) * pf) * t
+    if tail_bits < 32:
+        assert (got[:, used - 1] >> np.uint32(tail_bits) == 0).all()
+    assert (got[:, used:] == 0).all()
+    assert (out[P * W:].cpu().numpy() == 0x5A5A5A5A).all()
+
+
 # --------------------------------------------------------------------- a3/a4
 @pytest.mark.parametrize("name", list(WORKLOADS))
 @pytest.mark.parametrize("swept", [1, 0])
