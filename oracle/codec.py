@@ -127,10 +127,21 @@ def representable_magnitudes(E, M):
 
 def quantize_enum(x, E, M):
     """Nearest representable magnitude, ties to the even code (t <= 16)."""
+    return _enum_nearest(np.asarray(x, np.float32), E, M)
+
+
+def quantize_enum_f64(x, E, M):
+    """The enumeration oracle on DOUBLE inputs (one rounding from the double
+    value): the independent pin of `quantize_f64` for values between FP32
+    numbers.  Near a tie the distances a - mags[lo] and mags[hi] - a are
+    exact in double (adjacent magnitudes lie within a factor 2, Sterbenz)."""
+    return _enum_nearest(np.asarray(x, np.float64), E, M)
+
+
+def _enum_nearest(x, E, M):
     t = total_bits(E, M)
     assert t <= 16, "enumeration oracle is for t <= 16"
     mags = representable_magnitudes(E, M)
-    x = np.asarray(x, np.float32)
     a = np.abs(x.astype(np.float64))
     sign = np.signbit(x).astype(np.uint32) << np.uint32(t - 1)
     top = len(mags) - 1

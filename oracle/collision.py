@@ -39,8 +39,10 @@ def box_sdf(c, R, t, h):
     """Signed distance and world-frame gradient of one oriented box.
 
     c [..., 3]; R [3, 3] world-from-box; t [3]; h [3].  Returns (sdf [...],
-    grad [..., 3], tie [...]) where `tie` flags inside points whose top two
-    face distances are within 1e-6 (gradient ambiguous, reading c16)."""
+    grad [..., 3], tie [...], grad_alt [..., 3], out_norm [...]): `tie` flags
+    inside points whose top two face distances are within 1e-6 (gradient
+    ambiguous, reading c16) and grad_alt is the gradient with the runner-up
+    face there (= grad elsewhere); out_norm = ||max(u, 0)||."""
     c = np.asarray(c, np.float64)
     R = np.asarray(R, np.float64)
     p = (c - t) @ R                      # = R^T (c - t), row-vector form
@@ -55,20 +57,35 @@ def box_sdf(c, R, t, h):
     g_in = np.zeros(u.shape)
     np.put_along_axis(g_in, kstar[..., None],
                       np.take_along_axis(sgn, kstar[..., None], -1), -1)
+    order = np.argsort(-u, axis=-1, kind="stable")
+    k2 = order[..., 1]                   # the runner-up face
+    g_in2 = np.zeros(u.shape)
+    np.put_along_axis(g_in2, k2[..., None], np.take_along_axis(sgn, k2[..., None], -1), -1)
     with np.errstate(invalid="ignore", divide="ignore"):
         g_out = sgn * upos / np.where(outside_norm > 0, outside_norm, 1.0)[..., None]
     g_local = np.where(inside[..., None], g_in, g_out)
     grad = g_local @ R.T                 # = R g_local
     us = np.sort(u, axis=-1)
     tie = inside & ((us[..., -1] - us[..., -2]) < 1e-6)
-    return sdf, grad, tie
+    grad_alt = np.where(tie[..., None], g_in2 @ R.T, grad)
+    return sdf, grad, tie, grad_alt, outside_norm
 
 
-# Length scale L (metres) of the workspace and the FP32 evaluation error
-# bound on a distance, used only to build per-element tolerance scales for the
-# parity tests: a term whose phi lies within NEAR of 0 may be
-# active on one side and inactive on the other; its derivative h' = phi/eta
-# carries an absolute error of about eps * L / eta.
+# Tolerance bookkeeping for the parity tests.  Besides each
+# value the oracle returns
+#   terms: the sum of the absolute values of the summands that make it (the
+#          FP32 summation error is relative to this, not to the value), and
+#   kappa: its condition number w.r.t. FP32 rounding of the evaluation, in
+#          units where the FP32 error is ~ 2^-24 kappa:
+#     * a term within NEAR of activation may be active on one side only, and
+#       h' = phi/eta carries the absolute error of phi (~ L, the coordinate
+#       magnitude, in units of 2^-24) over eta: w L / eta;
+#     * the cost term h(phi) carries the error of phi: w L;
+#     * an outside box gradient max(u,0)/||max(u,0)|| has a direction error
+#       ~ L / ||max(u,0)||, weighted by h';
+#     * a self pair's phi is computed from the pair distance d (error ~
+#       d + r_i + r_j), so its h' error is w (d + r_i + r_j + eta) / eta; its
+#       direction (c_i - c_j)/d is accurate to a few ulps (w h').
 L_SCALE = 1.0
 NEAR = 1e-6
 
@@ -76,69 +93,81 @@ NEAR = 1e-6
 def world_point_cost(c, radius, cuboids, eta, w):
     """f and grad f for points c [N, S, 3] of one world.
 
-    cuboids [K, 16] float32 rows (R, t, h, pad).  Returns cost [N, S],
-    grad [N, S, 3], cost scale [N, S], grad scale [N, S] and tie flags
-    [N, S]."""
+    cuboids [K, 16] float32 rows (R, t, h, pad).  Returns a dict of cost
+    [N, S], grad / grad_alt [N, S, 3], cost_terms / cost_kappa [N, S],
+    grad_terms / grad_kappa [N, S] (per sphere, bounding each component) and
+    tie [N, S]."""
     N, S = c.shape[0], c.shape[1]
     cost = np.zeros((N, S))
     grad = np.zeros((N, S, 3))
-    cscale = np.zeros((N, S))
-    gscale = np.zeros((N, S))
+    grad_alt = np.zeros((N, S, 3))
+    cterms = np.zeros((N, S))
+    ckappa = np.zeros((N, S))
+    gterms = np.zeros((N, S))
+    gkappa = np.zeros((N, S))
     tie = np.zeros((N, S), bool)
     for k in range(cuboids.shape[0]):
         row = cuboids[k].astype(np.float64)
         R = row[0:9].reshape(3, 3)
-        sdf, gs, tk = box_sdf(c, R, row[9:12], row[12:15])
+        sdf, gs, tk, gs_alt, onorm = box_sdf(c, R, row[9:12], row[12:15])
         phi = radius[None, :] + eta - sdf
         hk, dhk = hinge(phi, eta)
         cost = cost + w * hk
         grad = grad + (-w * dhk)[..., None] * gs
+        grad_alt = grad_alt + (-w * dhk)[..., None] * gs_alt
         near = phi > -NEAR
-        cscale = cscale + w * (hk + near * L_SCALE)
-        gscale = gscale + w * near * (1.0 + L_SCALE / eta)
+        cterms = cterms + w * hk
+        ckappa = ckappa + w * near * L_SCALE
+        gterms = gterms + w * dhk
+        with np.errstate(divide="ignore"):
+            cond_dir = np.where(onorm > 0, L_SCALE / np.maximum(onorm, 1e-300), 0.0)
+        gkappa = gkappa + w * near * (1.0 + L_SCALE / eta + dhk * cond_dir)
         tie |= tk & near
-    return cost, grad, cscale, gscale, tie
+    return dict(cost=cost, grad=grad, grad_alt=grad_alt, cost_terms=cterms, cost_kappa=ckappa,
+                grad_terms=gterms, grad_kappa=gkappa, tie=tie)
 
 
 def world_cost(c, radius, cuboids, eta, w, swept=False, n=1):
     """World collision for trajectories c [nb, H, S, 3] of ONE world (float64).
 
-    Returns cost_pose [nb, H], grad [nb, H, S, 3] (closest_pt or
-    closest_pt_swept), cost scale [nb, H], grad scale [nb, H, S], tie
-    [nb, H, S]."""
+    Returns a dict: cost [nb, H] (cost_pose), grad / grad_alt [nb, H, S, 3]
+    (closest_pt or closest_pt_swept), cost_terms / cost_kappa [nb, H],
+    grad_terms / grad_kappa [nb, H, S], tie [nb, H, S]."""
     nb, H, S = c.shape[0], c.shape[1], c.shape[2]
 
     def point(x):
-        f, g, cs, gs, t = world_point_cost(x.reshape(-1, S, 3), radius, cuboids, eta, w)
+        r = world_point_cost(x.reshape(-1, S, 3), radius, cuboids, eta, w)
         sh = x.shape[:-2]
-        return (f.reshape(sh + (S,)), g.reshape(sh + (S, 3)), cs.reshape(sh + (S,)),
-                gs.reshape(sh + (S,)), t.reshape(sh + (S,)))
+        return {k: v.reshape(sh + v.shape[1:]) for k, v in r.items()}
 
-    f, gf, cs, gsc, tie = point(c)
-    cost = f.sum(axis=-1)
-    cscale = cs.sum(axis=-1)
-    grad = gf.copy()
-    gscale = gsc.copy()
+    r0 = point(c)
+    out = dict(cost=r0["cost"].sum(axis=-1), cost_terms=r0["cost_terms"].sum(axis=-1),
+               cost_kappa=r0["cost_kappa"].sum(axis=-1), grad=r0["grad"].copy(),
+               grad_alt=r0["grad_alt"].copy(), grad_terms=r0["grad_terms"].copy(),
+               grad_kappa=r0["grad_kappa"].copy(), tie=r0["tie"].copy())
     if swept and n > 0 and H >= 2:
         for j in range(1, n + 1):
             tau = j / (n + 1.0)
             p = (1.0 - tau) * c[:, :-1] + tau * c[:, 1:]    # segments h = 0..H-2
-            fp, gp, csp, gsp, tp = point(p)
-            cost[:, :-1] += fp.sum(axis=-1)
-            cscale[:, :-1] += csp.sum(axis=-1)
-            grad[:, :-1] += (1.0 - tau) * gp
-            grad[:, 1:] += tau * gp
-            gscale[:, :-1] += gsp
-            gscale[:, 1:] += gsp
-            tie[:, :-1] |= tp
-            tie[:, 1:] |= tp
-    return cost, grad, cscale, gscale, tie
+            rp = point(p)
+            for k in ("cost", "cost_terms", "cost_kappa"):
+                out[k][:, :-1] += rp[k].sum(axis=-1)
+            for k in ("grad", "grad_alt"):
+                out[k][:, :-1] += (1.0 - tau) * rp[k]
+                out[k][:, 1:] += tau * rp[k]
+            for k in ("grad_terms", "grad_kappa"):
+                out[k][:, :-1] += (1.0 - tau) * rp[k]
+                out[k][:, 1:] += tau * rp[k]
+            out["tie"][:, :-1] |= rp["tie"]
+            out["tie"][:, 1:] |= rp["tie"]
+    return out
 
 
 def self_cost(c, radius, pairs, eta, w):
     """Self collision for poses c [N, S, 3] (float64) over the listed pairs.
 
-    Returns cost [N], out_vec [N, S, 3], cost scale [N], grad scale [N, S]."""
+    Returns a dict: cost [N], grad (out_vec) [N, S, 3], cost_terms /
+    cost_kappa [N], grad_terms / grad_kappa [N, S]."""
     N, S = c.shape[0], c.shape[1]
     i = pairs[:, 0].astype(np.int64)
     j = pairs[:, 1].astype(np.int64)
@@ -152,13 +181,19 @@ def self_cost(c, radius, pairs, eta, w):
     u = np.where((d > 0)[..., None], u, np.array([1.0, 0.0, 0.0]))
     contrib = (w * dh)[..., None] * u                   # [N, npairs, 3]
     near = phi > -NEAR
-    cscale = w * np.sum(h + near * L_SCALE, axis=1)
-    pscale = w * near * (1.0 + L_SCALE / eta + L_SCALE / np.maximum(d, 1e-3))
+    cterms = w * h.sum(axis=1)
+    ckappa = w * np.sum(near * (d + radius[i] + radius[j] + eta), axis=1)
+    pterms = w * dh
+    pkappa = w * near * (1.0 + (d + radius[i] + radius[j] + eta) / eta)
     out = np.zeros((N, S, 3))
-    gscale = np.zeros((N, S))
+    gterms = np.zeros((N, S))
+    gkappa = np.zeros((N, S))
     for k in range(len(i)):                             # plain pair loop
         out[:, i[k]] -= contrib[:, k]
         out[:, j[k]] += contrib[:, k]
-        gscale[:, i[k]] += pscale[:, k]
-        gscale[:, j[k]] += pscale[:, k]
-    return cost, out, cscale, gscale
+        gterms[:, i[k]] += pterms[:, k]
+        gterms[:, j[k]] += pterms[:, k]
+        gkappa[:, i[k]] += pkappa[:, k]
+        gkappa[:, j[k]] += pkappa[:, k]
+    return dict(cost=cost, grad=out, cost_terms=cterms, cost_kappa=ckappa,
+                grad_terms=gterms, grad_kappa=gkappa)

@@ -124,3 +124,22 @@ def backward_terms_abs(q, g, robot):
         out[:, j - 1] = np.sum(np.linalg.norm(r, axis=-1) *
                                np.linalg.norm(g[:, sel], axis=-1), axis=1)
     return out
+
+
+def backward_kappa(q, kappa, robot):
+    """sum over spheres of |c_s - o_j| kappa_s: the condition number of joint
+    j's gradient when each sphere gradient g_s carries an FP32 evaluation
+    error ~ 2^-24 kappa_s (the lever arm times that error; parity-test
+    tolerance bookkeeping)."""
+    q = np.asarray(q, np.float64).reshape(-1, 7)
+    kappa = np.asarray(kappa, np.float64).reshape(q.shape[0], -1)
+    F = link_frames(q, robot)
+    c = sphere_centers(q, robot)
+    link = robot["sphere_link"]
+    out = np.zeros((q.shape[0], 7))
+    for j in range(1, 8):
+        o = F[:, j, :3, 3]
+        sel = link >= j
+        r = c[:, sel] - o[:, None, :]
+        out[:, j - 1] = np.sum(np.linalg.norm(r, axis=-1) * kappa[:, sel], axis=1)
+    return out

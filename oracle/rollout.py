@@ -51,43 +51,53 @@ def fk_stage(q, robot, fmt_os):
 
 def world_stage(os_words, fmt_os, world_idx, cuboids, offsets, robot, B, H,
                 eta, w, swept, n, fmt_out):
-    """World collision on packed out_spheres.  Returns dict with cost [B, H],
-    cost_scale [B, H], words (closest_pt[_swept]), v [P, 3S], gscale [P, S],
-    tie [P, S]."""
+    """World collision on packed out_spheres.  Returns a dict with cost
+    [B, H], cost_terms / cost_kappa [B, H], words (closest_pt[_swept]), v and
+    v_alt [P, 3S] (v_alt: the runner-up face at SDF ties), gterms / gkappa
+    [P, S] and tie [P, S] (tolerance bookkeeping: oracle/collision.py)."""
     S = len(robot["sphere_link"])
     c = decode_rows(os_words, fmt_os, 3 * S).reshape(B, H, S, 3)
     radius = robot["sphere_xyzr"][:, 3].astype(np.float64)
-    cost = np.zeros((B, H))
-    cscale = np.zeros((B, H))
-    grad = np.zeros((B, H, S, 3))
-    gscale = np.zeros((B, H, S))
-    tie = np.zeros((B, H, S), bool)
+    keys_bh = ("cost", "cost_terms", "cost_kappa")
+    keys_bhs = ("grad_terms", "grad_kappa")
+    acc = {k: np.zeros((B, H)) for k in keys_bh}
+    acc.update({k: np.zeros((B, H, S)) for k in keys_bhs})
+    acc["grad"] = np.zeros((B, H, S, 3))
+    acc["grad_alt"] = np.zeros((B, H, S, 3))
+    acc["tie"] = np.zeros((B, H, S), bool)
     world_idx = np.asarray(world_idx)
     for wi in np.unique(world_idx):
         sel = np.nonzero(world_idx == wi)[0]
         cub = cuboids[offsets[wi]:offsets[wi + 1]]
         r = world_cost(c[sel], radius, cub, eta, w, swept=bool(swept), n=n)
-        cost[sel], grad[sel], cscale[sel], gscale[sel], tie[sel] = r
-    v = grad.reshape(B * H, 3 * S)
-    return dict(cost=cost, cost_scale=cscale, words=quantize_rows(v, fmt_out),
-                v=v, gscale=gscale.reshape(B * H, S), tie=tie.reshape(B * H, S))
+        for k in acc:
+            acc[k][sel] = r[k]
+    v = acc["grad"].reshape(B * H, 3 * S)
+    return dict(cost=acc["cost"], cost_terms=acc["cost_terms"], cost_kappa=acc["cost_kappa"],
+                words=quantize_rows(v, fmt_out), v=v,
+                v_alt=acc["grad_alt"].reshape(B * H, 3 * S),
+                gterms=acc["grad_terms"].reshape(B * H, S), gkappa=acc["grad_kappa"].reshape(B * H, S),
+                tie=acc["tie"].reshape(B * H, S))
 
 
 def self_stage(os_words, fmt_os, robot, eta, w, fmt_ov):
     S = len(robot["sphere_link"])
     c = decode_rows(os_words, fmt_os, 3 * S).reshape(-1, S, 3)
     radius = robot["sphere_xyzr"][:, 3].astype(np.float64)
-    cost, out, cscale, gscale = self_cost(c, radius, robot["pairs"], eta, w)
-    v = out.reshape(out.shape[0], -1)
-    return dict(cost=cost, cost_scale=cscale, words=quantize_rows(v, fmt_ov),
-                v=v, gscale=gscale)
+    r = self_cost(c, radius, robot["pairs"], eta, w)
+    v = r["grad"].reshape(r["grad"].shape[0], -1)
+    return dict(cost=r["cost"], cost_terms=r["cost_terms"], cost_kappa=r["cost_kappa"],
+                words=quantize_rows(v, fmt_ov), v=v, gterms=r["grad_terms"], gkappa=r["grad_kappa"])
 
 
 def aggregate_stage(cp_words, fmt_cp, ov_words, fmt_ov, fmt_gos, cols):
     """grad_out_spheres = dequant(closest_pt[_swept]) + dequant(out_vec),
-    quantised to t_gos.  The sum is exact in double."""
-    v = decode_rows(cp_words, fmt_cp, cols) + decode_rows(ov_words, fmt_ov, cols)
-    return dict(words=quantize_rows(v, fmt_gos), v=v)
+    quantised to t_gos (SURVEY.md §8(c) step 6).  The sum is exact in double;
+    terms = |a| + |b| bounds the FP32 sum's rounding."""
+    a = decode_rows(cp_words, fmt_cp, cols)
+    b = decode_rows(ov_words, fmt_ov, cols)
+    v = a + b
+    return dict(words=quantize_rows(v, fmt_gos), v=v, terms=np.abs(a) + np.abs(b))
 
 
 def bk_stage(q, gos_words, fmt_gos, robot):

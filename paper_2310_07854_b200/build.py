@@ -30,17 +30,38 @@ def _stale(so=SO):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, extra=(), tap=True):
-    """libvapr.so (release) and, with tap, libvapr_tap.so (the test-only
-    debug-tap build of the same sources)."""
-    outs = [(SO, [])] + ([(TAP_SO, ["-DVAPR_DEBUG_TAP"])] if tap else [])
-    for so, defs in outs:
-        if not force and not _stale(so):
-            continue
-        cmd = [NVCC, *FLAGS, *extra, *defs, "-o", so] + [os.path.join(CSRC, s) for s in SOURCES]
+def _compile_link(so, defs, extra=(), verbose=False):
+    """Compile every source to an object in parallel (one nvcc per file),
+    then link the shared library: the same flags as one nvcc call, a few
+    times faster on a many-core host."""
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build", os.path.basename(so).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, *extra, *defs, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(one, SOURCES))
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                           "-Xcompiler", "-fPIC", "-o", so, *objs])
+
+
+def build(force=False, verbose=False, extra=(), tap=True):
+    """libvapr.so (release) and, with tap, libvapr_tap.so (the test-only
+    debug-tap build of the same sources)."""
+    from concurrent.futures import ThreadPoolExecutor
+    outs = [(SO, [])] + ([(TAP_SO, ["-DVAPR_DEBUG_TAP"])] if tap else [])
+    outs = [(so, defs) for so, defs in outs if force or _stale(so)]
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        for f in [ex.submit(_compile_link, so, defs, extra, verbose) for so, defs in outs]:
+            f.result()
     return SO
 
 
@@ -48,8 +69,7 @@ def build_variant(name, defines):
     """Build a variant library (extra -D flags) to variants/libvapr_NAME.so."""
     out = os.path.join(HERE, "variants", f"libvapr_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [NVCC, *FLAGS, *defines, "-o", out] + [os.path.join(CSRC, s) for s in SOURCES]
-    subprocess.check_call(cmd)
+    _compile_link(out, list(defines))
     return out
 
 

@@ -101,6 +101,7 @@ Fmt make_fmt(vapr_format v) {
     const uint32_t rnd = f.sh > 0 ? (1u << (f.sh - 1)) - 1u : 0u;
     const uint32_t off = (uint32_t)(127 - bias) << f.M;
     f.K = rnd - (off << f.sh);                                  // mod 2^32
+    f.lsb = f.sh > 0 ? 1u : 0u;                               // E<8, M=23: no rounding
     f.minnorm = (uint32_t)(128 - bias) << 23;                 // 2^(1-bias)
     f.magic_bits = (uint32_t)(127 + 24 - bias - f.M) << 23;    // 2^(24-bias-M)
     const uint32_t emax = (f.E == 8) ? 254u : (1u << f.E) - 1u;
@@ -197,7 +198,6 @@ vapr_status vapr_create(int device, vapr_ctx** out) {
         if (!g.ok || cudaMalloc(&c->d_sched, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess ||
             cudaMemset(c->d_sched, 0, sizeof(unsigned int) * 2 * kSchedSlots) != cudaSuccess) {
             if (c->d_sched) cudaFree(c->d_sched);
-    if (c->d_goals) cudaFree(c->d_goals);
             delete c;
             cudaGetLastError();
             return VAPR_ERR_CUDA;

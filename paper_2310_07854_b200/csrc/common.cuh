@@ -57,17 +57,20 @@ struct Fmt {
     uint32_t hw_limit;     // hardware fast path valid while |x| bits < hw_limit
     float dscale;          // 2^(127 - bias): decode re-bias
     uint32_t nancode;      // encode of NaN: maxcode (c8) / 0x7FFF (IEEE)
+    uint32_t lsb;          // RNE tie bit mask: 1 when sh > 0; 0 for M = 23 (nothing is
+                           // dropped, so nothing rounds: code = a - off exactly)
 };
 
 // FP32 -> code, round to nearest even (single rounding), saturating, NaN ->
 // +max, -0 kept (readings c2-c8).  Normal range: integer RNE on the FP32 bit
-// pattern (a carry into the exponent is the correct binade change).  Format
+// pattern (a carry into the exponent is the correct binade change; for M = 23
+// nothing is dropped and both the half-ulp constant and the tie bit are 0).  Format
 // subnormal range: |x| + 2^(24-bias-M) rounds |x| to the subnormal quantum in
 // the FP32 adder (RN-even), exact because no FTZ is used anywhere.
 __device__ __forceinline__ uint32_t encode_generic(float x, const Fmt& f) {
     const uint32_t u = __float_as_uint(x);
     const uint32_t a = u & 0x7fffffffu;
-    const uint32_t cn = (a + f.K + ((a >> f.sh) & 1u)) >> f.sh;
+    const uint32_t cn = (a + f.K + ((a >> f.sh) & f.lsb)) >> f.sh;
     const uint32_t cs =
         __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits))) - f.magic_bits;
     uint32_t c = (a < f.minnorm) ? cs : cn;

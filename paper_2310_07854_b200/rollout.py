@@ -119,34 +119,48 @@ class Rollout:
                                self.grad_q, cost_traj_host, grad_q_host, n_chunks,
                                stream=stream, _p=self._p)
 
-    def sparse_gos(self):
+    def sparse_gos(self, rows=None):
         """N3 (sparse mode): grad_out_spheres' mask [P] uint64, off [P], the
-        pool (its whole capacity) and the count of words in use, as numpy arrays."""
+        pool (its whole capacity) and the count of words in use, as numpy
+        arrays.  rows (a slice of poses): only those rows' masks / offsets,
+        and `row_words` = each of those rows' pool words."""
         torch.cuda.synchronize(self.device)
         (mo, oo, uo, po, _, _), pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
         P = self.B * self.H
         ws = self.workspace
-        mask = ws[mo:mo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64)
-        off = ws[oo:oo + 4 * P].view(torch.int32).cpu().numpy().view(np.uint32)
+        mask = ws[mo:mo + 8 * P].view(torch.int64)
+        off = ws[oo:oo + 4 * P].view(torch.int32)
         used = int(ws[uo:uo + 4].view(torch.int32).cpu().numpy().view(np.uint32)[0])
-        pool = ws[po:po + 4 * pw].view(torch.int32).cpu().numpy().view(np.uint32)
-        return dict(mask=mask, off=off, pool=pool, used=used)
+        pool_t = ws[po:po + 4 * pw].view(torch.int32)
+        if rows is None:
+            return dict(mask=mask.cpu().numpy().view(np.uint64), off=off.cpu().numpy().view(np.uint32),
+                        pool=pool_t.cpu().numpy().view(np.uint32), used=used)
+        m = mask[rows].cpu().numpy().view(np.uint64)
+        o = off[rows].cpu().numpy().view(np.uint32)
+        fmt = self.ctx.formats[vb.VAPR_GRAD_OUT_SPHERES]
+        pf = 32 // (1 + fmt[0] + (fmt[1] & 0xFF))
+        rw = []
+        for mi, oi in zip(m, o):
+            n = -(-3 * bin(int(mi)).count("1") // pf)
+            rw.append(pool_t[int(oi):int(oi) + n].cpu().numpy().view(np.uint32))
+        return dict(mask=m, off=o, row_words=rw, used=used)
 
-    def sphere_masks(self):
+    def sphere_masks(self, rows=None):
         """N3 (sparse mode): per-pose sphere bitmaps of closest_pt[_swept] and
-        out_vec (uint64 [P] each)."""
+        out_vec (uint64 [P] each, or of the poses in `rows`)."""
         torch.cuda.synchronize(self.device)
         (_, _, _, _, cmo, omo), _ = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
         P = self.B * self.H
         ws = self.workspace
-        return (ws[cmo:cmo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64),
-                ws[omo:omo + 8 * P].view(torch.int64).cpu().numpy().view(np.uint64))
+        rows = rows if rows is not None else slice(0, P)
+        return (ws[cmo:cmo + 8 * P].view(torch.int64)[rows].cpu().numpy().view(np.uint64),
+                ws[omo:omo + 8 * P].view(torch.int64)[rows].cpu().numpy().view(np.uint64))
 
-    def packed_masked(self, slot):
+    def packed_masked(self, slot, rows=None):
         """N3 (sparse mode): a collision slot's rows with the fields of unset
-        spheres zeroed -- the dense mode's rows."""
-        words = self.packed(slot)
-        cm, om = self.sphere_masks()
+        spheres zeroed -- the dense mode's rows (all, or the poses in `rows`)."""
+        words = self.packed(slot, rows)
+        cm, om = self.sphere_masks(rows)
         m = om if slot == vb.VAPR_OUT_VEC else cm
         fmt = self.ctx.formats[slot]
         t = 1 + fmt[0] + (fmt[1] & 0xFF)
@@ -166,8 +180,9 @@ class Rollout:
             out[:, w] &= ~fm
         return out
 
-    def packed(self, slot):
-        """The packed tensor of `slot` inside the workspace, as uint32 [P, W]."""
+    def packed(self, slot, rows=None):
+        """The packed tensor of `slot` inside the workspace, as uint32 [P, W]
+        (or the poses in `rows`, a slice)."""
         lay = vb.vapr_cost_grad_workspace_layout(self.ctx.h, self.B, self.H, self.params["swept"])
         off = lay[slot]
         if off is None:
@@ -176,6 +191,8 @@ class Rollout:
         W = vb.vapr_packed_row_words(fmt, 3 * len(self.wl.robot["sphere_link"]))
         P = self.B * self.H
         words = self.workspace[off:off + 4 * W * P].view(torch.int32).view(P, W)
+        if rows is not None:
+            words = words[rows]
         return words.cpu().numpy().view(np.uint32)
 
     def results(self):

@@ -22,3 +22,16 @@ def golden(name):
             if line and not line.startswith("#"):
                 rows.append(line.split())
     return rows
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With VAPR_PARITY_REPORT=<path>: write the largest err / limit of every
+    FP32 comparison and the largest code distance of every packed comparison
+    (tests/parity_utils.py records them) -- how tight the tolerances are."""
+    path = os.environ.get("VAPR_PARITY_REPORT")
+    if not path:
+        return
+    import json
+    import parity_utils
+    with open(path, "w") as f:
+        json.dump(parity_utils.REPORT, f, indent=1, sort_keys=True)

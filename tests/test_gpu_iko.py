@@ -11,7 +11,7 @@ import torch
 
 from oracle import ikcost as K
 from oracle import rollout as orc
-from parity_utils import check_close
+from parity_utils import check_close, e2e_kw, ik_kw
 from workloads import config_iko
 
 pytestmark = pytest.mark.gpu
@@ -53,22 +53,18 @@ def test_ik_terms_match_oracle(vb, w):
     G = wl.goals.astype(np.float64)[gi]
     cost = np.zeros(len(q64))
     grad = np.zeros_like(q64)
-    scale_c = np.zeros(len(q64))
     if w["w_pose_pos"] or w["w_pose_rot"]:
         c, g = K.pose_cost(q64, wl.robot, G[:, :9].reshape(-1, 3, 3), G[:, 9:], w["w_pose_pos"],
                            w["w_pose_rot"])
         cost += c
         grad += g
-        scale_c += c
     if w["w_bound"]:
         c, g = K.bound_cost(q64, wl.robot["q_lo"], wl.robot["q_hi"], w["w_bound"])
         cost += c
         grad += g
-        scale_c += c
-    check_close(out["cost_pose"].reshape(-1), cost, scale_c + 1.0, "ik cost", tol=1e-5)
-    # gradient scale: |lever| |F| + |tau| per joint (FP32 error of z.(r x F) + z.tau)
-    check_close(out["grad_q"].reshape(-1, 7), grad, np.abs(grad) + 10.0 * (scale_c[:, None] + 1.0),
-                "ik grad", tol=1e-5)
+    kw = ik_kw(q64, wl.robot, G, w["w_pose_pos"], w["w_pose_rot"], w["w_bound"])
+    check_close(out["cost_pose"].reshape(-1), cost, what="ik cost", **kw["cost"])
+    check_close(out["grad_q"].reshape(-1, 7), grad, what="ik grad", **kw["grad"])
 
 
 def test_iko_full_cost_fp32_end_to_end(vb):
@@ -80,12 +76,15 @@ def test_iko_full_cost_fp32_end_to_end(vb):
     r.run()
     out = r.results()
     res = orc.rollout_workload(wl)
-    st = res.stages
-    scale = (st["world"]["cost_scale"].reshape(-1) + st["self"]["cost_scale"]
-             + st["ik"][0] + 1.0).reshape(wl.B, wl.H)
-    check_close(out["cost_traj"], res.cost_traj, scale.sum(1), "cost_traj", tol=1e-4)
-    gscale = np.abs(res.grad_q).reshape(-1, 7) + st["bk"]["scale"] + 10.0 * (st["ik"][0][:, None] + 1.0)
-    check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), gscale, "grad_q", tol=1e-4)
+    kw = e2e_kw(res, wl)
+    p = wl.params
+    G = np.asarray(wl.goals, np.float64)[np.repeat(wl.world_idx, wl.H)]
+    ik = ik_kw(wl.q, wl.robot, G, p["w_pose_pos"], p["w_pose_rot"], p["w_bound"])
+    ct_terms = kw["cost_traj"]["terms"] + ik["cost"]["terms"].reshape(wl.B, wl.H).sum(1)
+    ct_kappa = kw["cost_traj"]["kappa"] + ik["cost"]["kappa"].reshape(wl.B, wl.H).sum(1)
+    check_close(out["cost_traj"], res.cost_traj, ct_terms, "cost_traj", kappa=ct_kappa)
+    check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), kw["grad_q"]["terms"] + ik["grad"]["terms"],
+                "grad_q", kappa=kw["grad_q"]["kappa"] + ik["grad"]["kappa"])
 
 
 def test_iko_requires_goals(vb):

@@ -6,13 +6,20 @@ import torch
 from oracle import codec
 from oracle import rollout as orc
 from oracle.formats import enumerate_formats
-from parity_utils import check_codes, check_close, sphere_to_elem
+from parity_utils import check_codes, check_close, cost_kw, e2e_kw, self_kw, sphere_to_elem, step_bound, world_kw
 from workloads import config1, config2, config4, make_workload
 from workloads.configs import FORMAT_SETS, codec_sweep_inputs, edge_values
 
 pytestmark = pytest.mark.gpu
 
-ALL_FORMATS = enumerate_formats() + [(6, 6), (5, 9), (6, 8)]
+CANONICAL = enumerate_formats() + [(6, 6), (5, 9), (6, 8)]   # P:221 + Table II
+# every format vapr_format_check accepts: E in [2,8], M in [1,23], t <= 32
+# (PAPER.md:221 defines ExMy for any split) -- 161 formats
+ALL_VALID = [(E, M) for E in range(2, 9) for M in range(1, 24) if 1 + E + M <= 32]
+ALL_FORMATS = CANONICAL
+# canonical formats at four ragged column counts, the rest of the 161 at one
+CODEC_CASES = ([(f, c) for f in CANONICAL for c in (157, 156, 1, 4097)] +
+               [(f, 157) for f in ALL_VALID if f not in CANONICAL])
 
 
 @pytest.fixture(scope="module")
@@ -27,21 +34,47 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+def sampled_magnitudes(E, M, n=1 << 16, key=11):
+    """Up to n representable magnitudes of the format, in code order, from the
+    oracle's decoder: every one for t <= 17, else a seeded sample of codes
+    plus the ends of every binade (so every exponent field is probed)."""
+    t = 1 + E + M
+    ncodes = 255 << M if E == 8 else 1 << (E + M)     # exponent 255 never produced (c7)
+    if ncodes <= n:
+        codes = np.arange(ncodes, dtype=np.uint64)
+    else:
+        rng = np.random.default_rng(key + 97 * E + M)
+        nexp = ncodes >> M
+        ends = np.concatenate([(np.arange(nexp, dtype=np.uint64) << np.uint64(M)),
+                               (np.arange(nexp, dtype=np.uint64) << np.uint64(M)) + np.uint64((1 << M) - 1),
+                               (np.arange(nexp, dtype=np.uint64) << np.uint64(M)) + np.uint64(1)])
+        codes = np.unique(np.concatenate([rng.integers(0, ncodes, n, dtype=np.uint64), ends]))
+        codes = codes[codes < ncodes]
+    pairs = np.stack([codes, np.minimum(codes + 1, ncodes - 1)]).astype(np.uint32)
+    v = codec.dequantize(pairs, E, M).astype(np.float64)
+    return v[0], v[1]
+
+
 def codec_inputs(fmt, n=1 << 16):
-    mags = codec.representable_magnitudes(*fmt)
-    if len(mags) > 1 << 16:
-        mags = mags[np.linspace(0, len(mags) - 1, 1 << 16).astype(np.int64)]
-    mids = ((mags[:-1] + mags[1:]) / 2).astype(np.float32)
+    """Random FP32 patterns, tensor-shaped values, and for the format: sampled
+    representable values, the midpoints between neighbours (the RNE ties) and
+    the FP32 values on either side of each midpoint, and FP32 edge cases."""
+    lo, hi = sampled_magnitudes(*fmt)
+    mids = ((lo + hi) / 2).astype(np.float32)      # exact for M <= 22; M = 23 rounds
     x = np.concatenate([codec_sweep_inputs(n, "bits", 1), codec_sweep_inputs(n, "position", 2),
                         codec_sweep_inputs(n, "gradient", 3), mids,
                         np.nextafter(mids, np.float32(np.inf)), np.nextafter(mids, np.float32(0)),
-                        mags.astype(np.float32), edge_values()])
+                        lo.astype(np.float32), edge_values()])
     return np.concatenate([x, -x])
 
 
 # --------------------------------------------------------------------- a1
-@pytest.mark.parametrize("fmt", ALL_FORMATS)
-@pytest.mark.parametrize("cols", [157, 156, 1, 4097])
+def test_codec_cases_cover_every_valid_format():
+    assert len(ALL_VALID) == 161
+    assert {f for f, _ in CODEC_CASES} == set(ALL_VALID)
+
+
+@pytest.mark.parametrize("fmt,cols", CODEC_CASES, ids=lambda v: str(v))
 def test_quantize_bit_exact(vb, fmt, cols):
     x = codec_inputs(fmt)
     rows = len(x) // cols
@@ -53,7 +86,7 @@ def test_quantize_bit_exact(vb, fmt, cols):
     np.testing.assert_array_equal(got, codec.quantize_packed(x, *fmt))
 
 
-@pytest.mark.parametrize("fmt", ALL_FORMATS)
+@pytest.mark.parametrize("fmt", ALL_VALID)
 def test_dequantize_bit_exact(vb, fmt):
     E, M = fmt
     t = 1 + E + M
@@ -75,6 +108,21 @@ def test_dequantize_bit_exact(vb, fmt):
     assert same.all()
 
 
+@pytest.mark.parametrize("fmt", [(E, 23) for E in range(2, 8)])
+def test_quantize_m23_odd_mantissas(vb, fmt):
+    """E<8, M=23 keeps all 23 FP32 mantissa bits: the code of a normal-range
+    value is its FP32 pattern re-biased, odd mantissas included (round 1
+    added the tie bit of an exact value and bumped every odd one)."""
+    E, M = fmt
+    bias = 2 ** (E - 1) - 1
+    x = np.float32(2.0 ** (1 - bias)) * (1 + np.arange(1, 4001, dtype=np.float32) * np.float32(2 ** -23))
+    out = torch.empty(vb.vapr_packed_row_words(fmt, len(x)), dtype=torch.int32, device="cuda")
+    vb.vapr_quantize(fmt, dev(x[None, :]), 1, len(x), out)
+    got = codec.unpack(out.cpu().numpy().view(np.uint32)[None, :], E, M, len(x))[0]
+    want = (1 << 23) + np.arange(1, 4001, dtype=np.uint32)      # exponent field 1, mantissa k
+    np.testing.assert_array_equal(got, want)
+
+
 def test_codec_empty_and_errors(vb):
     x = torch.zeros(16, device="cuda")
     out = torch.zeros(16, dtype=torch.int32, device="cuda")
@@ -86,7 +134,7 @@ def test_codec_empty_and_errors(vb):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("fmt", ALL_FORMATS)
+@pytest.mark.parametrize("fmt", ALL_VALID)
 def test_quantize_exhaustive_all_fp32(vb, fmt):
     """All 2^32 FP32 bit patterns (SURVEY.md §4 codec tier).  Long: runs only
     with VAPR_EXHAUSTIVE=1 (a dedicated GPU call), not in the default suite."""
@@ -204,8 +252,8 @@ def test_fk_spheres(vb, name):
     vb.vapr_fk_spheres(c.h, dev(wl.q), wl.B, wl.H, out)
     words, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, fos)
     got = out.cpu().numpy().view(np.uint32).reshape(P, -1)
-    exact = check_codes(got, v, 1.0, fos, 156, what="out_spheres",
-                        min_exact=0.999 if fos != (8, 23) else None)
+    exact, _ = check_codes(got, v, 1.0, 0.0, fos, 156, what="out_spheres",
+                           min_exact=0.999 if fos != (8, 23) else None)
     assert exact > 0.99 or fos == (8, 23)
 
 
@@ -225,7 +273,7 @@ def test_fk_chunk_tails(vb, formats):
     vb.vapr_fk_spheres(c.h, dev(wl.q), wl.B, wl.H, out)
     words, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, fos)
     got = out[:P * W].cpu().numpy().view(np.uint32).reshape(P, -1)
-    check_codes(got, v, 1.0, fos, 156, what="out_spheres",
+    check_codes(got, v, 1.0, 0.0, fos, 156, what="out_spheres",
                 min_exact=0.999 if fos != (8, 23) else None)
     # padding: the unused code slots of the last used word and every word after it are +0
     t = 1 + fos[0] + fos[1]
@@ -258,13 +306,14 @@ def test_collision_stage(vb, name, swept):
                          B, H, p["eta_world"], p["w_world"], swept, p["sweep_steps"], f[slot])
     ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
     ref_cost = ws["cost"].reshape(-1) + ss["cost"]
-    scale = ws["cost_scale"].reshape(-1) + ss["cost_scale"]
-    check_close(cost.cpu().numpy(), ref_cost, scale, "cost_pose")
-    check_close(ctraj.cpu().numpy(), ref_cost.reshape(B, H).sum(1), scale.reshape(B, H).sum(1), "cost_traj")
-    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], sphere_to_elem(ws["gscale"]),
-                f[slot], 156, skip=sphere_to_elem(ws["tie"]), what="closest_pt", min_exact=0.999)
-    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], sphere_to_elem(ss["gscale"]),
-                f[2], 156, what="out_vec", min_exact=0.999)
+    ck = cost_kw(ws, ss)
+    check_close(cost.cpu().numpy(), ref_cost, what="cost_pose", **ck)
+    check_close(ctraj.cpu().numpy(), ref_cost.reshape(B, H).sum(1), ck["terms"].reshape(B, H).sum(1),
+                "cost_traj", kappa=ck["kappa"].reshape(B, H).sum(1))
+    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], fmt=f[slot], cols=156,
+                what="closest_pt", min_exact=0.999, max_steps=step_bound(f[slot]), **world_kw(ws))
+    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], fmt=f[2], cols=156,
+                what="out_vec", min_exact=0.999, max_steps=step_bound(f[2]), **self_kw(ss))
 
 
 def test_world_and_self_separately(vb):
@@ -280,15 +329,16 @@ def test_world_and_self_separately(vb):
     vb.vapr_world_collision(c.h, osd, dev(wl.world_idx), B, H, 1, 1, p["eta_world"], p["w_world"], cost, cp)
     ws = orc.world_stage(os_words, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
                          B, H, p["eta_world"], p["w_world"], 1, 1, f[4])
-    check_close(cost.cpu().numpy(), ws["cost"].reshape(-1), ws["cost_scale"].reshape(-1), "world cost")
-    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], sphere_to_elem(ws["gscale"]),
-                f[4], 156, skip=sphere_to_elem(ws["tie"]), what="closest_pt_swept")
+    check_close(cost.cpu().numpy(), ws["cost"].reshape(-1), ws["cost_terms"].reshape(-1), "world cost",
+                kappa=ws["cost_kappa"].reshape(-1))
+    check_codes(cp.cpu().numpy().view(np.uint32).reshape(P, -1), ws["v"], fmt=f[4], cols=156,
+                what="closest_pt_swept", max_steps=step_bound(f[4]), **world_kw(ws))
     ov = torch.empty(P * c.W(2), dtype=torch.int32, device="cuda")
     vb.vapr_self_collision(c.h, osd, B, H, p["eta_self"], p["w_self"], cost, ov)
     ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
-    check_close(cost.cpu().numpy(), ss["cost"], ss["cost_scale"], "self cost")
-    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], sphere_to_elem(ss["gscale"]),
-                f[2], 156, what="out_vec")
+    check_close(cost.cpu().numpy(), ss["cost"], ss["cost_terms"], "self cost", kappa=ss["cost_kappa"])
+    check_codes(ov.cpu().numpy().view(np.uint32).reshape(P, -1), ss["v"], fmt=f[2], cols=156,
+                what="out_vec", max_steps=step_bound(f[2]), **self_kw(ss))
 
 
 # --------------------------------------------------------------------- a5
@@ -301,11 +351,11 @@ def test_aggregate(vb, fs):
     res = orc.rollout_workload(wl)
     gos = torch.empty(P * c.W(1), dtype=torch.int32, device="cuda")
     vb.vapr_aggregate(c.h, dev(res.cp_words.view(np.int32)), 1, dev(res.ov_words.view(np.int32)), P, gos)
-    v = res.stages["aggregate"]["v"]
-    check_codes(gos.cpu().numpy().view(np.uint32).reshape(P, -1), v, 0.0, f[1], 156,
-                what="grad_out_spheres", min_exact=0.999)
+    ag = res.stages["aggregate"]
     # FP32 sum then one rounding: the only allowed differences are at midpoints
-    # within 2^-24 relative of v, covered by TOL
+    # within 2^-24 (|a| + |b|) of v
+    check_codes(gos.cpu().numpy().view(np.uint32).reshape(P, -1), ag["v"], ag["terms"], 0.0, f[1], 156,
+                what="grad_out_spheres", min_exact=0.999, max_steps=step_bound(f[1]))
 
 
 # --------------------------------------------------------------------- a6
@@ -337,19 +387,22 @@ def test_cost_grad_stagewise(vb, name):
     slot = 4 if p["swept"] else 3
     os_w, cp_w, ov_w, gos_w = r.packed(0), r.packed(slot), r.packed(2), r.packed(1)
     _, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
-    check_codes(os_w, v, 1.0, f[0], 156, what="out_spheres")
+    check_codes(os_w, v, 1.0, 0.0, f[0], 156, what="out_spheres")
     ws = orc.world_stage(os_w, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot, B, H,
                          p["eta_world"], p["w_world"], p["swept"], p["sweep_steps"], f[slot])
     ss = orc.self_stage(os_w, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
-    check_codes(cp_w, ws["v"], sphere_to_elem(ws["gscale"]), f[slot], 156,
-                skip=sphere_to_elem(ws["tie"]), what="closest_pt_swept")
-    check_codes(ov_w, ss["v"], sphere_to_elem(ss["gscale"]), f[2], 156, what="out_vec")
+    check_codes(cp_w, ws["v"], fmt=f[slot], cols=156, what="closest_pt_swept",
+                max_steps=step_bound(f[slot]), **world_kw(ws))
+    check_codes(ov_w, ss["v"], fmt=f[2], cols=156, what="out_vec", max_steps=step_bound(f[2]), **self_kw(ss))
     ref_cost = (ws["cost"].reshape(-1) + ss["cost"]).reshape(B, H)
-    scale = (ws["cost_scale"].reshape(-1) + ss["cost_scale"]).reshape(B, H)
-    check_close(out["cost_pose"], ref_cost, scale, "cost_pose")
-    check_close(out["cost_traj"], ref_cost.sum(1), scale.sum(1), "cost_traj")
+    ck = cost_kw(ws, ss)
+    check_close(out["cost_pose"], ref_cost, ck["terms"].reshape(B, H), "cost_pose",
+                kappa=ck["kappa"].reshape(B, H))
+    check_close(out["cost_traj"], ref_cost.sum(1), ck["terms"].reshape(B, H).sum(1), "cost_traj",
+                kappa=ck["kappa"].reshape(B, H).sum(1))
     ag = orc.aggregate_stage(cp_w, f[slot], ov_w, f[2], f[1], 156)
-    check_codes(gos_w, ag["v"], 0.0, f[1], 156, what="grad_out_spheres")
+    check_codes(gos_w, ag["v"], ag["terms"], 0.0, f[1], 156, what="grad_out_spheres",
+                max_steps=step_bound(f[1]))
     bk = orc.bk_stage(wl.q.reshape(-1, 7), gos_w, f[1], wl.robot)
     check_close(out["grad_q"].reshape(P, 7), bk["grad_q"], bk["scale"], "grad_q")
 
@@ -363,11 +416,10 @@ def test_cost_grad_fp32_end_to_end(vb):
     r.run()
     out = r.results()
     res = orc.rollout_workload(wl)
-    st = res.stages
-    scale = (st["world"]["cost_scale"].reshape(-1) + st["self"]["cost_scale"]).reshape(wl.B, wl.H)
-    check_close(out["cost_traj"], res.cost_traj, scale.sum(1), "cost_traj", tol=1e-4)
-    gscale = np.abs(res.grad_q).reshape(-1, 7) + st["bk"]["scale"]
-    check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), gscale, "grad_q", tol=1e-4)
+    kw = e2e_kw(res, wl)
+    r1 = check_close(out["cost_traj"], res.cost_traj, what="cost_traj", **kw["cost_traj"])
+    r2 = check_close(out["grad_q"].reshape(-1, 7), res.grad_q.reshape(-1, 7), what="grad_q", **kw["grad_q"])
+    print(f"fp32 end-to-end: max err/limit cost_traj {r1:.3g}, grad_q {r2:.3g}")
 
 
 @pytest.mark.parametrize("n_chunks,pinned", [(1, True), (5, True), (0, True), (7, False)])
@@ -437,10 +489,17 @@ def test_discrete_h1_and_best_per_problem(vb):
     r = Rollout(wl)
     r.run()
     out = r.results()
-    res = orc.rollout_workload(wl)
-    st = res.stages
-    scale = (st["world"]["cost_scale"].reshape(-1) + st["self"]["cost_scale"]).reshape(wl.B, 1)
-    check_close(out["cost_traj"], res.cost_traj, scale.sum(1), "cost_traj h=1", tol=1e-3)
+    # 43-bit formats: compare stage-wise (the GPU's own packed intermediates)
+    f = r.ctx.formats
+    p = wl.params
+    os_w = r.packed(0)
+    ws = orc.world_stage(os_w, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot, wl.B, 1,
+                         p["eta_world"], p["w_world"], 0, p["sweep_steps"], f[3])
+    ss = orc.self_stage(os_w, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    ck = cost_kw(ws, ss)
+    check_close(out["cost_traj"], ws["cost"].reshape(-1) + ss["cost"], what="cost_traj h=1", **ck)
+    check_codes(r.packed(3), ws["v"], fmt=f[3], cols=156, what="closest_pt h=1",
+                max_steps=step_bound(f[3]), **world_kw(ws))
     bc = torch.empty(1, dtype=torch.float32, device="cuda")
     bs = torch.empty(1, dtype=torch.int32, device="cuda")
     vb.vapr_best_per_problem(r.cost_traj, 1, 5, bc, bs)
@@ -448,37 +507,55 @@ def test_discrete_h1_and_best_per_problem(vb):
     assert bs.item() == int(np.argmin(ct)) and bc.item() == ct.min()
 
 
-def test_full_size_sampled(vb):
-    """config4 at full size (2.56M poses, the bench launch), checked on a
-    sample of trajectories the oracle can recompute one by one."""
+@pytest.mark.parametrize("storage", ["sparse", "dense"])
+def test_full_size_sampled(vb, storage):
+    """config4 at full size (2.56M poses) in the bench's launch -- sparse
+    storage is the bench default -- checked on a sample of trajectories the
+    oracle recomputes one by one: every packed tensor (out_spheres,
+    closest_pt_swept, out_vec, grad_out_spheres) and the FP32 outputs."""
+    from oracle import sparse as osp
     from paper_2310_07854_b200.rollout import Rollout
     wl = config4()
-    r = Rollout(wl)
+    r = Rollout(wl, sparse=(storage == "sparse"))
     r.run()
     out = r.results()
     rng = np.random.default_rng(0)
     picks = np.sort(rng.choice(wl.B, 12, replace=False))
+    picks[-1] = wl.B - 1                   # the last trajectory (tail tile) too
     f = r.ctx.formats
+    p = wl.params
+    cols = 156
     for b in picks:
-        sub = make_workload("sample", [wl.envs[wl.world_idx[b]]], [0], 1, wl.H, f)
-        sub.q = wl.q[b:b + 1].copy()
         w = wl.world_idx[b]
-        sub.cuboids = wl.cuboids[wl.world_offsets[w]:wl.world_offsets[w + 1]]
-        sub.world_offsets = np.array([0, len(sub.cuboids)], np.int32)
-        sub.world_idx = np.zeros(1, np.int32)
+        cub = wl.cuboids[wl.world_offsets[w]:wl.world_offsets[w + 1]]
+        offs = np.array([0, len(cub)], np.int32)
+        q = wl.q[b:b + 1].reshape(-1, 7)
         rows = slice(b * wl.H, (b + 1) * wl.H)
-        os_w = r.packed(0)[rows]
-        _, v = orc.fk_stage(sub.q.reshape(-1, 7), wl.robot, f[0])
-        check_codes(os_w, v, 1.0, f[0], 156, what=f"out_spheres traj {b}")
-        gos_w = r.packed(1)[rows]
-        bk = orc.bk_stage(sub.q.reshape(-1, 7), gos_w, f[1], wl.robot)
+        os_w = r.packed(0, rows)
+        _, v = orc.fk_stage(q, wl.robot, f[0])
+        check_codes(os_w, v, 1.0, 0.0, f[0], cols, what=f"out_spheres traj {b}")
+        ws = orc.world_stage(os_w, f[0], np.zeros(1, np.int32), cub, offs, wl.robot, 1, wl.H,
+                             p["eta_world"], p["w_world"], 1, p["sweep_steps"], f[4])
+        ss = orc.self_stage(os_w, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+        if storage == "sparse":
+            cp_w, ov_w = r.packed_masked(4, rows), r.packed_masked(2, rows)
+            sg = r.sparse_gos(rows)
+            gos_w = codec.pack(osp.densify(sg["mask"], sg["row_words"], *f[1], cols), *f[1])
+        else:
+            cp_w, ov_w, gos_w = r.packed(4, rows), r.packed(2, rows), r.packed(1, rows)
+        check_codes(cp_w, ws["v"], fmt=f[4], cols=cols, what=f"closest_pt_swept traj {b}",
+                    max_steps=step_bound(f[4]), **world_kw(ws))
+        check_codes(ov_w, ss["v"], fmt=f[2], cols=cols, what=f"out_vec traj {b}",
+                    max_steps=step_bound(f[2]), **self_kw(ss))
+        ag = orc.aggregate_stage(cp_w, f[4], ov_w, f[2], f[1], cols)
+        check_codes(gos_w, ag["v"], ag["terms"], 0.0, f[1], cols, what=f"grad_out_spheres traj {b}",
+                    max_steps=step_bound(f[1]))
+        bk = orc.bk_stage(q, gos_w, f[1], wl.robot)
         check_close(out["grad_q"][b], bk["grad_q"], bk["scale"], f"grad_q traj {b}")
-        ws = orc.world_stage(os_w, f[0], sub.world_idx, sub.cuboids, sub.world_offsets, wl.robot, 1,
-                             wl.H, 0.025, 1.0, 1, 1, f[4])
-        ss = orc.self_stage(os_w, f[0], wl.robot, 0.01, 1.0, f[2])
-        ref = ws["cost"].reshape(-1) + ss["cost"]
-        sc = ws["cost_scale"].reshape(-1) + ss["cost_scale"]
-        check_close(out["cost_pose"][b], ref, sc, f"cost_pose traj {b}")
+        ck = cost_kw(ws, ss)
+        check_close(out["cost_pose"][b], ws["cost"].reshape(-1) + ss["cost"], what=f"cost_pose traj {b}", **ck)
+        check_close(np.atleast_1d(out["cost_traj"][b]), np.atleast_1d(ws["cost"].sum() + ss["cost"].sum()),
+                    ck["terms"].sum(), f"cost_traj {b}", kappa=ck["kappa"].sum())
 
 
 @pytest.mark.parametrize("name", ["config2", "mixed_envs", "bookshelf_tall", "fp32", "ragged_43"])

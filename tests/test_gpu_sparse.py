@@ -20,7 +20,7 @@ import torch
 from oracle import codec
 from oracle import rollout as orc
 from oracle import sparse as osp
-from parity_utils import check_close, check_codes
+from parity_utils import check_close, check_codes, ik_kw
 from workloads import config4, config_iko
 
 pytestmark = pytest.mark.gpu
@@ -206,12 +206,16 @@ def check_pair(wl, a, b):
                                        for m, o in zip(sg["mask"], sg["off"])], *fg, cols)
     g_words = codec.pack(g_codes, *fg)
     ag = orc.aggregate_stage(b.packed_masked(slot), f[slot], b.packed_masked(2), f[2], fg, cols)
-    check_codes(g_words, ag["v"], 0.0, fg, cols, what="sparse grad_out_spheres")
+    check_codes(g_words, ag["v"], ag["terms"], 0.0, fg, cols, what="sparse grad_out_spheres")
     bk = orc.bk_stage(wl.q.reshape(-1, 7), g_words, fg, wl.robot)
     ik = orc.ik_terms(wl.q, wl.world_idx, wl.robot, p, getattr(wl, "goals", None), wl.H)
     ref = bk["grad_q"] + (ik[1] if ik is not None else 0.0)
-    scale = bk["scale"] + (10.0 * (ik[0][:, None] + 1.0) if ik is not None else 0.0)
-    check_close(rb["grad_q"].reshape(-1, 7), ref, scale, "grad_q")
+    terms, kappa = bk["scale"], 0.0
+    if ik is not None:
+        G = np.asarray(wl.goals, np.float64)[np.repeat(wl.world_idx, wl.H)]
+        ikw = ik_kw(wl.q, wl.robot, G, p["w_pose_pos"], p["w_pose_rot"], p["w_bound"])["grad"]
+        terms, kappa = terms + ikw["terms"], ikw["kappa"]
+    check_close(rb["grad_q"].reshape(-1, 7), ref, terms, "grad_q", kappa=kappa)
     return rb
 
 

@@ -174,6 +174,53 @@ def test_quantize_f64_matches_f32_path(fmt):
         np.testing.assert_array_equal(a, codec.quantize(x, *fmt))
 
 
+def _between_fp32_doubles(E, M, key):
+    """Doubles that are NOT FP32 values: each format midpoint (the RNE tie)
+    nudged by +-2^-40 relative, and random doubles -- the inputs on which a
+    double -> FP32 -> ExMy double rounding would differ from one rounding."""
+    mags = codec.representable_magnitudes(E, M)
+    mids = (mags[:-1] + mags[1:]) / 2
+    rng = np.random.default_rng(key)
+    rnd = rng.uniform(-1.0, 1.0, 20000) * 2.0 ** rng.integers(-30, 20, 20000)
+    x = np.concatenate([mids * (1 + 2.0 ** -40), mids * (1 - 2.0 ** -40), rnd])
+    x = x[np.isfinite(x)]
+    x = x[x.astype(np.float32).astype(np.float64) != x]
+    return np.concatenate([x, -x])
+
+
+@pytest.mark.parametrize("fmt", [f for f in ALL_FORMATS if 1 + f[0] + f[1] <= 16])
+def test_quantize_f64_single_rounding_vs_enumeration(fmt):
+    """quantize_f64 pinned on non-FP32 doubles by the independent enumeration
+    oracle (nearest magnitude, ties to the even code) -- a double rounding
+    (double -> FP32 -> ExMy) fails at the nudged midpoints."""
+    x = _between_fp32_doubles(*fmt, key=17)
+    np.testing.assert_array_equal(codec.quantize_f64(x, *fmt), codec.quantize_enum_f64(x, *fmt))
+
+
+def test_quantize_f64_vs_numpy_float16_and_float32():
+    """numpy's float64 -> float16 and float64 -> float32 conversions round once
+    (RNE) from the double: E5M10 below 65520 and E8M23 on finite values."""
+    x = _between_fp32_doubles(5, 10, key=19)
+    x = x[np.abs(x) < 65520.0]
+    np.testing.assert_array_equal(codec.quantize_f64(x, 5, 10),
+                                  x.astype(np.float16).view(np.uint16).astype(np.uint32))
+    y = _between_fp32_doubles(8, 7, key=23)
+    np.testing.assert_array_equal(codec.quantize_f64(y, 8, 23), y.astype(np.float32).view(np.uint32))
+
+
+def test_quantize_f64_double_rounding_traps():
+    """Hand-worked (reading c4, one rounding): 1 + 2^-4 + 2^-30 lies just above
+    the E4M3 tie between 1 (code 0x38) and 1.125 (0x39), so it rounds up to
+    0x39, whereas via FP32 it would first become the tie 1.0625 and then round
+    to the even 1.0.  Likewise 1 + 2^-11 + 2^-40 -> E5M10 1 + 2^-10 (0x3C01),
+    and 2.5 + 2^-30 -> E2M1 3.0 (0x5) instead of the tie's even 2.0 (0x4)."""
+    assert codec.quantize_f64(np.array([1 + 2.0 ** -4 + 2.0 ** -30]), 4, 3)[0] == 0x39
+    assert codec.quantize_f64(np.array([1 + 2.0 ** -4 - 2.0 ** -30]), 4, 3)[0] == 0x38
+    assert codec.quantize_f64(np.array([1 + 2.0 ** -11 + 2.0 ** -40]), 5, 10)[0] == 0x3C01
+    assert codec.quantize_f64(np.array([2.5 + 2.0 ** -30]), 2, 1)[0] == 0x5
+    assert codec.quantize_f64(np.array([2.5]), 2, 1)[0] == 0x4
+
+
 def test_pack_layout_hand_built():
     # E2M1: eight 4-bit codes per word, LSB first (PAPER.md:218 "eight FP4")
     w = codec.pack(np.array([[1, 2, 3, 4, 5, 6, 7, 0]], np.uint32), 2, 1)

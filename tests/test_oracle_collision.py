@@ -23,9 +23,10 @@ def test_sdf_golden_cases():
     for row in golden("sdf_box_cases.txt"):
         cx, cy, cz, sdf, cost, gx, gy, gz = map(float, row)
         c = np.array([[[cx, cy, cz]]])
-        s, _, _ = box_sdf(c, np.eye(3), np.zeros(3), np.array([0.1, 0.2, 0.3]))
+        s = box_sdf(c, np.eye(3), np.zeros(3), np.array([0.1, 0.2, 0.3]))[0]
         assert abs(s[0, 0] - sdf) < 1e-12
-        f, g, _, _, _ = world_point_cost(c, np.array([0.05]), BOX, 0.02, 1.0)
+        r = world_point_cost(c, np.array([0.05]), BOX, 0.02, 1.0)
+        f, g = r["cost"], r["grad"]
         assert abs(f[0, 0] - cost) < 1e-12, (row, f)
         np.testing.assert_allclose(g[0, 0], [gx, gy, gz], atol=1e-12)
 
@@ -48,12 +49,14 @@ def test_translation_and_rotation_invariance():
     yaw = 0.6
     R = np.array([[math.cos(yaw), -math.sin(yaw), 0], [math.sin(yaw), math.cos(yaw), 0], [0, 0, 1]])
     t = np.array([0.3, -0.2, 0.5])
-    f0, g0, _, _, _ = world_point_cost(c, r, BOX, 0.025, 1.0)
+    w0 = world_point_cost(c, r, BOX, 0.025, 1.0)
+    f0, g0 = w0["cost"], w0["grad"]
     moved = cub_row(R, t, (0.1, 0.2, 0.3), np.float32)[None].astype(np.float64)
     Rm = moved[0, 0:9].reshape(3, 3)   # the float32-rounded rotation the world stores
     tm = moved[0, 9:12]
     c2 = c @ Rm.T + tm
-    f1, g1, _, _, _ = world_point_cost(c2, r, moved, 0.025, 1.0)
+    w1 = world_point_cost(c2, r, moved, 0.025, 1.0)
+    f1, g1 = w1["cost"], w1["grad"]
     np.testing.assert_allclose(f1, f0, atol=1e-6)
     np.testing.assert_allclose(g1, g0 @ Rm.T, atol=1e-5)
 
@@ -74,9 +77,10 @@ def test_world_discrete_finite_differences():
     c = rng.uniform(-0.25, 0.25, (1, 1, 12, 3))
     r = rng.uniform(0.04, 0.08, 12)
     cub = np.stack([BOX[0], cub_row(np.eye(3), (0.2, 0.1, 0.0), (0.05, 0.05, 0.05))])
-    cost, grad, _, _, tie = world_cost(c, r, cub, 0.025, 1.3)
+    wc = world_cost(c, r, cub, 0.025, 1.3)
+    cost, grad, tie = wc["cost"], wc["grad"], wc["tie"]
     assert not tie.any()
-    fd = _fd_grad(lambda x: world_cost(x, r, cub, 0.025, 1.3)[0].sum(), c)
+    fd = _fd_grad(lambda x: world_cost(x, r, cub, 0.025, 1.3)["cost"].sum(), c)
     np.testing.assert_allclose(grad, fd, atol=2e-6)
 
 
@@ -86,8 +90,9 @@ def test_world_swept_finite_differences_and_n0():
     c = rng.uniform(-0.3, 0.3, (2, H, S, 3))
     r = rng.uniform(0.04, 0.08, S)
     for n in (1, 2):
-        cost, grad, _, _, _ = world_cost(c, r, BOX, 0.025, 1.0, swept=True, n=n)
-        fd = _fd_grad(lambda x: world_cost(x, r, BOX, 0.025, 1.0, swept=True, n=n)[0].sum(), c)
+        wc = world_cost(c, r, BOX, 0.025, 1.0, swept=True, n=n)
+        cost, grad = wc["cost"], wc["grad"]
+        fd = _fd_grad(lambda x: world_cost(x, r, BOX, 0.025, 1.0, swept=True, n=n)["cost"].sum(), c)
         np.testing.assert_allclose(grad, fd, atol=2e-6)
     d = world_cost(c, r, BOX, 0.025, 1.0)
     s0 = world_cost(c, r, BOX, 0.025, 1.0, swept=True, n=0)
@@ -100,9 +105,10 @@ def test_swept_through_slab_hits_only_at_sample():
     slab = cub_row(np.eye(3), (0, 0, 0), (0.01, 1.0, 1.0))[None]
     c = np.array([[[[-0.5, 0, 0]], [[0.5, 0, 0]]]])
     r = np.array([0.05])
-    cost_d = world_cost(c, r, slab, 0.025, 1.0)[0]
+    cost_d = world_cost(c, r, slab, 0.025, 1.0)["cost"]
     assert not cost_d.any()                                  # endpoints free
-    cost_s, grad_s, _, _, _ = world_cost(c, r, slab, 0.025, 1.0, swept=True, n=1)
+    ws_ = world_cost(c, r, slab, 0.025, 1.0, swept=True, n=1)
+    cost_s, grad_s = ws_["cost"], ws_["grad"]
     # midpoint at the slab centre: sdf = -0.01, phi = 0.05+0.025+0.01 = 0.085 > eta
     assert abs(cost_s[0, 0] - (0.085 - 0.0125)) < 1e-12 and cost_s[0, 1] == 0
     # gradient split (1 - tau, tau) = (0.5, 0.5) between the endpoints; the
@@ -114,7 +120,8 @@ def test_swept_through_slab_hits_only_at_sample():
 def test_self_golden_pairs_and_action_reaction():
     for d, cost, gnorm in (map(float, r) for r in golden("self_pair_cases.txt")):
         c = np.array([[[0.0, 0, 0], [d, 0, 0]]])
-        f, g, _, _ = self_cost(c, np.array([0.05, 0.05]), np.array([[0, 1]], np.uint16), 0.01, 1.0)
+        sc = self_cost(c, np.array([0.05, 0.05]), np.array([[0, 1]], np.uint16), 0.01, 1.0)
+        f, g = sc["cost"], sc["grad"]
         assert abs(f[0] - cost) < 1e-12
         assert abs(np.linalg.norm(g[0, 0]) - gnorm) < 1e-12
         np.testing.assert_allclose(g[0, 0], -g[0, 1])
@@ -123,10 +130,27 @@ def test_self_golden_pairs_and_action_reaction():
     rng = np.random.default_rng(3)
     c = rng.uniform(-0.1, 0.1, (3, 10, 3))
     pairs = np.array([(i, j) for i in range(10) for j in range(i + 2, 10)], np.uint16)
-    f, g, _, _ = self_cost(c, np.full(10, 0.05), pairs, 0.01, 1.0)
+    sc = self_cost(c, np.full(10, 0.05), pairs, 0.01, 1.0)
+    f, g = sc["cost"], sc["grad"]
     np.testing.assert_allclose(g.sum(axis=1), 0, atol=1e-12)   # sum out_vec = 0
-    fd = _fd_grad(lambda x: self_cost(x, np.full(10, 0.05), pairs, 0.01, 1.0)[0].sum(), c)
+    fd = _fd_grad(lambda x: self_cost(x, np.full(10, 0.05), pairs, 0.01, 1.0)["cost"].sum(), c)
     np.testing.assert_allclose(g, fd, atol=2e-6)
     # coincident centres -> direction (1, 0, 0)
-    f, g, _, _ = self_cost(np.zeros((1, 2, 3)), np.array([0.05, 0.05]), np.array([[0, 1]], np.uint16), 0.01, 1.0)
+    sc = self_cost(np.zeros((1, 2, 3)), np.array([0.05, 0.05]), np.array([[0, 1]], np.uint16), 0.01, 1.0)
+    f, g = sc["cost"], sc["grad"]
     np.testing.assert_allclose(g[0, 0], [-1, 0, 0])
+
+
+def test_sdf_tie_runner_up_face():
+    """Reading c16: inside a cube at its centre all three faces tie; the
+    gradient takes the lowest index (+x, sign(0) = +1) and the alternative
+    the runner-up face (+y); away from ties the alternative is the gradient."""
+    cube = np.array([0.1, 0.1, 0.1])
+    sdf, g, tie, g_alt, _ = box_sdf(np.zeros((1, 3)), np.eye(3), np.zeros(3), cube)
+    assert tie[0] and sdf[0] == -0.1
+    np.testing.assert_array_equal(g[0], [1.0, 0.0, 0.0])
+    np.testing.assert_array_equal(g_alt[0], [0.0, 1.0, 0.0])
+    c = np.array([[0.05, 0.0, -0.02]])          # x face nearest, no tie
+    sdf, g, tie, g_alt, _ = box_sdf(c, np.eye(3), np.zeros(3), cube)
+    assert not tie[0]
+    np.testing.assert_array_equal(g_alt, g)

@@ -23,8 +23,8 @@ def _total_cost_double(q, wl):
         w = wl.world_idx[b]
         cub = wl.cuboids[wl.world_offsets[w]:wl.world_offsets[w + 1]]
         tot += world_cost(c[b:b + 1], r, cub, p["eta_world"], p["w_world"],
-                          swept=True, n=p["sweep_steps"])[0].sum()
-    tot += self_cost(c.reshape(-1, S, 3), r, wl.robot["pairs"], p["eta_self"], p["w_self"])[0].sum()
+                          swept=True, n=p["sweep_steps"])["cost"].sum()
+    tot += self_cost(c.reshape(-1, S, 3), r, wl.robot["pairs"], p["eta_self"], p["w_self"])["cost"].sum()
     return tot
 
 
@@ -40,8 +40,8 @@ def test_chain_rule_finite_differences():
     for b in range(B):
         w = wl.world_idx[b]
         cub = wl.cuboids[wl.world_offsets[w]:wl.world_offsets[w + 1]]
-        g[b] = world_cost(c[b:b + 1], r, cub, 0.025, 1.0, swept=True, n=1)[1][0]
-    g += self_cost(c.reshape(-1, S, 3), r, wl.robot["pairs"], 0.01, 1.0)[1].reshape(B, H, S, 3)
+        g[b] = world_cost(c[b:b + 1], r, cub, 0.025, 1.0, swept=True, n=1)["grad"][0]
+    g += self_cost(c.reshape(-1, S, 3), r, wl.robot["pairs"], 0.01, 1.0)["grad"].reshape(B, H, S, 3)
     assert np.abs(g).sum() > 0, "workload should have active terms"
     an = backward(q.reshape(-1, 7), g.reshape(-1, S, 3), wl.robot).reshape(B, H, 7)
     h = 1e-6
