@@ -7,7 +7,6 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
-#include <memory>
 #include <new>
 #include <vector>
 
@@ -39,9 +38,6 @@ struct vapr_ctx {
     cudaStream_t par[8] = {};
     // N3: grad_out_spheres in the sparse form (VAPR_OPT_SPARSE)
     int sparse = 0;
-    // self-collision broadphase tables (device copy of SelfDev)
-    SelfDev* d_self = nullptr;
-    SelfDev self{};
     // IKO goals (N2)
     float* d_goals = nullptr;
     int32_t n_goals = 0;
@@ -75,7 +71,7 @@ struct DeviceGuard {
 };
 
 // vapr_cost_grad_sparse_layout entries (N3)
-constexpr int kSparseOffs = 8;
+constexpr int kSparseOffs = 6;
 
 // sparse form of a tensor (N3): pool capacity in words (every row full)
 size_t sparse_pool_words_of(const Fmt& f, int cols, long long rows) {
@@ -222,7 +218,6 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     if (c->d_off) cudaFree(c->d_off);
     if (c->d_sched) cudaFree(c->d_sched);
     if (c->d_goals) cudaFree(c->d_goals);
-    if (c->d_self) cudaFree(c->d_self);
     for (cudaStream_t st : c->par)
         if (st) cudaStreamDestroy(st);
     if (c->s_in) cudaStreamDestroy(c->s_in);
@@ -332,9 +327,42 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
     }
     std::sort(plist.begin(), plist.end());
     plist.erase(std::unique(plist.begin(), plist.end()), plist.end());
-    // the reference sphere of a run [b0, b1) of spheres: the one minimising
-    // max_s(|o_s - o_ref| + r_s); the radius rounded up so the FP32 value
-    // never under-states the double bound
+    R.n_pairs = (int32_t)plist.size();
+    std::vector<std::vector<std::pair<int, int>>> adj(r->n_spheres);   // (partner, pid)
+    for (int k = 0; k < (int)plist.size(); ++k) {
+        R.pair_i[k] = (uint8_t)plist[k].first;
+        R.pair_j[k] = (uint8_t)plist[k].second;
+        adj[plist[k].first].emplace_back(plist[k].second, k);
+        adj[plist[k].second].emplace_back(plist[k].first, k);
+    }
+    for (int a = 0; a < kLinks; ++a)
+        for (int b = 0; b < kLinks; ++b) R.lp_index[a][b] = -1;
+    int nlp = 0;
+    int o = 0;
+    for (int s = 0; s < r->n_spheres; ++s) {
+        R.adj_off[s] = (uint16_t)o;
+        std::vector<std::pair<int, int>>& a = adj[s];
+        std::sort(a.begin(), a.end());
+        const int ls = r->sphere_link[s];
+        int L = 0;
+        for (const auto& pv : a) {
+            const int v = pv.first;
+            const int lv = r->sphere_link[v];
+            while (L <= lv) R.adj_link_off[s][L++] = (uint16_t)o;
+            if (R.lp_index[ls][lv] < 0) {
+                CHECK(nlp < 32, VAPR_ERR_UNSUPPORTED);
+                R.lp_a[nlp] = (int8_t)std::min(ls, lv);
+                R.lp_b[nlp] = (int8_t)std::max(ls, lv);
+                R.lp_index[ls][lv] = R.lp_index[lv][ls] = (int8_t)nlp++;
+            }
+            R.adj_pid[o] = (uint16_t)pv.second;
+            R.adj[o++] = (uint8_t)v;
+        }
+        while (L <= kLinks) R.adj_link_off[s][L++] = (uint16_t)o;
+    }
+    R.adj_off[r->n_spheres] = (uint16_t)o;
+    R.n_link_pairs = nlp;
+    // sub-link groups: the spheres of each link split into two contiguous halves
     auto one_center = [&](int b0, int b1, int& ref, float& rl) {
         ref = b0;
         rl = -1.f;
@@ -353,91 +381,70 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
         }
         if (best < 1e300) rl = std::nextafter((float)best, 3e38f);
     };
-    for (int l = 0; l < kLinks; ++l) one_center(R.link_start[l], R.link_start[l + 1], R.link_ref[l], R.link_rl[l]);
-    // self-collision tables (SelfDev, common.cuh)
-    std::unique_ptr<SelfDev> SD(new SelfDev());
-    std::memset(SD.get(), 0, sizeof(SelfDev));
-    SD->n_pairs = (int32_t)plist.size();
-    for (int k = 0; k < (int)plist.size(); ++k)
-        SD->pij[k] = (uint16_t)(plist[k].first | (plist[k].second << 8));
-    // groups: each link's spheres in contiguous runs of <= kGMax, at least two
-    // runs for a link of >= 4 spheres (a finer cull level), balanced sizes
-    std::vector<int> grp_of(r->n_spheres, 0), grp_link;
+    std::vector<int> grp_of(r->n_spheres, 0);
     int ng = 0;
+    std::vector<int> grp_link;
     for (int l = 0; l < kLinks; ++l) {
-        const int b0 = R.link_start[l], n = R.link_start[l + 1] - b0;
-        if (n == 0) continue;
-        const int k = n <= 3 ? 1 : std::max(2, (n + kGMax - 1) / kGMax);
-        int at = b0;
-        for (int q = 0; q < k; ++q) {
-            const int sz = n / k + (q < n % k ? 1 : 0);
-            CHECK(ng < kMaxGroups && sz <= kGMax, VAPR_ERR_UNSUPPORTED);
-            SD->g_start[ng] = (uint8_t)at;
-            SD->g_n[ng] = (uint8_t)sz;
-            int ref;
-            one_center(at, at + sz, ref, SD->g_rl[ng]);
-            SD->g_ref[ng] = (uint8_t)ref;
-            for (int s2 = at; s2 < at + sz; ++s2) grp_of[s2] = ng;
+        const int b0 = R.link_start[l], b1 = R.link_start[l + 1];
+        if (b1 == b0) continue;
+        const int mid = b0 + (b1 - b0 + 1) / 2;
+        const int cuts[3] = {b0, mid, b1};
+        for (int h = 0; h < 2; ++h) {
+            if (cuts[h + 1] == cuts[h]) continue;
+            one_center(cuts[h], cuts[h + 1], R.grp_ref[ng], R.grp_rl[ng]);
+            for (int s2 = cuts[h]; s2 < cuts[h + 1]; ++s2) grp_of[s2] = ng;
             grp_link.push_back(l);
-            at += sz;
             ++ng;
         }
     }
-    SD->n_groups = ng;
-    // link pairs (a <= b) in ascending order, each with its group pairs
-    // (ga <= gb), each with the listed pairs it holds
-    int nlp = 0, ngp = 0;
-    std::memset(SD->lp_of, -1, sizeof(SD->lp_of));
-    for (int la = 0; la < kLinks; ++la)
-        for (int lb = la; lb < kLinks; ++lb) {
-            const int gp_first = ngp;
-            for (int ga = 0; ga < ng; ++ga) {
-                if (grp_link[ga] != la) continue;
-                for (int gb = (la == lb ? ga : 0); gb < ng; ++gb) {
-                    if (grp_link[gb] != lb) continue;
-                    uint32_t L = 0u;
-                    uint16_t pid[kGMax * kGMax];
-                    for (int u = 0; u < kGMax * kGMax; ++u) pid[u] = 0xFFFFu;
+    R.n_groups = ng;
+    {
+        // group pairs, ordered by link pair then (ga, gb); pair ids of each
+        int ngp = 0, npid = 0;
+        for (int lp = 0; lp < nlp; ++lp) {
+            R.lp_gp_off[lp] = (uint8_t)ngp;
+            for (int ga = 0; ga < ng; ++ga)
+                for (int gb = ga; gb < ng; ++gb) {
+                    const int la = grp_link[ga], lb = grp_link[gb];
+                    if (!((la == R.lp_a[lp] && lb == R.lp_b[lp]) ||
+                          (la == R.lp_b[lp] && lb == R.lp_a[lp])))
+                        continue;
+                    const int start = npid;
                     for (int k = 0; k < (int)plist.size(); ++k) {
-                        const int i = plist[k].first, j = plist[k].second;
-                        if (grp_of[i] != ga || grp_of[j] != gb) continue;
-                        const int u = i - SD->g_start[ga], v = j - SD->g_start[gb];
-                        L |= 1u << (kGMax * u + v);
-                        pid[kGMax * u + v] = (uint16_t)k;
+                        const int gi = grp_of[plist[k].first], gj = grp_of[plist[k].second];
+                        if ((gi == ga && gj == gb) || (gi == gb && gj == ga)) R.gp_pid[npid++] = (uint16_t)k;
                     }
-                    if (!L) continue;
-                    CHECK(ngp < kMaxGP, VAPR_ERR_UNSUPPORTED);
-                    SD->gp_a[ngp] = (uint8_t)ga;
-                    SD->gp_b[ngp] = (uint8_t)gb;
-                    SD->gp_L[ngp] = L;
-                    std::memcpy(SD->gp_pid[ngp], pid, sizeof(pid));
+                    if (npid == start) continue;
+                    CHECK(ngp < kMaxGroupPairs, VAPR_ERR_UNSUPPORTED);
+                    R.gp_a[ngp] = (uint8_t)ga;
+                    R.gp_b[ngp] = (uint8_t)gb;
+                    R.gp_off[ngp] = (uint16_t)start;
                     ++ngp;
                 }
-            }
-            if (ngp == gp_first) continue;
-            SD->lp_a[nlp] = (uint8_t)la;
-            SD->lp_b[nlp] = (uint8_t)lb;
-            SD->lp_of[la][lb] = (int8_t)nlp;
-            SD->lp_gp0[nlp] = (uint16_t)gp_first;
-            ++nlp;
         }
-    SD->lp_gp0[nlp] = (uint16_t)ngp;
-    SD->n_lp = nlp;
-    SD->n_gp = ngp;
-    {
-        DeviceGuard g(c->device);
-        CHECK(g.ok, VAPR_ERR_CUDA);
-        if (!c->d_self && cudaMalloc(&c->d_self, sizeof(SelfDev)) != cudaSuccess) {
-            c->d_self = nullptr;
-            cudaGetLastError();
-            return VAPR_ERR_CUDA;
-        }
-        // synchronous: the host table is freed on return and no kernel of
-        // this context may read a half-written table
-        if (cudaMemcpy(c->d_self, SD.get(), sizeof(SelfDev), cudaMemcpyHostToDevice) != cudaSuccess)
-            return cuda_status(cudaGetLastError());
+        R.lp_gp_off[nlp] = (uint8_t)ngp;
+        R.gp_off[ngp] = (uint16_t)npid;
     }
-    c->self = *SD;
+    // per-link reference sphere: the sphere minimising max_s(|o_s - o_ref| + r_s)
+    for (int l = 0; l < kLinks; ++l) {
+        R.link_ref[l] = R.link_start[l];
+        R.link_rl[l] = -1.f;
+        double best = 1e300;
+        for (int a = R.link_start[l]; a < R.link_start[l + 1]; ++a) {
+            double m = 0.0;
+            for (int b = R.link_start[l]; b < R.link_start[l + 1]; ++b) {
+                const double dx = (double)R.sx[b] - R.sx[a], dy = (double)R.sy[b] - R.sy[a],
+                             dz = (double)R.sz[b] - R.sz[a];
+                m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz) + (double)R.sr[b]);
+            }
+            if (m < best) {
+                best = m;
+                R.link_ref[l] = a;
+            }
+        }
+        // round up so the FP32 radius never under-states the double bound
+        if (best < 1e300) R.link_rl[l] = std::nextafter((float)best, 3e38f);
+    }
     c->robot = R;
     c->robot_set = true;
     return VAPR_OK;
@@ -648,9 +655,8 @@ static vapr_status collision_common(vapr_ctx* c, const uint32_t* os, const int32
     a.cp = cp;
     a.ov = ov;
     const Fmt& fcp = c->dfmt[swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT];
-    cudaError_t e = launch_collision(c->robot, c->d_self, c->self, worlds_of(c),
-                                     c->dfmt[VAPR_OUT_SPHERES], fcp, c->dfmt[VAPR_OUT_VEC], a,
-                                     c->d_sched, &c->sched_next, s);
+    cudaError_t e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], fcp,
+                                     c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     if (e == cudaSuccess && cost_traj) e = launch_traj_reduce(cost, B, H, cost_traj, s);
     return cuda_status(e);
 }
@@ -720,46 +726,37 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
     off[VAPR_OUT_SPHERES] = o;
     o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_SPHERES], cols, P));
     const int cps = swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
+    off[cps] = o;
+    // reserve the larger of the two collision slots so one workspace serves both modes
+    o = align256(o + std::max(packed_bytes(c->dfmt[VAPR_CLOSEST_PT], cols, P),
+                              packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
+    off[VAPR_OUT_VEC] = o;
+    o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
     if (c->sparse) {
-        // N3: the three gradient tensors in the sparse form -- per row a
-        // sphere bitmap and the non-zero codes packed at pool + row * wmax
-        // (closest_pt[_swept], out_vec), or at the row's own offset
-        // (grad_out_spheres; off [P] and the words-in-use counter)
         size_t so[kSparseOffs];
-        so[0] = o;                                            // gos mask [P] uint64
+        so[0] = o;                                            // mask [P] uint64
         o = align256(o + sizeof(uint64_t) * (size_t)P);
-        so[1] = o;                                            // gos off [P] uint32
+        so[1] = o;                                            // off [P] uint32
         o = align256(o + sizeof(uint32_t) * (size_t)P);
-        so[2] = o;                                            // gos used
+        so[2] = o;                                            // used
         o = align256(o + sizeof(uint32_t));
-        so[3] = o;                                            // gos pool
+        so[3] = o;                                            // pool
         const size_t pw = sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P);
         o = align256(o + sizeof(uint32_t) * pw);
         so[4] = o;                                            // closest_pt bitmaps [P]
         o = align256(o + sizeof(uint64_t) * (size_t)P);
         so[5] = o;                                            // out_vec bitmaps [P]
         o = align256(o + sizeof(uint64_t) * (size_t)P);
-        so[6] = o;                                            // closest_pt pool (either slot)
-        o = align256(o + sizeof(uint32_t) *
-                             std::max(sparse_pool_words_of(c->dfmt[VAPR_CLOSEST_PT], cols, P),
-                                      sparse_pool_words_of(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
-        so[7] = o;                                            // out_vec pool
-        o = align256(o + sizeof(uint32_t) * sparse_pool_words_of(c->dfmt[VAPR_OUT_VEC], cols, P));
         if (sp)
             for (int i = 0; i < kSparseOffs; ++i) sp[i] = so[i];
         if (pool_words) *pool_words = pw;
     } else {
-        off[cps] = o;
-        // reserve the larger of the two collision slots so one workspace serves both modes
-        o = align256(o + std::max(packed_bytes(c->dfmt[VAPR_CLOSEST_PT], cols, P),
-                                  packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
-        off[VAPR_OUT_VEC] = o;
-        o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
         off[VAPR_GRAD_OUT_SPHERES] = o;
         o = align256(o + packed_bytes(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P));
     }
     *cost_off = o;
     o = align256(o + sizeof(float) * (size_t)P);
+    o = align256(o + sizeof(float) * (size_t)P);     // the self pass's cost (after cost_off)
     *total = o;
 }
 
@@ -809,13 +806,15 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         return reinterpret_cast<uint32_t*>(ws + off[slot]) + p0 * row_words_of(c->dfmt[slot], cols);
     };
     uint32_t* os = rows_of(VAPR_OUT_SPHERES);
-    uint32_t *cp = nullptr, *ov = nullptr, *gos = nullptr;
-    // N3: the gradient tensors in the sparse form (rows p0.. of the bitmaps,
-    // pool segments and offsets; grad_out_spheres' pool cursor is shared by
-    // all chunks)
+    uint32_t* cp = rows_of(cps);
+    uint32_t* ov = rows_of(VAPR_OUT_VEC);
+    uint32_t* gos = c->sparse ? nullptr : rows_of(VAPR_GRAD_OUT_SPHERES);
+    // N3: grad_out_spheres in the sparse form (rows p0.. of mask / off; the
+    // pool and its cursor are shared by all chunks)
     SparseOut spo{};
     SparseIn spi{};
     unsigned long long *cp_mask = nullptr, *ov_mask = nullptr;
+    float* self_cost = nullptr;
     if (c->sparse) {
         size_t so[kSparseOffs], pw, o2[VAPR_NUM_SLOTS], co2, tot2;
         ws_layout(c, (long long)B * H, p->swept, o2, &co2, &tot2, so, &pw);
@@ -826,18 +825,12 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         spo.seg0 = (uint32_t)sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, p0);
         cp_mask = reinterpret_cast<unsigned long long*>(ws + so[4]) + p0;
         ov_mask = reinterpret_cast<unsigned long long*>(ws + so[5]) + p0;
-        cp = reinterpret_cast<uint32_t*>(ws + so[6]) + sparse_pool_words_of(c->dfmt[cps], cols, p0);
-        ov = reinterpret_cast<uint32_t*>(ws + so[7]) + sparse_pool_words_of(c->dfmt[VAPR_OUT_VEC], cols, p0);
         spi.mask = spo.mask;
         spi.off = spo.off;
         spi.pool = spo.pool;
-    } else {
-        cp = rows_of(cps);
-        ov = rows_of(VAPR_OUT_VEC);
-        gos = rows_of(VAPR_GRAD_OUT_SPHERES);
     }
     const float* qc = q + p0 * kJoints;
-    // IKO terms (N2): FK writes cost_pose = pose + bound, the collision pass adds
+    // IKO terms (N2): FK writes cost_pose = pose + bound, the collision passes add
     IkArgs ik{};
     ik.goals = c->d_goals;
     ik.n_goals = c->n_goals;
@@ -870,13 +863,20 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.cost_accumulate = iko ? 1 : 0;
         a.cp_mask = cp_mask;
         a.ov_mask = ov_mask;
-        e = launch_collision(c->robot, c->d_self, c->self, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES],
-                             c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
+        {   // the self pass's separate cost (workspace, after the scratch cost_pose)
+            size_t o3[VAPR_NUM_SLOTS], co3, tot3;
+            ws_layout(c, (long long)B * H, p->swept, o3, &co3, &tot3);
+            self_cost = reinterpret_cast<float*>(ws + align256(co3 + sizeof(float) * (size_t)B * H)) + p0;
+        }
+        a.self_cost = self_cost;
+        e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
+                             c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
-    if (e == cudaSuccess && cost_traj)
-        e = launch_traj_reduce(cpose + p0, nb, H, cost_traj + b0, s);
+    // combines the self pass's cost into cost_pose (always) and sums cost_traj
     if (e == cudaSuccess)
-        e = c->sparse ? launch_aggregate_sparse(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
+        e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost);
+    if (e == cudaSuccess)
+        e = c->sparse ? launch_aggregate_masked(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
                                                 ov, ov_mask, P, spo, s)
                       : launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],

@@ -1,34 +1,33 @@
 // collision.cu -- a3 + a4: world (sphere-vs-cuboid, discrete or swept) and
-// self (sphere-pair) collision costs and their gradients in ONE pass over the
-// packed out_spheres, writing packed closest_pt[_swept] / out_vec (dense rows,
-// or the N3 sparse form).
+// self (sphere-pair) collision costs and their gradients, reading packed
+// out_spheres and writing packed closest_pt[_swept] / out_vec.
 // P:86 ("Robot-environment and robot-self distance queries are utilized in the
 // cost function"), P:189 (tensor roles).  Cost form: DESIGN.md readings
 // c13-c17 (box SDF, smooth hinge, summed over cuboids / listed pairs; swept =
 // linear sub-samples with the exact gradient to both endpoints).
 //
-// Lane = pose.  A warp owns a tile of 32 consecutive poses (31 plus a halo
-// pose when trajectories do not align with 32-pose tiles), decodes their
-// packed rows once into an FP32 tile in shared memory laid out [element][33]
-// (a uniform element index across the lanes is a conflict-free read), and
-// then every lane evaluates its own pose with warp-uniform loops:
-//  1. world broadphase: the spheres of a link lie in a ball around a
-//     reference sphere (rigid radius, host-computed, plus the quantisation
-//     margin); per (link, cuboid) a ball-box distance test -- for the swept
-//     cost a ball around the segment (pose, next pose) -- gives per-lane
-//     cuboid masks;
-//  2. world narrowphase over the links some lane has live, sphere by sphere:
-//     the pose's own term and, swept, the samples of its forward segment,
-//     each sample evaluated ONCE: the lane keeps (1 - tau) of its gradient
-//     and hands tau of it to the next pose's lane (shuffle); a sample is
-//     skipped when the endpoint SDFs already prove it inactive (the box SDF
-//     is 1-Lipschitz: sdf(p_j) >= sdf(c_h) - tau |c_h+1 - c_h|, and from the
-//     other end);
-//  3. self broadphase: link pairs (link balls), group pairs (balls of runs of
-//     <= 5 spheres), then sphere-vs-group-ball, then the listed sphere pairs;
-//     active pairs are marked in a per-pose pair-id bitmask;
-//  4. self gradients: per touched sphere, the active pairs in pair-id order.
-// Every lane writes its own pose's outputs (no atomics).
+// One warp per tile of kTP = 31 consecutive poses, one pose per lane, plus
+// the halo poses p0-1 and p0+31 for the swept samples (warps are independent:
+// no CTA barrier in the tile loop; the robot tables are staged once per CTA):
+//  1. load the packed rows (16-byte loads, all in flight) and decode them into
+//     an FP32 tile (odd row stride: lane-per-pose accesses are conflict-free);
+//     track the largest decoded coordinate;
+//  2. broadphase, 32 poses per instruction.  The spheres of a link (or of a
+//     half-link group) lie in a ball around a reference sphere whose radius is
+//     rigid (computed once on the host) plus the quantisation-error margin.
+//     World: per (segment, link, cuboid) -- or per (pose, link, cuboid) for
+//     the discrete cost -- a cull bit from the squared distance of the ball
+//     centre to the box.  Self: per (pose, link pair) a ball-ball test that
+//     selects half-link group pairs;
+//  3. the sparse work goes through warp work queues (every lane gets an item):
+//     live (pose, sphere) world items gather the complete gradient of the
+//     sphere (no scatter) and OR its codes into shared packed rows (OR is
+//     order-independent); live (pose, group pair) self items test the group
+//     balls and then the candidate sphere pairs, marking active pairs in a
+//     per-pose bitmask over canonical pair ids; (pose, touched sphere) items
+//     gather the self gradient over the active pairs in id order.  Costs come
+//     back to the pose's lane and are summed in a fixed order;
+//  4. the packed rows are streamed out with coalesced 16-byte stores.
 //
 // Culling is exact: a term is skipped only when its bound clears the
 // activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
@@ -48,40 +47,20 @@ namespace vapr {
 namespace {
 
 constexpr float kSlack = 1e-4f;
-constexpr int kTS = 33;            // FP32 tile row stride (lanes 0..31 + the halo pose)
 
-#ifndef VAPR_COLL_WARPS           // warps per CTA
-#define VAPR_COLL_WARPS 4
-#endif
-#ifndef VAPR_COLL_MINB_W          // CTAs per SM the register allocation targets (world, self)
-#define VAPR_COLL_MINB_W 2
-#endif
-#ifndef VAPR_COLL_MINB_S
-#define VAPR_COLL_MINB_S 2
-#endif
-constexpr int kWarps = VAPR_COLL_WARPS;
+struct Acc {
+    float cost, gx, gy, gz;
+};
 
 struct Cub {
     float4 q0, q1, q2, q3;   // R^T (9), t (3), h (3), pad
 };
 
-__device__ __forceinline__ Cub load_cub(const float4* c) {
-    return Cub{__ldg(c), __ldg(c + 1), __ldg(c + 2), __ldg(c + 3)};
-}
-
-struct WTerm {
-    float sdf;               // the box SDF, or a lower bound of it when inactive
-    float h, s;              // hinge value and -w h'(phi) (0 when inactive)
-    float gx, gy, gz;        // world-frame SDF gradient (valid when s != 0)
-};
-
-// One sphere-vs-cuboid term at centre c with activation distance A = r + eta.
-__device__ __forceinline__ WTerm world_term(const Cub& b, float cx, float cy, float cz, float A,
-                                            float eta, float inv_eta, float hoe, float w) {
-    WTerm t;
-    t.h = 0.f;
-    t.s = 0.f;
-    t.gx = t.gy = t.gz = 0.f;
+// One sphere-vs-cuboid term: adds cw * w * h(phi) to the cost and
+// -gw * w * h'(phi) * grad sdf to the gradient.
+__device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, float cz, float A,
+                                           float eta, float inv_eta, float half_over_eta,
+                                           float w, float cw, float gw, Acc& acc) {
     const float dx = cx - b.q2.y, dy = cy - b.q2.z, dz = cz - b.q2.w;
     const float px = fmaf(b.q0.x, dx, fmaf(b.q0.y, dy, b.q0.z * dz));
     const float py = fmaf(b.q0.w, dx, fmaf(b.q1.x, dy, b.q1.y * dz));
@@ -89,20 +68,19 @@ __device__ __forceinline__ WTerm world_term(const Cub& b, float cx, float cy, fl
     const float ux = fabsf(px) - b.q3.x, uy = fabsf(py) - b.q3.y, uz = fabsf(pz) - b.q3.z;
     const float umax = fmaxf(ux, fmaxf(uy, uz));
     // sdf >= umax in FP32 (sqrt(fl(a^2)) rounds back to a; adding terms only
-    // grows it), so A - umax <= 0 implies phi = A - sdf <= 0: exact early out,
-    // and umax is a valid lower bound of the SDF for the swept sample cull
-    t.sdf = umax;
-    if (A - umax <= 0.f) return t;
-    float glx, gly, glz;
+    // grows it), so A - umax <= 0 implies phi = A - sdf <= 0: exact early out.
+    if (A - umax <= 0.f) return;
+    float sdf, glx, gly, glz;
     if (umax <= 0.f) {                 // inside: nearest face, lowest index on ties
+        sdf = umax;
         glx = gly = glz = 0.f;
         if (ux >= uy && ux >= uz) glx = (px >= 0.f) ? 1.f : -1.f;
         else if (uy >= uz) gly = (py >= 0.f) ? 1.f : -1.f;
         else glz = (pz >= 0.f) ? 1.f : -1.f;
     } else {
         const float ox = fmaxf(ux, 0.f), oy = fmaxf(uy, 0.f), oz = fmaxf(uz, 0.f);
-        // |o| and 1/|o| from one MUFU rsqrt (~2 ulp; parity tolerance), the
-        // IEEE path for arguments near the FP32 underflow
+        // |o| and 1/|o| from one MUFU rsqrt (~2 ulp; parity tolerance 1e-5),
+        // the IEEE path for arguments near the FP32 underflow
         const float o2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
         float on, inv;
         if (o2 >= 1e-30f) {
@@ -112,37 +90,97 @@ __device__ __forceinline__ WTerm world_term(const Cub& b, float cx, float cy, fl
             on = sqrtf(o2);
             inv = 1.f / on;
         }
-        t.sdf = on;
+        sdf = on;
         glx = (px >= 0.f) ? ox * inv : -(ox * inv);
         gly = (py >= 0.f) ? oy * inv : -(oy * inv);
         glz = (pz >= 0.f) ? oz * inv : -(oz * inv);
     }
-    const float phi = A - t.sdf;
-    if (phi <= 0.f) return t;
-    float dh;
+    const float phi = A - sdf;
+    if (phi <= 0.f) return;
+    float h, dh;
     if (phi <= eta) {
-        t.h = phi * phi * hoe;
+        h = phi * phi * half_over_eta;
         dh = phi * inv_eta;
     } else {
-        t.h = phi - 0.5f * eta;
+        h = phi - 0.5f * eta;
         dh = 1.f;
     }
-    t.s = -w * dh;
+    acc.cost = fmaf(cw * w, h, acc.cost);
     // world gradient = R g_local with R = (R^T)^T
-    t.gx = fmaf(b.q0.x, glx, fmaf(b.q0.w, gly, b.q1.z * glz));
-    t.gy = fmaf(b.q0.y, glx, fmaf(b.q1.x, gly, b.q1.w * glz));
-    t.gz = fmaf(b.q0.z, glx, fmaf(b.q1.y, gly, b.q2.x * glz));
-    return t;
+    const float gxw = fmaf(b.q0.x, glx, fmaf(b.q0.w, gly, b.q1.z * glz));
+    const float gyw = fmaf(b.q0.y, glx, fmaf(b.q1.x, gly, b.q1.w * glz));
+    const float gzw = fmaf(b.q0.z, glx, fmaf(b.q1.y, gly, b.q2.x * glz));
+    const float sc = -w * dh * gw;
+    acc.gx = fmaf(sc, gxw, acc.gx);
+    acc.gy = fmaf(sc, gyw, acc.gy);
+    acc.gz = fmaf(sc, gzw, acc.gz);
 }
 
-// Self pair (i, j), i < j, at centres ci, cj: false when inactive; else the
-// gradient contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the
-// cost w h.  Rs = r_i + r_j + eta.
-__device__ __forceinline__ bool self_pair(float ix, float iy, float iz, float jx, float jy, float jz,
-                                          float Rs, float eta, float inv_eta, float hoe, float w,
-                                          float& vx, float& vy, float& vz, float& cost) {
-    const float dx = ix - jx, dy = iy - jy, dz = iz - jz;
+// N3 masked rows (not zero-filled): a sphere with a non-zero code sets its
+// bitmap bit and overwrites its three fields (clear, then OR: the other
+// spheres' fields of a shared word are untouched)
+__device__ __forceinline__ void or_code3_masked(uint32_t* row, int e, float vx, float vy, float vz,
+                                                const Fmt& f, uint32_t rc,
+                                                unsigned long long* pmask) {
+    const float v[3] = {vx, vy, vz};
+    uint32_t c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c[k] = (__float_as_uint(v[k]) != 0u) ? encode(v[k], f) : 0u;
+    if (!(c[0] | c[1] | c[2])) return;
+    atomicOr(pmask, 1ull << (e / 3));
+    int cw = -1;
+    uint32_t acc = 0u, fm = 0u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int ec = e + k;
+        const int w = int((ec * rc) >> 16);
+        if (w != cw) {
+            if (cw >= 0) {
+                atomicAnd(row + cw, ~fm);
+                if (acc) atomicOr(row + cw, acc);
+            }
+            cw = w;
+            acc = fm = 0u;
+        }
+        const int sh = (ec - w * f.pf) * f.t;
+        acc |= c[k] << sh;
+        fm |= f.mask << sh;
+    }
+    atomicAnd(row + cw, ~fm);
+    if (acc) atomicOr(row + cw, acc);
+}
+
+// OR the codes of the vector (vx, vy, vz) at elements e .. e+2 into a packed
+// row: codes sharing a word go in one atomic, +0 components (code 0, the
+// sparse common case) in none.
+__device__ __forceinline__ void or_code3(uint32_t* row, int e, float vx, float vy, float vz,
+                                         const Fmt& f, uint32_t rc) {
+    const float v[3] = {vx, vy, vz};
+    int cw = -1;
+    uint32_t acc = 0u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int ec = e + c;
+        const int w = int((ec * rc) >> 16);            // ec / pf (ec < 4096)
+        if (w != cw) {
+            if (acc) atomicOr(row + cw, acc);
+            cw = w;
+            acc = 0u;
+        }
+        if (__float_as_uint(v[c]) != 0u) acc |= encode(v[c], f) << ((ec - w * f.pf) * f.t);
+    }
+    if (acc) atomicOr(row + cw, acc);
+}
+
+// Self pair (i, j), i < j: false when inactive; else the gradient
+// contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
+__device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const float* sr,
+                                          float eta, float inv_eta, float hoe, float w, float& vx,
+                                          float& vy, float& vz, float& cost) {
+    const float dx = crow[3 * i] - crow[3 * j], dy = crow[3 * i + 1] - crow[3 * j + 1],
+                dz = crow[3 * i + 2] - crow[3 * j + 2];
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float Rs = sr[i] + sr[j] + eta;
     // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so d2 >= fl(Rs^2)
     // implies fl(sqrt(d2)) >= Rs, i.e. phi <= 0: exact early out.
     if (d2 >= Rs * Rs) return false;
@@ -179,304 +217,378 @@ __device__ __forceinline__ bool self_pair(float ix, float iy, float iz, float jx
 }
 
 // ---------------------------------------------------------------------------
-// Per-pose output of one gradient tensor: dense rows (zero-filled per tile,
-// then the words holding non-zero codes rewritten) or the N3 sparse form (the
-// row's sphere bitmap and its non-zero codes packed in ascending sphere order
-// at pool + pose * wmax; reading c42).  Spheres arrive in ascending order; one
-// writer per pose at a time.
-struct RowOut {
-    uint32_t word;        // sparse: the word being filled
-    uint32_t qnw;         // sparse: codes in `word` (low 8 bits), words written (<< 8)
-    unsigned long long mask;
-    float cost;           // the pose's cost terms carried with its codes (world)
-    uint32_t pad;
+// Shared-memory carve-up, computed once on the host and passed by value:
+// the robot tables every warp of the CTA reads (staged once per CTA), then one
+// private workspace per warp.
+#ifndef VAPR_DEC_LOADS          // 16-byte loads in flight per lane in the tile decode
+#define VAPR_DEC_LOADS 2
+#endif
+#ifndef VAPR_FUSED_SPLIT         // 1: world and self as two passes
+#define VAPR_FUSED_SPLIT 1
+#endif
+#ifndef VAPR_MAX_WARPS          // cap on warps per (persistent, one per SM) CTA
+#define VAPR_MAX_WARPS 16
+#endif
+#ifndef VAPR_GRAB                // consecutive tiles a warp takes per scheduler grab
+#define VAPR_GRAB 1
+#endif
+constexpr int kDecLoads = VAPR_DEC_LOADS;
+constexpr int kGrab = VAPR_GRAB;
+#ifdef VAPR_STATS
+// work counters of the variant build -DVAPR_STATS (scripts/collision_stats.py)
+__device__ unsigned long long g_stats[8];
+#define VAPR_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define VAPR_STAT(i, v)
+#endif
+constexpr int kLPP = 2;            // lanes per pose: lane = half * 16 + p
+constexpr int kPL = 32 / kLPP;     // pose lanes per half
+constexpr int kTP = kPL - 1;       // poses per warp tile (pose lane kPL-1: the halo pose)
+constexpr int kTR = kTP + 2;       // tile rows: poses p0 - 1 .. p0 + kTP
+constexpr int kLH = (kLinks + kLPP - 1) / kLPP;   // links per half in the world broadphase
+constexpr int kQ = 128;            // work-queue window (items)
+
+struct Geo {
+    int Wos, Wcp, Wov;             // packed row words
+    int Qos;                       // 16-byte groups per out_spheres row
+    int cs;                        // FP32 tile row stride (odd: lane-per-pose access is conflict-free)
+    int pmw;                       // words of the per-pose active-pair mask
+    int ngp, npairs, nlp, S;
+    uint32_t rc_cp, rc_ov;         // e / pf reciprocals (16-bit fixed point)
+    uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
+    unsigned long long lmask[kLinks];   // spheres of each link
+    // CTA tables (byte offsets from the start of dynamic shared memory)
+    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, slink, lrec, lgp, tables;
+    // per-warp workspace (byte offsets from the warp's base), its size
+    unsigned rows, pmask, pwm, wm, pk0, qi, qc, warp;
 };
 
-__device__ __forceinline__ void out_put(RowOut& o, uint32_t* row, bool sparse, int s, float vx,
-                                        float vy, float vz, const Fmt& f, uint32_t rc) {
-    const float v[3] = {vx + 0.f, vy + 0.f, vz + 0.f};
-    uint32_t c[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) c[k] = (__float_as_uint(v[k]) != 0u) ? encode(v[k], f) : 0u;
-    if (!(c[0] | c[1] | c[2])) return;
-    if (sparse) {
-        o.mask |= 1ull << s;
-        int q = int(o.qnw & 0xffu), nw = int(o.qnw >> 8);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            o.word |= (f.t == 32) ? c[k] : (c[k] << (q * f.t));
-            if (++q == f.pf) {
-                row[nw++] = o.word;
-                o.word = 0u;
-                q = 0;
-            }
-        }
-        o.qnw = uint32_t(q) | (uint32_t(nw) << 8);
-    } else {
-        // the row was zero-filled at the tile start: OR the codes into the
-        // words holding them (one writer per pose)
-        int cw = -1;
-        uint32_t acc = 0u;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const int e = 3 * s + k;
-            const int w = int((uint32_t(e) * rc) >> 16);      // e / pf (e < 4096)
-            if (w != cw) {
-                if (acc) row[cw] |= acc;
-                cw = w;
-                acc = 0u;
-            }
-            acc |= (f.t == 32) ? c[k] : (c[k] << ((e - w * f.pf) * f.t));
-        }
-        if (acc) row[cw] |= acc;
-    }
-}
-
-__device__ __forceinline__ void out_finish(RowOut& o, uint32_t* row, bool sparse,
-                                           unsigned long long* mask_out) {
-    if (!sparse) return;
-    const int q = int(o.qnw & 0xffu), nw = int(o.qnw >> 8);
-    if (q) row[nw] = o.word;
-    *mask_out = o.mask;
-}
-
-// ---------------------------------------------------------------------------
-// The pose tile: FP32 values [E][kTS] (element e of the pose in column col at
-// e * kTS + col), E = Wos * pf (padded rows: the decode needs no bounds checks).
-__device__ __forceinline__ void tsph(const float* T, int s, int col, float& x, float& y, float& z) {
-    const float* c = T + 3 * s * kTS + col;
-    x = c[0];
-    y = c[kTS];
-    z = c[2 * kTS];
-}
-
-// Warp pairs: the two warps of a pair share one 32-pose tile.  The even warp
-// (W) runs the world cost, the odd warp (S) the self cost and writes the
-// pose's total; both unpack the tile.  Shared-memory carve-up (bytes): CTA
-// tables (pair table, sphere radii), then per pair: the tile; W's region (link
-// masks [kLinks][32], world of each pose, link blocks, per-pose output
-// states, item window, world costs); S's region (active-pair bitmask
-// [pmw][32], live group pairs, touched / word masks, item window); the pair's
-// exchange words.  The unpacking's staging (kStage 16-byte groups per thread
-// in flight) spans W's and S's regions.
-constexpr int kStage = 7;
-constexpr int kPairs = kWarps / 2;
-struct LinkBlk {
-    uint32_t pm;          // poses (lanes) with a live cuboid for the link
-    int start, cnt;       // first item, poses
-    float rcp;            // 1 / cnt
-};
-struct PairX {
-    long long tile;
-    float amax[2];
-};
-struct CGeo {
-    int Wos;                      // packed out_spheres row words
-    int Qos;                      // 16-byte groups per row
-    uint32_t rc_q;                // q / Qos reciprocal (20-bit fixed point)
-    int Wcp, Wov;                 // dense output row words
-    int wmax_cp, wmax_ov;         // sparse output row capacity (words)
-    uint32_t rc_cp, rc_ov;        // e / pf reciprocals (16-bit fixed point)
-    int pmw;                      // active-pair bitmask words per pose
-    int own0;                     // 1: lane 0 is the halo pose p0 - 1 (swept, unaligned H)
-    unsigned off_sr, cta_bytes;   // CTA tables: pair table at 0, radii at off_sr
-    // per pair
-    unsigned off_wm, off_kk, off_lb, off_rs, off_qdw, off_qrw, off_wc;
-    unsigned off_pm, off_gl, off_tc, off_wk, off_qds, off_qrs, off_x, w_bytes, s_bytes;
-};
-
-CGeo make_cgeo(const RobotDev& R, const SelfDev& SD, const Fmt& fos, const Fmt& fcp,
-               const Fmt& fov, const CollisionArgs& a) {
-    CGeo g{};
+Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
+             int do_self) {
+    Geo g{};
     g.Wos = row_words_of(fos, R.cols);
+    g.Wcp = do_world ? row_words_of(fcp, R.cols) : 0;
+    g.Wov = do_self ? row_words_of(fov, R.cols) : 0;
     g.Qos = g.Wos / 4;
-    g.rc_q = (1u << 20) / (uint32_t)g.Qos + 1u;      // exact for q < kTS * Qos (checked)
-    for (int q = 0; q < kTS * g.Qos; ++q)
-        if (int((uint32_t(q) * g.rc_q) >> 20) != q / g.Qos) g.rc_q = 0;
-    g.Wcp = row_words_of(fcp, R.cols);
-    g.Wov = row_words_of(fov, R.cols);
-    g.wmax_cp = (R.cols + fcp.pf - 1) / fcp.pf;
-    g.wmax_ov = (R.cols + fov.pf - 1) / fov.pf;
+    int cs = std::max(R.cols, g.Wos * fos.pf);
+    g.cs = cs | 1;
+    g.pmw = (R.n_pairs + 31) >> 5;
+    g.ngp = R.lp_gp_off[R.n_link_pairs];
+    g.npairs = R.n_pairs;
+    g.nlp = R.n_link_pairs;
+    g.S = R.n_spheres;
     g.rc_cp = 65536u / fcp.pf + 1u;
     g.rc_ov = 65536u / fov.pf + 1u;
-    g.pmw = a.do_self ? (SD.n_pairs + 31) / 32 : 0;
-    // swept tiles must hold whole segments: 32 poses per tile when every
-    // trajectory boundary is a tile boundary, else 31 plus the halo pose
-    g.own0 = (a.do_world && a.swept && (32 % a.H) != 0) ? 1 : 0;
-    g.off_sr = (unsigned)((2 * SD.n_pairs + 15) & ~15);
-    g.cta_bytes = g.off_sr + 4u * kMaxSpheres;
-    unsigned o = (unsigned)(4 * g.Wos * fos.pf * kTS);
-    auto take = [&](unsigned bytes) {
-        o = (o + 15u) & ~15u;
+    g.rc_q = (1u << 20) / (uint32_t)g.Qos + 1u;     // exact for q < kTR * Qos (checked below)
+    for (int q = 0; q < kTR * g.Qos; ++q)
+        if (int((uint32_t(q) * g.rc_q) >> 20) != q / g.Qos) g.rc_q = 0;
+    for (int l = 0; l < kLinks; ++l) {
+        unsigned long long m = 0;
+        for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) m |= 1ull << s;
+        g.lmask[l] = m;
+    }
+    unsigned o = 0;
+    auto take = [&](unsigned bytes, unsigned align) {
+        o = (o + align - 1) / align * align;
         const unsigned at = o;
         o += bytes;
         return at;
     };
-    const unsigned t_end = o;
-    // W (world kernel)
-    g.off_wm = take(4u * kLinks * 32u);
-    g.off_kk = take(4u * 32u);
-    g.off_lb = take((unsigned)sizeof(LinkBlk) * kLinks);
-    g.off_rs = take((unsigned)sizeof(RowOut) * 32u);
-    g.off_qdw = take(4u * 32u);
-    g.off_qrw = take(16u * 32u);
-    g.off_wc = take(4u * 32u);
-    g.w_bytes = std::max(o, t_end + 16u * kStage * 32u);
-    // S (self kernel), from the tile's end again
-    o = t_end;
-    g.off_pm = take(4u * g.pmw * 32u);
-    g.off_gl = take(8u * (SD.n_gp + 1));
-    g.off_tc = take(8u * 32u);
-    g.off_wk = take(4u * 32u);
-    g.off_qds = take(4u * 32u);
-    g.off_qrs = take(16u * 32u);
-    g.s_bytes = std::max(o, t_end + 16u * kStage * 32u);
-    g.off_x = 0;
-    g.w_bytes = (g.w_bytes + 15u) & ~15u;
-    g.s_bytes = (g.s_bytes + 15u) & ~15u;
+    g.sr = take(4u * kMaxSpheres, 4);
+    g.rl = take(4u * 3 * kLinks, 4);
+    g.ref = take(4u * 3 * kLinks, 4);
+    g.pij = take(2u * g.npairs, 2);
+    g.prec = take(8u * g.npairs, 8);
+    g.gpid = take(2u * g.npairs, 2);
+    g.grec = take(8u * kMaxGroupPairs, 8);
+    g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
+    g.slink = take(kMaxSpheres, 1);
+    g.lrec = take(8u * 32, 8);
+    g.lgp = take(33, 1);
+    g.tables = take(0, 16);
+    o = 0;
+    g.rows = take(4u * kTR * g.cs, 16);
+    g.pmask = take(do_self ? 4u * kTP * g.pmw : 0u, 4);
+    g.pwm = take(do_self ? 4u * kTP : 0u, 4);
+    g.wm = take(do_world ? 4u * kTP * kLinks : 0u, 4);
+    g.pk0 = take(do_world ? 4u * kTP : 0u, 4);
+    g.qi = take(2u * kQ, 2);
+    g.qc = take(4u * kQ, 4);
+    g.warp = take(0, 16);
     return g;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+// Warp work queue.  Every lane owns the items given by the set bits of its
+// 128-bit mask (item = p << shift | bit); the warp processes all of them, kQ
+// at a time, LPI lanes per item (fn(item, sub) with sub = 0 .. LPI-1), and,
+// with LPI == 1, each lane gets back the sum of the costs `fn` returned for
+// its own items in ascending bit order (the items of a lane are contiguous in
+// the queue, so the order is fixed by the mask alone and never by which lane
+// processed what).  All lanes must call it.
+template <int LPI, typename Fn>
+__device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long long hi, int p,
+                                            int shift, uint16_t* qi, float* qc, int lane,
+                                            Fn&& fn) {
+    const int n = __popcll(lo) + __popcll(hi);
+    int inc = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    const int T = __shfl_sync(0xffffffffu, inc, 31);
+    const int base = inc - n;
+    float sum = 0.f;
+    int cur = base;
+    for (int win = 0; win < T; win += kQ) {
+        const int wend = win + kQ;
+        while (cur < base + n && cur < wend) {
+            int bit;
+            if (lo) {
+                bit = __ffsll((long long)lo) - 1;
+                lo &= lo - 1;
+            } else {
+                bit = 63 + __ffsll((long long)hi);
+                hi &= hi - 1;
+            }
+            qi[cur - win] = (uint16_t)((p << shift) | bit);
+            ++cur;
+        }
+        __syncwarp();
+        const int cnt = min(kQ, T - win);
+        if constexpr (LPI == 1) {
+            for (int i = lane; i < cnt; i += 32) qc[i] = fn((int)qi[i], 0);
+            __syncwarp();
+            const int e = min(base + n, win + cnt);
+            for (int idx = max(base, win); idx < e; ++idx) sum += qc[idx - win];
+        } else {
+            const int sub = lane % LPI;
+            for (int i = lane / LPI; i < cnt; i += 32 / LPI) fn((int)qi[i], sub);
+        }
+        __syncwarp();
+    }
+    return sum;
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// the two warps of a pair (named barrier 1 + pair; constant ids)
-__device__ __forceinline__ void pair_sync(int pair) {
-    static_assert(kPairs <= 4, "named barriers 1..4");
-    if (pair == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
-    else if (pair == 1) asm volatile("bar.sync 2, 64;" ::: "memory");
-    else if (pair == 2) asm volatile("bar.sync 3, 64;" ::: "memory");
-    else asm volatile("bar.sync 4, 64;" ::: "memory");
-}
-
-// ---------------------------------------------------------------------------
-template <bool SWEPT, int ROLE>
-__global__ void __launch_bounds__(32 * kWarps, ROLE == 0 ? VAPR_COLL_MINB_W : VAPR_COLL_MINB_S)
-collision_kernel(const __grid_constant__ RobotDev R, const SelfDev* __restrict__ SD,
-                 const CGeo G, const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
+// One warp processes a tile of kTP consecutive poses, one pose per lane (the
+// arithmetic of every broadphase test runs for 32 poses per instruction, with
+// uniform loops and no index math); the sparse narrowphase work (live world
+// spheres, live group pairs, touched spheres) goes through warp work queues
+// so that every lane has an item.  Warps are independent: no CTA barrier in
+// the tile loop.
+// MASKED (N3, VAPR_OPT_SPARSE): per-pose sphere bitmaps instead of zero-filled
+// rows -- its own instantiation, so the dense one carries no extra code (the
+// kernel is instruction-cache sensitive).
+template <bool MASKED>
+__global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
+collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
+                 const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
+    // programmatic dependent launch (vapr_cost_grad): the first pass lets the
+    // second launch at once, so its CTAs take SMs as the first's retire
+    if (a.pdl == 1) asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
-    uint16_t* spij = reinterpret_cast<uint16_t*>(base);            // pair id -> i | j << 8
-    float* ssr = reinterpret_cast<float*>(base + G.off_sr);         // sphere radii
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int role = ROLE;                                      // 0: world, 1: self
-    char* wb = base + G.cta_bytes + (unsigned)warp * (ROLE == 0 ? G.w_bytes : G.s_bytes);
-    float* T = reinterpret_cast<float*>(wb);                        // the tile [E][kTS]
-    uint4* stage = reinterpret_cast<uint4*>(wb + (ROLE == 0 ? G.off_wm : G.off_pm));  // [kStage][32]
-    uint32_t* WM = reinterpret_cast<uint32_t*>(wb + G.off_wm);      // W: [kLinks][32]
-    uint32_t* KK = reinterpret_cast<uint32_t*>(wb + G.off_kk);      // W: [32] k0 | K << 16
-    LinkBlk* LB = reinterpret_cast<LinkBlk*>(wb + G.off_lb);        // W: [kLinks]
-    RowOut* RS = reinterpret_cast<RowOut*>(wb + G.off_rs);          // W: [32] per-pose output
-    float* WC = reinterpret_cast<float*>(wb + G.off_wc);            // W: [32] world cost
-    uint32_t* PM = reinterpret_cast<uint32_t*>(wb + G.off_pm);      // S: [pmw][32]
-    uint2* GL = reinterpret_cast<uint2*>(wb + G.off_gl);            // S: live group pairs
-    unsigned long long* TC = reinterpret_cast<unsigned long long*>(wb + G.off_tc);  // S: touched
-    uint32_t* WK = reinterpret_cast<uint32_t*>(wb + G.off_wk);      // S: pair-mask words
-    uint32_t* QD = reinterpret_cast<uint32_t*>(wb + (role ? G.off_qds : G.off_qdw));  // window items
-    float4* QR = reinterpret_cast<float4*>(wb + (role ? G.off_qrs : G.off_qrw));      // their results
+    float* ssr = reinterpret_cast<float*>(base + G.sr);
+    float* srl = reinterpret_cast<float*>(base + G.rl);        // link_rl[9], grp_rl[18]
+    int* sref = reinterpret_cast<int*>(base + G.ref);          // link_ref[9], grp_ref[18]
+    uint16_t* spij = reinterpret_cast<uint16_t*>(base + G.pij);     // i | j << 8
+    uint2* sprec = reinterpret_cast<uint2*>(base + G.prec);        // candidate pairs in group-pair order
+    uint2* sgrec = reinterpret_cast<uint2*>(base + G.grec);        // group-pair ball tests
+    uint16_t* sgpid = reinterpret_cast<uint16_t*>(base + G.gpid);  // pair id of each record
+    uint16_t* sgpoff = reinterpret_cast<uint16_t*>(base + G.gpoff);
+    uint8_t* slink = reinterpret_cast<uint8_t*>(base + G.slink);
+    uint2* slrec = reinterpret_cast<uint2*>(base + G.lrec);        // link-pair ball tests
+    uint8_t* slgp = reinterpret_cast<uint8_t*>(base + G.lgp);      // group pairs of link pair lp
 
-    const int npairs = a.do_self ? __ldg(&SD->n_pairs) : 0;
-    for (int i = tid; i < npairs; i += blockDim.x) spij[i] = __ldg(&SD->pij[i]);
-    for (int i = tid; i < R.n_spheres; i += blockDim.x) ssr[i] = R.sr[i];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
+    const int PMW = G.pmw;
+
+    // ---- stage the robot tables (once per CTA)
+    for (int i = tid; i < G.S; i += blockDim.x) {
+        ssr[i] = R.sr[i];
+        int l = 0;
+        while (l < kLinks - 1 && i >= R.link_start[l + 1]) ++l;
+        slink[i] = (uint8_t)l;
+    }
+    if (tid < kLinks) {
+        srl[tid] = R.link_rl[tid];
+        sref[tid] = R.link_ref[tid];
+    }
+    if (tid < 2 * kLinks) {
+        srl[kLinks + tid] = R.grp_rl[tid];
+        sref[kLinks + tid] = R.grp_ref[tid];
+    }
+    if (a.do_self) {
+        for (int i = tid; i < G.npairs; i += blockDim.x) {
+            spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
+            // record k of the group-pair order: byte offsets 12 i | 12 j << 16 in
+            // a row, and the activation distance r_i + r_j + eta; its pair id
+            // (needed only for an active pair) in sgpid[k]
+            const int pid = R.gp_pid[i], pi = R.pair_i[pid], pj = R.pair_j[pid];
+            sprec[i] = make_uint2((uint32_t)(12 * pi) | ((uint32_t)(12 * pj) << 16),
+                                  __float_as_uint(R.sr[pi] + R.sr[pj] + a.eta_s));
+            sgpid[i] = (uint16_t)pid;
+        }
+        for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
+        for (int i = tid; i < G.nlp; i += blockDim.x) {
+            // link pair i: byte offsets 12 ref_a | 12 ref_b << 16 in a row and
+            // the static part of the cull distance; its group pairs
+            const int la = R.lp_a[i], lb = R.lp_b[i];
+            slrec[i] = make_uint2((uint32_t)(12 * R.link_ref[la]) | ((uint32_t)(12 * R.link_ref[lb]) << 16),
+                                  __float_as_uint(R.link_rl[la] + R.link_rl[lb] + a.eta_s + kSlack));
+        }
+        for (int i = tid; i <= G.nlp; i += blockDim.x) slgp[i] = R.lp_gp_off[i];
+        for (int i = tid; i < G.ngp; i += blockDim.x) {
+            // byte offsets 12 ref_a | 12 ref_b << 16 in a row, and the static
+            // part of the cull distance
+            const int ga = R.gp_a[i], gb = R.gp_b[i];
+            sgrec[i] = make_uint2((uint32_t)(12 * R.grp_ref[ga]) | ((uint32_t)(12 * R.grp_ref[gb]) << 16),
+                                  __float_as_uint(R.grp_rl[ga] + R.grp_rl[gb] + a.eta_s + kSlack));
+        }
+    }
     __syncthreads();
 
-    const int cols = R.cols;       // (the debug tap's row stride)
-    (void)cols;
+    // ---- the warp's workspace
+    char* wb = base + G.tables + (unsigned)warp * G.warp;
+    float* rows = reinterpret_cast<float*>(wb + G.rows);
+    uint32_t* pmask = reinterpret_cast<uint32_t*>(wb + G.pmask);
+    uint32_t* pwm = reinterpret_cast<uint32_t*>(wb + G.pwm);
+    uint32_t* wm = reinterpret_cast<uint32_t*>(wb + G.wm);
+    int* pk0 = reinterpret_cast<int*>(wb + G.pk0);
+    uint16_t* qi = reinterpret_cast<uint16_t*>(wb + G.qi);
+    float* qc = reinterpret_cast<float*>(wb + G.qc);
+
+    const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
-    const int own0 = G.own0;
-    const int TP = 32 - own0;                     // poses owned per tile
-    const long long n_tiles = (P + TP - 1) / TP;
+    const long long n_tiles = (P + kTP - 1) / kTP;
+    // dynamic scheduling: a warp takes kGrab consecutive tiles at a time
+    // from a global counter (collision-dense tiles cost several times the
+    // average, so static ranges leave a long tail; consecutive tiles share
+    // the problem and its cuboids)
+    unsigned int* sched = a.sched;              // [0] next grab, [1] finished CTAs
+    const long long n_grabs = (n_tiles + kGrab - 1) / kGrab;
+    long long grab = -1, tile = 0, t_end = 0;
+
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
-    const int nsub = SWEPT ? a.sweep_steps : 0;
+    const bool swept = a.do_world && a.swept;
+    const int nsub = swept ? a.sweep_steps : 0;
     const float inv_n1 = 1.f / float(nsub + 1);
     const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
     // the clamp code's value: coordinates at or beyond it may be saturated
     // (all-finite) or inf (IEEE mode: 65536 for E5M10, inf for E8M7)
     const float fmax_os = decode(fos.maxcode, fos);
-    const bool sp_cp = a.cp_mask != nullptr, sp_ov = a.ov_mask != nullptr;
-    unsigned int* sched = a.sched;                // [0] next tile, [1] finished CTAs
 
     for (;;) {
-        unsigned int ti = 0;
-        if (lane == 0) ti = atomicAdd(sched, 1u);
-        const long long tile = __shfl_sync(0xffffffffu, ti, 0);
-        if (tile >= n_tiles) break;
-        const long long p0 = tile * TP - own0;     // pose of lane 0
-        const long long pg = p0 + lane;
-        const bool valid = pg >= 0 && pg < P;
-        const bool owner = valid && lane >= own0;
-        int h = 0;
-        long long b = 0;
-        if (valid) {
-            b = pg / a.H;
-            h = int(pg - b * a.H);
+        if (tile >= t_end) {
+            unsigned int gi = 0;
+            if (lane == 0) gi = atomicAdd(sched, 1u);
+            grab = __shfl_sync(0xffffffffu, gi, 0);
+            if (grab >= n_grabs) break;
+            tile = grab * kGrab;
+            t_end = min(n_tiles, tile + kGrab);
         }
-        // tile rows: poses p0 .. p0 + 32 (row 32 = the pose after lane 31,
-        // needed only by a swept segment crossing the tile end)
-        const bool need_hi = SWEPT && own0 && (p0 + 32 < P);
-        const long long r_lo = max(p0, 0LL);
-        const long long r_hi = min(p0 + (need_hi ? 33 : 32), P);      // exclusive
-        const int row_off = int(r_lo - p0);
+        const long long p0 = tile * kTP;
+        const int np = (int)min((long long)kTP, P - p0);
+        // halo rows p0 - 1 and p0 + 15 only for the swept world pass (the
+        // segments that cross the tile edges); self and discrete need none
+        const long long r_lo = swept ? max(p0 - 1, 0LL) : p0;
+        const long long r_hi = swept ? min(p0 + kTP + 1, P) : p0 + np;   // exclusive
+        const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
+        // the lane's pose p0 + lane = tile row lane + 1 (lane 31: the halo
+        // pose, used only for the segment that ends there)
+        const long long pg = p0 + pl;
+        int h = -1, k0 = 0, K = 0;
+        if (pg < P) {
+            const long long b = pg / a.H;
+            h = int(pg - b * a.H);
+            if (a.do_world) {
+                const int wi = __ldg(a.world_idx + b);
+                if (wi >= 0 && wi < Wd.n_worlds) {
+                    k0 = __ldg(Wd.off + wi);
+                    K = __ldg(Wd.off + wi + 1) - k0;
+                }
+            }
+        }
 
-        // ---- 1. the tile rows into T[e][row]: kStage 16-byte groups per lane
-        // in flight (cp.async into the staging region), unpacked one group at
-        // a time (a compact loop: the kernels are instruction-cache sensitive)
+        // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
         float amax = 0.f;
         {
             const int nq = int(r_hi - r_lo) * G.Qos;
             const uint4* src = os4 + r_lo * G.Qos;
+            float* dst0 = rows + row_off * cs;
             with_pf(fos.pf, [&](auto Pc) {
                 constexpr int PF = decltype(Pc)::value;
-                for (int q0 = 0; q0 < nq; q0 += 32 * kStage) {
+                // kDecLoads 16-byte loads in flight per lane, then one word
+                // at a time through the decoder (few live temporaries)
+                for (int q0 = lane; q0 < nq; q0 += 32 * kDecLoads) {
+                    uint4 v[kDecLoads];
 #pragma unroll
-                    for (int u = 0; u < kStage; ++u) {
-                        const int q = q0 + 32 * u + lane;
-                        if (q < nq) cp_async16(stage + 32 * u + lane, src + q);
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
+                        v[u] = (q < nq) ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
                     }
-                    cp_async_wait_all();
-#pragma unroll 1
-                    for (int u = 0; u < kStage; ++u) {
-                        const int q = q0 + 32 * u + lane;
+#pragma unroll
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
                         if (q >= nq) break;
-                        const uint4 v = stage[32 * u + lane];
                         const int r = int((uint32_t(q) * G.rc_q) >> 20);
                         const int g = q - r * G.Qos;
-                        float* d = T + row_off + r + (4 * PF * g) * kTS;
-                        float x[4 * PF];
+                        float* d = dst0 + r * cs + 4 * PF * g;
                         if constexpr (PF == 2) {
-                            decode_group_t<2>(v, x, fos);
+                            // E5M10 (the 43-bit set): one SWAR special-code test per group
+                            float x[8];
+                            decode_group_t<2>(v[u], x, fos);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                d[j] = x[j];
+                                amax = fmaxf(amax, fabsf(x[j]));
+                            }
                         } else {
-                            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                            const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-                            for (int j4 = 0; j4 < 4; ++j4) decode_word_t<PF>(w4[j4], x + j4 * PF, fos);
-                        }
+                            for (int j4 = 0; j4 < 4; ++j4) {
+                                float x[PF];
+                                decode_word_t<PF>(w4[j4], x, fos);
 #pragma unroll
-                        for (int j = 0; j < 4 * PF; ++j) {
-                            d[j * kTS] = x[j];
-                            amax = fmaxf(amax, fabsf(x[j]));
+                                for (int j = 0; j < PF; ++j) {
+                                    d[j4 * PF + j] = x[j];
+                                    amax = fmaxf(amax, fabsf(x[j]));
+                                }
+                            }
                         }
                     }
                 }
             });
-            amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(amax)));
         }
-        // dense outputs: zero-fill the tile's owned rows (coalesced); the pose
-        // writers then OR in their non-zero codes
-        const long long o_lo = p0 + own0;
-        const int n_own = (int)max(0LL, min((long long)TP, P - o_lo));
-        if (role == 0 && a.do_world && !sp_cp)
-            for (int i = lane; i < n_own * G.Wcp / 4; i += 32)
-                reinterpret_cast<uint4*>(a.cp + o_lo * G.Wcp)[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (role == 1 && a.do_self && !sp_ov)
-            for (int i = lane; i < n_own * G.Wov / 4; i += 32)
-                reinterpret_cast<uint4*>(a.ov + o_lo * G.Wov)[i] = make_uint4(0u, 0u, 0u, 0u);
+        amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(amax)));
+        // the output rows are zero-filled here and their non-zero codes ORed in
+        // with atomics (__syncwarp orders the fill before every lane's atomics)
+        uint32_t* const cpg = a.do_world ? a.cp + p0 * G.Wcp : nullptr;
+        uint32_t* const ovg = a.do_self ? a.ov + p0 * G.Wov : nullptr;
+        // N3 masked rows: only the tile's bitmaps are cleared
+        unsigned long long* const cpm = (MASKED && a.do_world) ? a.cp_mask + p0 : nullptr;
+        unsigned long long* const ovm = (MASKED && a.do_self) ? a.ov_mask + p0 : nullptr;
+        if (cpm) {
+            if (lane < np) cpm[lane] = 0ull;
+        } else if (a.do_world) {
+            for (int i = lane; i < np * G.Wcp / 4; i += 32)
+                reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (a.do_self) {
+            if (ovm) {
+                if (lane < np) ovm[lane] = 0ull;
+            } else {
+                for (int i = lane; i < np * G.Wov / 4; i += 32)
+                    reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
+            if (lane < kTP) pwm[lane] = 0u;
+        }
+        if (a.do_world && half == 0 && pl < kTP) pk0[pl] = k0;
         __syncwarp();
-        if (role == 0) RS[lane] = RowOut{0u, 0u, 0ull, 0.f, 0u};   // (after the staging's last read)
 
         // Quantisation margin: a decoded coordinate y of an FK value x
         // satisfies |y - x| <= 2^-(M+1) |x| + 2^-(bias+M) unless the code
@@ -485,421 +597,350 @@ collision_kernel(const __grid_constant__ RobotDev R, const SelfDev* __restrict__
         bool can_cull = a.cull != 0;
         float margin = 0.f;
         if (fos.kind != KIND_IDENTITY) {
-            if (!(amax < fmax_os)) can_cull = false;
+            if (amax >= fmax_os) can_cull = false;
             const float rel = ldexpf(1.f, -(fos.M + 1));
             const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
             margin = 2.f * 1.7320509f * (rel * amax * 1.01f + sub);
         }
+        const float* myrow = rows + (pl + 1) * cs;
+        const bool owner = half == 0 && pl < np;     // the lane that owns pose pl's results
 
-        // link reference spheres of the lane's pose (registers, static index)
-        float rx[kLinks], ry[kLinks], rz[kLinks];
+        // ---- 2. world
+        float wcost = 0.f;
+        if (a.do_world) {
+            // test ball per link: swept -> the segment (pose pg-1, pose pg),
+            // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
+            // (it bounds every sample on the segment); discrete -> pose pg
+            const bool tv = swept ? (h >= 1) : (pl < np);
+            float bx[kLH], by[kLH], bz[kLH], lim2[kLH];
+            const float* prow = rows + pl * cs;
 #pragma unroll
-        for (int l = 0; l < kLinks; ++l)
-            tsph(T, min(max(R.link_ref[l], 0), R.n_spheres - 1), lane, rx[l], ry[l], rz[l]);
-
-        // self broadphase, link level (needs the reference spheres, which die
-        // after the world broadphase)
-        const float m2 = 2.f * margin + kSlack + a.eta_s;
-        unsigned long long lpm = 0ull;
-        if (role == 1 && a.do_self) {
-            // link pairs: bit i <=> link pair i's balls are within reach (the
-            // reference spheres in registers: a static loop over link pairs)
-#pragma unroll
-            for (int la = 0; la < kLinks; ++la)
-#pragma unroll
-                for (int lb = la; lb < kLinks; ++lb) {
-                    const int i = __ldg(&SD->lp_of[la][lb]);
-                    if (i < 0) continue;
-                    const float dx = rx[la] - rx[lb], dy = ry[la] - ry[lb], dz = rz[la] - rz[lb];
-                    const float lim = R.link_rl[la] + R.link_rl[lb] + m2;
-                    if (owner && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim))
-                        lpm |= 1ull << i;
-                }
-        }
-        float wcost = 0.f, scost = 0.f;
-        // ---- 2. world (W)
-        if (role == 0 && a.do_world) {
-            int k0 = 0, K = 0;
-            if (valid) {
-                const int wi = __ldg(a.world_idx + b);
-                if (wi >= 0 && wi < Wd.n_worlds) {
-                    k0 = __ldg(Wd.off + wi);
-                    K = __ldg(Wd.off + wi + 1) - k0;
-                }
-            }
-            KK[lane] = uint32_t(k0) | (uint32_t(K) << 16);
-            // test balls per link: swept -> the forward segment (pose, next
-            // pose), a ball around both endpoint balls (it bounds every sample
-            // on the segment); discrete -> the pose's own ball
-            const bool has_fwd = SWEPT && valid && h < a.H - 1;
-            const bool tv = SWEPT ? has_fwd : valid;
-            float bx[kLinks], by[kLinks], bz[kLinks], lim2[kLinks];
-#pragma unroll
-            for (int l = 0; l < kLinks; ++l) {
-                float cx = rx[l], cy = ry[l], cz = rz[l];
-                float rr = R.link_rl[l] + margin;
-                if (SWEPT) {
-                    float nx = __shfl_down_sync(0xffffffffu, cx, 1);
-                    float ny = __shfl_down_sync(0xffffffffu, cy, 1);
-                    float nz = __shfl_down_sync(0xffffffffu, cz, 1);
-                    if (lane == 31 && has_fwd)       // the halo row
-                        tsph(T, min(max(R.link_ref[l], 0), R.n_spheres - 1), 32, nx, ny, nz);
-                    if (!has_fwd) nx = cx, ny = cy, nz = cz;
-                    const float dx = nx - cx, dy = ny - cy, dz = nz - cz;
+            for (int u = 0; u < kLH; ++u) {
+                const int l = half * kLH + u;
+                const int lc = min(l, kLinks - 1);
+                const int r3 = 3 * sref[lc];
+                float cx = myrow[r3], cy = myrow[r3 + 1], cz = myrow[r3 + 2];
+                float rr = srl[lc] + margin;
+                if (swept) {
+                    const float dx = prow[r3] - cx, dy = prow[r3 + 1] - cy, dz = prow[r3 + 2] - cz;
                     cx = fmaf(0.5f, dx, cx);
                     cy = fmaf(0.5f, dy, cy);
                     cz = fmaf(0.5f, dz, cz);
                     rr += 0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                 }
-                bx[l] = cx;
-                by[l] = cy;
-                bz[l] = cz;
+                bx[u] = cx;
+                by[u] = cy;
+                bz[u] = cz;
                 const float lim = rr + a.eta_w + kSlack;
-                // a link without spheres: never live
-                lim2[l] = (R.link_rl[l] < 0.f) ? -1.f : lim * lim;
+                // a link without spheres (or past the last link): never live
+                lim2[u] = (l >= kLinks || srl[lc] < 0.f) ? -1.f : lim * lim;
             }
-            uint32_t fm[kLinks];
+            uint32_t fm[kLH];
 #pragma unroll
-            for (int l = 0; l < kLinks; ++l) fm[l] = 0u;
+            for (int u = 0; u < kLH; ++u) fm[u] = 0u;
             const int Kw = __reduce_max_sync(0xffffffffu, tv ? K : 0);
             for (int k = 0; k < Kw; ++k) {
-                const Cub c = load_cub(Wd.cub + 4 * ((k < K) ? k0 + k : 0));
+                const int ci = (k < K) ? k0 + k : 0;
+                const float4 q0 = __ldg(Wd.cub + 4 * ci), q1 = __ldg(Wd.cub + 4 * ci + 1);
+                const float4 q2 = __ldg(Wd.cub + 4 * ci + 2), q3 = __ldg(Wd.cub + 4 * ci + 3);
                 const bool kv = tv && k < K;
 #pragma unroll
-                for (int l = 0; l < kLinks; ++l) {
+                for (int u = 0; u < kLH; ++u) {
                     // squared distance from the ball centre to the box (0 inside)
-                    const float dx = bx[l] - c.q2.y, dy = by[l] - c.q2.z, dz = bz[l] - c.q2.w;
-                    const float px = fmaf(c.q0.x, dx, fmaf(c.q0.y, dy, c.q0.z * dz));
-                    const float py = fmaf(c.q0.w, dx, fmaf(c.q1.x, dy, c.q1.y * dz));
-                    const float pz = fmaf(c.q1.z, dx, fmaf(c.q1.w, dy, c.q2.x * dz));
-                    const float ox = fmaxf(fabsf(px) - c.q3.x, 0.f);
-                    const float oy = fmaxf(fabsf(py) - c.q3.y, 0.f);
-                    const float oz = fmaxf(fabsf(pz) - c.q3.z, 0.f);
+                    const float dx = bx[u] - q2.y, dy = by[u] - q2.z, dz = bz[u] - q2.w;
+                    const float px = fmaf(q0.x, dx, fmaf(q0.y, dy, q0.z * dz));
+                    const float py = fmaf(q0.w, dx, fmaf(q1.x, dy, q1.y * dz));
+                    const float pz = fmaf(q1.z, dx, fmaf(q1.w, dy, q2.x * dz));
+                    const float ox = fmaxf(fabsf(px) - q3.x, 0.f);
+                    const float oy = fmaxf(fabsf(py) - q3.y, 0.f);
+                    const float oz = fmaxf(fabsf(pz) - q3.z, 0.f);
                     const float o2 = fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-                    const bool live = (o2 <= lim2[l]) || (!can_cull && lim2[l] >= 0.f);
-                    if (kv && live) fm[l] |= 1u << k;
+                    const bool live = (o2 <= lim2[u]) || (!can_cull && lim2[u] >= 0.f);
+                    if (kv && live) fm[u] |= 1u << k;
                 }
             }
-            // per pose and link: forward-segment mask (low 16 bits) and the
-            // backward segment's (the previous pose's forward mask, high 16);
-            // the link blocks of the item stream: item = (link, sphere, pose)
-            // for every pose with a live cuboid, sphere-major -- so the pose
-            // after a segment's start holds the next item of the same sphere
-            int tot = 0;
+            // per pose: own / forward / backward cuboid masks of each link
+            // (forward = the segment of pose lane pl + 1, same half)
+            unsigned long long smask = 0ull;
 #pragma unroll
-            for (int l = 0; l < kLinks; ++l) {
-                if (SWEPT) {
-                    const uint32_t bwd = __shfl_up_sync(0xffffffffu, fm[l], 1);
-                    fm[l] |= (lane > 0 && valid && h > 0 ? bwd : 0u) << 16;
+            for (int u = 0; u < kLH; ++u) {
+                const int l = half * kLH + u;
+                uint32_t v, own;
+                if (swept) {
+                    const uint32_t fwd = __shfl_down_sync(0xffffffffu, fm[u], 1);
+                    v = (fwd & 0xffffu) | (fm[u] << 16);
+                    own = fwd | fm[u];
+                } else {
+                    v = own = fm[u];
                 }
-                WM[32 * l + lane] = fm[l];
-                const uint32_t pm = __ballot_sync(0xffffffffu, fm[l] != 0u);
-                const int cnt = __popc(pm);
-                if (lane == l)
-                    LB[l] = LinkBlk{pm, tot, cnt, cnt ? 1.f / float(cnt) : 0.f};
-                tot += cnt * (R.link_start[l + 1] - R.link_start[l]);
+                if (pl < np && l < kLinks) {
+                    wm[pl * kLinks + l] = v;
+                    if (own) smask |= G.lmask[l];
+                }
             }
+            smask |= __shfl_xor_sync(0xffffffffu, smask, kPL);
+            if (!owner) smask = 0ull;
             __syncwarp();
-            // the item stream, 32 items per window
-            float carry_x = 0.f, carry_y = 0.f, carry_z = 0.f;
-            uint32_t carry_id = 0xffffffffu;      // (sphere << 8 | pose) of the window's last item
-            for (int w0 = 0; w0 < tot; w0 += 32) {
-                const int idx = w0 + lane;
-                const bool have = idx < tot;
-                int l = 0;
-#pragma unroll
-                for (int q = 1; q < kLinks; ++q)
-                    if (idx >= LB[q].start) l = q;
-                const LinkBlk lb = LB[l];
-                const int r = idx - lb.start;
-                const int qs = int((float(r) + 0.5f) * lb.rcp);      // exact: r < 2^10, cnt <= 32
-                const int rank = r - qs * lb.cnt;
-                const int s = R.link_start[l] + qs;
-                const int pl = have ? __fns(lb.pm, 0, rank + 1) : 0;
-                float gx = 0.f, gy = 0.f, gz = 0.f, sx = 0.f, sy = 0.f, sz = 0.f, icost = 0.f;
-                if (have) {
-                    const uint32_t m = WM[32 * l + pl];
-                    const uint32_t fwd = m & 0xffffu, own = fwd | (m >> 16);
-                    const uint32_t kk = KK[pl];
-                    const int k0i = int(kk & 0xffffu), Ki = int(kk >> 16);
-                    float cx, cy, cz, nx, ny, nz, L = 0.f;
-                    tsph(T, s, pl, cx, cy, cz);
-                    nx = cx, ny = cy, nz = cz;
-                    if (SWEPT && fwd) {
-                        tsph(T, s, pl + 1, nx, ny, nz);   // pl = 31: the halo row
-                        const float dx = nx - cx, dy = ny - cy, dz = nz - cz;
-                        L = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+            // live (pose, sphere) items: the complete gradient of the sphere
+            // (no scatter), its codes ORed into the packed tile row
+            VAPR_STAT(0, __popcll(smask));
+            wcost = warp_queue<1>(smask, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
+                const int p = it >> 6, sp = it & 63;
+                const int l = slink[sp];
+                const uint32_t v = wm[p * kLinks + l];
+                uint32_t m_own, m_fwd = 0u, m_bwd = 0u;
+                if (swept) {
+                    m_fwd = v & 0xffffu;
+                    m_bwd = v >> 16;
+                    m_own = m_fwd | m_bwd;
+                } else {
+                    m_own = v;
+                }
+                const float4* cub = Wd.cub + 4 * pk0[p];
+                auto cuboid = [&](int kk) -> Cub {
+                    return Cub{__ldg(cub + 4 * kk), __ldg(cub + 4 * kk + 1), __ldg(cub + 4 * kk + 2),
+                               __ldg(cub + 4 * kk + 3)};
+                };
+                const float* crow = rows + (p + 1) * cs;
+                const float cx = crow[3 * sp], cy = crow[3 * sp + 1], cz = crow[3 * sp + 2];
+                const float A = ssr[sp] + a.eta_w;
+                Acc acc{0.f, 0.f, 0.f, 0.f};
+                // terms in a fixed order: the pose itself, the samples of
+                // segment (h, h+1) (cost + (1-tau) grad), the samples of
+                // segment (h-1, h) (tau grad only) -- one call site
+                const float* nrow = crow + cs;
+                const float* qrow = crow - cs;
+                const int nt = 1 + (m_fwd ? nsub : 0) + (m_bwd ? nsub : 0);
+                for (int t = 0; t < nt; ++t) {
+                    float sx = cx, sy = cy, sz = cz, cw = 1.f, gw = 1.f;
+                    uint32_t m = m_own;
+                    if (t > 0) {
+                        const bool fw = m_fwd && t <= nsub;
+                        const int j = fw ? t : t - (m_fwd ? nsub : 0);
+                        const float tau = float(j) * inv_n1, omt = 1.f - tau;
+                        const float* o = fw ? nrow : qrow;
+                        const float ox = o[3 * sp], oy = o[3 * sp + 1], oz = o[3 * sp + 2];
+                        if (fw) {
+                            sx = fmaf(tau, ox, omt * cx);
+                            sy = fmaf(tau, oy, omt * cy);
+                            sz = fmaf(tau, oz, omt * cz);
+                            gw = omt;
+                            m = m_fwd;
+                        } else {
+                            sx = fmaf(tau, cx, omt * ox);
+                            sy = fmaf(tau, cy, omt * oy);
+                            sz = fmaf(tau, cz, omt * oz);
+                            cw = 0.f;
+                            gw = tau;
+                            m = m_bwd;
+                        }
                     }
-                    const float A = ssr[s] + a.eta_w;
-                    for (uint32_t mk = own; mk; mk &= mk - 1) {
-                        const int k = __ffs(mk) - 1;
-                        const bool fw = (fwd >> k) & 1u;
-                        const Cub c = load_cub(Wd.cub + 4 * ((k < Ki) ? k0i + k : 0));
-                        // the SDF at the pose bounds each forward sample's from
-                        // below (1-Lipschitz: sdf(p_j) >= sdf(c_h) - tau |c_h+1 - c_h|)
-                        float sdf0 = -3.0e38f;
-                        // term t = 0: the pose itself (weight 1); t = j >= 1:
-                        // forward sample j, (1 - tau) kept, tau sent to the
-                        // next pose -- one world_term call site
-                        const int nt = (SWEPT && fw) ? nsub : 0;
-                        for (int t = 0; t <= nt; ++t) {
-                            float qx = cx, qy = cy, qz = cz, wo = 1.f, wsend = 0.f;
-                            if (SWEPT && t > 0) {
-                                const float tau = float(t) * inv_n1, omt = 1.f - tau;
-                                if (can_cull && sdf0 - tau * L - A > kSlack) continue;
-                                qx = fmaf(tau, nx, omt * cx);
-                                qy = fmaf(tau, ny, omt * cy);
-                                qz = fmaf(tau, nz, omt * cz);
-                                wo = omt;
-                                wsend = tau;
+                    VAPR_STAT(1, __popc(m));
+                    for (; m; m &= m - 1)
+                        world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
+                                   a.w_w, cw, gw, acc);
+                }
+                uint32_t* orow = cpg + p * G.Wcp;
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp, acc.gx + 0.f);
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 1, acc.gy + 0.f);
+                VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 2, acc.gz + 0.f);
+                if (MASKED)
+                    or_code3_masked(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp,
+                                    G.rc_cp, cpm + p);
+                else
+                    or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
+                return acc.cost;
+            });
+        }
+
+        // ---- 3. self
+        float scost = 0.f;
+        if (a.do_self) {
+            // broadphase, per pose, two levels (the two lanes of a pose split
+            // each list): the link pairs' balls, then the half-link group
+            // pairs of the live link pairs; glo / ghi bit g <=> group pair g
+            // (g < 64 / >= 64) is live
+            const float m2 = 2.f * margin;
+            const char* rb = reinterpret_cast<const char*>(myrow);
+            auto ball = [&](uint2 r) -> bool {
+                const float* ca = reinterpret_cast<const float*>(rb + (r.x & 0xffffu));
+                const float* cb = reinterpret_cast<const float*>(rb + (r.x >> 16));
+                const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
+                const float lim = __uint_as_float(r.y) + m2;
+                return !can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim;
+            };
+            uint32_t lpm = 0u;
+            if (pl < np)
+                for (int lp = half; lp < G.nlp; lp += kLPP)
+                    if (ball(slrec[lp])) lpm |= 1u << lp;
+            lpm |= __shfl_xor_sync(0xffffffffu, lpm, kPL);
+            // group pairs: a uniform loop over the link pairs live for some
+            // pose of the tile, each lane testing its pose's (the two lanes of
+            // a pose alternate over the group pairs)
+            unsigned long long glo = 0ull, ghi = 0ull;
+            for (uint32_t m = __reduce_or_sync(0xffffffffu, lpm); m; m &= m - 1) {
+                const int lp = __ffs(m) - 1;
+                const bool live = (lpm >> lp) & 1u;
+                const int g1 = slgp[lp + 1];
+                for (int g = slgp[lp] + half; g < g1; g += kLPP)
+                    if (live && ball(sgrec[g])) {
+                        if (g < 64) glo |= 1ull << g;
+                        else ghi |= 1ull << (g - 64);
+                    }
+            }
+            static_assert(kLPP == 2, "the exchange below assumes two lanes per pose");
+            glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
+            ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
+            if (!owner) glo = ghi = 0ull;
+            VAPR_STAT(2, __popcll(glo) + __popcll(ghi));
+            // narrowphase: the live (pose, group pair) entries are listed, each
+            // expanded into chunks of <= 4 candidate pairs, one chunk per lane
+            // (balanced whatever the group-pair sizes); active pairs are marked
+            // in the pose's pair-id mask
+            {
+                uint16_t* qx = reinterpret_cast<uint16_t*>(qc);     // kQ floats = 2 kQ chunk items
+                constexpr int kX = 2 * kQ;
+                const int n = __popcll(glo) + __popcll(ghi);
+                int inc = n;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += t;
+                }
+                const int T = __shfl_sync(0xffffffffu, inc, 31);
+                const int base = inc - n;
+                int cur = base;
+                for (int win = 0; win < T; win += kQ) {
+                    while (cur < base + n && cur < win + kQ) {
+                        int bit;
+                        if (glo) {
+                            bit = __ffsll((long long)glo) - 1;
+                            glo &= glo - 1;
+                        } else {
+                            bit = 63 + __ffsll((long long)ghi);
+                            ghi &= ghi - 1;
+                        }
+                        qi[cur - win] = (uint16_t)((pl << 7) | bit);
+                        ++cur;
+                    }
+                    __syncwarp();
+                    const int cnt = min(kQ, T - win);
+                    for (int e0 = 0; e0 < cnt; e0 += 32) {
+                        const int e = e0 + lane;
+                        int nch = 0;
+                        if (e < cnt) {
+                            const int g = qi[e] & 127;
+                            nch = (sgpoff[g + 1] - sgpoff[g] + 3) >> 2;
+                        }
+                        int cinc = nch;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const int t = __shfl_up_sync(0xffffffffu, cinc, d);
+                            if (lane >= d) cinc += t;
+                        }
+                        const int C = __shfl_sync(0xffffffffu, cinc, 31);
+                        const int off = cinc - nch;
+                        for (int cw = 0; cw < C; cw += kX) {
+                            const int c0 = max(0, cw - off), c1 = min(nch, cw + kX - off);
+                            for (int c = c0; c < c1; ++c) qx[off + c - cw] = (uint16_t)(e | (c << 7));
+                            __syncwarp();
+                            const int ccnt = min(kX, C - cw);
+                            for (int i = lane; i < ccnt; i += 32) {
+                                const int xi = qx[i];
+                                const int ent = qi[xi & 127];
+                                const int p = ent >> 7, g = ent & 127;
+                                const float* crow = rows + (p + 1) * cs;
+                                const int k0c = sgpoff[g] + 4 * (xi >> 7);
+                                const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
+                                VAPR_STAT(3, 1);
+                                VAPR_STAT(4, k1c - k0c);
+                                uint32_t wmk = 0u;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int k = k0c + u;
+                                    const uint2 rec = sprec[min(k, k1c - 1)];
+                                    const char* cb8 = reinterpret_cast<const char*>(crow);
+                                    const float* ci = reinterpret_cast<const float*>(cb8 + (rec.x & 0xffffu));
+                                    const float* cj = reinterpret_cast<const float*>(cb8 + (rec.x >> 16));
+                                    const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
+                                    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                                    const float Rs = __uint_as_float(rec.y);
+                                    // d2 >= fl(Rs^2) => phi <= 0 (self_pair's exact early-out);
+                                    // the rare d2 within an ulp of Rs^2 is settled by self_pair
+                                    // in the gather (an inactive marked pair contributes nothing)
+                                    if (k >= k1c || d2 >= Rs * Rs) continue;
+                                    const int pid = sgpid[k];
+                                    atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
+                                    wmk |= 1u << (pid >> 5);
+                                }
+                                if (wmk) atomicOr(pwm + p, wmk);
                             }
-                            const WTerm tm = world_term(c, qx, qy, qz, A, a.eta_w, inv_eta_w, hoe_w, a.w_w);
-                            if (t == 0) sdf0 = tm.sdf;
-                            if (tm.s == 0.f) continue;
-                            icost = fmaf(a.w_w, tm.h, icost);
-                            const float so = tm.s * wo, st = tm.s * wsend;
-                            gx = fmaf(so, tm.gx, gx);
-                            gy = fmaf(so, tm.gy, gy);
-                            gz = fmaf(so, tm.gz, gz);
-                            sx = fmaf(st, tm.gx, sx);
-                            sy = fmaf(st, tm.gy, sy);
-                            sz = fmaf(st, tm.gz, sz);
+                            __syncwarp();
                         }
                     }
                 }
-                // the tau parts of the previous item's forward samples: it is
-                // the same sphere at the previous pose when that pose's segment
-                // ends here (a sent part is then always non-zero only for such)
-                const uint32_t id = have ? (uint32_t(s) << 8) | uint32_t(pl) : 0xffffffffu;
-                float rxs = __shfl_up_sync(0xffffffffu, sx, 1);
-                float rys = __shfl_up_sync(0xffffffffu, sy, 1);
-                float rzs = __shfl_up_sync(0xffffffffu, sz, 1);
-                uint32_t pid_ = __shfl_up_sync(0xffffffffu, id, 1);
-                if (lane == 0) {
-                    rxs = carry_x, rys = carry_y, rzs = carry_z;
-                    pid_ = carry_id;
-                }
-                carry_x = __shfl_sync(0xffffffffu, sx, 31);
-                carry_y = __shfl_sync(0xffffffffu, sy, 31);
-                carry_z = __shfl_sync(0xffffffffu, sz, 31);
-                carry_id = __shfl_sync(0xffffffffu, id, 31);
-                if (SWEPT && have && pid_ + 1u == id) {
-                    gx += rxs;
-                    gy += rys;
-                    gz += rzs;
-                }
-                // outputs: per pose, its items of the window in ascending lane
-                // (= sphere) order, through its output state
-                QR[lane] = make_float4(gx, gy, gz, icost);
-                QD[lane] = uint32_t(s);
-                const uint32_t grp = __match_any_sync(0xffffffffu, have ? pl : 64 + lane);
-                __syncwarp();
-                if (have && lane == __ffs(grp) - 1) {
-                    RowOut o = RS[pl];
-                    uint32_t* row = sp_cp ? a.cp + (p0 + pl) * G.wmax_cp : a.cp + (p0 + pl) * G.Wcp;
-                    const bool own_p = pl >= own0;
-                    for (uint32_t gm = grp; gm; gm &= gm - 1) {
-                        const int j = __ffs(gm) - 1;
-                        const float4 rv = QR[j];
-                        const int sj = int(QD[j]);
-                        o.cost += rv.w;
-                        if (own_p) {
-                            VAPR_TAP(a.swept ? 4 : 3, (p0 + pl) * cols + 3 * sj, rv.x + 0.f);
-                            VAPR_TAP(a.swept ? 4 : 3, (p0 + pl) * cols + 3 * sj + 1, rv.y + 0.f);
-                            VAPR_TAP(a.swept ? 4 : 3, (p0 + pl) * cols + 3 * sj + 2, rv.z + 0.f);
-                            out_put(o, row, sp_cp, sj, rv.x, rv.y, rv.z, fcp, G.rc_cp);
-                        }
-                    }
-                    RS[pl] = o;
-                }
-                __syncwarp();
             }
-            {
-                RowOut o = RS[lane];
-                wcost = o.cost;
-                if (owner) out_finish(o, a.cp + pg * G.wmax_cp, sp_cp, a.cp_mask + pg);
-            }
-        }
-
-
-        // ---- 3. self (S)
-        if (role == 1 && a.do_self) {
-            TC[lane] = 0ull;
-            WK[lane] = 0u;
-            for (int w = 0; w < G.pmw; ++w) PM[32 * w + lane] = 0u;
             __syncwarp();
-            // group pairs of the link pairs some pose has live (uniform
-            // loops, lane = pose): the group-ball test; the group pairs live
-            // for some pose are listed with their poses (a ballot)
-            int ngl = 0, tot = 0;
-            const unsigned long long ulp =
-                ((unsigned long long)__reduce_or_sync(0xffffffffu, (uint32_t)(lpm >> 32)) << 32) |
-                __reduce_or_sync(0xffffffffu, (uint32_t)lpm);
-            for (unsigned long long ul = ulp; ul; ul &= ul - 1) {
-                const int i = __ffsll((long long)ul) - 1;
-                const bool lp_live = (lpm >> i) & 1ull;
-                const int g1 = __ldg(&SD->lp_gp0[i + 1]);
-                for (int gp = __ldg(&SD->lp_gp0[i]); gp < g1; ++gp) {
-                    const int ga = __ldg(&SD->gp_a[gp]), gb = __ldg(&SD->gp_b[gp]);
-                    float ax0, ay0, az0, bx0, by0, bz0;
-                    tsph(T, __ldg(&SD->g_ref[ga]), lane, ax0, ay0, az0);
-                    tsph(T, __ldg(&SD->g_ref[gb]), lane, bx0, by0, bz0);
-                    const float dx = ax0 - bx0, dy = ay0 - by0, dz = az0 - bz0;
-                    const float lim = __ldg(&SD->g_rl[ga]) + __ldg(&SD->g_rl[gb]) + m2;
-                    const bool gl = lp_live && (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim);
-                    const uint32_t bm = __ballot_sync(0xffffffffu, gl);
-                    if (bm) {
-                        if (lane == 0) GL[ngl] = make_uint2(uint32_t(gp) | (uint32_t(tot) << 16), bm);
-                        ++ngl;
-                        tot += __popc(bm);
+            // gradients: one item per (pose, touched sphere), gathered over its
+            // active pairs in canonical id order (for a fixed sphere: its
+            // partners ascending, independent of culling and of the task
+            // order); the item also returns the cost of the pairs it leads
+            // (i == s), so a pose's self cost is summed in pair-id order
+            // the pose's touched spheres, from its active pairs
+            unsigned long long tb = 0ull;
+            if (owner)
+                for (uint32_t wmk = pwm[pl]; wmk; wmk &= wmk - 1) {
+                    const int wd = __ffs(wmk) - 1;
+                    for (uint32_t m = pmask[pl * PMW + wd]; m; m &= m - 1) {
+                        const int ij = spij[(wd << 5) + __ffs(m) - 1];
+                        tb |= (1ull << (ij & 0xff)) | (1ull << (ij >> 8));
                     }
                 }
-            }
-            if (lane == 0) GL[ngl] = make_uint2(uint32_t(tot) << 16, 0u);
-            __syncwarp();
-            // items = (live group pair, pose), group-pair-major, 32 per window
-            // (neighbouring lanes share the group pair's loops): each sphere
-            // vs the other group's ball, then the listed sphere pairs; active
-            // pairs go to the pose's pair-id bitmask
-            {
-                int e = 0;
-                for (int w0 = 0; w0 < tot; w0 += 32) {
-                    const int idx = w0 + lane;
-                    const bool have = idx < tot;
-                    if (have)
-                        while (idx >= int(GL[e + 1].x >> 16)) ++e;
-                    // explicit reconvergence after each divergent loop: the
-                    // item body is the same code for every lane
-                    __syncwarp();
-                    const uint2 ent = GL[e];
-                    const int gp = int(ent.x & 0xffffu);
-                    const int pl = have ? __fns(ent.y, 0, idx - int(ent.x >> 16) + 1) : 0;
-                    const int ga = __ldg(&SD->gp_a[gp]), gb = __ldg(&SD->gp_b[gp]);
-                    const float rla = __ldg(&SD->g_rl[ga]), rlb = __ldg(&SD->g_rl[gb]);
-                    float ax0, ay0, az0, bx0, by0, bz0;
-                    tsph(T, __ldg(&SD->g_ref[ga]), pl, ax0, ay0, az0);
-                    tsph(T, __ldg(&SD->g_ref[gb]), pl, bx0, by0, bz0);
-                    const int sa = __ldg(&SD->g_start[ga]), na = have ? __ldg(&SD->g_n[ga]) : 0;
-                    const int sb = __ldg(&SD->g_start[gb]), nb = have ? __ldg(&SD->g_n[gb]) : 0;
-                    uint32_t ma = 0u, mb = 0u;
-                    // each sphere vs the other group's ball
-#pragma unroll 1
-                    for (int u = 0; u < na; ++u) {
-                        float x, y, z;
-                        tsph(T, sa + u, pl, x, y, z);
-                        const float dx = x - bx0, dy = y - by0, dz = z - bz0;
-                        const float lim = ssr[sa + u] + rlb + m2;
-                        if (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) ma |= 1u << u;
+            VAPR_STAT(5, __popcll(tb));
+            if (owner) VAPR_STAT(6, __popc(pwm[pl]));
+            scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
+                const int p = it >> 6, s = it & 63;
+                const float* crow = rows + (p + 1) * cs;
+                const uint32_t* pm = pmask + p * PMW;
+                float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
+                // the pose's active pairs in id order, those with sphere s
+                for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
+                    const int wd = __ffs(wmk) - 1;
+                    for (uint32_t m = pm[wd]; m; m &= m - 1) {
+                        const int pid = (wd << 5) + __ffs(m) - 1;
+                        const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
+                        if (i != s && j != s) continue;
+                        float vx, vy, vz, c;
+                        // always active here (same test as the narrowphase that marked it)
+                        if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy,
+                                       vz, c))
+                            continue;
+                        const float sg = (i == s) ? -1.f : 1.f;
+                        gx = fmaf(sg, vx, gx);
+                        gy = fmaf(sg, vy, gy);
+                        gz = fmaf(sg, vz, gz);
+                        if (i == s) c_lead += c;
                     }
-                    __syncwarp();
-#pragma unroll 1
-                    for (int v = 0; v < nb; ++v) {
-                        float x, y, z;
-                        tsph(T, sb + v, pl, x, y, z);
-                        const float dx = x - ax0, dy = y - ay0, dz = z - az0;
-                        const float lim = ssr[sb + v] + rla + m2;
-                        if (!can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim) mb |= 1u << v;
-                    }
-                    __syncwarp();
-                    uint32_t cand = 0u;
-#pragma unroll
-                    for (int u = 0; u < kGMax; ++u)
-                        if ((ma >> u) & 1u) cand |= mb << (kGMax * u);
-                    cand &= __ldg(&SD->gp_L[gp]);
-                    // the listed sphere pairs that survive (per lane)
-                    for (; cand; cand &= cand - 1) {
-                        const int bit = __ffs(cand) - 1;
-                        const int u = (bit * 205) >> 10, v = bit - kGMax * u;  // bit / 5, bit % 5
-                        float xi, yi, zi, xj, yj, zj;
-                        tsph(T, sa + u, pl, xi, yi, zi);
-                        tsph(T, sb + v, pl, xj, yj, zj);
-                        const float dx = xi - xj, dy = yi - yj, dz = zi - zj;
-                        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                        const float Rs = ssr[sa + u] + ssr[sb + v] + a.eta_s;
-                        // d2 >= fl(Rs^2) => phi <= 0 (self_pair's exact early
-                        // out); the rare d2 within an ulp of Rs^2 is settled by
-                        // self_pair in the gather
-                        if (d2 >= Rs * Rs) continue;
-                        const int pid = __ldg(&SD->gp_pid[gp][bit]);
-                        atomicOr(PM + 32 * (pid >> 5) + pl, 1u << (pid & 31));
-                        atomicOr(WK + pl, 1u << (pid >> 5));
-                        atomicOr(TC + pl, (1ull << (sa + u)) | (1ull << (sb + v)));
-                    }
-                    __syncwarp();
                 }
-            }
-            // gradients, warp-cooperatively: items = (pose, touched sphere) in
-            // (lane, sphere) order, 32 per window; an item sums its sphere's
-            // active pairs in pair-id order (and the cost of the pairs it
-            // leads, i == s), then each pose's owner takes its items' results
-            // in ascending sphere order -- so the pose's self cost is summed in
-            // pair-id order and its codes leave in ascending sphere order
-            const unsigned long long touched = owner ? TC[lane] : 0ull;
-            const int nt = __popcll(touched);
-            int incl = nt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += t;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
-            const int ibase = incl - nt;
-            RowOut oo{};
-            uint32_t* orow = sp_ov ? a.ov + pg * G.wmax_ov : a.ov + pg * G.Wov;
-            unsigned long long tb = touched;
-            int cur = ibase;
-            for (int w0 = 0; w0 < total; w0 += 32) {
-                for (; tb && cur < w0 + 32; ++cur, tb &= tb - 1)
-                    QD[cur - w0] = uint32_t(lane) | (uint32_t(__ffsll((long long)tb) - 1) << 8);
-                __syncwarp();
-                if (w0 + lane < total) {
-                    const uint32_t d = QD[lane];
-                    const int pl = int(d & 0xffu), s = int(d >> 8);
-                    const uint32_t* pmp = PM + pl;
-                    float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
-                    for (uint32_t wm = WK[pl]; wm; wm &= wm - 1) {
-                        const int wd = __ffs(wm) - 1;
-                        for (uint32_t m = pmp[wd * 32]; m; m &= m - 1) {
-                            const int pid = (wd << 5) + __ffs(m) - 1;
-                            const int ij = spij[pid];
-                            const int i = ij & 0xff, j = ij >> 8;
-                            if (i != s && j != s) continue;
-                            float xi, yi, zi, xj, yj, zj;
-                            tsph(T, i, pl, xi, yi, zi);
-                            tsph(T, j, pl, xj, yj, zj);
-                            float vx, vy, vz, c;
-                            if (!self_pair(xi, yi, zi, xj, yj, zj, ssr[i] + ssr[j] + a.eta_s, a.eta_s,
-                                           inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
-                                continue;
-                            const float sg = (i == s) ? -1.f : 1.f;
-                            gx = fmaf(sg, vx, gx);
-                            gy = fmaf(sg, vy, gy);
-                            gz = fmaf(sg, vz, gz);
-                            if (i == s) c_lead += c;
-                        }
-                    }
-                    QR[lane] = make_float4(gx, gy, gz, c_lead);
-                }
-                __syncwarp();
-                const int lo = max(ibase, w0), hi = min(incl, w0 + 32);
-                for (int idx = lo; idx < hi; ++idx) {
-                    const float4 rv = QR[idx - w0];
-                    const int sq = int(QD[idx - w0] >> 8);
-                    scost += rv.w;
-                    VAPR_TAP(2, pg * cols + 3 * sq, rv.x + 0.f);
-                    VAPR_TAP(2, pg * cols + 3 * sq + 1, rv.y + 0.f);
-                    VAPR_TAP(2, pg * cols + 3 * sq + 2, rv.z + 0.f);
-                    out_put(oo, orow, sp_ov, sq, rv.x, rv.y, rv.z, fov, G.rc_ov);
-                }
-                __syncwarp();
-            }
-            if (owner) out_finish(oo, orow, sp_ov, a.ov_mask + pg);
+                uint32_t* orow = ovg + p * G.Wov;
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 1, gy + 0.f);
+                VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 2, gz + 0.f);
+                if (MASKED)
+                    or_code3_masked(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov, ovm + p);
+                else
+                    or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
+                return c_lead;
+            });
         }
+        if (owner) VAPR_STAT(7, 1);
         if (owner) {
-            const float c = role == 0 ? wcost : scost;
-            a.cost[pg] = a.cost_accumulate ? a.cost[pg] + c : c;
+            const float c = wcost + scost;
+            a.cost[p0 + pl] = a.cost_accumulate ? a.cost[p0 + pl] + c : c;
         }
         __syncwarp();
+
+        ++tile;
     }  // tile loop
     // the last CTA to finish resets the scheduler slot for its next use
     __syncthreads();
@@ -911,15 +952,25 @@ collision_kernel(const __grid_constant__ RobotDev R, const SelfDev* __restrict__
             __threadfence();
         }
     }
+    // the second pass completes only after the first: stream-ordered work
+    // after it (aggregation, BK) sees both passes' outputs
+    if (a.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-__global__ void traj_reduce_kernel(const float* __restrict__ cost_pose, int B, int H,
-                                   float* __restrict__ cost_traj) {
+__global__ void traj_reduce_kernel(float* __restrict__ cost_pose, int B, int H,
+                                   float* __restrict__ cost_traj, const float* __restrict__ add) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     float c = 0.f;
-    for (int h = 0; h < H; ++h) c += cost_pose[(long long)b * H + h];
-    cost_traj[b] = c;
+    for (int h = 0; h < H; ++h) {
+        float v = cost_pose[(long long)b * H + h];
+        if (add) {                      // world (+ IKO) then self: the fused order
+            v = v + add[(long long)b * H + h];
+            cost_pose[(long long)b * H + h] = v;
+        }
+        c += v;
+    }
+    if (cost_traj) cost_traj[b] = c;
 }
 
 __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems, int seeds,
@@ -939,79 +990,132 @@ __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems,
     best_seed[p] = arg;
 }
 
+
 }  // namespace
 
-// World and self as two kernels over the tile rows (each keeps a small
-// instruction working set; out_spheres is read twice).  The CTAs are
-// persistent: as many as fit on the SMs, each warp taking 32-pose tiles from
-// the context's scheduler slot.
-static cudaError_t launch_role(int role, const RobotDev& R, const SelfDev* SD_dev, const SelfDev& SD,
-                               const WorldsDev& W, const Fmt& fos, const Fmt& fcp, const Fmt& fov,
-                               const CollisionArgs& a0, unsigned int* sched_ring,
-                               unsigned int* sched_next, cudaStream_t s) {
-    const long long P = (long long)a0.B * a0.H;
-    CollisionArgs a = a0;
-    // each launch takes the next scheduler slot of the context's ring (the
-    // kernel's last CTA leaves it zeroed); kSchedSlots launches may be in flight
-    const unsigned k = __atomic_fetch_add(sched_next, 1u, __ATOMIC_RELAXED) % kSchedSlots;
-    a.sched = sched_ring + 2 * k;
-    const CGeo G = make_cgeo(R, SD, fos, fcp, fov, a);
+#ifdef VAPR_STATS
+extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+#ifndef VAPR_SPREAD_SMALL
+#define VAPR_SPREAD_SMALL 1
+#endif
+#ifndef VAPR_PDL
+#define VAPR_PDL 1
+#endif
+cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                                  const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                                  cudaStream_t s) {
+    const long long P = (long long)a.B * a.H;
+    const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self);
     if (G.rc_q == 0) return cudaErrorInvalidValue;
-    int dev = 0, sms = 148;
+    int dev = 0, sms = 148, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = G.cta_bytes + (size_t)kWarps * (role == 0 ? G.w_bytes : G.s_bytes);
-    const bool sw = a.do_world && a.swept;
-    auto kern = role == 0 ? (sw ? collision_kernel<true, 0> : collision_kernel<false, 0>)
-                          : (sw ? collision_kernel<true, 1> : collision_kernel<false, 1>);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // as many warps per CTA as shared memory holds (the tables are staged
+    // once per CTA), at most 8; one persistent CTA per SM
+    int nw = (optin - (int)G.tables) / (int)G.warp;
+    nw = std::min(nw, VAPR_MAX_WARPS);
+    if (nw < 1) return cudaErrorInvalidValue;
+    const size_t smem = G.tables + (size_t)nw * G.warp;
+    auto kern = (a.cp_mask || a.ov_mask) ? collision_kernel<true> : collision_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kWarps, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const long long TP = 32 - G.own0;
-    const long long tiles = (P + TP - 1) / TP;
-    // enough CTAs for every warp to have a tile, at most the resident ones
-    const long long grid = std::max(1LL, std::min<long long>((tiles + kWarps - 1) / kWarps,
-                                                             (long long)sms * per_sm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nw, smem);
+    const long long tiles = (P + kTP - 1) / kTP;
+    // enough CTAs for every warp to have a chunk; small batches: spread up to
+    // one CTA per tile over the SMs (latency: a lone SM's issue slots shared
+    // by its 16 warps would serialise the few tiles there are)
+    const long long need = (tiles + kGrab * nw - 1) / (kGrab * nw);
+    const long long spread = VAPR_SPREAD_SMALL ? std::min<long long>(tiles, sms) : need;
+    const long long grid = std::min<long long>(std::max(need, spread),
+                                               (long long)sms * std::max(per_sm, 1));
 #ifdef VAPR_DEBUG_TAP
     const int tw = a.swept ? 4 : 3;
-    const bool tapped = role == 0 ? tap_arm(tw, P, R.cols, s) : tap_arm(2, P, R.cols, s);
+    const bool tap_w = a.do_world && tap_arm(tw, P, R.cols, s);
+    const bool tap_s = a.do_self && tap_arm(2, P, R.cols, s);
 #endif
-    kern<<<(unsigned)grid, 32 * kWarps, smem, s>>>(R, SD_dev, G, W, fos, fcp, fov, a);
+    if (a.pdl == 2) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(32 * nw);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, R, G, W, fos, fcp, fov, a);
+        if (e != cudaSuccess) return e;
+    } else {
+        kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
+    }
 #ifdef VAPR_DEBUG_TAP
-    if (tapped) tap_disarm(role == 0 ? tw : 2, s);
+    if (tap_w) tap_disarm(tw, s);
+    if (tap_s) tap_disarm(2, s);
 #endif
     return cudaGetLastError();
 }
 
-cudaError_t launch_collision(const RobotDev& R, const SelfDev* SD_dev, const SelfDev& SD,
-                             const WorldsDev& W, const Fmt& fos, const Fmt& fcp, const Fmt& fov,
-                             const CollisionArgs& a0, unsigned int* sched_ring,
-                             unsigned int* sched_next, cudaStream_t s) {
+// World and self run as two passes over the tile rows: each pass keeps a
+// smaller instruction working set, which beats re-reading out_spheres.  With
+// a0.self_cost (vapr_cost_grad) the self pass runs first into its own cost
+// array and the world pass is its programmatic dependent launch (traj_reduce
+// adds the two in the fused order); otherwise world first, the self pass
+// adding its cost to the world pass's (the same wcost + scost).
+cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a0,
+                             unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s) {
     const long long P = (long long)a0.B * a0.H;
     if (P <= 0) return cudaSuccess;
-    cudaError_t e = cudaSuccess;
-    if (a0.do_world) {
-        CollisionArgs aw = a0;
-        aw.do_self = 0;
-        e = launch_role(0, R, SD_dev, SD, W, fos, fcp, fov, aw, sched_ring, sched_next, s);
+    // each pass takes the next scheduler slot of the context's ring (the
+    // kernel's last CTA leaves it zeroed); kSchedSlots passes may be in flight
+    auto slot = [&]() {
+        const unsigned k = __atomic_fetch_add(sched_next, 1u, __ATOMIC_RELAXED) % kSchedSlots;
+        return sched_ring + 2 * k;
+    };
+    CollisionArgs a = a0;
+    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self)) {
+        a.sched = slot();
+        return launch_collision_pass(R, W, fos, fcp, fov, a, s);
     }
-    if (e == cudaSuccess && a0.do_self) {
-        CollisionArgs as = a0;
-        as.do_world = 0;
-        as.swept = 0;
-        as.cost_accumulate = a0.do_world ? 1 : a0.cost_accumulate;   // world + self
-        e = launch_role(1, R, SD_dev, SD, W, fos, fcp, fov, as, sched_ring, sched_next, s);
+    CollisionArgs aw = a, as = a;
+    aw.sched = slot();
+    as.sched = slot();
+    aw.do_self = 0;
+    as.do_world = 0;
+    as.cost_accumulate = 1;
+    if (VAPR_PDL && a.self_cost) {
+        // the self pass writes its own cost, so neither pass depends on the
+        // other (both read only out_spheres): the self pass (the longer tail)
+        // runs first and the world pass starts on the SMs its CTAs leave
+        as.cost = a.self_cost;
+        as.cost_accumulate = 0;
+        as.pdl = 1;
+        aw.pdl = 2;
+        cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, as, s);
+        if (e != cudaSuccess) return e;
+        return launch_collision_pass(R, W, fos, fcp, fov, aw, s);
     }
-    return e;
+    cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, aw, s);
+    if (e != cudaSuccess) return e;
+    return launch_collision_pass(R, W, fos, fcp, fov, as, s);
 }
 
-cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s) {
-    if (B <= 0 || cost_traj == nullptr) return cudaSuccess;
-    traj_reduce_kernel<<<(B + 255) / 256, 256, 0, s>>>(cost_pose, B, H, cost_traj);
+cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
+                               cudaStream_t s, const float* add) {
+    if (B <= 0) return cudaSuccess;
+    traj_reduce_kernel<<<(B + 255) / 256, 256, 0, s>>>(cost_pose, B, H, cost_traj, add);
     return cudaGetLastError();
 }
 

@@ -358,34 +358,37 @@ struct RobotDev {
     float q_lo[kJoints], q_hi[kJoints];  // joint limits (bound cost, N2)
     int32_t link_start[kLinks + 1];      // spheres sorted by link
     float sx[kMaxSpheres], sy[kMaxSpheres], sz[kMaxSpheres], sr[kMaxSpheres];
+    // self-collision adjacency (CSR): partners of sphere s are
+    // adj[adj_off[s] .. adj_off[s+1]), each pair listed from both ends, in
+    // ascending partner order; the partners on link L are the sub-range
+    // adj[adj_link_off[s][L] .. adj_link_off[s][L+1]).
+    uint16_t adj_off[kMaxSpheres + 1];
+    uint16_t adj_link_off[kMaxSpheres][kLinks + 1];
+    // link-pair broadphase: index (0..31) of the link pair (a, b) in the
+    // per-pose self mask, -1 when no listed sphere pair joins the two links
+    int8_t lp_index[kLinks][kLinks];
+    int8_t lp_a[32], lp_b[32];           // links of link pair i (lp_a <= lp_b)
+    int32_t n_link_pairs;
     // link bounding spheres: reference sphere of each link and the radius
-    // max_s(|o_s - o_ref| + r_s) over its spheres (rigid: the same in any
-    // pose), -1 for a link without spheres
+    // max_s(|o_s - o_ref| + r_s) over its spheres (rigid: the same in any pose)
     int32_t link_ref[kLinks];
     float link_rl[kLinks];
-};
-
-// Self-collision broadphase tables (built by vapr_set_robot from the pair
-// list; read by the collision kernel from global memory with warp-uniform
-// indices).  Three levels: link pairs (link balls), group pairs (groups =
-// contiguous runs of <= kGMax spheres of one link, each with a reference
-// sphere and a rigid radius), then the listed sphere pairs of a group pair,
-// addressed by (u, v) = (sphere - group start) of each side.
-constexpr int kGMax = 5;
-constexpr int kMaxGroups = 64;
-constexpr int kMaxGP = 320;
-constexpr int kMaxLP = kLinks * (kLinks + 1) / 2;
-struct SelfDev {
-    int32_t n_lp, n_groups, n_gp, n_pairs;
-    uint8_t lp_a[kMaxLP], lp_b[kMaxLP];     // links of link pair i (a <= b)
-    int8_t lp_of[kLinks][kLinks];           // link pair of links (a, b), a <= b; -1: none
-    uint16_t lp_gp0[kMaxLP + 1];            // its group pairs: [lp_gp0[i], lp_gp0[i + 1])
-    uint8_t g_start[kMaxGroups], g_n[kMaxGroups], g_ref[kMaxGroups];
-    float g_rl[kMaxGroups];                 // max_s(|o_s - o_ref| + r_s) over the group (rounded up)
-    uint8_t gp_a[kMaxGP], gp_b[kMaxGP];     // groups of group pair g (same link: a <= b)
-    uint32_t gp_L[kMaxGP];                  // bit kGMax u + v <=> sphere pair (start_a + u, start_b + v) listed
-    uint16_t gp_pid[kMaxGP][kGMax * kGMax]; // its canonical pair id (pairs sorted by (i, j), i < j)
-    uint16_t pij[kMaxPairs];                // pair id -> i | j << 8
+    // canonical pair ids: pairs sorted by (i, j), i < j; adj_pid[jj] is the id
+    // of the pair (s, adj[jj]); pair_i / pair_j map an id back to its spheres
+    int32_t n_pairs;
+    uint16_t adj_pid[2 * kMaxPairs];
+    uint8_t pair_i[kMaxPairs], pair_j[kMaxPairs];
+    // sub-link groups (each link's spheres split in two contiguous halves),
+    // each with a reference sphere and a rigid bounding radius, for the
+    // two-level self-collision broadphase: link pair -> group pairs -> pairs.
+    int32_t n_groups;
+    int32_t grp_ref[2 * kLinks];
+    float grp_rl[2 * kLinks];
+    uint8_t lp_gp_off[33];               // group pairs of link pair lp: [off[lp], off[lp+1])
+    uint8_t gp_a[kMaxGroupPairs], gp_b[kMaxGroupPairs];
+    uint16_t gp_off[kMaxGroupPairs + 1]; // pair ids of group pair g: gp_pid[gp_off[g] ..]
+    uint16_t gp_pid[kMaxPairs];
+    uint8_t adj[2 * kMaxPairs];
 };
 
 // 3x4 rigid transform, row-major rotation r[3][3] and translation p[3].

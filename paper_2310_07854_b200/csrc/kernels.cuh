@@ -26,15 +26,21 @@ struct CollisionArgs {
     float eta_w, w_w, eta_s, w_s;
     int32_t cull;
     float* cost;              // [B*H] (world + self of the enabled parts)
-    uint32_t* cp;             // world gradient: dense rows, or (cp_mask) the sparse pool
-    uint32_t* ov;             // self gradient: dense rows, or (ov_mask) the sparse pool
-    // N3 (VAPR_OPT_SPARSE; nullable = dense rows): per-pose sphere bitmaps.
-    // With them a pose's non-zero codes are packed in ascending sphere order
-    // at pool + pose * ceil(cols / pf) (reading c42)
+    uint32_t* cp;             // packed world gradient (nullable iff !do_world)
+    uint32_t* ov;             // packed self gradient (nullable iff !do_self)
+    // N3 (VAPR_OPT_SPARSE; nullable = dense): per-pose sphere bitmaps of cp / ov.
+    // With them the rows are not zero-filled: a sphere with a non-zero code
+    // sets its bit and overwrites its own fields, and readers take only the
+    // fields of set spheres.
     unsigned long long* cp_mask;
     unsigned long long* ov_mask;
-    int32_t cost_accumulate;  // cost += (this pass) instead of cost =
-    unsigned int* sched;      // internal: tile-scheduler slot {next tile, finished CTAs}, zero
+    // vapr_cost_grad (nullable): the self pass writes its cost here and
+    // traj_reduce adds it, so the self pass may overlap the world pass's tail
+    // (programmatic dependent launch); the order of the sums is unchanged
+    float* self_cost;
+    int32_t pdl;              // internal: 1 = trigger dependents at start, 2 = wait at exit
+    int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
+    unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero
 };
 
 cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t cols,
@@ -58,15 +64,14 @@ inline bool ik_on(const IkArgs& k) { return k.w_pos != 0.f || k.w_rot != 0.f || 
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
                       uint32_t* os, cudaStream_t s, const IkArgs* ik = nullptr,
                       float* ee = nullptr);
-// SD_dev: the device copy of SD (the kernel reads it; the host copy sizes the launch)
-cudaError_t launch_collision(const RobotDev& R, const SelfDev* SD_dev, const SelfDev& SD,
-                             const WorldsDev& W, const Fmt& fos, const Fmt& fcp, const Fmt& fov,
-                             const CollisionArgs& a, unsigned int* sched_ring,
-                             unsigned int* sched_next, cudaStream_t s);
+cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
+                             const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                             unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);
 constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight collision passes)
-// cost_traj (nullable): the per-trajectory sums of cost_pose
-cudaError_t launch_traj_reduce(const float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s);
+// add (nullable): cost_pose += add first (the self pass's separate cost);
+// cost_traj (nullable): the per-trajectory sums
+cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
+                               cudaStream_t s, const float* add = nullptr);
 // N3 sparse form of a sphere tensor (include/vapr.h "N3"; sparse.cuh)
 struct SparseOut {
     unsigned long long* mask;  // [rows] (the caller offsets it to the first row)
@@ -90,11 +95,10 @@ cudaError_t launch_densify(const Fmt& f, const SparseIn& in, long long rows, int
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
                              uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr);
-// N3 sparse inputs (cp / ov: sphere bitmaps + packed non-zero codes at
-// pool + row * ceil(cols / pf)) -> the sparse form of grad_out_spheres
-cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
-                                    const uint32_t* cp_pool, const unsigned long long* cpm,
-                                    const uint32_t* ov_pool, const unsigned long long* ovm,
+// N3 masked inputs (cp / ov rows + sphere bitmaps, not zero-filled) -> sparse form
+cudaError_t launch_aggregate_masked(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
+                                    const uint32_t* cp, const unsigned long long* cpm,
+                                    const uint32_t* ov, const unsigned long long* ovm,
                                     long long rows, const SparseOut& sparse, cudaStream_t s);
 // sparse (nullable): read grad_out_spheres from the sparse form instead of gos
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
