@@ -1,15 +1,19 @@
 """bench.py -- rollout cost+grad throughput of the VaPr hot path on B200.
 
     python bench.py [--gpus N --steps K --warmup W] [--formats 43bit] [--impl vapr|reference]
+                    [--scaling strong|weak] [--storage sparse|dense]
 
-A step = one vapr_cost_grad over the whole resident batch (FK -> fused world
-(swept) + self collision -> aggregate -> BK, every live tensor packed in HBM)
-plus the per-problem best-seed reduction (and, for N > 1, one NCCL all-gather
-of the per-problem results).  Workload = BASELINE.json config 4 per GPU:
-800 problems (100 per MotionBenchMaker-like environment) x 100 TO seeds x 32
-steps = 2.56M poses, 52 spheres (weak scaling: every rank owns its own 800
-problems).  The working set (~1.5 GB of packed tensors at 43 bits) is >10x
-the 126 MB L2, so no flush is needed between steps.  One JSON line on rank 0.
+A step = one vapr_cost_grad over the whole resident batch (FK -> world (swept)
+and self collision -> aggregate -> BK, every live tensor packed in HBM) plus
+the per-problem best-seed reduction (and, for N > 1, one NCCL all-gather of
+the per-problem results).  Workload = BASELINE.json config 4: 800 problems
+(100 per MotionBenchMaker-like environment) x 100 TO seeds x 32 steps, 52
+spheres; `--scaling strong` (default, the configured split)
+shards the 800 problems round-robin (problem p on rank p mod N, so every rank
+keeps the environment mix); `--scaling weak` gives every rank its own 800.
+At N = 1 both are the 2.56M-pose batch.  The working set (~1.5 GB of packed
+tensors at 43 bits) is >10x the 126 MB L2, so no flush is needed between
+steps.  One JSON line on rank 0.
 """
 import argparse
 import json
@@ -30,6 +34,7 @@ UNIT = "sphere-evals/s"
 # traj_reduce, aggregate, bk (vapr_cost_grad) + best_per_problem
 LAUNCHES_PER_STEP = 7
 S = 52
+N_GLOBAL_PROBLEMS = 800
 
 
 def parse():
@@ -39,6 +44,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="vapr", choices=["vapr", "reference"])
     ap.add_argument("--formats", default="43bit")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: config 4's 800 problems sharded round-robin over the ranks; "
+                         "weak: 800 problems per rank")
     ap.add_argument("--problems-per-env", type=int, default=100)
     ap.add_argument("--seeds", type=int, default=100)
     ap.add_argument("--H", type=int, default=32)
@@ -47,7 +55,8 @@ def parse():
     ap.add_argument("--storage", default="sparse", choices=["sparse", "dense"],
                     help="grad_out_spheres / collision-output storage inside vapr_cost_grad "
                          "(VAPR_OPT_SPARSE, N3; results bit-identical)")
-    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 comparison run")
+    ap.add_argument("--no-formats", action="store_true",
+                    help="skip the format-set legs (FP32, FP16, per-environment Table II, dense)")
     ap.add_argument("--no-iko", action="store_true",
                     help="skip the IKO leg (N2: H = 1, 1000 seeds x 800 problems, pose + bound costs)")
     ap.add_argument("--no-to", action="store_true",
@@ -75,8 +84,17 @@ def stage_bytes(fm, swept=True):
     """Algorithmic HBM bytes per pose of each kernel."""
     os_, gos, ov, cp, cps = (v_alg(f) for f in fm)
     c = cps if swept else cp
-    return {"fk": 28 + os_, "collision": os_ + c + ov + 4, "aggregate": c + ov + gos,
-            "bk": 28 + gos + 28}
+    return {"fk": 28 + os_, "collision": os_ + c + ov + 4, "reduce": 4 + 4.0 / 32,
+            "aggregate": c + ov + gos, "bk": 28 + gos + 28}
+
+
+def a_min(fm, swept=True):
+    """A_min: the path's algorithmic bytes per pose: q read
+    twice, grad_q written, one FP32 cost, every live packed tensor written
+    once and read once."""
+    os_, gos, ov, cp, cps = (v_alg(f) for f in fm)
+    c = cps if swept else cp
+    return 28 + 28 + 28 + 4 + 2 * (os_ + c + ov + gos)
 
 
 class Clocks:
@@ -133,57 +151,114 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def shard_ids(scaling, rank, world, problems_per_env):
+    from paper_2310_07854_b200.dist import shard_problems
+    n = problems_per_env * 8
+    if scaling == "weak":
+        return shard_problems(rank, world, per_rank=n)
+    return shard_problems(rank, world, n_global=n, mode="strong")
+
+
 # ----------------------------------------------------------------- cpu / oracle
-def oracle_sample(fm, n_poses, H, key_offset=0):
-    """A bounded sample of the config-4 workload (same generator, same
-    formats) for the oracle: n_poses // H trajectories spread over the 8
-    environments."""
+# The oracle (test infrastructure, oracle/) timed on the host cores: a bounded
+# sample of the config-4 workload (same generator, same formats), on one core
+# and on all of them (a process pool over trajectory chunks).
+def oracle_sample(fm, n_poses, H):
+    """n_poses // H trajectories spread over the 8 environments."""
     from workloads import config4
     from workloads.scenes import ENVIRONMENTS
     n_traj = max(8, n_poses // H)
     seeds = max(1, n_traj // len(ENVIRONMENTS))
     return config4(problems_per_env=1, seeds=seeds, H=H, formats=fm,
-                   problem_offset=key_offset, n_problems=len(ENVIRONMENTS))
+                   problem_offset=0, n_problems=len(ENVIRONMENTS))
 
 
-def run_oracle(wl):
+def _oracle_chunk(args):
+    """Worker: the oracle rollout of trajectories [b0, b1) of the sample."""
+    import dataclasses
     from oracle.rollout import rollout_workload
+    wl, b0, b1 = args
+    sub = dataclasses.replace(wl, q=wl.q[b0:b1], world_idx=wl.world_idx[b0:b1])
     t0 = time.perf_counter()
-    rollout_workload(wl)
+    rollout_workload(sub)
+    return time.perf_counter() - t0
+
+
+def _pool(cores):
+    import multiprocessing as mp
+    env = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
+    os.environ.update(env)
+    ctx = mp.get_context("spawn")          # no CUDA state crosses into the workers
+    pool = ctx.Pool(cores)
+    pool.map(_oracle_chunk, [(oracle_sample(((8, 23),) * 5, 64, 32), 0, 1)] * cores)   # warm up
+    return pool
+
+
+def oracle_time(wl, cores, pool=None):
+    """Wall seconds of the oracle over the sample: 1 core in-process, or
+    `cores` workers over equal trajectory chunks."""
+    if cores == 1:
+        return _oracle_chunk((wl, 0, wl.B))
+    cuts = np.linspace(0, wl.B, cores + 1).astype(int)
+    t0 = time.perf_counter()
+    pool.map(_oracle_chunk, [(wl, int(cuts[i]), int(cuts[i + 1])) for i in range(cores)])
     return time.perf_counter() - t0
 
 
 def cpu_baseline(fm, H, n_poses):
     wl = oracle_sample(fm, n_poses, H)
-    dt = run_oracle(wl)
-    return {"value": wl.poses * S / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{wl.poses} poses ({wl.B} trajectories x {H} steps, 8 envs) of the same "
-                      f"workload generator, float64 numpy + C codec, single thread, {dt:.1f} s"}
+    cores = os.cpu_count() or 1
+    t1 = oracle_time(wl, 1)
+    out = {"value": None, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "value_1core": wl.poses * S / t1,
+           "sample": f"{wl.poses} poses ({wl.B} trajectories x {H} steps, 8 envs) of the same "
+                     f"workload generator, float64 numpy + C codec; 1 core {t1:.1f} s"}
+    if cores > 1:
+        pool = _pool(cores)
+        try:
+            tn = oracle_time(wl, cores, pool)
+        finally:
+            pool.close()
+            pool.join()
+        out["value"] = wl.poses * S / tn
+        out["sample"] += f", {cores} cores (process pool over trajectory chunks) {tn:.2f} s"
+    else:
+        out["value"] = out["value_1core"]
+    return out
 
 
 # ----------------------------------------------------------------- reference arm
 def reference_arm(args):
+    """The base contract's reference arm for this tier: the oracle as it
+    stands, on the box's host cores (a process pool), on the same metric."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from workloads.configs import FORMAT_SETS
     fm = FORMAT_SETS[args.formats]
-    n_poses = max(args.H * 8, args.cpu_sample_poses // 4)
+    cores = os.cpu_count() or 1
+    n_poses = max(args.H * 8 * cores, args.cpu_sample_poses)
     wl = oracle_sample(fm, n_poses, args.H)
-    for _ in range(args.warmup):
-        run_oracle(wl)
-    times = [run_oracle(wl) for _ in range(args.steps)]
+    pool = _pool(cores) if cores > 1 else None
+    try:
+        for _ in range(args.warmup):
+            oracle_time(wl, cores, pool)
+        times = [oracle_time(wl, cores, pool) for _ in range(args.steps)]
+    finally:
+        if pool is not None:
+            pool.close()
+            pool.join()
     t = float(np.sum(times))
     value = wl.poses * S * args.steps / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config4 sample: {wl.poses} poses/step ({wl.B} traj x "
                                    f"{args.H} steps, 8 envs), formats {args.formats}",
                        "formats": args.formats},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{wl.poses} poses per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{wl.poses} poses per step, {cores} worker processes"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -199,31 +274,34 @@ def main():
     import torch.distributed as dist
     from paper_2310_07854_b200 import binding as vb
     from paper_2310_07854_b200.rollout import Rollout
-    from paper_2310_07854_b200.dist import shard_problems, gather_best, max_over_ranks
+    from paper_2310_07854_b200.dist import gather_best, max_over_ranks
     from workloads import config4
     from workloads.configs import FORMAT_SETS
+    from workloads.scenes import ENVIRONMENTS
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("VAPR_DIST_BACKEND", "nccl") != "nccl":
+    backend = os.environ.get("VAPR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
         local = 0                     # functional multi-rank check on one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        # NCCL over NVLink; VAPR_DIST_BACKEND=gloo is a functional check of the
-        # multi-rank logic on one GPU (never a measurement)
-        backend = os.environ.get("VAPR_DIST_BACKEND", "nccl")
+        # NCCL over NVLink, its init log on (the driver checks nranks);
+        # VAPR_DIST_BACKEND=gloo is a functional check of the multi-rank logic
+        # on one GPU (never a measurement)
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     fm = FORMAT_SETS[args.formats]
-    n_prob = args.problems_per_env * 8
-    # weak scaling: rank r owns global problems [r*n_prob, (r+1)*n_prob)
-    ids = shard_problems(rank, world, per_rank=n_prob)
+    ids = shard_ids(args.scaling, rank, world, args.problems_per_env)
+    n_prob = len(ids)
     wl = config4(problems_per_env=args.problems_per_env, seeds=args.seeds, H=args.H,
-                 formats=fm, problem_offset=ids[0], n_problems=len(ids))
+                 formats=fm, problem_ids=ids)
     P = wl.poses
     sparse = args.storage == "sparse"
     r = Rollout(wl, device=local, sparse=sparse)
@@ -231,10 +309,14 @@ def main():
     best_c = torch.empty(n_prob, dtype=torch.float32, device=dev)
     best_s = torch.empty(n_prob, dtype=torch.int32, device=dev)
 
-    def step():
-        r.run()
-        vb.vapr_best_per_problem(r.cost_traj, n_prob, args.seeds, best_c, best_s)
-        gather_best(best_c, best_s, world)       # the path's only collective
+    def step_of(rr, n_p=n_prob, seeds=args.seeds, bc=best_c, bs=best_s):
+        def f():
+            rr.run()
+            vb.vapr_best_per_problem(rr.cost_traj, n_p, seeds, bc, bs)
+            gather_best(bc, bs, world)       # the path's only collective
+        return f
+
+    step = step_of(r)
 
     def barrier():
         if world > 1:
@@ -254,10 +336,13 @@ def main():
         barrier()
         return max_over_ranks(e0.elapsed_time(e1), dev) / k
 
+    # poses processed by all ranks per step
+    poses_total = (P * world if args.scaling == "weak"
+                   else args.problems_per_env * 8 * args.seeds * args.H)
     with Clocks(local) as clk:
         ms = timed(step, args.steps, args.warmup)
     clocks = clk.summary()
-    value = world * P * S / (ms * 1e-3)
+    value = poses_total * S / (ms * 1e-3)
 
     # measured sparsity of the gradient tensors ("report the
     # measured nonzero fraction per run"; PAPER.md:196 >99 % zeros), from the
@@ -275,88 +360,61 @@ def main():
             sparsity[nm] = {"nonzero_sphere_frac": round(float(bits.sum()) / (P * S), 5),
                             "nonzero_pose_frac": round(float((bits > 0).sum()) / P, 4)}
 
-    # ---- per-kernel durations (the stage entry points, launched stage by
-    # stage on the same stream with events between them; dense storage: the
-    # standalone calls take dense tensors) for the roofline of the dominant one
-    p = wl.params
-    swept = p["swept"]
-    rd = Rollout(wl, device=local) if sparse else r
-    lay = vb.vapr_cost_grad_workspace_layout(rd.ctx.h, wl.B, wl.H, swept)
-    W = {i: vb.vapr_packed_row_words(fm[i], 3 * S) for i in range(5)}
-    cps = 4 if swept else 3
-    ws = rd.workspace
-
-    def slot(i):
-        return ws[lay[i]:lay[i] + 4 * W[i] * P]
-
-    names = ["fk", "collision", "aggregate", "bk"]
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    # ---- per-kernel durations of the timed step itself: vapr_cost_grad
+    # records caller-owned CUDA events between its launches on its stream
+    # (vapr_set_stage_events), so the roofline is taken on exactly the kernels
+    # the step runs (sparse storage included)
+    names = ["fk", "collision", "reduce", "aggregate", "bk"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    vb.vapr_set_stage_events(r.ctx.h, ev)
     acc = {n: 0.0 for n in names}
-
-    def staged():
-        ev[0].record(stream)
-        vb.vapr_fk_spheres(rd.ctx.h, rd.q, wl.B, wl.H, slot(0))
-        ev[1].record(stream)
-        vb.vapr_collision(rd.ctx.h, slot(0), rd.world_idx, wl.B, wl.H, p, rd.cost_pose,
-                          rd.cost_traj, slot(cps), slot(2))
-        ev[2].record(stream)
-        vb.vapr_aggregate(rd.ctx.h, slot(cps), swept, slot(2), P, slot(1))
-        ev[3].record(stream)
-        vb.vapr_backward_kinematics(rd.ctx.h, rd.q, wl.B, wl.H, slot(1), rd.grad_q)
-        ev[4].record(stream)
-
     for _ in range(2):
-        staged()
+        r.run()
     torch.cuda.synchronize(dev)
     for _ in range(args.steps):
-        staged()
+        r.run()
         torch.cuda.synchronize(dev)
         for i, n in enumerate(names):
             acc[n] += ev[i].elapsed_time(ev[i + 1])
+    vb.vapr_set_stage_events(r.ctx.h, None)
     kms = {n: acc[n] / args.steps for n in names}
-    sb = stage_bytes(fm, bool(swept))
-    a_min = sum(sb.values())
+    swept = bool(wl.params["swept"])
+    sb = stage_bytes(fm, swept)
     dom = max(kms, key=kms.get)
     hbm, peak_kind = peaks()
     achieved = sb[dom] * P / (kms[dom] * 1e-3) / 1e9
-    traffic = None
-    try:        # DRAM bytes per launch from the committed ncu capture of this workload
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r1", "traffic.json")))
-        if tj["formats"] == args.formats and tj["poses"] == P:
-            traffic = tj["bytes_per_launch"].get(dom)
+    prof = {}
+    try:        # DRAM bytes per launch and the limiter, from the committed ncu capture
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2", "roofline_ncu.json")))
     except Exception:
         pass
-    if rd is not r:
-        del rd, ws
-        torch.cuda.empty_cache()
-    issue = None
-    try:        # the dominant kernel is issue-bound: its ncu issue utilisation
-        ij = json.load(open(os.path.join(ROOT, "profiles", "r1", "issue.json")))
-        issue = ij.get(dom)
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "kernel": dom, "stage_calls": "dense standalone entry points", "achieved": achieved, "peak": hbm,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "bytes_per_launch_alg": sb[dom] * P, "bytes_per_pose": sb[dom],
-                "limiter": ("instruction issue (ncu, profiles/r1/issue.json); HBM frac is low "
-                            "because the collision passes spend ~10x more issue slots than bytes"),
-                "issue": issue,
+    kp = prof.get("kernels", {}).get(dom, {}) if prof.get("formats") == args.formats and \
+        prof.get("poses") == P else {}
+    roofline = {"bound": "hbm", "kernel": dom,
+                "stage_calls": "the timed step's own launches (vapr_set_stage_events, "
+                               f"{args.storage} storage)",
+                "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": kp.get("dram_bytes"),
+                "bytes_per_launch_alg": sb[dom] * P, "bytes_per_pose": sb[dom],
+                "limiter": kp.get("limiter", "see profiles/r2 (ncu)"),
+                "issue": kp.get("issue"),
                 "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
                 "kernel_frac": {n: round(sb[n] * P / (kms[n] * 1e-3) / 1e9 / hbm, 4) for n in names}}
 
     # ---- the step as a CUDA graph (SURVEY.md §8(d) timing protocol), on the
-    # bench workload and on the launch-bound config 2 (eager vs graph)
+    # bench workload and on the launch-bound configs 1 and 2 (eager vs graph)
     graph = None
     if not args.no_graph:
-        from workloads import config2
+        from workloads import config1, config2
         g = r.capture_graph()
         graph = {"ms_per_step": timed(g.replay, args.steps, args.warmup)}
         del g
-        r2 = Rollout(config2(), device=local, sparse=sparse)
-        g2 = r2.capture_graph()
-        graph["config2_eager_us"] = 1e3 * timed(r2.run, 50, 10)
-        graph["config2_graph_us"] = 1e3 * timed(g2.replay, 50, 10)
-        del g2, r2
+        for nm, wsmall in (("config1", config1()), ("config2", config2())):
+            r2 = Rollout(wsmall, device=local, sparse=sparse)
+            g2 = r2.capture_graph()
+            graph[f"{nm}_eager_us"] = 1e3 * timed(r2.run, 50, 10)
+            graph[f"{nm}_graph_us"] = 1e3 * timed(g2.replay, 50, 10)
+            del g2, r2
         torch.cuda.empty_cache()
 
     # ---- end to end through the public API with host buffers
@@ -374,7 +432,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
-        e2e = {"value": world * P * S / (e2e_ms * 1e-3), "unit": UNIT, "chunks": args.chunks,
+        e2e = {"value": poses_total * S / (e2e_ms * 1e-3), "unit": UNIT, "chunks": args.chunks,
                "h2d_bytes_per_step": q_host.numel() * 4,
                "d2h_bytes_per_step": gq_host.numel() * 4 + ct_host.numel() * 4,
                "ms_per_step": e2e_ms}
@@ -388,9 +446,9 @@ def main():
         opt.reset()
         to_ms = timed(opt.step, max(3, args.steps // 4), 2)
         to_iter = {"ms_per_iteration": to_ms, "line_search_scales": list(opt.scales),
-                   "trajectories": opt.B * world, "poses_evaluated_per_iteration": opt.N * P * world,
-                   "trajectory_iterations_per_s": opt.B * world / (to_ms * 1e-3),
-                   "history_m": opt.m}
+                   "trajectories": opt.B, "poses_evaluated_per_iteration": opt.N * P,
+                   "trajectory_iterations_per_s": opt.B / (to_ms * 1e-3),
+                   "history_m": opt.m, "per_rank": True}
         del opt
         torch.cuda.empty_cache()
 
@@ -401,41 +459,73 @@ def main():
         from paper_2310_07854_b200.optimize import TrajOpt
         from workloads import config_iko
         wli = config_iko(problems_per_env=args.problems_per_env, seeds=1000, formats=fm,
-                         problem_offset=ids[0], n_problems=len(ids))
+                         problem_ids=ids)
         opt = TrajOpt(wli, device=local, sparse=sparse)
         opt.reset()
         ev_ms = timed(opt.base.run, max(3, args.steps // 2), 2)
         it_ms = timed(opt.step, max(3, args.steps // 4), 2)
-        iko = {"poses": wli.poses * world, "seeds_per_problem": 1000,
-               "cost_grad_ms": ev_ms, "cost_grad_pose_evals_per_s": wli.poses * world / (ev_ms * 1e-3),
+        iko = {"poses": wli.poses, "seeds_per_problem": 1000,
+               "cost_grad_ms": ev_ms, "cost_grad_pose_evals_per_s": wli.poses / (ev_ms * 1e-3),
                "iteration_ms": it_ms, "line_search_scales": list(opt.scales),
-               "seed_iterations_per_s": wli.B * world / (it_ms * 1e-3)}
+               "seed_iterations_per_s": wli.B / (it_ms * 1e-3), "per_rank": True}
         del opt
         torch.cuda.empty_cache()
 
-    # ---- FP32 comparison (the >= 2x target of BASELINE.json) on the same batch
-    fp32 = None
-    if not args.no_fp32 and args.formats != "fp32":
-        r.set_formats(FORMAT_SETS["fp32"])
-        ms32 = timed(step, max(3, args.steps // 2), 2)
-        fp32 = {"value": world * P * S / (ms32 * 1e-3), "ms_per_step": ms32,
-                "speedup_of_formats": ms32 / ms, "storage": args.storage}
-        r.set_formats(fm)
-        if sparse:
-            # the paper's baseline layout: FP32 in dense storage (its sparsity is
-            # compute skipping only)
-            r32 = Rollout(wl, device=local, formats=FORMAT_SETS["fp32"])
+    # ---- format sets on the same batch (FP32,
+    # FP16-all, each environment's own Table II row, and the 43-bit set in
+    # dense storage -- the method's materialised layout)
+    formats = None
+    if not args.no_formats:
+        formats = {}
 
-            def step32():
-                r32.run()
-                vb.vapr_best_per_problem(r32.cost_traj, n_prob, args.seeds, best_c, best_s)
-                gather_best(best_c, best_s, world)
+        def leg(name, fmt_set, storage):
+            rr = r if (storage == args.storage and fmt_set == fm) else \
+                Rollout(wl, device=local, formats=fmt_set, sparse=(storage == "sparse"))
+            t = timed(step_of(rr), max(3, args.steps // 2), 2)
+            bits = sum(1 + e + m for e, m in fmt_set)
+            formats[name] = {"ms_per_step": t, "value": poses_total * S / (t * 1e-3),
+                             "storage": storage, "bits": bits,
+                             "hbm_frac_step": a_min(fmt_set, swept) * P / (t * 1e-3) / 1e9 / hbm}
+            if rr is not r:
+                del rr
+                torch.cuda.empty_cache()
 
-            ms32d = timed(step32, max(3, args.steps // 2), 2)
-            fp32["dense_ms_per_step"] = ms32d
-            fp32["speedup_vs_dense_fp32"] = ms32d / ms
-            del r32
-            torch.cuda.empty_cache()
+        for st in ("sparse", "dense"):
+            leg(f"fp32_{st}", FORMAT_SETS["fp32"], st)
+            leg(f"fp16_{st}", FORMAT_SETS["fp16"], st)
+            leg(f"{args.formats}_{st}", fm, st)
+        # every environment with its own Table II row: the
+        # rank's problems of environment e as one sub-batch with e's formats,
+        # the eight sub-batches back to back as one step
+        subs = []
+        for e, env in enumerate(ENVIRONMENTS):
+            eids = [p for p in ids if p % 8 == e]
+            if not eids:
+                continue
+            we = config4(problems_per_env=args.problems_per_env, seeds=args.seeds, H=args.H,
+                         formats=FORMAT_SETS[env], problem_ids=eids)
+            re_ = Rollout(we, device=local, sparse=sparse)
+            bc = torch.empty(len(eids), dtype=torch.float32, device=dev)
+            bs = torch.empty(len(eids), dtype=torch.int32, device=dev)
+            subs.append((re_, len(eids), bc, bs))
+
+        def env_step():
+            for re_, ne, bc, bs in subs:
+                re_.run()
+                vb.vapr_best_per_problem(re_.cost_traj, ne, args.seeds, bc, bs)
+            gather_best(best_c, best_s, world)
+
+        t = timed(env_step, max(3, args.steps // 2), 2)
+        formats["per_env_table2"] = {
+            "ms_per_step": t, "value": poses_total * S / (t * 1e-3), "storage": args.storage,
+            "bits": {env: sum(1 + e + m for e, m in FORMAT_SETS[env]) for env in ENVIRONMENTS}}
+        del subs
+        torch.cuda.empty_cache()
+        for st in ("sparse", "dense"):
+            f32 = formats[f"fp32_{st}"]["ms_per_step"]
+            for k in list(formats):
+                if k.endswith(st) or (k == "per_env_table2" and st == args.storage):
+                    formats[k][f"speedup_vs_fp32_{st}"] = f32 / formats[k]["ms_per_step"]
 
     if rank == 0:
         # the oracle leg runs on rank 0 of a 1-GPU run only (the contract)
@@ -444,11 +534,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32+packed-ExMy", "data": "synthetic",
-            "config": {"workload": f"config4: {n_prob} problems ({args.problems_per_env} per "
-                                   f"MBM-like env) x {args.seeds} TO seeds x {args.H} steps per GPU, "
-                                   "52 spheres, swept n=1",
+            "config": {"workload": f"config4: {args.problems_per_env * 8} problems "
+                                   f"({args.problems_per_env} per MBM-like env) x {args.seeds} TO "
+                                   f"seeds x {args.H} steps, 52 spheres, swept n=1, "
+                                   + ("sharded round-robin over the ranks (problem p on rank p mod N)"
+                                      if args.scaling == "strong" else "per rank"),
                        "formats": args.formats, "format_bits": bits,
                        "storage": args.storage + (" (VAPR_OPT_SPARSE: collision outputs as masked "
                                                    "rows, grad_out_spheres as bitmap + packed codes)"
@@ -456,15 +548,16 @@ def main():
                        "formats_exmy": ["E%dM%d" % f for f in fm],
                        "poses_per_gpu": P, "problems_per_gpu": n_prob,
                        "l2": "inputs > L2 (packed working set >> 126 MB), no flush",
-                       "parallelism": f"problem-sharded x{world}"},
-            "hbm_alg_gbs": a_min * P * world / (ms * 1e-3) / 1e9,
-            "hbm_frac_step": a_min * P / (ms * 1e-3) / 1e9 / hbm,
-            "bytes_per_pose_alg": a_min,
+                       "parallelism": f"problem-sharded x{world} ({args.scaling})"},
+            "nccl_ranks": world,
+            "hbm_alg_gbs": a_min(fm, swept) * poses_total / (ms * 1e-3) / 1e9,
+            "hbm_frac_step": a_min(fm, swept) * P / (ms * 1e-3) / 1e9 / hbm,
+            "bytes_per_pose_alg": a_min(fm, swept),
             "roofline": roofline,
             "e2e": e2e,
             "graph": graph,
             "sparsity": sparsity,
-            "fp32": fp32,
+            "format_sets": formats,
             "to_iteration": to_iter,
             "iko": iko,
             "cpu_baseline": cpu,

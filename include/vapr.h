@@ -69,11 +69,12 @@ typedef enum {
 typedef struct { int32_t exp_bits, man_bits; } vapr_format;
 
 /* IEEE special-value mode: OR'd into man_bits of E5M10
- * or E8M7 only.  Encoding is the hardware round-to-nearest conversion
- * unconditionally (overflow -> +-inf, NaN -> NaN: PAPER.md:259's
- * __floats2half2_rn path) and the top exponent decodes to inf / NaN, instead
- * of the all-finite reading (c3-c7).  Identical to the reading for every
- * finite |x| below the format's overflow threshold. */
+ * or E8M7 only.  Encoding is IEEE round-to-nearest-even -- the library's
+ * generic integer encoder with the inf code as its clamp (overflow -> +-inf)
+ * and 0x7FFF for NaN, which is what PAPER.md:259's __floats2half2_rn path
+ * produces -- and the top exponent decodes to inf / NaN, instead of the
+ * all-finite reading (c3-c7).  Identical to the reading for every finite |x|
+ * below the format's overflow threshold. */
 #define VAPR_FMT_IEEE 0x100
 
 /* Tensor slots, in Table II column order (names from P:189). */
@@ -177,6 +178,14 @@ vapr_status vapr_set_robot(vapr_ctx *ctx, const vapr_robot *robot);
 vapr_status vapr_set_worlds(vapr_ctx *ctx, int32_t n_worlds, const vapr_cuboid *cuboids,
                             const int32_t *offsets);
 vapr_status vapr_set_option(vapr_ctx *ctx, int32_t option, int32_t value);
+/* Stage timing hook (measurement): with n = 6 caller-owned
+ * cudaEvent_t handles, every later vapr_cost_grad on one stream
+ * (VAPR_OPT_STREAMS = 1) records events[0] before FK and events[i] after
+ * stage i: 1 FK, 2 collision (both passes), 3 cost reduction, 4 aggregation,
+ * 5 BK -- the per-kernel durations of the launches the call makes, on its own
+ * stream.  n = 0 clears it.  The events stay owned by the caller (destroying
+ * one while set is undefined).  VAPR_ERR_INVALID_ARG for other n. */
+vapr_status vapr_set_stage_events(vapr_ctx *ctx, void *const *events, int32_t n);
 
 /* ---- a1: codec (context free) ------------------------------------------ */
 /* Quantise x [rows, cols] float32 to packed [rows, row_words] (P:227

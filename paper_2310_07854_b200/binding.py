@@ -32,7 +32,7 @@ EXPORTS = ("vapr_create", "vapr_destroy", "vapr_status_string", "vapr_version",
            "vapr_last_cuda_error",
            "vapr_format_parse", "vapr_format_check", "vapr_packed_row_words",
            "vapr_set_formats", "vapr_set_robot", "vapr_set_worlds", "vapr_set_goals",
-           "vapr_set_option",
+           "vapr_set_option", "vapr_set_stage_events",
            "vapr_quantize", "vapr_dequantize", "vapr_fk_spheres", "vapr_world_collision",
            "vapr_self_collision", "vapr_collision", "vapr_aggregate",
            "vapr_backward_kinematics", "vapr_cost_grad_workspace_bytes",
@@ -90,6 +90,7 @@ def _load():
         "vapr_set_worlds": ([P, I32, P, P], I32),
         "vapr_set_goals": ([P, P, I32], I32),
         "vapr_set_option": ([P, I32, I32], I32),
+        "vapr_set_stage_events": ([P, P, I32], I32),
         "vapr_quantize": ([vapr_format, P, SZ, SZ, P, P], I32),
         "vapr_dequantize": ([vapr_format, P, SZ, SZ, P, P], I32),
         "vapr_fk_spheres": ([P, P, I32, I32, P, P, P], I32),
@@ -270,6 +271,18 @@ def vapr_set_goals(ctx, goals):
 
 def vapr_set_option(ctx, option, value):
     _check(lib.vapr_set_option(ctx, option, int(value)), "vapr_set_option")
+
+
+def vapr_set_stage_events(ctx, events):
+    """events: 6 torch.cuda.Event (or None to clear) -- vapr_cost_grad then
+    records them between its stages on its stream (include/vapr.h)."""
+    if not events:
+        _check(lib.vapr_set_stage_events(ctx, None, 0), "vapr_set_stage_events")
+        return
+    for e in events:            # torch creates the CUDA event lazily
+        e.record()
+    arr = (ctypes.c_void_p * 6)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    _check(lib.vapr_set_stage_events(ctx, arr, 6), "vapr_set_stage_events")
 
 
 def cost_params(p):

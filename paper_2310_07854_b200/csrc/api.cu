@@ -38,6 +38,10 @@ struct vapr_ctx {
     cudaStream_t par[8] = {};
     // N3: grad_out_spheres in the sparse form (VAPR_OPT_SPARSE)
     int sparse = 0;
+    // stage timing hook (vapr_set_stage_events): caller-owned events recorded
+    // between the launches of vapr_cost_grad
+    cudaEvent_t stage_ev[6] = {};
+    int n_stage_ev = 0;
     // IKO goals (N2)
     float* d_goals = nullptr;
     int32_t n_goals = 0;
@@ -518,6 +522,14 @@ vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
     return VAPR_ERR_UNSUPPORTED;
 }
 
+vapr_status vapr_set_stage_events(vapr_ctx* c, void* const* events, int32_t n) {
+    CHECK(c != nullptr, VAPR_ERR_INVALID_ARG);
+    CHECK(n == 0 || (n == 6 && events != nullptr), VAPR_ERR_INVALID_ARG);
+    for (int i = 0; i < 6; ++i) c->stage_ev[i] = (n == 6) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+    c->n_stage_ev = n;
+    return VAPR_OK;
+}
+
 // ---- test-only debug tap (tap.cuh) -----------------------
 #ifdef VAPR_DEBUG_TAP
 vapr_status vapr_debug_tap(vapr_ctx* c, int32_t slot, float* dst) {
@@ -841,7 +853,13 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     ik.w_bound = p->w_bound;
     ik.cost = cpose + p0;
     const bool iko = ik_on(ik);
+    // stage timing hook: event i after stage i (0: before FK)
+    auto mark = [&](int i) {
+        if (c->n_stage_ev == 6) cudaEventRecord(c->stage_ev[i], s);
+    };
+    mark(0);
     cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], qc, P, os, s, iko ? &ik : nullptr);
+    mark(1);
     if (e == cudaSuccess) {
         CollisionArgs a{};
         a.os = os;
@@ -872,18 +890,22 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES], c->dfmt[cps],
                              c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
+    mark(2);
     // combines the self pass's cost into cost_pose (always) and sums cost_traj
     if (e == cudaSuccess)
         e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost);
+    mark(3);
     if (e == cudaSuccess)
         e = c->sparse ? launch_aggregate_masked(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
                                                 ov, ov_mask, P, spo, s)
                       : launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                          c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, ov, P, gos, s);
+    mark(4);
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
                       iko ? &ik : nullptr, c->sparse ? &spi : nullptr);
+    mark(5);
     return e;
 }
 

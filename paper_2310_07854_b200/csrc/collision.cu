@@ -6,19 +6,21 @@
 // c13-c17 (box SDF, smooth hinge, summed over cuboids / listed pairs; swept =
 // linear sub-samples with the exact gradient to both endpoints).
 //
-// One warp per tile of kTP = 31 consecutive poses, one pose per lane, plus
-// the halo poses p0-1 and p0+31 for the swept samples (warps are independent:
-// no CTA barrier in the tile loop; the robot tables are staged once per CTA):
+// One warp per tile of kTP = 15 consecutive poses, two lanes per pose (lane =
+// half * 16 + pose; lane 15 / 31: the halo pose p0 + 15), plus the halo rows
+// p0-1 and p0+15 for the swept samples (warps are independent: no CTA
+// barrier in the tile loop; the robot tables are staged once per CTA):
 //  1. load the packed rows (16-byte loads, all in flight) and decode them into
-//     an FP32 tile (odd row stride: lane-per-pose accesses are conflict-free);
+//     an FP32 tile (odd row stride: pose-per-lane accesses are conflict-free);
 //     track the largest decoded coordinate;
-//  2. broadphase, 32 poses per instruction.  The spheres of a link (or of a
+//  2. broadphase, 16 poses per instruction, the two lanes of a pose splitting
+//     its list.  The spheres of a link (or of a
 //     half-link group) lie in a ball around a reference sphere whose radius is
 //     rigid (computed once on the host) plus the quantisation-error margin.
 //     World: per (segment, link, cuboid) -- or per (pose, link, cuboid) for
 //     the discrete cost -- a cull bit from the squared distance of the ball
-//     centre to the box.  Self: per (pose, link pair) a ball-ball test that
-//     selects half-link group pairs;
+//     centre to the box.  Self: per (pose, link pair) a ball-ball test, then
+//     per live link pair its half-link group pairs;
 //  3. the sparse work goes through warp work queues (every lane gets an item):
 //     live (pose, sphere) world items gather the complete gradient of the
 //     sphere (no scatter) and OR its codes into shared packed rows (OR is
@@ -1021,7 +1023,7 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     // as many warps per CTA as shared memory holds (the tables are staged
-    // once per CTA), at most 8; one persistent CTA per SM
+    // once per CTA), at most VAPR_MAX_WARPS (16); one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
     nw = std::min(nw, VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
@@ -1085,9 +1087,15 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
         return sched_ring + 2 * k;
     };
     CollisionArgs a = a0;
+    // a.self_cost (vapr_cost_grad) is added by traj_reduce: a path that puts
+    // the self cost into a.cost itself leaves it zero
+    auto zero_self = [&]() -> cudaError_t {
+        return a.self_cost ? cudaMemsetAsync(a.self_cost, 0, sizeof(float) * (size_t)P, s) : cudaSuccess;
+    };
     if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self)) {
         a.sched = slot();
-        return launch_collision_pass(R, W, fos, fcp, fov, a, s);
+        const cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, a, s);
+        return e == cudaSuccess ? zero_self() : e;
     }
     CollisionArgs aw = a, as = a;
     aw.sched = slot();
@@ -1109,7 +1117,8 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     }
     cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, aw, s);
     if (e != cudaSuccess) return e;
-    return launch_collision_pass(R, W, fos, fcp, fov, as, s);
+    e = launch_collision_pass(R, W, fos, fcp, fov, as, s);
+    return e == cudaSuccess ? zero_self() : e;
 }
 
 cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,

@@ -13,15 +13,21 @@ import torch
 import torch.distributed as dist
 
 
-def shard_problems(rank, world, per_rank=None, n_global=None, mode="weak"):
+def shard_problems(rank, world, per_rank=None, n_global=None, mode="weak", cycle=8):
     """Global problem ids owned by `rank`.
 
     weak:   [rank * per_rank, (rank + 1) * per_rank)
-    strong: rank, rank + world, rank + 2 world, ... < n_global"""
+    strong: round-robin within each environment: problem p of config 4 is the
+            (p // cycle)-th problem of environment p mod cycle (cycle = 8) and
+            goes to rank (p // cycle + p mod cycle) mod world.  Every rank gets
+            the same number of problems of each environment (+-1) and the
+            same total -- the same mix of cuboid counts (K = 3..9) and so the
+            same work; a plain p mod world would put only
+            the even environments on rank 0 of 2."""
     if mode == "weak":
         return list(range(rank * per_rank, (rank + 1) * per_rank))
     if mode == "strong":
-        return list(range(rank, n_global, world))
+        return [p for p in range(n_global) if (p // cycle + p % cycle) % world == rank]
     raise ValueError(mode)
 
 

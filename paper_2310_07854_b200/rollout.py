@@ -89,6 +89,10 @@ class Rollout:
             self.workspace = torch.zeros(need, dtype=torch.uint8, device=self.device)
 
     def run(self, stream=None):
+        """Enqueue vapr_cost_grad on `stream` (default: the current stream of
+        this rollout's device, not of the current device)."""
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
         vb.vapr_cost_grad(self.ctx.h, self.q, self.world_idx, self.B, self.H, self.params,
                           self.workspace, self.cost_pose, self.cost_traj, self.grad_q,
                           stream=stream, _p=self._p)

@@ -426,10 +426,10 @@ def main():
     # multi-GPU (torchrun): candidates of every batch spread over the ranks
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        local = int(os.environ.get("LOCAL_RANK", "0"))
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -437,7 +437,7 @@ def main():
             dist.init_process_group("gloo")
     if a.evaluator == "pipeline":
         from .pipeline import PipelineEvaluator
-        ev = PipelineEvaluator(problems_per_env=a.problems_per_env)
+        ev = PipelineEvaluator(problems_per_env=a.problems_per_env, device=local)
         base = ev.evaluate((FP32,) * 5)
         targets = dict(base)              # no lower success than FP32
         envs = sorted(base)
@@ -446,7 +446,7 @@ def main():
     else:
         from workloads import config5
         wl = config5(problems_per_env=a.problems_per_env, seeds=a.seeds)
-        ev = GpuProxyEvaluator(wl, a.seeds)
+        ev = GpuProxyEvaluator(wl, a.seeds, device=local)
         envs = sorted(set(wl.envs))
         targets = {e: a.target for e in envs}
         poses = wl.poses

@@ -139,3 +139,80 @@ def test_search_candidates_sharded_over_ranks():
     total = sum(r[4] for r in res)
     assert total == len(ref_trials)
     assert abs(res[0][4] - res[1][4]) <= len(ref_trials) // 4 + 8   # roughly half each
+
+
+def test_strong_shard_round_robin():
+    """bench.py --scaling strong: the 800 problems of config
+    4 split round-robin within each environment: every problem exactly once,
+    every rank the same total and the same environment mix (+-1)."""
+    import bench
+    for G in (1, 2, 4, 8):
+        shards = [bench.shard_ids("strong", r, G, 100) for r in range(G)]
+        flat = sorted(p for s in shards for p in s)
+        assert flat == list(range(800))
+        for r, s in enumerate(shards):
+            assert all((p // 8 + p % 8) % G == r for p in s) and len(s) == 800 // G
+            env_counts = np.bincount(np.asarray(s) % 8, minlength=8)
+            assert env_counts.max() - env_counts.min() <= 1
+
+
+def _bench_shard_worker(rank, world, port, q, ppe, seeds, H):
+    """One rank of the bench's strong-scaling step on cuda:0 (gloo): its
+    round-robin shard of config 4, vapr_cost_grad, vapr_best_per_problem and
+    the final gather (bench.py's own calls)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2310_07854_b200 import binding as vb
+        from paper_2310_07854_b200.rollout import Rollout
+        ids = bench.shard_ids("strong", rank, world, ppe)
+        wl = config4(problems_per_env=ppe, seeds=seeds, H=H, problem_ids=ids)
+        r = Rollout(wl, device=0, sparse=True)
+        r.run()
+        bc = torch.empty(len(ids), dtype=torch.float32, device="cuda")
+        bs = torch.empty(len(ids), dtype=torch.int32, device="cuda")
+        vb.vapr_best_per_problem(r.cost_traj, len(ids), seeds, bc, bs)
+        gc, gs = gather_best(bc, bs, world)
+        q.put((rank, gc.cpu().numpy(), gs.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_bench_strong_sharding_two_ranks_equals_one():
+    """Two gloo ranks on one GPU running the bench's strong-scaling shards
+    give, after the all-gather, exactly the per-problem (best cost, best
+    seed) of the single-rank run over all problems (rank-major result: rank
+    r's entries are its shard's problems in order)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2310_07854_b200 import binding as vb
+    from paper_2310_07854_b200.rollout import Rollout
+    ppe, seeds, H, world = 2, 5, 32, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_shard_worker, args=(r, world, port, q, ppe, seeds, H))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=500) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 8 * ppe
+    wl = config4(problems_per_env=ppe, seeds=seeds, H=H)
+    r = Rollout(wl, device=0, sparse=True)
+    r.run()
+    bc = torch.empty(n, dtype=torch.float32, device="cuda")
+    bs = torch.empty(n, dtype=torch.int32, device="cuda")
+    vb.vapr_best_per_problem(r.cost_traj, n, seeds, bc, bs)
+    ref_c, ref_s = bc.cpu().numpy(), bs.cpu().numpy()
+    import bench
+    order = np.asarray([p for rr in range(world) for p in bench.shard_ids("strong", rr, world, ppe)])
+    for rank, gc, gs in res:
+        np.testing.assert_array_equal(gc.view(np.uint32), ref_c[order].view(np.uint32))
+        np.testing.assert_array_equal(gs, ref_s[order])

@@ -28,9 +28,11 @@ def test_pipeline_rates_deterministic_and_consistent(ev):
     assert set(a) == set(ev.envs) and all(0.0 <= v <= 1.0 for v in a.values())
     for k in last_a:
         assert np.array_equal(last_a[k], ev.last[k])
-    # success <=> IK accepted and a collision-free TO seed
-    ok = ev.last["ik_ok"] & np.any(ev.last["to_cost"] <= 0.0, axis=1)
+    # success <=> IK accepted (at full precision) and a TO seed collision-free
+    # at full precision
+    ok = ev.last["ik_ok"] & np.any(ev.last["to_cost_fp32"] <= 0.0, axis=1)
     assert np.array_equal(ok, ev.last["success"])
+    assert np.array_equal(ev.last["ik_ok"], ev.last["ik_cost_fp32"] <= ev.ik_tol)
 
 
 def test_pipeline_endpoints_frozen(ev):
@@ -57,3 +59,48 @@ def test_pipeline_as_search_evaluator(ev):
     memo = S.Memo(ev, targets, io.StringIO())
     (trial,) = memo.run([FP32], "pipeline")
     assert trial.feasible and set(trial.rates) == set(targets)
+
+
+def test_pipeline_validation_is_full_precision(ev):
+    """The success criterion uses all-E8M23 costs of the optimised variables:
+    with all-E8M23 formats they equal the optimiser's own costs bit for bit;
+    with a coarse out_spheres format a collision the quantised geometry hides
+    still fails the problem; and the validated TO costs agree with the oracle
+    rollout (oracle/rollout.py, all-E8M23) of the same trajectories."""
+    from oracle import rollout as orc
+    from parity_utils import check_close, e2e_kw
+    from workloads.configs import FP32
+    import dataclasses
+    ev.evaluate(FP32)
+    assert np.array_equal(ev.last["to_cost"].view(np.uint32), ev.last["to_cost_fp32"].view(np.uint32))
+    ev.evaluate(((2, 1),) + FP32[1:])                # E2M1 sphere positions
+    ok = ev.last["ik_ok"] & np.any(ev.last["to_cost_fp32"] <= 0.0, axis=1)
+    assert np.array_equal(ok, ev.last["success"])
+    x = ev.to.x.cpu().numpy().reshape(-1, ev.H, 7)
+    wl = dataclasses.replace(ev.to_wl, q=np.ascontiguousarray(x, np.float32), formats=FP32)
+    res = orc.rollout_workload(wl)
+    kw = e2e_kw(res, wl)
+    check_close(ev.last["to_cost_fp32"].reshape(-1), res.cost_traj, what="pipeline TO cost (fp32)",
+                **kw["cost_traj"])
+
+
+def test_pipeline_attempts():
+    """PAPER.md:78 retry attempts (reading c44): more attempts never lose a
+    success, the attempt counts are within the budget, deterministic."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2310_07854_b200.pipeline import PipelineEvaluator
+    from workloads.configs import FORMAT_SETS
+    kw = dict(problems_per_env=1, ik_seeds=16, to_seeds=4, H=16, ik_iters=15, to_iters=15)
+    one = PipelineEvaluator(attempts=1, **kw)
+    three = PipelineEvaluator(attempts=3, **kw)
+    cfg = FORMAT_SETS["43bit"]
+    r1 = one.evaluate(cfg)
+    r3 = three.evaluate(cfg)
+    s1, s3 = one.last["success"], three.last["success"]
+    assert np.all(s3 >= s1)                        # attempt 1 is the same plan
+    assert all(r3[e] >= r1[e] for e in r1)
+    used = three.last["attempts_used"]
+    assert used.min() >= 1 and used.max() <= 3
+    assert np.all(used[s3 & ~s1] >= 2)
+    assert three.evaluate(cfg) == r3

@@ -111,16 +111,18 @@ def config2():
 
 
 def config4(problems_per_env=100, seeds=100, H=32, formats="43bit",
-            problem_offset=0, n_problems=None):
+            problem_offset=0, n_problems=None, problem_ids=None):
     """800 problems (100 per environment) x 100 TO seeds x 32 steps.
 
     Problem p (global id) uses environment ENVIRONMENTS[p % 8] so that any
     contiguous or strided shard keeps the environment mix.  `problem_offset`
-    / `n_problems` select a shard of the global problem ids."""
+    / `n_problems` select a contiguous shard of the global problem ids,
+    `problem_ids` any list of them (the strong-scaling round-robin shard)."""
     total = problems_per_env * len(ENVIRONMENTS)
     if n_problems is None:
         n_problems = total
-    ids = list(range(problem_offset, problem_offset + n_problems))
+    ids = (list(problem_ids) if problem_ids is not None
+           else list(range(problem_offset, problem_offset + n_problems)))
     envs = [ENVIRONMENTS[p % len(ENVIRONMENTS)] for p in ids]
     fm = FORMAT_SETS[formats] if isinstance(formats, str) else formats
     return make_workload("config4", envs, ids, seeds, H, fm, salt=4)
@@ -168,7 +170,7 @@ IKO_PARAMS = dict(swept=0, sweep_steps=0, w_pose_pos=1.0, w_pose_rot=0.5, w_boun
 
 
 def config_iko(problems_per_env=10, seeds=400, formats="43bit", problem_offset=0,
-               n_problems=None):
+               n_problems=None, problem_ids=None):
     """N2 IKO workload: H = 1, `seeds` random joint configurations per problem
     (100-2000 IKO seeds), discrete world collision (closest_pt,
     slot 3), self collision, pose cost to the problem's goal and joint-bound
@@ -176,7 +178,8 @@ def config_iko(problems_per_env=10, seeds=400, formats="43bit", problem_offset=0
     total = problems_per_env * len(ENVIRONMENTS)
     if n_problems is None:
         n_problems = total
-    ids = list(range(problem_offset, problem_offset + n_problems))
+    ids = (list(problem_ids) if problem_ids is not None
+           else list(range(problem_offset, problem_offset + n_problems)))
     envs = [ENVIRONMENTS[p % len(ENVIRONMENTS)] for p in ids]
     fm = FORMAT_SETS[formats] if isinstance(formats, str) else formats
     wl = make_workload("iko", envs, ids, seeds, 1, fm, params=IKO_PARAMS, salt=7)
