@@ -137,9 +137,11 @@ enum {
     VAPR_OPT_STREAMS = 1,  /* vapr_cost_grad: trajectory chunks on this many context-owned
                               streams (1..8, default 1), forked from and joined back to the
                               caller's stream; results are bit-identical for any value */
-    VAPR_OPT_SPARSE = 2    /* N3: 1 = vapr_cost_grad stores grad_out_spheres in the sparse
-                              form (aggregation writes it, BK reads it; the workspace holds
-                              the sparse region instead of the dense slot, see
+    VAPR_OPT_SPARSE = 2    /* N3: 1 = vapr_cost_grad stores the three gradient tensors
+                              (closest_pt[_swept], out_vec, grad_out_spheres) in the sparse
+                              form (the collision passes write the first two, aggregation
+                              reads them and writes the third, BK reads it; the workspace
+                              holds the sparse regions instead of the dense slots, see
                               vapr_cost_grad_sparse_layout); 0 (default) = dense.  cost and
                               grad_q are bit-identical either way.  Changes the workspace
                               size: query vapr_cost_grad_workspace_bytes after setting it. */
@@ -363,15 +365,15 @@ vapr_status vapr_densify(vapr_format f, const uint64_t *mask, const uint32_t *of
                          void *stream);
 /* With VAPR_OPT_SPARSE = 1: byte offsets inside vapr_cost_grad's workspace
  * of (0) grad_out_spheres' mask [B*H], (1) its off [B*H], (2) used [1], (3)
- * the pool [pool_words], and the per-pose sphere bitmaps [B*H] uint64 of (4)
- * closest_pt[_swept] and (5) out_vec; *pool_words = the pool capacity.  In
- * this mode the collision passes do not zero-fill their rows: a field of a
- * closest_pt / out_vec row is valid only where its sphere's bit is set (the
- * others are stale), and the aggregation reads only those.  The dense
- * grad_out_spheres entry of vapr_cost_grad_workspace_layout is SIZE_MAX.
+ * its pool [pool_words]; (4) closest_pt[_swept]'s and (5) out_vec's mask
+ * [B*H] uint64; (6) closest_pt[_swept]'s and (7) out_vec's pool.  The two
+ * collision outputs use implicit row offsets: row p's codes start at word
+ * p * ceil(cols / pf) of their pool (capacity B*H*ceil(cols / pf) words);
+ * *pool_words = grad_out_spheres' pool capacity.  The dense entries of
+ * vapr_cost_grad_workspace_layout for the three gradient slots are SIZE_MAX.
  * VAPR_ERR_INVALID_ARG when the option is off. */
 vapr_status vapr_cost_grad_sparse_layout(const vapr_ctx *ctx, int32_t B, int32_t H,
-                                         size_t offsets[6], size_t *pool_words);
+                                         size_t offsets[8], size_t *pool_words);
 
 /* ---- test-only export (libvapr_tap.so, built with -DVAPR_DEBUG_TAP) ----- */
 /* SURVEY.md §8(b) "Test-only export", §8(c) parity contract (i): the next

@@ -111,7 +111,7 @@ def _load():
         "vapr_sparse_pool_words": ([vapr_format, SZ, SZ], SZ),
         "vapr_sparsify": ([vapr_format, P, SZ, SZ, P, P, P, SZ, P, P], I32),
         "vapr_densify": ([vapr_format, P, P, P, SZ, SZ, P, P], I32),
-        "vapr_cost_grad_sparse_layout": ([P, I32, I32, ctypes.POINTER(SZ * 6), ctypes.POINTER(SZ)],
+        "vapr_cost_grad_sparse_layout": ([P, I32, I32, ctypes.POINTER(SZ * 8), ctypes.POINTER(SZ)],
                                          I32),
     }
     for name, (args, res) in sig.items():
@@ -343,9 +343,9 @@ def vapr_cost_grad_workspace_layout(ctx, B, H, swept):
 
 
 def vapr_cost_grad_sparse_layout(ctx, B, H):
-    """(byte offsets of gos mask, off, used, pool, cp bitmaps, ov bitmaps; pool
-    capacity in words) with VAPR_OPT_SPARSE."""
-    arr = (ctypes.c_size_t * 6)()
+    """(byte offsets of gos mask, off, used, pool, cp bitmaps, ov bitmaps, cp
+    pool, ov pool; gos pool capacity in words) with VAPR_OPT_SPARSE."""
+    arr = (ctypes.c_size_t * 8)()
     pw = ctypes.c_size_t()
     _check(lib.vapr_cost_grad_sparse_layout(ctx, B, H, ctypes.byref(arr), ctypes.byref(pw)),
            "vapr_cost_grad_sparse_layout")

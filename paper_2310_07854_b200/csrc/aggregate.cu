@@ -143,17 +143,16 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
     });
 }
 
-// ---------------------------------------------------------------------------
-// N3, masked inputs (VAPR_OPT_SPARSE inside vapr_cost_grad): closest_pt and
-// out_vec come as rows plus per-pose sphere bitmaps (the collision passes do
-// not zero-fill; a field is valid only if its sphere's bit is set), the
-// output is the sparse form with row p at pool word seg0 + p * wmax.  One
-// thread per row: a row with both bitmaps empty (most rows) costs two 8-byte
-// loads; otherwise the set spheres in ascending order, each element
-// dec(cp) + dec(ov) in FP32 (+0 for an unset sphere: the dense value), encode3,
-// and the codes of spheres with a non-zero code are packed as they come.
+// N3 (VAPR_OPT_SPARSE): closest_pt[_swept] and out_vec in the sparse form
+// (per-row sphere bitmap, the non-zero spheres' codes packed in ascending
+// sphere order at pool + row * ceil(cols / pf)) -> grad_out_spheres in the
+// sparse form.  A thread per row: a row with both bitmaps empty (most rows)
+// costs two 8-byte loads; otherwise the union of the two bitmaps in ascending
+// order, each element dec(cp) + dec(ov) in FP32 (+0 for a sphere absent from
+// one side: its dense value), encode3, and the codes of the spheres with a
+// non-zero code packed as they come.
 __global__ void __launch_bounds__(128)
-aggregate_masked_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int Wc, int Wo,
+aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int wo,
                         const uint32_t* __restrict__ cp, const unsigned long long* __restrict__ cpm,
                         const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
                         long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
@@ -164,10 +163,11 @@ aggregate_masked_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int Wc, int 
         unsigned long long m = mc | mo, mg = 0ull;
         const uint32_t o = sp.seg0 + (uint32_t)p * sp.wmax;
         if (m) {
-            const uint32_t* rc = cp + p * Wc;
-            const uint32_t* ro = ov + p * Wo;
+            const uint32_t* rc = cp + p * wc;
+            const uint32_t* ro = ov + p * wo;
             uint32_t word = 0u;
             int q = 0;
+            int kc = 0, ko = 0;                       // codes consumed from each side
             while (m) {
                 const int s = __ffsll((long long)m) - 1;
                 m &= m - 1;
@@ -175,25 +175,26 @@ aggregate_masked_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int Wc, int 
                 float x[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const uint32_t e = 3u * s + c;
                     float a = 0.f, b = 0.f;
                     if (inc) {
-                        const uint32_t w = (e * rcp_c) >> 16;
-                        a = decode_sp(code_at(__ldcs(rc + w), (int)(e - w * fcp.pf), fcp), fcp);
+                        const uint32_t e = kc + c, w = (e * rcp_c) >> 16;      // e / pf
+                        a = decode_sp(code_at(__ldcs(rc + w), int(e - w * fcp.pf), fcp), fcp);
                     }
                     if (ino) {
-                        const uint32_t w = (e * rcp_o) >> 16;
-                        b = decode_sp(code_at(__ldcs(ro + w), (int)(e - w * fov.pf), fov), fov);
+                        const uint32_t e = ko + c, w = (e * rcp_o) >> 16;
+                        b = decode_sp(code_at(__ldcs(ro + w), int(e - w * fov.pf), fov), fov);
                     }
                     x[c] = a + b;
                 }
+                kc += inc ? 3 : 0;
+                ko += ino ? 3 : 0;
                 uint32_t c3[3];
                 encode3(x[0], x[1], x[2], fg, c3);
                 if (!(c3[0] | c3[1] | c3[2])) continue;
                 mg |= 1ull << s;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    word |= c3[c] << (q * fg.t);
+                    word |= (fg.t == 32) ? c3[c] : (c3[c] << (q * fg.t));
                     if (++q == fg.pf) {
                         sp.pool[o + nw++] = word;
                         word = 0u;
@@ -214,18 +215,18 @@ aggregate_masked_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int Wc, int 
 
 }  // namespace
 
-cudaError_t launch_aggregate_masked(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
-                                    const uint32_t* cp, const unsigned long long* cpm,
-                                    const uint32_t* ov, const unsigned long long* ovm,
+cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
+                                    const uint32_t* cp_pool, const unsigned long long* cpm,
+                                    const uint32_t* ov_pool, const unsigned long long* ovm,
                                     long long rows, const SparseOut& sparse, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
     SparseOut spo = sparse;
     spo.wmax = (uint32_t)((cols + fgos.pf - 1) / fgos.pf);
     spo.rcp = 65536u / fgos.pf + 1u;
-    const int Wc = row_words_of(fcp, cols), Wo = row_words_of(fov, cols);
+    const int wc = (cols + fcp.pf - 1) / fcp.pf, wo = (cols + fov.pf - 1) / fov.pf;
     const long long grid = (rows + 127) / 128;
-    aggregate_masked_kernel<<<(unsigned)grid, 128, 0, s>>>(fcp, fov, fgos, Wc, Wo, cp, cpm, ov, ovm,
-                                                           rows, 65536u / fcp.pf + 1u,
+    aggregate_sparse_kernel<<<(unsigned)grid, 128, 0, s>>>(fcp, fov, fgos, wc, wo, cp_pool, cpm,
+                                                           ov_pool, ovm, rows, 65536u / fcp.pf + 1u,
                                                            65536u / fov.pf + 1u, spo);
     return cudaGetLastError();
 }

@@ -75,7 +75,7 @@ struct DeviceGuard {
 };
 
 // vapr_cost_grad_sparse_layout entries (N3)
-constexpr int kSparseOffs = 6;
+constexpr int kSparseOffs = 8;
 
 // sparse form of a tensor (N3): pool capacity in words (every row full)
 size_t sparse_pool_words_of(const Fmt& f, int cols, long long rows) {
@@ -738,31 +738,41 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
     off[VAPR_OUT_SPHERES] = o;
     o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_SPHERES], cols, P));
     const int cps = swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
-    off[cps] = o;
-    // reserve the larger of the two collision slots so one workspace serves both modes
-    o = align256(o + std::max(packed_bytes(c->dfmt[VAPR_CLOSEST_PT], cols, P),
-                              packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
-    off[VAPR_OUT_VEC] = o;
-    o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
     if (c->sparse) {
+        // N3: the three gradient tensors in the sparse form -- per row a
+        // sphere bitmap and the non-zero codes packed at pool + row * wmax
+        // (closest_pt[_swept], out_vec) or at the row's own offset
+        // (grad_out_spheres: off [P] and the words-in-use counter)
         size_t so[kSparseOffs];
-        so[0] = o;                                            // mask [P] uint64
+        so[0] = o;                                            // gos mask [P] uint64
         o = align256(o + sizeof(uint64_t) * (size_t)P);
-        so[1] = o;                                            // off [P] uint32
+        so[1] = o;                                            // gos off [P] uint32
         o = align256(o + sizeof(uint32_t) * (size_t)P);
-        so[2] = o;                                            // used
+        so[2] = o;                                            // gos used
         o = align256(o + sizeof(uint32_t));
-        so[3] = o;                                            // pool
+        so[3] = o;                                            // gos pool
         const size_t pw = sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P);
         o = align256(o + sizeof(uint32_t) * pw);
         so[4] = o;                                            // closest_pt bitmaps [P]
         o = align256(o + sizeof(uint64_t) * (size_t)P);
         so[5] = o;                                            // out_vec bitmaps [P]
         o = align256(o + sizeof(uint64_t) * (size_t)P);
+        so[6] = o;                                            // closest_pt pool (either slot)
+        o = align256(o + sizeof(uint32_t) *
+                             std::max(sparse_pool_words_of(c->dfmt[VAPR_CLOSEST_PT], cols, P),
+                                      sparse_pool_words_of(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
+        so[7] = o;                                            // out_vec pool
+        o = align256(o + sizeof(uint32_t) * sparse_pool_words_of(c->dfmt[VAPR_OUT_VEC], cols, P));
         if (sp)
             for (int i = 0; i < kSparseOffs; ++i) sp[i] = so[i];
         if (pool_words) *pool_words = pw;
     } else {
+        off[cps] = o;
+        // reserve the larger of the two collision slots so one workspace serves both modes
+        o = align256(o + std::max(packed_bytes(c->dfmt[VAPR_CLOSEST_PT], cols, P),
+                                  packed_bytes(c->dfmt[VAPR_CLOSEST_PT_SWEPT], cols, P)));
+        off[VAPR_OUT_VEC] = o;
+        o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_VEC], cols, P));
         off[VAPR_GRAD_OUT_SPHERES] = o;
         o = align256(o + packed_bytes(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, P));
     }
@@ -818,8 +828,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         return reinterpret_cast<uint32_t*>(ws + off[slot]) + p0 * row_words_of(c->dfmt[slot], cols);
     };
     uint32_t* os = rows_of(VAPR_OUT_SPHERES);
-    uint32_t* cp = rows_of(cps);
-    uint32_t* ov = rows_of(VAPR_OUT_VEC);
+    uint32_t* cp = c->sparse ? nullptr : rows_of(cps);
+    uint32_t* ov = c->sparse ? nullptr : rows_of(VAPR_OUT_VEC);
     uint32_t* gos = c->sparse ? nullptr : rows_of(VAPR_GRAD_OUT_SPHERES);
     // N3: grad_out_spheres in the sparse form (rows p0.. of mask / off; the
     // pool and its cursor are shared by all chunks)
@@ -837,6 +847,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         spo.seg0 = (uint32_t)sparse_pool_words_of(c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, p0);
         cp_mask = reinterpret_cast<unsigned long long*>(ws + so[4]) + p0;
         ov_mask = reinterpret_cast<unsigned long long*>(ws + so[5]) + p0;
+        cp = reinterpret_cast<uint32_t*>(ws + so[6]) + sparse_pool_words_of(c->dfmt[cps], cols, p0);
+        ov = reinterpret_cast<uint32_t*>(ws + so[7]) + sparse_pool_words_of(c->dfmt[VAPR_OUT_VEC], cols, p0);
         spi.mask = spo.mask;
         spi.off = spo.off;
         spi.pool = spo.pool;
@@ -896,7 +908,7 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost);
     mark(3);
     if (e == cudaSuccess)
-        e = c->sparse ? launch_aggregate_masked(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
+        e = c->sparse ? launch_aggregate_sparse(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
                                                 ov, ov_mask, P, spo, s)
                       : launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],

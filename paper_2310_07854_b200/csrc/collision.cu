@@ -39,6 +39,7 @@
 // without culling, so VAPR_OPT_CULL on and off give bit-identical results
 // (tests/test_gpu_parity.py::test_cull_is_exact).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -118,39 +119,56 @@ __device__ __forceinline__ void world_term(const Cub& b, float cx, float cy, flo
     acc.gz = fmaf(sc, gzw, acc.gz);
 }
 
-// N3 masked rows (not zero-filled): a sphere with a non-zero code sets its
-// bitmap bit and overwrites its three fields (clear, then OR: the other
-// spheres' fields of a shared word are untouched)
-__device__ __forceinline__ void or_code3_masked(uint32_t* row, int e, float vx, float vy, float vz,
-                                                const Fmt& f, uint32_t rc,
-                                                unsigned long long* pmask) {
-    const float v[3] = {vx, vy, vz};
-    uint32_t c[3];
+// N3 sparse form of a gradient tensor (VAPR_OPT_SPARSE; reading c42): a
+// pose's sphere bitmap and its non-zero codes packed in ascending sphere
+// order at pool + pose * ceil(cols / pf).  The owner lane of a pose appends
+// its spheres in order (the warp queue hands them back in ascending order).
+struct SparseRow {
+    uint32_t* row;
+    uint32_t word = 0u;
+    int q = 0, nw = 0;
+    unsigned long long mask = 0ull;
+    // the codes of a vector (computed by the item, in parallel)
+    // (float2: the three codes in one word, t <= 10; float4: one word each)
+    template <typename QT>
+    __device__ __forceinline__ static QT codes(float vx, float vy, float vz, float cost,
+                                               const Fmt& f) {
+        const float v[3] = {vx + 0.f, vy + 0.f, vz + 0.f};
+        uint32_t c[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) c[k] = (__float_as_uint(v[k]) != 0u) ? encode(v[k], f) : 0u;
-    if (!(c[0] | c[1] | c[2])) return;
-    atomicOr(pmask, 1ull << (e / 3));
-    int cw = -1;
-    uint32_t acc = 0u, fm = 0u;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int ec = e + k;
-        const int w = int((ec * rc) >> 16);
-        if (w != cw) {
-            if (cw >= 0) {
-                atomicAnd(row + cw, ~fm);
-                if (acc) atomicOr(row + cw, acc);
-            }
-            cw = w;
-            acc = fm = 0u;
-        }
-        const int sh = (ec - w * f.pf) * f.t;
-        acc |= c[k] << sh;
-        fm |= f.mask << sh;
+        for (int k = 0; k < 3; ++k) c[k] = (__float_as_uint(v[k]) != 0u) ? encode(v[k], f) : 0u;
+        if constexpr (sizeof(QT) == 8)
+            return make_float2(__uint_as_float(c[0] | (c[1] << f.t) | (c[2] << (2 * f.t))), cost);
+        else
+            return make_float4(__uint_as_float(c[0]), __uint_as_float(c[1]), __uint_as_float(c[2]), cost);
     }
-    atomicAnd(row + cw, ~fm);
-    if (acc) atomicOr(row + cw, acc);
-}
+    // append one sphere's codes (the owner, in ascending sphere order)
+    __device__ __forceinline__ void put(int s, const float2& r, const Fmt& f) {
+        const uint32_t w = __float_as_uint(r.x);
+        put3(s, w & f.mask, (w >> f.t) & f.mask, (w >> (2 * f.t)) & f.mask, f);
+    }
+    __device__ __forceinline__ void put(int s, const float4& r, const Fmt& f) {
+        put3(s, __float_as_uint(r.x), __float_as_uint(r.y), __float_as_uint(r.z), f);
+    }
+    __device__ __forceinline__ void put3(int s, uint32_t c0, uint32_t c1, uint32_t c2, const Fmt& f) {
+        const uint32_t c[3] = {c0, c1, c2};
+        if (!(c[0] | c[1] | c[2])) return;
+        mask |= 1ull << s;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            word |= (f.t == 32) ? c[k] : (c[k] << (q * f.t));
+            if (++q == f.pf) {
+                row[nw++] = word;
+                word = 0u;
+                q = 0;
+            }
+        }
+    }
+    __device__ __forceinline__ void finish(unsigned long long* mask_out) {
+        if (q) row[nw] = word;
+        *mask_out = mask;
+    }
+};
 
 // OR the codes of the vector (vx, vy, vz) at elements e .. e+2 into a packed
 // row: codes sharing a word go in one atomic, +0 components (code 0, the
@@ -252,6 +270,7 @@ constexpr int kQ = 128;            // work-queue window (items)
 
 struct Geo {
     int Wos, Wcp, Wov;             // packed row words
+    int wmax_cp, wmax_ov;          // sparse pool segment per pose (words)
     int Qos;                       // 16-byte groups per out_spheres row
     int cs;                        // FP32 tile row stride (odd: lane-per-pose access is conflict-free)
     int pmw;                       // words of the per-pose active-pair mask
@@ -266,11 +285,13 @@ struct Geo {
 };
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
-             int do_self) {
+             int do_self, int sparse) {
     Geo g{};
     g.Wos = row_words_of(fos, R.cols);
     g.Wcp = do_world ? row_words_of(fcp, R.cols) : 0;
     g.Wov = do_self ? row_words_of(fov, R.cols) : 0;
+    g.wmax_cp = (R.cols + fcp.pf - 1) / fcp.pf;
+    g.wmax_ov = (R.cols + fov.pf - 1) / fov.pf;
     g.Qos = g.Wos / 4;
     int cs = std::max(R.cols, g.Wos * fos.pf);
     g.cs = cs | 1;
@@ -315,7 +336,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.wm = take(do_world ? 4u * kTP * kLinks : 0u, 4);
     g.pk0 = take(do_world ? 4u * kTP : 0u, 4);
     g.qi = take(2u * kQ, 2);
-    g.qc = take(4u * kQ, 4);
+    g.qc = take((sparse == 2 ? 16u : sparse == 1 ? 8u : 4u) * kQ, 16);   // item results: codes + cost / cost
     g.warp = take(0, 16);
     return g;
 }
@@ -323,14 +344,22 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
 // Warp work queue.  Every lane owns the items given by the set bits of its
 // 128-bit mask (item = p << shift | bit); the warp processes all of them, kQ
 // at a time, LPI lanes per item (fn(item, sub) with sub = 0 .. LPI-1), and,
-// with LPI == 1, each lane gets back the sum of the costs `fn` returned for
-// its own items in ascending bit order (the items of a lane are contiguous in
-// the queue, so the order is fixed by the mask alone and never by which lane
-// processed what).  All lanes must call it.
-template <int LPI, typename Fn>
+// with LPI == 1, each lane gets back the results fn returned for its own
+// items in ascending bit order -- cons(item, result) per item, and the sum of
+// the results' .w (the items of a lane are contiguous in the queue, so the
+// order is fixed by the mask alone and never by which lane processed what).
+// All lanes must call it.
+struct NoCons {
+    template <typename T>
+    __device__ __forceinline__ void operator()(int, const T&) const {}
+};
+__device__ __forceinline__ float cost_of(float r) { return r; }
+__device__ __forceinline__ float cost_of(const float4& r) { return r.w; }
+__device__ __forceinline__ float cost_of(const float2& r) { return r.y; }
+template <int LPI, typename QT, typename Fn, typename Cons = NoCons>
 __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long long hi, int p,
-                                            int shift, uint16_t* qi, float* qc, int lane,
-                                            Fn&& fn) {
+                                            int shift, uint16_t* qi, QT* qc, int lane,
+                                            Fn&& fn, Cons&& cons = Cons{}) {
     const int n = __popcll(lo) + __popcll(hi);
     int inc = n;
 #pragma unroll
@@ -362,7 +391,11 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
             for (int i = lane; i < cnt; i += 32) qc[i] = fn((int)qi[i], 0);
             __syncwarp();
             const int e = min(base + n, win + cnt);
-            for (int idx = max(base, win); idx < e; ++idx) sum += qc[idx - win];
+            for (int idx = max(base, win); idx < e; ++idx) {
+                const QT r = qc[idx - win];
+                sum += cost_of(r);
+                cons((int)qi[idx - win], r);
+            }
         } else {
             const int sub = lane % LPI;
             for (int i = lane / LPI; i < cnt; i += 32 / LPI) fn((int)qi[i], sub);
@@ -378,10 +411,12 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
 // spheres, live group pairs, touched spheres) goes through warp work queues
 // so that every lane has an item.  Warps are independent: no CTA barrier in
 // the tile loop.
-// MASKED (N3, VAPR_OPT_SPARSE): per-pose sphere bitmaps instead of zero-filled
-// rows -- its own instantiation, so the dense one carries no extra code (the
-// kernel is instruction-cache sensitive).
-template <bool MASKED>
+// SPARSE (N3, VAPR_OPT_SPARSE): the gradient outputs in the sparse form
+// (SparseRow) instead of zero-filled dense rows -- its own instantiation, so
+// the dense one carries no extra code (the kernel is instruction-cache
+// sensitive); SP_WIDE: the item results hold one code per word (formats of
+// more than 10 bits) rather than all three in one word.
+template <bool SPARSE, bool SP_WIDE>
 __global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
@@ -460,7 +495,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint32_t* wm = reinterpret_cast<uint32_t*>(wb + G.wm);
     int* pk0 = reinterpret_cast<int*>(wb + G.pk0);
     uint16_t* qi = reinterpret_cast<uint16_t*>(wb + G.qi);
-    float* qc = reinterpret_cast<float*>(wb + G.qc);
+    // item results in the queue window: the codes + cost (sparse) or the cost
+    using QcT = typename std::conditional<SPARSE, typename std::conditional<SP_WIDE, float4, float2>::type,
+                                          float>::type;
+    QcT* qc = reinterpret_cast<QcT*>(wb + G.qc);
 
     const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
@@ -566,26 +604,19 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             });
         }
         amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(amax)));
-        // the output rows are zero-filled here and their non-zero codes ORed in
-        // with atomics (__syncwarp orders the fill before every lane's atomics)
-        uint32_t* const cpg = a.do_world ? a.cp + p0 * G.Wcp : nullptr;
-        uint32_t* const ovg = a.do_self ? a.ov + p0 * G.Wov : nullptr;
-        // N3 masked rows: only the tile's bitmaps are cleared
-        unsigned long long* const cpm = (MASKED && a.do_world) ? a.cp_mask + p0 : nullptr;
-        unsigned long long* const ovm = (MASKED && a.do_self) ? a.ov_mask + p0 : nullptr;
-        if (cpm) {
-            if (lane < np) cpm[lane] = 0ull;
-        } else if (a.do_world) {
+        // dense: the output rows are zero-filled here and their non-zero codes
+        // ORed in with atomics (__syncwarp orders the fill before every lane's
+        // atomics); sparse: each pose's owner lane appends its codes to the
+        // pose's pool segment and writes its bitmap
+        uint32_t* const cpg = (!SPARSE && a.do_world) ? a.cp + p0 * G.Wcp : nullptr;
+        uint32_t* const ovg = (!SPARSE && a.do_self) ? a.ov + p0 * G.Wov : nullptr;
+        if (!SPARSE && a.do_world)
             for (int i = lane; i < np * G.Wcp / 4; i += 32)
                 reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
-        }
         if (a.do_self) {
-            if (ovm) {
-                if (lane < np) ovm[lane] = 0ull;
-            } else {
+            if (!SPARSE)
                 for (int i = lane; i < np * G.Wov / 4; i += 32)
                     reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
-            }
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
             if (lane < kTP) pwm[lane] = 0u;
         }
@@ -686,7 +717,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // live (pose, sphere) items: the complete gradient of the sphere
             // (no scatter), its codes ORed into the packed tile row
             VAPR_STAT(0, __popcll(smask));
-            wcost = warp_queue<1>(smask, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
+            SparseRow sr_cp;
+            if (SPARSE && owner) sr_cp.row = a.cp + (p0 + pl) * G.wmax_cp;
+            wcost = warp_queue<1>(smask, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> QcT {
                 const int p = it >> 6, sp = it & 63;
                 const int l = slink[sp];
                 const uint32_t v = wm[p * kLinks + l];
@@ -742,17 +775,20 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
                                    a.w_w, cw, gw, acc);
                 }
-                uint32_t* orow = cpg + p * G.Wcp;
+                uint32_t* orow = SPARSE ? nullptr : cpg + p * G.Wcp;
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp, acc.gx + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 1, acc.gy + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 2, acc.gz + 0.f);
-                if (MASKED)
-                    or_code3_masked(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp,
-                                    G.rc_cp, cpm + p);
-                else
+                if constexpr (SPARSE) {
+                    return SparseRow::codes<QcT>(acc.gx, acc.gy, acc.gz, acc.cost, fcp);
+                } else {
                     or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
-                return acc.cost;
+                    return acc.cost;
+                }
+            }, [&](int it, const QcT& r) {
+                if constexpr (SPARSE) sr_cp.put(it & 63, r, fcp);
             });
+            if (SPARSE && owner) sr_cp.finish(a.cp_mask + p0 + pl);
         }
 
         // ---- 3. self
@@ -900,7 +936,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 }
             VAPR_STAT(5, __popcll(tb));
             if (owner) VAPR_STAT(6, __popc(pwm[pl]));
-            scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> float {
+            SparseRow sr_ov;
+            if (SPARSE && owner) sr_ov.row = a.ov + (p0 + pl) * G.wmax_ov;
+            scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> QcT {
                 const int p = it >> 6, s = it & 63;
                 const float* crow = rows + (p + 1) * cs;
                 const uint32_t* pm = pmask + p * PMW;
@@ -924,16 +962,20 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         if (i == s) c_lead += c;
                     }
                 }
-                uint32_t* orow = ovg + p * G.Wov;
+                uint32_t* orow = SPARSE ? nullptr : ovg + p * G.Wov;
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 1, gy + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 2, gz + 0.f);
-                if (MASKED)
-                    or_code3_masked(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov, ovm + p);
-                else
+                if constexpr (SPARSE) {
+                    return SparseRow::codes<QcT>(gx, gy, gz, c_lead, fov);
+                } else {
                     or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
-                return c_lead;
+                    return c_lead;
+                }
+            }, [&](int it, const QcT& r) {
+                if constexpr (SPARSE) sr_ov.put(it & 63, r, fov);
             });
+            if (SPARSE && owner) sr_ov.finish(a.ov_mask + p0 + pl);
         }
         if (owner) VAPR_STAT(7, 1);
         if (owner) {
@@ -1016,7 +1058,9 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
                                   const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                                   cudaStream_t s) {
     const long long P = (long long)a.B * a.H;
-    const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self);
+    const bool sparse = a.cp_mask || a.ov_mask;
+    const bool wide = (a.do_world && fcp.t > 10) || (a.do_self && fov.t > 10);
+    const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0);
     if (G.rc_q == 0) return cudaErrorInvalidValue;
     int dev = 0, sms = 148, optin = 0;
     cudaGetDevice(&dev);
@@ -1028,7 +1072,8 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     nw = std::min(nw, VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
-    auto kern = (a.cp_mask || a.ov_mask) ? collision_kernel<true> : collision_kernel<false>;
+    auto kern = !sparse ? collision_kernel<false, false>
+                        : (wide ? collision_kernel<true, true> : collision_kernel<true, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;

@@ -26,12 +26,11 @@ struct CollisionArgs {
     float eta_w, w_w, eta_s, w_s;
     int32_t cull;
     float* cost;              // [B*H] (world + self of the enabled parts)
-    uint32_t* cp;             // packed world gradient (nullable iff !do_world)
-    uint32_t* ov;             // packed self gradient (nullable iff !do_self)
-    // N3 (VAPR_OPT_SPARSE; nullable = dense): per-pose sphere bitmaps of cp / ov.
-    // With them the rows are not zero-filled: a sphere with a non-zero code
-    // sets its bit and overwrites its own fields, and readers take only the
-    // fields of set spheres.
+    uint32_t* cp;             // world gradient: dense rows, or (cp_mask) the sparse pool
+    uint32_t* ov;             // self gradient: dense rows, or (ov_mask) the sparse pool
+    // N3 (VAPR_OPT_SPARSE; nullable = dense rows): per-pose sphere bitmaps.
+    // With them a pose's non-zero codes are packed in ascending sphere order
+    // at pool + pose * ceil(cols / pf) (reading c42)
     unsigned long long* cp_mask;
     unsigned long long* ov_mask;
     // vapr_cost_grad (nullable): the self pass writes its cost here and
@@ -95,10 +94,11 @@ cudaError_t launch_densify(const Fmt& f, const SparseIn& in, long long rows, int
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
                              uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr);
-// N3 masked inputs (cp / ov rows + sphere bitmaps, not zero-filled) -> sparse form
-cudaError_t launch_aggregate_masked(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
-                                    const uint32_t* cp, const unsigned long long* cpm,
-                                    const uint32_t* ov, const unsigned long long* ovm,
+// N3 sparse inputs (cp / ov: sphere bitmaps + packed non-zero codes at
+// pool + row * ceil(cols / pf)) -> the sparse form of grad_out_spheres
+cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
+                                    const uint32_t* cp_pool, const unsigned long long* cpm,
+                                    const uint32_t* ov_pool, const unsigned long long* ovm,
                                     long long rows, const SparseOut& sparse, cudaStream_t s);
 // sparse (nullable): read grad_out_spheres from the sparse form instead of gos
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,

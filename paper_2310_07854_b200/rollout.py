@@ -123,13 +123,22 @@ class Rollout:
                                self.grad_q, cost_traj_host, grad_q_host, n_chunks,
                                stream=stream, _p=self._p)
 
+    def _rows_of_pool(self, mask, pool_t, base, wmax, pf):
+        out = []
+        for i, mi in enumerate(mask):
+            n = -(-3 * bin(int(mi)).count("1") // pf)
+            o = base + i * wmax
+            out.append(pool_t[o:o + n].cpu().numpy().view(np.uint32))
+        return out
+
     def sparse_gos(self, rows=None):
         """N3 (sparse mode): grad_out_spheres' mask [P] uint64, off [P], the
         pool (its whole capacity) and the count of words in use, as numpy
         arrays.  rows (a slice of poses): only those rows' masks / offsets,
         and `row_words` = each of those rows' pool words."""
         torch.cuda.synchronize(self.device)
-        (mo, oo, uo, po, _, _), pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        lay, pw = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        mo, oo, uo, po = lay[:4]
         P = self.B * self.H
         ws = self.workspace
         mask = ws[mo:mo + 8 * P].view(torch.int64)
@@ -149,40 +158,34 @@ class Rollout:
             rw.append(pool_t[int(oi):int(oi) + n].cpu().numpy().view(np.uint32))
         return dict(mask=m, off=o, row_words=rw, used=used)
 
-    def sphere_masks(self, rows=None):
-        """N3 (sparse mode): per-pose sphere bitmaps of closest_pt[_swept] and
-        out_vec (uint64 [P] each, or of the poses in `rows`)."""
+    def sparse_slot(self, slot, rows=None):
+        """N3 (sparse mode): a collision output (closest_pt[_swept] or out_vec)
+        in the sparse form -- its sphere bitmaps [P] (or of the poses in `rows`)
+        and each row's packed codes (row p at pool word p * ceil(cols / pf))."""
         torch.cuda.synchronize(self.device)
-        (_, _, _, _, cmo, omo), _ = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        lay, _ = vb.vapr_cost_grad_sparse_layout(self.ctx.h, self.B, self.H)
+        is_ov = slot == vb.VAPR_OUT_VEC
+        mo, po = (lay[5], lay[7]) if is_ov else (lay[4], lay[6])
         P = self.B * self.H
+        fmt = self.ctx.formats[slot]
+        pf = 32 // (1 + fmt[0] + (fmt[1] & 0xFF))
+        cols = 3 * len(self.wl.robot["sphere_link"])
+        wmax = -(-cols // pf)
         ws = self.workspace
         rows = rows if rows is not None else slice(0, P)
-        return (ws[cmo:cmo + 8 * P].view(torch.int64)[rows].cpu().numpy().view(np.uint64),
-                ws[omo:omo + 8 * P].view(torch.int64)[rows].cpu().numpy().view(np.uint64))
+        mask = ws[mo:mo + 8 * P].view(torch.int64)[rows].cpu().numpy().view(np.uint64)
+        pool_t = ws[po:po + 4 * wmax * P].view(torch.int32)
+        return dict(mask=mask, row_words=self._rows_of_pool(mask, pool_t, wmax * rows.start, wmax, pf))
 
-    def packed_masked(self, slot, rows=None):
-        """N3 (sparse mode): a collision slot's rows with the fields of unset
-        spheres zeroed -- the dense mode's rows (all, or the poses in `rows`)."""
-        words = self.packed(slot, rows)
-        cm, om = self.sphere_masks(rows)
-        m = om if slot == vb.VAPR_OUT_VEC else cm
+    def packed_dense(self, slot, rows=None):
+        """N3 (sparse mode): a collision output densified by the oracle's
+        definition (oracle/sparse.py) into the dense packed rows."""
+        from oracle import codec, sparse as osp
+        sp = self.sparse_slot(slot, rows)
         fmt = self.ctx.formats[slot]
-        t = 1 + fmt[0] + (fmt[1] & 0xFF)
-        pf = 32 // t
         cols = 3 * len(self.wl.robot["sphere_link"])
-        out = words.copy()
-        for e in range(cols):
-            keep = ((m >> np.uint64(e // 3)) & np.uint64(1)).astype(bool)
-            w, q = e // pf, e % pf
-            fm = np.uint32(((1 << t) - 1) << (q * t)) if t < 32 else np.uint32(0xFFFFFFFF)
-            out[~keep, w] &= ~fm
-        W = words.shape[1]
-        # padding slots of the last used word and padding words are never written
-        for e in range(cols, W * pf):
-            w, q = e // pf, e % pf
-            fm = np.uint32(((1 << t) - 1) << (q * t)) if t < 32 else np.uint32(0xFFFFFFFF)
-            out[:, w] &= ~fm
-        return out
+        return codec.pack(osp.densify(sp["mask"], sp["row_words"], fmt[0], fmt[1] & 0xFF, cols),
+                          fmt[0], fmt[1] & 0xFF)
 
     def packed(self, slot, rows=None):
         """The packed tensor of `slot` inside the workspace, as uint32 [P, W]

@@ -538,7 +538,7 @@ def test_full_size_sampled(vb, storage):
                              p["eta_world"], p["w_world"], 1, p["sweep_steps"], f[4])
         ss = orc.self_stage(os_w, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
         if storage == "sparse":
-            cp_w, ov_w = r.packed_masked(4, rows), r.packed_masked(2, rows)
+            cp_w, ov_w = r.packed_dense(4, rows), r.packed_dense(2, rows)
             sg = r.sparse_gos(rows)
             gos_w = codec.pack(osp.densify(sg["mask"], sg["row_words"], *f[1], cols), *f[1])
         else:

@@ -192,11 +192,19 @@ def check_pair(wl, a, b):
     sg = b.sparse_gos()
     check_sparse_rows(sg["mask"], sg["off"], sg["pool"], sg["used"], ref_mask, ref_rows)
     assert b.packed(1) is None         # no dense slot in sparse mode
-    # the collision rows (not zero-filled in sparse mode) restricted to their
-    # bitmaps' spheres are the dense mode's rows
+    # the collision outputs in the sparse form: exactly the oracle's sparse
+    # form of the dense mode's rows (mask and packed codes), and densified
+    # they are those rows
     slot = 4 if wl.params["swept"] else 3
     for sl in (slot, 2):
-        assert np.array_equal(b.packed_masked(sl), a.packed(sl)), sl
+        fs = a.ctx.formats[sl]
+        assert b.packed(sl) is None, sl          # no dense slot in sparse mode
+        m_ref, rows_ref = osp.sparsify(codec.unpack(a.packed(sl), *fs, cols), *fs)
+        got = b.sparse_slot(sl)
+        assert np.array_equal(got["mask"], m_ref), sl
+        for k, (x, y) in enumerate(zip(got["row_words"], rows_ref)):
+            assert np.array_equal(x, y), (sl, k)
+        assert np.array_equal(b.packed_dense(sl), a.packed(sl)), sl
     # oracle parity of the sparse mode itself: its rows, densified by the
     # oracle, against the oracle's aggregation of the GPU's own collision
     # outputs (the dense stagewise rule), and BK of those codes
@@ -205,7 +213,7 @@ def check_pair(wl, a, b):
     g_codes = osp.densify(sg["mask"], [sg["pool"][int(o):int(o) + osp.row_words(m, *fg)]
                                        for m, o in zip(sg["mask"], sg["off"])], *fg, cols)
     g_words = codec.pack(g_codes, *fg)
-    ag = orc.aggregate_stage(b.packed_masked(slot), f[slot], b.packed_masked(2), f[2], fg, cols)
+    ag = orc.aggregate_stage(b.packed_dense(slot), f[slot], b.packed_dense(2), f[2], fg, cols)
     check_codes(g_words, ag["v"], ag["terms"], 0.0, fg, cols, what="sparse grad_out_spheres")
     bk = orc.bk_stage(wl.q.reshape(-1, 7), g_words, fg, wl.robot)
     ik = orc.ik_terms(wl.q, wl.world_idx, wl.robot, p, getattr(wl, "goals", None), wl.H)
