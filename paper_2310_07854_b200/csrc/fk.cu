@@ -2,8 +2,8 @@
 // P:86 (forward kinematics), P:189 ("The output of forward kinematics:
 // out_spheres"); quantised at the store (reading c19).
 //
-// One thread per pose walks the 8-row modified-DH chain in FP32 (full
-// precision sincosf) and places the spheres of each link as soon as its frame
+// One thread per pose walks the 8-row modified-DH chain in FP32 (sincos_joint:
+// ~1 ulp, bounded argument) and places the spheres of each link as soon as its frame
 // is known.  The 3S coordinates stream through a PF-deep register shift
 // buffer (PF = codes per word, a compile-time constant via with_pf; the
 // element count is warp-uniform, so there is no divergence) and every full
