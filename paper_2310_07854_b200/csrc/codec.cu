@@ -10,6 +10,13 @@
 // coalesced loads/stores through a bank-padded shared-memory staging buffer.
 // Packed words are moved as one 16-byte vector per lane: a warp touches 512
 // contiguous bytes per instruction.
+//
+// Fast path (cols % 4 == 0, 16-byte aligned arrays -- every group then starts
+// on a 16-byte boundary of the FP32 array): no staging, a thread per group
+// moves its 4*pf FP32 values with pf 16-byte loads / stores of its own, and
+// E8M23 is a plain 16-byte copy.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -125,6 +132,125 @@ dequantize_kernel(const uint4* __restrict__ in, float* __restrict__ y, GroupGeom
     }
 }
 
+// ---- fast path: cols % 4 == 0 ------------------------------------------------
+// group -> (first element, count) with a 32-bit row division when the group
+// count fits (the usual case), 64-bit otherwise
+__device__ __forceinline__ void group_span_fast(const GroupGeom& G, long long g, long long& flat,
+                                                int& n) {
+    if (G.groups < (1ll << 32)) {
+        const uint32_t r = uint32_t(g) / uint32_t(G.gpr);
+        const int e0 = int(uint32_t(g) - r * uint32_t(G.gpr)) * G.epg;
+        flat = (long long)r * G.cols + e0;
+        n = max(0, min(G.epg, G.cols - e0));
+    } else {
+        group_span(G, g, flat, n);
+    }
+}
+
+// A warp's 32 consecutive groups cover one contiguous, 16-byte aligned span
+// of the FP32 array (rows are contiguous, a partial group ends a row and has a
+// multiple of 4 elements).  The span moves between HBM and a per-warp shared
+// buffer as coalesced 16-byte accesses (lane i takes float4 i, i + 32, ...);
+// a lane reads / writes its group's float4s in the buffer, which inserts one
+// float4 of padding per 8 so that both access patterns are conflict-free.
+constexpr int kAWarps = 8;
+constexpr int kAF4 = 32 * kMaxPf;                      // float4 per span (max: 32 groups x pf)
+__device__ __forceinline__ int pad4(int i) { return i + (i >> 3); }
+
+__global__ void __launch_bounds__(32 * kAWarps)
+dequantize_aligned_kernel(const uint4* __restrict__ in, float4* __restrict__ y, GroupGeom G, Fmt f) {
+    __shared__ float4 stage[kAWarps][kAF4 + kAF4 / 8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4* sm = stage[warp];
+    const long long nw = (long long)gridDim.x * kAWarps;
+    with_pf(f.pf, [&](auto P) {
+        constexpr int PF = decltype(P)::value;
+        for (long long g0 = ((long long)blockIdx.x * kAWarps + warp) * 32; g0 < G.groups; g0 += nw * 32) {
+            long long flat0, flat_last, flat;
+            int n0, nl, n;
+            group_span_fast(G, g0, flat0, n0);
+            const long long glast = min(g0 + 31, G.groups - 1);
+            group_span_fast(G, glast, flat_last, nl);
+            const int span4 = int(flat_last + nl - flat0) >> 2;
+            const long long g = g0 + lane;
+            if (g < G.groups) {
+                group_span_fast(G, g, flat, n);
+                const uint4 q = __ldcs(in + g);
+                float v[4 * PF];
+                if constexpr (PF == 2) {
+                    decode_group_t<2>(q, v, f);
+                } else {
+                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) decode_word_t<PF>(w[k], v + k * PF, f);
+                }
+                const int b4 = int(flat - flat0) >> 2;
+#pragma unroll
+                for (int k = 0; k < PF; ++k)
+                    if (4 * k < n) sm[pad4(b4 + k)] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+            __syncwarp();
+            float4* dst = y + (flat0 >> 2);
+            for (int i = lane; i < span4; i += 32) __stcs(dst + i, sm[pad4(i)]);
+            __syncwarp();
+        }
+    });
+}
+
+// Direct variants (no staging): a thread moves its group's pf float4s with
+// its own 16-byte accesses -- faster for the wide formats (pf <= 3), whose
+// groups are short; quantize's loads go through L1 (each 32-byte sector is
+// read by consecutive lanes' loads).
+__global__ void __launch_bounds__(256)
+quantize_direct_kernel(const float4* __restrict__ x, uint4* __restrict__ out, GroupGeom G, Fmt f) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    with_pf(f.pf, [&](auto P) {
+        constexpr int PF = decltype(P)::value;
+        for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G.groups; g += stride) {
+            long long flat;
+            int n;
+            group_span_fast(G, g, flat, n);
+            const float4* src = x + (flat >> 2);
+            float v[4 * PF];
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const float4 q = (4 * k < n) ? __ldg(src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+            }
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = encode_word_t<PF>(v + k * PF, f);
+            __stcs(out + g, make_uint4(w[0], w[1], w[2], w[3]));
+        }
+    });
+}
+
+__global__ void __launch_bounds__(256)
+dequantize_direct_kernel(const uint4* __restrict__ in, float4* __restrict__ y, GroupGeom G, Fmt f) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    with_pf(f.pf, [&](auto P) {
+        constexpr int PF = decltype(P)::value;
+        for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G.groups; g += stride) {
+            long long flat;
+            int n;
+            group_span_fast(G, g, flat, n);
+            const uint4 q = __ldcs(in + g);
+            float v[4 * PF];
+            if constexpr (PF == 2) {
+                decode_group_t<2>(q, v, f);
+            } else {
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) decode_word_t<PF>(w[k], v + k * PF, f);
+            }
+            float4* dst = y + (flat >> 2);
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                if (4 * k < n) __stcs(dst + k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+        }
+    });
+}
+
 int grid_for(long long groups, int sms) {
     const long long per_cta = 32LL * kWarpsPerCta;
     long long ctas = (groups + per_cta - 1) / per_cta;
@@ -140,6 +266,14 @@ cudaError_t launch_quantize(const Fmt& f, const float* x, size_t rows, size_t co
     GroupGeom G{(long long)rows * (long long)(row_words / 4), int(row_words / 4), int(cols),
                 4 * f.pf};
     if (G.groups == 0) return cudaSuccess;
+    if (cols % 4 == 0) {
+        if (f.kind == KIND_IDENTITY)              // E8M23: the packed rows are the FP32 rows
+            return cudaMemcpyAsync(packed, x, sizeof(float) * rows * cols, cudaMemcpyDeviceToDevice, s);
+        const long long blocks = std::min<long long>((G.groups + 255) / 256, (long long)sms * 16);
+        quantize_direct_kernel<<<(unsigned)std::max(1LL, blocks), 256, 0, s>>>(
+            reinterpret_cast<const float4*>(x), reinterpret_cast<uint4*>(packed), G, f);
+        return cudaGetLastError();
+    }
     quantize_kernel<<<grid_for(G.groups, sms), 32 * kWarpsPerCta, 0, s>>>(
         x, reinterpret_cast<uint4*>(packed), G, f);
     return cudaGetLastError();
@@ -150,6 +284,21 @@ cudaError_t launch_dequantize(const Fmt& f, const uint32_t* packed, size_t rows,
     GroupGeom G{(long long)rows * (long long)(row_words / 4), int(row_words / 4), int(cols),
                 4 * f.pf};
     if (G.groups == 0) return cudaSuccess;
+    if (cols % 4 == 0) {
+        if (f.kind == KIND_IDENTITY)
+            return cudaMemcpyAsync(y, packed, sizeof(float) * rows * cols, cudaMemcpyDeviceToDevice, s);
+        if (f.pf <= 3) {
+            const long long blocks = std::min<long long>((G.groups + 255) / 256, (long long)sms * 16);
+            dequantize_direct_kernel<<<(unsigned)std::max(1LL, blocks), 256, 0, s>>>(
+                reinterpret_cast<const uint4*>(packed), reinterpret_cast<float4*>(y), G, f);
+        } else {
+            const long long blocks = std::min<long long>((G.groups + 32 * kAWarps - 1) / (32 * kAWarps),
+                                                         (long long)sms * 6);
+            dequantize_aligned_kernel<<<(unsigned)std::max(1LL, blocks), 32 * kAWarps, 0, s>>>(
+                reinterpret_cast<const uint4*>(packed), reinterpret_cast<float4*>(y), G, f);
+        }
+        return cudaGetLastError();
+    }
     dequantize_kernel<<<grid_for(G.groups, sms), 32 * kWarpsPerCta, 0, s>>>(
         reinterpret_cast<const uint4*>(packed), y, G, f);
     return cudaGetLastError();
