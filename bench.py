@@ -34,7 +34,6 @@ UNIT = "sphere-evals/s"
 # traj_reduce, aggregate, bk (vapr_cost_grad) + best_per_problem
 LAUNCHES_PER_STEP = 7
 S = 52
-N_GLOBAL_PROBLEMS = 800
 
 
 def parse():
@@ -480,17 +479,20 @@ def main():
 
         def leg(name, fmt_set, storage):
             rr = r if (storage == args.storage and fmt_set == fm) else \
-                Rollout(wl, device=local, formats=fmt_set, sparse=(storage == "sparse"))
+                Rollout(wl, device=local, formats=fmt_set, sparse=(storage == "sparse"),
+                        fused=(storage == "fused"))
             t = timed(step_of(rr), max(3, args.steps // 2), 2)
             bits = sum(1 + e + m for e, m in fmt_set)
             formats[name] = {"ms_per_step": t, "value": poses_total * S / (t * 1e-3),
                              "storage": storage, "bits": bits,
-                             "hbm_frac_step": a_min(fmt_set, swept) * P / (t * 1e-3) / 1e9 / hbm}
+                             # fused (N4): no tensor touches HBM -- q in, grad_q / cost out
+                             "hbm_frac_step": (a_min(fmt_set, swept) if storage != "fused" else 60)
+                             * P / (t * 1e-3) / 1e9 / hbm}
             if rr is not r:
                 del rr
                 torch.cuda.empty_cache()
 
-        for st in ("sparse", "dense"):
+        for st in ("sparse", "dense", "fused"):
             leg(f"fp32_{st}", FORMAT_SETS["fp32"], st)
             leg(f"fp16_{st}", FORMAT_SETS["fp16"], st)
             leg(f"{args.formats}_{st}", fm, st)
@@ -521,7 +523,7 @@ def main():
             "bits": {env: sum(1 + e + m for e, m in FORMAT_SETS[env]) for env in ENVIRONMENTS}}
         del subs
         torch.cuda.empty_cache()
-        for st in ("sparse", "dense"):
+        for st in ("sparse", "dense", "fused"):
             f32 = formats[f"fp32_{st}"]["ms_per_step"]
             for k in list(formats):
                 if k.endswith(st) or (k == "per_env_table2" and st == args.storage):

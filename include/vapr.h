@@ -137,7 +137,7 @@ enum {
     VAPR_OPT_STREAMS = 1,  /* vapr_cost_grad: trajectory chunks on this many context-owned
                               streams (1..8, default 1), forked from and joined back to the
                               caller's stream; results are bit-identical for any value */
-    VAPR_OPT_SPARSE = 2    /* N3: 1 = vapr_cost_grad stores the three gradient tensors
+    VAPR_OPT_SPARSE = 2,   /* N3: 1 = vapr_cost_grad stores the three gradient tensors
                               (closest_pt[_swept], out_vec, grad_out_spheres) in the sparse
                               form (the collision passes write the first two, aggregation
                               reads them and writes the third, BK reads it; the workspace
@@ -145,6 +145,19 @@ enum {
                               vapr_cost_grad_sparse_layout); 0 (default) = dense.  cost and
                               grad_q are bit-identical either way.  Changes the workspace
                               size: query vapr_cost_grad_workspace_bytes after setting it. */
+    VAPR_OPT_FUSED = 3     /* N4: 1 = vapr_cost_grad runs the whole rollout
+                              -- FK, world + self collision, aggregation, BK -- in ONE kernel
+                              (plus the per-trajectory cost sum): every tensor of the five
+                              slots is quantise->dequantised in registers / shared memory
+                              (its format's exact RNE codes, decoded at once: the error a
+                              stored tensor injects, "quantizing the tensors from FP32
+                              to the specified data format and dequantizing them back to
+                              FP32") and never written to HBM.  cost_pose, cost_traj and
+                              grad_q are bit-identical to the materialised path.  The
+                              workspace shrinks to the cost scratch (query
+                              vapr_cost_grad_workspace_bytes after setting it); IKO weights
+                              and VAPR_OPT_SPARSE = 1 are VAPR_ERR_UNSUPPORTED with it.
+                              0 (default) = materialised. */
 };
 
 /* ---- context and tables ------------------------------------------------ */

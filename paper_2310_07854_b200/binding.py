@@ -23,6 +23,7 @@ VAPR_NUM_SLOTS = 5
 VAPR_OPT_CULL = 0
 VAPR_OPT_STREAMS = 1
 VAPR_OPT_SPARSE = 2
+VAPR_OPT_FUSED = 3
 STATUS = {0: "VAPR_OK", 1: "VAPR_ERR_INVALID_FORMAT", 2: "VAPR_ERR_INVALID_ARG",
           3: "VAPR_ERR_SHAPE", 4: "VAPR_ERR_CUDA", 5: "VAPR_ERR_NOT_INITIALIZED",
           6: "VAPR_ERR_UNSUPPORTED"}

@@ -38,6 +38,8 @@ struct vapr_ctx {
     cudaStream_t par[8] = {};
     // N3: grad_out_spheres in the sparse form (VAPR_OPT_SPARSE)
     int sparse = 0;
+    // N4: the fused on-chip rollout (VAPR_OPT_FUSED)
+    int fused = 0;
     // stage timing hook (vapr_set_stage_events): caller-owned events recorded
     // between the launches of vapr_cost_grad
     cudaEvent_t stage_ev[6] = {};
@@ -134,6 +136,26 @@ Fmt make_fmt(vapr_format v) {
         f.maxcode = (f.E == 5) ? 0x7C00u : 0x7F80u;   // the encode clamp: overflow -> inf
         f.nancode = 0x7FFFu;                          // the hardware conversions' canonical NaN
     }
+    // fake_quant constants (N4): the values decode() gives for the largest
+    // finite code and for nancode, by the same bit recipe as decode_slot
+    f.fq_rnd = rnd;
+    f.fq_keep = ~((f.sh > 0 ? (1u << f.sh) : 1u) - 1u);
+    auto dec_bits = [&](uint32_t code) {
+        if (f.E == 8 && f.M == 23) return code;
+        const uint32_t u = code << (32 - f.t);
+        const uint32_t x = uint32_t(int32_t(u) >> (8 - f.E)) & f.keep;
+        if (f.E == 8) return x;
+        float fx, r;
+        std::memcpy(&fx, &x, 4);
+        r = fx * f.dscale;
+        uint32_t b;
+        std::memcpy(&b, &r, 4);
+        return b;
+    };
+    const uint32_t maxfin_code = ieee ? f.maxcode - 1u : f.maxcode;
+    f.fq_maxfin = dec_bits(maxfin_code);
+    f.fq_sat = ieee ? 0x7F800000u : f.fq_maxfin;
+    f.fq_nan = (ieee && f.E == 5) ? (0x7F800000u | (0x3FFu << 13)) : dec_bits(f.nancode);
     return f;
 }
 
@@ -519,6 +541,11 @@ vapr_status vapr_set_option(vapr_ctx* c, int32_t option, int32_t value) {
         c->sparse = value;
         return VAPR_OK;
     }
+    if (option == VAPR_OPT_FUSED) {
+        CHECK(value == 0 || value == 1, VAPR_ERR_INVALID_ARG);
+        c->fused = value;
+        return VAPR_OK;
+    }
     return VAPR_ERR_UNSUPPORTED;
 }
 
@@ -738,7 +765,11 @@ static void ws_layout(const vapr_ctx* c, long long P, int swept, size_t off[VAPR
     off[VAPR_OUT_SPHERES] = o;
     o = align256(o + packed_bytes(c->dfmt[VAPR_OUT_SPHERES], cols, P));
     const int cps = swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
-    if (c->sparse) {
+    if (c->fused) {
+        // N4: no tensor is materialised -- only the cost scratch below
+        off[VAPR_OUT_SPHERES] = SIZE_MAX;
+        o = 0;
+    } else if (c->sparse) {
         // N3: the three gradient tensors in the sparse form -- per row a
         // sphere bitmap and the non-zero codes packed at pool + row * wmax
         // (closest_pt[_swept], out_vec) or at the row's own offset
@@ -824,6 +855,44 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     const int cps = p->swept ? VAPR_CLOSEST_PT_SWEPT : VAPR_CLOSEST_PT;
     const long long p0 = (long long)b0 * H, P = (long long)nb * H;
     const int cols = c->robot.cols;
+    if (c->fused) {
+        const float* qc = q + p0 * kJoints;
+        auto mark = [&](int i) {
+            if (c->n_stage_ev == 6) cudaEventRecord(c->stage_ev[i], s);
+        };
+        // N4: one kernel for FK, both collision parts, aggregation and BK
+        // (the FK / aggregation / BK events are recorded back to back)
+        CollisionArgs a{};
+        a.world_idx = world_idx + b0;
+        a.B = nb;
+        a.H = H;
+        a.do_world = 1;
+        a.do_self = 1;
+        a.swept = p->swept ? 1 : 0;
+        a.sweep_steps = p->sweep_steps;
+        a.eta_w = p->eta_world;
+        a.w_w = p->w_world;
+        a.eta_s = p->eta_self;
+        a.w_s = p->w_self;
+        a.cull = c->cull;
+        a.cost = cpose + p0;
+        a.fused = 1;
+        a.q = qc;
+        a.grad_q = grad_q + p0 * kJoints;
+        a.fgos = c->dfmt[VAPR_GRAD_OUT_SPHERES];
+        mark(0);
+        mark(1);
+        cudaError_t e = launch_collision(c->robot, worlds_of(c), c->dfmt[VAPR_OUT_SPHERES],
+                                         c->dfmt[cps], c->dfmt[VAPR_OUT_VEC], a, c->d_sched,
+                                         &c->sched_next, s);
+        mark(2);
+        if (e == cudaSuccess)
+            e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, nullptr);
+        mark(3);
+        mark(4);
+        mark(5);
+        return e;
+    }
     auto rows_of = [&](int slot) {
         return reinterpret_cast<uint32_t*>(ws + off[slot]) + p0 * row_words_of(c->dfmt[slot], cols);
     };
@@ -854,6 +923,10 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         spi.pool = spo.pool;
     }
     const float* qc = q + p0 * kJoints;
+    // stage timing hook: event i after stage i (0: before FK)
+    auto mark = [&](int i) {
+        if (c->n_stage_ev == 6) cudaEventRecord(c->stage_ev[i], s);
+    };
     // IKO terms (N2): FK writes cost_pose = pose + bound, the collision passes add
     IkArgs ik{};
     ik.goals = c->d_goals;
@@ -865,10 +938,6 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     ik.w_bound = p->w_bound;
     ik.cost = cpose + p0;
     const bool iko = ik_on(ik);
-    // stage timing hook: event i after stage i (0: before FK)
-    auto mark = [&](int i) {
-        if (c->n_stage_ev == 6) cudaEventRecord(c->stage_ev[i], s);
-    };
     mark(0);
     cudaError_t e = launch_fk(c->robot, c->dfmt[VAPR_OUT_SPHERES], qc, P, os, s, iko ? &ik : nullptr);
     mark(1);
@@ -944,6 +1013,10 @@ vapr_status vapr_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_idx
               std::isfinite(p->w_bound),
           VAPR_ERR_INVALID_ARG);
     CHECK((p->w_pose_pos == 0.f && p->w_pose_rot == 0.f) || c->goals_set, VAPR_ERR_NOT_INITIALIZED);
+    // N4 fused: the TO cost only, dense (no IKO terms, no sparse tensors)
+    CHECK(!c->fused || (!c->sparse && p->w_pose_pos == 0.f && p->w_pose_rot == 0.f &&
+                        p->w_bound == 0.f),
+          VAPR_ERR_UNSUPPORTED);
     const long long P = (long long)B * H;
     size_t off[VAPR_NUM_SLOTS], co, total;
     ws_layout(c, P, p->swept, off, &co, &total);
@@ -1013,6 +1086,10 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
               std::isfinite(p->w_bound),
           VAPR_ERR_INVALID_ARG);
     CHECK((p->w_pose_pos == 0.f && p->w_pose_rot == 0.f) || c->goals_set, VAPR_ERR_NOT_INITIALIZED);
+    // N4 fused: the TO cost only, dense (no IKO terms, no sparse tensors)
+    CHECK(!c->fused || (!c->sparse && p->w_pose_pos == 0.f && p->w_pose_rot == 0.f &&
+                        p->w_bound == 0.f),
+          VAPR_ERR_UNSUPPORTED);
     const long long P = (long long)B * H;
     size_t off[VAPR_NUM_SLOTS], co, total;
     ws_layout(c, P, p->swept, off, &co, &total);

@@ -279,13 +279,13 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, slink, lrec, lgp, tables;
+    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, slink, lrec, lgp, so, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
-    unsigned rows, pmask, pwm, wm, pk0, qi, qc, warp;
+    unsigned rows, pmask, pwm, wm, pk0, qi, qc, gfw, gt, warp;
 };
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
-             int do_self, int sparse) {
+             int do_self, int sparse, int fused = 0) {
     Geo g{};
     g.Wos = row_words_of(fos, R.cols);
     g.Wcp = do_world ? row_words_of(fcp, R.cols) : 0;
@@ -328,6 +328,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.slink = take(kMaxSpheres, 1);
     g.lrec = take(8u * 32, 8);
     g.lgp = take(33, 1);
+    g.so = take(fused ? 16u * kMaxSpheres : 0u, 16);      // N4: sphere offsets (BK)
     g.tables = take(0, 16);
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
@@ -337,6 +338,9 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.pk0 = take(do_world ? 4u * kTP : 0u, 4);
     g.qi = take(2u * kQ, 2);
     g.qc = take((sparse == 2 ? 16u : sparse == 1 ? 8u : 4u) * kQ, 16);   // item results: codes + cost / cost
+    // N4: each pose's world-live spheres, and the FP32 grad_out_spheres tile
+    g.gfw = take(fused ? 8u * kTP : 0u, 8);
+    g.gt = take(fused ? 4u * kTP * R.cols : 0u, 16);
     g.warp = take(0, 16);
     return g;
 }
@@ -405,6 +409,88 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
     return sum;
 }
 
+// N4: quantise -> dequantise in registers (the error a stored tensor of format
+// f would inject; exact RNE encode, exact decode -- the same value the
+// materialised path reads back from HBM)
+// -- computed on the FP32 bits without forming the code: the normal range
+// rounds the dropped mantissa bits RNE in place (a carry into the exponent is
+// the binade change), the format's subnormal range rounds in the FP32 adder
+// (|x| + 2^(24-bias-M) has the subnormal quantum as its ulp; subtracting it
+// back is exact), an overflow saturates (or is inf in IEEE mode), NaN gives
+// decode(nancode), the sign is kept -- value for value decode(encode(x)),
+// checked against it by tests/test_gpu_fused.py through the materialised path.
+__device__ __forceinline__ float fake_quant(float x, const Fmt& f) {
+    if (f.kind == KIND_IDENTITY) return x;
+    const uint32_t u = __float_as_uint(x), a = u & 0x7fffffffu;
+    uint32_t r = (a + f.fq_rnd + ((a >> f.sh) & f.lsb)) & f.fq_keep;
+    const float mg = __uint_as_float(f.magic_bits);
+    const float sv = __fsub_rn(__fadd_rn(__uint_as_float(a), mg), mg);
+    r = (a < f.minnorm) ? __float_as_uint(sv) : r;
+    r = (r > f.fq_maxfin) ? f.fq_sat : r;
+    r |= u & 0x80000000u;
+    return __uint_as_float(a > 0x7f800000u ? f.fq_nan : r);
+}
+
+// N4: backward kinematics of one pose inside the fused kernel -- bk.cu's chain
+// (the same operations in the same order, so grad_q matches the materialised
+// path bit for bit): g(s, c) returns sphere s's dequantised grad_out_spheres
+// component c; spheres outside `mask` or with three zero codes are skipped
+// (bk.cu's zero skip).
+template <typename Gf>
+__device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsigned long long mask,
+                                        const float4* so, Gf&& gfun, float* gq) {
+#pragma unroll
+    for (int j = 0; j < kJoints; ++j) gq[j] = 0.f;
+    float zx[kJoints], zy[kJoints], zz[kJoints], ox[kJoints], oy[kJoints], oz[kJoints];
+    Xf X;
+    xf_identity(X);
+#pragma unroll
+    for (int l = 1; l < kLinks; ++l) {
+        if (l <= kJoints) {
+            fk_step(X, R, l - 1, qp[l - 1]);
+            zx[l - 1] = X.r[2];
+            zy[l - 1] = X.r[5];
+            zz[l - 1] = X.r[8];
+            ox[l - 1] = X.p[0];
+            oy[l - 1] = X.p[1];
+            oz[l - 1] = X.p[2];
+        } else {
+            fk_hand(X, R);
+        }
+        const int s0 = R.link_start[l], s1 = R.link_start[l + 1];
+        unsigned long long lm = (mask >> s0) & ((s1 - s0 >= 64) ? ~0ull : ((1ull << (s1 - s0)) - 1ull));
+        if (!lm) continue;
+        float Fx = 0.f, Fy = 0.f, Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f;
+        bool any = false;
+        while (lm) {
+            const int s = s0 + __ffsll((long long)lm) - 1;
+            lm &= lm - 1;
+            float g[3];
+            if (!gfun(s, g)) continue;
+            any = true;
+            float cx, cy, cz;
+            const float4 o4 = so[s];
+            xf_apply(X, o4.x, o4.y, o4.z, cx, cy, cz);
+            Fx += g[0];
+            Fy += g[1];
+            Fz += g[2];
+            Mx += cy * g[2] - cz * g[1];
+            My += cz * g[0] - cx * g[2];
+            Mz += cx * g[1] - cy * g[0];
+        }
+        if (!any) continue;
+#pragma unroll
+        for (int j = 0; j < kJoints; ++j) {
+            if (j < l) {
+                const float tx = Mx - (oy[j] * Fz - oz[j] * Fy);
+                const float ty = My - (oz[j] * Fx - ox[j] * Fz);
+                const float tz = Mz - (ox[j] * Fy - oy[j] * Fx);
+                gq[j] += zx[j] * tx + zy[j] * ty + zz[j] * tz;
+            }
+        }
+    }
+}
+
 // One warp processes a tile of kTP consecutive poses, one pose per lane (the
 // arithmetic of every broadphase test runs for 32 poses per instruction, with
 // uniform loops and no index math); the sparse narrowphase work (live world
@@ -416,7 +502,9 @@ __device__ __forceinline__ float warp_queue(unsigned long long lo, unsigned long
 // the dense one carries no extra code (the kernel is instruction-cache
 // sensitive); SP_WIDE: the item results hold one code per word (formats of
 // more than 10 bits) rather than all three in one word.
-template <bool SPARSE, bool SP_WIDE>
+// FUSED (N4, VAPR_OPT_FUSED): FK in the tile fill, the gradients summed in a
+// shared FP32 tile, BK per pose at the tile's end (CollisionArgs::fused).
+template <bool SPARSE, bool SP_WIDE, bool FUSED>
 __global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
@@ -437,6 +525,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     uint8_t* slink = reinterpret_cast<uint8_t*>(base + G.slink);
     uint2* slrec = reinterpret_cast<uint2*>(base + G.lrec);        // link-pair ball tests
     uint8_t* slgp = reinterpret_cast<uint8_t*>(base + G.lgp);      // group pairs of link pair lp
+    float4* sso = reinterpret_cast<float4*>(base + G.so);          // N4: sphere offsets
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
@@ -448,6 +537,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         int l = 0;
         while (l < kLinks - 1 && i >= R.link_start[l + 1]) ++l;
         slink[i] = (uint8_t)l;
+        if (FUSED) sso[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
     }
     if (tid < kLinks) {
         srl[tid] = R.link_rl[tid];
@@ -499,6 +589,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     using QcT = typename std::conditional<SPARSE, typename std::conditional<SP_WIDE, float4, float2>::type,
                                           float>::type;
     QcT* qc = reinterpret_cast<QcT*>(wb + G.qc);
+    unsigned long long* gfw = reinterpret_cast<unsigned long long*>(wb + G.gfw);   // N4
+    float* gt = reinterpret_cast<float*>(wb + G.gt);                               // N4 [kTP][cols]
 
     const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
@@ -555,7 +647,36 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
         // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
         float amax = 0.f;
-        {
+        if constexpr (FUSED) {
+            // N4: the tile rows from FK, one lane per row (<= kTR of the 32),
+            // every coordinate quantise->dequantised with the out_spheres
+            // format (fk.cu's chain and its exact RNE codes)
+            const int nr = int(r_hi - r_lo);
+            if (lane < nr) {
+                const float* qr = a.q + (r_lo + lane) * kJoints;
+                float qv[kJoints];
+#pragma unroll
+                for (int j = 0; j < kJoints; ++j) qv[j] = __ldg(qr + j);
+                float* d = rows + (row_off + lane) * cs;
+                Xf X;
+                xf_identity(X);
+                for (int l = 0; l < kLinks; ++l) {
+                    if (l >= 1 && l <= kJoints) fk_step(X, R, l - 1, qv[l - 1]);
+                    if (l == kLinks - 1) fk_hand(X, R);
+                    for (int s = R.link_start[l]; s < R.link_start[l + 1]; ++s) {
+                        float cx, cy, cz;
+                        xf_apply(X, sso[s].x, sso[s].y, sso[s].z, cx, cy, cz);
+                        cx = fake_quant(cx, fos);
+                        cy = fake_quant(cy, fos);
+                        cz = fake_quant(cz, fos);
+                        d[3 * s] = cx;
+                        d[3 * s + 1] = cy;
+                        d[3 * s + 2] = cz;
+                        amax = fmaxf(amax, fmaxf(fabsf(cx), fmaxf(fabsf(cy), fabsf(cz))));
+                    }
+                }
+            }
+        } else {
             const int nq = int(r_hi - r_lo) * G.Qos;
             const uint4* src = os4 + r_lo * G.Qos;
             float* dst0 = rows + row_off * cs;
@@ -608,13 +729,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ORed in with atomics (__syncwarp orders the fill before every lane's
         // atomics); sparse: each pose's owner lane appends its codes to the
         // pose's pool segment and writes its bitmap
-        uint32_t* const cpg = (!SPARSE && a.do_world) ? a.cp + p0 * G.Wcp : nullptr;
-        uint32_t* const ovg = (!SPARSE && a.do_self) ? a.ov + p0 * G.Wov : nullptr;
-        if (!SPARSE && a.do_world)
+        uint32_t* const cpg = (!SPARSE && !FUSED && a.do_world) ? a.cp + p0 * G.Wcp : nullptr;
+        uint32_t* const ovg = (!SPARSE && !FUSED && a.do_self) ? a.ov + p0 * G.Wov : nullptr;
+        if (!SPARSE && !FUSED && a.do_world)
             for (int i = lane; i < np * G.Wcp / 4; i += 32)
                 reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
         if (a.do_self) {
-            if (!SPARSE)
+            if (!SPARSE && !FUSED)
                 for (int i = lane; i < np * G.Wov / 4; i += 32)
                     reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
@@ -779,7 +900,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp, acc.gx + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 1, acc.gy + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 2, acc.gz + 0.f);
-                if constexpr (SPARSE) {
+                if constexpr (FUSED) {
+                    float* gr = gt + p * R.cols + 3 * sp;
+                    gr[0] = fake_quant(acc.gx + 0.f, fcp);
+                    gr[1] = fake_quant(acc.gy + 0.f, fcp);
+                    gr[2] = fake_quant(acc.gz + 0.f, fcp);
+                    return acc.cost;
+                } else if constexpr (SPARSE) {
                     return SparseRow::codes<QcT>(acc.gx, acc.gy, acc.gz, acc.cost, fcp);
                 } else {
                     or_code3(orow, 3 * sp, acc.gx + 0.f, acc.gy + 0.f, acc.gz + 0.f, fcp, G.rc_cp);
@@ -789,6 +916,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 if constexpr (SPARSE) sr_cp.put(it & 63, r, fcp);
             });
             if (SPARSE && owner) sr_cp.finish(a.cp_mask + p0 + pl);
+            if (FUSED && half == 0 && pl < kTP) gfw[pl] = smask;
         }
 
         // ---- 3. self
@@ -966,7 +1094,18 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 1, gy + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 2, gz + 0.f);
-                if constexpr (SPARSE) {
+                if constexpr (FUSED) {
+                    // aggregation on chip: closest_pt + out_vec (world first;
+                    // 0 + v where the sphere had no world item)
+                    float* gr = gt + p * R.cols + 3 * s;
+                    const bool wl = (gfw[p] >> s) & 1ull;
+                    const float vx = fake_quant(gx + 0.f, fov), vy = fake_quant(gy + 0.f, fov),
+                                vz = fake_quant(gz + 0.f, fov);
+                    gr[0] = wl ? gr[0] + vx : vx;
+                    gr[1] = wl ? gr[1] + vy : vy;
+                    gr[2] = wl ? gr[2] + vz : vz;
+                    return c_lead;
+                } else if constexpr (SPARSE) {
                     return SparseRow::codes<QcT>(gx, gy, gz, c_lead, fov);
                 } else {
                     or_code3(orow, 3 * s, gx + 0.f, gy + 0.f, gz + 0.f, fov, G.rc_ov);
@@ -976,6 +1115,28 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 if constexpr (SPARSE) sr_ov.put(it & 63, r, fov);
             });
             if (SPARSE && owner) sr_ov.finish(a.ov_mask + p0 + pl);
+            if constexpr (FUSED) {
+                // ---- 4. N4: backward kinematics of the owned poses, from the
+                // on-chip grad_out_spheres (quantise->dequantised with fgos)
+                if (owner) {
+                    float qv[kJoints], gq[kJoints];
+                    const float* qr = a.q + (p0 + pl) * kJoints;
+#pragma unroll
+                    for (int j = 0; j < kJoints; ++j) qv[j] = __ldg(qr + j);
+                    const float* gr = gt + pl * R.cols;
+                    const unsigned long long m = gfw[pl] | tb;
+                    bk_pose(R, qv, m, sso, [&](int s, float* g) -> bool {
+                        // a zero code <=> a +0 value (-0 has the sign bit)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) g[c] = fake_quant(gr[3 * s + c], a.fgos);
+                        return (__float_as_uint(g[0]) | __float_as_uint(g[1]) |
+                                __float_as_uint(g[2])) != 0u;
+                    }, gq);
+                    float* go = a.grad_q + (p0 + pl) * kJoints;
+#pragma unroll
+                    for (int j = 0; j < kJoints; ++j) go[j] = gq[j];
+                }
+            }
         }
         if (owner) VAPR_STAT(7, 1);
         if (owner) {
@@ -1060,7 +1221,10 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const long long P = (long long)a.B * a.H;
     const bool sparse = a.cp_mask || a.ov_mask;
     const bool wide = (a.do_world && fcp.t > 10) || (a.do_self && fov.t > 10);
-    const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0);
+    const bool fused = a.fused != 0;
+    if (fused && (sparse || !a.do_world || !a.do_self)) return cudaErrorInvalidValue;
+    const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0,
+                           fused ? 1 : 0);
     if (G.rc_q == 0) return cudaErrorInvalidValue;
     int dev = 0, sms = 148, optin = 0;
     cudaGetDevice(&dev);
@@ -1072,8 +1236,9 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     nw = std::min(nw, VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
-    auto kern = !sparse ? collision_kernel<false, false>
-                        : (wide ? collision_kernel<true, true> : collision_kernel<true, false>);
+    auto kern = fused ? collision_kernel<false, false, true>
+                : !sparse ? collision_kernel<false, false, false>
+                          : (wide ? collision_kernel<true, true, false> : collision_kernel<true, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
@@ -1137,7 +1302,7 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
     auto zero_self = [&]() -> cudaError_t {
         return a.self_cost ? cudaMemsetAsync(a.self_cost, 0, sizeof(float) * (size_t)P, s) : cudaSuccess;
     };
-    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self)) {
+    if (!(VAPR_FUSED_SPLIT && a.do_world && a.do_self) || a.fused) {
         a.sched = slot();
         const cudaError_t e = launch_collision_pass(R, W, fos, fcp, fov, a, s);
         return e == cudaSuccess ? zero_self() : e;

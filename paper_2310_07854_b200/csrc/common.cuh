@@ -59,6 +59,12 @@ struct Fmt {
     uint32_t nancode;      // encode of NaN: maxcode (c8) / 0x7FFF (IEEE)
     uint32_t lsb;          // RNE tie bit mask: 1 when sh > 0; 0 for M = 23 (nothing is
                            // dropped, so nothing rounds: code = a - off exactly)
+    // fake_quant (N4): decode(encode(x)) straight on the FP32 bit pattern
+    uint32_t fq_rnd;       // (1 << (sh-1)) - 1: the RNE half-ulp constant (0 for sh = 0)
+    uint32_t fq_keep;      // ~((1 << sh) - 1): the kept mantissa bits
+    uint32_t fq_maxfin;    // FP32 bits of the largest finite value of the format
+    uint32_t fq_sat;       // bits of an overflow's result: fq_maxfin (c7) / inf (IEEE)
+    uint32_t fq_nan;       // bits of decode(nancode)
 };
 
 // FP32 -> code, round to nearest even (single rounding), saturating, NaN ->

@@ -37,6 +37,15 @@ struct CollisionArgs {
     // traj_reduce adds it, so the self pass may overlap the world pass's tail
     // (programmatic dependent launch); the order of the sums is unchanged
     float* self_cost;
+    // N4 fused rollout (VAPR_OPT_FUSED; fused = 1, world and self in one
+    // pass): the tile rows come from FK of q in the kernel (os unused), each
+    // out_spheres coordinate quantise->dequantised in registers; the world /
+    // self gradients likewise (cp / ov unused), summed on chip, quantised with
+    // fgos and folded by BK into grad_q -- no tensor makes an HBM round trip
+    int32_t fused;
+    const float* q;           // [B*H, 7]
+    float* grad_q;            // [B*H, 7]
+    Fmt fgos;
     int32_t pdl;              // internal: 1 = trigger dependents at start, 2 = wait at exit
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
     unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero

@@ -44,6 +44,10 @@ class Context:
         """N3: grad_out_spheres in the sparse form inside vapr_cost_grad."""
         vb.vapr_set_option(self.h, vb.VAPR_OPT_SPARSE, int(on))
 
+    def set_fused(self, on):
+        """N4: the whole rollout in one kernel, no tensor materialised."""
+        vb.vapr_set_option(self.h, vb.VAPR_OPT_FUSED, int(on))
+
     def close(self):
         if self.h is not None:
             vb.vapr_destroy(self.h)
@@ -59,7 +63,7 @@ class Context:
 class Rollout:
     """One batch [B, H] of trajectories resident in HBM."""
 
-    def __init__(self, workload, device=0, formats=None, ctx=None, sparse=False):
+    def __init__(self, workload, device=0, formats=None, ctx=None, sparse=False, fused=False):
         self.wl = workload
         self.device = torch.device("cuda", device)
         self.ctx = ctx or Context(device, workload.robot, formats or workload.formats,
@@ -70,6 +74,9 @@ class Rollout:
         self.sparse = bool(sparse)
         if sparse:
             self.ctx.set_sparse(True)
+        self.fused = bool(fused)
+        if fused:
+            self.ctx.set_fused(True)
         self.B, self.H = workload.B, workload.H
         self.params = dict(workload.params)
         self._p = vb.cost_params(self.params)
