@@ -35,6 +35,9 @@ constexpr int kRows = VAPR_AGG_ROWS;
 #define VAPR_AGG_THREADS 128
 #endif
 constexpr int kThreads = VAPR_AGG_THREADS;
+#ifndef VAPR_AGG_ROWS_BELOW       // vapr_cost_grad sparse aggregation: warp-per-row form below
+#define VAPR_AGG_ROWS_BELOW 65536
+#endif
 
 // Decode the packed tile `src` (rows of W words, pf values per word) into the
 // FP32 tile x (stride xs): x = value (ADD = false) or x += value (ADD = true).
@@ -76,6 +79,8 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
                  const uint32_t* __restrict__ cp, const uint32_t* __restrict__ ov,
                  long long rows, uint32_t* __restrict__ gos, uint32_t rw_c, uint32_t rw_o,
                  uint32_t rw_g, int xs, const SparseOut sp) {
+    pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
+    pdl_trigger();
     extern __shared__ uint4 smem_a[];
     uint32_t* sc = reinterpret_cast<uint32_t*>(smem_a);     // [kRows * Wc]
     uint32_t* so = sc + kRows * Wc;                         // [kRows * Wo]
@@ -156,6 +161,8 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
                         const uint32_t* __restrict__ cp, const unsigned long long* __restrict__ cpm,
                         const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
                         long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
+    pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
+    pdl_trigger();
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nw = 0u;
     if (p < rows) {
@@ -213,27 +220,83 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
     if ((threadIdx.x & 31) == 0 && nw) atomicAdd(sp.used, nw);
 }
 
+// The same sums, a warp per row and a lane per sphere (emit_sparse_rows):
+// every code load of a row is in flight at once -- the latency form for
+// small batches, where the thread-per-row kernel's serial sphere loop (a
+// dependent global load per sphere) is the critical path.  Bit-identical
+// (the same a + b and encode3); pool layout: the tile segments of
+// emit_sparse_rows (readers go through off[]).
+constexpr int kSmRows = 16, kSmWarps = 4;
+__global__ void __launch_bounds__(32 * kSmWarps)
+aggregate_sparse_rows_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int wc, int wo,
+                             const uint32_t* __restrict__ cp, const unsigned long long* __restrict__ cpm,
+                             const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
+                             long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
+    pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
+    pdl_trigger();
+    __shared__ SparseTileSmem<kSmRows> sm;
+    __shared__ uint32_t wbuf[kSmWarps * 3 * 64];
+    __shared__ unsigned long long smc[kSmRows], smo[kSmRows];
+    const long long r0 = (long long)blockIdx.x * kSmRows;
+    const int nr = (int)min((long long)kSmRows, rows - r0);
+    if ((int)threadIdx.x < nr) {
+        smc[threadIdx.x] = __ldcs(cpm + r0 + threadIdx.x);
+        smo[threadIdx.x] = __ldcs(ovm + r0 + threadIdx.x);
+    }
+    __syncthreads();
+    const uint32_t seg = sp.seg0 + (uint32_t)r0 * sp.wmax;
+    emit_sparse_rows<kSmRows, kSmWarps>(
+        nr, cols / 3, fg, sp.rcp, sm, wbuf, 3 * 64, r0, seg, sp.mask + 0, sp.off + 0, sp.pool,
+        sp.used, [&](int r, int s, uint32_t* c) {
+            const unsigned long long mc = smc[r], mo = smo[r], bit = 1ull << s;
+            if (!((mc | mo) & bit)) return;
+            const long long p = r0 + r;
+            float x[3];
+            const int kc = 3 * __popcll(mc & (bit - 1ull)), ko = 3 * __popcll(mo & (bit - 1ull));
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                float a = 0.f, b = 0.f;
+                if (mc & bit) {
+                    const uint32_t e = kc + q, w = (e * rcp_c) >> 16;
+                    a = decode_sp(code_at(__ldcs(cp + p * wc + w), int(e - w * fcp.pf), fcp), fcp);
+                }
+                if (mo & bit) {
+                    const uint32_t e = ko + q, w = (e * rcp_o) >> 16;
+                    b = decode_sp(code_at(__ldcs(ov + p * wo + w), int(e - w * fov.pf), fov), fov);
+                }
+                x[q] = a + b;
+            }
+            encode3(x[0], x[1], x[2], fg, c);
+        });
+}
+
 }  // namespace
 
 cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                                     const uint32_t* cp_pool, const unsigned long long* cpm,
                                     const uint32_t* ov_pool, const unsigned long long* ovm,
-                                    long long rows, const SparseOut& sparse, cudaStream_t s) {
+                                    long long rows, const SparseOut& sparse, cudaStream_t s,
+                                    bool pdl) {
     if (rows <= 0) return cudaSuccess;
     SparseOut spo = sparse;
     spo.wmax = (uint32_t)((cols + fgos.pf - 1) / fgos.pf);
     spo.rcp = 65536u / fgos.pf + 1u;
     const int wc = (cols + fcp.pf - 1) / fcp.pf, wo = (cols + fov.pf - 1) / fov.pf;
+    if (rows < VAPR_AGG_ROWS_BELOW) {       // small batch: latency form
+        const long long g = (rows + kSmRows - 1) / kSmRows;
+        return launch_k(aggregate_sparse_rows_kernel, dim3((unsigned)g), dim3(32 * kSmWarps), 0, s,
+                        pdl, fcp, fov, fgos, cols, wc, wo, cp_pool, cpm, ov_pool, ovm, rows,
+                        65536u / fcp.pf + 1u, 65536u / fov.pf + 1u, spo);
+    }
     const long long grid = (rows + 127) / 128;
-    aggregate_sparse_kernel<<<(unsigned)grid, 128, 0, s>>>(fcp, fov, fgos, wc, wo, cp_pool, cpm,
-                                                           ov_pool, ovm, rows, 65536u / fcp.pf + 1u,
-                                                           65536u / fov.pf + 1u, spo);
-    return cudaGetLastError();
+    return launch_k(aggregate_sparse_kernel, dim3((unsigned)grid), dim3(128), 0, s, pdl, fcp, fov,
+                    fgos, wc, wo, cp_pool, cpm, ov_pool, ovm, rows, 65536u / fcp.pf + 1u,
+                    65536u / fov.pf + 1u, spo);
 }
 
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
-                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse) {
+                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse, bool pdl) {
     if (rows <= 0) return cudaSuccess;
     const int Wc = row_words_of(fcp, cols), Wo = row_words_of(fov, cols),
               Wg = row_words_of(fgos, cols);
@@ -263,8 +326,9 @@ cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, in
 #ifdef VAPR_DEBUG_TAP
     const bool tapped = tap_arm(1, rows, cols, s) != nullptr;
 #endif
-    kern<<<(unsigned)grid, kThreads, smem, s>>>(fcp, fov, fgos, cols, Wc, Wo, Wg, cp, ov, rows, gos,
-                                                rw_c, rw_o, rw_g, xs, spo);
+    e = launch_k(kern, dim3((unsigned)grid), dim3(kThreads), smem, s, pdl, fcp, fov, fgos, cols, Wc,
+                 Wo, Wg, cp, ov, rows, gos, rw_c, rw_o, rw_g, xs, spo);
+    if (e != cudaSuccess) return e;
 #ifdef VAPR_DEBUG_TAP
     if (tapped) tap_disarm(1, s);
 #endif

@@ -50,6 +50,9 @@ struct vapr_ctx {
     bool goals_set = false;
 };
 
+#ifndef VAPR_CHAIN_PDL             // vapr_cost_grad: chain its kernels by programmatic dependent launch
+#define VAPR_CHAIN_PDL 1
+#endif
 #ifndef VAPR_END_CHUNK_WEIGHT      // vapr_cost_grad_host: first / last chunk size relative to the others
 #define VAPR_END_CHUNK_WEIGHT 0.25
 #endif
@@ -972,20 +975,26 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
                              c->dfmt[VAPR_OUT_VEC], a, c->d_sched, &c->sched_next, s);
     }
     mark(2);
-    // combines the self pass's cost into cost_pose (always) and sums cost_traj
+    // combines the self pass's cost into cost_pose (always) and sums cost_traj;
+    // the rest of the chain as programmatic dependent launches (each kernel
+    // waits for its predecessor at its start; measured runs with stage
+    // events are plain launches)
+    const bool pdl = VAPR_CHAIN_PDL && c->n_stage_ev == 0;
     if (e == cudaSuccess)
-        e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost);
+        e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost,
+                               pdl);
     mark(3);
     if (e == cudaSuccess)
         e = c->sparse ? launch_aggregate_sparse(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
-                                                ov, ov_mask, P, spo, s)
+                                                ov, ov_mask, P, spo, s, pdl)
                       : launch_aggregate(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
-                                         c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, ov, P, gos, s);
+                                         c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, ov, P, gos, s,
+                                         nullptr, pdl);
     mark(4);
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
-                      iko ? &ik : nullptr, c->sparse ? &spi : nullptr);
+                      iko ? &ik : nullptr, c->sparse ? &spi : nullptr, pdl);
     mark(5);
     return e;
 }

@@ -56,6 +56,8 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     __shared__ unsigned long long s_mask[kTile];
     __shared__ int s_act[kTile];
     __shared__ int s_nact;
+    pdl_wait();         // vapr_cost_grad: the aggregation's output is complete
+    pdl_trigger();
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;
@@ -230,7 +232,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s, const IkArgs* ik,
-                      const SparseIn* sparse) {
+                      const SparseIn* sparse, bool pdl) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
     const size_t smem = sizeof(float4) * kMaxSpheres +
@@ -261,9 +263,8 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     if (e != cudaSuccess) return e;
     IkArgs none{};
     const SparseIn dense{};
-    kern<<<(unsigned)grid, kTile, smem, s>>>(R, fgos, q, P, W, gos, grad_q, rc, rq, f_lo, f_hi, rt,
-                                             iko ? *ik : none, sparse ? *sparse : dense);
-    return cudaGetLastError();
+    return launch_k(kern, dim3((unsigned)grid), dim3(kTile), smem, s, pdl, R, fgos, q, P, W, gos,
+                    grad_q, rc, rq, f_lo, f_hi, rt, iko ? *ik : none, sparse ? *sparse : dense);
 }
 
 }  // namespace vapr

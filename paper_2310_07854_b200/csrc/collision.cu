@@ -39,6 +39,7 @@
 // without culling, so VAPR_OPT_CULL on and off give bit-identical results
 // (tests/test_gpu_parity.py::test_cull_is_exact).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -248,6 +249,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #endif
 #ifndef VAPR_MAX_WARPS          // cap on warps per (persistent, one per SM) CTA
 #define VAPR_MAX_WARPS 16
+#endif
+#ifndef VAPR_SMALL_WARPS          // small batches: tiles (of fewer poses) per SM to aim for
+#define VAPR_SMALL_WARPS 32
 #endif
 #ifndef VAPR_GRAB                // consecutive tiles a warp takes per scheduler grab
 #define VAPR_GRAB 1
@@ -511,7 +515,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                  const CollisionArgs a) {
     // programmatic dependent launch (vapr_cost_grad): the first pass lets the
     // second launch at once, so its CTAs take SMs as the first's retire
-    if (a.pdl == 1) asm volatile("griddepcontrol.launch_dependents;");
+    // programmatic dependent launch (vapr_cost_grad): the world pass lets its
+    // successor (the cost reduction) launch at once; the self pass waits for
+    // FK after staging its tables (below)
+    if (a.pdl == 2) pdl_trigger();
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
     float* ssr = reinterpret_cast<float*>(base + G.sr);
@@ -576,6 +583,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         }
     }
     __syncthreads();
+    if (a.pdl == 1) {
+        // out_spheres is complete after this; only then may the world pass
+        // (which reads it without waiting) launch
+        pdl_wait();
+        pdl_trigger();
+    }
 
     // ---- the warp's workspace
     char* wb = base + G.tables + (unsigned)warp * G.warp;
@@ -594,7 +607,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
     const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
-    const long long n_tiles = (P + kTP - 1) / kTP;
+    // poses per tile: kTP, or fewer for a small batch (more warps, each with
+    // a shorter serial item list: latency)
+    const int tp = a.tile_poses;
+    const long long n_tiles = (P + tp - 1) / tp;
+    // one-pose tiles (the smallest batches): the broadphase loops of the pose
+    // (and of its swept halo) spread over all 32 lanes instead of its 2
+    const bool wide = tp == 1;
     // dynamic scheduling: a warp takes kGrab consecutive tiles at a time
     // from a global counter (collision-dense tiles cost several times the
     // average, so static ranges leave a long tail; consecutive tiles share
@@ -622,16 +641,18 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             tile = grab * kGrab;
             t_end = min(n_tiles, tile + kGrab);
         }
-        const long long p0 = tile * kTP;
-        const int np = (int)min((long long)kTP, P - p0);
+        const long long p0 = tile * tp;
+        const int np = (int)min((long long)tp, P - p0);
         // halo rows p0 - 1 and p0 + 15 only for the swept world pass (the
         // segments that cross the tile edges); self and discrete need none
         const long long r_lo = swept ? max(p0 - 1, 0LL) : p0;
-        const long long r_hi = swept ? min(p0 + kTP + 1, P) : p0 + np;   // exclusive
+        const long long r_hi = swept ? min(p0 + np + 1, P) : p0 + np;   // exclusive
         const int row_off = int(r_lo - (p0 - 1));         // tile row of global row r_lo
         // the lane's pose p0 + lane = tile row lane + 1 (lane 31: the halo
         // pose, used only for the segment that ends there)
-        const long long pg = p0 + pl;
+        // wide: lanes pl = 2k + j work for pose lane j (the pose, the halo)
+        const int plb = wide ? (pl & 1) : pl;
+        const long long pg = p0 + plb;
         int h = -1, k0 = 0, K = 0;
         if (pg < P) {
             const long long b = pg / a.H;
@@ -765,15 +786,16 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // test ball per link: swept -> the segment (pose pg-1, pose pg),
             // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
             // (it bounds every sample on the segment); discrete -> pose pg
-            const bool tv = swept ? (h >= 1) : (pl < np);
+            const bool tv = swept ? (h >= 1 && plb <= np) : (plb < np);
             float bx[kLH], by[kLH], bz[kLH], lim2[kLH];
-            const float* prow = rows + pl * cs;
+            const float* prow = rows + plb * cs;
+            const float* brow = rows + (plb + 1) * cs;
 #pragma unroll
             for (int u = 0; u < kLH; ++u) {
                 const int l = half * kLH + u;
                 const int lc = min(l, kLinks - 1);
                 const int r3 = 3 * sref[lc];
-                float cx = myrow[r3], cy = myrow[r3 + 1], cz = myrow[r3 + 2];
+                float cx = brow[r3], cy = brow[r3 + 1], cz = brow[r3 + 2];
                 float rr = srl[lc] + margin;
                 if (swept) {
                     const float dx = prow[r3] - cx, dy = prow[r3 + 1] - cy, dz = prow[r3 + 2] - cz;
@@ -793,7 +815,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 #pragma unroll
             for (int u = 0; u < kLH; ++u) fm[u] = 0u;
             const int Kw = __reduce_max_sync(0xffffffffu, tv ? K : 0);
-            for (int k = 0; k < Kw; ++k) {
+            const int kstep = wide ? kPL / 2 : 1;
+            for (int k = wide ? (pl >> 1) : 0; k < Kw; k += kstep) {
                 const int ci = (k < K) ? k0 + k : 0;
                 const float4 q0 = __ldg(Wd.cub + 4 * ci), q1 = __ldg(Wd.cub + 4 * ci + 1);
                 const float4 q2 = __ldg(Wd.cub + 4 * ci + 2), q3 = __ldg(Wd.cub + 4 * ci + 3);
@@ -812,6 +835,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     const bool live = (o2 <= lim2[u]) || (!can_cull && lim2[u] >= 0.f);
                     if (kv && live) fm[u] |= 1u << k;
                 }
+            }
+            if (wide) {                 // gather the cuboid subsets of a pose lane
+#pragma unroll
+                for (int u = 0; u < kLH; ++u)
+#pragma unroll
+                    for (int d = 2; d < kPL; d <<= 1) fm[u] |= __shfl_xor_sync(0xffffffffu, fm[u], d);
             }
             // per pose: own / forward / backward cuboid masks of each link
             // (forward = the segment of pose lane pl + 1, same half)
@@ -927,7 +956,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // pairs of the live link pairs; glo / ghi bit g <=> group pair g
             // (g < 64 / >= 64) is live
             const float m2 = 2.f * margin;
-            const char* rb = reinterpret_cast<const char*>(myrow);
+            const char* rb = reinterpret_cast<const char*>(wide ? rows + cs : myrow);
             auto ball = [&](uint2 r) -> bool {
                 const float* ca = reinterpret_cast<const float*>(rb + (r.x & 0xffffu));
                 const float* cb = reinterpret_cast<const float*>(rb + (r.x >> 16));
@@ -935,11 +964,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const float lim = __uint_as_float(r.y) + m2;
                 return !can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim;
             };
+            // wide: the 32 lanes split the one pose's lists
+            const int bl0 = wide ? lane : half, bls = wide ? 32 : kLPP;
             uint32_t lpm = 0u;
-            if (pl < np)
-                for (int lp = half; lp < G.nlp; lp += kLPP)
+            if (pl < np || wide)
+                for (int lp = bl0; lp < G.nlp; lp += bls)
                     if (ball(slrec[lp])) lpm |= 1u << lp;
-            lpm |= __shfl_xor_sync(0xffffffffu, lpm, kPL);
+            lpm = wide ? __reduce_or_sync(0xffffffffu, lpm) : (lpm | __shfl_xor_sync(0xffffffffu, lpm, kPL));
             // group pairs: a uniform loop over the link pairs live for some
             // pose of the tile, each lane testing its pose's (the two lanes of
             // a pose alternate over the group pairs)
@@ -948,15 +979,25 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const int lp = __ffs(m) - 1;
                 const bool live = (lpm >> lp) & 1u;
                 const int g1 = slgp[lp + 1];
-                for (int g = slgp[lp] + half; g < g1; g += kLPP)
+                for (int g = slgp[lp] + bl0; g < g1; g += bls)
                     if (live && ball(sgrec[g])) {
                         if (g < 64) glo |= 1ull << g;
                         else ghi |= 1ull << (g - 64);
                     }
             }
             static_assert(kLPP == 2, "the exchange below assumes two lanes per pose");
-            glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
-            ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
+            if (wide) {
+                auto or64 = [](unsigned long long v) {
+                    const uint32_t l = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+                    const uint32_t h = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+                    return (unsigned long long)l | ((unsigned long long)h << 32);
+                };
+                glo = or64(glo);
+                ghi = or64(ghi);
+            } else {
+                glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
+                ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
+            }
             if (!owner) glo = ghi = 0ull;
             VAPR_STAT(2, __popcll(glo) + __popcll(ghi));
             // narrowphase: the live (pose, group pair) entries are listed, each
@@ -1159,11 +1200,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     }
     // the second pass completes only after the first: stream-ordered work
     // after it (aggregation, BK) sees both passes' outputs
-    if (a.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.pdl == 2) pdl_wait();
 }
 
 __global__ void traj_reduce_kernel(float* __restrict__ cost_pose, int B, int H,
                                    float* __restrict__ cost_traj, const float* __restrict__ add) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     float c = 0.f;
@@ -1216,8 +1259,9 @@ extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
 #define VAPR_PDL 1
 #endif
 cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
-                                  const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
+                                  const Fmt& fcp, const Fmt& fov, const CollisionArgs& a_in,
                                   cudaStream_t s) {
+    CollisionArgs a = a_in;
     const long long P = (long long)a.B * a.H;
     const bool sparse = a.cp_mask || a.ov_mask;
     const bool wide = (a.do_world && fcp.t > 10) || (a.do_self && fov.t > 10);
@@ -1243,7 +1287,16 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     if (e != cudaSuccess) return e;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nw, smem);
-    const long long tiles = (P + kTP - 1) / kTP;
+    // small batches: fewer poses per tile so that the tiles fill ~VAPR_SMALL_WARPS
+    // warps per SM (a tile's latency is its warp's serial item list)
+    {
+        const long long full = (P + kTP - 1) / kTP;
+        const long long target = (long long)sms * VAPR_SMALL_WARPS;
+        a.tile_poses = kTP;
+        if (full < target) a.tile_poses = (int)std::max(1LL, std::min<long long>(kTP, (P + target - 1) / target));
+        if (const char* e = getenv("VAPR_TILE_POSES")) a.tile_poses = std::max(1, std::min(kTP, atoi(e)));
+    }
+    const long long tiles = (P + a.tile_poses - 1) / a.tile_poses;
     // enough CTAs for every warp to have a chunk; small batches: spread up to
     // one CTA per tile over the SMs (latency: a lone SM's issue slots shared
     // by its 16 warps would serialise the few tiles there are)
@@ -1256,22 +1309,11 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const bool tap_w = a.do_world && tap_arm(tw, P, R.cols, s);
     const bool tap_s = a.do_self && tap_arm(2, P, R.cols, s);
 #endif
-    if (a.pdl == 2) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)grid);
-        cfg.blockDim = dim3(32 * nw);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, R, G, W, fos, fcp, fov, a);
-        if (e != cudaSuccess) return e;
-    } else {
-        kern<<<(unsigned)grid, 32 * nw, smem, s>>>(R, G, W, fos, fcp, fov, a);
-    }
+    // pdl 1: the self pass, a programmatic dependent of FK; pdl 2: the world
+    // pass, a programmatic dependent of the self pass
+    e = launch_k(kern, dim3((unsigned)grid), dim3(32 * nw), smem, s, a.pdl != 0, R, G, W, fos, fcp,
+                 fov, a);
+    if (e != cudaSuccess) return e;
 #ifdef VAPR_DEBUG_TAP
     if (tap_w) tap_disarm(tw, s);
     if (tap_s) tap_disarm(2, s);
@@ -1332,10 +1374,10 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
 }
 
 cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s, const float* add) {
+                               cudaStream_t s, const float* add, bool pdl) {
     if (B <= 0) return cudaSuccess;
-    traj_reduce_kernel<<<(B + 255) / 256, 256, 0, s>>>(cost_pose, B, H, cost_traj, add);
-    return cudaGetLastError();
+    return launch_k(traj_reduce_kernel, dim3((B + 255) / 256), dim3(256), 0, s, pdl, cost_pose, B,
+                    H, cost_traj, add);
 }
 
 cudaError_t launch_best_per_problem(const float* cost_traj, int32_t n_problems, int32_t seeds,

@@ -397,6 +397,14 @@ struct RobotDev {
     uint8_t adj[2 * kMaxPairs];
 };
 
+// Programmatic dependent launch (vapr_cost_grad chains its kernels with it:
+// a kernel launched with the programmatic-serialization attribute may start
+// while its predecessor drains; pdl_wait() returns once the predecessor grid
+// has completed and its writes are visible -- a no-op for a kernel launched
+// normally).  pdl_trigger() lets the successor launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // 3x4 rigid transform, row-major rotation r[3][3] and translation p[3].
 struct Xf {
     float r[9];

@@ -9,6 +9,29 @@
 
 namespace vapr {
 
+// Launch `kern` normally, or (pdl) as a programmatic dependent of the previous
+// kernel on the stream -- the kernel must pdl_wait() before touching its
+// predecessor's outputs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, bool pdl, Args&&... args) {
+    if (!pdl) {
+        kern<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // World table on the device: per cuboid 16 floats = R^T (row-major 3x3), t,
 // half extents, pad; offsets [n_worlds + 1].
 struct WorldsDev {
@@ -46,7 +69,9 @@ struct CollisionArgs {
     const float* q;           // [B*H, 7]
     float* grad_q;            // [B*H, 7]
     Fmt fgos;
-    int32_t pdl;              // internal: 1 = trigger dependents at start, 2 = wait at exit
+    int32_t tile_poses;       // internal: poses per warp tile (<= 15; fewer for small batches)
+    int32_t pdl;              // internal: 1 = PDL dependent of FK (wait, then trigger the
+                              // second pass), 2 = trigger at start, wait for pass 1 at exit
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
     unsigned int* sched;      // internal: tile-scheduler slot {next grab, finished CTAs}, zero
 };
@@ -79,7 +104,7 @@ constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight col
 // add (nullable): cost_pose += add first (the self pass's separate cost);
 // cost_traj (nullable): the per-trajectory sums
 cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
-                               cudaStream_t s, const float* add = nullptr);
+                               cudaStream_t s, const float* add = nullptr, bool pdl = false);
 // N3 sparse form of a sphere tensor (include/vapr.h "N3"; sparse.cuh)
 struct SparseOut {
     unsigned long long* mask;  // [rows] (the caller offsets it to the first row)
@@ -102,17 +127,20 @@ cudaError_t launch_densify(const Fmt& f, const SparseIn& in, long long rows, int
 // sparse (nullable): write grad_out_spheres in the sparse form instead of gos
 cudaError_t launch_aggregate(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                              const uint32_t* cp, const uint32_t* ov, long long rows,
-                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr);
+                             uint32_t* gos, cudaStream_t s, const SparseOut* sparse = nullptr,
+                             bool pdl = false);
 // N3 sparse inputs (cp / ov: sphere bitmaps + packed non-zero codes at
 // pool + row * ceil(cols / pf)) -> the sparse form of grad_out_spheres
 cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& fgos, int cols,
                                     const uint32_t* cp_pool, const unsigned long long* cpm,
                                     const uint32_t* ov_pool, const unsigned long long* ovm,
-                                    long long rows, const SparseOut& sparse, cudaStream_t s);
+                                    long long rows, const SparseOut& sparse, cudaStream_t s,
+                                    bool pdl = false);
 // sparse (nullable): read grad_out_spheres from the sparse form instead of gos
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s,
-                      const IkArgs* ik = nullptr, const SparseIn* sparse = nullptr);
+                      const IkArgs* ik = nullptr, const SparseIn* sparse = nullptr,
+                      bool pdl = false);
 // N1 optimiser (lbfgs.cu)
 struct LbfgsScales {
     float s[32];

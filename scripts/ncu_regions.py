@@ -14,7 +14,11 @@ for a in sys.argv[4:]:
     name, rng = a.split(":")
     lo, hi = (int(x) for x in rng.split("-"))
     regions.append((name, lo, hi))
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}",
+import os as _os
+# NCU_LAUNCH=i picks the i-th matching launch of the report
+EXTRA = (["--launch-skip", _os.environ["NCU_LAUNCH"], "--launch-count", "1"]
+         if _os.environ.get("NCU_LAUNCH") else [])
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}", *EXTRA,
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 rows = []
