@@ -80,7 +80,6 @@ aggregate_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int cols, int Wc, i
                  long long rows, uint32_t* __restrict__ gos, uint32_t rw_c, uint32_t rw_o,
                  uint32_t rw_g, int xs, const SparseOut sp) {
     pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
-    pdl_trigger();
     extern __shared__ uint4 smem_a[];
     uint32_t* sc = reinterpret_cast<uint32_t*>(smem_a);     // [kRows * Wc]
     uint32_t* so = sc + kRows * Wc;                         // [kRows * Wo]
@@ -162,7 +161,6 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
                         const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
                         long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
     pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
-    pdl_trigger();
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nw = 0u;
     if (p < rows) {
@@ -233,7 +231,6 @@ aggregate_sparse_rows_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int col
                              const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
                              long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
     pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
-    pdl_trigger();
     __shared__ SparseTileSmem<kSmRows> sm;
     __shared__ uint32_t wbuf[kSmWarps * 3 * 64];
     __shared__ unsigned long long smc[kSmRows], smo[kSmRows];

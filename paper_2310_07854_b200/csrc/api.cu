@@ -50,9 +50,9 @@ struct vapr_ctx {
     bool goals_set = false;
 };
 
-#ifndef VAPR_CHAIN_PDL             // vapr_cost_grad: chain its kernels by programmatic dependent launch
-#define VAPR_CHAIN_PDL 1
-#endif
+#ifndef VAPR_CHAIN_PDL             // vapr_cost_grad: reduce / aggregate / BK as programmatic dependents
+#define VAPR_CHAIN_PDL 0           // measured slower (bench step 4.39 -> 4.38 ms, config 1 / 2 71 / 68 ->
+#endif                             // 80 / 76 us; early triggers: per-env leg 5.7 -> 6.9 ms); FK -> self stays
 #ifndef VAPR_END_CHUNK_WEIGHT      // vapr_cost_grad_host: first / last chunk size relative to the others
 #define VAPR_END_CHUNK_WEIGHT 0.25
 #endif

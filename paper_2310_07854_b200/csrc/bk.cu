@@ -57,7 +57,6 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     __shared__ int s_act[kTile];
     __shared__ int s_nact;
     pdl_wait();         // vapr_cost_grad: the aggregation's output is complete
-    pdl_trigger();
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x;

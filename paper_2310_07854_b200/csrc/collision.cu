@@ -515,10 +515,11 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                  const CollisionArgs a) {
     // programmatic dependent launch (vapr_cost_grad): the first pass lets the
     // second launch at once, so its CTAs take SMs as the first's retire
-    // programmatic dependent launch (vapr_cost_grad): the world pass lets its
-    // successor (the cost reduction) launch at once; the self pass waits for
-    // FK after staging its tables (below)
-    if (a.pdl == 2) pdl_trigger();
+    // programmatic dependent launch (vapr_cost_grad): the self pass waits for
+    // FK after staging its tables (below) and then lets the world pass launch;
+    // every other kernel of the chain lets its successor launch by exiting (an
+    // early trigger would park the successor's CTAs on the SMs, blocked in
+    // their wait, and take occupancy from the running grid)
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
     float* ssr = reinterpret_cast<float*>(base + G.sr);
@@ -1206,7 +1207,6 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 __global__ void traj_reduce_kernel(float* __restrict__ cost_pose, int B, int H,
                                    float* __restrict__ cost_traj, const float* __restrict__ add) {
     pdl_wait();
-    pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     float c = 0.f;

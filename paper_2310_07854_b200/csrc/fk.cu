@@ -162,7 +162,9 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
           float* __restrict__ ee) {
     __shared__ float sq[kTile * kJoints];
     __shared__ uint32_t sw[kTile * kCS];
-    pdl_trigger();      // vapr_cost_grad: the self collision pass may launch (it waits for us)
+    // vapr_cost_grad: the self collision pass (a programmatic dependent) may
+    // launch and stage its tables while FK drains; it waits for FK's output
+    pdl_trigger();
     const long long p0 = (long long)blockIdx.x * kTile;
     const int np = (int)min((long long)kTile, P - p0);
     const int tid = threadIdx.x, lane = tid & 31, w0 = tid & ~31;

@@ -1,0 +1,41 @@
+#!/bin/bash
+# Round-2 measurement session (one gpurun call): GPU suite + smoke, the bench
+# line and the oracle arm, an ncu launch list of the bench step, full ncu
+# captures of the step's kernels (sparse and dense 43-bit, fused), small-batch
+# latency.  Outputs under gpurun_out/r2/.
+set -u
+O=gpurun_out/r2
+mkdir -p $O
+python -m pytest tests -m gpu -q > $O/gpu_tests.txt 2>&1; tail -1 $O/gpu_tests.txt
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1; tail -1 $O/smoke.txt
+python bench.py > $O/bench.json 2> $O/bench.err; tail -c 200 $O/bench.json
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
+python scripts/time_tiles.py > $O/small_latency.txt 2>&1
+python scripts/time_small.py > $O/small_stages.txt 2>&1
+B="bench.py --steps 2 --warmup 1 --no-formats --no-iko --no-to --no-e2e --no-cpu --no-graph"
+python $B > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $O/launches_bench.csv python $B > $O/ncu_list.log 2>&1
+K='regex:fk_kernel|collision_kernel|traj_reduce|aggregate|bk_kernel'
+for m in sparse dense; do
+  python scripts/run_mode.py 43bit $m > /dev/null && ncu --set full --import-source on --clock-control none \
+      -k "$K" -c 6 -o $O/step_${m}43 -f python scripts/run_mode.py 43bit $m > $O/ncu_${m}.log 2>&1
+done
+python scripts/run_mode.py 43bit fused > /dev/null && ncu --set full --import-source on --clock-control none \
+    -k "$K" -c 2 -o $O/step_fused43 -f python scripts/run_mode.py 43bit fused > $O/ncu_fused.log 2>&1
+python scripts/run_mode.py fp32 sparse > /dev/null && ncu --set full --clock-control none \
+    -k "$K" -c 6 -o $O/step_sparse32 -f python scripts/run_mode.py fp32 sparse > $O/ncu_sparse32.log 2>&1
+ls $O
+# summaries on the box (the reports themselves exceed gpurun's copy-back cap)
+for r in $O/*.ncu-rep; do
+  b=${r%.ncu-rep}
+  python scripts/ncu_summary.py $r > $b.summary.txt 2>&1
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+done
+for L in 1 2; do
+  NCU_LAUNCH=$L python scripts/ncu_regions.py $O/step_sparse43.ncu-rep collision_kernel collision.cu \
+      helpers:1-512 stage:513-668 decode:669-748 zero:749-782 world:783-950 self_bp:951-1002 \
+      self_np:1003-1090 self_grad:1091-1190 > $O/regions_sparse43_launch$L.txt 2>&1
+done
+NCU_LAUNCH=1 python scripts/ncu_lines.py $O/step_sparse43.ncu-rep collision_kernel 40 > $O/lines_sparse43_self.txt 2>&1
+rm -f $O/step_dense43.ncu-rep $O/step_sparse32.ncu-rep $O/step_fused43.ncu-rep
+du -sh $O
