@@ -40,6 +40,9 @@ struct vapr_ctx {
     int sparse = 0;
     // N4: the fused on-chip rollout (VAPR_OPT_FUSED)
     int fused = 0;
+    // the collision kernel's robot tables as a device image (vapr_set_robot)
+    void* d_tab_img = nullptr;
+    int32_t tab_img_bytes = 0;
     // stage timing hook (vapr_set_stage_events): caller-owned events recorded
     // between the launches of vapr_cost_grad
     cudaEvent_t stage_ev[6] = {};
@@ -247,6 +250,7 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     if (c->d_off) cudaFree(c->d_off);
     if (c->d_sched) cudaFree(c->d_sched);
     if (c->d_goals) cudaFree(c->d_goals);
+    if (c->d_tab_img) cudaFree(c->d_tab_img);
     for (cudaStream_t st : c->par)
         if (st) cudaStreamDestroy(st);
     if (c->s_in) cudaStreamDestroy(c->s_in);
@@ -474,6 +478,20 @@ vapr_status vapr_set_robot(vapr_ctx* c, const vapr_robot* r) {
         // round up so the FP32 radius never under-states the double bound
         if (best < 1e300) R.link_rl[l] = std::nextafter((float)best, 3e38f);
     }
+    {   // the collision kernel's shared tables, staged from this image
+        DeviceGuard g(c->device);
+        CHECK(g.ok, VAPR_ERR_CUDA);
+        const std::vector<uint8_t> img = collision_table_image(R);
+        if (c->d_tab_img) {                       // kernels in flight may read the old one
+            cudaDeviceSynchronize();
+            cudaFree(c->d_tab_img);
+            c->d_tab_img = nullptr;
+        }
+        CHECK(cudaMalloc(&c->d_tab_img, img.size()) == cudaSuccess, VAPR_ERR_CUDA);
+        CHECK(cudaMemcpy(c->d_tab_img, img.data(), img.size(), cudaMemcpyHostToDevice) == cudaSuccess,
+              VAPR_ERR_CUDA);
+        c->tab_img_bytes = (int32_t)img.size();
+    }
     c->robot = R;
     c->robot_set = true;
     return VAPR_OK;
@@ -693,6 +711,8 @@ static vapr_status collision_common(vapr_ctx* c, const uint32_t* os, const int32
     a.eta_s = do_self ? eta_s : 1.f;
     a.w_s = w_s;
     a.cull = c->cull;
+    a.tab_img = static_cast<const uint4*>(c->d_tab_img);
+    a.tab_img_bytes = c->tab_img_bytes;
     a.cost = cost;
     a.cp = cp;
     a.ov = ov;
@@ -878,6 +898,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.eta_s = p->eta_self;
         a.w_s = p->w_self;
         a.cull = c->cull;
+        a.tab_img = static_cast<const uint4*>(c->d_tab_img);
+        a.tab_img_bytes = c->tab_img_bytes;
         a.cost = cpose + p0;
         a.fused = 1;
         a.q = qc;
@@ -959,6 +981,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
         a.eta_s = p->eta_self;
         a.w_s = p->w_self;
         a.cull = c->cull;
+        a.tab_img = static_cast<const uint4*>(c->d_tab_img);
+        a.tab_img_bytes = c->tab_img_bytes;
         a.cost = cpose + p0;
         a.cp = cp;
         a.ov = ov;

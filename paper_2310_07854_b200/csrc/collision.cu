@@ -40,6 +40,7 @@
 // (tests/test_gpu_parity.py::test_cull_is_exact).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -539,48 +540,23 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     const int pl = lane % kPL, half = lane / kPL;   // pose lane, its share of the per-pose work
     const int PMW = G.pmw;
 
-    // ---- stage the robot tables (once per CTA)
-    for (int i = tid; i < G.S; i += blockDim.x) {
-        ssr[i] = R.sr[i];
-        int l = 0;
-        while (l < kLinks - 1 && i >= R.link_start[l + 1]) ++l;
-        slink[i] = (uint8_t)l;
-        if (FUSED) sso[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
-    }
-    if (tid < kLinks) {
-        srl[tid] = R.link_rl[tid];
-        sref[tid] = R.link_ref[tid];
-    }
-    if (tid < 2 * kLinks) {
-        srl[kLinks + tid] = R.grp_rl[tid];
-        sref[kLinks + tid] = R.grp_ref[tid];
-    }
-    if (a.do_self) {
-        for (int i = tid; i < G.npairs; i += blockDim.x) {
-            spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
-            // record k of the group-pair order: byte offsets 12 i | 12 j << 16 in
-            // a row, and the activation distance r_i + r_j + eta; its pair id
-            // (needed only for an active pair) in sgpid[k]
-            const int pid = R.gp_pid[i], pi = R.pair_i[pid], pj = R.pair_j[pid];
-            sprec[i] = make_uint2((uint32_t)(12 * pi) | ((uint32_t)(12 * pj) << 16),
-                                  __float_as_uint(R.sr[pi] + R.sr[pj] + a.eta_s));
-            sgpid[i] = (uint16_t)pid;
-        }
-        for (int i = tid; i <= G.ngp; i += blockDim.x) sgpoff[i] = R.gp_off[i];
-        for (int i = tid; i < G.nlp; i += blockDim.x) {
-            // link pair i: byte offsets 12 ref_a | 12 ref_b << 16 in a row and
-            // the static part of the cull distance; its group pairs
-            const int la = R.lp_a[i], lb = R.lp_b[i];
-            slrec[i] = make_uint2((uint32_t)(12 * R.link_ref[la]) | ((uint32_t)(12 * R.link_ref[lb]) << 16),
-                                  __float_as_uint(R.link_rl[la] + R.link_rl[lb] + a.eta_s + kSlack));
-        }
-        for (int i = tid; i <= G.nlp; i += blockDim.x) slgp[i] = R.lp_gp_off[i];
-        for (int i = tid; i < G.ngp; i += blockDim.x) {
-            // byte offsets 12 ref_a | 12 ref_b << 16 in a row, and the static
-            // part of the cull distance
-            const int ga = R.gp_a[i], gb = R.gp_b[i];
-            sgrec[i] = make_uint2((uint32_t)(12 * R.grp_ref[ga]) | ((uint32_t)(12 * R.grp_ref[gb]) << 16),
-                                  __float_as_uint(R.grp_rl[ga] + R.grp_rl[gb] + a.eta_s + kSlack));
+    // ---- stage the robot tables (once per CTA): the device image (16-byte
+    // loads), then eta_s added to the three distance tables -- the same
+    // FP32 sums, in the same order, as building them from R directly
+    {
+        const uint4* img = a.tab_img;
+        uint4* dst = reinterpret_cast<uint4*>(base);
+        for (int i = tid; i < a.tab_img_bytes / 16; i += blockDim.x) dst[i] = __ldg(img + i);
+        if (FUSED)
+            for (int i = tid; i < G.S; i += blockDim.x) sso[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
+        __syncthreads();
+        if (a.do_self) {
+            for (int i = tid; i < G.npairs; i += blockDim.x)
+                sprec[i].y = __float_as_uint(__uint_as_float(sprec[i].y) + a.eta_s);
+            for (int i = tid; i < G.nlp; i += blockDim.x)
+                slrec[i].y = __float_as_uint(__uint_as_float(slrec[i].y) + a.eta_s + kSlack);
+            for (int i = tid; i < G.ngp; i += blockDim.x)
+                sgrec[i].y = __float_as_uint(__uint_as_float(sgrec[i].y) + a.eta_s + kSlack);
         }
     }
     __syncthreads();
@@ -611,7 +587,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     // poses per tile: kTP, or fewer for a small batch (more warps, each with
     // a shorter serial item list: latency)
     const int tp = a.tile_poses;
-    const long long n_tiles = (P + tp - 1) / tp;
+    const long long n_tiles = a.n_tiles;
     // one-pose tiles (the smallest batches): the broadphase loops of the pose
     // (and of its swept halo) spread over all 32 lanes instead of its 2
     const bool wide = tp == 1;
@@ -656,7 +632,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         const long long pg = p0 + plb;
         int h = -1, k0 = 0, K = 0;
         if (pg < P) {
-            const long long b = pg / a.H;
+            // (32-bit division while the batch fits: the 64-bit one is a long
+            // subroutine on every lane of every tile)
+            const long long b = (P < 0x7fffffffLL) ? (long long)((uint32_t)pg / (uint32_t)a.H) : pg / a.H;
             h = int(pg - b * a.H);
             if (a.do_world) {
                 const int wi = __ldg(a.world_idx + b);
@@ -1252,6 +1230,70 @@ extern "C" int vapr_debug_stats(unsigned long long* out, int reset) {
 }
 #endif
 
+std::vector<uint8_t> collision_table_image(const RobotDev& R) {
+    Fmt f32{};
+    f32.pf = 1;
+    f32.t = 32;
+    const Geo G = make_geo(R, f32, f32, f32, 1, 1, 0, 0);
+    std::vector<uint8_t> img((G.so + 15) / 16 * 16, 0);
+    uint8_t* base = img.data();
+    auto at = [&](unsigned off) { return base + off; };
+    float* ssr = reinterpret_cast<float*>(at(G.sr));
+    float* srl = reinterpret_cast<float*>(at(G.rl));
+    int* sref = reinterpret_cast<int*>(at(G.ref));
+    uint16_t* spij = reinterpret_cast<uint16_t*>(at(G.pij));
+    uint32_t* sprec = reinterpret_cast<uint32_t*>(at(G.prec));
+    uint16_t* sgpid = reinterpret_cast<uint16_t*>(at(G.gpid));
+    uint32_t* sgrec = reinterpret_cast<uint32_t*>(at(G.grec));
+    uint16_t* sgpoff = reinterpret_cast<uint16_t*>(at(G.gpoff));
+    uint8_t* slink = at(G.slink);
+    uint32_t* slrec = reinterpret_cast<uint32_t*>(at(G.lrec));
+    uint8_t* slgp = at(G.lgp);
+    auto fb = [](float x) {
+        uint32_t u;
+        std::memcpy(&u, &x, 4);
+        return u;
+    };
+    for (int i = 0; i < G.S; ++i) {
+        ssr[i] = R.sr[i];
+        int l = 0;
+        while (l < kLinks - 1 && i >= R.link_start[l + 1]) ++l;
+        slink[i] = (uint8_t)l;
+    }
+    for (int t = 0; t < kLinks; ++t) {
+        srl[t] = R.link_rl[t];
+        sref[t] = R.link_ref[t];
+    }
+    for (int t = 0; t < 2 * kLinks; ++t) {
+        srl[kLinks + t] = R.grp_rl[t];
+        sref[kLinks + t] = R.grp_ref[t];
+    }
+    for (int i = 0; i < G.npairs; ++i) {
+        spij[i] = (uint16_t)(R.pair_i[i] | (R.pair_j[i] << 8));
+        // record k of the group-pair order: byte offsets 12 i | 12 j << 16 in
+        // a row, and r_i + r_j (+ eta_s in the kernel); its pair id in sgpid[k]
+        const int pid = R.gp_pid[i], pi = R.pair_i[pid], pj = R.pair_j[pid];
+        sprec[2 * i] = (uint32_t)(12 * pi) | ((uint32_t)(12 * pj) << 16);
+        sprec[2 * i + 1] = fb(R.sr[pi] + R.sr[pj]);
+        sgpid[i] = (uint16_t)pid;
+    }
+    for (int i = 0; i <= G.ngp; ++i) sgpoff[i] = R.gp_off[i];
+    for (int i = 0; i < G.nlp; ++i) {
+        // link pair i: byte offsets 12 ref_a | 12 ref_b << 16 in a row and the
+        // static part of the cull distance (+ eta_s + slack in the kernel)
+        const int la = R.lp_a[i], lb = R.lp_b[i];
+        slrec[2 * i] = (uint32_t)(12 * R.link_ref[la]) | ((uint32_t)(12 * R.link_ref[lb]) << 16);
+        slrec[2 * i + 1] = fb(R.link_rl[la] + R.link_rl[lb]);
+    }
+    for (int i = 0; i <= G.nlp; ++i) slgp[i] = R.lp_gp_off[i];
+    for (int i = 0; i < G.ngp; ++i) {
+        const int ga = R.gp_a[i], gb = R.gp_b[i];
+        sgrec[2 * i] = (uint32_t)(12 * R.grp_ref[ga]) | ((uint32_t)(12 * R.grp_ref[gb]) << 16);
+        sgrec[2 * i + 1] = fb(R.grp_rl[ga] + R.grp_rl[gb]);
+    }
+    return img;
+}
+
 #ifndef VAPR_SPREAD_SMALL
 #define VAPR_SPREAD_SMALL 1
 #endif
@@ -1297,6 +1339,8 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
         if (const char* e = getenv("VAPR_TILE_POSES")) a.tile_poses = std::max(1, std::min(kTP, atoi(e)));
     }
     const long long tiles = (P + a.tile_poses - 1) / a.tile_poses;
+    a.n_tiles = tiles;
+    if (!a.tab_img || a.tab_img_bytes != (int)((G.so + 15) / 16 * 16)) return cudaErrorInvalidValue;
     // enough CTAs for every warp to have a chunk; small batches: spread up to
     // one CTA per tile over the SMs (latency: a lone SM's issue slots shared
     // by its 16 warps would serialise the few tiles there are)

@@ -235,6 +235,63 @@ fk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     }
 }
 
+// Small batches (latency): kSL lanes per pose, each walking the whole chain
+// (it is short) but placing only the spheres s = sub, sub + kSL, ... into a
+// shared FP32 row tile; the CTA then encodes the tile word-parallel and
+// stores its rows as one contiguous, coalesced range.  The same chain
+// arithmetic and exact codes as fk_kernel, so the output is bit-identical;
+// the serial work per thread drops from the whole row to ~1/kSL of it.
+constexpr int kSL = 8;                       // lanes per pose
+constexpr int kSRows = 128 / kSL;            // poses per CTA
+__global__ void __launch_bounds__(128)
+fk_small_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
+                long long P, int W, uint32_t* __restrict__ os) {
+    extern __shared__ float st[];            // [kSRows][xs] FP32 rows (+0 beyond cols)
+    pdl_trigger();
+    const int xs = W * f.pf;
+    const long long p0 = (long long)blockIdx.x * kSRows;
+    const int np = (int)min((long long)kSRows, P - p0);
+    const int r = threadIdx.x / kSL, sub = threadIdx.x % kSL;
+    for (int i = threadIdx.x; i < kSRows * xs; i += 128) st[i] = 0.f;
+    __syncthreads();
+    if (r < np) {
+        float qv[kJoints];
+#pragma unroll
+        for (int j = 0; j < kJoints; ++j) qv[j] = __ldg(q + (p0 + r) * kJoints + j);
+        float* row = st + r * xs;
+        Xf X;
+        xf_identity(X);
+        for (int l = 0; l < kLinks; ++l) {
+            if (l >= 1 && l <= kJoints) fk_step(X, R, l - 1, qv[l - 1]);
+            if (l == kLinks - 1) fk_hand(X, R);
+            const int s0 = R.link_start[l], s1 = R.link_start[l + 1];
+            // this lane's spheres of the link: s = sub (mod kSL)
+            for (int s = s0 + ((sub - s0) % kSL + kSL) % kSL; s < s1; s += kSL) {
+                float cx, cy, cz;
+                xf_apply(X, R.sx[s], R.sy[s], R.sz[s], cx, cy, cz);
+                row[3 * s] = cx;
+                row[3 * s + 1] = cy;
+                row[3 * s + 2] = cz;
+                VAPR_TAP(0, (p0 + r) * R.cols + 3 * s, cx);
+                VAPR_TAP(0, (p0 + r) * R.cols + 3 * s + 1, cy);
+                VAPR_TAP(0, (p0 + r) * R.cols + 3 * s + 2, cz);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t* dst = os + p0 * W;
+    with_pf(f.pf, [&](auto Pc) {
+        constexpr int PF = decltype(Pc)::value;
+        for (int i = threadIdx.x; i < np * W; i += 128) {
+            const int rr = i / W, w = i - rr * W;
+            float x[PF];
+#pragma unroll
+            for (int j = 0; j < PF; ++j) x[j] = st[rr * xs + w * PF + j];
+            __stcs(dst + i, encode_word_t<PF>(x, f));
+        }
+    });
+}
+
 }  // namespace
 
 cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long long P,
@@ -244,6 +301,22 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
     const bool iko = ik && ik_on(*ik);
     auto kern = iko ? (ee ? fk_kernel<true, true> : fk_kernel<true, false>)
                     : (ee ? fk_kernel<false, true> : fk_kernel<false, false>);
+#ifndef VAPR_FK_SMALL_BELOW
+#define VAPR_FK_SMALL_BELOW 8192
+#endif
+    if (!iko && !ee && P < VAPR_FK_SMALL_BELOW) {
+        const size_t smem = sizeof(float) * kSRows * W * fos.pf;
+        if (smem <= 48 * 1024) {
+#ifdef VAPR_DEBUG_TAP
+            const bool tapped_s = tap_arm(0, P, R.cols, s) != nullptr;
+#endif
+            fk_small_kernel<<<(unsigned)((P + kSRows - 1) / kSRows), 128, smem, s>>>(R, fos, q, P, W, os);
+#ifdef VAPR_DEBUG_TAP
+            if (tapped_s) tap_disarm(0, s);
+#endif
+            return cudaGetLastError();
+        }
+    }
     const long long grid = (P + kTile - 1) / kTile;
     IkArgs none{};
 #ifdef VAPR_DEBUG_TAP

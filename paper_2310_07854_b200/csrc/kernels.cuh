@@ -4,6 +4,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <vector>
 
 #include "common.cuh"
 
@@ -69,7 +70,13 @@ struct CollisionArgs {
     const float* q;           // [B*H, 7]
     float* grad_q;            // [B*H, 7]
     Fmt fgos;
+    // the robot's CTA tables as a device image (collision_table_image; the
+    // eta-dependent distances without eta): staged with 16-byte loads instead
+    // of divergent parameter-space reads
+    const uint4* tab_img;
+    int32_t tab_img_bytes;
     int32_t tile_poses;       // internal: poses per warp tile (<= 15; fewer for small batches)
+    long long n_tiles;        // internal: ceil(B H / tile_poses)
     int32_t pdl;              // internal: 1 = PDL dependent of FK (wait, then trigger the
                               // second pass), 2 = trigger at start, wait for pass 1 at exit
     int32_t cost_accumulate;  // internal: cost += (this pass) instead of cost =
@@ -100,6 +107,9 @@ cudaError_t launch_fk(const RobotDev& R, const Fmt& fos, const float* q, long lo
 cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& fos,
                              const Fmt& fcp, const Fmt& fov, const CollisionArgs& a,
                              unsigned int* sched_ring, unsigned int* sched_next, cudaStream_t s);
+// The byte image of the collision kernel's shared robot tables (layout of
+// its Geo; the activation distances without eta_s), built once per robot.
+std::vector<uint8_t> collision_table_image(const RobotDev& R);
 constexpr int kSchedSlots = 256;   // scheduler slots per context (in-flight collision passes)
 // add (nullable): cost_pose += add first (the self pass's separate cost);
 // cost_traj (nullable): the per-trajectory sums
