@@ -31,10 +31,10 @@ for r in $O/*.ncu-rep; do
   python scripts/ncu_summary.py $r > $b.summary.txt 2>&1
   ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
 done
-for L in 1 2; do
+for L in 0 1; do
   NCU_LAUNCH=$L python scripts/ncu_regions.py $O/step_sparse43.ncu-rep collision_kernel collision.cu \
-      helpers:1-512 stage:513-668 decode:669-748 zero:749-782 world:783-950 self_bp:951-1002 \
-      self_np:1003-1090 self_grad:1091-1190 > $O/regions_sparse43_launch$L.txt 2>&1
+      helpers:1-513 stage:514-647 decode:648-727 zero:728-761 world:762-929 self_bp:930-981 \
+      self_np:982-1069 self_grad:1070-1160 > $O/regions_sparse43_launch$L.txt 2>&1
 done
 NCU_LAUNCH=1 python scripts/ncu_lines.py $O/step_sparse43.ncu-rep collision_kernel 40 > $O/lines_sparse43_self.txt 2>&1
 rm -f $O/step_dense43.ncu-rep $O/step_sparse32.ncu-rep $O/step_fused43.ncu-rep
