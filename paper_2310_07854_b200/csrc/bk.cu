@@ -29,13 +29,17 @@ namespace {
 #ifndef VAPR_BK_TILE
 #define VAPR_BK_TILE 128
 #endif
-constexpr int kTile = VAPR_BK_TILE;         // poses (= threads) per CTA
+constexpr int kTile = VAPR_BK_TILE;         // threads per CTA
+constexpr int kMaxTP = 4 * kTile;           // poses per CTA at most
 
 // IKO: the N2 pose / bound terms; SP: the gradient slot is IEEE E5M10 (its
 // exponent-31 codes decode to inf / NaN, reading c41) -- a separate
 // instantiation so the common ones carry no fixup.
 // VAPR_BK_MINB (tuning knob): minimum resident CTAs per SM; unset = the plain
 // bound (an explicit 1 lets ptxas use ~150 registers and is slower)
+#ifndef VAPR_BK_PPT               // poses per thread (CTA tile = VAPR_BK_PPT x threads, at most 4)
+#define VAPR_BK_PPT 2
+#endif
 #ifdef VAPR_BK_MINB
 #define VAPR_BK_BOUNDS __launch_bounds__(kTile, VAPR_BK_MINB)
 #else
@@ -46,19 +50,22 @@ __global__ void VAPR_BK_BOUNDS
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
           uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik,
-          const SparseIn spi) {
+          const SparseIn spi, int tp) {
+    // tp poses per CTA (a multiple of kTile): with about half of the poses
+    // carrying a gradient, two poses per thread keep the compacted chains
+    // on every warp instead of leaving half the CTA at the barrier
     extern __shared__ unsigned long long smem8[];
     const int WS = W + 4;                 // 16-byte aligned rows
     float4* so = reinterpret_cast<float4*>(smem8);                    // [kMaxSpheres] sphere offsets
-    float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [kTile * 7]
-    uint32_t* sw = reinterpret_cast<uint32_t*>(sq + kTile * kJoints); // [kTile * WS]
-    float* sg = reinterpret_cast<float*>(sw + kTile * WS);            // [kTile * 7] grad_q
-    __shared__ unsigned long long s_mask[kTile];
-    __shared__ int s_act[kTile];
+    float* sq = reinterpret_cast<float*>(so + kMaxSpheres);           // [tp * 7]
+    uint32_t* sw = reinterpret_cast<uint32_t*>(sq + tp * kJoints);    // [tp * WS]
+    float* sg = reinterpret_cast<float*>(sw + tp * WS);               // [tp * 7] grad_q
+    __shared__ unsigned long long s_mask[kMaxTP];
+    __shared__ int16_t s_act[kMaxTP];
     __shared__ int s_nact;
     pdl_wait();         // vapr_cost_grad: the aggregation's output is complete
-    const long long p0 = (long long)blockIdx.x * kTile;
-    const int np = (int)min((long long)kTile, P - p0);
+    const long long p0 = (long long)blockIdx.x * tp;
+    const int np = (int)min((long long)tp, P - p0);
     const int tid = threadIdx.x;
     if (tid == 0) s_nact = 0;
 
@@ -84,22 +91,26 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     // the pose's non-zero spheres, from its own row (16-byte reads, stride
     // W + 4 words: conflict-free per quarter warp); a word's non-zero fields
     // come from one SWAR test, the rare non-zero words are then walked
+    // compact the poses with a non-zero gradient so the chains below run in
+    // full warps (each pose's result is independent of the order)
+    // with the IKO pose cost every pose is active (its hand frame carries a
+    // force and a torque whatever its sphere gradients)
+    const bool pose_on = IKO && (ik.w_pos != 0.f || ik.w_rot != 0.f);
+    for (int pt = tid; pt < np; pt += kTile) {
     unsigned long long mask = 0ull;
     if (SPR) {
         // the row's pool words (ceil(3 popc / pf), contiguous) into the
         // pose's shared row: independent loads, all in flight, instead of a
         // global load per sphere inside the chain
-        if (tid < np) {
-            mask = __ldcs(spi.mask + p0 + tid);
-            if (mask) {
-                const uint32_t n = ((uint32_t)(3 * __popcll(mask) + f.pf - 1) * rc) >> 16;
-                const uint32_t* src = spi.pool + __ldcs(spi.off + p0 + tid);
-                uint32_t* dst = sw + tid * WS;
-                for (uint32_t w = 0; w < n; ++w) dst[w] = __ldcs(src + w);
-            }
+        mask = __ldcs(spi.mask + p0 + pt);
+        if (mask) {
+            const uint32_t n = ((uint32_t)(3 * __popcll(mask) + f.pf - 1) * rc) >> 16;
+            const uint32_t* src = spi.pool + __ldcs(spi.off + p0 + pt);
+            uint32_t* dst = sw + pt * WS;
+            for (uint32_t w = 0; w < n; ++w) dst[w] = __ldcs(src + w);
         }
-    } else if (tid < np) {
-        const uint4* r4 = reinterpret_cast<const uint4*>(sw + tid * WS);
+    } else {
+        const uint4* r4 = reinterpret_cast<const uint4*>(sw + pt * WS);
         for (int g = 0; g < W / 4; ++g) {
             const uint4 v = r4[g];
             if (!(v.x | v.y | v.z | v.w)) continue;
@@ -119,15 +130,11 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
         }
     }
 
-    // compact the poses with a non-zero gradient so the chains below run in
-    // full warps (each pose's result is independent of the order)
-    // with the IKO pose cost every pose is active (its hand frame carries a
-    // force and a torque whatever its sphere gradients)
-    const bool pose_on = IKO && (ik.w_pos != 0.f || ik.w_rot != 0.f);
-    if (tid < np && (mask || pose_on)) {
+    if (mask || pose_on) {
         const int k = atomicAdd(&s_nact, 1);
-        s_act[k] = tid;
+        s_act[k] = (int16_t)pt;
         s_mask[k] = mask;
+    }
     }
     for (int i = tid; i < np * kJoints; i += kTile) sg[i] = 0.f;
     __syncthreads();
@@ -216,12 +223,13 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     }
     __syncthreads();
     // N2 bound cost: its gradient is per joint, for every pose
-    if (IKO && ik.w_bound != 0.f && tid < np)
-        for (int j = 0; j < kJoints; ++j) {
-            float dq;
-            ik_bound(sq[tid * kJoints + j], R.q_lo[j], R.q_hi[j], ik.w_bound, dq);
-            sg[tid * kJoints + j] += dq;
-        }
+    if (IKO && ik.w_bound != 0.f)
+        for (int pt = tid; pt < np; pt += kTile)
+            for (int j = 0; j < kJoints; ++j) {
+                float dq;
+                ik_bound(sq[pt * kJoints + j], R.q_lo[j], R.q_hi[j], ik.w_bound, dq);
+                sg[pt * kJoints + j] += dq;
+            }
     __syncthreads();
     // coalesced grad_q store (zero for poses without a gradient)
     for (int i = tid; i < np * kJoints; i += kTile) __stcs(grad_q + p0 * kJoints + i, sg[i]);
@@ -234,13 +242,30 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
                       const SparseIn* sparse, bool pdl) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
-    const size_t smem = sizeof(float4) * kMaxSpheres +
-                        sizeof(float) * kTile * kJoints +
-                        sizeof(uint32_t) * kTile * (W + 4) +
-                        sizeof(float) * kTile * kJoints;
+    // poses per CTA: the most (up to 4 per thread) whose tile keeps 4 CTAs
+    // per SM (the register bound) in shared memory
+    auto smem_of = [&](int t) {
+        return sizeof(float4) * kMaxSpheres + sizeof(float) * t * kJoints +
+               sizeof(uint32_t) * t * (W + 4) + sizeof(float) * t * kJoints;
+    };
+    const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < tp * W / 4
+    // (i rq) >> 20 = i / Q while i (rq Q - 2^20) < 2^20 (the excess stays below
+    // one quotient step)
+    auto rq_exact = [&](int t) {
+        const long long Q = W / 4, e = (long long)rq * Q - (1ll << 20);
+        return e >= 0 && (long long)t * Q * e < (1ll << 20);
+    };
+    // (small batches keep one pose per thread: more CTAs, shorter latency)
+    int tp = kTile;
+    for (int t = VAPR_BK_PPT * kTile; t > kTile && P >= (long long)t * 4 * 148; t /= 2)
+        if (smem_of(t) <= 56 * 1024 && rq_exact(t)) {
+            tp = t;
+            break;
+        }
+    if (!rq_exact(tp)) return cudaErrorInvalidValue;
+    const size_t smem = smem_of(tp);
     cudaError_t e = cudaSuccess;
     const uint32_t rc = 65536u / fgos.pf + 1u;
-    const uint32_t rq = (1u << 20) / (W / 4) + 1u;      // i / (W/4) for i < kTile * 39
     // SWAR masks of the format's fields: top bits, low t-1 bits; slot = (b+1)/t - 1
     uint32_t f_lo = 0u, f_hi = 0u;
     for (int j = 0; j < fgos.pf; ++j) {
@@ -249,7 +274,7 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
         f_lo |= (uint32_t)(((1ull << (fgos.t - 1)) - 1ull) << at);
     }
     const uint32_t rt = 65536u / fgos.t + 1u;
-    const long long grid = (P + kTile - 1) / kTile;
+    const long long grid = (P + tp - 1) / tp;
     const bool iko = ik && ik_on(*ik);
     const bool sp = fgos.kind == KIND_F16_IEEE;
     auto pick = [&](auto spr) {
@@ -263,7 +288,7 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     IkArgs none{};
     const SparseIn dense{};
     return launch_k(kern, dim3((unsigned)grid), dim3(kTile), smem, s, pdl, R, fgos, q, P, W, gos,
-                    grad_q, rc, rq, f_lo, f_hi, rt, iko ? *ik : none, sparse ? *sparse : dense);
+                    grad_q, rc, rq, f_lo, f_hi, rt, iko ? *ik : none, sparse ? *sparse : dense, tp);
 }
 
 }  // namespace vapr
