@@ -251,6 +251,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_MAX_WARPS          // cap on warps per (persistent, one per SM) CTA
 #define VAPR_MAX_WARPS 16
 #endif
+#ifndef VAPR_DEC_ASYNC           // tile rows: cp.async staging + in-place decode (1) or loads (0)
+#define VAPR_DEC_ASYNC 1
+#endif
 #ifndef VAPR_SMALL_WARPS          // small batches: tiles (of fewer poses) per SM to aim for
 #define VAPR_SMALL_WARPS 32
 #endif
@@ -680,10 +683,46 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             const int nq = int(r_hi - r_lo) * G.Qos;
             const uint4* src = os4 + r_lo * G.Qos;
             float* dst0 = rows + row_off * cs;
+#if VAPR_DEC_ASYNC
+            // the tile's packed rows land at the start of the row buffer by
+            // asynchronous 16-byte copies, all in flight at once (one memory
+            // latency per tile, no registers held); they are then decoded in
+            // place, in waves of rows from the last one down: FP32 row r starts
+            // at or after the end of packed row r - 1 (cs >= row words), so a
+            // wave's stores never reach the packed rows still to be read, and
+            // within a wave every lane reads before any lane writes
+            uint4* stage = reinterpret_cast<uint4*>(rows);
+            {
+                const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
+                for (int q = lane; q < nq; q += 32)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + 16u * q),
+                                 "l"(src + q)
+                                 : "memory");
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+            }
+            const int rpw = max(1, (32 * kDecLoads) / G.Qos);     // rows per wave
+#endif
             with_pf(fos.pf, [&](auto Pc) {
                 constexpr int PF = decltype(Pc)::value;
                 // kDecLoads 16-byte loads in flight per lane, then one word
                 // at a time through the decoder (few live temporaries)
+#if VAPR_DEC_ASYNC
+                for (int r1 = int(r_hi - r_lo); r1 > 0; r1 -= rpw) {
+                    const int qa = max(0, r1 - rpw) * G.Qos, qb = r1 * G.Qos;
+                    const int q0 = qa + lane;
+                    uint4 v[kDecLoads];
+#pragma unroll
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
+                        v[u] = (q < qb) ? stage[q] : make_uint4(0u, 0u, 0u, 0u);
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < kDecLoads; ++u) {
+                        const int q = q0 + 32 * u;
+                        if (q >= qb) break;
+#else
                 for (int q0 = lane; q0 < nq; q0 += 32 * kDecLoads) {
                     uint4 v[kDecLoads];
 #pragma unroll
@@ -695,6 +734,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     for (int u = 0; u < kDecLoads; ++u) {
                         const int q = q0 + 32 * u;
                         if (q >= nq) break;
+#endif
                         const int r = int((uint32_t(q) * G.rc_q) >> 20);
                         const int g = q - r * G.Qos;
                         float* d = dst0 + r * cs + 4 * PF * g;
@@ -721,6 +761,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                             }
                         }
                     }
+#if VAPR_DEC_ASYNC
+                    __syncwarp();
+#endif
                 }
             });
         }
