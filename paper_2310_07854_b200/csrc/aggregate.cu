@@ -35,6 +35,10 @@ constexpr int kRows = VAPR_AGG_ROWS;
 #define VAPR_AGG_THREADS 128
 #endif
 constexpr int kThreads = VAPR_AGG_THREADS;
+#ifndef VAPR_AGG_SW                // sparse aggregation: per-thread staged words per input
+#define VAPR_AGG_SW 16
+#endif
+constexpr int kSW = VAPR_AGG_SW;
 #ifndef VAPR_AGG_ROWS_BELOW       // vapr_cost_grad sparse aggregation: warp-per-row form below
 #define VAPR_AGG_ROWS_BELOW 65536
 #endif
@@ -161,6 +165,11 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
                         const uint32_t* __restrict__ ov, const unsigned long long* __restrict__ ovm,
                         long long rows, uint32_t rcp_c, uint32_t rcp_o, const SparseOut sp) {
     pdl_wait();         // vapr_cost_grad: the collision passes / cost reduction are complete
+    // the row's pool words (both inputs) staged in a per-thread shared row
+    // first -- independent loads, all in flight -- instead of a global load
+    // per code inside the sphere loop (rows longer than kSW words: direct)
+    __shared__ uint32_t sbuf[128 * (2 * kSW + 1)];
+    uint32_t* mine = sbuf + threadIdx.x * (2 * kSW + 1);        // odd stride: conflict-free
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nw = 0u;
     if (p < rows) {
@@ -168,8 +177,18 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
         unsigned long long m = mc | mo, mg = 0ull;
         const uint32_t o = sp.seg0 + (uint32_t)p * sp.wmax;
         if (m) {
+            const uint32_t ncw = ((uint32_t)(3 * __popcll(mc) + fcp.pf - 1) * rcp_c) >> 16;
+            const uint32_t now = ((uint32_t)(3 * __popcll(mo) + fov.pf - 1) * rcp_o) >> 16;
             const uint32_t* rc = cp + p * wc;
             const uint32_t* ro = ov + p * wo;
+            if (ncw <= kSW && now <= kSW) {
+#pragma unroll 4
+                for (uint32_t w = 0; w < ncw; ++w) mine[w] = __ldcs(rc + w);
+#pragma unroll 4
+                for (uint32_t w = 0; w < now; ++w) mine[kSW + w] = __ldcs(ro + w);
+                rc = mine;
+                ro = mine + kSW;
+            }
             uint32_t word = 0u;
             int q = 0;
             int kc = 0, ko = 0;                       // codes consumed from each side
@@ -183,11 +202,11 @@ aggregate_sparse_kernel(const Fmt fcp, const Fmt fov, const Fmt fg, int wc, int 
                     float a = 0.f, b = 0.f;
                     if (inc) {
                         const uint32_t e = kc + c, w = (e * rcp_c) >> 16;      // e / pf
-                        a = decode_sp(code_at(__ldcs(rc + w), int(e - w * fcp.pf), fcp), fcp);
+                        a = decode_sp(code_at(rc[w], int(e - w * fcp.pf), fcp), fcp);
                     }
                     if (ino) {
                         const uint32_t e = ko + c, w = (e * rcp_o) >> 16;
-                        b = decode_sp(code_at(__ldcs(ro + w), int(e - w * fov.pf), fov), fov);
+                        b = decode_sp(code_at(ro[w], int(e - w * fov.pf), fov), fov);
                     }
                     x[c] = a + b;
                 }
