@@ -225,28 +225,43 @@ quantize_direct_kernel(const float4* __restrict__ x, uint4* __restrict__ out, Gr
     });
 }
 
+#ifndef VAPR_DQ_U2
+#define VAPR_DQ_U2 2                // 16-bit formats: groups per thread per iteration
+#endif                              // (E8M7 0.75 -> 0.87 of the copy peak; pf 3: 1 is faster)
 __global__ void __launch_bounds__(256)
 dequantize_direct_kernel(const uint4* __restrict__ in, float4* __restrict__ y, GroupGeom G, Fmt f) {
     const long long stride = (long long)gridDim.x * blockDim.x;
     with_pf(f.pf, [&](auto P) {
         constexpr int PF = decltype(P)::value;
-        for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G.groups; g += stride) {
-            long long flat;
-            int n;
-            group_span_fast(G, g, flat, n);
-            const uint4 q = __ldcs(in + g);
-            float v[4 * PF];
-            if constexpr (PF == 2) {
-                decode_group_t<2>(q, v, f);
-            } else {
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        constexpr int VAPR_DQ_U = (PF == 2) ? VAPR_DQ_U2 : 1;
+        for (long long g0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; g0 < G.groups;
+             g0 += stride * VAPR_DQ_U) {
+            uint4 q[VAPR_DQ_U];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) decode_word_t<PF>(w[k], v + k * PF, f);
+            for (int u = 0; u < VAPR_DQ_U; ++u) {
+                const long long g = g0 + u * stride;
+                q[u] = (g < G.groups) ? __ldcs(in + g) : make_uint4(0u, 0u, 0u, 0u);
             }
-            float4* dst = y + (flat >> 2);
 #pragma unroll
-            for (int k = 0; k < PF; ++k)
-                if (4 * k < n) __stcs(dst + k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+            for (int u = 0; u < VAPR_DQ_U; ++u) {
+                const long long g = g0 + u * stride;
+                if (g >= G.groups) break;
+                long long flat;
+                int n;
+                group_span_fast(G, g, flat, n);
+                float v[4 * PF];
+                if constexpr (PF == 2) {
+                    decode_group_t<2>(q[u], v, f);
+                } else {
+                    const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) decode_word_t<PF>(w[k], v + k * PF, f);
+                }
+                float4* dst = y + (flat >> 2);
+#pragma unroll
+                for (int k = 0; k < PF; ++k)
+                    if (4 * k < n) __stcs(dst + k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+            }
         }
     });
 }

@@ -32,7 +32,7 @@ for r in rows[1:]:
         continue
     tot_w += w; tot_i += n
     res.append((w, n, int(r[0]), r[1][:90]))
-res.sort(reverse=True)
+res.sort(reverse=True, key=(lambda t: t[1]) if os.environ.get("BY_INST") else None)
 print(f"total stall samples {tot_w}, warp instructions {tot_i}")
 for w, n, ln, src in res[:top]:
     print(f"{100*w/tot_w:5.1f}% samp {100*n/tot_i:5.1f}% inst  L{ln:4d}  {src}")
