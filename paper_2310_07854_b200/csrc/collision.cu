@@ -1083,7 +1083,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
                                 VAPR_STAT(3, 1);
                                 VAPR_STAT(4, k1c - k0c);
-                                uint32_t wmk = 0u;
+                                // the four tests first (no shared-memory stores between
+                                // them, so their loads are all in flight), then the marks
+                                bool act[4];
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
                                     const int k = k0c + u;
@@ -1097,8 +1099,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                     // d2 >= fl(Rs^2) => phi <= 0 (self_pair's exact early-out);
                                     // the rare d2 within an ulp of Rs^2 is settled by self_pair
                                     // in the gather (an inactive marked pair contributes nothing)
-                                    if (k >= k1c || d2 >= Rs * Rs) continue;
-                                    const int pid = sgpid[k];
+                                    act[u] = k < k1c && d2 < Rs * Rs;
+                                }
+                                uint32_t wmk = 0u;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    if (!act[u]) continue;
+                                    const int pid = sgpid[k0c + u];
                                     atomicOr(pmask + p * PMW + (pid >> 5), 1u << (pid & 31));
                                     wmk |= 1u << (pid >> 5);
                                 }
