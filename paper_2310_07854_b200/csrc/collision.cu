@@ -6,13 +6,15 @@
 // c13-c17 (box SDF, smooth hinge, summed over cuboids / listed pairs; swept =
 // linear sub-samples with the exact gradient to both endpoints).
 //
-// One warp per tile of kTP = 15 consecutive poses, two lanes per pose (lane =
-// half * 16 + pose; lane 15 / 31: the halo pose p0 + 15), plus the halo rows
-// p0-1 and p0+15 for the swept samples (warps are independent: no CTA
-// barrier in the tile loop; the robot tables are staged once per CTA):
-//  1. load the packed rows (16-byte loads, all in flight) and decode them into
-//     an FP32 tile (odd row stride: pose-per-lane accesses are conflict-free);
-//     track the largest decoded coordinate;
+// One warp per tile of up to 16 consecutive poses, two lanes per pose (lane =
+// half * 16 + pose): kTP = 15 poses for the swept world pass, whose pose lane
+// 15 / 31 is the halo pose p0 + 15 and whose tile adds the halo rows p0-1 and
+// p0+15 for the swept samples; 16 for the self pass and the discrete world
+// pass (warps are independent: no CTA barrier in the tile loop; the robot
+// tables are staged once per CTA from a device image):
+//  1. stage the packed rows (cp.async, all 16-byte copies in flight) and
+//     decode them in place into an FP32 tile (odd row stride: pose-per-lane
+//     accesses are conflict-free); track the largest decoded coordinate;
 //  2. broadphase, 16 poses per instruction, the two lanes of a pose splitting
 //     its list.  The spheres of a link (or of a
 //     half-link group) lie in a ball around a reference sphere whose radius is
@@ -340,15 +342,16 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.tables = take(0, 16);
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
-    g.pmask = take(do_self ? 4u * kTP * g.pmw : 0u, 4);
-    g.pwm = take(do_self ? 4u * kTP : 0u, 4);
-    g.wm = take(do_world ? 4u * kTP * kLinks : 0u, 4);
-    g.pk0 = take(do_world ? 4u * kTP : 0u, 4);
+    // (a self-only pass has no halo pose: its tiles take all kPL pose lanes)
+    g.pmask = take(do_self ? 4u * kPL * g.pmw : 0u, 4);
+    g.pwm = take(do_self ? 4u * kPL : 0u, 4);
+    g.wm = take(do_world ? 4u * kPL * kLinks : 0u, 4);
+    g.pk0 = take(do_world ? 4u * kPL : 0u, 4);
     g.qi = take(2u * kQ, 2);
     g.qc = take((sparse == 2 ? 16u : sparse == 1 ? 8u : 4u) * kQ, 16);   // item results: codes + cost / cost
     // N4: each pose's world-live spheres, and the FP32 grad_out_spheres tile
-    g.gfw = take(fused ? 8u * kTP : 0u, 8);
-    g.gt = take(fused ? 4u * kTP * R.cols : 0u, 16);
+    g.gfw = take(fused ? 8u * kPL : 0u, 8);
+    g.gt = take(fused ? 4u * kPL * R.cols : 0u, 16);
     g.warp = take(0, 16);
     return g;
 }
@@ -499,8 +502,8 @@ __device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsi
     }
 }
 
-// One warp processes a tile of kTP consecutive poses, one pose per lane (the
-// arithmetic of every broadphase test runs for 32 poses per instruction, with
+// One warp processes a tile of up to 16 consecutive poses, two lanes per pose
+// (the arithmetic of every broadphase test runs for 16 poses per instruction, with
 // uniform loops and no index math); the sparse narrowphase work (live world
 // spheres, live group pairs, touched spheres) goes through warp work queues
 // so that every lane has an item.  Warps are independent: no CTA barrier in
@@ -583,7 +586,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                           float>::type;
     QcT* qc = reinterpret_cast<QcT*>(wb + G.qc);
     unsigned long long* gfw = reinterpret_cast<unsigned long long*>(wb + G.gfw);   // N4
-    float* gt = reinterpret_cast<float*>(wb + G.gt);                               // N4 [kTP][cols]
+    float* gt = reinterpret_cast<float*>(wb + G.gt);                               // N4 [kPL][cols]
 
     const int cs = G.cs;
     const long long P = (long long)a.B * a.H;
@@ -782,9 +785,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 for (int i = lane; i < np * G.Wov / 4; i += 32)
                     reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
-            if (lane < kTP) pwm[lane] = 0u;
+            if (lane < kPL) pwm[lane] = 0u;
         }
-        if (a.do_world && half == 0 && pl < kTP) pk0[pl] = k0;
+        if (a.do_world && half == 0) pk0[pl] = k0;
         __syncwarp();
 
         // Quantisation margin: a decoded coordinate y of an FK value x
@@ -967,7 +970,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 if constexpr (SPARSE) sr_cp.put(it & 63, r, fcp);
             });
             if (SPARSE && owner) sr_cp.finish(a.cp_mask + p0 + pl);
-            if (FUSED && half == 0 && pl < kTP) gfw[pl] = smask;
+            if (FUSED && half == 0) gfw[pl] = smask;
         }
 
         // ---- 3. self
@@ -1382,11 +1385,14 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // small batches: fewer poses per tile so that the tiles fill ~VAPR_SMALL_WARPS
     // warps per SM (a tile's latency is its warp's serial item list)
     {
-        const long long full = (P + kTP - 1) / kTP;
+        // only the swept world part needs the halo pose: otherwise kPL poses
+        // per tile
+        const int tmax = (a.do_world && a.swept) ? kTP : kPL;
+        const long long full = (P + tmax - 1) / tmax;
         const long long target = (long long)sms * VAPR_SMALL_WARPS;
-        a.tile_poses = kTP;
-        if (full < target) a.tile_poses = (int)std::max(1LL, std::min<long long>(kTP, (P + target - 1) / target));
-        if (const char* e = getenv("VAPR_TILE_POSES")) a.tile_poses = std::max(1, std::min(kTP, atoi(e)));
+        a.tile_poses = tmax;
+        if (full < target) a.tile_poses = (int)std::max(1LL, std::min<long long>(tmax, (P + target - 1) / target));
+        if (const char* e = getenv("VAPR_TILE_POSES")) a.tile_poses = std::max(1, std::min(tmax, atoi(e)));
     }
     const long long tiles = (P + a.tile_poses - 1) / a.tile_poses;
     a.n_tiles = tiles;

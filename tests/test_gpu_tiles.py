@@ -2,7 +2,8 @@
 warp tile (VAPR_TILE_POSES; the launcher picks fewer than 15 for small
 batches, and one-pose tiles spread the broadphase over the warp) change
 nothing -- cost, grad_q and every stored tensor are bit-identical for 1, 2,
-7 and 15 poses per tile, dense and sparse, swept and discrete."""
+7, 15 and 16 poses per tile (16: the passes without a halo pose -- self, and
+discrete world), dense, sparse and fused, swept and discrete."""
 import dataclasses
 import os
 
@@ -53,7 +54,7 @@ def test_tile_poses_invisible(vb, name, mode):
           "discrete": lambda: _discrete(config4(problems_per_env=1, seeds=2, H=16)),
           "config1": config1}[name]()
     ref = _run(wl, 15, mode == "sparse", mode == "fused")
-    for tp in (1, 2, 7):
+    for tp in (1, 2, 7, 16):
         got = _run(wl, tp, mode == "sparse", mode == "fused")
         for k, v in ref.items():
             a, b = np.asarray(v), np.asarray(got[k])
