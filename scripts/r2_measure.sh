@@ -33,8 +33,8 @@ for r in $O/*.ncu-rep; do
 done
 for L in 0 1; do
   NCU_LAUNCH=$L python scripts/ncu_regions.py $O/step_sparse43.ncu-rep collision_kernel collision.cu \
-      helpers:1-516 stage:517-650 decode:651-770 zero:771-804 world:805-972 self_bp:973-1024 \
-      self_np:1025-1112 self_grad:1113-1203 > $O/regions_sparse43_launch$L.txt 2>&1
+      helpers:1-519 stage:520-653 decode:654-773 zero:774-807 world:808-975 self_bp:976-1027 \
+      self_np:1028-1122 self_grad:1123-1213 > $O/regions_sparse43_launch$L.txt 2>&1
 done
 NCU_LAUNCH=1 python scripts/ncu_lines.py $O/step_sparse43.ncu-rep collision_kernel 40 > $O/lines_sparse43_self.txt 2>&1
 rm -f $O/step_dense43.ncu-rep $O/step_sparse32.ncu-rep $O/step_fused43.ncu-rep
