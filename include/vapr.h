@@ -283,7 +283,7 @@ vapr_status vapr_cost_grad(vapr_ctx *ctx, const float *q, const int32_t *world_i
 /* The same computation from HOST buffers: q_host [B, H, 7] in, grad_q_host
  * [B, H, 7] and cost_traj_host [B] (nullable) out, with the host<->device
  * copies pipelined against the compute.  The batch is split into n_chunks
- * contiguous trajectory ranges (0 = automatic: up to ~900k poses per chunk;
+ * contiguous trajectory ranges (0 = automatic: up to ~700k poses per chunk;
  * the first and last chunks are a quarter of the others, so the exposed
  * copies are short); chunk i's H2D copy, chunk i-1's compute and chunk i-2's
  * D2H copies run concurrently on two context-owned copy streams and `stream`.  Every output

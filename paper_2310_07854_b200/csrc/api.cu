@@ -1131,11 +1131,12 @@ vapr_status vapr_cost_grad_host(vapr_ctx* c, const float* q_host, const int32_t*
     CHECK(g.ok && pending_fault() == VAPR_OK, VAPR_ERR_CUDA);
     float* cpose = cost_pose_dev ? cost_pose_dev
                                  : reinterpret_cast<float*>(static_cast<char*>(workspace) + co);
-    // chunking: whole trajectories, up to ~900k poses per (full-size) chunk
-    // by default (measured on the 2.56M-pose bench workload: 3 chunks 6.2 ms,
-    // 4: 6.25, 6: 6.7, 8: 7.1, against a 5.24 ms device step)
+    // chunking: whole trajectories, up to ~700k poses per (full-size) chunk
+    // by default (measured on the 2.56M-pose bench workload against a 4.0 ms
+    // device step: 2 chunks 5.51 ms, 3: 5.03, 4: 4.92, 5: 4.99, 6: 5.16, 8:
+    // 5.55; round 1, against a 5.24 ms step, 3 was best)
     int nc = n_chunks;
-    if (nc == 0) nc = (int)std::max(1LL, std::min<long long>(16, (P + 899999) / 900000));
+    if (nc == 0) nc = (int)std::max(1LL, std::min<long long>(16, (P + 699999) / 700000));
     nc = std::min(nc, B);
     // chunk boundaries: the first and last chunks a quarter of the others,
     // so the only copies left exposed (the first upload, the last download)
