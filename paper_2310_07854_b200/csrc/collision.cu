@@ -256,6 +256,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_DEC_ASYNC           // tile rows: cp.async staging + in-place decode (1) or loads (0)
 #define VAPR_DEC_ASYNC 1
 #endif
+#ifndef VAPR_HALF_SM_TILES        // small-batch side-by-side passes below sms x warps x this tiles
+#define VAPR_HALF_SM_TILES 1
+#endif
 #ifndef VAPR_SMALL_WARPS          // small batches: tiles (of fewer poses) per SM to aim for
 #define VAPR_SMALL_WARPS 32
 #endif
@@ -1401,7 +1404,13 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // one CTA per tile over the SMs (latency: a lone SM's issue slots shared
     // by its 16 warps would serialise the few tiles there are)
     const long long need = (tiles + kGrab * nw - 1) / (kGrab * nw);
-    const long long spread = VAPR_SPREAD_SMALL ? std::min<long long>(tiles, sms) : need;
+    // the two passes of vapr_cost_grad (pdl != 0) on a small batch: each
+    // spreads over half of the SMs, so that they run side by side (one CTA
+    // fills an SM's shared memory: a full-width first pass would keep the
+    // second off every SM until its CTAs retire)
+    const long long sms_pass = (a.pdl != 0 && tiles < (long long)sms * nw * VAPR_HALF_SM_TILES)
+                                   ? std::max(1, sms / 2) : sms;
+    const long long spread = VAPR_SPREAD_SMALL ? std::min<long long>(tiles, sms_pass) : need;
     const long long grid = std::min<long long>(std::max(need, spread),
                                                (long long)sms * std::max(per_sm, 1));
 #ifdef VAPR_DEBUG_TAP
