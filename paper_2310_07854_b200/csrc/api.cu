@@ -28,6 +28,10 @@ struct vapr_ctx {
     int cull = 1;
     // vapr_cost_grad_host: copy streams and an event pool (created lazily)
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    // small batches: the per-trajectory cost reduction on a side stream,
+    // beside aggregation and BK (fork / join events)
+    cudaStream_t s_red = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> events;
     // collision tile-scheduler slots (device, kSchedSlots x {next, done}) and
     // the host-side slot cursor
@@ -53,6 +57,12 @@ struct vapr_ctx {
     bool goals_set = false;
 };
 
+#ifndef VAPR_SIDE_REDUCE           // small batches: cost reduction on a side stream
+#define VAPR_SIDE_REDUCE 1
+#endif
+#ifndef VAPR_SIDE_REDUCE_BELOW
+#define VAPR_SIDE_REDUCE_BELOW 65536
+#endif
 #ifndef VAPR_CHAIN_PDL             // vapr_cost_grad: reduce / aggregate / BK as programmatic dependents
 #define VAPR_CHAIN_PDL 0           // measured slower (bench step 4.39 -> 4.38 ms, config 1 / 2 71 / 68 ->
 #endif                             // 80 / 76 us; early triggers: per-env leg 5.7 -> 6.9 ms); FK -> self stays
@@ -254,6 +264,9 @@ vapr_status vapr_destroy(vapr_ctx* c) {
     for (cudaStream_t st : c->par)
         if (st) cudaStreamDestroy(st);
     if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_red) cudaStreamDestroy(c->s_red);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->s_out) cudaStreamDestroy(c->s_out);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     delete c;
@@ -1004,9 +1017,26 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     // waits for its predecessor at its start; measured runs with stage
     // events are plain launches)
     const bool pdl = VAPR_CHAIN_PDL && c->n_stage_ev == 0;
-    if (e == cudaSuccess)
+    // small batches (latency): the reduction needs only the collision passes,
+    // so it runs on a side stream beside aggregation and BK and joins at the end
+    bool side = VAPR_SIDE_REDUCE && P < VAPR_SIDE_REDUCE_BELOW && c->n_stage_ev == 0;
+    if (side && !c->s_red) {
+        if (cudaStreamCreateWithFlags(&c->s_red, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+            side = false;
+    }
+    if (e == cudaSuccess && side) {
+        e = cudaEventRecord(c->ev_fork, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_red, c->ev_fork, 0);
+        if (e == cudaSuccess)
+            e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, c->s_red,
+                                   self_cost, false);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_join, c->s_red);
+    } else if (e == cudaSuccess) {
         e = launch_traj_reduce(cpose + p0, nb, H, cost_traj ? cost_traj + b0 : nullptr, s, self_cost,
                                pdl);
+    }
     mark(3);
     if (e == cudaSuccess)
         e = c->sparse ? launch_aggregate_sparse(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
@@ -1019,6 +1049,10 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
                       iko ? &ik : nullptr, c->sparse ? &spi : nullptr, pdl);
+    if (side) {
+        const cudaError_t ej = cudaStreamWaitEvent(s, c->ev_join, 0);
+        if (e == cudaSuccess) e = ej;
+    }
     mark(5);
     return e;
 }
