@@ -389,7 +389,12 @@ def main():
         pass
     kp = prof.get("kernels", {}).get(dom, {}) if prof.get("formats") == args.formats and \
         prof.get("poses") == P else {}
+    # "bound" names the roofline the fraction is taken against (the path is
+    # HBM-shaped: bytes per pose, no dense contraction); "regime" what ncu
+    # measured the dominant kernel to be limited by (profiles/r2)
     roofline = {"bound": "hbm", "kernel": dom,
+                "regime": ("latency / occupancy (issue-active ~57 %, 15-16 warps per SM)"
+                           if dom == "collision" else "see limiter"),
                 "stage_calls": "the timed step's own launches (vapr_set_stage_events, "
                                f"{args.storage} storage)",
                 "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
