@@ -57,6 +57,12 @@ struct vapr_ctx {
     bool goals_set = false;
 };
 
+#ifndef VAPR_AGG_IN_BK             // small sparse batches: aggregation inside BK's CTAs
+#define VAPR_AGG_IN_BK 1
+#endif
+#ifndef VAPR_AGG_ROWS_BELOW_BK
+#define VAPR_AGG_ROWS_BELOW_BK 16384
+#endif
 #ifndef VAPR_SIDE_REDUCE           // small batches: cost reduction on a side stream
 #define VAPR_SIDE_REDUCE 1
 #endif
@@ -1038,7 +1044,25 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
                                pdl);
     }
     mark(3);
-    if (e == cudaSuccess)
+    // small sparse batches: the aggregation runs inside BK's CTAs (one launch
+    // fewer on the latency-bound path; the same rows, codes and layout)
+    const bool agg_in_bk = VAPR_AGG_IN_BK && c->sparse && !iko && P < VAPR_AGG_ROWS_BELOW_BK;
+    AggArgs ag{};
+    if (agg_in_bk) {
+        const Fmt& fc = c->dfmt[cps];
+        const Fmt& fo = c->dfmt[VAPR_OUT_VEC];
+        ag.fcp = fc;
+        ag.fov = fo;
+        ag.cp = cp;
+        ag.cpm = cp_mask;
+        ag.ov = ov;
+        ag.ovm = ov_mask;
+        ag.cols = cols;
+        ag.wc = (cols + fc.pf - 1) / fc.pf;
+        ag.wo = (cols + fo.pf - 1) / fo.pf;
+        ag.sp = spo;
+    }
+    if (e == cudaSuccess && !agg_in_bk)
         e = c->sparse ? launch_aggregate_sparse(c->dfmt[cps], c->dfmt[VAPR_OUT_VEC],
                                                 c->dfmt[VAPR_GRAD_OUT_SPHERES], cols, cp, cp_mask,
                                                 ov, ov_mask, P, spo, s, pdl)
@@ -1048,7 +1072,8 @@ cudaError_t enqueue_cost_grad(vapr_ctx* c, const float* q, const int32_t* world_
     mark(4);
     if (e == cudaSuccess)
         e = launch_bk(c->robot, c->dfmt[VAPR_GRAD_OUT_SPHERES], qc, P, gos, grad_q + p0 * kJoints, s,
-                      iko ? &ik : nullptr, c->sparse ? &spi : nullptr, pdl);
+                      iko ? &ik : nullptr, c->sparse ? &spi : nullptr, pdl,
+                      agg_in_bk ? &ag : nullptr);
     if (side) {
         const cudaError_t ej = cudaStreamWaitEvent(s, c->ev_join, 0);
         if (e == cudaSuccess) e = ej;

@@ -21,6 +21,7 @@
 // codes are 3k + c of it; no dense tile copy, no SWAR scan.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sparse.cuh"
 
 namespace vapr {
 
@@ -31,6 +32,7 @@ namespace {
 #endif
 constexpr int kTile = VAPR_BK_TILE;         // threads per CTA
 constexpr int kMaxTP = 4 * kTile;           // poses per CTA at most
+constexpr int kAggRows = 16;                // AGG: poses per CTA (the aggregation tile)
 
 // IKO: the N2 pose / bound terms; SP: the gradient slot is IEEE E5M10 (its
 // exponent-31 codes decode to inf / NaN, reading c41) -- a separate
@@ -45,12 +47,12 @@ constexpr int kMaxTP = 4 * kTile;           // poses per CTA at most
 #else
 #define VAPR_BK_BOUNDS __launch_bounds__(kTile)
 #endif
-template <bool IKO, bool SP, bool SPR>
+template <bool IKO, bool SP, bool SPR, bool AGG>
 __global__ void VAPR_BK_BOUNDS
 bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restrict__ q,
           long long P, int W, const uint32_t* __restrict__ gos, float* __restrict__ grad_q,
           uint32_t rc, uint32_t rq, uint32_t f_lo, uint32_t f_hi, uint32_t rt, const IkArgs ik,
-          const SparseIn spi, int tp) {
+          const SparseIn spi, int tp, const AggArgs ag) {
     // tp poses per CTA (a multiple of kTile): with about half of the poses
     // carrying a gradient, two poses per thread keep the compacted chains
     // on every warp instead of leaving half the CTA at the barrier
@@ -66,6 +68,46 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     pdl_wait();         // vapr_cost_grad: the aggregation's output is complete
     const long long p0 = (long long)blockIdx.x * tp;
     const int np = (int)min((long long)tp, P - p0);
+    if constexpr (AGG) {
+        // the CTA's rows of grad_out_spheres from closest_pt + out_vec (tp <=
+        // kAggRows): aggregate_sparse_rows_kernel's sums, codes and layout
+        __shared__ SparseTileSmem<kAggRows> asm_;
+        __shared__ uint32_t awbuf[(kTile / 32) * 3 * kMaxSpheres];
+        __shared__ unsigned long long amc[kAggRows], amo[kAggRows];
+        if ((int)threadIdx.x < np) {
+            amc[threadIdx.x] = __ldcs(ag.cpm + p0 + threadIdx.x);
+            amo[threadIdx.x] = __ldcs(ag.ovm + p0 + threadIdx.x);
+        }
+        __syncthreads();
+        const uint32_t rcp_c = 65536u / ag.fcp.pf + 1u, rcp_o = 65536u / ag.fov.pf + 1u;
+        emit_sparse_rows<kAggRows, kTile / 32>(
+            np, ag.cols / 3, f, ag.sp.rcp, asm_, awbuf, 3 * kMaxSpheres, p0,
+            ag.sp.seg0 + (uint32_t)p0 * ag.sp.wmax, ag.sp.mask, ag.sp.off, ag.sp.pool, ag.sp.used,
+            [&](int r, int s, uint32_t* c) {
+                const unsigned long long mc = amc[r], mo = amo[r], bit = 1ull << s;
+                if (!((mc | mo) & bit)) return;
+                const long long p = p0 + r;
+                float x[3];
+                const int kc = 3 * __popcll(mc & (bit - 1ull)), ko = 3 * __popcll(mo & (bit - 1ull));
+#pragma unroll
+                for (int q3 = 0; q3 < 3; ++q3) {
+                    float a = 0.f, b = 0.f;
+                    if (mc & bit) {
+                        const uint32_t e = kc + q3, w = (e * rcp_c) >> 16;
+                        a = decode_sp(code_at(__ldcs(ag.cp + p * ag.wc + w), int(e - w * ag.fcp.pf), ag.fcp),
+                                      ag.fcp);
+                    }
+                    if (mo & bit) {
+                        const uint32_t e = ko + q3, w = (e * rcp_o) >> 16;
+                        b = decode_sp(code_at(__ldcs(ag.ov + p * ag.wo + w), int(e - w * ag.fov.pf), ag.fov),
+                                      ag.fov);
+                    }
+                    x[q3] = a + b;
+                }
+                encode3(x[0], x[1], x[2], f, c);
+            });
+        __syncthreads();          // the rows above are read below (global, same CTA)
+    }
     const int tid = threadIdx.x;
     if (tid == 0) s_nact = 0;
 
@@ -239,7 +281,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
 
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s, const IkArgs* ik,
-                      const SparseIn* sparse, bool pdl) {
+                      const SparseIn* sparse, bool pdl, const AggArgs* agg) {
     if (P <= 0) return cudaSuccess;
     const int W = row_words_of(fgos, R.cols);
     // poses per CTA: the most (up to 4 per thread) whose tile keeps 4 CTAs
@@ -255,9 +297,10 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
         const long long Q = W / 4, e = (long long)rq * Q - (1ll << 20);
         return e >= 0 && (long long)t * Q * e < (1ll << 20);
     };
-    // (small batches keep one pose per thread: more CTAs, shorter latency)
-    int tp = kTile;
-    for (int t = VAPR_BK_PPT * kTile; t > kTile && P >= (long long)t * 4 * 148; t /= 2)
+    // (small batches keep one pose per thread: more CTAs, shorter latency;
+    // with the aggregation in front, kAggRows poses per CTA)
+    int tp = (agg && sparse) ? kAggRows : kTile;
+    for (int t = VAPR_BK_PPT * kTile; !agg && t > kTile && P >= (long long)t * 4 * 148; t /= 2)
         if (smem_of(t) <= 56 * 1024 && rq_exact(t)) {
             tp = t;
             break;
@@ -279,16 +322,26 @@ cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long l
     const bool sp = fgos.kind == KIND_F16_IEEE;
     auto pick = [&](auto spr) {
         constexpr bool S = decltype(spr)::value;
-        return iko ? (sp ? bk_kernel<true, true, S> : bk_kernel<true, false, S>)
-                   : (sp ? bk_kernel<false, true, S> : bk_kernel<false, false, S>);
+        return iko ? (sp ? bk_kernel<true, true, S, false> : bk_kernel<true, false, S, false>)
+                   : (sp ? bk_kernel<false, true, S, false> : bk_kernel<false, false, S, false>);
     };
     auto kern = sparse ? pick(IC<1>{}) : pick(IC<0>{});
+    AggArgs ag{};
+    if (agg && sparse && !iko) {
+        kern = sp ? bk_kernel<false, true, true, true> : bk_kernel<false, false, true, true>;
+        ag = *agg;
+        ag.sp.wmax = (uint32_t)((R.cols + fgos.pf - 1) / fgos.pf);
+        ag.sp.rcp = 65536u / fgos.pf + 1u;
+    } else if (agg) {
+        return cudaErrorInvalidValue;
+    }
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     IkArgs none{};
     const SparseIn dense{};
     return launch_k(kern, dim3((unsigned)grid), dim3(kTile), smem, s, pdl, R, fgos, q, P, W, gos,
-                    grad_q, rc, rq, f_lo, f_hi, rt, iko ? *ik : none, sparse ? *sparse : dense, tp);
+                    grad_q, rc, rq, f_lo, f_hi, rt, iko ? *ik : none, sparse ? *sparse : dense, tp,
+                    ag);
 }
 
 }  // namespace vapr

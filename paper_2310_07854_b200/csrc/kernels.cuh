@@ -146,11 +146,24 @@ cudaError_t launch_aggregate_sparse(const Fmt& fcp, const Fmt& fov, const Fmt& f
                                     const uint32_t* ov_pool, const unsigned long long* ovm,
                                     long long rows, const SparseOut& sparse, cudaStream_t s,
                                     bool pdl = false);
+// Small batches (sparse storage): the aggregation done by BK's own CTAs for
+// their poses first (aggregate_sparse_rows_kernel's arithmetic and layout),
+// then BK on the rows just written -- one launch fewer
+struct AggArgs {
+    Fmt fcp, fov;
+    const uint32_t* cp;        // closest_pt[_swept] pool (rows at p * wc)
+    const unsigned long long* cpm;
+    const uint32_t* ov;        // out_vec pool (rows at p * wo)
+    const unsigned long long* ovm;
+    int32_t cols, wc, wo;
+    SparseOut sp;              // grad_out_spheres (seg0 / mask / off of the launch's rows)
+};
 // sparse (nullable): read grad_out_spheres from the sparse form instead of gos
+// agg (nullable, with sparse): aggregate first (AggArgs)
 cudaError_t launch_bk(const RobotDev& R, const Fmt& fgos, const float* q, long long P,
                       const uint32_t* gos, float* grad_q, cudaStream_t s,
                       const IkArgs* ik = nullptr, const SparseIn* sparse = nullptr,
-                      bool pdl = false);
+                      bool pdl = false, const AggArgs* agg = nullptr);
 // N1 optimiser (lbfgs.cu)
 struct LbfgsScales {
     float s[32];
