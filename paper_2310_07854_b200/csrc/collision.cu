@@ -253,6 +253,9 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_MAX_WARPS          // cap on warps per (persistent, one per SM) CTA
 #define VAPR_MAX_WARPS 16
 #endif
+#ifndef VAPR_MAX_WARPS_W        // the same for the world-only pass
+#define VAPR_MAX_WARPS_W VAPR_MAX_WARPS
+#endif
 #ifndef VAPR_DEC_ASYNC           // tile rows: cp.async staging + in-place decode (1) or loads (0)
 #define VAPR_DEC_ASYNC 1
 #endif
@@ -292,7 +295,7 @@ struct Geo {
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
-    unsigned sr, rl, ref, pij, prec, gpid, grec, gpoff, slink, lrec, lgp, so, tables;
+    unsigned sr, rl, ref, slink, wtab, pij, prec, gpid, grec, gpoff, lrec, lgp, so, tables;
     // per-warp workspace (byte offsets from the warp's base), its size
     unsigned rows, pmask, pwm, wm, pk0, qi, qc, gfw, gt, warp;
 };
@@ -330,19 +333,21 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
         o += bytes;
         return at;
     };
+    // the world pass's tables first: a world-only pass stages only those
     g.sr = take(4u * kMaxSpheres, 4);
     g.rl = take(4u * 3 * kLinks, 4);
     g.ref = take(4u * 3 * kLinks, 4);
+    g.slink = take(kMaxSpheres, 1);
+    g.wtab = take(0, 16);
     g.pij = take(2u * g.npairs, 2);
     g.prec = take(8u * g.npairs, 8);
     g.gpid = take(2u * g.npairs, 2);
     g.grec = take(8u * kMaxGroupPairs, 8);
     g.gpoff = take(2u * (kMaxGroupPairs + 1), 2);
-    g.slink = take(kMaxSpheres, 1);
     g.lrec = take(8u * 32, 8);
     g.lgp = take(33, 1);
     g.so = take(fused ? 16u * kMaxSpheres : 0u, 16);      // N4: sphere offsets (BK)
-    g.tables = take(0, 16);
+    g.tables = (do_self || fused) ? take(0, 16) : g.wtab;
     o = 0;
     g.rows = take(4u * kTR * g.cs, 16);
     // (a self-only pass has no halo pose: its tiles take all kPL pose lanes)
@@ -518,8 +523,8 @@ __device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsi
 // more than 10 bits) rather than all three in one word.
 // FUSED (N4, VAPR_OPT_FUSED): FK in the tile fill, the gradients summed in a
 // shared FP32 tile, BK per pose at the tile's end (CollisionArgs::fused).
-template <bool SPARSE, bool SP_WIDE, bool FUSED>
-__global__ void __launch_bounds__(32 * VAPR_MAX_WARPS, 1)
+template <bool SPARSE, bool SP_WIDE, bool FUSED, int PASS>
+__global__ void __launch_bounds__(32 * (PASS == 1 ? VAPR_MAX_WARPS_W : VAPR_MAX_WARPS), 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
@@ -530,6 +535,11 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     // every other kernel of the chain lets its successor launch by exiting (an
     // early trigger would park the successor's CTAs on the SMs, blocked in
     // their wait, and take occupancy from the running grid)
+    // PASS 1 / 2: a world-only / self-only instantiation (the two passes of
+    // vapr_cost_grad: each kernel holds only its own code); 0: both from the
+    // runtime flags
+    const bool do_world = PASS == 1 || (PASS == 0 && a.do_world);
+    const bool do_self = PASS == 2 || (PASS == 0 && a.do_self);
     extern __shared__ float4 smem4[];
     char* base = reinterpret_cast<char*>(smem4);
     float* ssr = reinterpret_cast<float*>(base + G.sr);
@@ -555,11 +565,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
     {
         const uint4* img = a.tab_img;
         uint4* dst = reinterpret_cast<uint4*>(base);
-        for (int i = tid; i < a.tab_img_bytes / 16; i += blockDim.x) dst[i] = __ldg(img + i);
+        const int n16 = (do_self || FUSED) ? a.tab_img_bytes / 16 : (int)(G.wtab / 16);
+        for (int i = tid; i < n16; i += blockDim.x) dst[i] = __ldg(img + i);
         if (FUSED)
             for (int i = tid; i < G.S; i += blockDim.x) sso[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
         __syncthreads();
-        if (a.do_self) {
+        if (do_self) {
             for (int i = tid; i < G.npairs; i += blockDim.x)
                 sprec[i].y = __float_as_uint(__uint_as_float(sprec[i].y) + a.eta_s);
             for (int i = tid; i < G.nlp; i += blockDim.x)
@@ -610,7 +621,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
     const float inv_eta_w = 1.f / a.eta_w, hoe_w = 0.5f / a.eta_w;
     const float inv_eta_s = 1.f / a.eta_s, hoe_s = 0.5f / a.eta_s;
-    const bool swept = a.do_world && a.swept;
+    const bool swept = do_world && a.swept;
     const int nsub = swept ? a.sweep_steps : 0;
     const float inv_n1 = 1.f / float(nsub + 1);
     const uint4* os4 = reinterpret_cast<const uint4*>(a.os);
@@ -645,7 +656,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // subroutine on every lane of every tile)
             const long long b = (P < 0x7fffffffLL) ? (long long)((uint32_t)pg / (uint32_t)a.H) : pg / a.H;
             h = int(pg - b * a.H);
-            if (a.do_world) {
+            if (do_world) {
                 const int wi = __ldg(a.world_idx + b);
                 if (wi >= 0 && wi < Wd.n_worlds) {
                     k0 = __ldg(Wd.off + wi);
@@ -778,19 +789,19 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ORed in with atomics (__syncwarp orders the fill before every lane's
         // atomics); sparse: each pose's owner lane appends its codes to the
         // pose's pool segment and writes its bitmap
-        uint32_t* const cpg = (!SPARSE && !FUSED && a.do_world) ? a.cp + p0 * G.Wcp : nullptr;
-        uint32_t* const ovg = (!SPARSE && !FUSED && a.do_self) ? a.ov + p0 * G.Wov : nullptr;
-        if (!SPARSE && !FUSED && a.do_world)
+        uint32_t* const cpg = (!SPARSE && !FUSED && do_world) ? a.cp + p0 * G.Wcp : nullptr;
+        uint32_t* const ovg = (!SPARSE && !FUSED && do_self) ? a.ov + p0 * G.Wov : nullptr;
+        if (!SPARSE && !FUSED && do_world)
             for (int i = lane; i < np * G.Wcp / 4; i += 32)
                 reinterpret_cast<uint4*>(cpg)[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (a.do_self) {
+        if (do_self) {
             if (!SPARSE && !FUSED)
                 for (int i = lane; i < np * G.Wov / 4; i += 32)
                     reinterpret_cast<uint4*>(ovg)[i] = make_uint4(0u, 0u, 0u, 0u);
             for (int i = lane; i < np * PMW; i += 32) pmask[i] = 0u;
             if (lane < kPL) pwm[lane] = 0u;
         }
-        if (a.do_world && half == 0) pk0[pl] = k0;
+        if (do_world && half == 0) pk0[pl] = k0;
         __syncwarp();
 
         // Quantisation margin: a decoded coordinate y of an FK value x
@@ -810,7 +821,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
         // ---- 2. world
         float wcost = 0.f;
-        if (a.do_world) {
+        if (do_world) {
             // test ball per link: swept -> the segment (pose pg-1, pose pg),
             // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
             // (it bounds every sample on the segment); discrete -> pose pg
@@ -978,7 +989,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
         // ---- 3. self
         float scost = 0.f;
-        if (a.do_self) {
+        if (do_self) {
             // broadphase, per pose, two levels (the two lanes of a pose split
             // each list): the link pairs' balls, then the half-link group
             // pairs of the live link pairs; glo / ghi bit g <=> group pair g
@@ -1147,24 +1158,32 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const float* crow = rows + (p + 1) * cs;
                 const uint32_t* pm = pmask + p * PMW;
                 float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
-                // the pose's active pairs in id order, those with sphere s
+                // the active partners of sphere s (a sphere's pairs in id
+                // order are its partners in ascending order: (t, s) for t < s,
+                // then (s, t)), collected first so that the pair evaluations
+                // below run together on the warp's lanes rather than one
+                // lane at a time inside the scan of the pose's pairs
+                unsigned long long part = 0ull;
                 for (uint32_t wmk = pwm[p]; wmk; wmk &= wmk - 1) {
                     const int wd = __ffs(wmk) - 1;
                     for (uint32_t m = pm[wd]; m; m &= m - 1) {
-                        const int pid = (wd << 5) + __ffs(m) - 1;
-                        const int i = spij[pid] & 0xff, j = spij[pid] >> 8;
-                        if (i != s && j != s) continue;
-                        float vx, vy, vz, c;
-                        // always active here (same test as the narrowphase that marked it)
-                        if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy,
-                                       vz, c))
-                            continue;
-                        const float sg = (i == s) ? -1.f : 1.f;
-                        gx = fmaf(sg, vx, gx);
-                        gy = fmaf(sg, vy, gy);
-                        gz = fmaf(sg, vz, gz);
-                        if (i == s) c_lead += c;
+                        const int ij = spij[(wd << 5) + __ffs(m) - 1];
+                        const int i = ij & 0xff, j = ij >> 8;
+                        part |= (i == s ? 1ull << j : 0ull) | (j == s ? 1ull << i : 0ull);
                     }
+                }
+                for (; part; part &= part - 1) {
+                    const int t = __ffsll((long long)part) - 1;
+                    const int i = min(s, t), j = max(s, t);
+                    float vx, vy, vz, c;
+                    // always active here (same test as the narrowphase that marked it)
+                    if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
+                        continue;
+                    const float sg = (i == s) ? -1.f : 1.f;
+                    gx = fmaf(sg, vx, gx);
+                    gy = fmaf(sg, vy, gy);
+                    gz = fmaf(sg, vz, gz);
+                    if (i == s) c_lead += c;
                 }
                 uint32_t* orow = SPARSE ? nullptr : ovg + p * G.Wov;
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
@@ -1375,12 +1394,18 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // as many warps per CTA as shared memory holds (the tables are staged
     // once per CTA), at most VAPR_MAX_WARPS (16); one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
-    nw = std::min(nw, VAPR_MAX_WARPS);
+    const int pass = (a.do_world && !a.do_self) ? 1 : (!a.do_world && a.do_self) ? 2 : 0;
+    nw = std::min(nw, (pass == 1 && !fused) ? VAPR_MAX_WARPS_W : VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
-    auto kern = fused ? collision_kernel<false, false, true>
-                : !sparse ? collision_kernel<false, false, false>
-                          : (wide ? collision_kernel<true, true, false> : collision_kernel<true, false, false>);
+    auto pick = [&](auto Pc) {
+        constexpr int PS = decltype(Pc)::value;
+        return !sparse ? collision_kernel<false, false, false, PS>
+                       : (wide ? collision_kernel<true, true, false, PS> : collision_kernel<true, false, false, PS>);
+    };
+    auto kern = fused ? collision_kernel<false, false, true, 0>
+                : pass == 1 ? pick(std::integral_constant<int, 1>{})
+                : pass == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
