@@ -148,8 +148,21 @@ struct SparseRow {
     }
     // append one sphere's codes (the owner, in ascending sphere order)
     __device__ __forceinline__ void put(int s, const float2& r, const Fmt& f) {
+        // the three codes as one block (t <= 10: pf >= 3, so they span at
+        // most two words); the word's bits above pf * t stay zero
         const uint32_t w = __float_as_uint(r.x);
-        put3(s, w & f.mask, (w >> f.t) & f.mask, (w >> (2 * f.t)) & f.mask, f);
+        if (!w) return;
+        mask |= 1ull << s;
+        const uint32_t used = (f.pf * f.t >= 32) ? ~0u : ((1u << (f.pf * f.t)) - 1u);
+        word |= (w << (q * f.t)) & used;
+        const int room = f.pf - q;
+        if (room > 3) {
+            q += 3;
+        } else {
+            row[nw++] = word;
+            word = (room == 3) ? 0u : (w >> (room * f.t));
+            q = 3 - room;
+        }
     }
     __device__ __forceinline__ void put(int s, const float4& r, const Fmt& f) {
         put3(s, __float_as_uint(r.x), __float_as_uint(r.y), __float_as_uint(r.z), f);
