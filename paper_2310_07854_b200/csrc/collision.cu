@@ -41,6 +41,7 @@
 // without culling, so VAPR_OPT_CULL on and off give bit-identical results
 // (tests/test_gpu_parity.py::test_cull_is_exact).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -362,7 +363,8 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.so = take(fused ? 16u * kMaxSpheres : 0u, 16);      // N4: sphere offsets (BK)
     g.tables = (do_self || fused) ? take(0, 16) : g.wtab;
     o = 0;
-    g.rows = take(4u * kTR * g.cs, 16);
+    // (the self-only pass has no halo row 0: kPL rows, see `rows` in the kernel)
+    g.rows = take(4u * (do_world ? kTR : kPL) * g.cs, 16);
     // (a self-only pass has no halo pose: its tiles take all kPL pose lanes)
     g.pmask = take(do_self ? 4u * kPL * g.pmw : 0u, 4);
     g.pwm = take(do_self ? 4u * kPL : 0u, 4);
@@ -602,7 +604,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
     // ---- the warp's workspace
     char* wb = base + G.tables + (unsigned)warp * G.warp;
-    float* rows = reinterpret_cast<float*>(wb + G.rows);
+    // tile row r at rows + r * cs (a pass without the world part allocates
+    // no row 0: its tiles use rows 1 .. kPL)
+    float* rows = reinterpret_cast<float*>(wb + G.rows) - (do_world ? 0 : G.cs);
     uint32_t* pmask = reinterpret_cast<uint32_t*>(wb + G.pmask);
     uint32_t* pwm = reinterpret_cast<uint32_t*>(wb + G.pwm);
     uint32_t* wm = reinterpret_cast<uint32_t*>(wb + G.wm);
@@ -721,7 +725,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // at or after the end of packed row r - 1 (cs >= row words), so a
             // wave's stores never reach the packed rows still to be read, and
             // within a wave every lane reads before any lane writes
-            uint4* stage = reinterpret_cast<uint4*>(rows);
+            uint4* stage = reinterpret_cast<uint4*>(wb + G.rows);   // (16-byte aligned, at or before dst0)
             {
                 const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
                 for (int q = lane; q < nq; q += 32)
@@ -1411,6 +1415,9 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     nw = std::min(nw, (pass == 1 && !fused) ? VAPR_MAX_WARPS_W : VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
+    if (getenv("VAPR_DEBUG_LAUNCH"))
+        fprintf(stderr, "collision pass %d: %d warps/CTA, tables %u B, %u B/warp, smem %zu B\n", pass, nw,
+                G.tables, G.warp, smem);
     auto pick = [&](auto Pc) {
         constexpr int PS = decltype(Pc)::value;
         return !sparse ? collision_kernel<false, false, false, PS>
