@@ -1041,20 +1041,9 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         else ghi |= 1ull << (g - 64);
                     }
             }
-            static_assert(kLPP == 2, "the exchange below assumes two lanes per pose");
-            if (wide) {
-                auto or64 = [](unsigned long long v) {
-                    const uint32_t l = __reduce_or_sync(0xffffffffu, (uint32_t)v);
-                    const uint32_t h = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
-                    return (unsigned long long)l | ((unsigned long long)h << 32);
-                };
-                glo = or64(glo);
-                ghi = or64(ghi);
-            } else {
-                glo |= __shfl_xor_sync(0xffffffffu, glo, kPL);
-                ghi |= __shfl_xor_sync(0xffffffffu, ghi, kPL);
-            }
-            if (!owner) glo = ghi = 0ull;
+            // each lane lists the live group pairs it found itself (the lanes
+            // of a pose tested disjoint ones; the marks below do not depend
+            // on the order of the entries)
             VAPR_STAT(2, __popcll(glo) + __popcll(ghi));
             // narrowphase: the live (pose, group pair) entries are listed, each
             // expanded into chunks of <= 4 candidate pairs, one chunk per lane
@@ -1083,7 +1072,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                             bit = 63 + __ffsll((long long)ghi);
                             ghi &= ghi - 1;
                         }
-                        qi[cur - win] = (uint16_t)((pl << 7) | bit);
+                        qi[cur - win] = (uint16_t)(((wide ? 0 : pl) << 7) | bit);
                         ++cur;
                     }
                     __syncwarp();
