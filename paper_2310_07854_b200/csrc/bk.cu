@@ -114,6 +114,7 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
     // sphere offsets are indexed per lane (by each pose's non-zero spheres):
     // stage them in shared memory instead of the serialising constant bank
     for (int i = tid; i < R.n_spheres; i += kTile) so[i] = make_float4(R.sx[i], R.sy[i], R.sz[i], 0.f);
+#pragma unroll 4
     for (int i = tid; i < np * kJoints; i += kTile) sq[i] = __ldcs(q + p0 * kJoints + i);
     __syncthreads();
     if (!SPR) {
@@ -149,7 +150,15 @@ bk_kernel(const __grid_constant__ RobotDev R, const Fmt f, const float* __restri
             const uint32_t n = ((uint32_t)(3 * __popcll(mask) + f.pf - 1) * rc) >> 16;
             const uint32_t* src = spi.pool + __ldcs(spi.off + p0 + pt);
             uint32_t* dst = sw + pt * WS;
-            for (uint32_t w = 0; w < n; ++w) dst[w] = __ldcs(src + w);
+            // four loads in flight at a time
+            for (uint32_t w = 0; w < n; w += 4) {
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (w + u < n) ? __ldcs(src + w + u) : 0u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (w + u < n) dst[w + u] = v[u];
+            }
         }
     } else {
         const uint4* r4 = reinterpret_cast<const uint4*>(sw + pt * WS);
