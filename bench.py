@@ -393,7 +393,7 @@ def main():
     # HBM-shaped: bytes per pose, no dense contraction); "regime" what ncu
     # measured the dominant kernel to be limited by (profiles/r2)
     roofline = {"bound": "hbm", "kernel": dom,
-                "regime": ("latency / occupancy (issue-active ~57 %, 15-16 warps per SM)"
+                "regime": ("latency / occupancy (issue-active ~60 %, 16 warps per SM per pass)"
                            if dom == "collision" else "see limiter"),
                 "stage_calls": "the timed step's own launches (vapr_set_stage_events, "
                                f"{args.storage} storage)",

@@ -76,17 +76,18 @@ for st, e in out["kernels"].items():
                   "warp_instructions": [l["warp_instructions"] for l in L],
                   "threads_per_instruction": [l["threads_per_instruction"] for l in L]}
 LIMITER = {
-    "collision": "latency / occupancy: 15-16 warps per SM (128 registers, one CTA per SM, shared "
-                 "memory bound), ~51-55 % issue-active, 20 of 32 threads per instruction, top stalls "
-                 "wait and short scoreboard (self pass) / long scoreboard (world pass), 70-111 M "
-                 "shared-memory bank conflicts per pass; DRAM traffic = out_spheres read twice + "
-                 "the sparse outputs",
+    "collision": "latency / occupancy: two passes, each 16 warps per SM (one CTA per SM; world "
+                 "pass register-bound at 128, self pass shared-memory bound at 13.6 KB per warp), "
+                 "58-61 % issue-active, 21-23 of 32 threads per instruction, top stalls wait and "
+                 "short scoreboard; DRAM traffic = out_spheres read by both passes + the sparse "
+                 "outputs (profiles/r2/collision_regions_*.txt)",
     "fk": "instruction issue: ~88 % issue-active at 40 warps per SM, 31.6 of 32 threads per "
           "instruction",
     "aggregate": "divergence: a thread per row over the set spheres (10.7 of 32 threads per "
                  "instruction), 67 % issue-active",
-    "bk": "barrier / occupancy: 16 warps per SM (117 registers), top stall the CTA barrier "
-          "(compaction of the poses with a gradient), 16.5 of 32 threads per instruction",
+    "bk": "latency / occupancy: 36 % issue-active, 18 % warps active, top stalls long "
+          "scoreboard and the CTA barrier (compaction of the poses with a gradient), 16.7 of "
+          "32 threads per instruction",
     "reduce": "memory latency (a thread per trajectory)",
 }
 for st, e in out["kernels"].items():

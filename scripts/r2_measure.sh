@@ -31,11 +31,12 @@ for r in $O/*.ncu-rep; do
   python scripts/ncu_summary.py $r > $b.summary.txt 2>&1
   ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
 done
+# the collision passes' per-SASS-instruction source pages (self = launch 0,
+# world = launch 1 of the collision kernels), mapped to source lines here
+# with scripts/sass_line_map.py and the same build's cubin
 for L in 0 1; do
-  NCU_LAUNCH=$L python scripts/ncu_regions.py $O/step_sparse43.ncu-rep collision_kernel collision.cu \
-      helpers:1-519 stage:520-653 decode:654-773 zero:774-807 world:808-975 self_bp:976-1027 \
-      self_np:1028-1122 self_grad:1123-1213 > $O/regions_sparse43_launch$L.txt 2>&1
+  ncu -i $O/step_sparse43.ncu-rep --page source --csv -k regex:collision --launch-skip $L --launch-count 1 \
+      --print-source sass > $O/sass_collision_$L.csv 2>/dev/null
 done
-NCU_LAUNCH=1 python scripts/ncu_lines.py $O/step_sparse43.ncu-rep collision_kernel 40 > $O/lines_sparse43_self.txt 2>&1
 rm -f $O/step_dense43.ncu-rep $O/step_sparse32.ncu-rep $O/step_fused43.ncu-rep
 du -sh $O

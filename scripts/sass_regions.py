@@ -1,0 +1,39 @@
+"""Region table (warp instructions, stall samples, threads per instruction)
+of a collision pass from the per-line output of scripts/sass_line_map.py,
+over the source-line ranges of csrc/collision.cu at the measured tree.
+
+    python scripts/sass_regions.py lines.txt
+"""
+import re
+import sys
+from collections import defaultdict
+
+# (name, first line, last line) of collision.cu at commit time of profiles/r2
+REGIONS = [("world_term", 66, 130), ("sparse_row", 131, 193), ("or_code3", 194, 214),
+           ("self_pair", 215, 260), ("warp_queue", 390, 450), ("kernel head", 541, 684),
+           ("tile stage+decode", 685, 823), ("margin+zero", 824, 838), ("world broadphase", 839, 922),
+           ("world items", 923, 1006), ("self broadphase", 1007, 1047), ("self narrowphase", 1048, 1142),
+           ("self touched", 1143, 1159), ("self gradients", 1160, 1230), ("tile tail", 1231, 1265)]
+acc = defaultdict(lambda: [0.0, 0.0, 0.0])
+head = ""
+for l in open(sys.argv[1]):
+    if l.startswith("total"):
+        head = l.strip()
+    m = re.match(r"\s*(\S+):(-?\d+)\s+inst\s+([\d.]+)%\s+samp\s+([\d.]+)%\s+thr/inst\s+([\d.]+)", l)
+    if not m:
+        continue
+    f, ln, ip, sp, thr = m.group(1), int(m.group(2)), float(m.group(3)), float(m.group(4)), float(m.group(5))
+    name = "(other) " + f
+    if f == "collision.cu":
+        name = "(other) collision.cu"
+        for n, a, b in REGIONS:
+            if a <= ln <= b:
+                name = n
+    acc[name][0] += ip
+    acc[name][1] += sp
+    acc[name][2] += ip * thr
+print(head)
+print(f"{'region':>28} {'warp-inst %':>11} {'samples %':>10} {'threads/inst':>12}")
+for k, v in sorted(acc.items(), key=lambda kv: -kv[1][0]):
+    if v[0] >= 0.3:
+        print(f"{k:>28} {v[0]:11.2f} {v[1]:10.2f} {v[2] / max(v[0], 1e-9):12.1f}")
