@@ -165,7 +165,16 @@ dequantize_aligned_kernel(const uint4* __restrict__ in, float4* __restrict__ y, 
     const long long nw = (long long)gridDim.x * kAWarps;
     with_pf(f.pf, [&](auto P) {
         constexpr int PF = decltype(P)::value;
-        for (long long g0 = ((long long)blockIdx.x * kAWarps + warp) * 32; g0 < G.groups; g0 += nw * 32) {
+        // the next span's packed group is loaded one iteration ahead (its
+        // latency overlaps this span's decode and stores)
+        long long g0 = ((long long)blockIdx.x * kAWarps + warp) * 32;
+        uint4 qn = (g0 + lane < G.groups) ? __ldcs(in + g0 + lane) : make_uint4(0u, 0u, 0u, 0u);
+        for (; g0 < G.groups; g0 += nw * 32) {
+            const uint4 q = qn;
+            {
+                const long long gn = g0 + nw * 32 + lane;
+                if (gn < G.groups) qn = __ldcs(in + gn);
+            }
             long long flat0, flat_last, flat;
             int n0, nl, n;
             group_span_fast(G, g0, flat0, n0);
@@ -175,7 +184,6 @@ dequantize_aligned_kernel(const uint4* __restrict__ in, float4* __restrict__ y, 
             const long long g = g0 + lane;
             if (g < G.groups) {
                 group_span_fast(G, g, flat, n);
-                const uint4 q = __ldcs(in + g);
                 float v[4 * PF];
                 if constexpr (PF == 2) {
                     decode_group_t<2>(q, v, f);
@@ -225,6 +233,9 @@ quantize_direct_kernel(const float4* __restrict__ x, uint4* __restrict__ out, Gr
     });
 }
 
+#ifndef VAPR_DQ_DIRECT_MAXPF      // dequantise: formats with pf up to this use the direct kernel
+#define VAPR_DQ_DIRECT_MAXPF 2
+#endif
 #ifndef VAPR_DQ_U2
 #define VAPR_DQ_U2 2                // 16-bit formats: groups per thread per iteration
 #endif                              // (E8M7 0.75 -> 0.87 of the copy peak; pf 3: 1 is faster)
@@ -302,7 +313,7 @@ cudaError_t launch_dequantize(const Fmt& f, const uint32_t* packed, size_t rows,
     if (cols % 4 == 0) {
         if (f.kind == KIND_IDENTITY)
             return cudaMemcpyAsync(y, packed, sizeof(float) * rows * cols, cudaMemcpyDeviceToDevice, s);
-        if (f.pf <= 3) {
+        if (f.pf <= VAPR_DQ_DIRECT_MAXPF) {
             const long long blocks = std::min<long long>((G.groups + 255) / 256, (long long)sms * 16);
             dequantize_direct_kernel<<<(unsigned)std::max(1LL, blocks), 256, 0, s>>>(
                 reinterpret_cast<const uint4*>(packed), reinterpret_cast<float4*>(y), G, f);
