@@ -210,13 +210,46 @@ __device__ __forceinline__ void or_code3(uint32_t* row, int e, float vx, float v
     if (acc) atomicOr(row + cw, acc);
 }
 
+// Tile-row coordinate access (byte offset 12 s of sphere s in an FP32 row):
+// the decoded FP32 rows, or (H16, the self pass with E5M10 out_spheres) the
+// staged E5M10 codes themselves -- 16-bit rows, half the shared memory, more
+// warps per SM; every E5M10 value is an f16 value except the exponent-31
+// codes (finite in the all-finite reading, inf / NaN to the hardware
+// conversion), so a tile holding one (gen) reads through the generic decoder.
+template <bool H16, bool GEN = false>
+struct RowView {
+    const Fmt* f;
+    __device__ __forceinline__ float h(uint16_t c) const {
+        if constexpr (GEN) return decode(c, *f);
+        float x;
+        asm("cvt.f32.f16 %0, %1;" : "=f"(x) : "h"(c));
+        return x;
+    }
+    __device__ __forceinline__ void c3(const char* rb, uint32_t off12, float& x, float& y, float& z) const {
+        if constexpr (H16) {
+            const uint16_t* p = reinterpret_cast<const uint16_t*>(rb + (off12 >> 1));
+            x = h(p[0]);
+            y = h(p[1]);
+            z = h(p[2]);
+        } else {
+            const float* p = reinterpret_cast<const float*>(rb + off12);
+            x = p[0];
+            y = p[1];
+            z = p[2];
+        }
+    }
+};
+
 // Self pair (i, j), i < j: false when inactive; else the gradient
 // contribution v (d cost / d c_i = -v, d cost / d c_j = +v) and the cost w h.
-__device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const float* sr,
+template <class RV>
+__device__ __forceinline__ bool self_pair(const RV& rv, const char* rb, int i, int j, const float* sr,
                                           float eta, float inv_eta, float hoe, float w, float& vx,
                                           float& vy, float& vz, float& cost) {
-    const float dx = crow[3 * i] - crow[3 * j], dy = crow[3 * i + 1] - crow[3 * j + 1],
-                dz = crow[3 * i + 2] - crow[3 * j + 2];
+    float xi, yi, zi, xj, yj, zj;
+    rv.c3(rb, 12u * i, xi, yi, zi);
+    rv.c3(rb, 12u * j, xj, yj, zj);
+    const float dx = xi - xj, dy = yi - yj, dz = zi - zj;
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float Rs = sr[i] + sr[j] + eta;
     // sqrt(fl(Rs^2)) rounds back to Rs and sqrt is monotone, so d2 >= fl(Rs^2)
@@ -270,6 +303,12 @@ __device__ __forceinline__ bool self_pair(const float* crow, int i, int j, const
 #ifndef VAPR_MAX_WARPS_W        // the same for the world-only pass
 #define VAPR_MAX_WARPS_W VAPR_MAX_WARPS
 #endif
+#ifndef VAPR_H16                 // self pass: 16-bit tile rows for E5M10 out_spheres
+#define VAPR_H16 1
+#endif
+#ifndef VAPR_MAX_WARPS_H        // the self pass with 16-bit tile rows (its kernel fits 96 registers)
+#define VAPR_MAX_WARPS_H 26
+#endif
 #ifndef VAPR_DEC_ASYNC           // tile rows: cp.async staging + in-place decode (1) or loads (0)
 #define VAPR_DEC_ASYNC 1
 #endif
@@ -307,6 +346,8 @@ struct Geo {
     int ngp, npairs, nlp, S;
     uint32_t rc_cp, rc_ov;         // e / pf reciprocals (16-bit fixed point)
     uint32_t rc_q;                 // q / Qos reciprocal (20-bit fixed point)
+    int n8;                        // H16: 8-byte chunks per staged E5M10 row
+    uint32_t rc_h;                 // H16: q / n8 reciprocal (20-bit fixed point)
     unsigned long long lmask[kLinks];   // spheres of each link
     // CTA tables (byte offsets from the start of dynamic shared memory)
     unsigned sr, rl, ref, slink, wtab, pij, prec, gpid, grec, gpoff, lrec, lgp, so, tables;
@@ -315,7 +356,7 @@ struct Geo {
 };
 
 Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, int do_world,
-             int do_self, int sparse, int fused = 0) {
+             int do_self, int sparse, int fused = 0, int h16 = 0) {
     Geo g{};
     g.Wos = row_words_of(fos, R.cols);
     g.Wcp = do_world ? row_words_of(fcp, R.cols) : 0;
@@ -325,6 +366,19 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.Qos = g.Wos / 4;
     int cs = std::max(R.cols, g.Wos * fos.pf);
     g.cs = cs | 1;
+    if (h16) {
+        // 16-bit rows (self-only pass, E5M10): the row's (cols + 1) / 2 words at
+        // a stride of 2 mod 4 words -- 8-byte aligned rows (8-byte cp.async),
+        // and lane-per-pose reads of 16 rows on 16 distinct banks
+        const int w16 = (R.cols + 1) / 2;
+        int st = w16;
+        while (st % 4 != 2) ++st;
+        g.cs = st;
+        g.n8 = (w16 + 1) / 2;
+        g.rc_h = (1u << 20) / (uint32_t)g.n8 + 1u;
+        for (int q = 0; q < kPL * g.n8; ++q)
+            if (int((uint32_t(q) * g.rc_h) >> 20) != q / g.n8) g.rc_h = 0;
+    }
     g.pmw = (R.n_pairs + 31) >> 5;
     g.ngp = R.lp_gp_off[R.n_link_pairs];
     g.npairs = R.n_pairs;
@@ -364,7 +418,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
     g.tables = (do_self || fused) ? take(0, 16) : g.wtab;
     o = 0;
     // (the self-only pass has no halo row 0: kPL rows, see `rows` in the kernel)
-    g.rows = take(4u * (do_world ? kTR : kPL) * g.cs, 16);
+    g.rows = take(4u * (do_world ? kTR : kPL) * g.cs, 16);   // (h16: words of 2 codes)
     // (a self-only pass has no halo pose: its tiles take all kPL pose lanes)
     g.pmask = take(do_self ? 4u * kPL * g.pmw : 0u, 4);
     g.pwm = take(do_self ? 4u * kPL : 0u, 4);
@@ -538,8 +592,8 @@ __device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsi
 // more than 10 bits) rather than all three in one word.
 // FUSED (N4, VAPR_OPT_FUSED): FK in the tile fill, the gradients summed in a
 // shared FP32 tile, BK per pose at the tile's end (CollisionArgs::fused).
-template <bool SPARSE, bool SP_WIDE, bool FUSED, int PASS>
-__global__ void __launch_bounds__(32 * (PASS == 1 ? VAPR_MAX_WARPS_W : VAPR_MAX_WARPS), 1)
+template <bool SPARSE, bool SP_WIDE, bool FUSED, int PASS, bool H16 = false>
+__global__ void __launch_bounds__(32 * (PASS == 1 ? VAPR_MAX_WARPS_W : H16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS), 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
@@ -684,6 +738,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 
         // ---- 1. load and decode the tile rows (16-byte loads, all in flight)
         float amax = 0.f;
+        bool gen16 = false;             // H16: the tile holds an exponent-31 code
         if constexpr (FUSED) {
             // N4: the tile rows from FK, one lane per row (<= kTR of the 32),
             // every coordinate quantise->dequantised with the out_spheres
@@ -713,6 +768,36 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     }
                 }
             }
+        } else if constexpr (H16) {
+            // the E5M10 codes are the tile: 8-byte asynchronous copies into
+            // 16-bit rows, then one pass over the words for the largest code
+            // magnitude (|x| is monotone in it) and exponent-31 codes
+            uint32_t* hr = reinterpret_cast<uint32_t*>(wb + G.rows);
+            const int nr = int(r_hi - r_lo), n8 = G.n8, nq = nr * n8;
+            {
+                const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(hr);
+                const char* src = reinterpret_cast<const char*>(os4 + r_lo * G.Qos);
+                for (int q = lane; q < nq; q += 32) {
+                    const int r = int((uint32_t(q) * G.rc_h) >> 20), k = q - r * n8;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 4u * (r * cs + 2 * k)),
+                                 "l"(src + (size_t)r * (16 * G.Qos) + 8 * k)
+                                 : "memory");
+                }
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+            }
+            uint32_t cmax = 0u, spec = 0u;
+            const int w16 = (R.cols + 1) / 2;     // (an odd cols leaves a +0 code in the last word)
+            for (int r = 0; r < nr; ++r)
+                for (int w = lane; w < w16; w += 32) {
+                    const uint32_t v = hr[r * cs + w];
+                    cmax = __vmaxu2(cmax, v & 0x7fff7fffu);
+                    spec |= ((v & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
+                }
+            cmax = __vmaxu2(cmax, cmax >> 16) & 0xffffu;
+            cmax = __reduce_max_sync(0xffffffffu, cmax);
+            gen16 = __any_sync(0xffffffffu, spec != 0u);
+            amax = decode(cmax, fos);
         } else {
             const int nq = int(r_hi - r_lo) * G.Qos;
             const uint4* src = os4 + r_lo * G.Qos;
@@ -833,7 +918,12 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             const float sub = ldexpf(1.f, -((1 << (fos.E - 1)) - 1) - fos.M);
             margin = 2.f * 1.7320509f * (rel * amax * 1.01f + sub);
         }
-        const float* myrow = rows + (pl + 1) * cs;
+        [[maybe_unused]] const float* myrow = rows + (pl + 1) * cs;
+        // tile row p (pose p0 + p)
+        auto rowb = [&](int p) -> const char* {
+            if constexpr (H16) return wb + G.rows + 4 * p * cs;
+            else return reinterpret_cast<const char*>(rows + (p + 1) * cs);
+        };
         const bool owner = half == 0 && pl < np;     // the lane that owns pose pl's results
 
         // ---- 2. world
@@ -1007,16 +1097,23 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
         // ---- 3. self
         float scost = 0.f;
         if (do_self) {
+            // (a generic lambda: tiles with an exponent-31 code read through the
+            // generic decoder in their own copy of the code, so the common
+            // copy carries no per-read branch)
+            auto self_part = [&](auto GenC) {
+            constexpr bool GEN = decltype(GenC)::value;
+            const RowView<H16, GEN> rv{&fos};
             // broadphase, per pose, two levels (the two lanes of a pose split
             // each list): the link pairs' balls, then the half-link group
             // pairs of the live link pairs; glo / ghi bit g <=> group pair g
             // (g < 64 / >= 64) is live
             const float m2 = 2.f * margin;
-            const char* rb = reinterpret_cast<const char*>(wide ? rows + cs : myrow);
+            const char* rb = rowb(wide ? 0 : pl);
             auto ball = [&](uint2 r) -> bool {
-                const float* ca = reinterpret_cast<const float*>(rb + (r.x & 0xffffu));
-                const float* cb = reinterpret_cast<const float*>(rb + (r.x >> 16));
-                const float dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
+                float ax, ay, az, bx, by, bz;
+                rv.c3(rb, r.x & 0xffffu, ax, ay, az);
+                rv.c3(rb, r.x >> 16, bx, by, bz);
+                const float dx = ax - bx, dy = ay - by, dz = az - bz;
                 const float lim = __uint_as_float(r.y) + m2;
                 return !can_cull || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim * lim;
             };
@@ -1101,7 +1198,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 const int xi = qx[i];
                                 const int ent = qi[xi & 127];
                                 const int p = ent >> 7, g = ent & 127;
-                                const float* crow = rows + (p + 1) * cs;
+                                const char* crow = rowb(p);
                                 const int k0c = sgpoff[g] + 4 * (xi >> 7);
                                 const int k1c = min(k0c + 4, (int)sgpoff[g + 1]);
                                 VAPR_STAT(3, 1);
@@ -1113,10 +1210,10 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                                 for (int u = 0; u < 4; ++u) {
                                     const int k = k0c + u;
                                     const uint2 rec = sprec[min(k, k1c - 1)];
-                                    const char* cb8 = reinterpret_cast<const char*>(crow);
-                                    const float* ci = reinterpret_cast<const float*>(cb8 + (rec.x & 0xffffu));
-                                    const float* cj = reinterpret_cast<const float*>(cb8 + (rec.x >> 16));
-                                    const float dx = ci[0] - cj[0], dy = ci[1] - cj[1], dz = ci[2] - cj[2];
+                                    float xi, yi, zi, xj, yj, zj;
+                                    rv.c3(crow, rec.x & 0xffffu, xi, yi, zi);
+                                    rv.c3(crow, rec.x >> 16, xj, yj, zj);
+                                    const float dx = xi - xj, dy = yi - yj, dz = zi - zj;
                                     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                                     const float Rs = __uint_as_float(rec.y);
                                     // d2 >= fl(Rs^2) => phi <= 0 (self_pair's exact early-out);
@@ -1161,7 +1258,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             if (SPARSE && owner) sr_ov.row = a.ov + (p0 + pl) * G.wmax_ov;
             scost = warp_queue<1>(tb, 0ull, pl, 6, qi, qc, lane, [&](int it, int) -> QcT {
                 const int p = it >> 6, s = it & 63;
-                const float* crow = rows + (p + 1) * cs;
+                const char* crow = rowb(p);
                 const uint32_t* pm = pmask + p * PMW;
                 float gx = 0.f, gy = 0.f, gz = 0.f, c_lead = 0.f;
                 // the active partners of sphere s (a sphere's pairs in id
@@ -1183,7 +1280,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     const int i = min(s, t), j = max(s, t);
                     float vx, vy, vz, c;
                     // always active here (same test as the narrowphase that marked it)
-                    if (!self_pair(crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
+                    if (!self_pair(rv, crow, i, j, ssr, a.eta_s, inv_eta_s, hoe_s, a.w_s, vx, vy, vz, c))
                         continue;
                     const float sg = (i == s) ? -1.f : 1.f;
                     gx = fmaf(sg, vx, gx);
@@ -1191,7 +1288,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     gz = fmaf(sg, vz, gz);
                     if (i == s) c_lead += c;
                 }
-                uint32_t* orow = SPARSE ? nullptr : ovg + p * G.Wov;
+                [[maybe_unused]] uint32_t* orow = SPARSE ? nullptr : ovg + p * G.Wov;
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s, gx + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 1, gy + 0.f);
                 VAPR_TAP(2, (p0 + p) * R.cols + 3 * s + 2, gz + 0.f);
@@ -1237,6 +1334,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
 #pragma unroll
                     for (int j = 0; j < kJoints; ++j) go[j] = gq[j];
                 }
+            }
+            };
+            if constexpr (H16) {
+                if (gen16) self_part(std::true_type{});
+                else self_part(std::false_type{});
+            } else {
+                self_part(std::false_type{});
             }
         }
         if (owner) VAPR_STAT(7, 1);
@@ -1390,9 +1494,13 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const bool wide = (a.do_world && fcp.t > 10) || (a.do_self && fov.t > 10);
     const bool fused = a.fused != 0;
     if (fused && (sparse || !a.do_world || !a.do_self)) return cudaErrorInvalidValue;
+    // the self-only pass with E5M10 out_spheres keeps the codes as 16-bit tile
+    // rows (RowView: half the shared memory, VAPR_MAX_WARPS_H warps per SM)
+    const bool h16 = VAPR_H16 && !fused && a.do_self && !a.do_world && fos.kind == KIND_F16 &&
+                     !getenv("VAPR_NO_H16");
     const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0,
-                           fused ? 1 : 0);
-    if (G.rc_q == 0) return cudaErrorInvalidValue;
+                           fused ? 1 : 0, h16 ? 1 : 0);
+    if (G.rc_q == 0 || (h16 && G.rc_h == 0)) return cudaErrorInvalidValue;
     int dev = 0, sms = 148, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1401,7 +1509,7 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // once per CTA), at most VAPR_MAX_WARPS (16); one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
     const int pass = (a.do_world && !a.do_self) ? 1 : (!a.do_world && a.do_self) ? 2 : 0;
-    nw = std::min(nw, (pass == 1 && !fused) ? VAPR_MAX_WARPS_W : VAPR_MAX_WARPS);
+    nw = std::min(nw, (pass == 1 && !fused) ? VAPR_MAX_WARPS_W : h16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
     if (getenv("VAPR_DEBUG_LAUNCH"))
@@ -1412,7 +1520,12 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
         return !sparse ? collision_kernel<false, false, false, PS>
                        : (wide ? collision_kernel<true, true, false, PS> : collision_kernel<true, false, false, PS>);
     };
+    auto pick16 = [&]() {
+        return !sparse ? collision_kernel<false, false, false, 2, true>
+                       : (wide ? collision_kernel<true, true, false, 2, true> : collision_kernel<true, false, false, 2, true>);
+    };
     auto kern = fused ? collision_kernel<false, false, true, 0>
+                : h16 ? pick16()
                 : pass == 1 ? pick(std::integral_constant<int, 1>{})
                 : pass == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -577,3 +577,47 @@ def test_cull_is_exact(vb, name):
     for x, y in zip(pa, pb):
         if x is not None:
             np.testing.assert_array_equal(x, y)
+
+
+# ------------------------------------------------- a4, 16-bit tile rows (H16)
+@pytest.mark.parametrize("shift", [0.0, 7.0e4, -1.2e5])
+def test_self_pass_16bit_rows(vb, shift, monkeypatch):
+    """The self pass keeps E5M10 out_spheres as 16-bit tile rows (collision.cu
+    RowView): the hardware f16 conversion is exact for every E5M10 code but
+    the exponent-31 ones, which the all-finite reading (DESIGN.md c3-c7)
+    makes finite |x| >= 65536 and a tile holding one reads through the
+    generic decoder.  shift != 0 moves every fifth trajectory by that many
+    metres in x (exponent-31 codes; coarse quantisation puts spheres on top
+    of each other, so those poses self-collide): against the oracle, and bit
+    for bit against the FP32-row pass (VAPR_NO_H16)."""
+    wl = config2()                       # E5M10 out_spheres (43-bit set)
+    c = Ctx(vb, wl)
+    P, B, H = wl.poses, wl.B, wl.H
+    f = c.formats
+    assert tuple(f[0]) == (5, 10)
+    p = wl.params
+    _, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
+    v = v.copy()
+    moved = (np.arange(P) // H) % 5 == 2
+    v[moved, 0::3] += shift
+    os_words = orc.quantize_rows(v, f[0])
+    osd = dev(os_words.view(np.int32))
+    ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    outs = []
+    for no16 in (False, True):
+        if no16:
+            monkeypatch.setenv("VAPR_NO_H16", "1")
+        cost = torch.empty(P, dtype=torch.float32, device="cuda")
+        ov = torch.empty(P * c.W(2), dtype=torch.int32, device="cuda")
+        vb.vapr_self_collision(c.h, osd, B, H, p["eta_self"], p["w_self"], cost, ov)
+        outs.append((cost.cpu().numpy(), ov.cpu().numpy().view(np.uint32).reshape(P, -1)))
+    monkeypatch.delenv("VAPR_NO_H16", raising=False)
+    (cost16, ov16), (cost32, ov32) = outs
+    assert np.array_equal(cost16.view(np.uint32), cost32.view(np.uint32))
+    assert np.array_equal(ov16, ov32)
+    check_close(cost16, ss["cost"].reshape(-1), ss["cost_terms"].reshape(-1), "self cost",
+                kappa=ss["cost_kappa"].reshape(-1))
+    check_codes(ov16, ss["v"], fmt=f[2], cols=156, what="out_vec", min_exact=0.999,
+                max_steps=step_bound(f[2]), **self_kw(ss))
+    if shift:
+        assert (np.abs(v[moved]) >= 65536).any() and ss["cost"].reshape(-1)[moved].max() > 0
