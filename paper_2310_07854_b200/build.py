@@ -67,9 +67,12 @@ def build(force=False, verbose=False, extra=(), tap=True):
 
 def build_variant(name, defines):
     """Build a variant library (extra -D flags) to variants/libvapr_NAME.so."""
+    import shutil
     out = os.path.join(HERE, "variants", f"libvapr_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     _compile_link(out, list(defines))
+    # (the variant's object files are not kept: they would travel with gpurun)
+    shutil.rmtree(os.path.join(HERE, "build", f"libvapr_{name}"), ignore_errors=True)
     return out
 
 
