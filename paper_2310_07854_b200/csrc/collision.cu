@@ -786,17 +786,17 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
             }
-            uint32_t cmax = 0u, spec = 0u;
-            const int w16 = (R.cols + 1) / 2;     // (an odd cols leaves a +0 code in the last word)
-            for (int r = 0; r < nr; ++r)
-                for (int w = lane; w < w16; w += 32) {
-                    const uint32_t v = hr[r * cs + w];
-                    cmax = __vmaxu2(cmax, v & 0x7fff7fffu);
-                    spec |= ((v & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
-                }
+            // (8-byte reads of the staged chunks; an exponent-31 code is a
+            // magnitude code >= 0x7C00, so the largest one also flags them)
+            uint32_t cmax = 0u;
+            for (int q = lane; q < nq; q += 32) {
+                const int r = int((uint32_t(q) * G.rc_h) >> 20), k = q - r * n8;
+                const uint2 v = *reinterpret_cast<const uint2*>(hr + r * cs + 2 * k);
+                cmax = __vmaxu2(cmax, __vmaxu2(v.x & 0x7fff7fffu, v.y & 0x7fff7fffu));
+            }
             cmax = __vmaxu2(cmax, cmax >> 16) & 0xffffu;
             cmax = __reduce_max_sync(0xffffffffu, cmax);
-            gen16 = __any_sync(0xffffffffu, spec != 0u);
+            gen16 = cmax >= 0x7C00u;
             amax = decode(cmax, fos);
         } else {
             const int nq = int(r_hi - r_lo) * G.Qos;

@@ -8,12 +8,12 @@ import re
 import sys
 from collections import defaultdict
 
-# (name, first line, last line) of collision.cu at commit time of profiles/r2
-REGIONS = [("world_term", 66, 130), ("sparse_row", 131, 193), ("or_code3", 194, 214),
-           ("self_pair", 215, 260), ("warp_queue", 390, 450), ("kernel head", 541, 684),
-           ("tile stage+decode", 685, 823), ("margin+zero", 824, 838), ("world broadphase", 839, 922),
-           ("world items", 923, 1006), ("self broadphase", 1007, 1047), ("self narrowphase", 1048, 1142),
-           ("self touched", 1143, 1159), ("self gradients", 1160, 1230), ("tile tail", 1231, 1265)]
+REGIONS = [("world_term", 66, 130), ("sparse_row", 131, 193), ("or_code3", 194, 218),
+           ("row reads (RowView)", 219, 244), ("self_pair", 245, 290), ("warp_queue", 444, 509),
+           ("kernel head", 595, 738), ("tile stage+decode", 739, 908), ("margin+zero", 909, 928),
+           ("world broadphase", 929, 1012), ("world items", 1013, 1096), ("self broadphase", 1097, 1144),
+           ("self narrowphase", 1145, 1239), ("self touched", 1240, 1256), ("self gradients", 1257, 1330),
+           ("tile tail", 1331, 1369)]
 acc = defaultdict(lambda: [0.0, 0.0, 0.0])
 head = ""
 for l in open(sys.argv[1]):
