@@ -76,11 +76,13 @@ for st, e in out["kernels"].items():
                   "warp_instructions": [l["warp_instructions"] for l in L],
                   "threads_per_instruction": [l["threads_per_instruction"] for l in L]}
 LIMITER = {
-    "collision": "latency / occupancy: two passes, each 16 warps per SM (one CTA per SM; world "
-                 "pass register-bound at 128, self pass shared-memory bound at 13.6 KB per warp), "
-                 "58-61 % issue-active, 21-23 of 32 threads per instruction, top stalls wait and "
-                 "short scoreboard; DRAM traffic = out_spheres read by both passes + the sparse "
-                 "outputs (profiles/r2/collision_regions_*.txt)",
+    "collision": "two passes, each its own kernel, one CTA per SM: the self pass (16-bit tile "
+                 "rows, 26 warps per SM, 71 registers) at 79 % issue-active (instruction issue; "
+                 "its occupancy sweep 12 -> 16 -> 26 warps: 1.64 -> 1.37 -> 1.15 ms), the world "
+                 "pass (FP32 rows, 16 warps, 127 registers) at 61 % issue-active, latency-bound "
+                 "and saturated in warps (18: 1 %); 21-23 of 32 threads per instruction; DRAM "
+                 "traffic = out_spheres read by both passes + the sparse outputs "
+                 "(profiles/r2/collision_regions_*.txt)",
     "fk": "instruction issue: ~88 % issue-active at 40 warps per SM, 31.6 of 32 threads per "
           "instruction",
     "aggregate": "divergence: a thread per row over the set spheres (10.7 of 32 threads per "
