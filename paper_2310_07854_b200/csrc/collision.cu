@@ -1384,6 +1384,37 @@ __global__ void traj_reduce_kernel(float* __restrict__ cost_pose, int B, int H,
     if (cost_traj) cost_traj[b] = c;
 }
 
+// The same sums with coalesced accesses: a CTA stages T whole trajectories'
+// pose costs (the world + self addition done on the way, in the same order)
+// in shared memory at stride H + 1 (conflict-free), then thread t sums
+// trajectory t over h in order -- bit-identical to traj_reduce_kernel.
+__global__ void __launch_bounds__(256)
+traj_reduce_tiled_kernel(float* __restrict__ cost_pose, int B, int H, int T,
+                         float* __restrict__ cost_traj, const float* __restrict__ add) {
+    extern __shared__ float sv[];
+    pdl_wait();
+    const long long b0 = (long long)blockIdx.x * T;
+    const int nb = (int)min((long long)T, B - b0);
+    const long long g0 = b0 * H;
+    const int n = nb * H;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        float v = cost_pose[g0 + i];
+        if (add) {
+            v = v + add[g0 + i];
+            cost_pose[g0 + i] = v;
+        }
+        const int t = i / H;
+        sv[i + t] = v;
+    }
+    __syncthreads();
+    if (cost_traj && threadIdx.x < nb) {
+        const float* r = sv + threadIdx.x * (H + 1);
+        float c = 0.f;
+        for (int h = 0; h < H; ++h) c += r[h];
+        cost_traj[b0 + threadIdx.x] = c;
+    }
+}
+
 __global__ void best_kernel(const float* __restrict__ cost_traj, int n_problems, int seeds,
                             float* __restrict__ best_cost, int32_t* __restrict__ best_seed) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1632,6 +1663,12 @@ cudaError_t launch_collision(const RobotDev& R, const WorldsDev& W, const Fmt& f
 cudaError_t launch_traj_reduce(float* cost_pose, int32_t B, int32_t H, float* cost_traj,
                                cudaStream_t s, const float* add, bool pdl) {
     if (B <= 0) return cudaSuccess;
+    if (H >= 1 && H <= 4096) {
+        const int T = std::max(1, std::min(256, 4096 / H));
+        const size_t smem = sizeof(float) * (size_t)T * (H + 1);
+        return launch_k(traj_reduce_tiled_kernel, dim3((unsigned)((B + T - 1) / T)), dim3(256), smem, s, pdl,
+                        cost_pose, B, H, T, cost_traj, add);
+    }
     return launch_k(traj_reduce_kernel, dim3((B + 255) / 256), dim3(256), 0, s, pdl, cost_pose, B,
                     H, cost_traj, add);
 }
