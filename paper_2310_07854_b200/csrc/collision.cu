@@ -306,6 +306,9 @@ __device__ __forceinline__ bool self_pair(const RV& rv, const char* rb, int i, i
 #ifndef VAPR_H16                 // self pass: 16-bit tile rows for E5M10 out_spheres
 #define VAPR_H16 1
 #endif
+#ifndef VAPR_H16_V16             // 16-bit rows staged by 16-byte copies (row stride 4 mod 8 words)
+#define VAPR_H16_V16 1
+#endif
 #ifndef VAPR_MAX_WARPS_H        // the self pass with 16-bit tile rows (its kernel fits 96 registers)
 #define VAPR_MAX_WARPS_H 26
 #endif
@@ -370,11 +373,20 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
         // 16-bit rows (self-only pass, E5M10): the row's (cols + 1) / 2 words at
         // a stride of 2 mod 4 words -- 8-byte aligned rows (8-byte cp.async),
         // and lane-per-pose reads of 16 rows on 16 distinct banks
+#if VAPR_H16_V16
+        // (16-byte copies of the whole packed row: a stride of 4 mod 8 words,
+        // 2-way bank conflicts for lane-per-pose reads)
+        int st = 4 * g.Qos;
+        while (st % 8 != 4) ++st;
+        g.cs = st;
+        g.n8 = g.Qos;
+#else
         const int w16 = (R.cols + 1) / 2;
         int st = w16;
         while (st % 4 != 2) ++st;
         g.cs = st;
         g.n8 = (w16 + 1) / 2;
+#endif
         g.rc_h = (1u << 20) / (uint32_t)g.n8 + 1u;
         for (int q = 0; q < kPL * g.n8; ++q)
             if (int((uint32_t(q) * g.rc_h) >> 20) != q / g.n8) g.rc_h = 0;
@@ -779,9 +791,15 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                 const char* src = reinterpret_cast<const char*>(os4 + r_lo * G.Qos);
                 for (int q = lane; q < nq; q += 32) {
                     const int r = int((uint32_t(q) * G.rc_h) >> 20), k = q - r * n8;
+#if VAPR_H16_V16
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + 4u * (r * cs + 4 * k)),
+                                 "l"(src + (size_t)r * (16 * G.Qos) + 16 * k)
+                                 : "memory");
+#else
                     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 4u * (r * cs + 2 * k)),
                                  "l"(src + (size_t)r * (16 * G.Qos) + 8 * k)
                                  : "memory");
+#endif
                 }
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
@@ -791,8 +809,14 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             uint32_t cmax = 0u;
             for (int q = lane; q < nq; q += 32) {
                 const int r = int((uint32_t(q) * G.rc_h) >> 20), k = q - r * n8;
+#if VAPR_H16_V16
+                const uint4 v = *reinterpret_cast<const uint4*>(hr + r * cs + 4 * k);
+                cmax = __vmaxu2(cmax, __vmaxu2(__vmaxu2(v.x & 0x7fff7fffu, v.y & 0x7fff7fffu),
+                                               __vmaxu2(v.z & 0x7fff7fffu, v.w & 0x7fff7fffu)));
+#else
                 const uint2 v = *reinterpret_cast<const uint2*>(hr + r * cs + 2 * k);
                 cmax = __vmaxu2(cmax, __vmaxu2(v.x & 0x7fff7fffu, v.y & 0x7fff7fffu));
+#endif
             }
             cmax = __vmaxu2(cmax, cmax >> 16) & 0xffffu;
             cmax = __reduce_max_sync(0xffffffffu, cmax);
