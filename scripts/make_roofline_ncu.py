@@ -77,8 +77,8 @@ for st, e in out["kernels"].items():
                   "threads_per_instruction": [l["threads_per_instruction"] for l in L]}
 LIMITER = {
     "collision": "two passes, each its own kernel, one CTA per SM: the self pass (16-bit tile "
-                 "rows, 26 warps per SM, 71 registers) at 79 % issue-active (instruction issue; "
-                 "its occupancy sweep 12 -> 16 -> 26 warps: 1.64 -> 1.37 -> 1.15 ms), the world "
+                 "rows, 26 warps per SM, 71 registers) at 76 % issue-active (instruction issue; "
+                 "its occupancy sweep 12 -> 16 -> 26 warps: 1.64 -> 1.37 -> 1.14 ms), the world "
                  "pass (FP32 rows, 16 warps, 127 registers) at 61 % issue-active, latency-bound "
                  "and saturated in warps (18: 1 %); 21-23 of 32 threads per instruction; DRAM "
                  "traffic = out_spheres read by both passes + the sparse outputs "

@@ -9,11 +9,11 @@ import sys
 from collections import defaultdict
 
 REGIONS = [("world_term", 66, 130), ("sparse_row", 131, 193), ("or_code3", 194, 218),
-           ("row reads (RowView)", 219, 244), ("self_pair", 245, 290), ("warp_queue", 444, 509),
-           ("kernel head", 595, 738), ("tile stage+decode", 739, 908), ("margin+zero", 909, 928),
-           ("world broadphase", 929, 1012), ("world items", 1013, 1096), ("self broadphase", 1097, 1144),
-           ("self narrowphase", 1145, 1239), ("self touched", 1240, 1256), ("self gradients", 1257, 1330),
-           ("tile tail", 1331, 1369)]
+           ("row reads (RowView)", 219, 244), ("self_pair", 245, 290), ("warp_queue", 456, 521),
+           ("kernel head", 607, 750), ("tile stage+decode", 751, 932), ("margin+zero", 933, 952),
+           ("world broadphase", 953, 1036), ("world items", 1037, 1120), ("self broadphase", 1121, 1168),
+           ("self narrowphase", 1169, 1263), ("self touched", 1264, 1280), ("self gradients", 1281, 1354),
+           ("tile tail", 1355, 1393)]
 acc = defaultdict(lambda: [0.0, 0.0, 0.0])
 head = ""
 for l in open(sys.argv[1]):
