@@ -11,10 +11,14 @@
 // 15 / 31 is the halo pose p0 + 15 and whose tile adds the halo rows p0-1 and
 // p0+15 for the swept samples; 16 for the self pass and the discrete world
 // pass (warps are independent: no CTA barrier in the tile loop; the robot
-// tables are staged once per CTA from a device image):
+// tables are staged once per CTA from a device image).  World and self run as
+// two passes, each its own kernel instantiation (PASS 1 / 2):
 //  1. stage the packed rows (cp.async, all 16-byte copies in flight) and
 //     decode them in place into an FP32 tile (odd row stride: pose-per-lane
-//     accesses are conflict-free); track the largest decoded coordinate;
+//     accesses are conflict-free); track the largest decoded coordinate.
+//     The self pass with E5M10 out_spheres (H16) keeps the staged codes as
+//     16-bit rows instead and converts each coordinate as it reads it
+//     (RowView): half the shared memory, 26 warps per SM;
 //  2. broadphase, 16 poses per instruction, the two lanes of a pose splitting
 //     its list.  The spheres of a link (or of a
 //     half-link group) lie in a ball around a reference sphere whose radius is
@@ -29,9 +33,11 @@
 //     order-independent); live (pose, group pair) self items test the group
 //     balls and then the candidate sphere pairs, marking active pairs in a
 //     per-pose bitmask over canonical pair ids; (pose, touched sphere) items
-//     gather the self gradient over the active pairs in id order.  Costs come
-//     back to the pose's lane and are summed in a fixed order;
-//  4. the packed rows are streamed out with coalesced 16-byte stores.
+//     gather the self gradient over the active pairs in id order (the
+//     sphere's partner mask first, then its pairs evaluated together).  Costs
+//     come back to the pose's lane and are summed in a fixed order;
+//  4. outputs: dense rows (codes ORed into zero-filled rows) or the N3 sparse
+//     form (each pose's owner lane appends its codes in sphere order).
 //
 // Culling is exact: a term is skipped only when its bound clears the
 // activation distance by kSlack = 1e-4 m, orders of magnitude above the FP32
