@@ -621,3 +621,29 @@ def test_self_pass_16bit_rows(vb, shift, monkeypatch):
                 max_steps=step_bound(f[2]), **self_kw(ss))
     if shift:
         assert (np.abs(v[moved]) >= 65536).any() and ss["cost"].reshape(-1)[moved].max() > 0
+
+
+@pytest.mark.parametrize("H", [1, 7, 4096, 4097])
+def test_traj_reduce_shapes(vb, H):
+    """cost_traj = the in-order FP32 sum of each trajectory's cost_pose (a CTA
+    stages whole trajectories for H <= 4096, a thread per trajectory above):
+    bit for bit against numpy's sequential float32 sum of the GPU's own
+    cost_pose, at the tile boundaries (H = 4096 / 4097) and for ragged B."""
+    from workloads.scenes import ENVIRONMENTS
+    B = 3 if H > 1000 else 37
+    wl = make_workload("traj", [ENVIRONMENTS[i % 8] for i in range(B)], list(range(B)), 1, H,
+                       FORMAT_SETS["43bit"], salt=5)
+    c = Ctx(vb, wl)
+    P = wl.poses
+    os_words, _ = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, c.formats[0])
+    cp = torch.empty(P * c.W(4), dtype=torch.int32, device="cuda")
+    ov = torch.empty(P * c.W(2), dtype=torch.int32, device="cuda")
+    cost = torch.empty(P, dtype=torch.float32, device="cuda")
+    ctraj = torch.empty(B, dtype=torch.float32, device="cuda")
+    p = dict(wl.params, swept=1 if H >= 2 else 0)      # (a swept cost needs H >= 2)
+    vb.vapr_collision(c.h, dev(os_words.view(np.int32)), dev(wl.world_idx), B, H, p, cost, ctraj, cp, ov)
+    cp_ = cost.cpu().numpy().reshape(B, H)
+    ref = np.zeros(B, np.float32)
+    for h in range(H):
+        ref = (ref + cp_[:, h]).astype(np.float32)
+    assert np.array_equal(ctraj.cpu().numpy().view(np.uint32), ref.view(np.uint32))
