@@ -315,6 +315,12 @@ __device__ __forceinline__ bool self_pair(const RV& rv, const char* rb, int i, i
 #ifndef VAPR_H16_V16             // 16-bit rows staged by 16-byte copies (row stride 4 mod 8 words)
 #define VAPR_H16_V16 1
 #endif
+#ifndef VAPR_H16_W               // world pass: the same 16-bit tile rows
+#define VAPR_H16_W 1
+#endif
+#ifndef VAPR_MAX_WARPS_WH       // warps per SM of the world pass with 16-bit rows
+#define VAPR_MAX_WARPS_WH 24
+#endif
 #ifndef VAPR_MAX_WARPS_H        // the self pass with 16-bit tile rows (its kernel fits 96 registers)
 #define VAPR_MAX_WARPS_H 26
 #endif
@@ -394,7 +400,7 @@ Geo make_geo(const RobotDev& R, const Fmt& fos, const Fmt& fcp, const Fmt& fov, 
         g.n8 = (w16 + 1) / 2;
 #endif
         g.rc_h = (1u << 20) / (uint32_t)g.n8 + 1u;
-        for (int q = 0; q < kPL * g.n8; ++q)
+        for (int q = 0; q < kTR * g.n8; ++q)
             if (int((uint32_t(q) * g.rc_h) >> 20) != q / g.n8) g.rc_h = 0;
     }
     g.pmw = (R.n_pairs + 31) >> 5;
@@ -611,7 +617,8 @@ __device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsi
 // FUSED (N4, VAPR_OPT_FUSED): FK in the tile fill, the gradients summed in a
 // shared FP32 tile, BK per pose at the tile's end (CollisionArgs::fused).
 template <bool SPARSE, bool SP_WIDE, bool FUSED, int PASS, bool H16 = false>
-__global__ void __launch_bounds__(32 * (PASS == 1 ? VAPR_MAX_WARPS_W : H16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS), 1)
+__global__ void __launch_bounds__(32 * (PASS == 1 ? (H16 ? VAPR_MAX_WARPS_WH : VAPR_MAX_WARPS_W)
+                                              : H16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS), 1)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
@@ -790,7 +797,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             // the E5M10 codes are the tile: 8-byte asynchronous copies into
             // 16-bit rows, then one pass over the words for the largest code
             // magnitude (|x| is monotone in it) and exponent-31 codes
-            uint32_t* hr = reinterpret_cast<uint32_t*>(wb + G.rows);
+            // (the world pass's rows start at tile row row_off: halo rows)
+            uint32_t* hr = reinterpret_cast<uint32_t*>(wb + G.rows) + (PASS == 2 ? 0 : row_off * cs);
             const int nr = int(r_hi - r_lo), n8 = G.n8, nq = nr * n8;
             {
                 const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(hr);
@@ -949,32 +957,42 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             margin = 2.f * 1.7320509f * (rel * amax * 1.01f + sub);
         }
         [[maybe_unused]] const float* myrow = rows + (pl + 1) * cs;
-        // tile row p (pose p0 + p)
-        auto rowb = [&](int p) -> const char* {
-            if constexpr (H16) return wb + G.rows + 4 * p * cs;
-            else return reinterpret_cast<const char*>(rows + (p + 1) * cs);
+        // tile row t (pose p0 + t - 1; a pass without the world part has no
+        // row 0), and rowb(p) = the row of pose p0 + p
+        auto rowt = [&](int t) -> const char* {
+            if constexpr (H16) return wb + G.rows + 4 * (t - (PASS == 2 ? 1 : 0)) * cs;
+            else return reinterpret_cast<const char*>(rows + t * cs);
         };
+        auto rowb = [&](int p) -> const char* { return rowt(p + 1); };
         const bool owner = half == 0 && pl < np;     // the lane that owns pose pl's results
 
         // ---- 2. world
         float wcost = 0.f;
         if (do_world) {
+            // (a generic lambda, as the self part below: tiles with an
+            // exponent-31 code in their own copy)
+            auto world_part = [&](auto GenC) {
+            constexpr bool GEN = decltype(GenC)::value;
+            const RowView<H16, GEN> rv{&fos};
             // test ball per link: swept -> the segment (pose pg-1, pose pg),
             // i.e. tile rows (lane, lane+1), a ball around both endpoint balls
             // (it bounds every sample on the segment); discrete -> pose pg
             const bool tv = swept ? (h >= 1 && plb <= np) : (plb < np);
             float bx[kLH], by[kLH], bz[kLH], lim2[kLH];
-            const float* prow = rows + plb * cs;
-            const float* brow = rows + (plb + 1) * cs;
+            const char* prow = rowt(plb);
+            const char* brow = rowt(plb + 1);
 #pragma unroll
             for (int u = 0; u < kLH; ++u) {
                 const int l = half * kLH + u;
                 const int lc = min(l, kLinks - 1);
-                const int r3 = 3 * sref[lc];
-                float cx = brow[r3], cy = brow[r3 + 1], cz = brow[r3 + 2];
+                const uint32_t r12 = 12u * sref[lc];
+                float cx, cy, cz;
+                rv.c3(brow, r12, cx, cy, cz);
                 float rr = srl[lc] + margin;
                 if (swept) {
-                    const float dx = prow[r3] - cx, dy = prow[r3 + 1] - cy, dz = prow[r3 + 2] - cz;
+                    float qx, qy, qz;
+                    rv.c3(prow, r12, qx, qy, qz);
+                    const float dx = qx - cx, dy = qy - cy, dz = qz - cz;
                     cx = fmaf(0.5f, dx, cx);
                     cy = fmaf(0.5f, dy, cy);
                     cz = fmaf(0.5f, dz, cz);
@@ -1062,15 +1080,16 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                     return Cub{__ldg(cub + 4 * kk), __ldg(cub + 4 * kk + 1), __ldg(cub + 4 * kk + 2),
                                __ldg(cub + 4 * kk + 3)};
                 };
-                const float* crow = rows + (p + 1) * cs;
-                const float cx = crow[3 * sp], cy = crow[3 * sp + 1], cz = crow[3 * sp + 2];
+                const char* crow = rowt(p + 1);
+                float cx, cy, cz;
+                rv.c3(crow, 12u * sp, cx, cy, cz);
                 const float A = ssr[sp] + a.eta_w;
                 Acc acc{0.f, 0.f, 0.f, 0.f};
                 // terms in a fixed order: the pose itself, the samples of
                 // segment (h, h+1) (cost + (1-tau) grad), the samples of
                 // segment (h-1, h) (tau grad only) -- one call site
-                const float* nrow = crow + cs;
-                const float* qrow = crow - cs;
+                const char* nrow = rowt(p + 2);
+                const char* qrow = rowt(p);
                 const int nt = 1 + (m_fwd ? nsub : 0) + (m_bwd ? nsub : 0);
                 for (int t = 0; t < nt; ++t) {
                     float sx = cx, sy = cy, sz = cz, cw = 1.f, gw = 1.f;
@@ -1079,8 +1098,8 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         const bool fw = m_fwd && t <= nsub;
                         const int j = fw ? t : t - (m_fwd ? nsub : 0);
                         const float tau = float(j) * inv_n1, omt = 1.f - tau;
-                        const float* o = fw ? nrow : qrow;
-                        const float ox = o[3 * sp], oy = o[3 * sp + 1], oz = o[3 * sp + 2];
+                        float ox, oy, oz;
+                        rv.c3(fw ? nrow : qrow, 12u * sp, ox, oy, oz);
                         if (fw) {
                             sx = fmaf(tau, ox, omt * cx);
                             sy = fmaf(tau, oy, omt * cy);
@@ -1122,6 +1141,13 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
             });
             if (SPARSE && owner) sr_cp.finish(a.cp_mask + p0 + pl);
             if (FUSED && half == 0) gfw[pl] = smask;
+            };
+            if constexpr (H16) {
+                if (gen16) world_part(std::true_type{});
+                else world_part(std::false_type{});
+            } else {
+                world_part(std::false_type{});
+            }
         }
 
         // ---- 3. self
@@ -1557,8 +1583,8 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     if (fused && (sparse || !a.do_world || !a.do_self)) return cudaErrorInvalidValue;
     // the self-only pass with E5M10 out_spheres keeps the codes as 16-bit tile
     // rows (RowView: half the shared memory, VAPR_MAX_WARPS_H warps per SM)
-    const bool h16 = VAPR_H16 && !fused && a.do_self && !a.do_world && fos.kind == KIND_F16 &&
-                     !getenv("VAPR_NO_H16");
+    const bool h16 = !fused && fos.kind == KIND_F16 && !getenv("VAPR_NO_H16") &&
+                     ((VAPR_H16 && a.do_self && !a.do_world) || (VAPR_H16_W && a.do_world && !a.do_self));
     const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0,
                            fused ? 1 : 0, h16 ? 1 : 0);
     if (G.rc_q == 0 || (h16 && G.rc_h == 0)) return cudaErrorInvalidValue;
@@ -1570,7 +1596,8 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     // once per CTA), at most VAPR_MAX_WARPS (16); one persistent CTA per SM
     int nw = (optin - (int)G.tables) / (int)G.warp;
     const int pass = (a.do_world && !a.do_self) ? 1 : (!a.do_world && a.do_self) ? 2 : 0;
-    nw = std::min(nw, (pass == 1 && !fused) ? VAPR_MAX_WARPS_W : h16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS);
+    nw = std::min(nw, (pass == 1 && !fused) ? (h16 ? VAPR_MAX_WARPS_WH : VAPR_MAX_WARPS_W)
+                                            : h16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS);
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
     if (getenv("VAPR_DEBUG_LAUNCH"))
@@ -1581,12 +1608,13 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
         return !sparse ? collision_kernel<false, false, false, PS>
                        : (wide ? collision_kernel<true, true, false, PS> : collision_kernel<true, false, false, PS>);
     };
-    auto pick16 = [&]() {
-        return !sparse ? collision_kernel<false, false, false, 2, true>
-                       : (wide ? collision_kernel<true, true, false, 2, true> : collision_kernel<true, false, false, 2, true>);
+    auto pick16 = [&](auto Pc) {
+        constexpr int PS = decltype(Pc)::value;
+        return !sparse ? collision_kernel<false, false, false, PS, true>
+                       : (wide ? collision_kernel<true, true, false, PS, true> : collision_kernel<true, false, false, PS, true>);
     };
     auto kern = fused ? collision_kernel<false, false, true, 0>
-                : h16 ? pick16()
+                : h16 ? (pass == 1 ? pick16(std::integral_constant<int, 1>{}) : pick16(std::integral_constant<int, 2>{}))
                 : pass == 1 ? pick(std::integral_constant<int, 1>{})
                 : pass == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

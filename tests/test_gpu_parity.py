@@ -647,3 +647,45 @@ def test_traj_reduce_shapes(vb, H):
     for h in range(H):
         ref = (ref + cp_[:, h]).astype(np.float32)
     assert np.array_equal(ctraj.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("shift", [0.0, 7.0e4])
+@pytest.mark.parametrize("swept", [1, 0])
+def test_world_pass_16bit_rows(vb, shift, swept, monkeypatch):
+    """The world pass keeps E5M10 out_spheres as 16-bit tile rows too (halo
+    rows included for the swept samples): against the oracle, and bit for bit
+    against the FP32-row pass (VAPR_NO_H16); shift moves every fifth
+    trajectory (and its cuboids' world) by that many metres in x, so its
+    tiles hold exponent-31 codes and read through the generic decoder."""
+    wl = config2()
+    c = Ctx(vb, wl)
+    P, B, H = wl.poses, wl.B, wl.H
+    f = c.formats
+    assert tuple(f[0]) == (5, 10)
+    p = wl.params
+    _, v = orc.fk_stage(wl.q.reshape(-1, 7), wl.robot, f[0])
+    v = v.copy()
+    moved = (np.arange(P) // H) % 5 == 2
+    v[moved, 0::3] += shift
+    os_words = orc.quantize_rows(v, f[0])
+    osd = dev(os_words.view(np.int32))
+    slot = 4 if swept else 3
+    ws = orc.world_stage(os_words, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
+                         B, H, p["eta_world"], p["w_world"], swept, p["sweep_steps"], f[slot])
+    outs = []
+    for no16 in (False, True):
+        if no16:
+            monkeypatch.setenv("VAPR_NO_H16", "1")
+        cost = torch.empty(P, dtype=torch.float32, device="cuda")
+        cp = torch.empty(P * c.W(slot), dtype=torch.int32, device="cuda")
+        vb.vapr_world_collision(c.h, osd, dev(wl.world_idx), B, H, swept, p["sweep_steps"],
+                                p["eta_world"], p["w_world"], cost, cp)
+        outs.append((cost.cpu().numpy(), cp.cpu().numpy().view(np.uint32).reshape(P, -1)))
+    monkeypatch.delenv("VAPR_NO_H16", raising=False)
+    (cost16, cp16), (cost32, cp32) = outs
+    assert np.array_equal(cost16.view(np.uint32), cost32.view(np.uint32))
+    assert np.array_equal(cp16, cp32)
+    check_close(cost16, ws["cost"].reshape(-1), ws["cost_terms"].reshape(-1), "world cost",
+                kappa=ws["cost_kappa"].reshape(-1))
+    check_codes(cp16, ws["v"], fmt=f[slot], cols=156, what="closest_pt", min_exact=0.999,
+                max_steps=step_bound(f[slot]), **world_kw(ws))
