@@ -318,6 +318,12 @@ __device__ __forceinline__ bool self_pair(const RV& rv, const char* rb, int i, i
 #ifndef VAPR_H16_W               // world pass: the same 16-bit tile rows
 #define VAPR_H16_W 1
 #endif
+#ifndef VAPR_H16_W_MIN_POSES     // ... from this batch size on
+#define VAPR_H16_W_MIN_POSES 16384
+#endif
+#ifndef VAPR_H16_S_MIN_POSES     // the self pass's
+#define VAPR_H16_S_MIN_POSES 1024
+#endif
 #ifndef VAPR_MAX_WARPS_WH       // warps per SM of the world pass with 16-bit rows
 #define VAPR_MAX_WARPS_WH 24
 #endif
@@ -1120,7 +1126,7 @@ collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo
                         world_term(cuboid(__ffs(m) - 1), sx, sy, sz, A, a.eta_w, inv_eta_w, hoe_w,
                                    a.w_w, cw, gw, acc);
                 }
-                uint32_t* orow = SPARSE ? nullptr : cpg + p * G.Wcp;
+                [[maybe_unused]] uint32_t* orow = SPARSE ? nullptr : cpg + p * G.Wcp;
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp, acc.gx + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 1, acc.gy + 0.f);
                 VAPR_TAP(a.swept ? 4 : 3, (p0 + p) * R.cols + 3 * sp + 2, acc.gz + 0.f);
@@ -1583,8 +1589,16 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     if (fused && (sparse || !a.do_world || !a.do_self)) return cudaErrorInvalidValue;
     // the self-only pass with E5M10 out_spheres keeps the codes as 16-bit tile
     // rows (RowView: half the shared memory, VAPR_MAX_WARPS_H warps per SM)
+    // (not on small batches, whose one-pose tiles measured faster with the
+    // FP32 rows: config 2 49.2 vs 50.8 us; from 1,024 poses for the self
+    // pass, 16,384 for the world pass)
+    // (VAPR_H16_MIN_POSES in the environment overrides both sizes: the tests)
+    const char* h16min = getenv("VAPR_H16_MIN_POSES");
+    const long long min_s = h16min ? atoll(h16min) : VAPR_H16_S_MIN_POSES;
+    const long long min_w = h16min ? atoll(h16min) : VAPR_H16_W_MIN_POSES;
     const bool h16 = !fused && fos.kind == KIND_F16 && !getenv("VAPR_NO_H16") &&
-                     ((VAPR_H16 && a.do_self && !a.do_world) || (VAPR_H16_W && a.do_world && !a.do_self));
+                     ((VAPR_H16 && a.do_self && !a.do_world && P >= min_s) ||
+                      (VAPR_H16_W && a.do_world && !a.do_self && P >= min_w));
     const Geo G = make_geo(R, fos, fcp, fov, a.do_world, a.do_self, sparse ? (wide ? 2 : 1) : 0,
                            fused ? 1 : 0, h16 ? 1 : 0);
     if (G.rc_q == 0 || (h16 && G.rc_h == 0)) return cudaErrorInvalidValue;

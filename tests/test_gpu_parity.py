@@ -603,6 +603,7 @@ def test_self_pass_16bit_rows(vb, shift, monkeypatch):
     os_words = orc.quantize_rows(v, f[0])
     osd = dev(os_words.view(np.int32))
     ss = orc.self_stage(os_words, f[0], wl.robot, p["eta_self"], p["w_self"], f[2])
+    monkeypatch.setenv("VAPR_H16_MIN_POSES", "0")     # (the 16-bit rows on this small batch too)
     outs = []
     for no16 in (False, True):
         if no16:
@@ -672,6 +673,7 @@ def test_world_pass_16bit_rows(vb, shift, swept, monkeypatch):
     slot = 4 if swept else 3
     ws = orc.world_stage(os_words, f[0], wl.world_idx, wl.cuboids, wl.world_offsets, wl.robot,
                          B, H, p["eta_world"], p["w_world"], swept, p["sweep_steps"], f[slot])
+    monkeypatch.setenv("VAPR_H16_MIN_POSES", "0")     # (the 16-bit rows on this small batch too)
     outs = []
     for no16 in (False, True):
         if no16:
