@@ -76,12 +76,12 @@ for st, e in out["kernels"].items():
                   "warp_instructions": [l["warp_instructions"] for l in L],
                   "threads_per_instruction": [l["threads_per_instruction"] for l in L]}
 LIMITER = {
-    "collision": "two passes, each its own kernel, one CTA per SM: the self pass (16-bit tile "
-                 "rows, 26 warps per SM, 71 registers) at 76 % issue-active (instruction issue; "
-                 "its occupancy sweep 12 -> 16 -> 26 warps: 1.64 -> 1.37 -> 1.14 ms), the world "
-                 "pass (FP32 rows, 16 warps, 127 registers) at 61 % issue-active, latency-bound "
-                 "and saturated in warps (18: 1 %); 21-23 of 32 threads per instruction; DRAM "
-                 "traffic = out_spheres read by both passes + the sparse outputs "
+    "collision": "two passes, each its own kernel, one CTA per SM, both with 16-bit tile rows "
+                 "(E5M10 out_spheres): self pass 25 warps per SM, 71 registers, world pass 24 "
+                 "warps, 78 registers; both ~75 % issue-active (instruction issue; the occupancy "
+                 "sweeps: self 12 -> 16 -> 26 warps 1.64 -> 1.37 -> 1.14 ms, world 16 -> 24 "
+                 "1.22 -> 1.03 ms); 21-23 of 32 threads per instruction; DRAM traffic = "
+                 "out_spheres read by both passes + the sparse outputs "
                  "(profiles/r2/collision_regions_*.txt)",
     "fk": "instruction issue: ~88 % issue-active at 40 warps per SM, 31.6 of 32 threads per "
           "instruction",

@@ -8,12 +8,12 @@ import re
 import sys
 from collections import defaultdict
 
-REGIONS = [("world_term", 66, 130), ("sparse_row", 131, 193), ("or_code3", 194, 218),
-           ("row reads (RowView)", 219, 244), ("self_pair", 245, 290), ("warp_queue", 456, 521),
-           ("kernel head", 607, 750), ("tile stage+decode", 751, 932), ("margin+zero", 933, 952),
-           ("world broadphase", 953, 1036), ("world items", 1037, 1120), ("self broadphase", 1121, 1168),
-           ("self narrowphase", 1169, 1263), ("self touched", 1264, 1280), ("self gradients", 1281, 1354),
-           ("tile tail", 1355, 1393)]
+REGIONS = [("world_term", 72, 136), ("sparse_row", 137, 199), ("or_code3", 200, 224),
+           ("row reads (RowView)", 225, 250), ("self_pair", 251, 296), ("warp_queue", 474, 539),
+           ("kernel head", 625, 769), ("tile stage+decode", 770, 952), ("margin+zero", 953, 974),
+           ("world broadphase", 975, 1066), ("world items", 1067, 1158), ("self broadphase", 1159, 1206),
+           ("self narrowphase", 1207, 1301), ("self touched", 1302, 1318), ("self gradients", 1319, 1392),
+           ("tile tail", 1393, 1431)]
 acc = defaultdict(lambda: [0.0, 0.0, 0.0])
 head = ""
 for l in open(sys.argv[1]):
