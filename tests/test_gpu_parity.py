@@ -34,6 +34,11 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+def dataclasses_replace(wl, **kw):
+    import dataclasses
+    return dataclasses.replace(wl, **kw)
+
+
 def sampled_magnitudes(E, M, n=1 << 16, key=11):
     """Up to n representable magnitudes of the format, in code order, from the
     oracle's decoder: every one for t <= 17, else a seeded sample of codes
@@ -691,3 +696,36 @@ def test_world_pass_16bit_rows(vb, shift, swept, monkeypatch):
                 kappa=ws["cost_kappa"].reshape(-1))
     check_codes(cp16, ws["v"], fmt=f[slot], cols=156, what="closest_pt", min_exact=0.999,
                 max_steps=step_bound(f[slot]), **world_kw(ws))
+
+
+@pytest.mark.parametrize("fs", ["43bit", "fp16"])
+@pytest.mark.parametrize("sparse", [True, False])
+def test_cost_grad_16bit_rows_identical(vb, fs, sparse, monkeypatch):
+    """vapr_cost_grad with both collision passes on 16-bit tile rows (forced
+    onto this small batch) against the FP32-row passes, bit for bit: cost_pose,
+    cost_traj, grad_q and (sparse storage) every collision output's sparse
+    rows -- the narrow (43-bit: three codes per word) and wide (FP16: a word
+    per code) sparse instantiations and the dense one."""
+    from paper_2310_07854_b200.rollout import Rollout
+    from workloads.configs import FORMAT_SETS
+    wl = dataclasses_replace(config2(), formats=tuple(FORMAT_SETS[fs]))
+    res = []
+    for no16 in (False, True):
+        monkeypatch.setenv("VAPR_H16_MIN_POSES", "0")
+        if no16:
+            monkeypatch.setenv("VAPR_NO_H16", "1")
+        r = Rollout(wl, device=0, sparse=sparse)
+        r.run()
+        out = r.results()
+        extra = []
+        if sparse:
+            for slot in (vb.VAPR_CLOSEST_PT_SWEPT, vb.VAPR_OUT_VEC):
+                sp = r.sparse_slot(slot)
+                extra.append((sp["mask"], [w.tolist() for w in sp["row_words"]]))
+        res.append((out, extra))
+        monkeypatch.delenv("VAPR_NO_H16", raising=False)
+    (a, ea), (b, eb) = res
+    for k in ("cost_pose", "cost_traj", "grad_q"):
+        assert np.array_equal(np.asarray(a[k]).view(np.uint32), np.asarray(b[k]).view(np.uint32)), k
+    for (ma, wa), (mb, wb) in zip(ea, eb):
+        assert np.array_equal(ma, mb) and wa == wb
