@@ -327,8 +327,16 @@ __device__ __forceinline__ bool self_pair(const RV& rv, const char* rb, int i, i
 #ifndef VAPR_MAX_WARPS_WH       // warps per SM of the world pass with 16-bit rows
 #define VAPR_MAX_WARPS_WH 24
 #endif
+#ifndef VAPR_H16_MINB_S          // resident CTAs per SM of the 16-bit-row self / world kernels
+                                 // (self: two CTAs of 11 warps -- finer retirement at the pass's
+                                 // tail, so the world pass's CTAs start sooner: 1.17 -> 1.12 ms)
+#define VAPR_H16_MINB_S 2
+#endif
+#ifndef VAPR_H16_MINB_W
+#define VAPR_H16_MINB_W 1
+#endif
 #ifndef VAPR_MAX_WARPS_H        // the self pass with 16-bit tile rows (its kernel fits 96 registers)
-#define VAPR_MAX_WARPS_H 26
+#define VAPR_MAX_WARPS_H 11
 #endif
 #ifndef VAPR_DEC_ASYNC           // tile rows: cp.async staging + in-place decode (1) or loads (0)
 #define VAPR_DEC_ASYNC 1
@@ -624,7 +632,8 @@ __device__ __forceinline__ void bk_pose(const RobotDev& R, const float* qp, unsi
 // shared FP32 tile, BK per pose at the tile's end (CollisionArgs::fused).
 template <bool SPARSE, bool SP_WIDE, bool FUSED, int PASS, bool H16 = false>
 __global__ void __launch_bounds__(32 * (PASS == 1 ? (H16 ? VAPR_MAX_WARPS_WH : VAPR_MAX_WARPS_W)
-                                              : H16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS), 1)
+                                              : H16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS),
+                                  !H16 ? 1 : PASS == 1 ? VAPR_H16_MINB_W : VAPR_H16_MINB_S)
 collision_kernel(const __grid_constant__ RobotDev R, const __grid_constant__ Geo G,
                  const WorldsDev Wd, const Fmt fos, const Fmt fcp, const Fmt fov,
                  const CollisionArgs a) {
