@@ -1621,6 +1621,13 @@ cudaError_t launch_collision_pass(const RobotDev& R, const WorldsDev& W, const F
     const int pass = (a.do_world && !a.do_self) ? 1 : (!a.do_world && a.do_self) ? 2 : 0;
     nw = std::min(nw, (pass == 1 && !fused) ? (h16 ? VAPR_MAX_WARPS_WH : VAPR_MAX_WARPS_W)
                                             : h16 ? VAPR_MAX_WARPS_H : VAPR_MAX_WARPS);
+    if (h16 && pass == 2 && VAPR_H16_MINB_S > 1) {
+        // the self pass's CTAs come VAPR_H16_MINB_S to an SM: size them so that
+        // they fit together (the wide sparse form's larger result buffers)
+        int sm_smem = 0;
+        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        nw = std::min(nw, (sm_smem / VAPR_H16_MINB_S - 1024 - (int)G.tables) / (int)G.warp);
+    }
     if (nw < 1) return cudaErrorInvalidValue;
     const size_t smem = G.tables + (size_t)nw * G.warp;
     if (getenv("VAPR_DEBUG_LAUNCH"))
