@@ -393,7 +393,7 @@ def main():
     # HBM-shaped: bytes per pose, no dense contraction); "regime" what ncu
     # measured the dominant kernel to be limited by (profiles/r2)
     roofline = {"bound": "hbm", "kernel": dom,
-                "regime": ("instruction issue (both passes ~75 % issue-active at 24-25 warps/SM, 16-bit tile rows)"
+                "regime": ("instruction issue (both passes ~75 % issue-active at 22-24 warps/SM, 16-bit tile rows)"
                            if dom == "collision" else "see limiter"),
                 "stage_calls": "the timed step's own launches (vapr_set_stage_events, "
                                f"{args.storage} storage)",

@@ -77,7 +77,7 @@ for st, e in out["kernels"].items():
                   "threads_per_instruction": [l["threads_per_instruction"] for l in L]}
 LIMITER = {
     "collision": "two passes, each its own kernel, one CTA per SM, both with 16-bit tile rows "
-                 "(E5M10 out_spheres): self pass 25 warps per SM, 71 registers, world pass 24 "
+                 "(E5M10 out_spheres): self pass 2 CTAs x 11 warps per SM, 80 registers, world pass 24 "
                  "warps, 78 registers; both ~75 % issue-active (instruction issue; the occupancy "
                  "sweeps: self 12 -> 16 -> 26 warps 1.64 -> 1.37 -> 1.14 ms, world 16 -> 24 "
                  "1.22 -> 1.03 ms); 21-23 of 32 threads per instruction; DRAM traffic = "

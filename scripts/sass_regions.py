@@ -9,11 +9,11 @@ import sys
 from collections import defaultdict
 
 REGIONS = [("world_term", 72, 136), ("sparse_row", 137, 199), ("or_code3", 200, 224),
-           ("row reads (RowView)", 225, 250), ("self_pair", 251, 296), ("warp_queue", 474, 539),
-           ("kernel head", 625, 769), ("tile stage+decode", 770, 952), ("margin+zero", 953, 974),
-           ("world broadphase", 975, 1066), ("world items", 1067, 1158), ("self broadphase", 1159, 1206),
-           ("self narrowphase", 1207, 1301), ("self touched", 1302, 1318), ("self gradients", 1319, 1392),
-           ("tile tail", 1393, 1431)]
+           ("row reads (RowView)", 225, 250), ("self_pair", 251, 296), ("warp_queue", 482, 547),
+           ("kernel head", 633, 778), ("tile stage+decode", 779, 961), ("margin+zero", 962, 983),
+           ("world broadphase", 984, 1075), ("world items", 1076, 1167), ("self broadphase", 1168, 1215),
+           ("self narrowphase", 1216, 1310), ("self touched", 1311, 1327), ("self gradients", 1328, 1401),
+           ("tile tail", 1402, 1440)]
 acc = defaultdict(lambda: [0.0, 0.0, 0.0])
 head = ""
 for l in open(sys.argv[1]):
