@@ -14,7 +14,7 @@
 // chunk is streamed to HBM at once, eight lanes per pose writing its 128
 // contiguous bytes (one whole line) with 16-byte stores.  Shared memory per
 // warp is a fixed 4.2 KB whatever the row width, so occupancy is set by
-// registers (10 CTAs, 40 warps per SM), not by a staged row tile.  Link frames are NOT written to
+// registers (9 CTAs, 36 warps per SM), not by a staged row tile.  Link frames are NOT written to
 // memory: backward kinematics recomputes them, so HBM sees q
 // (28 B/pose) in and out_spheres out.
 #include "common.cuh"
@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kTile = 128;   // poses (= threads) per CTA
 #ifndef VAPR_FK_MINB             // resident CTAs per SM the register budget targets
-#define VAPR_FK_MINB 10
+#define VAPR_FK_MINB 9
 #endif
 
 #ifndef VAPR_FK_CHUNK            // words per pose per warp flush (a multiple of 4)
